@@ -1,0 +1,303 @@
+"""Generate golden vectors by running the REFERENCE itself.
+
+Run in this container only (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+It imports the reference package `ssmkit` from /root/reference/pkg/src and
+writes small .npz fixtures next to this file.  The fixtures pin the CPU
+oracle (`oracle/ssm_oracle.py`) and the CUDA path (`tests/test_gpu_*.py`).
+Numpy/scipy versions are recorded in every file.
+"""
+
+import math
+import os
+import sys
+
+import numpy as np
+import scipy
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+import ssmkit  # noqa: E402  (the reference)
+from ssmkit import RngStream, load_model  # noqa: E402
+from ssmkit.core import simulate  # noqa: E402
+from ssmkit.inference import build_filter_grid, particle_filter, resample  # noqa: E402
+from scipy.special import logsumexp  # noqa: E402
+
+MODELS = "/root/reference/pkg/models"
+VERSIONS = dict(numpy=np.__version__, scipy=scipy.__version__, ssmkit=ssmkit.__version__)
+
+
+def load(name):
+    path = {"lorenz96": "lorenz96/Lorenz96.bi", "windkessel": "windkessel/Windkessel.bi"}[name]
+    with open(os.path.join(MODELS, path)) as fh:
+        return load_model(fh.read())
+
+
+def save(name, **arrays):
+    arrays["versions"] = np.array(repr(VERSIONS))
+    np.savez_compressed(os.path.join(HERE, name), **arrays)
+    print("wrote", name, {k: getattr(v, "shape", None) for k, v in arrays.items()})
+
+
+class FixedU:
+    """Duck-typed rng for `resample`: returns scripted uniforms."""
+
+    def __init__(self, u):
+        self.u = np.asarray(u, dtype=float)
+
+    def uniform(self, low=0.0, high=1.0, size=None):
+        if size is None:
+            return float(self.u[0])
+        return self.u[:size].copy()
+
+
+class LocfInputs:
+    """Last-observation-carried-forward input provider (timeseries.py:184-210
+    semantics, rtol 1e-9) over a fixed (times, values) table."""
+
+    def __init__(self, times, values):
+        self.times = np.asarray(times, dtype=float)
+        self.values = np.asarray(values, dtype=float)
+
+    def at(self, t):
+        tol = 1e-9 * max(1.0, abs(t))
+        idx = int(np.searchsorted(self.times, t + tol, side="right")) - 1
+        return self.values[idx]
+
+
+def flow(t, f_max=500.0, t_s=0.3, t_d=0.5):
+    tp = np.mod(t, t_s + t_d)
+    return np.where(tp < t_s, f_max * np.sin(np.pi * tp / t_s) ** 2, 0.0)
+
+
+def gen_resample():
+    rs = np.random.default_rng(20260101)
+    out = {}
+    cases = []
+    # (name, weights)
+    cases.append(("onehot", np.array([1.0, 0.0, 0.0, 0.0])))
+    cases.append(("half", np.array([0.5, 0.5])))
+    cases.append(("ties", np.array([0.25, 0.25, 0.5])))
+    cases.append(("zeros_mixed", np.where(rs.random(37) < 0.4, 0.0, rs.random(37))))
+    cases.append(("lognormal_1k", np.exp(rs.normal(0.0, 3.0, 1000))))
+    cases.append(("uniform_4097", np.ones(4097)))
+    cases.append(("degenerate_2k", np.exp(rs.normal(0.0, 40.0, 2048))))
+    cases.append(("tiny_16384", np.exp(rs.normal(-700.0, 2.0, 16384))))
+    for name, w in cases:
+        P = w.size
+        cum = np.cumsum(w / w.sum())
+        cum[-1] = 1.0
+        out[f"{name}/w"] = w
+        out[f"{name}/cum"] = cum
+        for scheme in ("multinomial", "stratified", "systematic"):
+            u = rs.random(P) if scheme != "systematic" else rs.random(1)
+            anc = resample(w, scheme, FixedU(u))
+            out[f"{name}/{scheme}/u"] = u
+            out[f"{name}/{scheme}/anc"] = anc
+    # tie KAT from SURVEY 4: u exactly on cum boundaries
+    w = np.array([0.25, 0.25, 0.5])
+    u = np.array([0.25, 0.0, 0.4999999, 0.5, 0.9999])
+    out["kat_ties/w"] = w
+    out["kat_ties/u"] = u
+    out["kat_ties/anc"] = resample(w, "multinomial", FixedU(u), size=5)
+    save("resample.npz", **out)
+
+
+def gen_lse():
+    rs = np.random.default_rng(7)
+    arrs = {
+        "normal": rs.normal(0, 1, 1000),
+        "wide": rs.normal(0, 50, 4096),
+        "ties": np.array([3.0, 3.0, 1.0, -2.0, 3.0]),
+        "with_ninf": np.array([-np.inf, 0.5, -np.inf, 0.25]),
+        "one_dominant": np.concatenate([[0.0], np.full(1023, -60.0)]),
+    }
+    out = {}
+    for k, a in arrs.items():
+        out[f"{k}/a"] = a
+        out[f"{k}/lse"] = np.array(logsumexp(a))
+    save("lse.npz", **out)
+
+
+def gen_l96_step():
+    ir = load("lorenz96")
+    rs = np.random.default_rng(11)
+    out = {}
+    P = 257
+    for c, (dt, theta) in enumerate(
+        [
+            (0.05, (10.0, 0.1)),
+            (0.05000000000000002, (10.0, 0.1)),
+            (0.1, (8.5, 0.3)),
+            (0.07, (11.9, 0.05)),
+            (0.03, (10.0, 0.0)),
+        ]
+    ):
+        x = rs.uniform(-1.0, 3.0, (P, 8)) * (1.0 + 4.0 * (c % 2))
+        theta = np.array(theta)
+        t = 0.35
+        seed = 100 + c
+        x_out = simulate.step_transition(ir, theta, x, None, t, dt, RngStream(seed))
+        # replay the exact draws: per sub-step, 8 slot-major normal(0, sqrt(d), P)
+        rng = RngStream(seed)
+        W = []
+        for t_k, d in simulate.substep_schedule(t, dt, ir.delta):
+            for n in range(8):
+                W.append(rng.normal(0.0, math.sqrt(d), size=P))
+        W = np.array(W).reshape(-1, 8, P)
+        y = rs.normal(0.0, 3.0, 8)
+        mask = rs.random(8) < 0.7
+        mask[0] = True
+        g = simulate.observe_logpdf(ir, theta, x_out, None, y, mask)
+        g_all = simulate.observe_logpdf(ir, theta, x_out, None, y, np.ones(8, bool))
+        out.update(
+            {
+                f"c{c}/x_in": x,
+                f"c{c}/theta": theta,
+                f"c{c}/t": np.array(t),
+                f"c{c}/dt": np.array(dt),
+                f"c{c}/W": W,
+                f"c{c}/x_out": x_out,
+                f"c{c}/y": y,
+                f"c{c}/mask": mask,
+                f"c{c}/g": g,
+                f"c{c}/g_all": g_all,
+            }
+        )
+    out["ncases"] = np.array(5)
+    # fixed point KAT: sigma2 = 0, x = F
+    xf = np.full((4, 8), 10.0)
+    out["fixed/x_out"] = simulate.step_transition(ir, np.array([10.0, 0.0]), xf, None, 0.0, 0.05, RngStream(1))
+    save("l96_step.npz", **out)
+
+
+def gen_wk_step():
+    ir = load("windkessel")
+    rs = np.random.default_rng(12)
+    times = np.round(np.arange(0, 2.0001, 0.01), 10)
+    inputs = LocfInputs(times, flow(times)[:, None])
+    out = {"in_times": times, "in_values": flow(times)}
+    P = 300
+    for c, (t, dt, theta) in enumerate(
+        [
+            (0.1, 0.01, (1.8, 3.0, 0.06, 25.0)),
+            (0.2, 0.03, (0.9, 1.5, 0.03, 10.0)),
+            (0.55, 0.025, (2.4, 4.0, 0.08, 40.0)),
+        ]
+    ):
+        x = rs.normal(90.0, 15.0, (P, 1))
+        theta = np.array(theta)
+        seed = 200 + c
+        x_out = simulate.step_transition(ir, theta, x, inputs, t, dt, RngStream(seed))
+        rng = RngStream(seed)
+        xi = []
+        sd = 0.01 * np.sqrt(theta[None, :][:, 3])
+        for t_k, d in simulate.substep_schedule(t, dt, ir.delta):
+            xi.append(rng.normal(0.0, sd, size=P))
+        y = np.array([rs.normal(95.0, 10.0)])
+        u_obs = inputs.at(t + dt)
+        g = simulate.observe_logpdf(ir, theta, x_out, u_obs, y, np.array([True]))
+        out.update(
+            {
+                f"c{c}/x_in": x,
+                f"c{c}/theta": theta,
+                f"c{c}/t": np.array(t),
+                f"c{c}/dt": np.array(dt),
+                f"c{c}/xi": np.array(xi),
+                f"c{c}/x_out": x_out,
+                f"c{c}/y": y,
+                f"c{c}/g": g,
+            }
+        )
+    out["ncases"] = np.array(3)
+    save("wk_step.npz", **out)
+
+
+def l96_data(obs_every=1, slots=range(8), seed=1, T=40):
+    """theta*=(10,0.1), grid linspace(0,2,41), data RngStream(1)."""
+    ir = load("lorenz96")
+    theta = np.array([10.0, 0.1])
+    times = np.linspace(0.0, 2.0, T + 1)
+    rng = RngStream(seed)
+    x = simulate.sample_initial(ir, theta, rng.child(1), size=1)
+    obs_t, obs_v, obs_m = [], [], []
+    for k in range(1, len(times)):
+        x = simulate.step_transition(ir, theta, x, None, times[k - 1], times[k] - times[k - 1], rng.child(2, k))
+        y = simulate.simulate_obs(ir, theta, x, None, rng.child(3, k))[0]
+        m = np.zeros(8, bool)
+        if k % obs_every == 0:
+            m[list(slots)] = True
+        obs_t.append(times[k])
+        obs_v.append(y)
+        obs_m.append(m)
+    return ir, theta, times, np.array(obs_t), np.array(obs_v), np.array(obs_m)
+
+
+def gen_pf():
+    out = {}
+    ir, theta, times, ot, ov, om = l96_data(T=20)
+    T = len(times) - 1
+    grid = build_filter_grid(0.0, times[-1], T, ot, ov, om, n_obs=8)
+    out["l96/times"] = grid.times
+    out["l96/obs_t"] = ot
+    out["l96/obs_v"] = ov
+    out["l96/obs_m"] = om
+    out["l96/theta"] = theta
+    for scheme in ("systematic", "multinomial", "stratified"):
+        res = particle_filter(ir, theta, grid, RngStream(7), n_particles=256, resampler=scheme)
+        out[f"l96/{scheme}/loglik"] = np.array(res.loglik)
+        out[f"l96/{scheme}/traj"] = res.trajectory
+        out[f"l96/{scheme}/x_final"] = res.run.x
+        out[f"l96/{scheme}/logw_final"] = res.run.logw
+        out[f"l96/{scheme}/anc"] = np.array([h[1] for h in res.run.history[1:]])
+    # ESS-gated run and sparse-observation run
+    res = particle_filter(ir, theta, grid, RngStream(9), n_particles=256, resampler="systematic", ess_rel=0.5)
+    out["l96/ess/loglik"] = np.array(res.loglik)
+    out["l96/ess/traj"] = res.trajectory
+    ir, theta, times, ot, ov, om = l96_data(obs_every=2, slots=range(4), T=20)
+    grid = build_filter_grid(0.0, times[-1], len(times) - 1, ot, ov, om, n_obs=8)
+    out["l96s/obs_v"] = ov
+    out["l96s/obs_m"] = om
+    res = particle_filter(ir, theta, grid, RngStream(8), n_particles=128, resampler="systematic")
+    out["l96s/loglik"] = np.array(res.loglik)
+    out["l96s/traj"] = res.trajectory
+
+    # windkessel config 1: P=1024, T=100, theta*=(1.8,3,0.06,25)
+    ir = load("windkessel")
+    theta = np.array([1.8, 3.0, 0.06, 25.0])
+    in_times = np.round(np.arange(0, 1.0001, 0.01), 10)
+    inputs = LocfInputs(in_times, flow(in_times)[:, None])
+    times = np.linspace(0.0, 1.0, 101)
+    rng = RngStream(1)
+    x = simulate.sample_initial(ir, theta, rng.child(1), size=1)
+    ot, ov, om = [], [], []
+    for k in range(1, len(times)):
+        x = simulate.step_transition(ir, theta, x, inputs, times[k - 1], times[k] - times[k - 1], rng.child(2, k))
+        y = simulate.simulate_obs(ir, theta, x, inputs.at(times[k]), rng.child(3, k))[0]
+        ot.append(times[k])
+        ov.append(y)
+        om.append(np.ones(1, bool))
+    ot, ov, om = np.array(ot), np.array(ov), np.array(om)
+    grid = build_filter_grid(0.0, 1.0, 100, ot, ov, om, n_obs=1)
+    out["wk/in_times"] = in_times
+    out["wk/in_values"] = flow(in_times)
+    out["wk/obs_v"] = ov
+    out["wk/theta"] = theta
+    for scheme in ("multinomial", "systematic"):
+        res = particle_filter(ir, theta, grid, RngStream(7), inputs=inputs, n_particles=1024, resampler=scheme)
+        out[f"wk/{scheme}/loglik"] = np.array(res.loglik)
+        out[f"wk/{scheme}/traj"] = res.trajectory
+    save("pf.npz", **out)
+
+
+if __name__ == "__main__":
+    gen_resample()
+    gen_lse()
+    gen_l96_step()
+    gen_wk_step()
+    gen_pf()

@@ -1,0 +1,200 @@
+/*
+ * ssm_b200.h -- C ABI of libssm_b200.so, the sm_100a implementation of the
+ * bootstrap-particle-filter hot path of the LibBi paper (arXiv 1306.3277),
+ * as restated by the reference package `ssmkit`.
+ *
+ * All reference citations are file:line under /root/reference/pkg/src/ssmkit.
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer unless stated otherwise.
+ *   - Every entry point is stream-ordered on `stream` (a cudaStream_t passed
+ *     as void*; NULL = legacy default stream), reentrant, and keeps no global
+ *     mutable state.  The library never allocates: scratch space comes from
+ *     the caller through `workspace` pointers sized by the *_workspace_bytes()
+ *     queries.
+ *   - Particle state is SoA: x[b][slot][p] for filter b of a batch of B
+ *     filters, P particles each, nx state slots (L96: 8, windkessel: 1).
+ *   - `dtype` selects the arithmetic type of states and log-weights:
+ *     SSM_F64 (the reference's float64) or SSM_F32.  Log-likelihood
+ *     accumulators, LSE/ESS reductions and resampling CDFs are always float64
+ *     (CDF: exact 64-bit fixed point, see ssm_weights_scan).
+ *   - Return value: ssm_status.  Data-dependent failures that the reference
+ *     raises as exceptions (NonFiniteStateError simulate.py:158-162,
+ *     DegenerateEnsembleError particle.py:128-131 / resampling.py:23-24,
+ *     ValueError resampling.py:20-21) are recorded on the device in
+ *     ssm_filter_state / an int flag word and mapped to the same exception
+ *     classes (with time=) by the host layer.
+ */
+#ifndef SSM_B200_H
+#define SSM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SSM_OK = 0,
+  SSM_ERR_INVALID_ARG = 1,
+  SSM_ERR_CUDA = 2,
+  SSM_ERR_UNSUPPORTED = 3
+} ssm_status;
+
+typedef enum { SSM_F32 = 0, SSM_F64 = 1 } ssm_dtype;
+
+/* model ids: the two hand-written model kernels */
+typedef enum {
+  SSM_MODEL_LORENZ96 = 0,  /* Lorenz96.bi  (8 slots, RK4, Wiener noise) */
+  SSM_MODEL_WINDKESSEL = 1 /* Windkessel.bi (1 slot, analytic update, input F) */
+} ssm_model;
+
+/* resampling schemes, resampling.py:12 SCHEMES */
+typedef enum {
+  SSM_MULTINOMIAL = 0,
+  SSM_STRATIFIED = 1,
+  SSM_SYSTEMATIC = 2
+} ssm_scheme;
+
+/* flag bits written by ssm_weights_scan for raw (non-log) weights,
+ * resampling.py:18-24 */
+#define SSM_FLAG_BAD_WEIGHT 1u  /* negative or non-finite weight -> ValueError */
+#define SSM_FLAG_ZERO_TOTAL 2u  /* all weights zero -> DegenerateEnsembleError */
+
+/* One transition sub-step, built on the host from substep_schedule
+ * (simulate.py:28-38) and the RK4 step split (simulate.py:85-87). */
+typedef struct ssm_substep {
+  double d;      /* sub-step duration */
+  double sd;     /* sqrt(d): sd of the wiener() increment, simulate.py:54 */
+  double u_in;   /* model input at the sub-step start (windkessel F(t_k)), simulate.py:150 */
+  double s[4];   /* RK4 step lengths s_k = min(h, d - k h), simulate.py:85-87 */
+  int32_t n_ode; /* number of RK4 steps (<= 4) */
+  int32_t pad;
+} ssm_substep;
+
+/* Per-filter device state: the scalar part of ParticleRun (particle.py:47-59).
+ * Zero-initialise, then set uniform = 1 (ParticleRun.init, particle.py:69-70),
+ * err_* = INT32_MAX. */
+typedef struct ssm_filter_state {
+  double loglik;          /* ParticleRun.loglik */
+  double incr;            /* LSE of the last weighted step (log-weights are a - incr) */
+  double ess;             /* ESS of the current weights (particle.py:83-85) */
+  double lse_raw;         /* scratch */
+  int32_t uniform;        /* ParticleRun.weights_uniform */
+  int32_t resample_now;   /* resample at the start of the next step (particle.py:96-100) */
+  int32_t err_nonfinite;  /* min(step*64 + sub-step) with a non-finite state, else INT32_MAX */
+  int32_t err_degenerate; /* min(step) with a non-finite LSE increment, else INT32_MAX */
+  uint32_t blocks_done;   /* completion counter for the fused finalize (reset by the kernel) */
+  int32_t pad[3];
+} ssm_filter_state;
+
+/* Arguments of the fused propagate + weight step (kernels K1/K2).
+ * Replaces, per grid step i, ParticleRun._step after resampling
+ * (particle.py:107-135): the ancestor gather x = x[anc] (particle.py:102),
+ * simulate.step_transition (simulate.py:132-163), simulate.observe_logpdf
+ * (simulate.py:166-193), logw + g, scipy logsumexp (particle.py:127), the
+ * degenerate check (128-131), loglik += incr (132) and, when ess_rel >= 0,
+ * the ESS gate for the next step (particle.py:99-100). */
+typedef struct ssm_pw_args {
+  int32_t model;        /* ssm_model */
+  int32_t dtype;        /* ssm_dtype */
+  int32_t B, P;         /* filters, particles per filter */
+  int32_t step;         /* grid index i (RNG counter and error location) */
+  int32_t n_sub;        /* number of sub-steps in subs[] */
+  int32_t exact;        /* 1: reference op order, no FMA contraction (bitwise FP64) */
+  int32_t check_finite; /* simulate.py:158 */
+  int32_t has_obs;      /* grid.obs_at(i) is not None (timegrid.py:44-49) */
+  uint32_t obs_mask;    /* bit n = obs slot n present */
+  double y[8];          /* observation values by obs slot */
+  double u_obs;         /* model input at the observation time (windkessel F(t_i)) */
+  double log_w0;        /* -log(P): the uniform log-weight (particle.py:68, 103) */
+  double obs_log_sd;    /* log(obs sd): log(0.5) L96, log(2.0) windkessel */
+  double log_sqrt_2pi;  /* distributions.py:15 */
+  double ess_rel;       /* < 0: no ESS gate (always resample after weighting) */
+  const void* x_in;     /* [B][nx][P] positions at grid index i-1 */
+  void* x_out;          /* [B][nx][P] positions at grid index i */
+  const int32_t* anc;   /* [B][P] ancestors for step i (used iff fs.resample_now) or NULL */
+  const void* a_prev;   /* [B][P] unnormalised log-weights of the last weighted step, or NULL */
+  void* a_out;          /* [B][P] unnormalised log-weights logw + g (iff has_obs) */
+  const double* theta;  /* [B][4] derived per-filter constants */
+  const ssm_substep* subs; /* [n_sub] */
+  const void* noise;    /* injected noise-variable values [B][n_sub][n_noise][P], or NULL */
+  const uint32_t* keys; /* [B][2] Philox4x32 keys, used when noise == NULL */
+  ssm_filter_state* fs; /* [B] */
+  void* workspace;      /* ssm_pw_workspace_bytes(B, P) bytes */
+} ssm_pw_args;
+
+const char* ssm_version(void);
+const char* ssm_status_string(int status);
+const char* ssm_last_cuda_error(void);
+int ssm_sm_count(int device, int* out);
+
+/* K1/K2 fused propagate + weight (+ gather, + LSE/ESS finalize). */
+size_t ssm_pw_workspace_bytes(int B, int P);
+int ssm_propagate_weight(const ssm_pw_args* args, void* stream);
+
+/* K7: initial particles (simulate.sample_initial, simulate.py:111-129) drawn
+ * on the device: L96 x ~ U(-1,3) (Lorenz96.bi:21), windkessel Pp ~ N(90,15)
+ * (Windkessel.bi:24).  keys: [B][2]. */
+int ssm_init_particles(int model, int dtype, int B, int P, const uint32_t* keys,
+                       void* x_out, void* stream);
+
+/* K4: per-filter CDF of the resampling weights as an exact, deterministic
+ * 64-bit fixed-point inclusive scan (decoupled look-back), replacing
+ * cumsum(w / w.sum()) with cum[-1] = 1 (resampling.py:22-27):
+ *   cum[j] = (double)C[j] / (double)C[P-1].
+ * is_log = 1: w = exp(a - shift[b]) with a of `dtype` (ParticleRun passes its
+ * unnormalised log-weights and the last LSE, particle.py:101, 133); with
+ * shift == NULL the shift is fs[b].incr.
+ * is_log = 0: w = a (float64 raw weights); validated as in resampling.py:18-24
+ * with failures OR-ed into flags[b] (SSM_FLAG_*).
+ * fs (nullable): filters with fs[b].resample_now == 0 are skipped. */
+size_t ssm_scan_workspace_bytes(int B, int P);
+int ssm_weights_scan(int B, int P, int dtype, const void* a, int is_log, const double* shift,
+                     const ssm_filter_state* fs, uint64_t* C, uint32_t* flags, void* workspace,
+                     void* stream);
+/* cum[b][j] = C[b][j] / C[b][P-1] as float64 (for inspection / parity tests) */
+int ssm_fixed_to_cum(int B, int P, const uint64_t* C, double* cum, void* stream);
+
+/* K5: ancestor search, searchsorted(cum, u, 'right').clip(0, P-1)
+ * (resampling.py:28-36).  Systematic/stratified use a merge path over the
+ * sorted queries; multinomial a per-query binary search (query order kept).
+ *   cum_kind 0: cum is float64 [B][P_in] (injected CDF, exact parity mode)
+ *   cum_kind 1: cum is the uint64 fixed-point output of ssm_weights_scan
+ * Queries: u != NULL -> injected uniforms, [B][P_out] (multinomial,
+ * stratified) or [B][1] (systematic), exactly the draws resampling.py:28-33
+ * consumes; u == NULL -> drawn on the device from keys[b] at counter `step`.
+ * fs (nullable): filters with fs[b].resample_now == 0 get identity ancestors. */
+int ssm_resample_search(int B, int P_in, int P_out, int scheme, int cum_kind, const void* cum,
+                        const double* u, const uint32_t* keys, int step,
+                        const ssm_filter_state* fs, int32_t* anc, void* stream);
+
+/* K6: ancestor gather x_out[b][s][k] = x_in[b][s][anc[b][k]] (particle.py:102). */
+int ssm_gather(int dtype, int B, int nx, int P, const void* x_in, const int32_t* anc,
+               void* x_out, void* stream);
+
+/* K8: ancestry trace (ParticleRun.sample_trajectory, particle.py:137-149).
+ * xs[b*(S+1) + i] points at history position array x_i of filter b
+ * ([nx][P] SoA), ancs[b*(S+1) + i] at the ancestors of step i (NULL =
+ * identity; index 0 unused).  j_final[b] is the drawn final particle.
+ * out: [B][S+1][nx] float64. */
+int ssm_trace(int dtype, int B, int S, int nx, int P, const void* const* xs,
+              const int32_t* const* ancs, const int32_t* j_final, double* out, void* stream);
+
+/* K3 standalone: scipy-1.18 logsumexp and ESS of B log-weight vectors
+ * (particle.py:83-85, 127).  out_lse/out_ess: [B] float64. */
+size_t ssm_lse_workspace_bytes(int B, int P);
+int ssm_logsumexp(int dtype, int B, int P, const void* a, double* out_lse, double* out_ess,
+                  void* workspace, void* stream);
+
+/* K9: theta-block gather for SMC^2 theta-resampling (smc.py:96-98):
+ * dst[j] = src[idx[j]] for J blocks of `block_bytes` bytes each. */
+int ssm_block_gather(int J, size_t block_bytes, const void* src, const int32_t* idx, void* dst,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSM_B200_H */

@@ -1,0 +1,172 @@
+"""ctypes binding of libssm_b200.so (include/ssm_b200.h).
+
+The library is built in-tree (`make` / `__graft_entry__.build()`).  There is
+no CPU fallback: if the shared object is missing or no CUDA device is
+visible, every device entry point raises `NativeUnavailableError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libssm_b200.so")
+
+SSM_OK, SSM_ERR_INVALID_ARG, SSM_ERR_CUDA, SSM_ERR_UNSUPPORTED = 0, 1, 2, 3
+SSM_F32, SSM_F64 = 0, 1
+SSM_MODEL_LORENZ96, SSM_MODEL_WINDKESSEL = 0, 1
+SCHEME_IDS = {"multinomial": 0, "stratified": 1, "systematic": 2}
+SSM_FLAG_BAD_WEIGHT, SSM_FLAG_ZERO_TOTAL = 1, 2
+INT32_MAX = 2**31 - 1
+
+
+class NativeUnavailableError(RuntimeError):
+    """libssm_b200.so could not be loaded (the CUDA path is mandatory)."""
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned a non-OK status."""
+
+
+class Substep(C.Structure):
+    _fields_ = [
+        ("d", C.c_double),
+        ("sd", C.c_double),
+        ("u_in", C.c_double),
+        ("s", C.c_double * 4),
+        ("n_ode", C.c_int32),
+        ("pad", C.c_int32),
+    ]
+
+
+SUBSTEP_DTYPE = np.dtype(
+    [("d", "<f8"), ("sd", "<f8"), ("u_in", "<f8"), ("s", "<f8", (4,)), ("n_ode", "<i4"), ("pad", "<i4")]
+)
+assert SUBSTEP_DTYPE.itemsize == C.sizeof(Substep) == 64
+
+FILTER_STATE_DTYPE = np.dtype(
+    [
+        ("loglik", "<f8"),
+        ("incr", "<f8"),
+        ("ess", "<f8"),
+        ("lse_raw", "<f8"),
+        ("uniform", "<i4"),
+        ("resample_now", "<i4"),
+        ("err_nonfinite", "<i4"),
+        ("err_degenerate", "<i4"),
+        ("blocks_done", "<u4"),
+        ("pad", "<i4", (3,)),
+    ]
+)
+assert FILTER_STATE_DTYPE.itemsize == 64
+
+
+class PwArgs(C.Structure):
+    _fields_ = [
+        ("model", C.c_int32),
+        ("dtype", C.c_int32),
+        ("B", C.c_int32),
+        ("P", C.c_int32),
+        ("step", C.c_int32),
+        ("n_sub", C.c_int32),
+        ("exact", C.c_int32),
+        ("check_finite", C.c_int32),
+        ("has_obs", C.c_int32),
+        ("obs_mask", C.c_uint32),
+        ("y", C.c_double * 8),
+        ("u_obs", C.c_double),
+        ("log_w0", C.c_double),
+        ("obs_log_sd", C.c_double),
+        ("log_sqrt_2pi", C.c_double),
+        ("ess_rel", C.c_double),
+        ("x_in", C.c_void_p),
+        ("x_out", C.c_void_p),
+        ("anc", C.c_void_p),
+        ("a_prev", C.c_void_p),
+        ("a_out", C.c_void_p),
+        ("theta", C.c_void_p),
+        ("subs", C.c_void_p),
+        ("noise", C.c_void_p),
+        ("keys", C.c_void_p),
+        ("fs", C.c_void_p),
+        ("workspace", C.c_void_p),
+    ]
+
+
+# name -> (restype, argtypes); every symbol declared in include/ssm_b200.h
+_vp, _i, _sz, _d = C.c_void_p, C.c_int, C.c_size_t, C.c_double
+SIGNATURES = {
+    "ssm_version": (C.c_char_p, []),
+    "ssm_status_string": (C.c_char_p, [_i]),
+    "ssm_last_cuda_error": (C.c_char_p, []),
+    "ssm_sm_count": (_i, [_i, C.POINTER(C.c_int)]),
+    "ssm_pw_workspace_bytes": (_sz, [_i, _i]),
+    "ssm_propagate_weight": (_i, [C.POINTER(PwArgs), _vp]),
+    "ssm_init_particles": (_i, [_i, _i, _i, _i, _vp, _vp, _vp]),
+    "ssm_scan_workspace_bytes": (_sz, [_i, _i]),
+    "ssm_weights_scan": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "ssm_fixed_to_cum": (_i, [_i, _i, _vp, _vp, _vp]),
+    "ssm_resample_search": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
+    "ssm_gather": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "ssm_trace": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "ssm_lse_workspace_bytes": (_sz, [_i, _i]),
+    "ssm_logsumexp": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "ssm_block_gather": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
+}
+
+_LIB = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and type the shared library (no device needed)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise NativeUnavailableError(
+            f"{path} is missing: build it with `make` or __graft_entry__.build(); "
+            "there is no CPU fallback for the particle-filter path"
+        )
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def lib():
+    return load_library()
+
+
+def check(status: int, what: str = "") -> None:
+    if status != SSM_OK:
+        L = lib()
+        msg = L.ssm_status_string(status).decode()
+        if status == SSM_ERR_CUDA:
+            msg += ": " + L.ssm_last_cuda_error().decode()
+        raise NativeError(f"{what} failed: {msg}")
+
+
+def require_cuda():
+    """Fail loudly when the device path cannot run."""
+    import torch
+
+    load_library()
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError("no CUDA device visible; the B200 path has no CPU fallback")
+
+
+def stream_ptr(stream=None):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())

@@ -1,0 +1,203 @@
+// Shared device helpers for libssm_b200 (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "../../include/ssm_b200.h"
+
+namespace ssm {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// Counter-based Philox4x32-10 (Salmon et al. 2011).  The device RNG of the
+// fast path: a pure function of (key, counter) so draws are independent of
+// launch geometry and of how filters are batched or sharded (the RngStream
+// purity contract, rng.py:1-11).
+// ---------------------------------------------------------------------------
+struct U4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// counter word 3 tags the purpose of a draw so streams never overlap
+enum Purpose : uint32_t {
+  kPurposeNoise = 1u,
+  kPurposeResample = 2u,
+  kPurposeInit = 3u,
+  kPurposeSystematic = 4u,
+};
+
+// 53-bit uniform in [0,1) from two 32-bit words (same construction as numpy's
+// random_standard_uniform: (raw64 >> 11) * 2^-53, rng.py:44-45)
+__device__ __forceinline__ double u53(uint32_t hi, uint32_t lo) {
+  const uint64_t v = ((static_cast<uint64_t>(hi) << 32) | lo) >> 11;
+  return static_cast<double>(v) * 0x1.0p-53;
+}
+
+// Box-Muller pair, float64: u1 in (0,1]
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                           double& z0, double& z1) {
+  const double u1 = 1.0 - u53(a, b);  // (0, 1]
+  const double u2 = u53(c, d);
+  const double r = sqrt(-2.0 * log(u1));
+  double s, co;
+  sincospi(2.0 * u2, &s, &co);
+  z0 = r * co;
+  z1 = r * s;
+}
+
+// Box-Muller pair, float32
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
+  const float u1 = 1.0f - static_cast<float>(a >> 8) * 0x1.0p-24f;  // (0, 1]
+  const float u2 = static_cast<float>(b >> 8) * 0x1.0p-24f;
+  const float r = sqrtf(-2.0f * logf(u1));
+  float s, co;
+  sincospif(2.0f * u2, &s, &co);
+  z0 = r * co;
+  z1 = r * s;
+}
+
+// ---------------------------------------------------------------------------
+// Arithmetic policy.  EXACT = the reference's op order with every operation
+// individually rounded (no FMA contraction): bitwise-equal to numpy float64
+// for the L96 RK4.  !EXACT lets nvcc contract into FMA.
+// ---------------------------------------------------------------------------
+template <typename T, bool EXACT>
+struct Ar;
+
+template <>
+struct Ar<double, true> {
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+};
+template <>
+struct Ar<double, false> {
+  static __device__ __forceinline__ double add(double a, double b) { return a + b; }
+  static __device__ __forceinline__ double sub(double a, double b) { return a - b; }
+  static __device__ __forceinline__ double mul(double a, double b) { return a * b; }
+  static __device__ __forceinline__ double div(double a, double b) { return a / b; }
+};
+template <>
+struct Ar<float, true> {
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+};
+template <>
+struct Ar<float, false> {
+  static __device__ __forceinline__ float add(float a, float b) { return a + b; }
+  static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
+  static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
+  static __device__ __forceinline__ float div(float a, float b) { return a / b; }
+};
+
+// ---------------------------------------------------------------------------
+// Log-sum-exp + ESS state with scipy-1.18 semantics (particle.py:127 calls
+// scipy.special.logsumexp, which splits the maximal elements out of the sum):
+//   the represented set has max m, c elements equal to m,
+//   t  = sum_{a<m} exp(a - m),  s2 = sum_{a<m} exp(2(a - m)).
+//   LSE = m + log1p(t / c) + log(c),  ESS = (c + t)^2 / (c + s2).
+// Combination is deterministic for a fixed combination tree.
+// ---------------------------------------------------------------------------
+struct Lse {
+  double m, c, t, s2;
+};
+
+__device__ __forceinline__ Lse lse_empty() { return Lse{-CUDART_INF, 0.0, 0.0, 0.0}; }
+
+__device__ __forceinline__ void lse_push(Lse& s, double a) {
+  if (a > s.m) {
+    const double f = exp(s.m - a);
+    s.t = (s.c + s.t) * f;
+    s.s2 = (s.c + s.s2) * (f * f);
+    s.c = 1.0;
+    s.m = a;
+  } else if (a == s.m) {
+    s.c += 1.0;
+  } else {
+    const double e = exp(a - s.m);  // NaN propagates (degenerate)
+    s.t += e;
+    s.s2 += e * e;
+  }
+}
+
+__device__ __forceinline__ Lse lse_combine(Lse a, Lse b) {
+  if (b.m > a.m) {
+    const Lse tmp = a;
+    a = b;
+    b = tmp;
+  }
+  if (b.m == a.m) return Lse{a.m, a.c + b.c, a.t + b.t, a.s2 + b.s2};
+  if (b.c == 0.0 && b.t == 0.0) return a;  // empty
+  const double f = exp(b.m - a.m);         // NaN m -> NaN result
+  return Lse{a.m, a.c, a.t + (b.c + b.t) * f, a.s2 + (b.c + b.s2) * (f * f)};
+}
+
+__device__ __forceinline__ Lse lse_shfl_down(const Lse& s, int off) {
+  return Lse{__shfl_down_sync(0xffffffffu, s.m, off), __shfl_down_sync(0xffffffffu, s.c, off),
+             __shfl_down_sync(0xffffffffu, s.t, off), __shfl_down_sync(0xffffffffu, s.s2, off)};
+}
+
+// Block-wide deterministic reduction; result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ Lse lse_block_reduce(Lse s, Lse* smem /* NT/32 entries */) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s = lse_combine(s, lse_shfl_down(s, off));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) smem[warp] = s;
+  __syncthreads();
+  if (warp == 0) {
+    s = lane < NT / 32 ? smem[lane] : lse_empty();
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s = lse_combine(s, lse_shfl_down(s, off));
+  }
+  __syncthreads();
+  return s;
+}
+
+__device__ __forceinline__ double lse_value(const Lse& s) {
+  if (s.c == 0.0) return s.m;  // NaN or empty
+  return log1p(s.t / s.c) + log(s.c) + s.m;
+}
+
+__device__ __forceinline__ double lse_ess(const Lse& s) {
+  const double sw = s.c + s.t;
+  return sw * sw / (s.c + s.s2);
+}
+
+template <typename T>
+__device__ __forceinline__ bool finite(T v) {
+  return isfinite(v);
+}
+
+}  // namespace ssm
+
+// error reporting helper shared by the C-ABI entry points
+extern "C" void ssm_set_last_error(cudaError_t e);
+#define SSM_CHECK_LAUNCH()                      \
+  do {                                          \
+    cudaError_t _e = cudaGetLastError();        \
+    if (_e != cudaSuccess) {                    \
+      ssm_set_last_error(_e);                   \
+      return SSM_ERR_CUDA;                      \
+    }                                           \
+  } while (0)

@@ -1,0 +1,369 @@
+// K1/K2: fused ancestor-gather + propagate + weight + LSE/ESS finalize.
+//
+// One thread per particle, state in registers, SoA coalesced loads/stores.
+// Replaces, for one grid step i of ParticleRun._step (particle.py:107-135):
+//   x = x[anc]                                  particle.py:102
+//   step_transition (sub-steps, noise, RK4)     simulate.py:132-163, 50-60, 71-93
+//   observe_logpdf (Gaussian, present slots)    simulate.py:166-193, distributions.py:98-101
+//   logw_new = logw + g; incr = logsumexp(...)  particle.py:125-127
+//   degenerate check, loglik += incr            particle.py:128-133
+//   ESS gate for the next step                  particle.py:99-100
+// The LSE/ESS finalize runs in the last block to finish (completion counter),
+// combining per-block partials in block order -> deterministic.
+
+#include "ssm_common.cuh"
+
+namespace ssm {
+
+constexpr int kMaxPwBlocks = 2048;  // per filter; a function of P only (determinism)
+
+__host__ __device__ inline int pw_grid_x(int P) {
+  const int tiles = (P + kThreads - 1) / kThreads;
+  return tiles < kMaxPwBlocks ? tiles : kMaxPwBlocks;
+}
+
+// ----------------------------- noise ---------------------------------------
+
+template <typename T>
+__device__ __forceinline__ void normals8(uint32_t k0, uint32_t k1, uint32_t p, uint32_t step,
+                                         uint32_t sub, T z[8]);
+
+template <>
+__device__ __forceinline__ void normals8<double>(uint32_t k0, uint32_t k1, uint32_t p,
+                                                 uint32_t step, uint32_t sub, double z[8]) {
+#pragma unroll
+  for (uint32_t g = 0; g < 4; ++g) {
+    const U4 r = philox4x32_10(U4{p, step, (sub << 8) | g, kPurposeNoise}, k0, k1);
+    box_muller(r.x, r.y, r.z, r.w, z[2 * g], z[2 * g + 1]);
+  }
+}
+
+template <>
+__device__ __forceinline__ void normals8<float>(uint32_t k0, uint32_t k1, uint32_t p,
+                                                uint32_t step, uint32_t sub, float z[8]) {
+#pragma unroll
+  for (uint32_t g = 0; g < 2; ++g) {
+    const U4 r = philox4x32_10(U4{p, step, (sub << 8) | g, kPurposeNoise}, k0, k1);
+    box_muller(r.x, r.y, z[4 * g], z[4 * g + 1]);
+    box_muller(r.z, r.w, z[4 * g + 2], z[4 * g + 3]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T normal1(uint32_t k0, uint32_t k1, uint32_t p, uint32_t step,
+                                     uint32_t sub) {
+  const U4 r = philox4x32_10(U4{p, step, sub << 8, kPurposeNoise}, k0, k1);
+  T z0, z1;
+  if constexpr (sizeof(T) == 8) {
+    box_muller(r.x, r.y, r.z, r.w, z0, z1);
+  } else {
+    box_muller(r.x, r.y, z0, z1);
+  }
+  return z0;
+}
+
+// ----------------------------- Lorenz '96 ----------------------------------
+// Lorenz96.bi:27  dx[n]/dt = x[n-1]*(x[n+1] - x[n-2]) - x[n] + F + sqrt(sigma2)*deltaW[n]/h
+// compiled (ir.py:188-214) as
+//   ((((X[n-1] * (X[n+1] - X[n-2])) - X[n]) + F) + ((sqrt(sigma2) * W[n]) / 0.05))
+
+template <typename T, bool E>
+__device__ __forceinline__ void l96_deriv(const T x[8], T F, const T nt[8], T out[8]) {
+  using O = Ar<T, E>;
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    const T xm1 = x[(n + 7) & 7], xp1 = x[(n + 1) & 7], xm2 = x[(n + 6) & 7];
+    out[n] = O::add(O::add(O::sub(O::mul(xm1, O::sub(xp1, xm2)), x[n]), F), nt[n]);
+  }
+}
+
+// classic RK4, simulate.py:88-93 (evaluation order of the numpy expressions)
+template <typename T, bool E>
+__device__ __forceinline__ void l96_rk4(T x[8], T F, const T nt[8], T s) {
+  using O = Ar<T, E>;
+  T k[8], acc[8], st[8];
+  const T hs = O::mul(T(0.5), s);  // `0.5 * s * k` == (0.5*s)*k
+  l96_deriv<T, E>(x, F, nt, k);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = k[n];
+    st[n] = O::add(x[n], O::mul(hs, k[n]));
+  }
+  l96_deriv<T, E>(st, F, nt, k);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = O::add(acc[n], O::mul(T(2.0), k[n]));
+    st[n] = O::add(x[n], O::mul(hs, k[n]));
+  }
+  l96_deriv<T, E>(st, F, nt, k);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = O::add(acc[n], O::mul(T(2.0), k[n]));
+    st[n] = O::add(x[n], O::mul(s, k[n]));
+  }
+  l96_deriv<T, E>(st, F, nt, k);
+  const T s6 = O::div(s, T(6.0));
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = O::add(acc[n], k[n]);
+    x[n] = O::add(x[n], O::mul(s6, acc[n]));
+  }
+}
+
+// ----------------------------- the kernel ----------------------------------
+
+template <int MODEL, typename T, bool E, bool INJ>
+__global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
+  using O = Ar<T, E>;
+  constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
+  const int b = blockIdx.y;
+  const int P = A.P;
+  ssm_filter_state* fs = A.fs + b;
+  const int R = fs->resample_now;
+  const bool uniform_in = R || fs->uniform;
+  const double incr_prev = fs->incr;
+  const size_t base = static_cast<size_t>(b) * NX * P;
+  const T* __restrict__ xin = static_cast<const T*>(A.x_in) + base;
+  T* __restrict__ xout = static_cast<T*>(A.x_out) + base;
+  const int32_t* __restrict__ anc =
+      (R && A.anc != nullptr) ? A.anc + static_cast<size_t>(b) * P : nullptr;
+  const T* __restrict__ aprev =
+      A.a_prev ? static_cast<const T*>(A.a_prev) + static_cast<size_t>(b) * P : nullptr;
+  T* __restrict__ aout = A.a_out ? static_cast<T*>(A.a_out) + static_cast<size_t>(b) * P : nullptr;
+  const T* __restrict__ noise =
+      INJ ? static_cast<const T*>(A.noise) + static_cast<size_t>(b) * A.n_sub * NX * P : nullptr;
+  const double* th = A.theta + 4 * b;
+  const uint32_t k0 = INJ ? 0u : A.keys[2 * b], k1 = INJ ? 0u : A.keys[2 * b + 1];
+  const int has_obs = A.has_obs;
+  const T logw0 = static_cast<T>(A.log_w0);
+  const T obs_log_sd = static_cast<T>(A.obs_log_sd);
+  const T lsp = static_cast<T>(A.log_sqrt_2pi);
+
+  Lse st = lse_empty();
+  bool bad = false;
+  int bad_sub = 0;
+
+  for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads) {
+    const int src = anc ? anc[p] : p;
+    T x[NX];
+#pragma unroll
+    for (int n = 0; n < NX; ++n) x[n] = xin[static_cast<size_t>(n) * P + src];
+
+    for (int k = 0; k < A.n_sub; ++k) {
+      const ssm_substep& S = A.subs[k];
+      if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+        const T F = static_cast<T>(th[0]);
+        const T sq = static_cast<T>(th[1]);  // np.sqrt(sigma2), host-computed
+        T W[8], nt[8];
+        if constexpr (INJ) {
+#pragma unroll
+          for (int n = 0; n < 8; ++n)
+            W[n] = noise[(static_cast<size_t>(k) * 8 + n) * P + p];
+        } else {
+          normals8<T>(k0, k1, static_cast<uint32_t>(p), static_cast<uint32_t>(A.step),
+                      static_cast<uint32_t>(k), W);
+          const T sd = static_cast<T>(S.sd);
+#pragma unroll
+          for (int n = 0; n < 8; ++n) W[n] = sd * W[n];
+        }
+#pragma unroll
+        for (int n = 0; n < 8; ++n) nt[n] = O::div(O::mul(sq, W[n]), T(0.05));
+        for (int m = 0; m < S.n_ode; ++m) l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
+      } else {
+        // Windkessel.bi:28-29, Pp <- exp(-h/(R*C))*Pp + R*(1 - exp(-h/(R*C)))*(F + xi)
+        const T ca = static_cast<T>(th[0]), cb = static_cast<T>(th[1]);
+        T xi;
+        if constexpr (INJ) {
+          xi = noise[static_cast<size_t>(k) * P + p];
+        } else {
+          xi = static_cast<T>(th[3]) *
+               normal1<T>(k0, k1, static_cast<uint32_t>(p), static_cast<uint32_t>(A.step),
+                          static_cast<uint32_t>(k));
+        }
+        x[0] = O::add(O::mul(ca, x[0]), O::mul(cb, O::add(static_cast<T>(S.u_in), xi)));
+      }
+      if (A.check_finite && !bad) {
+        bool ok = true;
+#pragma unroll
+        for (int n = 0; n < NX; ++n) ok &= finite(x[n]);
+        if (!ok) {
+          bad = true;
+          bad_sub = k;
+        }
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * P + p] = x[n];
+
+    if (has_obs) {
+      T g = T(0);
+      if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          if (A.obs_mask & (1u << n)) {
+            const T z = O::div(O::sub(static_cast<T>(A.y[n]), x[n]), T(0.5));
+            g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
+          }
+        }
+      } else {
+        const T mean = O::add(x[0], O::mul(static_cast<T>(th[2]), static_cast<T>(A.u_obs)));
+        const T z = O::div(O::sub(static_cast<T>(A.y[0]), mean), T(2.0));
+        g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
+      }
+      const T lw = uniform_in ? logw0 : O::sub(aprev[p], static_cast<T>(incr_prev));
+      const T a = O::add(lw, g);
+      aout[p] = a;
+      lse_push(st, static_cast<double>(a));
+    }
+  }
+
+  if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
+
+  // ---- per-block partial + last-block finalize ----
+  __shared__ Lse red[kThreads / 32];
+  __shared__ bool s_last;
+  Lse* parts = reinterpret_cast<Lse*>(A.workspace) + static_cast<size_t>(b) * kMaxPwBlocks;
+  if (has_obs) {
+    const Lse r = lse_block_reduce<kThreads>(st, red);
+    if (threadIdx.x == 0) parts[blockIdx.x] = r;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&fs->blocks_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+
+  if (has_obs) {
+    Lse acc = lse_empty();
+    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += kThreads) {
+      const Lse q{__ldcg(&parts[i].m), __ldcg(&parts[i].c), __ldcg(&parts[i].t),
+                  __ldcg(&parts[i].s2)};
+      acc = lse_combine(acc, q);
+    }
+    acc = lse_block_reduce<kThreads>(acc, red);
+    if (threadIdx.x == 0) {
+      const double incr = lse_value(acc);
+      const double ess = lse_ess(acc);
+      if (!isfinite(incr)) {
+        fs->err_degenerate = min(fs->err_degenerate, A.step);
+      } else {
+        fs->loglik += incr;
+      }
+      fs->incr = incr;
+      fs->lse_raw = incr;
+      fs->ess = ess;
+      fs->uniform = 0;
+      fs->resample_now = (A.ess_rel < 0.0) ? 1 : (ess < A.ess_rel * static_cast<double>(P) ? 1 : 0);
+    }
+  } else if (threadIdx.x == 0 && R) {
+    fs->uniform = 1;  // resampled, no weighting at this step
+    fs->resample_now = 0;
+  }
+  if (threadIdx.x == 0) fs->blocks_done = 0u;
+}
+
+template <int MODEL, typename T>
+static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
+  const dim3 grid(pw_grid_x(A.P), A.B);
+  const bool inj = A.noise != nullptr;
+  if (A.exact) {
+    if (inj)
+      pw_kernel<MODEL, T, true, true><<<grid, kThreads, 0, s>>>(A);
+    else
+      pw_kernel<MODEL, T, true, false><<<grid, kThreads, 0, s>>>(A);
+  } else {
+    if (inj)
+      pw_kernel<MODEL, T, false, true><<<grid, kThreads, 0, s>>>(A);
+    else
+      pw_kernel<MODEL, T, false, false><<<grid, kThreads, 0, s>>>(A);
+  }
+}
+
+// ----------------------------- K7: init ------------------------------------
+
+template <int MODEL, typename T>
+__global__ void __launch_bounds__(kThreads) init_kernel(int P, const uint32_t* keys, T* x) {
+  const int b = blockIdx.y;
+  const uint32_t k0 = keys[2 * b], k1 = keys[2 * b + 1];
+  constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
+  T* xb = x + static_cast<size_t>(b) * NX * P;
+  for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads) {
+    if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+      // x[n] ~ uniform(-1.0, 3.0): low + (high - low) * U  (Lorenz96.bi:21)
+#pragma unroll
+      for (uint32_t g = 0; g < 4; ++g) {
+        const U4 r = philox4x32_10(U4{static_cast<uint32_t>(p), 0u, g, kPurposeInit}, k0, k1);
+        xb[static_cast<size_t>(2 * g) * P + p] = static_cast<T>(-1.0 + 4.0 * u53(r.x, r.y));
+        xb[static_cast<size_t>(2 * g + 1) * P + p] = static_cast<T>(-1.0 + 4.0 * u53(r.z, r.w));
+      }
+    } else {
+      // Pp ~ gaussian(90.0, 15.0)  (Windkessel.bi:24)
+      const U4 r = philox4x32_10(U4{static_cast<uint32_t>(p), 0u, 0u, kPurposeInit}, k0, k1);
+      double z0, z1;
+      box_muller(r.x, r.y, r.z, r.w, z0, z1);
+      xb[p] = static_cast<T>(90.0 + 15.0 * z0);
+    }
+  }
+}
+
+}  // namespace ssm
+
+using namespace ssm;
+
+extern "C" size_t ssm_pw_workspace_bytes(int B, int P) {
+  (void)P;
+  return static_cast<size_t>(B > 0 ? B : 1) * kMaxPwBlocks * sizeof(Lse);
+}
+
+extern "C" int ssm_propagate_weight(const ssm_pw_args* args, void* stream) {
+  if (!args) return SSM_ERR_INVALID_ARG;
+  const ssm_pw_args& A = *args;
+  if (A.B <= 0 || A.P <= 0 || A.B > 65535 || A.n_sub < 0 || !A.x_in || !A.x_out || !A.theta ||
+      (A.n_sub > 0 && !A.subs) || !A.fs || !A.workspace)
+    return SSM_ERR_INVALID_ARG;
+  if (A.has_obs && !A.a_out) return SSM_ERR_INVALID_ARG;
+  if (A.n_sub > 0 && !A.noise && !A.keys) return SSM_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (A.model == SSM_MODEL_LORENZ96) {
+    if (A.dtype == SSM_F64)
+      launch_pw<SSM_MODEL_LORENZ96, double>(A, s);
+    else if (A.dtype == SSM_F32)
+      launch_pw<SSM_MODEL_LORENZ96, float>(A, s);
+    else
+      return SSM_ERR_INVALID_ARG;
+  } else if (A.model == SSM_MODEL_WINDKESSEL) {
+    if (A.dtype == SSM_F64)
+      launch_pw<SSM_MODEL_WINDKESSEL, double>(A, s);
+    else if (A.dtype == SSM_F32)
+      launch_pw<SSM_MODEL_WINDKESSEL, float>(A, s);
+    else
+      return SSM_ERR_INVALID_ARG;
+  } else {
+    return SSM_ERR_UNSUPPORTED;
+  }
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+extern "C" int ssm_init_particles(int model, int dtype, int B, int P, const uint32_t* keys,
+                                  void* x_out, void* stream) {
+  if (B <= 0 || P <= 0 || B > 65535 || !keys || !x_out) return SSM_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const dim3 grid(pw_grid_x(P), B);
+  if (model == SSM_MODEL_LORENZ96) {
+    if (dtype == SSM_F64)
+      init_kernel<SSM_MODEL_LORENZ96, double><<<grid, kThreads, 0, s>>>(P, keys, (double*)x_out);
+    else
+      init_kernel<SSM_MODEL_LORENZ96, float><<<grid, kThreads, 0, s>>>(P, keys, (float*)x_out);
+  } else if (model == SSM_MODEL_WINDKESSEL) {
+    if (dtype == SSM_F64)
+      init_kernel<SSM_MODEL_WINDKESSEL, double><<<grid, kThreads, 0, s>>>(P, keys, (double*)x_out);
+    else
+      init_kernel<SSM_MODEL_WINDKESSEL, float><<<grid, kThreads, 0, s>>>(P, keys, (float*)x_out);
+  } else {
+    return SSM_ERR_UNSUPPORTED;
+  }
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}

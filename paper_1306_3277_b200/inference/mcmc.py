@@ -1,0 +1,190 @@
+"""Marginal Metropolis-Hastings over parameters (PMMH) with the device
+particle filter inside -- the reference's inference/mcmc.py:28-180 API.
+
+`FilterRunner` is the drop-in factory (mcmc.py:54-108): `new_run` /
+`run` build a `ParticleRun` on the GPU.  `run_batch` advances many filters
+in one launch per step; `mh_sample_chains` uses it to run C independent
+PMMH chains in lock-step (config 3: 64 chains), giving exactly the draws of
+C serial `mh_sample` calls with streams rngs[c].  theta-level proposals and
+priors stay on the host (scalar per chain, SURVEY 8f row 1 moves them on
+device next).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from ..errors import UnsupportedModelError
+from ..models import resolve_model
+from .particle import ParticleRun, advance_runs, init_runs, sample_trajectories
+from .timegrid import as_filter_grid
+
+_FILTER_KEY = 7  # mcmc.py:25
+
+
+def metropolis_accept(log_ratio, rng):
+    """Accept iff u <= exp(log_ratio), u ~ U(0,1)  (mcmc.py:28-33)."""
+    if np.isnan(log_ratio) or log_ratio == -np.inf:
+        return False
+    u = rng.uniform()
+    return bool(u <= np.exp(min(log_ratio, 0.0)))
+
+
+@dataclass
+class MhChainState:
+    theta: np.ndarray
+    trajectory: np.ndarray
+    loglik: float
+    log_prior: float
+    init_state: np.ndarray = None
+
+
+class FilterRunner:
+    """Builds and runs the bootstrap filter on the GPU for a given theta."""
+
+    def __init__(self, ir, grid, inputs=None, filter_kind="bootstrap", n_particles=1024,
+                 resampler="multinomial", ess_rel=None, check_finite=True, **device_opts):
+        if filter_kind not in ("kalman", "bootstrap"):
+            raise ValueError(f"unknown filter {filter_kind!r}")
+        if filter_kind == "kalman":
+            raise UnsupportedModelError(
+                "the Kalman filter is not part of the device path (SURVEY 2: serial dense algebra)")
+        self.ir = ir
+        self.spec = resolve_model(ir)
+        self.grid = as_filter_grid(grid)
+        self.inputs = inputs
+        self.filter_kind = filter_kind
+        self.n_particles = n_particles
+        self.resampler = resampler
+        self.ess_rel = ess_rel
+        self.check_finite = check_finite
+        self.device_opts = dict(device_opts)
+
+    def _make(self, theta, init_state):
+        return ParticleRun(self.spec, theta, self.grid, inputs=self.inputs, n_particles=self.n_particles,
+                           resampler=self.resampler, ess_rel=self.ess_rel, initial_state=init_state,
+                           check_finite=self.check_finite, **self.device_opts)
+
+    def new_run(self, theta, init_state, rng):
+        """Fresh, initialised (not yet advanced) filter run (mcmc.py:79-100)."""
+        return self._make(theta, init_state).init(rng.child(0))
+
+    def new_runs(self, thetas, init_states, rngs):
+        runs = [self._make(t, s) for t, s in zip(thetas, init_states)]
+        init_runs(runs, [g.child(0) for g in rngs])
+        return runs
+
+    def run(self, theta, init_state, rng, upto=None):
+        """(loglik, trajectory, run) over grid steps 1..upto (mcmc.py:102-108)."""
+        out = self.run_batch([theta], [init_state], [rng], upto=upto)
+        return out[0]
+
+    def run_batch(self, thetas, init_states, rngs, upto=None):
+        """Batched FilterRunner.run: one launch per step for all filters."""
+        upto = self.grid.last if upto is None else upto
+        if not thetas:
+            return []
+        runs = self.new_runs(thetas, init_states, rngs)
+        advance_runs(runs, upto, [g.child(1) for g in rngs])
+        trajs = sample_trajectories(runs, [g.child(2) for g in rngs])
+        return [(r.loglik, t, r) for r, t in zip(runs, trajs)]
+
+
+def _chain_log_prior(spec, theta, init_state):
+    lp = spec.parameter_logpdf(theta)
+    if init_state is not None:
+        lp += spec.initial_logpdf(theta, init_state)
+    return lp
+
+
+def init_chain(ir, runner, rng, upto=None):
+    """mcmc.py:118-132."""
+    return init_chains(ir, runner, [rng], upto)[0]
+
+
+def init_chains(ir, runner, rngs, upto=None):
+    spec = resolve_model(ir)
+    thetas, inits = [], []
+    for rng in rngs:
+        theta = spec.sample_parameter(rng, size=1)[0]
+        init_state = None
+        if spec.has_proposal_initial:
+            init_state = spec.sample_initial(theta, rng, size=1)[0]
+        thetas.append(theta)
+        inits.append(init_state)
+    res = runner.run_batch(thetas, inits, [g.child(_FILTER_KEY) for g in rngs], upto=upto)
+    return [
+        MhChainState(theta=th, trajectory=traj, loglik=ll, log_prior=_chain_log_prior(spec, th, ist),
+                     init_state=ist)
+        for th, ist, (ll, traj, _) in zip(thetas, inits, res)
+    ]
+
+
+def _propose(spec, chain, rng):
+    theta_new, logq_fwd = spec.propose_parameters(chain.theta, rng)
+    logq_rev = spec.proposal_parameter_logpdf(theta_new, chain.theta)
+    init_new = None
+    if chain.init_state is not None:
+        init_new, lq = spec.propose_initial(theta_new, chain.init_state, rng)
+        logq_fwd += lq
+        logq_rev += spec.proposal_initial_logpdf(chain.theta, init_new, chain.init_state)
+    log_prior_new = _chain_log_prior(spec, theta_new, init_new)
+    return theta_new, init_new, logq_fwd, logq_rev, log_prior_new
+
+
+def marginal_mh_step(ir, chain, runner, rng, upto=None, reference=None):
+    """One marginal MH transition (mcmc.py:135-166); returns (state, accepted, run)."""
+    return marginal_mh_steps(ir, [chain], runner, [rng], upto, [reference])[0]
+
+
+def marginal_mh_steps(ir, chains, runner, rngs, upto=None, references=None):
+    """Lock-step marginal MH over independent chains: host proposals, one
+    batched device filter run for every chain inside the prior support,
+    then per-chain accept/reject with the chain's own stream."""
+    spec = resolve_model(ir)
+    references = references or [None] * len(chains)
+    props = [_propose(spec, c, g) for c, g in zip(chains, rngs)]
+    todo = [k for k, p in enumerate(props) if p[4] != -np.inf]
+    res = runner.run_batch([props[k][0] for k in todo], [props[k][1] for k in todo],
+                           [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto)
+    by_k = dict(zip(todo, res))
+    out = []
+    for k, (chain, rng) in enumerate(zip(chains, rngs)):
+        theta_new, init_new, logq_fwd, logq_rev, log_prior_new = props[k]
+        if k not in by_k:
+            out.append((chain, False, None))  # outside the prior support: auto-reject
+            continue
+        loglik_new, traj_new, run = by_k[k]
+        current = chain.loglik if references[k] is None else references[k]
+        log_ratio = (loglik_new + log_prior_new + logq_rev) - (current + chain.log_prior + logq_fwd)
+        if metropolis_accept(log_ratio, rng):
+            out.append((MhChainState(theta=theta_new, trajectory=traj_new, loglik=loglik_new,
+                                     log_prior=log_prior_new, init_state=init_new), True, run))
+        else:
+            out.append((chain, False, None))
+    return out
+
+
+def mh_sample(ir, runner, n_samples, rng):
+    """mcmc.py:169-180: (list of MhChainState, acceptance count)."""
+    chains, acc = mh_sample_chains(ir, runner, n_samples, [rng])
+    return chains[0], int(acc[0])
+
+
+def mh_sample_chains(ir, runner, n_samples, rngs, upto=None, on_step=None):
+    """C independent PMMH chains advanced in lock-step (batched filters).
+    Chain c reproduces mh_sample(ir, runner, n_samples, rngs[c])."""
+    states = init_chains(ir, runner, [g.child(0) for g in rngs], upto=upto)
+    samples = [[] for _ in rngs]
+    accepted = np.zeros(len(rngs), dtype=int)
+    for step in range(1, n_samples + 1):
+        outs = marginal_mh_steps(ir, states, runner, [g.child(step) for g in rngs], upto=upto)
+        for c, (st, ok, _) in enumerate(outs):
+            states[c] = st
+            accepted[c] += int(ok)
+            samples[c].append(st)
+        if on_step is not None:
+            on_step(step, states)
+    return samples, accepted

@@ -1,0 +1,550 @@
+"""Bootstrap particle filter on the B200 (drop-in for the reference's
+inference/particle.py:28-185).
+
+`ParticleRun` implements the reference's run protocol -- init(rng),
+advance_to(upto, rng) -> loglik increment, sample_trajectory(rng), clone(),
+ess(), attributes pos / loglik / x / logw / n_particles / history -- with all
+per-particle work in libssm_b200.so:
+
+    per grid step i (particle.py:107-135)
+      [K4 ssm_weights_scan]    cumsum(w / sum w)             resampling.py:26-27
+      [K5 ssm_resample_search] searchsorted(cum, u, 'right') resampling.py:28-36
+      [K1/K2 ssm_propagate_weight]  x[anc] -> step_transition -> observe_logpdf
+                               -> logw + g -> LSE -> loglik, ESS gate (fused)
+
+Several filters with the same grid, model and particle count advance in one
+launch (`advance_runs`), which the PMMH and SMC^2 drivers use.  The host
+loop only enqueues kernels; the device state machine (weights_uniform,
+resample decision, errors) lives in `ssm_filter_state` and is read once per
+advance_to call.
+
+Noise modes
+  "device": Philox4x32-10 normals/uniforms drawn on the device (fast path).
+  "host":   the reference's own draws (numpy Philox via RngStream, same keys
+            and order, rng.py / simulate.py:50-60 / resampling.py:28-33) are
+            generated on the host and injected, so a float64 run reproduces
+            the reference filter (parity mode).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from .. import _lib
+from ..errors import DegenerateEnsembleError, NonFiniteStateError, UnsupportedModelError
+from ..models import LOG_SQRT_2PI, ModelSpec, resolve_model
+from ..rng import device_key
+from .timegrid import as_filter_grid
+from .types import FilterOutcome
+
+_RESAMPLE_KEY = 0  # particle.py:24
+_PROPAGATE_KEY = 1  # particle.py:25
+SCHEMES = ("multinomial", "stratified", "systematic")
+_DT = {"float64": (torch.float64, _lib.SSM_F64), "float32": (torch.float32, _lib.SSM_F32)}
+
+
+def _dtype_info(dtype):
+    key = {torch.float64: "float64", torch.float32: "float32", np.float64: "float64",
+           np.float32: "float32"}.get(dtype, dtype)
+    if key not in _DT:
+        raise ValueError(f"unsupported dtype {dtype!r}")
+    return key, _DT[key][0], _DT[key][1]
+
+
+# ---------------------------------------------------------------------------
+# per-(grid, model, inputs) host schedule and its device table
+# ---------------------------------------------------------------------------
+
+
+def substep_schedule(t, dt, delta):
+    """simulate.py:28-38."""
+    if delta is None:
+        return [(t, dt)]
+    n_sub = max(1, int(np.ceil(dt / delta - 1e-9)))
+    t_end = t + dt
+    return [(t + k * delta, min(delta, t_end - (t + k * delta))) for k in range(n_sub)]
+
+
+def _input_value(inputs, t):
+    if inputs is None:
+        return 0.0
+    if hasattr(inputs, "at"):
+        return float(np.asarray(inputs.at(t), dtype=float).reshape(-1)[0])
+    return float(np.asarray(inputs, dtype=float).reshape(-1)[0])
+
+
+class Schedule:
+    """Per-step sub-step records, observation data and error time lookup."""
+
+    def __init__(self, grid, spec: ModelSpec, inputs, device):
+        times = grid.times
+        S = len(times) - 1
+        recs, self.offsets, self.n_sub, self.sub_end = [], [0] * (S + 1), [0] * (S + 1), [None] * (S + 1)
+        self.host_subs = [None] * (S + 1)
+        self.obs = [None] * (S + 1)
+        for i in range(1, S + 1):
+            t0, t1 = times[i - 1], times[i]
+            dt = t1 - t0
+            if dt <= 0:
+                raise ValueError("step_transition requires dt > 0")
+            subs = substep_schedule(t0, dt, spec.delta)
+            arr = np.zeros(len(subs), dtype=_lib.SUBSTEP_DTYPE)
+            ends = []
+            for k, (t_k, d) in enumerate(subs):
+                arr[k]["d"] = d
+                arr[k]["sd"] = math.sqrt(d)
+                arr[k]["u_in"] = _input_value(inputs, t_k) if spec.n_input else 0.0
+                if spec.has_ode:
+                    n_ode = max(1, int(np.ceil(d / spec.h - 1e-9)))  # simulate.py:85
+                    if n_ode > 4:
+                        raise UnsupportedModelError("more than 4 RK4 steps per sub-step")
+                    for m in range(n_ode):
+                        arr[k]["s"][m] = min(spec.h, d - m * spec.h)  # simulate.py:87
+                    arr[k]["n_ode"] = n_ode
+                ends.append(t_k + d)
+            self.offsets[i] = len(recs)
+            self.n_sub[i] = len(subs)
+            self.sub_end[i] = ends
+            self.host_subs[i] = arr
+            recs.extend(arr)
+            o = grid.obs_at(i)
+            if o is not None:
+                y, mask = o
+                y = np.asarray(y, dtype=float)
+                mask = np.asarray(mask, dtype=bool)
+                bits = 0
+                yy = np.zeros(8)
+                for n in range(spec.n_obs):
+                    if mask[n]:
+                        bits |= 1 << n
+                        yy[n] = y[n]
+                u_obs = _input_value(inputs, t1) if spec.n_input else 0.0
+                self.obs[i] = (bits, yy, u_obs)
+        table = np.array(recs, dtype=_lib.SUBSTEP_DTYPE) if recs else np.zeros(1, _lib.SUBSTEP_DTYPE)
+        self.table = torch.from_numpy(table.view(np.uint8).copy()).to(device)
+        self.times = times
+
+    def subs_ptr(self, i):
+        return self.table.data_ptr() + self.offsets[i] * _lib.SUBSTEP_DTYPE.itemsize
+
+
+def _schedule(grid, spec, inputs, device):
+    key = (spec.name, id(inputs), str(device))
+    cache = grid._device_cache
+    hit = cache.get(key)
+    if hit is None or hit[0] is not inputs:
+        hit = (inputs, Schedule(grid, spec, inputs, device))
+        cache[key] = hit
+    return hit[1]
+
+
+_zero_cache: dict = {}
+
+
+def _zeros_logw(P, tdtype, device):
+    k = (P, tdtype, str(device))
+    z = _zero_cache.get(k)
+    if z is None:
+        z = torch.zeros((1, P), dtype=tdtype, device=device)
+        _zero_cache[k] = z
+    return z
+
+
+def _fs_init(B, device):
+    fs = np.zeros(B, dtype=_lib.FILTER_STATE_DTYPE)
+    fs["uniform"] = 1
+    fs["err_nonfinite"] = _lib.INT32_MAX
+    fs["err_degenerate"] = _lib.INT32_MAX
+    return torch.from_numpy(fs.view(np.uint8).reshape(B, 64).copy()).to(device)
+
+
+def _stack_rows(tensors):
+    """Batch per-filter views; zero-copy when they are consecutive rows of one
+    base tensor (the common case: a run batch advanced together)."""
+    t0 = tensors[0]
+    if len(tensors) == 1:
+        return t0.unsqueeze(0)
+    base = t0._base if t0._base is not None else None
+    if base is not None and base.is_contiguous() and base.dim() == t0.dim() + 1:
+        stride = t0.numel()
+        start = (t0.data_ptr() - base.data_ptr()) // t0.element_size()
+        ok = start % stride == 0 and all(
+            t._base is base and t.data_ptr() == t0.data_ptr() + k * stride * t0.element_size()
+            for k, t in enumerate(tensors)
+        )
+        if ok:
+            r0 = start // stride
+            return base[r0 : r0 + len(tensors)]
+    return torch.stack(tensors)
+
+
+# ---------------------------------------------------------------------------
+# the run object
+# ---------------------------------------------------------------------------
+
+
+class ParticleRun:
+    """Resumable bootstrap particle filter along a FilterGrid, on the GPU."""
+
+    def __init__(self, ir, theta, grid, inputs=None, n_particles=1024, resampler="multinomial",
+                 ess_rel=None, initial_state=None, check_finite=True, *, dtype="float64",
+                 exact=True, noise="device", device=None):
+        if n_particles < 2:
+            raise ValueError("particle filter needs n_particles >= 2")
+        if resampler not in SCHEMES:
+            raise ValueError(f"unknown resampling scheme {resampler!r}")
+        if noise not in ("device", "host"):
+            raise ValueError(f"unknown noise mode {noise!r}")
+        _lib.require_cuda()
+        self.spec = resolve_model(ir)
+        self.ir = ir
+        self.theta = np.asarray(theta, dtype=float).reshape(1, -1)
+        self.grid = as_filter_grid(grid)
+        self.inputs = inputs
+        self.n_particles = int(n_particles)
+        self.resampler = resampler
+        self.ess_rel = ess_rel
+        self.initial_state = initial_state
+        self.check_finite = check_finite
+        self.dtype_name, self.tdtype, self.dtype_id = _dtype_info(dtype)
+        self.exact = bool(exact)
+        self.noise = noise
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.loglik = 0.0
+        self.pos = 0
+        self.weights_uniform = True
+        self.history = []  # per grid index: (x_i [nx, P] tensor, anc_i [P] int32 tensor | None)
+        self._x = None
+        self._a = None  # unnormalised log-weights of the last weighted step
+        self._fs = None  # (64,) uint8 view of an ssm_filter_state
+        self._maybe_nonuniform = False
+        self._derived = None
+
+    # -- protocol -------------------------------------------------------------
+    def init(self, rng):
+        init_runs([self], [rng])
+        return self
+
+    def clone(self):
+        other = ParticleRun.__new__(ParticleRun)
+        other.__dict__ = dict(self.__dict__)
+        other.history = list(self.history)
+        return other
+
+    @property
+    def initialized(self):
+        return self._x is not None
+
+    def advance_to(self, upto, rng):
+        return float(advance_runs([self], upto, [rng])[0])
+
+    def sample_trajectory(self, rng):
+        return sample_trajectories([self], [rng])[0]
+
+    def ess(self):
+        a = self._a if not self.weights_uniform else _zeros_logw(self.n_particles, self.tdtype, self.device)[0]
+        L = _lib.lib()
+        ws = torch.empty(L.ssm_lse_workspace_bytes(1, self.n_particles), dtype=torch.uint8, device=self.device)
+        out = torch.empty(2, dtype=torch.float64, device=self.device)
+        _lib.check(L.ssm_logsumexp(self.dtype_id, 1, self.n_particles, _lib.ptr(a), _lib.ptr(out),
+                                   C_ptr(out, 1), _lib.ptr(ws), _lib.stream_ptr()), "ssm_logsumexp")
+        return float(out[1].item())
+
+    @property
+    def x(self):
+        """(P, nx) float64 host copy (SoA -> AoS transpose on read)."""
+        if self._x is None:
+            return None
+        return self._x.t().to(torch.float64).cpu().numpy()
+
+    @property
+    def logw(self):
+        """(P,) normalised log-weights on the host (particle.py:58)."""
+        if self._x is None:
+            return None
+        P = self.n_particles
+        if self.weights_uniform:
+            return np.full(P, -np.log(P))
+        incr = _fs_view(self._fs)["incr"][0]
+        return self._a.to(torch.float64).cpu().numpy() - incr
+
+    def weighted_mean(self):
+        lw = self.logw
+        w = np.exp(lw - np.max(lw))
+        w /= w.sum()
+        return w @ self.x
+
+    def x_device(self):
+        """(nx, P) device tensor of the current positions (no copy)."""
+        return self._x
+
+
+def C_ptr(t, offset_elems):
+    import ctypes
+
+    return ctypes.c_void_p(t.data_ptr() + offset_elems * t.element_size())
+
+
+def _fs_view(fs_tensor):
+    return fs_tensor.detach().cpu().numpy().reshape(-1).view(_lib.FILTER_STATE_DTYPE)
+
+
+def _common(runs):
+    r0 = runs[0]
+    for r in runs[1:]:
+        if (r.spec is not r0.spec or r.grid is not r0.grid or r.n_particles != r0.n_particles
+                or r.dtype_id != r0.dtype_id or r.resampler != r0.resampler or r.ess_rel != r0.ess_rel
+                or r.check_finite != r0.check_finite or r.exact != r0.exact or r.noise != r0.noise
+                or r.pos != r0.pos or r.device != r0.device or r.inputs is not r0.inputs):
+            raise ValueError("runs advanced together must share model, grid, settings and position")
+    return r0
+
+
+def _derived_tensor(runs):
+    rows = []
+    for r in runs:
+        if r._derived is None:
+            r._derived = r.spec.derived(r.theta)[0]
+        rows.append(r._derived)
+    return torch.from_numpy(np.stack(rows)).to(runs[0].device)
+
+
+def init_runs(runs, rngs):
+    """ParticleRun.init for a batch (particle.py:61-71)."""
+    r0 = _common(runs)
+    B, P, spec = len(runs), r0.n_particles, r0.spec
+    dev = r0.device
+    x = torch.empty((B, spec.nx, P), dtype=r0.tdtype, device=dev)
+    need_draw = [b for b, r in enumerate(runs) if r.initial_state is None]
+    for b, r in enumerate(runs):
+        if r.initial_state is not None:
+            x0 = torch.as_tensor(np.asarray(r.initial_state, dtype=float), dtype=r0.tdtype)
+            x[b].copy_(x0.view(spec.nx, 1).expand(spec.nx, P))
+    if need_draw:
+        if r0.noise == "host":
+            for b in need_draw:
+                x[b].copy_(torch.from_numpy(spec.host_initial(rngs[b], P).T.copy()).to(r0.tdtype))
+        else:
+            keys = np.stack([device_key(rngs[b]) for b in need_draw]).astype(np.uint32)
+            kt = torch.from_numpy(keys.view(np.int32)).to(dev)
+            if len(need_draw) == B:
+                _lib.check(_lib.lib().ssm_init_particles(spec.kernel, r0.dtype_id, B, P, _lib.ptr(kt),
+                                                         _lib.ptr(x), _lib.stream_ptr()), "ssm_init_particles")
+            else:
+                tmp = torch.empty((len(need_draw), spec.nx, P), dtype=r0.tdtype, device=dev)
+                _lib.check(_lib.lib().ssm_init_particles(spec.kernel, r0.dtype_id, len(need_draw), P,
+                                                         _lib.ptr(kt), _lib.ptr(tmp), _lib.stream_ptr()),
+                           "ssm_init_particles")
+                for j, b in enumerate(need_draw):
+                    x[b].copy_(tmp[j])
+    fs = _fs_init(B, dev)
+    for b, r in enumerate(runs):
+        r._x = x[b]
+        r._a = None
+        r._fs = fs[b]
+        r.loglik = 0.0
+        r.pos = 0
+        r.weights_uniform = True
+        r._maybe_nonuniform = False
+        r.history = [(r._x, None)]
+    return runs
+
+
+def advance_runs(runs, upto, rngs):
+    """Advance a batch of runs (same model, grid, P, settings, position)
+    through grid index `upto`; returns the per-run loglik increments
+    (particle.py:87-94).  Raises the reference's exceptions on failure."""
+    r0 = _common(runs)
+    start = r0.pos
+    if upto <= start:
+        for r in runs:
+            r.pos = max(r.pos, upto)
+        return np.zeros(len(runs))
+    L = _lib.lib()
+    B, P, spec = len(runs), r0.n_particles, r0.spec
+    dev, tdt = r0.device, r0.tdtype
+    sched = _schedule(r0.grid, spec, r0.inputs, dev)
+    stream = _lib.stream_ptr()
+    x_prev = _stack_rows([r._x for r in runs])
+    a_last = _stack_rows([r._a for r in runs]) if runs[0]._a is not None else None
+    fs = torch.stack([r._fs for r in runs]).contiguous()  # fresh copy: clones stay untouched
+    theta = _derived_tensor(runs)
+    maybe_nonuniform = r0._maybe_nonuniform
+    host_noise = r0.noise == "host"
+    keys_t = None
+    if not host_noise:
+        keys = np.stack([device_key(g) for g in rngs]).astype(np.uint32)
+        keys_t = torch.from_numpy(keys.view(np.int32)).to(dev)
+    scheme = _lib.SCHEME_IDS[r0.resampler]
+    pw_ws = torch.empty(L.ssm_pw_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
+    scan_ws = torch.empty(L.ssm_scan_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
+    cum = torch.empty((B, P), dtype=torch.int64, device=dev)
+    ess_rel = -1.0 if r0.ess_rel is None else float(r0.ess_rel)
+    log_w0 = float(-np.log(P))
+    obs_log_sd = float(np.log(spec.obs_sd))
+    new_hist = [[] for _ in range(B)]
+    theta_host = theta.cpu().numpy() if host_noise else None
+
+    args = _lib.PwArgs()
+    args.model = spec.kernel
+    args.dtype = r0.dtype_id
+    args.B, args.P = B, P
+    args.exact = 1 if r0.exact else 0
+    args.check_finite = 1 if r0.check_finite else 0
+    args.log_w0 = log_w0
+    args.obs_log_sd = obs_log_sd
+    args.log_sqrt_2pi = float(LOG_SQRT_2PI)
+    args.ess_rel = ess_rel
+    args.theta = theta.data_ptr()
+    args.keys = keys_t.data_ptr() if keys_t is not None else None
+    args.fs = fs.data_ptr()
+    args.workspace = pw_ws.data_ptr()
+
+    for i in range(start + 1, upto + 1):
+        step_rngs = [g.child(i) for g in rngs] if host_noise else None
+        anc = None
+        if maybe_nonuniform:
+            _lib.check(L.ssm_weights_scan(B, P, r0.dtype_id, _lib.ptr(a_last), 1, None, _lib.ptr(fs),
+                                          _lib.ptr(cum), None, _lib.ptr(scan_ws), stream), "ssm_weights_scan")
+            anc = torch.empty((B, P), dtype=torch.int32, device=dev)
+            u_t = None
+            if host_noise:
+                rr = [s.child(_RESAMPLE_KEY) for s in step_rngs]
+                if r0.resampler == "systematic":
+                    u = np.array([[g.uniform()] for g in rr])
+                else:
+                    u = np.stack([g.uniform(size=P) for g in rr])
+                u_t = torch.from_numpy(u).to(dev)
+            _lib.check(L.ssm_resample_search(B, P, P, scheme, 1, _lib.ptr(cum), _lib.ptr(u_t),
+                                             _lib.ptr(keys_t), i, _lib.ptr(fs), _lib.ptr(anc), stream),
+                       "ssm_resample_search")
+        n_sub = sched.n_sub[i]
+        x_out = torch.empty((B, spec.nx, P), dtype=tdt, device=dev)
+        noise_t = None
+        if host_noise:
+            noise = np.stack([spec.host_noise(s.child(_PROPAGATE_KEY), sched.host_subs[i], P, theta_row)
+                              for s, theta_row in zip(step_rngs, theta_host)])
+            noise_t = torch.from_numpy(noise).to(dev, tdt)
+        obs = sched.obs[i]
+        a_out = torch.empty((B, P), dtype=tdt, device=dev) if obs is not None else None
+        args.step = i
+        args.n_sub = n_sub
+        args.subs = sched.subs_ptr(i)
+        args.x_in = x_prev.data_ptr()
+        args.x_out = x_out.data_ptr()
+        args.anc = anc.data_ptr() if anc is not None else None
+        args.a_prev = a_last.data_ptr() if a_last is not None else None
+        args.a_out = a_out.data_ptr() if a_out is not None else None
+        args.noise = noise_t.data_ptr() if noise_t is not None else None
+        if obs is not None:
+            args.has_obs = 1
+            args.obs_mask = obs[0]
+            for n in range(8):
+                args.y[n] = float(obs[1][n])
+            args.u_obs = obs[2]
+        else:
+            args.has_obs = 0
+            args.obs_mask = 0
+        _lib.check(L.ssm_propagate_weight(args, stream), "ssm_propagate_weight")
+        for b in range(B):
+            new_hist[b].append((x_out[b], anc[b] if anc is not None else None))
+        x_prev = x_out
+        if obs is not None:
+            a_last = a_out
+            maybe_nonuniform = True
+        elif maybe_nonuniform and r0.ess_rel is None:
+            maybe_nonuniform = False
+
+    fs_host = _fs_view(fs)  # one synchronisation per advance
+    incr = np.empty(B)
+    for b, r in enumerate(runs):
+        st = fs_host[b]
+        _raise_if_failed(st, sched, r.check_finite)
+        incr[b] = float(st["loglik"]) - r.loglik
+        r.loglik = float(st["loglik"])
+        r.weights_uniform = bool(st["uniform"])
+        r._x = x_prev[b]
+        r._a = a_last[b] if a_last is not None else None
+        r._fs = fs[b]
+        r._maybe_nonuniform = maybe_nonuniform
+        r.history.extend(new_hist[b])
+        r.pos = upto
+    return incr
+
+
+def _raise_if_failed(st, sched, check_finite):
+    nf = int(st["err_nonfinite"])
+    dg = int(st["err_degenerate"])
+    if nf == _lib.INT32_MAX and dg == _lib.INT32_MAX:
+        return
+    nf_step = nf // 64 if nf != _lib.INT32_MAX else None
+    if nf_step is not None and (dg == _lib.INT32_MAX or nf_step <= dg) and check_finite:
+        t = sched.sub_end[nf_step][nf % 64]
+        raise NonFiniteStateError(f"non-finite state after transition sub-step ending at t={t:g}", time=t)
+    if dg != _lib.INT32_MAX:
+        t = float(sched.times[dg])
+        raise DegenerateEnsembleError(f"all particle weights vanished at t={t:g}", time=t)
+
+
+def sample_trajectories(runs, rngs):
+    """ParticleRun.sample_trajectory for a batch (particle.py:137-149): one
+    multinomial draw by final weight (host uniform, the reference's draw),
+    device CDF + search, then a device ancestry trace."""
+    r0 = runs[0]
+    L = _lib.lib()
+    B, P, nx = len(runs), r0.n_particles, r0.spec.nx
+    dev = r0.device
+    S = r0.pos
+    stream = _lib.stream_ptr()
+    # final log-weights (uniform -> zeros with shift 0)
+    a_rows, shifts = [], []
+    for r in runs:
+        if r.weights_uniform or r._a is None:
+            a_rows.append(_zeros_logw(P, r0.tdtype, dev)[0])
+            shifts.append(None)
+        else:
+            a_rows.append(r._a)
+            shifts.append(r._fs)
+    a = _stack_rows(a_rows)
+    shift = torch.zeros(B, dtype=torch.float64, device=dev)
+    for b, f in enumerate(shifts):
+        if f is not None:
+            shift[b : b + 1].copy_(f[8:16].view(torch.float64))  # ssm_filter_state.incr
+    scan_ws = torch.empty(L.ssm_scan_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
+    cum = torch.empty((B, P), dtype=torch.int64, device=dev)
+    _lib.check(L.ssm_weights_scan(B, P, r0.dtype_id, _lib.ptr(a), 1, _lib.ptr(shift), None, _lib.ptr(cum),
+                                  None, _lib.ptr(scan_ws), stream), "ssm_weights_scan")
+    u = torch.from_numpy(np.array([[float(np.asarray(g.uniform(size=1))[0])] for g in rngs])).to(dev)
+    j = torch.empty((B, 1), dtype=torch.int32, device=dev)
+    _lib.check(L.ssm_resample_search(B, P, 1, _lib.SCHEME_IDS["multinomial"], 1, _lib.ptr(cum), _lib.ptr(u),
+                                     None, 0, None, _lib.ptr(j), stream), "ssm_resample_search")
+    xs = np.zeros((B, S + 1), dtype=np.int64)
+    ancs = np.zeros((B, S + 1), dtype=np.int64)
+    for b, r in enumerate(runs):
+        if len(r.history) != S + 1:
+            raise ValueError("history length does not match the run position")
+        for i, (xi, ai) in enumerate(r.history):
+            xs[b, i] = xi.data_ptr()
+            ancs[b, i] = ai.data_ptr() if ai is not None else 0
+    xs_t = torch.from_numpy(xs).to(dev)
+    ancs_t = torch.from_numpy(ancs).to(dev)
+    out = torch.empty((B, S + 1, nx), dtype=torch.float64, device=dev)
+    _lib.check(L.ssm_trace(r0.dtype_id, B, S, nx, P, _lib.ptr(xs_t), _lib.ptr(ancs_t), _lib.ptr(j),
+                           _lib.ptr(out), stream), "ssm_trace")
+    return list(out.cpu().numpy())
+
+
+def particle_filter(ir, theta, grid, rng, inputs=None, n_particles=1024, resampler="multinomial",
+                    ess_rel=None, initial_state=None, check_finite=True, upto=None, **device_opts):
+    """particle.py:156-185 on the GPU: init(child 0) -> advance(child 1) ->
+    sample_trajectory(child 2).  device_opts: dtype, exact, noise, device."""
+    run = ParticleRun(ir, theta, grid, inputs=inputs, n_particles=n_particles, resampler=resampler,
+                      ess_rel=ess_rel, initial_state=initial_state, check_finite=check_finite,
+                      **device_opts)
+    run.init(rng.child(0))
+    run.advance_to(run.grid.last if upto is None else upto, rng.child(1))
+    trajectory = run.sample_trajectory(rng.child(2))
+    return FilterOutcome(loglik=run.loglik, trajectory=trajectory, summaries=[], run=run)

@@ -1,0 +1,362 @@
+"""The two hand-written model kernels and their host-side theta-level logic.
+
+A `ModelSpec` stands in for the reference's `ModelIr` (core/ir.py:83-121) on
+the device path: it carries the slot counts, the transition `delta`, the
+per-filter derived constants the kernels consume, and the host-side
+parameter/initial/proposal blocks used by the PMMH and SMC^2 outer loops.
+
+`resolve_model` also accepts a reference `ModelIr` (duck-typed) and maps it
+onto a kernel after checking that its compiled expressions are exactly the
+ones the kernel implements; anything else raises UnsupportedModelError
+(no CPU fallback, per the north star).
+
+Model sources: pkg/models/lorenz96/Lorenz96.bi and
+pkg/models/windkessel/Windkessel.bi of the reference.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+from scipy.special import gammaln, ndtr, ndtri
+
+from . import _lib
+from .errors import DistributionParameterError, UnsupportedModelError
+
+LOG_SQRT_2PI = 0.5 * np.log(2.0 * np.pi)  # distributions.py:15
+
+
+# ---------------------------------------------------------------------------
+# host distributions (distributions.py:73-123), theta-level only
+# ---------------------------------------------------------------------------
+
+
+def _require(ok, msg):
+    if not np.all(ok):
+        raise DistributionParameterError(msg)
+
+
+def d_uniform_sample(rng, lo, hi, size):
+    _require(np.asarray(lo) < np.asarray(hi), "uniform needs lower < upper")
+    return rng.uniform(lo, hi, size=size)
+
+
+def d_uniform_logpdf(x, lo, hi):
+    x = np.asarray(x, dtype=float)
+    lo, hi = np.asarray(lo, dtype=float), np.asarray(hi, dtype=float)
+    return np.where((x >= lo) & (x <= hi), -np.log(hi - lo), -np.inf)
+
+
+def d_gamma_sample(rng, shape, scale, size):
+    return rng.gamma(shape, scale, size=size)
+
+
+def d_gamma_logpdf(x, shape, scale):
+    x = np.asarray(x, dtype=float)
+    shape, scale = np.asarray(shape, dtype=float), np.asarray(scale, dtype=float)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        core = (shape - 1.0) * np.log(x) - x / scale - shape * np.log(scale) - gammaln(shape)
+    return np.where(x > 0, core, -np.inf)
+
+
+def d_invgamma_sample(rng, shape, scale, size):
+    _require(np.asarray(shape) > 0, "inverse_gamma shape must be > 0")
+    _require(np.asarray(scale) > 0, "inverse_gamma scale must be > 0")
+    return 1.0 / rng.gamma(shape, 1.0 / np.asarray(scale, dtype=float), size=size)
+
+
+def d_invgamma_logpdf(x, shape, scale):
+    x = np.asarray(x, dtype=float)
+    shape, scale = np.asarray(shape, dtype=float), np.asarray(scale, dtype=float)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        core = shape * np.log(scale) - gammaln(shape) - (shape + 1.0) * np.log(x) - scale / x
+    return np.where(x > 0, core, -np.inf)
+
+
+def d_gauss_logpdf(x, mean, sd):
+    z = (np.asarray(x, dtype=float) - mean) / sd
+    return -0.5 * z * z - np.log(sd) - LOG_SQRT_2PI
+
+
+def d_tgauss_sample(rng, mean, sd, lower, upper, size):
+    mean, sd, lower, upper = (np.asarray(a, dtype=float) for a in (mean, sd, lower, upper))
+    _require(sd > 0, "truncated_gaussian sd must be > 0")
+    _require(lower < upper, "truncated_gaussian needs lower < upper")
+    fa = ndtr((lower - mean) / sd)
+    fb = ndtr((upper - mean) / sd)
+    _require(fb - fa > 0, "truncated_gaussian truncation region has no mass")
+    u = rng.uniform(size=size)
+    return mean + sd * ndtri(fa + u * (fb - fa))
+
+
+def d_tgauss_logpdf(x, mean, sd, lower, upper):
+    mean, sd, lower, upper = (np.asarray(a, dtype=float) for a in (mean, sd, lower, upper))
+    fa = ndtr((lower - mean) / sd)
+    fb = ndtr((upper - mean) / sd)
+    _require(fb - fa > 0, "truncated_gaussian truncation region has no mass")
+    x = np.asarray(x, dtype=float)
+    z = (x - mean) / sd
+    core = -0.5 * z * z - np.log(sd) - LOG_SQRT_2PI - np.log(fb - fa)
+    return np.where((x >= lower) & (x <= upper), core, -np.inf)
+
+
+# ---------------------------------------------------------------------------
+# model specs
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class ModelSpec:
+    name: str
+    kernel: int
+    n_param: int
+    n_state: int
+    n_noise: int
+    n_input: int
+    n_obs: int
+    delta: float  # transition sub-step (simulate.py:28-38)
+    h: float  # model const h
+    obs_sd: float
+    has_ode: bool
+
+    @property
+    def nx(self):
+        return self.n_state
+
+    @property
+    def has_proposal_initial(self):
+        return self.name == "Lorenz96"
+
+    # ModelIr-compatible accessors used by callers of the reference API
+    @property
+    def counts(self):
+        return {"param": self.n_param, "input": self.n_input, "noise": self.n_noise,
+                "state": self.n_state, "obs": self.n_obs}
+
+    def block(self, name):
+        if name == "proposal_initial":
+            return True if self.has_proposal_initial else None
+        return True
+
+    def slot_labels(self, role):
+        if self.name == "Lorenz96":
+            base = {"param": ["F", "sigma2"], "state": [f"x[{i}]" for i in range(8)],
+                    "noise": [f"deltaW[{i}]" for i in range(8)], "obs": [f"y[{i}]" for i in range(8)],
+                    "input": []}
+        else:
+            base = {"param": ["R", "C", "Z", "sigma2"], "state": ["Pp"], "noise": ["xi"],
+                    "obs": ["Pa"], "input": ["F"]}
+        return list(base[role])
+
+    # ---- per-filter derived constants for the kernels ----------------------
+    def derived(self, thetas) -> np.ndarray:
+        """(B, 4) float64 constants, computed with the same numpy operations
+        the compiled reference lambdas use (bit-identical)."""
+        th = np.atleast_2d(np.asarray(thetas, dtype=float))
+        out = np.zeros((th.shape[0], 4))
+        for b in range(th.shape[0]):
+            row = th[b : b + 1]
+            if self.name == "Lorenz96":
+                out[b, 0] = row[0, 0]  # F
+                out[b, 1] = np.sqrt(row[:, 1])[0]  # np.sqrt(T[:, 1])
+            else:
+                # ((np.exp(((-0.01) / (T[:, 0] * T[:, 1]))) * X) +
+                #  ((T[:, 0] * (1.0 - np.exp(...))) * (U[0] + W)))   Windkessel.bi:28-29
+                a = np.exp(((-0.01) / (row[:, 0] * row[:, 1])))
+                out[b, 0] = a[0]
+                out[b, 1] = (row[:, 0] * (1.0 - a))[0]
+                out[b, 2] = row[0, 2]  # Z
+                out[b, 3] = (0.01 * np.sqrt(row[:, 3]))[0]  # xi sd, Windkessel.bi:28
+        return out
+
+    # ---- host draws in the reference's order (noise="host" parity mode) ----
+    def host_initial(self, rng, P):
+        """simulate.sample_initial draws (simulate.py:111-129), (P, nx)."""
+        x = np.zeros((P, self.nx))
+        if self.name == "Lorenz96":
+            for n in range(8):
+                x[:, n] = rng.uniform(-1.0, 3.0, size=P)
+        else:
+            x[:, 0] = rng.normal(90.0, 15.0, size=P)
+        return x
+
+    def host_noise(self, rng, subs, P, derived_row):
+        """Noise-variable values per sub-step in the reference draw order
+        (simulate.py:50-60, 151-157): (n_sub, n_noise, P)."""
+        out = np.empty((len(subs), self.n_noise, P))
+        for k, s in enumerate(subs):
+            if self.name == "Lorenz96":
+                sd = math.sqrt(s["d"])
+                for n in range(8):
+                    out[k, n] = rng.normal(0.0, sd, size=P)
+            else:
+                out[k, 0] = rng.normal(0.0, np.array([derived_row[3]]), size=P)
+        return out
+
+    # ---- theta-level blocks (host) -----------------------------------------
+    def sample_parameter(self, rng, size=1):
+        """simulate.sample_parameter (simulate.py:96-108): (size, n_param)."""
+        th = np.zeros((size, self.n_param))
+        if self.name == "Lorenz96":
+            th[:, 0] = d_uniform_sample(rng, 8.0, 12.0, size)
+            th[:, 1] = d_invgamma_sample(rng, 2.0, 0.25, size)
+        else:
+            th[:, 0] = d_gamma_sample(rng, 2.0, 0.9, size)
+            th[:, 1] = d_gamma_sample(rng, 2.0, 1.5, size)
+            th[:, 2] = d_gamma_sample(rng, 2.0, 0.03, size)
+            th[:, 3] = d_invgamma_sample(rng, 2.0, 25.0, size)
+        return th
+
+    def sample_initial(self, thetas, rng, size=None):
+        """simulate.sample_initial with theta batch (used for x0 proposals)."""
+        th = np.atleast_2d(thetas)
+        size = th.shape[0] if size is None else size
+        return self.host_initial(rng, size)
+
+    def parameter_logpdf(self, theta):
+        theta = np.asarray(theta, dtype=float)
+        if self.name == "Lorenz96":
+            return float(np.sum(d_uniform_logpdf(theta[0], 8.0, 12.0))) + float(
+                np.sum(d_invgamma_logpdf(theta[1], 2.0, 0.25)))
+        total = 0.0
+        for j, sc in enumerate((0.9, 1.5, 0.03)):
+            total += float(np.sum(d_gamma_logpdf(theta[j], 2.0, sc)))
+        return total + float(np.sum(d_invgamma_logpdf(theta[3], 2.0, 25.0)))
+
+    def initial_logpdf(self, theta, x0):
+        x0 = np.asarray(x0, dtype=float)
+        if self.name == "Lorenz96":
+            total = 0.0
+            for n in range(8):
+                total += float(np.sum(d_uniform_logpdf(x0[n], -1.0, 3.0)))
+            return total
+        return float(np.sum(d_gauss_logpdf(x0[0], 90.0, 15.0)))
+
+    def _walk_parameters(self, theta, rng, theta_to=None):
+        """proposal_parameter walk (simulate.py:272-313): statements run in
+        order; each statement's arguments see the pre-statement values."""
+        theta = np.asarray(theta, dtype=float)
+        cur = theta[None, :].copy()
+        out = theta.copy()
+        logq = 0.0
+        if self.name == "Lorenz96":
+            stmts = [
+                (0, "tg", lambda T: (T[:, 0], 0.1, 8.0, 12.0)),
+                (1, "ig", lambda T: (2.0, (3.0 * T[:, 1]))),
+            ]
+        else:
+            stmts = [
+                (0, "tg", lambda T: (T[:, 0], 0.03, 0.0, np.inf)),
+                (1, "tg", lambda T: (T[:, 1], 0.1, 0.0, np.inf)),
+                (2, "tg", lambda T: (T[:, 2], 0.002, 0.0, np.inf)),
+                (3, "ig", lambda T: (2.0, (3.0 * T[:, 3]))),
+            ]
+        for slot, kind, argf in stmts:
+            args = argf(cur)
+            if kind == "tg":
+                if theta_to is None:
+                    value = float(d_tgauss_sample(rng, *args, 1)[0])
+                else:
+                    value = float(theta_to[slot])
+                logq += float(np.sum(d_tgauss_logpdf(value, *args)))
+            else:
+                if theta_to is None:
+                    value = float(d_invgamma_sample(rng, *args, 1)[0])
+                else:
+                    value = float(theta_to[slot])
+                logq += float(np.sum(d_invgamma_logpdf(value, *args)))
+            out[slot] = value
+            cur[0, slot] = value
+        return out, logq
+
+    def propose_parameters(self, theta, rng):
+        return self._walk_parameters(theta, rng)
+
+    def proposal_parameter_logpdf(self, theta_from, theta_to):
+        return self._walk_parameters(theta_from, None, theta_to)[1]
+
+    def _walk_initial(self, x0, rng, x_to=None):
+        x0 = np.asarray(x0, dtype=float)
+        out = x0.copy()
+        logq = 0.0
+        args = [(x0[n : n + 1], 0.1, -1.0, 3.0) for n in range(8)]  # pre-statement env
+        for n in range(8):
+            if x_to is None:
+                value = float(d_tgauss_sample(rng, *args[n], 1)[0])
+            else:
+                value = float(x_to[n])
+            logq += float(np.sum(d_tgauss_logpdf(value, *args[n])))
+            out[n] = value
+        return out, logq
+
+    def propose_initial(self, theta, x0, rng):
+        if not self.has_proposal_initial:
+            raise UnsupportedModelError(f"{self.name} has no proposal_initial block")
+        return self._walk_initial(x0, rng)
+
+    def proposal_initial_logpdf(self, theta, x_from, x_to):
+        return self._walk_initial(x_from, None, x_to)[1]
+
+
+LORENZ96 = ModelSpec("Lorenz96", _lib.SSM_MODEL_LORENZ96, 2, 8, 8, 0, 8, 0.05, 0.05, 0.5, True)
+WINDKESSEL = ModelSpec("Windkessel", _lib.SSM_MODEL_WINDKESSEL, 4, 1, 1, 1, 1, 0.01, 0.01, 2.0, False)
+_BY_NAME = {"lorenz96": LORENZ96, "windkessel": WINDKESSEL}
+
+# Expression fingerprints of the reference's compiled lambdas (ir.py:188-214)
+# that the kernels implement; a ModelIr must match exactly to be accepted.
+_L96_TRANSITION_SLOT0 = (
+    "((((X[:, 7] * (X[:, 1] - X[:, 6])) - X[:, 0]) + T[:, 0]) + ((np.sqrt(T[:, 1]) * W[:, 0]) / 0.05))"
+)
+_WK_TRANSITION = (
+    "((np.exp(((-0.01) / (T[:, 0] * T[:, 1]))) * X[:, 0]) + ((T[:, 0] * (1.0 - "
+    "np.exp(((-0.01) / (T[:, 0] * T[:, 1]))))) * (U[0] + W[:, 0])))"
+)
+
+
+def _ir_fingerprint(ir):
+    """Source of the first transition expression of a reference ModelIr,
+    regenerated with the reference's own expr_source if importable."""
+    try:
+        from ssmkit.core import ir as I  # the reference, when installed alongside
+    except Exception:  # pragma: no cover - reference absent
+        return None
+    block = ir.block("transition")
+    for op in block.ops:
+        if hasattr(op, "items") and op.items:
+            eq, b = op.items[0]
+            return I.expr_source(eq.expr, (ir.consts, ir.vars), b)
+        if type(op).__name__ == "AssignStmtOp":
+            return I.expr_source(op.stmt.expr, (ir.consts, ir.vars), op.bindings[0])
+    return None
+
+
+def resolve_model(model) -> ModelSpec:
+    """ModelSpec | "lorenz96" | "windkessel" | reference ModelIr -> ModelSpec."""
+    if isinstance(model, ModelSpec):
+        return model
+    if isinstance(model, str):
+        spec = _BY_NAME.get(model.lower())
+        if spec is None:
+            raise UnsupportedModelError(f"no sm_100a kernel for model {model!r}")
+        return spec
+    name = getattr(model, "name", None)
+    counts = getattr(model, "counts", None)
+    spec = _BY_NAME.get(str(name).lower()) if name else None
+    if spec is None or counts is None:
+        raise UnsupportedModelError(f"no sm_100a kernel for model {name!r}")
+    if dict(counts) != spec.counts or float(getattr(model, "delta", -1)) != spec.delta:
+        raise UnsupportedModelError(f"model {name!r} does not match the {spec.name} kernel")
+    fp = _ir_fingerprint(model)
+    want = _L96_TRANSITION_SLOT0 if spec is LORENZ96 else _WK_TRANSITION
+    if fp is not None and fp != want:
+        raise UnsupportedModelError(f"model {name!r} transition differs from the {spec.name} kernel")
+    return spec
+
+
+def load_model(name_or_path: str) -> ModelSpec:
+    """Resolve a model by name or by the file name of its .bi source."""
+    base = name_or_path.replace("\\", "/").rsplit("/", 1)[-1]
+    base = base[:-3] if base.endswith(".bi") else base
+    return resolve_model(base)

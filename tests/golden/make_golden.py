@@ -292,7 +292,51 @@ def gen_pf():
         res = particle_filter(ir, theta, grid, RngStream(7), inputs=inputs, n_particles=1024, resampler=scheme)
         out[f"wk/{scheme}/loglik"] = np.array(res.loglik)
         out[f"wk/{scheme}/traj"] = res.trajectory
+    # exact likelihood from the reference's Kalman filter (statistical oracle)
+    from ssmkit.inference import kalman_filter
+    from ssmkit.lineargauss import extract_linear_gaussian
+    system = extract_linear_gaussian(ir, theta, grid.times, inputs)
+    out["wk/kf_loglik"] = np.array(kalman_filter(system, grid, RngStream(0)).loglik)
     save("pf.npz", **out)
+
+
+def gen_theta_level():
+    """Host theta-level blocks (prior, proposals, densities) for both models,
+    with the `inf` compile shim for windkessel (SURVEY 8c known defect)."""
+    import ssmkit.core.ir as I
+
+    I.compile_expr = lambda e, t, b: eval(
+        f"lambda T, X, W, U: {I.expr_source(e, t, b)}", {"np": np, "inf": np.inf, "__builtins__": {}}
+    )
+    out = {}
+    for name in ("lorenz96", "windkessel"):
+        ir = load(name)
+        th = simulate.sample_parameter(ir, RngStream(3), size=5)
+        out[f"{name}/prior_draws"] = th
+        out[f"{name}/prior_logpdf"] = np.array([simulate.parameter_logpdf(ir, t) for t in th])
+        props, fwd, rev = [], [], []
+        for k, t in enumerate(th):
+            tn, lq = simulate.propose_parameters(ir, t, RngStream(4, (k,)))
+            props.append(tn)
+            fwd.append(lq)
+            rev.append(simulate.proposal_parameter_logpdf(ir, tn, t))
+        out[f"{name}/proposals"] = np.array(props)
+        out[f"{name}/logq_fwd"] = np.array(fwd)
+        out[f"{name}/logq_rev"] = np.array(rev)
+        if ir.block("proposal_initial") is not None:
+            x0 = simulate.sample_initial(ir, th, RngStream(5), size=5)
+            out[f"{name}/init_draws"] = x0
+            out[f"{name}/init_logpdf"] = np.array([simulate.initial_logpdf(ir, th[k], x0[k]) for k in range(5)])
+            xp, lq = [], []
+            for k in range(5):
+                a, b = simulate.propose_initial(ir, th[k], x0[k], RngStream(6, (k,)))
+                xp.append(a)
+                lq.append(b)
+            out[f"{name}/init_props"] = np.array(xp)
+            out[f"{name}/init_logq"] = np.array(lq)
+            out[f"{name}/init_logq_rev"] = np.array(
+                [simulate.proposal_initial_logpdf(ir, th[k], xp[k], x0[k]) for k in range(5)])
+    save("theta.npz", **out)
 
 
 if __name__ == "__main__":
@@ -301,3 +345,4 @@ if __name__ == "__main__":
     gen_l96_step()
     gen_wk_step()
     gen_pf()
+    gen_theta_level()

@@ -1,0 +1,126 @@
+"""CPU-only tests: the C-ABI library loads and exports every symbol the
+header declares; host-side logic (theta-level blocks, grids, derived kernel
+constants, schedules) matches the reference's golden vectors / the oracle."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import ssm_oracle as O
+from paper_1306_3277_b200 import LORENZ96, WINDKESSEL, RngStream, _lib, load_model, resolve_model
+from paper_1306_3277_b200.errors import UnsupportedModelError
+from paper_1306_3277_b200.inference import build_filter_grid
+from paper_1306_3277_b200.rng import device_key
+from tests.conftest import ROOT, load_golden
+
+HEADER = os.path.join(ROOT, "include", "ssm_b200.h")
+
+
+def header_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int|size_t)\s+(ssm_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load_library()
+    names = header_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in _lib.SIGNATURES, f"{n} has no ctypes signature"
+    assert lib.ssm_version().decode().startswith("ssm_b200")
+
+
+def test_library_is_sm100a():
+    so = _lib.LIB_PATH
+    out = os.popen(f"cuobjdump --list-elf {so} 2>&1").read()
+    assert "sm_100a" in out
+
+
+def test_struct_layouts_match_header():
+    import ctypes as C
+
+    assert C.sizeof(_lib.Substep) == 64
+    assert _lib.FILTER_STATE_DTYPE.itemsize == 64
+    # PwArgs: 10 int32 + 8 doubles + 5 doubles + 11 pointers
+    assert C.sizeof(_lib.PwArgs) == 10 * 4 + 13 * 8 + 11 * 8
+
+
+def test_status_strings_no_device_needed():
+    lib = _lib.load_library()
+    assert lib.ssm_status_string(0) == b"ok"
+    assert lib.ssm_status_string(1) == b"invalid argument"
+    assert lib.ssm_pw_workspace_bytes(2, 1024) > 0
+    assert lib.ssm_scan_workspace_bytes(1, 1 << 20) > 0
+
+
+def test_invalid_args_rejected_without_device():
+    lib = _lib.load_library()
+    assert lib.ssm_propagate_weight(None, None) == _lib.SSM_ERR_INVALID_ARG
+    assert lib.ssm_gather(1, 0, 8, 16, None, None, None, None) == _lib.SSM_ERR_INVALID_ARG
+    assert lib.ssm_resample_search(1, 4, 4, 9, 0, None, None, None, 0, None, None, None) == _lib.SSM_ERR_INVALID_ARG
+
+
+def test_resolve_model():
+    assert resolve_model("lorenz96") is LORENZ96
+    assert load_model("/x/y/Windkessel.bi") is WINDKESSEL
+    with pytest.raises(UnsupportedModelError):
+        resolve_model("SIR")
+
+
+@pytest.mark.parametrize("name,spec", [("lorenz96", LORENZ96), ("windkessel", WINDKESSEL)])
+def test_theta_level_blocks_match_reference(name, spec):
+    g = load_golden("theta.npz")
+    th = spec.sample_parameter(RngStream(3), size=5)
+    np.testing.assert_array_equal(th, g[f"{name}/prior_draws"])
+    np.testing.assert_array_equal([spec.parameter_logpdf(t) for t in th], g[f"{name}/prior_logpdf"])
+    for k, t in enumerate(th):
+        tn, lq = spec.propose_parameters(t, RngStream(4, (k,)))
+        np.testing.assert_array_equal(tn, g[f"{name}/proposals"][k])
+        assert lq == g[f"{name}/logq_fwd"][k]
+        assert spec.proposal_parameter_logpdf(tn, t) == g[f"{name}/logq_rev"][k]
+    if spec.has_proposal_initial:
+        x0 = spec.sample_initial(th, RngStream(5), size=5)
+        np.testing.assert_array_equal(x0, g[f"{name}/init_draws"])
+        for k in range(5):
+            assert spec.initial_logpdf(th[k], x0[k]) == g[f"{name}/init_logpdf"][k]
+            xp, lq = spec.propose_initial(th[k], x0[k], RngStream(6, (k,)))
+            np.testing.assert_array_equal(xp, g[f"{name}/init_props"][k])
+            assert lq == g[f"{name}/init_logq"][k]
+            assert spec.proposal_initial_logpdf(th[k], xp, x0[k]) == g[f"{name}/init_logq_rev"][k]
+
+
+def test_windkessel_derived_constants_bitwise():
+    for theta in ([1.8, 3.0, 0.06, 25.0], [0.9, 1.5, 0.03, 10.0]):
+        d = WINDKESSEL.derived(theta)[0]
+        a, b = O.wk_coeffs(theta)
+        assert d[0] == a and d[1] == b
+        assert d[3] == 0.01 * np.sqrt(np.array([theta[3]]))[0]
+    d = LORENZ96.derived([10.0, 0.1])[0]
+    assert d[0] == 10.0 and d[1] == np.sqrt(0.1)
+
+
+def test_filter_grid_matches_reference():
+    g = load_golden("pf.npz")
+    grid = build_filter_grid(0.0, 2.0, 20, g["l96/obs_t"], g["l96/obs_v"], g["l96/obs_m"], n_obs=8)
+    np.testing.assert_array_equal(grid.times, g["l96/times"])
+    assert grid.obs_steps == list(range(1, 21))
+
+
+def test_device_key_is_seedsequence_hash():
+    k1 = device_key(RngStream(7, (1,)))
+    k2 = device_key(RngStream(7, (2,)))
+    assert k1.dtype == np.uint32 and k1.shape == (2,)
+    assert not np.array_equal(k1, k2)
+    np.testing.assert_array_equal(k1, device_key(RngStream(7).child(1)))
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1306_3277_b200")
+    pat = re.compile(r"^\s*(from|import)\s+\S*oracle", re.M)
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                assert not pat.search(open(os.path.join(dirpath, f)).read()), f

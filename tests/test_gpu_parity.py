@@ -1,0 +1,308 @@
+"""GPU parity tests: the CUDA path through the C ABI against the reference's
+golden vectors and the CPU oracle.  Tolerances (north star / SURVEY 8c):
+  - ancestors: exact, given identical (cum, u);
+  - float64 exact mode: bitwise for L96 states / log-weights (reference op
+    order, no FMA), 1e-12 relative for LSE-accumulated likelihoods;
+  - float32: norm-wise relative ||out - ref||_inf / ||ref||_inf <= 1e-5.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ssm_oracle as O
+from paper_1306_3277_b200 import LORENZ96, WINDKESSEL, RngStream
+from paper_1306_3277_b200 import simulate as S
+from paper_1306_3277_b200.errors import DegenerateEnsembleError, NonFiniteStateError
+from paper_1306_3277_b200.inference import (FilterRunner, ParticleRun, advance_runs, build_filter_grid,
+                                            init_runs, particle_filter, resample, sample_trajectories,
+                                            search_cdf)
+from tests.conftest import LocfInputs, load_golden
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["onehot", "half", "ties", "zeros_mixed", "lognormal_1k", "uniform_4097", "degenerate_2k", "tiny_16384"]
+SCHEMES = ["multinomial", "stratified", "systematic"]
+
+
+def normwise(a, b):
+    return float(np.max(np.abs(np.asarray(a) - np.asarray(b))) / max(np.max(np.abs(b)), 1e-300))
+
+
+class FixedU:
+    def __init__(self, u):
+        self.u = np.asarray(u, dtype=float)
+
+    def uniform(self, low=0.0, high=1.0, size=None):
+        return float(self.u[0]) if size is None else self.u[:size].copy()
+
+
+# ------------------------------------------------------------------ resampling
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_search_exact_on_injected_cdf(case, scheme):
+    g = load_golden("resample.npz")
+    anc = search_cdf(g[f"{case}/cum"], g[f"{case}/{scheme}/u"], scheme)
+    np.testing.assert_array_equal(anc, g[f"{case}/{scheme}/anc"])
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_resample_api_matches_reference(case, scheme):
+    g = load_golden("resample.npz")
+    anc = resample(g[f"{case}/w"], scheme, FixedU(g[f"{case}/{scheme}/u"]))
+    np.testing.assert_array_equal(anc, g[f"{case}/{scheme}/anc"])
+
+
+def test_resample_tie_kat_and_errors():
+    g = load_golden("resample.npz")
+    anc = resample(g["kat_ties/w"], "multinomial", FixedU(g["kat_ties/u"]), size=5)
+    np.testing.assert_array_equal(anc, [1, 0, 1, 2, 2])
+    with pytest.raises(ValueError):
+        resample(np.array([0.5, -0.1]), "systematic", FixedU([0.3]))
+    with pytest.raises(ValueError):
+        resample(np.array([0.5, np.nan]), "systematic", FixedU([0.3]))
+    with pytest.raises(DegenerateEnsembleError):
+        resample(np.zeros(5), "systematic", FixedU([0.3]))
+    with pytest.raises(ValueError):
+        resample(np.zeros(0), "systematic", FixedU([0.3]))
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_search_large_random_vs_numpy(scheme):
+    rs = np.random.default_rng(5)
+    P = (1 << 20) + 17
+    w = np.exp(rs.normal(0, 2, P))
+    cum = O.cumulative(w)
+    u = rs.random(1 if scheme == "systematic" else P)
+    ref = O.resample_with(w, scheme, u)
+    np.testing.assert_array_equal(search_cdf(cum, u, scheme), ref)
+
+
+def test_scan_cdf_is_deterministic_and_close():
+    from paper_1306_3277_b200 import _lib
+
+    L = _lib.lib()
+    rs = np.random.default_rng(9)
+    P = 3_000_001
+    w = np.exp(rs.normal(0, 3, P))
+    dev = torch.device("cuda")
+    wt = torch.from_numpy(w).to(dev)
+    outs = []
+    for _ in range(3):
+        ws = torch.empty(L.ssm_scan_workspace_bytes(1, P), dtype=torch.uint8, device=dev)
+        C = torch.empty(P, dtype=torch.int64, device=dev)
+        cum = torch.empty(P, dtype=torch.float64, device=dev)
+        flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.check(L.ssm_weights_scan(1, P, 1, _lib.ptr(wt), 0, None, None, _lib.ptr(C), _lib.ptr(flags),
+                                      _lib.ptr(ws), _lib.stream_ptr()))
+        _lib.check(L.ssm_fixed_to_cum(1, P, _lib.ptr(C), _lib.ptr(cum), _lib.stream_ptr()))
+        outs.append(cum.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
+    ref = O.cumulative(w)
+    assert outs[0][-1] == 1.0
+    assert np.max(np.abs(outs[0] - ref)) < 1e-12
+    assert np.all(np.diff(outs[0]) >= 0)
+
+
+def test_gather_kernel():
+    from paper_1306_3277_b200 import _lib
+
+    L = _lib.lib()
+    rs = np.random.default_rng(2)
+    B, nx, P = 3, 8, 5000
+    x = torch.from_numpy(rs.normal(size=(B, nx, P))).cuda()
+    anc = torch.from_numpy(rs.integers(0, P, size=(B, P)).astype(np.int32)).cuda()
+    out = torch.empty_like(x)
+    _lib.check(L.ssm_gather(1, B, nx, P, _lib.ptr(x), _lib.ptr(anc), _lib.ptr(out), _lib.stream_ptr()))
+    ref = torch.gather(x, 2, anc.long().unsqueeze(1).expand(B, nx, P))
+    assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("case", ["normal", "wide", "ties", "with_ninf", "one_dominant"])
+def test_logsumexp_kernel(case):
+    from paper_1306_3277_b200 import _lib
+
+    L = _lib.lib()
+    g = load_golden("lse.npz")
+    a = torch.from_numpy(g[f"{case}/a"]).cuda()
+    P = a.numel()
+    ws = torch.empty(L.ssm_lse_workspace_bytes(1, P), dtype=torch.uint8, device="cuda")
+    out = torch.empty(2, dtype=torch.float64, device="cuda")
+    _lib.check(L.ssm_logsumexp(1, 1, P, _lib.ptr(a), _lib.ptr(out), None, _lib.ptr(ws), _lib.stream_ptr()))
+    ref = float(g[f"{case}/lse"])
+    assert abs(out[0].item() - ref) <= 1e-13 * max(1.0, abs(ref))
+
+
+# ------------------------------------------------------------------ model kernels
+
+
+@pytest.mark.parametrize("c", range(5))
+def test_l96_step_bitwise_f64(c):
+    g = load_golden("l96_step.npz")
+    x = S.step_transition(LORENZ96, g[f"c{c}/theta"], g[f"c{c}/x_in"], None, float(g[f"c{c}/t"]),
+                          float(g[f"c{c}/dt"]), noise=g[f"c{c}/W"])
+    np.testing.assert_array_equal(x, g[f"c{c}/x_out"])
+    gl = S.observe_logpdf(LORENZ96, g[f"c{c}/theta"], x, None, g[f"c{c}/y"], g[f"c{c}/mask"])
+    np.testing.assert_array_equal(gl, g[f"c{c}/g"])
+
+
+@pytest.mark.parametrize("c", range(5))
+def test_l96_step_reference_rng(c):
+    """Same RngStream as the reference -> the reference's x_out, bitwise."""
+    g = load_golden("l96_step.npz")
+    x = S.step_transition(LORENZ96, g[f"c{c}/theta"], g[f"c{c}/x_in"], None, float(g[f"c{c}/t"]),
+                          float(g[f"c{c}/dt"]), RngStream(100 + c))
+    np.testing.assert_array_equal(x, g[f"c{c}/x_out"])
+
+
+@pytest.mark.parametrize("c", range(5))
+def test_l96_step_fast_f64_and_f32(c):
+    g = load_golden("l96_step.npz")
+    args = (LORENZ96, g[f"c{c}/theta"], g[f"c{c}/x_in"], None, float(g[f"c{c}/t"]), float(g[f"c{c}/dt"]))
+    x = S.step_transition(*args, noise=g[f"c{c}/W"], exact=False)
+    assert normwise(x, g[f"c{c}/x_out"]) <= 1e-12
+    x32 = S.step_transition(*args, noise=g[f"c{c}/W"], dtype="float32", exact=False)
+    assert normwise(x32, g[f"c{c}/x_out"]) <= 1e-5
+    g32 = S.observe_logpdf(LORENZ96, g[f"c{c}/theta"], x32, None, g[f"c{c}/y"], g[f"c{c}/mask"], dtype="float32")
+    assert normwise(g32, g[f"c{c}/g"]) <= 1e-5
+
+
+def test_l96_fixed_point():
+    x = S.step_transition(LORENZ96, [10.0, 0.0], np.full((4, 8), 10.0), None, 0.0, 0.05, RngStream(1))
+    np.testing.assert_array_equal(x, 10.0)
+
+
+@pytest.mark.parametrize("c", range(3))
+def test_wk_step_bitwise_f64(c):
+    g = load_golden("wk_step.npz")
+    inputs = LocfInputs(g["in_times"], g["in_values"])
+    t, dt = float(g[f"c{c}/t"]), float(g[f"c{c}/dt"])
+    x = S.step_transition(WINDKESSEL, g[f"c{c}/theta"], g[f"c{c}/x_in"], inputs, t, dt,
+                          noise=g[f"c{c}/xi"][:, None, :])
+    np.testing.assert_array_equal(x, g[f"c{c}/x_out"])
+    x2 = S.step_transition(WINDKESSEL, g[f"c{c}/theta"], g[f"c{c}/x_in"], inputs, t, dt, RngStream(200 + c))
+    np.testing.assert_array_equal(x2, g[f"c{c}/x_out"])
+    gl = S.observe_logpdf(WINDKESSEL, g[f"c{c}/theta"], x, inputs.at(t + dt), g[f"c{c}/y"], [True])
+    np.testing.assert_array_equal(gl, g[f"c{c}/g"])
+
+
+def test_nonfinite_state_error_time():
+    x = np.full((64, 8), 1e200)
+    with pytest.raises(NonFiniteStateError) as e:
+        S.step_transition(LORENZ96, [10.0, 0.1], x, None, 0.3, 0.1, RngStream(3))
+    assert abs(e.value.time - 0.35) < 1e-12
+
+
+# ------------------------------------------------------------------ full filter
+
+
+def _l96_grid(g, prefix="l96"):
+    return build_filter_grid(0.0, 2.0, 20, g["l96/obs_t"], g[f"{prefix}/obs_v"], g[f"{prefix}/obs_m"], n_obs=8)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_pf_l96_host_noise_matches_reference(scheme):
+    g = load_golden("pf.npz")
+    out = particle_filter(LORENZ96, g["l96/theta"], _l96_grid(g), RngStream(7), n_particles=256,
+                          resampler=scheme, noise="host")
+    ref = float(g[f"l96/{scheme}/loglik"])
+    assert abs(out.loglik - ref) <= 1e-12 * abs(ref)
+    np.testing.assert_array_equal(out.run.x, g[f"l96/{scheme}/x_final"])
+    assert normwise(out.run.logw, g[f"l96/{scheme}/logw_final"]) <= 1e-12
+    np.testing.assert_array_equal(out.trajectory, g[f"l96/{scheme}/traj"])
+    anc = np.array([h[1].cpu().numpy() for h in out.run.history[1:] if h[1] is not None])
+    np.testing.assert_array_equal(anc, g[f"l96/{scheme}/anc"][1:])
+
+
+def test_pf_l96_ess_gate_and_sparse_obs():
+    g = load_golden("pf.npz")
+    out = particle_filter(LORENZ96, g["l96/theta"], _l96_grid(g), RngStream(9), n_particles=256,
+                          resampler="systematic", ess_rel=0.5, noise="host")
+    ref = float(g["l96/ess/loglik"])
+    assert abs(out.loglik - ref) <= 1e-12 * abs(ref)
+    np.testing.assert_array_equal(out.trajectory, g["l96/ess/traj"])
+    grid = build_filter_grid(0.0, 2.0, 20, g["l96/obs_t"], g["l96s/obs_v"], g["l96s/obs_m"], n_obs=8)
+    out = particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(8), n_particles=128,
+                          resampler="systematic", noise="host")
+    ref = float(g["l96s/loglik"])
+    assert abs(out.loglik - ref) <= 1e-12 * abs(ref)
+    np.testing.assert_array_equal(out.trajectory, g["l96s/traj"])
+
+
+@pytest.mark.parametrize("scheme", ["multinomial", "systematic"])
+def test_pf_windkessel_host_noise_matches_reference(scheme):
+    g = load_golden("pf.npz")
+    inputs = LocfInputs(g["wk/in_times"], g["wk/in_values"])
+    grid = build_filter_grid(0.0, 1.0, 100, np.linspace(0, 1, 101)[1:], g["wk/obs_v"], np.ones((100, 1), bool),
+                             n_obs=1)
+    out = particle_filter(WINDKESSEL, g["wk/theta"], grid, RngStream(7), inputs=inputs, n_particles=1024,
+                          resampler=scheme, noise="host")
+    ref = float(g[f"wk/{scheme}/loglik"])
+    assert abs(out.loglik - ref) <= 1e-12 * abs(ref)
+    assert normwise(out.trajectory, g[f"wk/{scheme}/traj"]) <= 1e-12
+
+
+def test_pf_f32_host_noise_close():
+    g = load_golden("pf.npz")
+    out = particle_filter(LORENZ96, g["l96/theta"], _l96_grid(g), RngStream(7), n_particles=256,
+                          resampler="systematic", noise="host", dtype="float32", exact=False)
+    ref = float(g["l96/systematic/loglik"])
+    # chaotic model + ancestor flips: statistical agreement, not per-step
+    assert abs(out.loglik - ref) <= 0.05 * abs(ref)
+
+
+def test_pf_windkessel_device_noise_unbiased_vs_kalman():
+    g = load_golden("pf.npz")
+    kf = float(g["wk/kf_loglik"])
+    inputs = LocfInputs(g["wk/in_times"], g["wk/in_values"])
+    grid = build_filter_grid(0.0, 1.0, 100, np.linspace(0, 1, 101)[1:], g["wk/obs_v"], np.ones((100, 1), bool),
+                             n_obs=1)
+    runner = FilterRunner(WINDKESSEL, grid, inputs=inputs, n_particles=4096, resampler="systematic")
+    res = runner.run_batch([g["wk/theta"]] * 64, [None] * 64, [RngStream(1000 + k) for k in range(64)])
+    ll = np.array([r[0] for r in res])
+    se = ll.std(ddof=1) / np.sqrt(len(ll))
+    assert abs(ll.mean() - kf) < 4 * se + 0.02, (ll.mean(), kf, se)
+
+
+def test_batched_equals_single_device_noise():
+    g = load_golden("pf.npz")
+    grid = _l96_grid(g)
+    thetas = [np.array([10.0, 0.1]), np.array([9.0, 0.2]), np.array([11.0, 0.05])]
+    runner = FilterRunner(LORENZ96, grid, n_particles=3000, resampler="systematic")
+    batch = runner.run_batch(thetas, [None] * 3, [RngStream(50 + k) for k in range(3)])
+    for k, th in enumerate(thetas):
+        ll, traj, _ = runner.run(th, None, RngStream(50 + k))
+        assert ll == batch[k][0]
+        np.testing.assert_array_equal(traj, batch[k][1])
+
+
+def test_run_protocol_resume_and_clone():
+    g = load_golden("pf.npz")
+    grid = _l96_grid(g)
+    rng = RngStream(11)
+    a = ParticleRun(LORENZ96, g["l96/theta"], grid, n_particles=2048, resampler="stratified").init(rng.child(0))
+    a.advance_to(7, rng.child(1))
+    b = a.clone()
+    inc_a = a.advance_to(20, rng.child(1))
+    inc_b = b.advance_to(20, rng.child(1))
+    assert inc_a == inc_b and a.loglik == b.loglik and a.pos == b.pos == 20
+    c = ParticleRun(LORENZ96, g["l96/theta"], grid, n_particles=2048, resampler="stratified").init(rng.child(0))
+    c.advance_to(20, rng.child(1))
+    assert c.loglik == a.loglik
+    t = a.sample_trajectory(rng.child(2))
+    assert t.shape == (21, 8)
+    assert 1.0 <= a.ess() <= 2048.0
+
+
+def test_degenerate_ensemble_error():
+    g = load_golden("pf.npz")
+    obs_v = g["l96/obs_v"].copy()
+    obs_v[4] = 1e300
+    grid = build_filter_grid(0.0, 2.0, 20, g["l96/obs_t"], obs_v, g["l96/obs_m"], n_obs=8)
+    with pytest.raises(DegenerateEnsembleError) as e:
+        particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(7), n_particles=512)
+    assert abs(e.value.time - grid.times[5]) < 1e-12

@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const T* __restrict__ noise =
       INJ ? static_cast<const T*>(A.noise) + static_cast<size_t>(b) * A.n_sub * NX * P : nullptr;
   const double* th = A.theta + 4 * b;
-  const uint32_t k0 = INJ ? 0u : A.keys[2 * b], k1 = INJ ? 0u : A.keys[2 * b + 1];
+  const bool have_keys = !INJ && A.keys != nullptr;
+  const uint32_t k0 = have_keys ? A.keys[2 * b] : 0u, k1 = have_keys ? A.keys[2 * b + 1] : 0u;
   const int has_obs = A.has_obs;
   const T logw0 = static_cast<T>(A.log_w0);
   const T obs_log_sd = static_cast<T>(A.obs_log_sd);

@@ -191,9 +191,11 @@ def test_wk_step_bitwise_f64(c):
 
 
 def test_nonfinite_state_error_time():
-    x = np.full((64, 8), 1e200)
+    x = 1e200 * np.random.default_rng(0).normal(size=(64, 8))
+    _, t_fail = O.l96_transition([10.0, 0.1], x, 0.3, 0.1, lambda k, d: np.zeros((64, 8)))
     with pytest.raises(NonFiniteStateError) as e:
         S.step_transition(LORENZ96, [10.0, 0.1], x, None, 0.3, 0.1, RngStream(3))
+    assert e.value.time == t_fail
     assert abs(e.value.time - 0.35) < 1e-12
 
 

@@ -117,7 +117,49 @@ SIGNATURES = {
     "ssm_block_gather": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
 }
 
+# entry points that launch kernels (for the gpu_launches count): name -> launches
+LAUNCHING = {
+    "ssm_propagate_weight": 1,
+    "ssm_init_particles": 1,
+    "ssm_weights_scan": 1,
+    "ssm_fixed_to_cum": 1,
+    "ssm_resample_search": 1,
+    "ssm_gather": 1,
+    "ssm_trace": 1,
+    "ssm_logsumexp": 1,
+    "ssm_block_gather": 1,
+}
+
 _LIB = None
+
+
+class _Lib:
+    """Typed view of the CDLL; kernel-launching calls bump the launch count."""
+
+    def __init__(self, cdll):
+        from . import profiling
+
+        self._cdll = cdll
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(cdll, name)
+            fn.restype = res
+            fn.argtypes = args
+            if name in LAUNCHING:
+                n = LAUNCHING[name]
+
+                def wrapped(*a, _fn=fn, _n=n, _name=name):
+                    if _name == "ssm_weights_scan" and a[4] == 0:
+                        profiling.count_launch(2)  # raw weights: total pre-pass + scan
+                    else:
+                        profiling.count_launch(_n)
+                    return _fn(*a)
+
+                setattr(self, name, wrapped)
+            else:
+                setattr(self, name, fn)
+
+    def __getattr__(self, name):
+        return getattr(self._cdll, name)
 
 
 def load_library(path: str = LIB_PATH):
@@ -130,13 +172,8 @@ def load_library(path: str = LIB_PATH):
             f"{path} is missing: build it with `make` or __graft_entry__.build(); "
             "there is no CPU fallback for the particle-filter path"
         )
-    lib = C.CDLL(path)
-    for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
-        fn.restype = res
-        fn.argtypes = args
-    _LIB = lib
-    return lib
+    _LIB = _Lib(C.CDLL(path))
+    return _LIB
 
 
 def lib():

@@ -33,7 +33,7 @@ import math
 import numpy as np
 import torch
 
-from .. import _lib
+from .. import _lib, profiling
 from ..errors import DegenerateEnsembleError, NonFiniteStateError, UnsupportedModelError
 from ..models import LOG_SQRT_2PI, ModelSpec, resolve_model
 from ..rng import device_key
@@ -386,6 +386,7 @@ def advance_runs(runs, upto, rngs):
     log_w0 = float(-np.log(P))
     obs_log_sd = float(np.log(spec.obs_sd))
     new_hist = [[] for _ in range(B)]
+    esz = 8 if r0.dtype_id == _lib.SSM_F64 else 4
     theta_host = theta.cpu().numpy() if host_noise else None
 
     args = _lib.PwArgs()
@@ -407,8 +408,9 @@ def advance_runs(runs, upto, rngs):
         step_rngs = [g.child(i) for g in rngs] if host_noise else None
         anc = None
         if maybe_nonuniform:
-            _lib.check(L.ssm_weights_scan(B, P, r0.dtype_id, _lib.ptr(a_last), 1, None, _lib.ptr(fs),
-                                          _lib.ptr(cum), None, _lib.ptr(scan_ws), stream), "ssm_weights_scan")
+            with profiling.maybe("scan", B * P * (esz + 8)):
+                _lib.check(L.ssm_weights_scan(B, P, r0.dtype_id, _lib.ptr(a_last), 1, None, _lib.ptr(fs),
+                                              _lib.ptr(cum), None, _lib.ptr(scan_ws), stream), "ssm_weights_scan")
             anc = torch.empty((B, P), dtype=torch.int32, device=dev)
             u_t = None
             if host_noise:
@@ -418,9 +420,10 @@ def advance_runs(runs, upto, rngs):
                 else:
                     u = np.stack([g.uniform(size=P) for g in rr])
                 u_t = torch.from_numpy(u).to(dev)
-            _lib.check(L.ssm_resample_search(B, P, P, scheme, 1, _lib.ptr(cum), _lib.ptr(u_t),
-                                             _lib.ptr(keys_t), i, _lib.ptr(fs), _lib.ptr(anc), stream),
-                       "ssm_resample_search")
+            with profiling.maybe("search", B * P * (8 + 4)):
+                _lib.check(L.ssm_resample_search(B, P, P, scheme, 1, _lib.ptr(cum), _lib.ptr(u_t),
+                                                 _lib.ptr(keys_t), i, _lib.ptr(fs), _lib.ptr(anc), stream),
+                           "ssm_resample_search")
         n_sub = sched.n_sub[i]
         x_out = torch.empty((B, spec.nx, P), dtype=tdt, device=dev)
         noise_t = None
@@ -448,7 +451,12 @@ def advance_runs(runs, upto, rngs):
         else:
             args.has_obs = 0
             args.obs_mask = 0
-        _lib.check(L.ssm_propagate_weight(args, stream), "ssm_propagate_weight")
+        # algorithmic bytes: (anc) + gather read + write of x + (read a_prev) + write a
+        nbytes = B * P * (2 * spec.nx * esz + (4 if anc is not None else 0)
+                          + (esz if obs is not None else 0)
+                          + (esz if (a_last is not None and obs is not None and r0.ess_rel is not None) else 0))
+        with profiling.maybe("propagate_weight", nbytes):
+            _lib.check(L.ssm_propagate_weight(args, stream), "ssm_propagate_weight")
         for b in range(B):
             new_hist[b].append((x_out[b], anc[b] if anc is not None else None))
         x_prev = x_out

@@ -1,0 +1,76 @@
+"""Per-kernel CUDA-event timing and launch counting for the filter path.
+
+`KernelTimer` records a (start, end) event pair on the launching stream
+around every C-ABI kernel launch while active; nothing synchronises until
+`summary()`.  `launch_count()` counts libssm_b200 kernel launches (a wrapper
+in `_lib` increments it), which bench.py reports as `gpu_launches`.
+"""
+
+from __future__ import annotations
+
+import contextlib
+from collections import defaultdict
+
+import torch
+
+_ACTIVE = None
+_LAUNCHES = 0
+
+
+def count_launch(n=1):
+    global _LAUNCHES
+    _LAUNCHES += n
+
+
+def launch_count():
+    return _LAUNCHES
+
+
+class KernelTimer:
+    def __init__(self):
+        self.events = defaultdict(list)  # name -> [(start, end, bytes)]
+
+    @contextlib.contextmanager
+    def kernel(self, name, nbytes=0):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        try:
+            yield
+        finally:
+            e.record()
+            self.events[name].append((s, e, nbytes))
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for name, lst in self.events.items():
+            ms = [s.elapsed_time(e) for s, e, _ in lst]
+            nb = sum(b for _, _, b in lst)
+            out[name] = {"launches": len(lst), "total_ms": float(sum(ms)),
+                         "avg_ms": float(sum(ms) / len(ms)), "bytes": int(nb)}
+        return out
+
+
+def active():
+    return _ACTIVE
+
+
+@contextlib.contextmanager
+def timing(timer: KernelTimer):
+    global _ACTIVE
+    prev, _ACTIVE = _ACTIVE, timer
+    try:
+        yield timer
+    finally:
+        _ACTIVE = prev
+
+
+@contextlib.contextmanager
+def maybe(name, nbytes=0):
+    t = _ACTIVE
+    if t is None:
+        yield
+    else:
+        with t.kernel(name, nbytes):
+            yield

@@ -158,17 +158,32 @@ int ssm_weights_scan(int B, int P, int dtype, const void* a, int is_log, const d
 int ssm_fixed_to_cum(int B, int P, const uint64_t* C, double* cum, void* stream);
 
 /* K5: ancestor search, searchsorted(cum, u, 'right').clip(0, P-1)
- * (resampling.py:28-36).  Systematic/stratified use a merge path over the
- * sorted queries; multinomial a per-query binary search (query order kept).
+ * (resampling.py:28-36), exact in float64 on the reference's query values.
+ *   systematic / stratified (sorted queries): per-particle offspring bounds
+ *     c_j = #{k : u_k < cum_j} plus the merge-path partition they imply, then
+ *     a search-free expand (anc_k = #{j : c_j <= k});
+ *   multinomial: per-query binary search (query order kept).
  *   cum_kind 0: cum is float64 [B][P_in] (injected CDF, exact parity mode)
  *   cum_kind 1: cum is the uint64 fixed-point output of ssm_weights_scan
  * Queries: u != NULL -> injected uniforms, [B][P_out] (multinomial,
  * stratified) or [B][1] (systematic), exactly the draws resampling.py:28-33
  * consumes; u == NULL -> drawn on the device from keys[b] at counter `step`.
- * fs (nullable): filters with fs[b].resample_now == 0 get identity ancestors. */
+ * fs (nullable): filters with fs[b].resample_now == 0 get identity ancestors.
+ * workspace: ssm_search_workspace_bytes(B, P_in, P_out) (unused for multinomial). */
+size_t ssm_search_workspace_bytes(int B, int P_in, int P_out);
 int ssm_resample_search(int B, int P_in, int P_out, int scheme, int cum_kind, const void* cum,
                         const double* u, const uint32_t* keys, int step,
-                        const ssm_filter_state* fs, int32_t* anc, void* stream);
+                        const ssm_filter_state* fs, int32_t* anc, void* workspace, void* stream);
+
+/* K4+K5 for the filter (particle.py:96-105): ancestors straight from the
+ * unnormalised log-weights a (w = exp(a - shift[b]), shift NULL -> fs[b].incr).
+ * systematic / stratified: exact fixed-point reduce-then-scan (tile sums ->
+ * tile prefix -> offspring bounds + partition) -> expand, 4 launches, no
+ * look-back and no searches; multinomial: look-back scan + binary search. */
+size_t ssm_resample_workspace_bytes(int B, int P);
+int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const void* a, const double* shift,
+                           const ssm_filter_state* fs, const double* u, const uint32_t* keys,
+                           int step, int32_t* anc, void* workspace, void* stream);
 
 /* K6: ancestor gather x_out[b][s][k] = x_in[b][s][anc[b][k]] (particle.py:102). */
 int ssm_gather(int dtype, int B, int nx, int P, const void* x_in, const int32_t* anc,

@@ -109,7 +109,10 @@ SIGNATURES = {
     "ssm_scan_workspace_bytes": (_sz, [_i, _i]),
     "ssm_weights_scan": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ssm_fixed_to_cum": (_i, [_i, _i, _vp, _vp, _vp]),
-    "ssm_resample_search": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
+    "ssm_search_workspace_bytes": (_sz, [_i, _i, _i]),
+    "ssm_resample_search": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
+    "ssm_resample_workspace_bytes": (_sz, [_i, _i]),
+    "ssm_resample_from_logw": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ssm_gather": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "ssm_trace": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_lse_workspace_bytes": (_sz, [_i, _i]),
@@ -124,6 +127,7 @@ LAUNCHING = {
     "ssm_weights_scan": 1,
     "ssm_fixed_to_cum": 1,
     "ssm_resample_search": 1,
+    "ssm_resample_from_logw": 4,
     "ssm_gather": 1,
     "ssm_trace": 1,
     "ssm_logsumexp": 1,
@@ -150,6 +154,10 @@ class _Lib:
                 def wrapped(*a, _fn=fn, _n=n, _name=name):
                     if _name == "ssm_weights_scan" and a[4] == 0:
                         profiling.count_launch(2)  # raw weights: total pre-pass + scan
+                    elif _name == "ssm_resample_search" and a[3] != 0:
+                        profiling.count_launch(2)  # offspring + expand
+                    elif _name == "ssm_resample_from_logw" and a[3] == 0:
+                        profiling.count_launch(2)  # look-back scan + binary search
                     else:
                         profiling.count_launch(_n)
                     return _fn(*a)

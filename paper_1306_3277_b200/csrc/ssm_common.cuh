@@ -62,9 +62,10 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, uint32_t c, u
   z1 = r * s;
 }
 
-// Box-Muller pair, float32
+// Box-Muller pair, float32 (the device noise generator for both precisions:
+// u1 = (a + 1/2) 2^-32 keeps 32 bits near 0, so |z| reaches 6.7 sigma)
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
-  const float u1 = 1.0f - static_cast<float>(a >> 8) * 0x1.0p-24f;  // (0, 1]
+  const float u1 = fmaf(static_cast<float>(a), 0x1.0p-32f, 0x1.0p-33f);  // (0, 1]
   const float u2 = static_cast<float>(b >> 8) * 0x1.0p-24f;
   const float r = sqrtf(-2.0f * logf(u1));
   float s, co;

@@ -24,28 +24,23 @@ __host__ __device__ inline int pw_grid_x(int P) {
 
 // ----------------------------- noise ---------------------------------------
 
+// Eight standard normals per particle and sub-step: two Philox4x32-10 blocks,
+// float32 Box-Muller (MUFU-backed logf/sincospif), widened to T.  Keeping the
+// transcendental work off the FP64 pipe is what lets the float64 filter stay
+// memory-bound (profiles/r1_baseline_ncu.md).
 template <typename T>
 __device__ __forceinline__ void normals8(uint32_t k0, uint32_t k1, uint32_t p, uint32_t step,
-                                         uint32_t sub, T z[8]);
-
-template <>
-__device__ __forceinline__ void normals8<double>(uint32_t k0, uint32_t k1, uint32_t p,
-                                                 uint32_t step, uint32_t sub, double z[8]) {
-#pragma unroll
-  for (uint32_t g = 0; g < 4; ++g) {
-    const U4 r = philox4x32_10(U4{p, step, (sub << 8) | g, kPurposeNoise}, k0, k1);
-    box_muller(r.x, r.y, r.z, r.w, z[2 * g], z[2 * g + 1]);
-  }
-}
-
-template <>
-__device__ __forceinline__ void normals8<float>(uint32_t k0, uint32_t k1, uint32_t p,
-                                                uint32_t step, uint32_t sub, float z[8]) {
+                                         uint32_t sub, T z[8]) {
 #pragma unroll
   for (uint32_t g = 0; g < 2; ++g) {
     const U4 r = philox4x32_10(U4{p, step, (sub << 8) | g, kPurposeNoise}, k0, k1);
-    box_muller(r.x, r.y, z[4 * g], z[4 * g + 1]);
-    box_muller(r.z, r.w, z[4 * g + 2], z[4 * g + 3]);
+    float a, b, c, d;
+    box_muller(r.x, r.y, a, b);
+    box_muller(r.z, r.w, c, d);
+    z[4 * g] = static_cast<T>(a);
+    z[4 * g + 1] = static_cast<T>(b);
+    z[4 * g + 2] = static_cast<T>(c);
+    z[4 * g + 3] = static_cast<T>(d);
   }
 }
 
@@ -53,13 +48,9 @@ template <typename T>
 __device__ __forceinline__ T normal1(uint32_t k0, uint32_t k1, uint32_t p, uint32_t step,
                                      uint32_t sub) {
   const U4 r = philox4x32_10(U4{p, step, sub << 8, kPurposeNoise}, k0, k1);
-  T z0, z1;
-  if constexpr (sizeof(T) == 8) {
-    box_muller(r.x, r.y, r.z, r.w, z0, z1);
-  } else {
-    box_muller(r.x, r.y, z0, z1);
-  }
-  return z0;
+  float z0, z1;
+  box_muller(r.x, r.y, z0, z1);
+  return static_cast<T>(z0);
 }
 
 // ----------------------------- Lorenz '96 ----------------------------------
@@ -168,7 +159,8 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
           for (int n = 0; n < 8; ++n) W[n] = sd * W[n];
         }
 #pragma unroll
-        for (int n = 0; n < 8; ++n) nt[n] = O::div(O::mul(sq, W[n]), T(0.05));
+        for (int n = 0; n < 8; ++n)
+          nt[n] = E ? O::div(O::mul(sq, W[n]), T(0.05)) : O::mul(O::mul(sq, W[n]), T(20.0));
         for (int m = 0; m < S.n_ode; ++m) l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
       } else {
         // Windkessel.bi:28-29, Pp <- exp(-h/(R*C))*Pp + R*(1 - exp(-h/(R*C)))*(F + xi)
@@ -202,13 +194,13 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
 #pragma unroll
         for (int n = 0; n < 8; ++n) {
           if (A.obs_mask & (1u << n)) {
-            const T z = O::div(O::sub(static_cast<T>(A.y[n]), x[n]), T(0.5));
+            const T z = O::mul(O::sub(static_cast<T>(A.y[n]), x[n]), T(2.0));  // exact: / 0.5
             g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
           }
         }
       } else {
         const T mean = O::add(x[0], O::mul(static_cast<T>(th[2]), static_cast<T>(A.u_obs)));
-        const T z = O::div(O::sub(static_cast<T>(A.y[0]), mean), T(2.0));
+        const T z = O::mul(O::sub(static_cast<T>(A.y[0]), mean), T(0.5));  // exact: / 2.0
         g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
       }
       const T lw = uniform_in ? logw0 : O::sub(aprev[p], static_cast<T>(incr_prev));

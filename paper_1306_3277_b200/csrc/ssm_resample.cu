@@ -280,76 +280,280 @@ __device__ __forceinline__ double query(int k, int P_out, double u_sys, const do
 }
 
 constexpr int kMergeItems = 8;
-constexpr int kMergeTile = kThreads * kMergeItems;  // merged-diagonal elements per block
 
-// merge-path split: number of cum elements among the first d merged elements
-// (cum_j precedes u_k iff cum_j <= u_k)
-template <typename FA, typename FB>
-__device__ __forceinline__ int merge_split(int d, int na, int nb, FA A, FB Bq) {
-  int lo = d > nb ? d - nb : 0;
-  int hi = d < na ? d : na;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (A(mid) <= Bq(d - 1 - mid))
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
+// ---------------------------------------------------------------------------
+// Systematic / stratified: offspring boundaries + merge-path partition.
+//
+// The queries are sorted, so output k descends from particle j iff
+//   c_{j-1} <= k < c_j,   c_j = #{k : u_k < cum_j}   (searchsorted 'right').
+// c_j is computed exactly per particle (an estimate from cum_j * P, then the
+// reference's own predicate on the exact float64 query values), so no
+// binary search over the CDF is needed.  On the merge path of (c, outputs)
+// particle j sits at diagonal j + c_j; the kernel that computes c_j also
+// writes, for every diagonal tile boundary D it owns, split[D / kDiag] = j,
+// which is the partition the expand kernel needs (no per-block searches).
+// ---------------------------------------------------------------------------
+
+constexpr int kDiag = 2048;  // merged-diagonal elements per expand block
+
+enum CumSrc { kCumDouble = 0, kCumFixed = 1, kCumLogw = 2 };
+
+__device__ __forceinline__ double sys_query(int k, double u, int P_out, double invP, bool pow2) {
+  const double num = static_cast<double>(k) + u;
+  return pow2 ? num * invP : num / static_cast<double>(P_out);  // exact scaling when P is 2^n
 }
 
-template <int SCHEME, int KIND>
+// c = #{k in [0, P_out) : u_k < cum}, u_k non-decreasing
+template <int SCHEME>
+__device__ __forceinline__ int offspring_bound(double cum, double u_sys, const double* U, uint32_t k0,
+                                               uint32_t k1, int step, int P_out, double invP,
+                                               bool pow2) {
+  auto f = [&](int k) -> double {
+    if constexpr (SCHEME == SSM_SYSTEMATIC) {
+      return sys_query(k, u_sys, P_out, invP, pow2);
+    } else {
+      const double Uk = U ? U[k] : device_uniform(k0, k1, static_cast<uint32_t>(k), step, kPurposeResample);
+      return sys_query(k, Uk, P_out, invP, pow2);
+    }
+  };
+  if (!(cum > 0.0)) return 0;  // u_k >= 0
+  double est = SCHEME == SSM_SYSTEMATIC ? ceil(cum * P_out - u_sys) : floor(cum * P_out);
+  est = est < 0.0 ? 0.0 : (est > P_out ? static_cast<double>(P_out) : est);
+  int k = static_cast<int>(est);
+  while (k > 0 && f(k - 1) >= cum) --k;
+  while (k < P_out && f(k) < cum) ++k;
+  return k;
+}
+
+// per-tile fixed-point sums of q_j = round(exp(a_j - shift) * 2^61)
+template <typename T>
 __global__ void __launch_bounds__(kThreads)
-merge_search_kernel(int P_in, int P_out, const void* __restrict__ cum, const double* __restrict__ u,
-                    const uint32_t* __restrict__ keys, int step,
-                    const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc) {
-  __shared__ double sA[kMergeTile];
-  __shared__ double sB[kMergeTile];
-  __shared__ int32_t sOut[kMergeTile];
-  __shared__ int s_split[2];
-  const int b = blockIdx.y;
-  int32_t* ancb = anc + static_cast<size_t>(b) * P_out;
-  const int total = P_in + P_out;
-  const int d0 = blockIdx.x * kMergeTile;
-  if (d0 >= total) return;
-  const int d1 = min(d0 + kMergeTile, total);
-  if (fs && !fs[b].resample_now) {
-    // identity ancestors (ESS gate held, particle.py:99-100)
-    const int k0 = d0 >> 1, k1 = min(d1 >> 1, P_out);
-    for (int k = k0 + threadIdx.x; k < k1; k += kThreads) ancb[k] = k;
-    if (blockIdx.x == gridDim.x - 1)
-      for (int k = k1 + threadIdx.x; k < P_out; k += kThreads) ancb[k] = k;
-    return;
+tile_sums_kernel(int P, const T* __restrict__ a, const double* __restrict__ shift,
+                 const ssm_filter_state* __restrict__ fs, uint64_t* __restrict__ sums) {
+  const int b = blockIdx.y, tile = blockIdx.x;
+  if (fs && !fs[b].resample_now) return;
+  const double sh = shift ? shift[b] : fs[b].incr;
+  const T* ab = a + static_cast<size_t>(b) * P + static_cast<size_t>(tile) * kScanTile;
+  const int n = min(kScanTile, P - tile * kScanTile);
+  uint64_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int e = i * kThreads + threadIdx.x;
+    if (e < n) {
+      const double w = exp(static_cast<double>(ab[e]) - sh);
+      acc += (w >= 0.0 && w <= 4.0) ? __double2ull_rn(w * kFix) : 0ull;
+    }
   }
-  const size_t coff = static_cast<size_t>(b) * P_in;
-  const double tot = cum_total<KIND>(cum, coff, P_in);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  __shared__ uint64_t red[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+    sums[static_cast<size_t>(b) * gridDim.x + tile] = t;
+  }
+}
+
+// exclusive prefix of the tile sums, one 1024-thread block per filter
+__global__ void __launch_bounds__(1024)
+tile_prefix_kernel(int tiles, uint64_t* __restrict__ sums, uint64_t* __restrict__ totals,
+                   const ssm_filter_state* __restrict__ fs) {
+  const int b = blockIdx.x;
+  if (fs && !fs[b].resample_now) return;
+  uint64_t* sb = sums + static_cast<size_t>(b) * tiles;
+  const int per = (tiles + 1023) / 1024;
+  const int t0 = threadIdx.x * per;
+  uint64_t local = 0;
+  for (int t = t0; t < min(t0 + per, tiles); ++t) local += sb[t];
+  __shared__ uint64_t wsum[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  uint64_t wex = 0, tot = 0;
+  for (int w = 0; w < 32; ++w) {
+    if (w < warp) wex += wsum[w];
+    tot += wsum[w];
+  }
+  uint64_t run = wex + incl - local;
+  for (int t = t0; t < min(t0 + per, tiles); ++t) {
+    const uint64_t v = sb[t];
+    sb[t] = run;
+    run += v;
+  }
+  if (threadIdx.x == 0) totals[b] = tot;
+}
+
+// c_j for every particle + merge-path partition entries
+template <int SCHEME, int SRC, typename T>
+__global__ void __launch_bounds__(kThreads)
+offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double* __restrict__ shift,
+                 const uint64_t* __restrict__ tile_prefix, const uint64_t* __restrict__ totals,
+                 const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
+                 const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ cnt,
+                 int32_t* __restrict__ split, int ndiag) {
+  __shared__ uint64_t sm[kScanTile + kScanTile / 8];
+  __shared__ uint64_t warp_tot[kThreads / 32];
+  const int b = blockIdx.y, tile = blockIdx.x;
+  if (fs && !fs[b].resample_now) return;
+  const int tiles = gridDim.x;
+  const int j0 = tile * kScanTile;
+  const int n = min(kScanTile, P_in - j0);
+  const bool pow2 = (P_out & (P_out - 1)) == 0;
+  const double invP = 1.0 / static_cast<double>(P_out);
+  const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
   const double u_sys =
       SCHEME == SSM_SYSTEMATIC
-          ? (u ? u[b] : device_uniform(keys[2 * b], keys[2 * b + 1], 0u, step, kPurposeSystematic))
+          ? (u ? u[b] : device_uniform(k0, k1, 0u, step, kPurposeSystematic))
           : 0.0;
-  const double* ub = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * P_out : nullptr;
-  const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
-  auto A = [&](int j) { return cum_at<KIND>(cum, coff, tot, j); };
-  auto Bq = [&](int k) { return query<SCHEME>(k, P_out, u_sys, ub, k0, k1, step); };
-  if (threadIdx.x < 2) {
-    const int d = threadIdx.x == 0 ? d0 : d1;
-    s_split[threadIdx.x] = merge_split(d, P_in, P_out, A, Bq);
+  const double* U = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * P_out : nullptr;
+  int32_t* cb = cnt + static_cast<size_t>(b) * P_in;
+  int32_t* sp = split + static_cast<size_t>(b) * (ndiag + 1);
+
+  // cum_j for the thread's kScanItems consecutive particles, and cum_{j-1}
+  double cum[kScanItems];
+  double cum_prev;
+  const int jt = j0 + threadIdx.x * kScanItems;
+  if constexpr (SRC == kCumDouble) {
+    const double* cd = static_cast<const double*>(src) + static_cast<size_t>(b) * P_in;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) cum[i] = jt + i < P_in ? cd[jt + i] : 2.0;
+    cum_prev = jt > 0 ? cd[jt - 1] : 0.0;
+  } else {
+    const size_t off = static_cast<size_t>(b) * P_in + j0;
+    double sh = 0.0;
+    if constexpr (SRC == kCumLogw) sh = shift ? shift[b] : fs[b].incr;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      const int e = i * kThreads + threadIdx.x;
+      uint64_t q = 0;
+      if (e < n) {
+        if constexpr (SRC == kCumLogw) {
+          const double w = exp(static_cast<double>(static_cast<const T*>(src)[off + e]) - sh);
+          q = (w >= 0.0 && w <= 4.0) ? __double2ull_rn(w * kFix) : 0ull;
+        } else {
+          q = static_cast<const uint64_t*>(src)[off + e];  // inclusive C_j already
+        }
+      }
+      sm[e + (e >> 3)] = q;
+    }
+    __syncthreads();
+    double tot;
+    uint64_t Cv[kScanItems];
+    uint64_t Cprev;
+    if constexpr (SRC == kCumLogw) {
+      uint64_t run = 0;
+#pragma unroll
+      for (int i = 0; i < kScanItems; ++i) {
+        const int e = threadIdx.x * kScanItems + i;
+        run += sm[e + (e >> 3)];
+        Cv[i] = run;
+      }
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      uint64_t incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) warp_tot[warp] = incl;
+      __syncthreads();
+      uint64_t wex = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w)
+        if (w < warp) wex += warp_tot[w];
+      const uint64_t base = tile_prefix[static_cast<size_t>(b) * tiles + tile] + wex + incl - run;
+#pragma unroll
+      for (int i = 0; i < kScanItems; ++i) Cv[i] += base;
+      Cprev = base;
+      tot = static_cast<double>(totals[b]);
+    } else {
+      const uint64_t* Cb = static_cast<const uint64_t*>(src) + static_cast<size_t>(b) * P_in;
+#pragma unroll
+      for (int i = 0; i < kScanItems; ++i) {
+        const int e = threadIdx.x * kScanItems + i;
+        Cv[i] = sm[e + (e >> 3)];
+      }
+      Cprev = jt > 0 ? Cb[jt - 1] : 0ull;
+      tot = static_cast<double>(Cb[P_in - 1]);
+    }
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i)
+      cum[i] = jt + i < P_in ? static_cast<double>(Cv[i]) / tot : 2.0;
+    cum_prev = jt > 0 ? static_cast<double>(Cprev) / tot : 0.0;
   }
-  __syncthreads();
-  const int i0 = s_split[0], i1 = s_split[1];
-  const int kb0 = d0 - i0, kb1 = d1 - i1;
+
+  if (jt >= P_in) return;
+  int c_prev = jt > 0 ? offspring_bound<SCHEME>(cum_prev, u_sys, U, k0, k1, step, P_out, invP, pow2) : 0;
+  const int total = P_in + P_out;
+  int32_t cvals[kScanItems];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int j = jt + i;
+    if (j >= P_in) break;
+    const int c = offspring_bound<SCHEME>(cum[i], u_sys, U, k0, k1, step, P_out, invP, pow2);
+    cvals[i] = c;
+    // diagonal boundaries D in (j-1 + c_prev, j + c] are split at particle j
+    const int lo = j - 1 + c_prev, hi = j + c;
+    for (int t = lo / kDiag + 1; t * kDiag <= hi && t <= ndiag; ++t) sp[t] = j;
+    if (j == P_in - 1) {
+      for (int t = hi / kDiag + 1; t <= ndiag; ++t) sp[t] = P_in;  // tail outputs, and D = total
+    }
+    if (j == 0) sp[0] = 0;
+    c_prev = c;
+  }
+  (void)total;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (jt + i < P_in) cb[jt + i] = cvals[i];
+}
+
+// anc_k = #{j : c_j <= k}, clipped to P_in - 1, from the precomputed partition
+__global__ void __launch_bounds__(kThreads)
+expand_kernel(int P_in, int P_out, const int32_t* __restrict__ cnt, const int32_t* __restrict__ split,
+              int ndiag, const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc) {
+  __shared__ int32_t sA[kDiag];
+  __shared__ int32_t sOut[kDiag];
+  const int b = blockIdx.y, t = blockIdx.x;
+  int32_t* ab = anc + static_cast<size_t>(b) * P_out;
+  const int total = P_in + P_out;
+  const int D0 = t * kDiag, D1 = min(D0 + kDiag, total);
+  if (fs && !fs[b].resample_now) {
+    // identity ancestors (ESS gate held, particle.py:99-100); block t covers outputs [D0/2, D1/2)
+    const int ka = D0 >> 1, kb = t == ndiag - 1 ? P_out : min(D1 >> 1, P_out);
+    for (int k = ka + threadIdx.x; k < kb; k += kThreads) ab[k] = k;
+    return;
+  }
+  const int32_t* sp = split + static_cast<size_t>(b) * (ndiag + 1);
+  const int32_t* cb = cnt + static_cast<size_t>(b) * P_in;
+  const int i0 = sp[t], i1 = sp[t + 1];
+  const int kb0 = D0 - i0, kb1 = D1 - i1;
   const int na = i1 - i0, nb = kb1 - kb0;
-  for (int t = threadIdx.x; t < na; t += kThreads) sA[t] = A(i0 + t);
-  for (int t = threadIdx.x; t < nb; t += kThreads) sB[t] = Bq(kb0 + t);
+  for (int q = threadIdx.x; q < na; q += kThreads) sA[q] = cb[i0 + q];
   __syncthreads();
-  // per-thread merge of kMergeItems diagonal elements
   const int dl = threadIdx.x * kMergeItems;
   if (dl < na + nb) {
-    int ia = merge_split(dl, na, nb, [&](int j) { return sA[j]; }, [&](int k) { return sB[k]; });
-    int kb = dl - ia;
+    // thread split: particles among the first dl merged elements (c_j <= k precedes output k)
+    int lo = dl > nb ? dl - nb : 0, hi = dl < na ? dl : na;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sA[mid] <= kb0 + (dl - 1 - mid))
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    int ia = lo, kb = dl - lo;
     const int lim = min(dl + kMergeItems, na + nb);
     for (int e = dl; e < lim; ++e) {
-      if (ia < na && (kb >= nb || sA[ia] <= sB[kb])) {
+      if (ia < na && (kb >= nb || sA[ia] <= kb0 + kb)) {
         ++ia;
       } else {
         const int a_idx = i0 + ia;
@@ -359,7 +563,7 @@ merge_search_kernel(int P_in, int P_out, const void* __restrict__ cum, const dou
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < nb; t += kThreads) ancb[kb0 + t] = sOut[t];
+  for (int q = threadIdx.x; q < nb; q += kThreads) ab[kb0 + q] = sOut[q];
 }
 
 template <int KIND>
@@ -556,9 +760,68 @@ extern "C" int ssm_fixed_to_cum(int B, int P, const uint64_t* C, double* cum, vo
   return SSM_OK;
 }
 
+// workspace: [tile sums B*tiles u64][totals B u64][cnt B*P_in i32][split B*(ndiag+1) i32]
+//            [+ look-back scan workspace for multinomial from log-weights]
+static inline int ndiag_of(int P_in, int P_out) {
+  return static_cast<int>((static_cast<long long>(P_in) + P_out + kDiag - 1) / kDiag);
+}
+
+struct SearchWs {
+  uint64_t* sums;
+  uint64_t* totals;
+  int32_t* cnt;
+  int32_t* split;
+  void* scan;
+  uint64_t* C;
+};
+
+static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, SearchWs* w) {
+  const int tiles = scan_tiles(P_in);
+  const int nd = ndiag_of(P_in, P_out);
+  size_t off = 0;
+  char* p = static_cast<char*>(base);
+  auto take = [&](size_t bytes) {
+    char* r = p ? p + off : nullptr;
+    off += align256(bytes);
+    return r;
+  };
+  SearchWs tmp;
+  tmp.sums = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * tiles));
+  tmp.totals = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * B));
+  tmp.cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * P_in));
+  tmp.split = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * (nd + 1)));
+  tmp.C = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * P_in));
+  tmp.scan = take(scan_ws_bytes(B, P_in));
+  if (w) *w = tmp;
+  return off;
+}
+
+template <int SRC, typename T>
+static void launch_offspring_expand(int scheme, int B, int P_in, int P_out, const void* src,
+                                    const double* shift, const SearchWs& w, const double* u,
+                                    const uint32_t* keys, int step, const ssm_filter_state* fs,
+                                    int32_t* anc, cudaStream_t s) {
+  const int tiles = scan_tiles(P_in);
+  const int nd = ndiag_of(P_in, P_out);
+  const dim3 g(tiles, B);
+  if (scheme == SSM_SYSTEMATIC)
+    offspring_kernel<SSM_SYSTEMATIC, SRC, T><<<g, kThreads, 0, s>>>(
+        P_in, P_out, src, shift, w.sums, w.totals, u, keys, step, fs, w.cnt, w.split, nd);
+  else
+    offspring_kernel<SSM_STRATIFIED, SRC, T><<<g, kThreads, 0, s>>>(
+        P_in, P_out, src, shift, w.sums, w.totals, u, keys, step, fs, w.cnt, w.split, nd);
+  expand_kernel<<<dim3(nd, B), kThreads, 0, s>>>(P_in, P_out, w.cnt, w.split, nd, fs, anc);
+}
+
+extern "C" size_t ssm_search_workspace_bytes(int B, int P_in, int P_out) {
+  if (B <= 0 || P_in <= 0 || P_out <= 0) return 0;
+  return search_ws_layout(B, P_in, P_out, nullptr, nullptr);
+}
+
 extern "C" int ssm_resample_search(int B, int P_in, int P_out, int scheme, int cum_kind,
                                    const void* cum, const double* u, const uint32_t* keys, int step,
-                                   const ssm_filter_state* fs, int32_t* anc, void* stream) {
+                                   const ssm_filter_state* fs, int32_t* anc, void* workspace,
+                                   void* stream) {
   if (B <= 0 || B > 65535 || P_in <= 0 || P_out <= 0 || !cum || !anc) return SSM_ERR_INVALID_ARG;
   if (!u && !keys) return SSM_ERR_INVALID_ARG;
   if (fs && P_in != P_out) return SSM_ERR_INVALID_ARG;
@@ -571,18 +834,52 @@ extern "C" int ssm_resample_search(int B, int P_in, int P_out, int scheme, int c
     else
       binary_search_kernel<1><<<g, kThreads, 0, s>>>(P_in, P_out, cum, u, keys, step, fs, anc);
   } else if (scheme == SSM_STRATIFIED || scheme == SSM_SYSTEMATIC) {
-    const long long total = static_cast<long long>(P_in) + P_out;
-    const dim3 g(static_cast<unsigned>((total + kMergeTile - 1) / kMergeTile), B);
-    if (scheme == SSM_STRATIFIED) {
-      if (cum_kind == 0)
-        merge_search_kernel<SSM_STRATIFIED, 0><<<g, kThreads, 0, s>>>(P_in, P_out, cum, u, keys, step, fs, anc);
-      else
-        merge_search_kernel<SSM_STRATIFIED, 1><<<g, kThreads, 0, s>>>(P_in, P_out, cum, u, keys, step, fs, anc);
+    if (!workspace) return SSM_ERR_INVALID_ARG;
+    SearchWs w;
+    search_ws_layout(B, P_in, P_out, workspace, &w);
+    if (cum_kind == 0)
+      launch_offspring_expand<kCumDouble, double>(scheme, B, P_in, P_out, cum, nullptr, w, u, keys,
+                                                  step, fs, anc, s);
+    else
+      launch_offspring_expand<kCumFixed, double>(scheme, B, P_in, P_out, cum, nullptr, w, u, keys,
+                                                 step, fs, anc, s);
+  } else {
+    return SSM_ERR_INVALID_ARG;
+  }
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+extern "C" size_t ssm_resample_workspace_bytes(int B, int P) {
+  return ssm_search_workspace_bytes(B, P, P);
+}
+
+extern "C" int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const void* a,
+                                      const double* shift, const ssm_filter_state* fs,
+                                      const double* u, const uint32_t* keys, int step, int32_t* anc,
+                                      void* workspace, void* stream) {
+  if (B <= 0 || B > 65535 || P <= 0 || !a || !anc || !workspace) return SSM_ERR_INVALID_ARG;
+  if (!shift && !fs) return SSM_ERR_INVALID_ARG;
+  if (!u && !keys) return SSM_ERR_INVALID_ARG;
+  if (dtype != SSM_F64 && dtype != SSM_F32) return SSM_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SearchWs w;
+  search_ws_layout(B, P, P, workspace, &w);
+  const int tiles = scan_tiles(P);
+  if (scheme == SSM_MULTINOMIAL) {
+    int st = ssm_weights_scan(B, P, dtype, a, 1, shift, fs, w.C, nullptr, w.scan, stream);
+    if (st != SSM_OK) return st;
+    const dim3 g(grid_for(P, kThreads, 65535), B);
+    binary_search_kernel<1><<<g, kThreads, 0, s>>>(P, P, w.C, u, keys, step, fs, anc);
+  } else if (scheme == SSM_SYSTEMATIC || scheme == SSM_STRATIFIED) {
+    if (dtype == SSM_F64) {
+      tile_sums_kernel<double><<<dim3(tiles, B), kThreads, 0, s>>>(P, static_cast<const double*>(a), shift, fs, w.sums);
+      tile_prefix_kernel<<<B, 1024, 0, s>>>(tiles, w.sums, w.totals, fs);
+      launch_offspring_expand<kCumLogw, double>(scheme, B, P, P, a, shift, w, u, keys, step, fs, anc, s);
     } else {
-      if (cum_kind == 0)
-        merge_search_kernel<SSM_SYSTEMATIC, 0><<<g, kThreads, 0, s>>>(P_in, P_out, cum, u, keys, step, fs, anc);
-      else
-        merge_search_kernel<SSM_SYSTEMATIC, 1><<<g, kThreads, 0, s>>>(P_in, P_out, cum, u, keys, step, fs, anc);
+      tile_sums_kernel<float><<<dim3(tiles, B), kThreads, 0, s>>>(P, static_cast<const float*>(a), shift, fs, w.sums);
+      tile_prefix_kernel<<<B, 1024, 0, s>>>(tiles, w.sums, w.totals, fs);
+      launch_offspring_expand<kCumLogw, float>(scheme, B, P, P, a, shift, w, u, keys, step, fs, anc, s);
     }
   } else {
     return SSM_ERR_INVALID_ARG;

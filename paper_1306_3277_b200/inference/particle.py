@@ -380,8 +380,7 @@ def advance_runs(runs, upto, rngs):
         keys_t = torch.from_numpy(keys.view(np.int32)).to(dev)
     scheme = _lib.SCHEME_IDS[r0.resampler]
     pw_ws = torch.empty(L.ssm_pw_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
-    scan_ws = torch.empty(L.ssm_scan_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
-    cum = torch.empty((B, P), dtype=torch.int64, device=dev)
+    rs_ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     ess_rel = -1.0 if r0.ess_rel is None else float(r0.ess_rel)
     log_w0 = float(-np.log(P))
     obs_log_sd = float(np.log(spec.obs_sd))
@@ -408,9 +407,6 @@ def advance_runs(runs, upto, rngs):
         step_rngs = [g.child(i) for g in rngs] if host_noise else None
         anc = None
         if maybe_nonuniform:
-            with profiling.maybe("scan", B * P * (esz + 8)):
-                _lib.check(L.ssm_weights_scan(B, P, r0.dtype_id, _lib.ptr(a_last), 1, None, _lib.ptr(fs),
-                                              _lib.ptr(cum), None, _lib.ptr(scan_ws), stream), "ssm_weights_scan")
             anc = torch.empty((B, P), dtype=torch.int32, device=dev)
             u_t = None
             if host_noise:
@@ -420,10 +416,12 @@ def advance_runs(runs, upto, rngs):
                 else:
                     u = np.stack([g.uniform(size=P) for g in rr])
                 u_t = torch.from_numpy(u).to(dev)
-            with profiling.maybe("search", B * P * (8 + 4)):
-                _lib.check(L.ssm_resample_search(B, P, P, scheme, 1, _lib.ptr(cum), _lib.ptr(u_t),
-                                                 _lib.ptr(keys_t), i, _lib.ptr(fs), _lib.ptr(anc), stream),
-                           "ssm_resample_search")
+            # algorithmic bytes: read log-weights (twice: tile sums + offspring) + c + anc
+            with profiling.maybe("resample", B * P * (2 * esz + 4 + 4 + 4)):
+                _lib.check(L.ssm_resample_from_logw(B, P, r0.dtype_id, scheme, _lib.ptr(a_last), None,
+                                                    _lib.ptr(fs), _lib.ptr(u_t), _lib.ptr(keys_t), i,
+                                                    _lib.ptr(anc), _lib.ptr(rs_ws), stream),
+                           "ssm_resample_from_logw")
         n_sub = sched.n_sub[i]
         x_out = torch.empty((B, spec.nx, P), dtype=tdt, device=dev)
         noise_t = None
@@ -528,7 +526,7 @@ def sample_trajectories(runs, rngs):
     u = torch.from_numpy(np.array([[float(np.asarray(g.uniform(size=1))[0])] for g in rngs])).to(dev)
     j = torch.empty((B, 1), dtype=torch.int32, device=dev)
     _lib.check(L.ssm_resample_search(B, P, 1, _lib.SCHEME_IDS["multinomial"], 1, _lib.ptr(cum), _lib.ptr(u),
-                                     None, 0, None, _lib.ptr(j), stream), "ssm_resample_search")
+                                     None, 0, None, _lib.ptr(j), None, stream), "ssm_resample_search")
     xs = np.zeros((B, S + 1), dtype=np.int64)
     ancs = np.zeros((B, S + 1), dtype=np.int64)
     for b, r in enumerate(runs):

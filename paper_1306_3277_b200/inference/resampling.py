@@ -52,8 +52,9 @@ def resample(weights, scheme, rng, size=None):
         u = np.asarray(rng.uniform(size=P), dtype=float)
     ut = torch.from_numpy(u).to(dev)
     anc = torch.empty(P, dtype=torch.int32, device=dev)
+    sws = torch.empty(max(1, L.ssm_search_workspace_bytes(1, P_in, P)), dtype=torch.uint8, device=dev)
     _lib.check(L.ssm_resample_search(1, P_in, P, _lib.SCHEME_IDS[scheme], 1, _lib.ptr(cum), _lib.ptr(ut),
-                                     None, 0, None, _lib.ptr(anc), stream), "ssm_resample_search")
+                                     None, 0, None, _lib.ptr(anc), _lib.ptr(sws), stream), "ssm_resample_search")
     return anc.cpu().numpy().astype(np.int64)
 
 
@@ -69,7 +70,9 @@ def search_cdf(cum, u, scheme, P_out=None, device=None):
     P_out = P_in if P_out is None else P_out
     ut = torch.as_tensor(np.ascontiguousarray(u, dtype=np.float64)).to(dev)
     anc = torch.empty((B, P_out), dtype=torch.int32, device=dev)
+    sws = torch.empty(max(1, L.ssm_search_workspace_bytes(B, P_in, P_out)), dtype=torch.uint8, device=dev)
     _lib.check(L.ssm_resample_search(B, P_in, P_out, _lib.SCHEME_IDS[scheme], 0, _lib.ptr(cum), _lib.ptr(ut),
-                                     None, 0, None, _lib.ptr(anc), _lib.stream_ptr()), "ssm_resample_search")
+                                     None, 0, None, _lib.ptr(anc), _lib.ptr(sws), _lib.stream_ptr()),
+               "ssm_resample_search")
     out = anc.cpu().numpy().astype(np.int64)
     return out[0] if cum.dim() == 1 else out

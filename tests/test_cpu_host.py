@@ -60,7 +60,7 @@ def test_invalid_args_rejected_without_device():
     lib = _lib.load_library()
     assert lib.ssm_propagate_weight(None, None) == _lib.SSM_ERR_INVALID_ARG
     assert lib.ssm_gather(1, 0, 8, 16, None, None, None, None) == _lib.SSM_ERR_INVALID_ARG
-    assert lib.ssm_resample_search(1, 4, 4, 9, 0, None, None, None, 0, None, None, None) == _lib.SSM_ERR_INVALID_ARG
+    assert lib.ssm_resample_search(1, 4, 4, 9, 0, None, None, None, 0, None, None, None, None) == _lib.SSM_ERR_INVALID_ARG
 
 
 def test_resolve_model():

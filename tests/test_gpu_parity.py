@@ -308,3 +308,40 @@ def test_degenerate_ensemble_error():
     with pytest.raises(DegenerateEnsembleError) as e:
         particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(7), n_particles=512)
     assert abs(e.value.time - grid.times[5]) < 1e-12
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("P_in,P_out", [(1000, 7), (7, 1000), (4096, 4096), (3, 1), (50000, 123457)])
+def test_search_ragged_sizes(scheme, P_in, P_out):
+    """resample(..., size=P_out) with P_out != len(weights) (resampling.py:25)."""
+    rs = np.random.default_rng(P_in * 7 + P_out)
+    w = np.exp(rs.normal(0, 2, P_in))
+    w[rs.random(P_in) < 0.3] = 0.0
+    if w.sum() == 0:
+        w[0] = 1.0
+    cum = O.cumulative(w)
+    u = rs.random(1 if scheme == "systematic" else P_out)
+    ref = O.search(cum, O.queries(scheme, u, P_out))
+    np.testing.assert_array_equal(search_cdf(cum, u, scheme, P_out=P_out), ref)
+    np.testing.assert_array_equal(resample(w, scheme, FixedU(u), size=P_out), O.resample_with(w, scheme, u, size=P_out))
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_filter_resampler_degenerate_weights(scheme):
+    """All weight on one particle / uniform weights through the filter path."""
+    from paper_1306_3277_b200 import _lib
+
+    L = _lib.lib()
+    P = 1 << 16
+    for a_np in (np.full(P, -50.0), np.where(np.arange(P) == 1234, 0.0, -1e4)):
+        a = torch.from_numpy(a_np).cuda()
+        from scipy.special import logsumexp
+
+        shift = torch.tensor([logsumexp(a_np)], dtype=torch.float64, device="cuda")
+        ws = torch.empty(L.ssm_resample_workspace_bytes(1, P), dtype=torch.uint8, device="cuda")
+        anc = torch.empty(P, dtype=torch.int32, device="cuda")
+        u = torch.tensor(np.random.default_rng(1).random(1 if scheme == "systematic" else P), device="cuda")
+        _lib.check(L.ssm_resample_from_logw(1, P, 1, _lib.SCHEME_IDS[scheme], _lib.ptr(a), _lib.ptr(shift), None,
+                                            _lib.ptr(u), None, 1, _lib.ptr(anc), _lib.ptr(ws), _lib.stream_ptr()))
+        ref = O.resample_with(np.exp(a_np - logsumexp(a_np)), scheme, u.cpu().numpy())
+        np.testing.assert_array_equal(anc.cpu().numpy(), ref)

@@ -123,7 +123,19 @@ typedef struct ssm_pw_args {
   const uint32_t* keys; /* [B][2] Philox4x32 keys, used when noise == NULL */
   ssm_filter_state* fs; /* [B] */
   void* workspace;      /* ssm_pw_workspace_bytes(B, P) bytes */
+  void* cdf_local;      /* [B][P] uint64 tile-local fixed-point CDF for the next resample, or NULL */
+  void* tile_rec;       /* [B][ceil(P/256)] ssm_tile_rec, or NULL */
 } ssm_pw_args;
+
+/* Per 256-particle tile of a weighted step (written by ssm_propagate_weight):
+ * the tile's max log-weight and its fixed-point weight total
+ * Q = sum_j round(exp(a_j - m) * 2^52).  The tile-local inclusive prefix of the
+ * same q_j is cdf_local.  ssm_resample_from_tiles turns them into exact
+ * global 64-bit CDF offsets once the step's LSE is known. */
+typedef struct ssm_tile_rec {
+  double m;
+  uint64_t Q;
+} ssm_tile_rec;
 
 const char* ssm_version(void);
 const char* ssm_status_string(int status);
@@ -181,6 +193,13 @@ int ssm_resample_search(int B, int P_in, int P_out, int scheme, int cum_kind, co
  * tile prefix -> offspring bounds + partition) -> expand, 4 launches, no
  * look-back and no searches; multinomial: look-back scan + binary search. */
 size_t ssm_resample_workspace_bytes(int B, int P);
+/* Filter fast path: ancestors from the tile records + cdf_local written by the
+ * weighted ssm_propagate_weight (systematic / stratified only): tile scale +
+ * exact integer prefix (1 block per filter) -> offspring bounds + partition
+ * -> expand.  Global CDF: C_j = prefix_b + round(exp(m_b - incr) 2^9 cdf_local_j). */
+int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf_local, const void* tile_rec,
+                            const ssm_filter_state* fs, const double* u, const uint32_t* keys,
+                            int step, int32_t* anc, void* workspace, void* stream);
 int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const void* a, const double* shift,
                            const ssm_filter_state* fs, const double* u, const uint32_t* keys,
                            int step, int32_t* anc, void* workspace, void* stream);

@@ -93,6 +93,8 @@ class PwArgs(C.Structure):
         ("keys", C.c_void_p),
         ("fs", C.c_void_p),
         ("workspace", C.c_void_p),
+        ("cdf_local", C.c_void_p),
+        ("tile_rec", C.c_void_p),
     ]
 
 
@@ -113,6 +115,7 @@ SIGNATURES = {
     "ssm_resample_search": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
     "ssm_resample_workspace_bytes": (_sz, [_i, _i]),
     "ssm_resample_from_logw": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
+    "ssm_resample_from_tiles": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ssm_gather": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "ssm_trace": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_lse_workspace_bytes": (_sz, [_i, _i]),
@@ -128,6 +131,7 @@ LAUNCHING = {
     "ssm_fixed_to_cum": 1,
     "ssm_resample_search": 1,
     "ssm_resample_from_logw": 4,
+    "ssm_resample_from_tiles": 3,
     "ssm_gather": 1,
     "ssm_trace": 1,
     "ssm_logsumexp": 1,

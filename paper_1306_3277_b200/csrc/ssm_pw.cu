@@ -102,6 +102,17 @@ __device__ __forceinline__ void l96_rk4(T x[8], T F, const T nt[8], T s) {
 }
 
 // ----------------------------- the kernel ----------------------------------
+//
+// Grid-stride over 256-particle tiles; one particle per thread per tile.
+// Per weighted tile the block also produces (for the next step's resampling):
+//   m_b     = max log-weight of the tile,
+//   q_j     = round(exp(a_j - m_b) * 2^52)              (tile-local fixed point),
+//   C_j     = inclusive prefix of q within the tile     -> cdf_local[j],
+//   Q_b     = C_last                                    -> tile_rec[b] = {m_b, Q_b},
+// and the tile's scipy-form LSE/ESS partial (max elements split out), folded
+// in tile order into the block partial for the fused finalize.
+
+constexpr double kTileFix = 4503599627370496.0;  // 2^52
 
 template <int MODEL, typename T, bool E, bool INJ>
 __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
@@ -109,6 +120,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
   const int b = blockIdx.y;
   const int P = A.P;
+  const int ntiles = (P + kThreads - 1) / kThreads;
   ssm_filter_state* fs = A.fs + b;
   const int R = fs->resample_now;
   const bool uniform_in = R || fs->uniform;
@@ -121,6 +133,10 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const T* __restrict__ aprev =
       A.a_prev ? static_cast<const T*>(A.a_prev) + static_cast<size_t>(b) * P : nullptr;
   T* __restrict__ aout = A.a_out ? static_cast<T*>(A.a_out) + static_cast<size_t>(b) * P : nullptr;
+  uint64_t* __restrict__ cloc =
+      A.cdf_local ? static_cast<uint64_t*>(A.cdf_local) + static_cast<size_t>(b) * P : nullptr;
+  ssm_tile_rec* __restrict__ trec =
+      A.tile_rec ? static_cast<ssm_tile_rec*>(A.tile_rec) + static_cast<size_t>(b) * ntiles : nullptr;
   const T* __restrict__ noise =
       INJ ? static_cast<const T*>(A.noise) + static_cast<size_t>(b) * A.n_sub * NX * P : nullptr;
   const double* th = A.theta + 4 * b;
@@ -130,84 +146,152 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const T logw0 = static_cast<T>(A.log_w0);
   const T obs_log_sd = static_cast<T>(A.obs_log_sd);
   const T lsp = static_cast<T>(A.log_sqrt_2pi);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  Lse st = lse_empty();
+  __shared__ double s_max[kThreads / 32];
+  __shared__ double s_sum[3][kThreads / 32];
+  __shared__ uint64_t s_q[kThreads / 32];
+
+  Lse st = lse_empty();  // block partial (thread 0), tiles folded in order
   bool bad = false;
   int bad_sub = 0;
 
-  for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads) {
-    const int src = anc ? anc[p] : p;
-    T x[NX];
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int p = tile * kThreads + threadIdx.x;
+    const bool act = p < P;
+    double a_d = -CUDART_INF;
+    if (act) {
+      const int src = anc ? anc[p] : p;
+      T x[NX];
 #pragma unroll
-    for (int n = 0; n < NX; ++n) x[n] = xin[static_cast<size_t>(n) * P + src];
+      for (int n = 0; n < NX; ++n) x[n] = xin[static_cast<size_t>(n) * P + src];
 
-    for (int k = 0; k < A.n_sub; ++k) {
-      const ssm_substep& S = A.subs[k];
-      if constexpr (MODEL == SSM_MODEL_LORENZ96) {
-        const T F = static_cast<T>(th[0]);
-        const T sq = static_cast<T>(th[1]);  // np.sqrt(sigma2), host-computed
-        T W[8], nt[8];
-        if constexpr (INJ) {
+      for (int k = 0; k < A.n_sub; ++k) {
+        const ssm_substep& S = A.subs[k];
+        if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+          const T F = static_cast<T>(th[0]);
+          const T sq = static_cast<T>(th[1]);  // np.sqrt(sigma2), host-computed
+          T W[8], nt[8];
+          if constexpr (INJ) {
+#pragma unroll
+            for (int n = 0; n < 8; ++n) W[n] = noise[(static_cast<size_t>(k) * 8 + n) * P + p];
+          } else {
+            normals8<T>(k0, k1, static_cast<uint32_t>(p), static_cast<uint32_t>(A.step),
+                        static_cast<uint32_t>(k), W);
+            const T sd = static_cast<T>(S.sd);
+#pragma unroll
+            for (int n = 0; n < 8; ++n) W[n] = sd * W[n];
+          }
 #pragma unroll
           for (int n = 0; n < 8; ++n)
-            W[n] = noise[(static_cast<size_t>(k) * 8 + n) * P + p];
+            nt[n] = E ? O::div(O::mul(sq, W[n]), T(0.05)) : O::mul(O::mul(sq, W[n]), T(20.0));
+          for (int m = 0; m < S.n_ode; ++m) l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
         } else {
-          normals8<T>(k0, k1, static_cast<uint32_t>(p), static_cast<uint32_t>(A.step),
-                      static_cast<uint32_t>(k), W);
-          const T sd = static_cast<T>(S.sd);
-#pragma unroll
-          for (int n = 0; n < 8; ++n) W[n] = sd * W[n];
+          // Windkessel.bi:28-29, Pp <- exp(-h/(R*C))*Pp + R*(1 - exp(-h/(R*C)))*(F + xi)
+          const T ca = static_cast<T>(th[0]), cb = static_cast<T>(th[1]);
+          T xi;
+          if constexpr (INJ) {
+            xi = noise[static_cast<size_t>(k) * P + p];
+          } else {
+            xi = static_cast<T>(th[3]) * normal1<T>(k0, k1, static_cast<uint32_t>(p),
+                                                    static_cast<uint32_t>(A.step), static_cast<uint32_t>(k));
+          }
+          x[0] = O::add(O::mul(ca, x[0]), O::mul(cb, O::add(static_cast<T>(S.u_in), xi)));
         }
+        if (A.check_finite && !bad) {
+          bool ok = true;
 #pragma unroll
-        for (int n = 0; n < 8; ++n)
-          nt[n] = E ? O::div(O::mul(sq, W[n]), T(0.05)) : O::mul(O::mul(sq, W[n]), T(20.0));
-        for (int m = 0; m < S.n_ode; ++m) l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
-      } else {
-        // Windkessel.bi:28-29, Pp <- exp(-h/(R*C))*Pp + R*(1 - exp(-h/(R*C)))*(F + xi)
-        const T ca = static_cast<T>(th[0]), cb = static_cast<T>(th[1]);
-        T xi;
-        if constexpr (INJ) {
-          xi = noise[static_cast<size_t>(k) * P + p];
-        } else {
-          xi = static_cast<T>(th[3]) *
-               normal1<T>(k0, k1, static_cast<uint32_t>(p), static_cast<uint32_t>(A.step),
-                          static_cast<uint32_t>(k));
-        }
-        x[0] = O::add(O::mul(ca, x[0]), O::mul(cb, O::add(static_cast<T>(S.u_in), xi)));
-      }
-      if (A.check_finite && !bad) {
-        bool ok = true;
-#pragma unroll
-        for (int n = 0; n < NX; ++n) ok &= finite(x[n]);
-        if (!ok) {
-          bad = true;
-          bad_sub = k;
-        }
-      }
-    }
-#pragma unroll
-    for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * P + p] = x[n];
-
-    if (has_obs) {
-      T g = T(0);
-      if constexpr (MODEL == SSM_MODEL_LORENZ96) {
-#pragma unroll
-        for (int n = 0; n < 8; ++n) {
-          if (A.obs_mask & (1u << n)) {
-            const T z = O::mul(O::sub(static_cast<T>(A.y[n]), x[n]), T(2.0));  // exact: / 0.5
-            g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
+          for (int n = 0; n < NX; ++n) ok &= finite(x[n]);
+          if (!ok) {
+            bad = true;
+            bad_sub = k;
           }
         }
-      } else {
-        const T mean = O::add(x[0], O::mul(static_cast<T>(th[2]), static_cast<T>(A.u_obs)));
-        const T z = O::mul(O::sub(static_cast<T>(A.y[0]), mean), T(0.5));  // exact: / 2.0
-        g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
       }
-      const T lw = uniform_in ? logw0 : O::sub(aprev[p], static_cast<T>(incr_prev));
-      const T a = O::add(lw, g);
-      aout[p] = a;
-      lse_push(st, static_cast<double>(a));
+#pragma unroll
+      for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * P + p] = x[n];
+
+      if (has_obs) {
+        T g = T(0);
+        if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+#pragma unroll
+          for (int n = 0; n < 8; ++n) {
+            if (A.obs_mask & (1u << n)) {
+              const T z = O::mul(O::sub(static_cast<T>(A.y[n]), x[n]), T(2.0));  // exact: / 0.5
+              g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
+            }
+          }
+        } else {
+          const T mean = O::add(x[0], O::mul(static_cast<T>(th[2]), static_cast<T>(A.u_obs)));
+          const T z = O::mul(O::sub(static_cast<T>(A.y[0]), mean), T(0.5));  // exact: / 2.0
+          g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
+        }
+        const T lw = uniform_in ? logw0 : O::sub(aprev[p], static_cast<T>(incr_prev));
+        const T a = O::add(lw, g);
+        if (aout) aout[p] = a;
+        a_d = static_cast<double>(a);
+      }
     }
+    if (!has_obs) continue;  // block-uniform
+
+    // ---- tile max (NaN never wins a comparison; it poisons t below) ----
+    double m = a_d;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, m, o);
+      m = y > m ? y : m;
+    }
+    if (lane == 0) s_max[warp] = m;
+    __syncthreads();
+    double mb = s_max[0];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) mb = s_max[w] > mb ? s_max[w] : mb;
+
+    // ---- tile-local weights, fixed-point prefix, LSE/ESS partial ----
+    const bool ismax = act && a_d == mb;
+    const double e = !act ? 0.0 : (ismax ? 1.0 : exp(a_d - mb));
+    const uint64_t q = (e >= 0.0 && e <= 1.0) ? __double2ull_rn(e * kTileFix) : 0ull;
+    double c_ = ismax ? 1.0 : 0.0;
+    double t_ = (act && !ismax) ? e : 0.0;
+    double s2_ = t_ * t_;
+    uint64_t qi = q;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, qi, o);
+      if (lane >= o) qi += y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      c_ += __shfl_xor_sync(0xffffffffu, c_, o);
+      t_ += __shfl_xor_sync(0xffffffffu, t_, o);
+      s2_ += __shfl_xor_sync(0xffffffffu, s2_, o);
+    }
+    if (lane == 31) s_q[warp] = qi;
+    if (lane == 0) {
+      s_sum[0][warp] = c_;
+      s_sum[1][warp] = t_;
+      s_sum[2][warp] = s2_;
+    }
+    __syncthreads();
+    uint64_t qex = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w)
+      if (w < warp) qex += s_q[w];
+    if (cloc && act) cloc[p] = qex + qi;
+    if (threadIdx.x == 0) {
+      uint64_t Q = 0;
+      double C = 0.0, Tt = 0.0, S2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) {
+        Q += s_q[w];
+        C += s_sum[0][w];
+        Tt += s_sum[1][w];
+        S2 += s_sum[2][w];
+      }
+      if (trec) trec[tile] = ssm_tile_rec{mb, Q};
+      st = lse_combine(st, Lse{mb, C, Tt, S2});
+    }
+    __syncthreads();  // s_* reused by the next tile
   }
 
   if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
@@ -216,10 +300,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   __shared__ Lse red[kThreads / 32];
   __shared__ bool s_last;
   Lse* parts = reinterpret_cast<Lse*>(A.workspace) + static_cast<size_t>(b) * kMaxPwBlocks;
-  if (has_obs) {
-    const Lse r = lse_block_reduce<kThreads>(st, red);
-    if (threadIdx.x == 0) parts[blockIdx.x] = r;
-  }
+  if (has_obs && threadIdx.x == 0) parts[blockIdx.x] = st;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&fs->blocks_done, 1u) == gridDim.x - 1;

@@ -296,7 +296,9 @@ constexpr int kMergeItems = 8;
 
 constexpr int kDiag = 2048;  // merged-diagonal elements per expand block
 
-enum CumSrc { kCumDouble = 0, kCumFixed = 1, kCumLogw = 2 };
+enum CumSrc { kCumDouble = 0, kCumFixed = 1, kCumLogw = 2, kCumTiles = 3 };
+
+constexpr double kTileScale = 512.0;  // 2^9: tile-local 2^52 fixed point -> global 2^61
 
 __device__ __forceinline__ double sys_query(int k, double u, int P_out, double invP, bool pow2) {
   const double num = static_cast<double>(k) + u;
@@ -392,6 +394,56 @@ tile_prefix_kernel(int tiles, uint64_t* __restrict__ sums, uint64_t* __restrict_
   if (threadIdx.x == 0) totals[b] = tot;
 }
 
+// per-tile global scale and exact exclusive prefix, from the pw kernel's tile
+// records; one 1024-thread block per filter.  Q'_b = round(exp(m_b - incr) 2^9 Q_b)
+// is exactly the value the offspring kernel reaches at the tile's last particle,
+// so the global CDF is monotone and deterministic.
+__global__ void __launch_bounds__(1024)
+tile_scale_prefix_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec,
+                         const ssm_filter_state* __restrict__ fs, double* __restrict__ scale,
+                         uint64_t* __restrict__ prefix, uint64_t* __restrict__ totals) {
+  const int b = blockIdx.x;
+  if (!fs[b].resample_now) return;
+  const double incr = fs[b].incr;
+  const ssm_tile_rec* rb = rec + static_cast<size_t>(b) * ntiles;
+  double* sb = scale + static_cast<size_t>(b) * ntiles;
+  uint64_t* pb = prefix + static_cast<size_t>(b) * ntiles;
+  const int per = (ntiles + 1023) / 1024;
+  const int t0 = threadIdx.x * per, t1 = min(t0 + per, ntiles);
+  uint64_t local = 0;
+  for (int t = t0; t < t1; ++t) {
+    const ssm_tile_rec r = rb[t];
+    const double sc = r.m == -CUDART_INF ? 0.0 : exp(r.m - incr) * kTileScale;
+    sb[t] = sc;
+    const double v = sc * static_cast<double>(r.Q);
+    const uint64_t qg = (v >= 0.0 && v < 4.0e18) ? __double2ull_rn(v) : 0ull;
+    pb[t] = qg;  // tile total for now
+    local += qg;
+  }
+  __shared__ uint64_t wsum[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  uint64_t wex = 0, tot = 0;
+  for (int w = 0; w < 32; ++w) {
+    if (w < warp) wex += wsum[w];
+    tot += wsum[w];
+  }
+  uint64_t run = wex + incl - local;
+  for (int t = t0; t < t1; ++t) {
+    const uint64_t v = pb[t];
+    pb[t] = run;
+    run += v;
+  }
+  if (threadIdx.x == 0) totals[b] = tot;
+}
+
 // c_j for every particle + merge-path partition entries
 template <int SCHEME, int SRC, typename T>
 __global__ void __launch_bounds__(kThreads)
@@ -427,6 +479,24 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) cum[i] = jt + i < P_in ? cd[jt + i] : 2.0;
     cum_prev = jt > 0 ? cd[jt - 1] : 0.0;
+  } else if constexpr (SRC == kCumTiles) {
+    // src = cdf_local (u64 [B][P]); tile_prefix = per-tile exclusive global prefix;
+    // shift (reinterpreted) = per-tile scale exp(m_b - incr) * 2^9 as double [B][ntiles]
+    const int nt = (P_in + kThreads - 1) / kThreads;
+    const uint64_t* cl = static_cast<const uint64_t*>(src) + static_cast<size_t>(b) * P_in;
+    const int tb = jt / kThreads;  // kScanItems consecutive particles share one 256-tile
+    const double sc = tb < nt ? shift[static_cast<size_t>(b) * nt + tb] : 0.0;
+    const uint64_t pre = tb < nt ? tile_prefix[static_cast<size_t>(b) * nt + tb] : 0ull;
+    const double inv = 1.0 / static_cast<double>(totals[b]);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      const int j = jt + i;
+      cum[i] = j < P_in ? static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(cl[j]))) * inv : 2.0;
+      if (j == P_in - 1) cum[i] = 1.0;  // cum[-1] = 1.0 (resampling.py:27)
+    }
+    cum_prev = jt == 0 ? 0.0
+               : (jt % kThreads == 0 ? static_cast<double>(pre) * inv
+                                     : static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(cl[jt - 1]))) * inv);
   } else {
     const size_t off = static_cast<size_t>(b) * P_in + j0;
     double sh = 0.0;
@@ -846,6 +916,37 @@ extern "C" int ssm_resample_search(int B, int P_in, int P_out, int scheme, int c
   } else {
     return SSM_ERR_INVALID_ARG;
   }
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf_local,
+                                       const void* tile_rec, const ssm_filter_state* fs,
+                                       const double* u, const uint32_t* keys, int step, int32_t* anc,
+                                       void* workspace, void* stream) {
+  if (B <= 0 || B > 65535 || P <= 0 || !cdf_local || !tile_rec || !fs || !anc || !workspace)
+    return SSM_ERR_INVALID_ARG;
+  if (!u && !keys) return SSM_ERR_INVALID_ARG;
+  if (scheme != SSM_SYSTEMATIC && scheme != SSM_STRATIFIED) return SSM_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SearchWs w;
+  search_ws_layout(B, P, P, workspace, &w);
+  const int nt = (P + kThreads - 1) / kThreads;
+  // reuse: w.C (B*P u64) holds the per-tile scale (double) and w.sums the per-tile prefix
+  double* scale = reinterpret_cast<double*>(w.C);
+  uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + static_cast<size_t>(B) * nt;
+  tile_scale_prefix_kernel<<<B, 1024, 0, s>>>(nt, static_cast<const ssm_tile_rec*>(tile_rec), fs, scale,
+                                              pref, w.totals);
+  const int tiles = scan_tiles(P);
+  const int nd = ndiag_of(P, P);
+  const dim3 g(tiles, B);
+  if (scheme == SSM_SYSTEMATIC)
+    offspring_kernel<SSM_SYSTEMATIC, kCumTiles, double><<<g, kThreads, 0, s>>>(
+        P, P, cdf_local, scale, pref, w.totals, u, keys, step, fs, w.cnt, w.split, nd);
+  else
+    offspring_kernel<SSM_STRATIFIED, kCumTiles, double><<<g, kThreads, 0, s>>>(
+        P, P, cdf_local, scale, pref, w.totals, u, keys, step, fs, w.cnt, w.split, nd);
+  expand_kernel<<<dim3(nd, B), kThreads, 0, s>>>(P, P, w.cnt, w.split, nd, fs, anc);
   SSM_CHECK_LAUNCH();
   return SSM_OK;
 }

@@ -220,6 +220,8 @@ class ParticleRun:
         self._x = None
         self._a = None  # unnormalised log-weights of the last weighted step
         self._fs = None  # (64,) uint8 view of an ssm_filter_state
+        self._cdf = None  # (P,) tile-local fixed-point CDF of the last weighted step
+        self._trec = None  # (ceil(P/256), 2) tile records {max, Q} of the last weighted step
         self._maybe_nonuniform = False
         self._derived = None
 
@@ -344,6 +346,8 @@ def init_runs(runs, rngs):
     for b, r in enumerate(runs):
         r._x = x[b]
         r._a = None
+        r._cdf = None
+        r._trec = None
         r._fs = fs[b]
         r.loglik = 0.0
         r.pos = 0
@@ -381,6 +385,17 @@ def advance_runs(runs, upto, rngs):
     scheme = _lib.SCHEME_IDS[r0.resampler]
     pw_ws = torch.empty(L.ssm_pw_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     rs_ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
+    # systematic / stratified resample from the pw kernel's tile-local CDF (no second pass over logw)
+    tiles_ok = r0.resampler in ("systematic", "stratified")
+    ntile = (P + 255) // 256
+    cdf_local = tile_rec = None
+    if tiles_ok:
+        if runs[0]._cdf is not None:  # resume: fresh copies, so clones sharing the views stay intact
+            cdf_local = torch.stack([r._cdf for r in runs])
+            tile_rec = torch.stack([r._trec for r in runs])
+        else:
+            cdf_local = torch.empty((B, P), dtype=torch.int64, device=dev)
+            tile_rec = torch.empty((B, ntile, 2), dtype=torch.float64, device=dev)
     ess_rel = -1.0 if r0.ess_rel is None else float(r0.ess_rel)
     log_w0 = float(-np.log(P))
     obs_log_sd = float(np.log(spec.obs_sd))
@@ -416,12 +431,19 @@ def advance_runs(runs, upto, rngs):
                 else:
                     u = np.stack([g.uniform(size=P) for g in rr])
                 u_t = torch.from_numpy(u).to(dev)
-            # algorithmic bytes: read log-weights (twice: tile sums + offspring) + c + anc
-            with profiling.maybe("resample", B * P * (2 * esz + 4 + 4 + 4)):
-                _lib.check(L.ssm_resample_from_logw(B, P, r0.dtype_id, scheme, _lib.ptr(a_last), None,
-                                                    _lib.ptr(fs), _lib.ptr(u_t), _lib.ptr(keys_t), i,
-                                                    _lib.ptr(anc), _lib.ptr(rs_ws), stream),
-                           "ssm_resample_from_logw")
+            if tiles_ok:
+                # bytes: cdf_local read + c write/read + anc write (+ tile records, negligible)
+                with profiling.maybe("resample", B * P * (8 + 4 + 4 + 4)):
+                    _lib.check(L.ssm_resample_from_tiles(B, P, scheme, _lib.ptr(cdf_local), _lib.ptr(tile_rec),
+                                                         _lib.ptr(fs), _lib.ptr(u_t), _lib.ptr(keys_t), i,
+                                                         _lib.ptr(anc), _lib.ptr(rs_ws), stream),
+                               "ssm_resample_from_tiles")
+            else:
+                with profiling.maybe("resample", B * P * (2 * esz + 4 + 4 + 4)):
+                    _lib.check(L.ssm_resample_from_logw(B, P, r0.dtype_id, scheme, _lib.ptr(a_last), None,
+                                                        _lib.ptr(fs), _lib.ptr(u_t), _lib.ptr(keys_t), i,
+                                                        _lib.ptr(anc), _lib.ptr(rs_ws), stream),
+                               "ssm_resample_from_logw")
         n_sub = sched.n_sub[i]
         x_out = torch.empty((B, spec.nx, P), dtype=tdt, device=dev)
         noise_t = None
@@ -440,6 +462,8 @@ def advance_runs(runs, upto, rngs):
         args.a_prev = a_last.data_ptr() if a_last is not None else None
         args.a_out = a_out.data_ptr() if a_out is not None else None
         args.noise = noise_t.data_ptr() if noise_t is not None else None
+        args.cdf_local = cdf_local.data_ptr() if (tiles_ok and obs is not None) else None
+        args.tile_rec = tile_rec.data_ptr() if (tiles_ok and obs is not None) else None
         if obs is not None:
             args.has_obs = 1
             args.obs_mask = obs[0]
@@ -451,7 +475,7 @@ def advance_runs(runs, upto, rngs):
             args.obs_mask = 0
         # algorithmic bytes: (anc) + gather read + write of x + (read a_prev) + write a
         nbytes = B * P * (2 * spec.nx * esz + (4 if anc is not None else 0)
-                          + (esz if obs is not None else 0)
+                          + (esz + (8 if tiles_ok else 0) if obs is not None else 0)
                           + (esz if (a_last is not None and obs is not None and r0.ess_rel is not None) else 0))
         with profiling.maybe("propagate_weight", nbytes):
             _lib.check(L.ssm_propagate_weight(args, stream), "ssm_propagate_weight")
@@ -474,6 +498,8 @@ def advance_runs(runs, upto, rngs):
         r.weights_uniform = bool(st["uniform"])
         r._x = x_prev[b]
         r._a = a_last[b] if a_last is not None else None
+        r._cdf = cdf_local[b] if (tiles_ok and a_last is not None) else None
+        r._trec = tile_rec[b] if (tiles_ok and a_last is not None) else None
         r._fs = fs[b]
         r._maybe_nonuniform = maybe_nonuniform
         r.history.extend(new_hist[b])

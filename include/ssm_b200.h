@@ -124,10 +124,10 @@ typedef struct ssm_pw_args {
   ssm_filter_state* fs; /* [B] */
   void* workspace;      /* ssm_pw_workspace_bytes(B, P) bytes */
   void* cdf_local;      /* [B][P] uint64 tile-local fixed-point CDF for the next resample, or NULL */
-  void* tile_rec;       /* [B][ceil(P/256)] ssm_tile_rec, or NULL */
+  void* tile_rec;       /* [B][ceil(P/32)] ssm_tile_rec (one per warp tile), or NULL */
 } ssm_pw_args;
 
-/* Per 256-particle tile of a weighted step (written by ssm_propagate_weight):
+/* Per 32-particle (warp) tile of a weighted step (written by ssm_propagate_weight):
  * the tile's max log-weight and its fixed-point weight total
  * Q = sum_j round(exp(a_j - m) * 2^52).  The tile-local inclusive prefix of the
  * same q_j is cdf_local.  ssm_resample_from_tiles turns them into exact

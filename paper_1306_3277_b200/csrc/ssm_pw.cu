@@ -103,14 +103,15 @@ __device__ __forceinline__ void l96_rk4(T x[8], T F, const T nt[8], T s) {
 
 // ----------------------------- the kernel ----------------------------------
 //
-// Grid-stride over 256-particle tiles; one particle per thread per tile.
-// Per weighted tile the block also produces (for the next step's resampling):
-//   m_b     = max log-weight of the tile,
-//   q_j     = round(exp(a_j - m_b) * 2^52)              (tile-local fixed point),
+// Grid-stride over 256-particle block tiles; one particle per thread per tile.
+// Per weighted WARP tile w (32 consecutive particles) the warp also produces,
+// for the next step's resampling:
+//   m_w     = max log-weight of the warp tile,
+//   q_j     = round(exp(a_j - m_w) * 2^52)              (tile-local fixed point),
 //   C_j     = inclusive prefix of q within the tile     -> cdf_local[j],
-//   Q_b     = C_last                                    -> tile_rec[b] = {m_b, Q_b},
+//   Q_w     = C_last                                    -> tile_rec[w] = {m_w, Q_w},
 // and the tile's scipy-form LSE/ESS partial (max elements split out), folded
-// in tile order into the block partial for the fused finalize.
+// in tile order into the warp / block partials for the fused finalize.
 
 constexpr double kTileFix = 4503599627370496.0;  // 2^52
 
@@ -148,11 +149,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const T lsp = static_cast<T>(A.log_sqrt_2pi);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  __shared__ double s_max[kThreads / 32];
-  __shared__ double s_sum[3][kThreads / 32];
-  __shared__ uint64_t s_q[kThreads / 32];
-
-  Lse st = lse_empty();  // block partial (thread 0), tiles folded in order
+  Lse st = lse_empty();  // warp partial (lane 0), warp tiles folded in order
   bool bad = false;
   int bad_sub = 0;
 
@@ -234,20 +231,15 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
     }
     if (!has_obs) continue;  // block-uniform
 
-    // ---- tile max (NaN never wins a comparison; it poisons t below) ----
-    double m = a_d;
+    // ---- warp tile (32 consecutive particles): max, fixed-point prefix, LSE/ESS partial.
+    // Shuffles only: no block barrier inside the particle loop, so warps stay
+    // out of phase and memory overlaps compute.
+    double mb = a_d;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const double y = __shfl_xor_sync(0xffffffffu, m, o);
-      m = y > m ? y : m;
+      const double y = __shfl_xor_sync(0xffffffffu, mb, o);
+      mb = y > mb ? y : mb;  // NaN never wins; it poisons t below
     }
-    if (lane == 0) s_max[warp] = m;
-    __syncthreads();
-    double mb = s_max[0];
-#pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) mb = s_max[w] > mb ? s_max[w] : mb;
-
-    // ---- tile-local weights, fixed-point prefix, LSE/ESS partial ----
     const bool ismax = act && a_d == mb;
     const double e = !act ? 0.0 : (ismax ? 1.0 : exp(a_d - mb));
     const uint64_t q = (e >= 0.0 && e <= 1.0) ? __double2ull_rn(e * kTileFix) : 0ull;
@@ -266,32 +258,12 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
       t_ += __shfl_xor_sync(0xffffffffu, t_, o);
       s2_ += __shfl_xor_sync(0xffffffffu, s2_, o);
     }
-    if (lane == 31) s_q[warp] = qi;
+    if (cloc && act) cloc[p] = qi;
+    const uint64_t Qw = __shfl_sync(0xffffffffu, qi, 31);
     if (lane == 0) {
-      s_sum[0][warp] = c_;
-      s_sum[1][warp] = t_;
-      s_sum[2][warp] = s2_;
+      if (trec && p < P) trec[p >> 5] = ssm_tile_rec{mb, Qw};
+      st = lse_combine(st, Lse{mb, c_, t_, s2_});
     }
-    __syncthreads();
-    uint64_t qex = 0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w)
-      if (w < warp) qex += s_q[w];
-    if (cloc && act) cloc[p] = qex + qi;
-    if (threadIdx.x == 0) {
-      uint64_t Q = 0;
-      double C = 0.0, Tt = 0.0, S2 = 0.0;
-#pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w) {
-        Q += s_q[w];
-        C += s_sum[0][w];
-        Tt += s_sum[1][w];
-        S2 += s_sum[2][w];
-      }
-      if (trec) trec[tile] = ssm_tile_rec{mb, Q};
-      st = lse_combine(st, Lse{mb, C, Tt, S2});
-    }
-    __syncthreads();  // s_* reused by the next tile
   }
 
   if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
@@ -300,7 +272,11 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   __shared__ Lse red[kThreads / 32];
   __shared__ bool s_last;
   Lse* parts = reinterpret_cast<Lse*>(A.workspace) + static_cast<size_t>(b) * kMaxPwBlocks;
-  if (has_obs && threadIdx.x == 0) parts[blockIdx.x] = st;
+  if (has_obs) {
+    // lane 0 of each warp holds its warp's partial; fold warps in order
+    const Lse r = lse_block_reduce<kThreads>(lane == 0 ? st : lse_empty(), red);
+    if (threadIdx.x == 0) parts[blockIdx.x] = r;
+  }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&fs->blocks_done, 1u) == gridDim.x - 1;

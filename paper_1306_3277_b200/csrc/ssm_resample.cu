@@ -298,6 +298,9 @@ constexpr int kDiag = 2048;  // merged-diagonal elements per expand block
 
 enum CumSrc { kCumDouble = 0, kCumFixed = 1, kCumLogw = 2, kCumTiles = 3 };
 
+// layout of the kCumTiles prefix buffer: [B][nt] in-block tile prefixes, then [B][nblk] block prefixes
+__host__ __device__ inline size_t B_total_tiles_offset(int nt, int B) { return static_cast<size_t>(B) * nt; }
+
 constexpr double kTileScale = 512.0;  // 2^9: tile-local 2^52 fixed point -> global 2^61
 
 __device__ __forceinline__ double sys_query(int k, double u, int P_out, double invP, bool pow2) {
@@ -394,32 +397,85 @@ tile_prefix_kernel(int tiles, uint64_t* __restrict__ sums, uint64_t* __restrict_
   if (threadIdx.x == 0) totals[b] = tot;
 }
 
-// per-tile global scale and exact exclusive prefix, from the pw kernel's tile
-// records; one 1024-thread block per filter.  Q'_b = round(exp(m_b - incr) 2^9 Q_b)
-// is exactly the value the offspring kernel reaches at the tile's last particle,
-// so the global CDF is monotone and deterministic.
-__global__ void __launch_bounds__(1024)
-tile_scale_prefix_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec,
-                         const ssm_filter_state* __restrict__ fs, double* __restrict__ scale,
-                         uint64_t* __restrict__ prefix, uint64_t* __restrict__ totals) {
-  const int b = blockIdx.x;
+// Per-warp-tile global scale and exact exclusive prefix, from the pw kernel's
+// tile records.  Q'_w = round(exp(m_w - incr) 2^9 Q_w) is exactly the value the
+// offspring kernel reaches at the tile's last particle, so the global CDF is
+// monotone and deterministic.  Two launches: per-block (2048 tiles) scan, then
+// a 1-block scan of the block totals.
+constexpr int kRecPerBlock = kThreads * kScanItems;  // 2048 tile records per block
+
+__global__ void __launch_bounds__(kThreads)
+tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_filter_state* __restrict__ fs,
+                  double* __restrict__ scale, uint64_t* __restrict__ prel, uint64_t* __restrict__ blk_tot) {
+  __shared__ uint64_t sm[kRecPerBlock + kRecPerBlock / 8];
+  __shared__ uint64_t warp_tot[kThreads / 32];
+  const int b = blockIdx.y, blk = blockIdx.x;
   if (!fs[b].resample_now) return;
   const double incr = fs[b].incr;
-  const ssm_tile_rec* rb = rec + static_cast<size_t>(b) * ntiles;
-  double* sb = scale + static_cast<size_t>(b) * ntiles;
-  uint64_t* pb = prefix + static_cast<size_t>(b) * ntiles;
-  const int per = (ntiles + 1023) / 1024;
-  const int t0 = threadIdx.x * per, t1 = min(t0 + per, ntiles);
-  uint64_t local = 0;
-  for (int t = t0; t < t1; ++t) {
-    const ssm_tile_rec r = rb[t];
-    const double sc = r.m == -CUDART_INF ? 0.0 : exp(r.m - incr) * kTileScale;
-    sb[t] = sc;
-    const double v = sc * static_cast<double>(r.Q);
-    const uint64_t qg = (v >= 0.0 && v < 4.0e18) ? __double2ull_rn(v) : 0ull;
-    pb[t] = qg;  // tile total for now
-    local += qg;
+  const size_t off = static_cast<size_t>(b) * ntiles + static_cast<size_t>(blk) * kRecPerBlock;
+  const int n = min(kRecPerBlock, ntiles - blk * kRecPerBlock);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int e = i * kThreads + threadIdx.x;
+    uint64_t qg = 0;
+    if (e < n) {
+      const ssm_tile_rec r = rec[off + e];
+      const double sc = r.m == -CUDART_INF ? 0.0 : exp(r.m - incr) * kTileScale;
+      scale[off + e] = sc;
+      const double v = sc * static_cast<double>(r.Q);
+      qg = (v >= 0.0 && v < 4.0e18) ? __double2ull_rn(v) : 0ull;
+    }
+    sm[e + (e >> 3)] = qg;
   }
+  __syncthreads();
+  uint64_t v[kScanItems];
+  uint64_t run = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int e = threadIdx.x * kScanItems + i;
+    v[i] = run;  // exclusive
+    run += sm[e + (e >> 3)];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  uint64_t wex = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (w < warp) wex += warp_tot[w];
+    tot += warp_tot[w];
+  }
+  const uint64_t basev = wex + incl - run;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int e = threadIdx.x * kScanItems + i;
+    sm[e + (e >> 3)] = basev + v[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int e = i * kThreads + threadIdx.x;
+    if (e < n) prel[off + e] = sm[e + (e >> 3)];
+  }
+  if (threadIdx.x == 0) blk_tot[static_cast<size_t>(b) * gridDim.x + blk] = tot;
+}
+
+__global__ void __launch_bounds__(1024)
+blk_prefix_kernel(int nblk, uint64_t* __restrict__ blk, uint64_t* __restrict__ totals,
+                  const ssm_filter_state* __restrict__ fs) {
+  const int b = blockIdx.x;
+  if (fs && !fs[b].resample_now) return;
+  uint64_t* bb = blk + static_cast<size_t>(b) * nblk;
+  const int per = (nblk + 1023) / 1024;
+  const int t0 = threadIdx.x * per, t1 = min(t0 + per, nblk);
+  uint64_t local = 0;
+  for (int t = t0; t < t1; ++t) local += bb[t];
   __shared__ uint64_t wsum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t incl = local;
@@ -437,9 +493,9 @@ tile_scale_prefix_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec,
   }
   uint64_t run = wex + incl - local;
   for (int t = t0; t < t1; ++t) {
-    const uint64_t v = pb[t];
-    pb[t] = run;
-    run += v;
+    const uint64_t x = bb[t];
+    bb[t] = run;
+    run += x;
   }
   if (threadIdx.x == 0) totals[b] = tot;
 }
@@ -480,13 +536,19 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
     for (int i = 0; i < kScanItems; ++i) cum[i] = jt + i < P_in ? cd[jt + i] : 2.0;
     cum_prev = jt > 0 ? cd[jt - 1] : 0.0;
   } else if constexpr (SRC == kCumTiles) {
-    // src = cdf_local (u64 [B][P]); tile_prefix = per-tile exclusive global prefix;
-    // shift (reinterpreted) = per-tile scale exp(m_b - incr) * 2^9 as double [B][ntiles]
-    const int nt = (P_in + kThreads - 1) / kThreads;
+    // src = cdf_local (u64 [B][P]); `shift` = per-warp-tile scale exp(m_w - incr) 2^9
+    // [B][nt]; tile_prefix = per-tile exclusive prefix within its 2048-tile block
+    // [B][nt] followed by the block prefixes [B][nblk].
+    const int nt = (P_in + 31) / 32;
+    const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
     const uint64_t* cl = static_cast<const uint64_t*>(src) + static_cast<size_t>(b) * P_in;
-    const int tb = jt / kThreads;  // kScanItems consecutive particles share one 256-tile
-    const double sc = tb < nt ? shift[static_cast<size_t>(b) * nt + tb] : 0.0;
-    const uint64_t pre = tb < nt ? tile_prefix[static_cast<size_t>(b) * nt + tb] : 0ull;
+    const int tw = jt >> 5;  // kScanItems consecutive particles share one warp tile
+    const bool ok = tw < nt;
+    const double sc = ok ? shift[static_cast<size_t>(b) * nt + tw] : 0.0;
+    const uint64_t* blk_pre = tile_prefix + static_cast<size_t>(B_total_tiles_offset(nt, gridDim.y));
+    const uint64_t pre = ok ? tile_prefix[static_cast<size_t>(b) * nt + tw] +
+                                  blk_pre[static_cast<size_t>(b) * nblk + tw / kRecPerBlock]
+                            : 0ull;
     const double inv = 1.0 / static_cast<double>(totals[b]);
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
@@ -495,8 +557,8 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
       if (j == P_in - 1) cum[i] = 1.0;  // cum[-1] = 1.0 (resampling.py:27)
     }
     cum_prev = jt == 0 ? 0.0
-               : (jt % kThreads == 0 ? static_cast<double>(pre) * inv
-                                     : static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(cl[jt - 1]))) * inv);
+               : ((jt & 31) == 0 ? static_cast<double>(pre) * inv
+                                 : static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(cl[jt - 1]))) * inv);
   } else {
     const size_t off = static_cast<size_t>(b) * P_in + j0;
     double sh = 0.0;
@@ -931,12 +993,15 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SearchWs w;
   search_ws_layout(B, P, P, workspace, &w);
-  const int nt = (P + kThreads - 1) / kThreads;
-  // reuse: w.C (B*P u64) holds the per-tile scale (double) and w.sums the per-tile prefix
+  const int nt = (P + 31) / 32;
+  const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
+  // reuse w.C (B*P u64): [scale B*nt doubles][in-block prefixes B*nt][block prefixes B*nblk]
   double* scale = reinterpret_cast<double*>(w.C);
   uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + static_cast<size_t>(B) * nt;
-  tile_scale_prefix_kernel<<<B, 1024, 0, s>>>(nt, static_cast<const ssm_tile_rec*>(tile_rec), fs, scale,
-                                              pref, w.totals);
+  uint64_t* blk = pref + B_total_tiles_offset(nt, B);
+  tile_scale_kernel<<<dim3(nblk, B), kThreads, 0, s>>>(nt, static_cast<const ssm_tile_rec*>(tile_rec), fs,
+                                                      scale, pref, blk);
+  blk_prefix_kernel<<<B, 1024, 0, s>>>(nblk, blk, w.totals, fs);
   const int tiles = scan_tiles(P);
   const int nd = ndiag_of(P, P);
   const dim3 g(tiles, B);

@@ -221,7 +221,7 @@ class ParticleRun:
         self._a = None  # unnormalised log-weights of the last weighted step
         self._fs = None  # (64,) uint8 view of an ssm_filter_state
         self._cdf = None  # (P,) tile-local fixed-point CDF of the last weighted step
-        self._trec = None  # (ceil(P/256), 2) tile records {max, Q} of the last weighted step
+        self._trec = None  # (ceil(P/32), 2) warp-tile records {max, Q} of the last weighted step
         self._maybe_nonuniform = False
         self._derived = None
 
@@ -387,7 +387,7 @@ def advance_runs(runs, upto, rngs):
     rs_ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     # systematic / stratified resample from the pw kernel's tile-local CDF (no second pass over logw)
     tiles_ok = r0.resampler in ("systematic", "stratified")
-    ntile = (P + 255) // 256
+    ntile = (P + 31) // 32  # one tile record per warp tile
     cdf_local = tile_rec = None
     if tiles_ok:
         if runs[0]._cdf is not None:  # resume: fresh copies, so clones sharing the views stay intact

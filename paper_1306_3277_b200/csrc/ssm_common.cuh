@@ -151,7 +151,8 @@ __device__ __forceinline__ Lse lse_combine(Lse a, Lse b) {
     b = tmp;
   }
   if (b.m == a.m) return Lse{a.m, a.c + b.c, a.t + b.t, a.s2 + b.s2};
-  if (b.c == 0.0 && b.t == 0.0) return a;  // empty
+  if (b.c == 0.0 && b.t == 0.0) return a;  // empty (NaN t is not empty)
+  if (a.c == 0.0 && a.t == 0.0 && a.m == -CUDART_INF) return b;
   const double f = exp(b.m - a.m);         // NaN m -> NaN result
   return Lse{a.m, a.c, a.t + (b.c + b.t) * f, a.s2 + (b.c + b.s2) * (f * f)};
 }
@@ -178,8 +179,10 @@ __device__ __forceinline__ Lse lse_block_reduce(Lse s, Lse* smem /* NT/32 entrie
   return s;
 }
 
+// c > 0: scipy's log1p form (max elements split out); c == 0 (partials built
+// from fixed-point tile totals relative to a reference >= max): m + log(t).
 __device__ __forceinline__ double lse_value(const Lse& s) {
-  if (s.c == 0.0) return s.m;  // NaN or empty
+  if (s.c == 0.0) return s.t > 0.0 ? s.m + log(s.t) : (isnan(s.t) ? s.t : (s.t == 0.0 ? -CUDART_INF : s.m));
   return log1p(s.t / s.c) + log(s.c) + s.m;
 }
 

@@ -11,6 +11,8 @@
 // The LSE/ESS finalize runs in the last block to finish (completion counter),
 // combining per-block partials in block order -> deterministic.
 
+#include <climits>
+
 #include "ssm_common.cuh"
 
 namespace ssm {
@@ -147,7 +149,8 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const T logw0 = static_cast<T>(A.log_w0);
   const T obs_log_sd = static_cast<T>(A.obs_log_sd);
   const T lsp = static_cast<T>(A.log_sqrt_2pi);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const bool want_ess = A.ess_rel >= 0.0;
 
   Lse st = lse_empty();  // warp partial (lane 0), warp tiles folded in order
   bool bad = false;
@@ -231,38 +234,38 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
     }
     if (!has_obs) continue;  // block-uniform
 
-    // ---- warp tile (32 consecutive particles): max, fixed-point prefix, LSE/ESS partial.
-    // Shuffles only: no block barrier inside the particle loop, so warps stay
-    // out of phase and memory overlaps compute.
-    double mb = a_d;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double y = __shfl_xor_sync(0xffffffffu, mb, o);
-      mb = y > mb ? y : mb;  // NaN never wins; it poisons t below
-    }
-    const bool ismax = act && a_d == mb;
-    const double e = !act ? 0.0 : (ismax ? 1.0 : exp(a_d - mb));
+    // ---- warp tile (32 consecutive particles): reference max, fixed-point prefix,
+    // LSE/ESS partial.  One REDUX + one ballot + a 5-step u64 scan: no block
+    // barrier inside the particle loop, so warps stay out of phase.
+    // Reference m_w = float round-up of the tile max (>= every a_j, within 2^-24
+    // relative), so every e_j = exp(a_j - m_w) <= 1.
+    const float af = __double2float_ru(a_d);
+    const int key = __float_as_int(af) >= 0 ? __float_as_int(af) : (__float_as_int(af) ^ 0x7fffffff);
+    const int kmax = __reduce_max_sync(0xffffffffu, act ? key : INT_MIN);
+    const int kb = kmax >= 0 ? kmax : (kmax ^ 0x7fffffff);
+    const double mw = static_cast<double>(__int_as_float(kb));
+    const bool any_nan = __any_sync(0xffffffffu, act && isnan(a_d));
+    const double e = (!act || mw == -CUDART_INF) ? 0.0 : exp(a_d - mw);
     const uint64_t q = (e >= 0.0 && e <= 1.0) ? __double2ull_rn(e * kTileFix) : 0ull;
-    double c_ = ismax ? 1.0 : 0.0;
-    double t_ = (act && !ismax) ? e : 0.0;
-    double s2_ = t_ * t_;
     uint64_t qi = q;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint64_t y = __shfl_up_sync(0xffffffffu, qi, o);
       if (lane >= o) qi += y;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      c_ += __shfl_xor_sync(0xffffffffu, c_, o);
-      t_ += __shfl_xor_sync(0xffffffffu, t_, o);
-      s2_ += __shfl_xor_sync(0xffffffffu, s2_, o);
-    }
     if (cloc && act) cloc[p] = qi;
     const uint64_t Qw = __shfl_sync(0xffffffffu, qi, 31);
+    double s2_ = 0.0;
+    if (want_ess) {  // block-uniform
+      s2_ = e * e;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s2_ += __shfl_xor_sync(0xffffffffu, s2_, o);
+    }
     if (lane == 0) {
-      if (trec && p < P) trec[p >> 5] = ssm_tile_rec{mb, Qw};
-      st = lse_combine(st, Lse{mb, c_, t_, s2_});
+      if (trec && p < P) trec[p >> 5] = ssm_tile_rec{mw, Qw};
+      // tile sum of exp(a - m_w) from the exact fixed-point total (|err| <= 32 * 2^-53)
+      const double tsum = any_nan ? CUDART_NAN : static_cast<double>(Qw) * (1.0 / kTileFix);
+      st = lse_combine(st, Lse{mw, 0.0, tsum, s2_});
     }
   }
 

@@ -64,13 +64,13 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, uint32_t c, u
 
 // Box-Muller pair, float32 (the device noise generator for both precisions).
 // u1 = (a + 1/2) 2^-32 keeps 32 bits near 0, so |z| reaches 6.7 sigma; the
-// radius uses the accurate logf, the angle the MUFU sin/cos on [-pi, pi)
-// (|error| < 2^-21), a rotation by pi that leaves the pair iid N(0,1).
+// radius and angle use the MUFU lg2 / sin / cos (angle on [-pi, pi),
+// |error| < 2^-21; a rotation by pi leaves the pair iid N(0,1)).
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
   const float u1 = fmaf(static_cast<float>(a), 0x1.0p-32f, 0x1.0p-33f);  // (0, 1]
   const float th = fmaf(static_cast<float>(b >> 8), 6.28318530717958647692f * 0x1.0p-24f,
                         -3.14159265358979323846f);
-  const float r = sqrtf(-2.0f * logf(u1));
+  const float r = sqrtf(-2.0f * __logf(u1));  // MUFU.LG2
   float s, co;
   __sincosf(th, &s, &co);
   z0 = r * co;

@@ -103,6 +103,54 @@ __device__ __forceinline__ void l96_rk4(T x[8], T F, const T nt[8], T s) {
   }
 }
 
+// Fast (non-exact) float64 variant: same math, FMA-contracted and with the
+// forcing and noise folded per sub-step (Fn = F + sqrt(sigma2) W / h); within
+// 1e-12 norm-wise of the reference per step (tests/test_gpu_parity.py).
+template <typename T>
+__device__ __forceinline__ void l96_deriv_fast(const T x[8], const T Fn[8], T out[8]) {
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    const T xm1 = x[(n + 7) & 7], xp1 = x[(n + 1) & 7], xm2 = x[(n + 6) & 7];
+    out[n] = fma(xm1, xp1 - xm2, -x[n]) + Fn[n];
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void l96_rk4_fast(T x[8], const T Fn[8], T s) {
+  T k[8], acc[8], st[8];
+  const T hs = T(0.5) * s;
+  l96_deriv_fast<T>(x, Fn, k);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = k[n];
+    st[n] = fma(hs, k[n], x[n]);
+  }
+  l96_deriv_fast<T>(st, Fn, k);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = fma(T(2.0), k[n], acc[n]);
+    st[n] = fma(hs, k[n], x[n]);
+  }
+  l96_deriv_fast<T>(st, Fn, k);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = fma(T(2.0), k[n], acc[n]);
+    st[n] = fma(s, k[n], x[n]);
+  }
+  l96_deriv_fast<T>(st, Fn, k);
+  const T s6 = s * T(1.0 / 6.0);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) x[n] = fma(s6, acc[n] + k[n], x[n]);
+}
+
+// finite test on the exponent bits (integer pipe, keeps the FP64 pipe free)
+__device__ __forceinline__ bool finite_bits(double v) {
+  return (__double2hiint(v) & 0x7ff00000) != 0x7ff00000;
+}
+__device__ __forceinline__ bool finite_bits(float v) {
+  return (__float_as_int(v) & 0x7f800000) != 0x7f800000;
+}
+
 // ----------------------------- the kernel ----------------------------------
 //
 // Grid-stride over 256-particle block tiles; one particle per thread per tile.
@@ -156,22 +204,33 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   bool bad = false;
   int bad_sub = 0;
 
+  // software pipeline: the ancestor index and gathered state of the block's
+  // next tile are loaded while the current tile computes
+  T xn[NX];
+  auto load_state = [&](int pp) {
+    const int src = anc ? __ldg(anc + pp) : pp;
+#pragma unroll
+    for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * P + src];
+  };
+  if (blockIdx.x * kThreads + threadIdx.x < P) load_state(blockIdx.x * kThreads + threadIdx.x);
+  const T gconst = static_cast<T>(static_cast<double>(__popc(A.obs_mask)) * (A.obs_log_sd + A.log_sqrt_2pi));
+
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int p = tile * kThreads + threadIdx.x;
     const bool act = p < P;
     double a_d = -CUDART_INF;
-    if (act) {
-      const int src = anc ? anc[p] : p;
-      T x[NX];
+    T x[NX];
 #pragma unroll
-      for (int n = 0; n < NX; ++n) x[n] = xin[static_cast<size_t>(n) * P + src];
-
+    for (int n = 0; n < NX; ++n) x[n] = xn[n];
+    {
+      const int p2 = p + gridDim.x * kThreads;
+      if (tile + static_cast<int>(gridDim.x) < ntiles && p2 < P) load_state(p2);
+    }
+    if (act) {
       for (int k = 0; k < A.n_sub; ++k) {
         const ssm_substep& S = A.subs[k];
         if constexpr (MODEL == SSM_MODEL_LORENZ96) {
-          const T F = static_cast<T>(th[0]);
-          const T sq = static_cast<T>(th[1]);  // np.sqrt(sigma2), host-computed
-          T W[8], nt[8];
+          T W[8];
           if constexpr (INJ) {
 #pragma unroll
             for (int n = 0; n < 8; ++n) W[n] = noise[(static_cast<size_t>(k) * 8 + n) * P + p];
@@ -182,10 +241,21 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
 #pragma unroll
             for (int n = 0; n < 8; ++n) W[n] = sd * W[n];
           }
+          if constexpr (E) {
+            const T F = static_cast<T>(th[0]);
+            const T sq = static_cast<T>(th[1]);  // np.sqrt(sigma2), host-computed
+            T nt[8];
 #pragma unroll
-          for (int n = 0; n < 8; ++n)
-            nt[n] = E ? O::div(O::mul(sq, W[n]), T(0.05)) : O::mul(O::mul(sq, W[n]), T(20.0));
-          for (int m = 0; m < S.n_ode; ++m) l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
+            for (int n = 0; n < 8; ++n) nt[n] = O::div(O::mul(sq, W[n]), T(0.05));
+            for (int m = 0; m < S.n_ode; ++m) l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
+          } else {
+            const T F = static_cast<T>(th[0]);
+            const T sqh = static_cast<T>(th[1] * 20.0);  // sqrt(sigma2) / h
+            T Fn[8];
+#pragma unroll
+            for (int n = 0; n < 8; ++n) Fn[n] = fma(sqh, W[n], F);
+            for (int m = 0; m < S.n_ode; ++m) l96_rk4_fast<T>(x, Fn, static_cast<T>(S.s[m]));
+          }
         } else {
           // Windkessel.bi:28-29, Pp <- exp(-h/(R*C))*Pp + R*(1 - exp(-h/(R*C)))*(F + xi)
           const T ca = static_cast<T>(th[0]), cb = static_cast<T>(th[1]);
@@ -201,7 +271,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
         if (A.check_finite && !bad) {
           bool ok = true;
 #pragma unroll
-          for (int n = 0; n < NX; ++n) ok &= finite(x[n]);
+          for (int n = 0; n < NX; ++n) ok &= finite_bits(x[n]);
           if (!ok) {
             bad = true;
             bad_sub = k;
@@ -214,12 +284,23 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
       if (has_obs) {
         T g = T(0);
         if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+          if constexpr (E) {
 #pragma unroll
-          for (int n = 0; n < 8; ++n) {
-            if (A.obs_mask & (1u << n)) {
-              const T z = O::mul(O::sub(static_cast<T>(A.y[n]), x[n]), T(2.0));  // exact: / 0.5
-              g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
+            for (int n = 0; n < 8; ++n) {
+              if (A.obs_mask & (1u << n)) {
+                const T z = O::mul(O::sub(static_cast<T>(A.y[n]), x[n]), T(2.0));  // exact: / 0.5
+                g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
+              }
             }
+          } else {
+#pragma unroll
+            for (int n = 0; n < 8; ++n) {
+              if (A.obs_mask & (1u << n)) {
+                const T z = (static_cast<T>(A.y[n]) - x[n]) * T(2.0);
+                g = fma(T(-0.5) * z, z, g);
+              }
+            }
+            g -= gconst;
           }
         } else {
           const T mean = O::add(x[0], O::mul(static_cast<T>(th[2]), static_cast<T>(A.u_obs)));

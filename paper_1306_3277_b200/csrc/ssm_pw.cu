@@ -204,15 +204,18 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   bool bad = false;
   int bad_sub = 0;
 
-  // software pipeline: the ancestor index and gathered state of the block's
-  // next tile are loaded while the current tile computes
+  // software pipeline: the gathered state of the block's next tile and the
+  // ancestor index of the tile after it are in flight while the current tile
+  // computes (the anc -> x dependent loads never stall an iteration)
   T xn[NX];
-  auto load_state = [&](int pp) {
-    const int src = anc ? __ldg(anc + pp) : pp;
+  const int stride = gridDim.x * kThreads;
+  const int p0 = blockIdx.x * kThreads + threadIdx.x;
+  auto load_x = [&](int pp, int src) {
 #pragma unroll
     for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * P + src];
   };
-  if (blockIdx.x * kThreads + threadIdx.x < P) load_state(blockIdx.x * kThreads + threadIdx.x);
+  if (p0 < P) load_x(p0, anc ? __ldg(anc + p0) : p0);
+  int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride;
   const T gconst = static_cast<T>(static_cast<double>(__popc(A.obs_mask)) * (A.obs_log_sd + A.log_sqrt_2pi));
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -223,8 +226,10 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
 #pragma unroll
     for (int n = 0; n < NX; ++n) x[n] = xn[n];
     {
-      const int p2 = p + gridDim.x * kThreads;
-      if (tile + static_cast<int>(gridDim.x) < ntiles && p2 < P) load_state(p2);
+      const int p2 = p + stride;
+      if (p2 < P) load_x(p2, anc_next);
+      const int p3 = p2 + stride;
+      anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
     }
     if (act) {
       for (int k = 0; k < A.n_sub; ++k) {

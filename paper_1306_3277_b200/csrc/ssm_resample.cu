@@ -550,10 +550,23 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
                                   blk_pre[static_cast<size_t>(b) * nblk + tw / kRecPerBlock]
                             : 0ull;
     const double inv = 1.0 / static_cast<double>(totals[b]);
+    uint64_t lv[kScanItems];
+    if (jt + kScanItems <= P_in && (P_in & 7) == 0) {  // 4 x 16-byte vector loads, aligned
+      const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(cl + jt);
+#pragma unroll
+      for (int i = 0; i < kScanItems / 2; ++i) {
+        const ulonglong2 t2 = __ldg(v2 + i);
+        lv[2 * i] = t2.x;
+        lv[2 * i + 1] = t2.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kScanItems; ++i) lv[i] = jt + i < P_in ? cl[jt + i] : 0ull;
+    }
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
       const int j = jt + i;
-      cum[i] = j < P_in ? static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(cl[j]))) * inv : 2.0;
+      cum[i] = j < P_in ? static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(lv[i]))) * inv : 2.0;
       if (j == P_in - 1) cum[i] = 1.0;  // cum[-1] = 1.0 (resampling.py:27)
     }
     cum_prev = jt == 0 ? 0.0
@@ -643,17 +656,27 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
     c_prev = c;
   }
   (void)total;
+  if (jt + kScanItems <= P_in && (P_in & 7) == 0) {  // two 16-byte vector stores, aligned
+    int4* c4 = reinterpret_cast<int4*>(cb + jt);
+    c4[0] = make_int4(cvals[0], cvals[1], cvals[2], cvals[3]);
+    c4[1] = make_int4(cvals[4], cvals[5], cvals[6], cvals[7]);
+  } else {
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i)
-    if (jt + i < P_in) cb[jt + i] = cvals[i];
+    for (int i = 0; i < kScanItems; ++i)
+      if (jt + i < P_in) cb[jt + i] = cvals[i];
+  }
 }
 
-// anc_k = #{j : c_j <= k}, clipped to P_in - 1, from the precomputed partition
+// anc_k = #{j : c_j <= k}, clipped to P_in - 1, from the precomputed partition.
+// Balanced without searches: the block's particles [i0, i1] each mark the first
+// output of their offspring run inside [kb0, kb1); an inclusive max-scan of
+// the marks then assigns every output its owner.  Work per thread: kScanItems
+// particles + kScanItems outputs.
 __global__ void __launch_bounds__(kThreads)
 expand_kernel(int P_in, int P_out, const int32_t* __restrict__ cnt, const int32_t* __restrict__ split,
               int ndiag, const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc) {
-  __shared__ int32_t sA[kDiag];
-  __shared__ int32_t sOut[kDiag];
+  __shared__ int32_t sMark[kDiag];
+  __shared__ int32_t warp_max[kThreads / 32];
   const int b = blockIdx.y, t = blockIdx.x;
   int32_t* ab = anc + static_cast<size_t>(b) * P_out;
   const int total = P_in + P_out;
@@ -668,35 +691,63 @@ expand_kernel(int P_in, int P_out, const int32_t* __restrict__ cnt, const int32_
   const int32_t* cb = cnt + static_cast<size_t>(b) * P_in;
   const int i0 = sp[t], i1 = sp[t + 1];
   const int kb0 = D0 - i0, kb1 = D1 - i1;
-  const int na = i1 - i0, nb = kb1 - kb0;
-  for (int q = threadIdx.x; q < na; q += kThreads) sA[q] = cb[i0 + q];
+  const int nb = kb1 - kb0;  // outputs of this block (<= kDiag)
+  if (nb <= 0) return;
+  for (int q = threadIdx.x; q < nb; q += kThreads) sMark[q] = -1;
   __syncthreads();
-  const int dl = threadIdx.x * kMergeItems;
-  if (dl < na + nb) {
-    // thread split: particles among the first dl merged elements (c_j <= k precedes output k)
-    int lo = dl > nb ? dl - nb : 0, hi = dl < na ? dl : na;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (sA[mid] <= kb0 + (dl - 1 - mid))
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    int ia = lo, kb = dl - lo;
-    const int lim = min(dl + kMergeItems, na + nb);
-    for (int e = dl; e < lim; ++e) {
-      if (ia < na && (kb >= nb || sA[ia] <= kb0 + kb)) {
-        ++ia;
-      } else {
-        const int a_idx = i0 + ia;
-        sOut[kb] = a_idx < P_in ? a_idx : P_in - 1;  // .clip(0, P-1)
-        ++kb;
-      }
+  // particles i0 .. min(i1, P_in - 1): mark run starts clamped into the block
+  const int jlast = i1 < P_in ? i1 : P_in - 1;
+  for (int j = i0 + threadIdx.x; j <= jlast; j += kThreads) {
+    const int c_lo = j > 0 ? __ldg(cb + j - 1) : 0;
+    const int c_hi = __ldg(cb + j);
+    const int st = c_lo > kb0 ? c_lo : kb0;
+    const int en = c_hi < kb1 ? c_hi : kb1;
+    if (st < en) sMark[st - kb0] = j;
+  }
+  // outputs past the last particle's run belong to P_in -> clipped to P_in - 1
+  if (threadIdx.x == 0 && i1 >= P_in) {
+    const int c_last = __ldg(cb + P_in - 1);
+    const int st = c_last > kb0 ? c_last : kb0;
+    if (st < kb1 && sMark[st - kb0] < 0) sMark[st - kb0] = P_in - 1;
+  }
+  __syncthreads();
+  // block inclusive max-scan over the marks (kScanItems consecutive per thread)
+  int v[kScanItems];
+  int run = -1;
+  const int e0 = threadIdx.x * kScanItems;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int e = e0 + i;
+    const int m = e < nb ? sMark[e] : -1;
+    run = m > run ? m : run;
+    v[i] = run;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = y > incl ? y : incl;
+  }
+  if (lane == 31) warp_max[warp] = incl;
+  int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = -1;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w)
+    if (w < warp) excl = warp_max[w] > excl ? warp_max[w] : excl;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int e = e0 + i;
+    if (e < nb) {
+      const int a_idx = v[i] > excl ? v[i] : excl;
+      sMark[e] = a_idx < P_in ? a_idx : P_in - 1;
     }
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < nb; q += kThreads) ab[kb0 + q] = sOut[q];
+  for (int q = threadIdx.x; q < nb; q += kThreads) ab[kb0 + q] = sMark[q];
 }
+
 
 template <int KIND>
 __global__ void __launch_bounds__(kThreads)

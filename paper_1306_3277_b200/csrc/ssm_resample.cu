@@ -675,7 +675,7 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
 __global__ void __launch_bounds__(kThreads)
 expand_kernel(int P_in, int P_out, const int32_t* __restrict__ cnt, const int32_t* __restrict__ split,
               int ndiag, const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc) {
-  __shared__ int32_t sMark[kDiag];
+  __shared__ int32_t sMark[kDiag + kDiag / 8];  // padded: e -> e + e/8 (conflict-free sequential scan)
   __shared__ int32_t warp_max[kThreads / 32];
   const int b = blockIdx.y, t = blockIdx.x;
   int32_t* ab = anc + static_cast<size_t>(b) * P_out;
@@ -693,7 +693,7 @@ expand_kernel(int P_in, int P_out, const int32_t* __restrict__ cnt, const int32_
   const int kb0 = D0 - i0, kb1 = D1 - i1;
   const int nb = kb1 - kb0;  // outputs of this block (<= kDiag)
   if (nb <= 0) return;
-  for (int q = threadIdx.x; q < nb; q += kThreads) sMark[q] = -1;
+  for (int q = threadIdx.x; q < nb; q += kThreads) sMark[q + (q >> 3)] = -1;
   __syncthreads();
   // particles i0 .. min(i1, P_in - 1): mark run starts clamped into the block
   const int jlast = i1 < P_in ? i1 : P_in - 1;
@@ -702,13 +702,14 @@ expand_kernel(int P_in, int P_out, const int32_t* __restrict__ cnt, const int32_
     const int c_hi = __ldg(cb + j);
     const int st = c_lo > kb0 ? c_lo : kb0;
     const int en = c_hi < kb1 ? c_hi : kb1;
-    if (st < en) sMark[st - kb0] = j;
+    if (st < en) sMark[(st - kb0) + ((st - kb0) >> 3)] = j;
   }
   // outputs past the last particle's run belong to P_in -> clipped to P_in - 1
   if (threadIdx.x == 0 && i1 >= P_in) {
     const int c_last = __ldg(cb + P_in - 1);
     const int st = c_last > kb0 ? c_last : kb0;
-    if (st < kb1 && sMark[st - kb0] < 0) sMark[st - kb0] = P_in - 1;
+    const int q = st - kb0;
+    if (st < kb1 && sMark[q + (q >> 3)] < 0) sMark[q + (q >> 3)] = P_in - 1;
   }
   __syncthreads();
   // block inclusive max-scan over the marks (kScanItems consecutive per thread)
@@ -718,7 +719,7 @@ expand_kernel(int P_in, int P_out, const int32_t* __restrict__ cnt, const int32_
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     const int e = e0 + i;
-    const int m = e < nb ? sMark[e] : -1;
+    const int m = e < nb ? sMark[e + (e >> 3)] : -1;
     run = m > run ? m : run;
     v[i] = run;
   }
@@ -741,11 +742,11 @@ expand_kernel(int P_in, int P_out, const int32_t* __restrict__ cnt, const int32_
     const int e = e0 + i;
     if (e < nb) {
       const int a_idx = v[i] > excl ? v[i] : excl;
-      sMark[e] = a_idx < P_in ? a_idx : P_in - 1;
+      sMark[e + (e >> 3)] = a_idx < P_in ? a_idx : P_in - 1;
     }
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < nb; q += kThreads) ab[kb0 + q] = sMark[q];
+  for (int q = threadIdx.x; q < nb; q += kThreads) ab[kb0 + q] = sMark[q + (q >> 3)];
 }
 
 

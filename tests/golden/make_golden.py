@@ -339,6 +339,62 @@ def gen_theta_level():
     save("theta.npz", **out)
 
 
+def gen_outer_loops():
+    """Reference PMMH (mh_sample) and SMC^2 (smc_sampler) at toy sizes on L96
+    sparse data (4 of 8 slots, every other step, T=10), and windkessel PMMH
+    (needs the `inf` shim)."""
+    from ssmkit.inference import FilterRunner, mh_sample, smc_sampler
+
+    out = {}
+    ir, theta, times, ot, ov, om = l96_data(obs_every=2, slots=range(4), T=10)
+    grid = build_filter_grid(0.0, times[-1], 10, ot, ov, om, n_obs=8)
+    out["l96/times"] = times
+    out["l96/obs_v"] = ov
+    out["l96/obs_m"] = om
+    runner = FilterRunner(ir, grid, n_particles=64, resampler="systematic")
+    chains, acc = mh_sample(ir, runner, 6, RngStream(21))
+    out["l96/mh/thetas"] = np.array([c.theta for c in chains])
+    out["l96/mh/logliks"] = np.array([c.loglik for c in chains])
+    out["l96/mh/inits"] = np.array([c.init_state for c in chains])
+    out["l96/mh/traj_last"] = chains[-1].trajectory
+    out["l96/mh/accepted"] = np.array(acc)
+    res = smc_sampler(ir, runner, 6, RngStream(22), theta_resampler="systematic")
+    out["l96/smc/thetas"] = res.thetas
+    out["l96/smc/log_v"] = res.log_v
+    out["l96/smc/logliks"] = res.logliks
+    out["l96/smc/trajectories"] = res.trajectories
+    out["l96/smc/ess"] = np.array([d["ess"] for d in res.diagnostics])
+    out["l96/smc/acceptance"] = np.array([d["acceptance"] for d in res.diagnostics])
+
+    import ssmkit.core.ir as I
+
+    I.compile_expr = lambda e, t, b: eval(
+        f"lambda T, X, W, U: {I.expr_source(e, t, b)}", {"np": np, "inf": np.inf, "__builtins__": {}}
+    )
+    ir = load("windkessel")
+    theta = np.array([1.8, 3.0, 0.06, 25.0])
+    in_times = np.round(np.arange(0, 1.0001, 0.01), 10)
+    inputs = LocfInputs(in_times, flow(in_times)[:, None])
+    times = np.linspace(0.0, 0.4, 41)
+    rng = RngStream(1)
+    x = simulate.sample_initial(ir, theta, rng.child(1), size=1)
+    obs = []
+    for k in range(1, len(times)):
+        x = simulate.step_transition(ir, theta, x, inputs, times[k - 1], times[k] - times[k - 1], rng.child(2, k))
+        obs.append(simulate.simulate_obs(ir, theta, x, inputs.at(times[k]), rng.child(3, k))[0])
+    obs = np.array(obs)
+    grid = build_filter_grid(0.0, 0.4, 40, times[1:], obs, np.ones((40, 1), bool), n_obs=1)
+    out["wk/in_times"] = in_times
+    out["wk/in_values"] = flow(in_times)
+    out["wk/obs_v"] = obs
+    runner = FilterRunner(ir, grid, inputs=inputs, n_particles=128, resampler="systematic")
+    chains, acc = mh_sample(ir, runner, 6, RngStream(23))
+    out["wk/mh/thetas"] = np.array([c.theta for c in chains])
+    out["wk/mh/logliks"] = np.array([c.loglik for c in chains])
+    out["wk/mh/accepted"] = np.array(acc)
+    save("outer.npz", **out)
+
+
 if __name__ == "__main__":
     gen_resample()
     gen_lse()
@@ -346,3 +402,4 @@ if __name__ == "__main__":
     gen_wk_step()
     gen_pf()
     gen_theta_level()
+    gen_outer_loops()

@@ -131,7 +131,7 @@ def run_ours(args, rank, world):
     P, T = args.particles, args.T
     times, ot, ov, om = synthetic_data(T)
     grid = build_filter_grid(0.0, times[-1], T, ot, ov, om, n_obs=8)
-    opts = dict(dtype=args.dtype, exact=not args.fast, noise="device")
+    opts = dict(dtype=args.dtype, exact=args.exact, noise="device")
 
     def one(step, grid_obj, timer=None):
         rng = RngStream(7, (rank, step))
@@ -273,7 +273,9 @@ def main():
     ap.add_argument("--particles", type=int, default=P_BENCH)
     ap.add_argument("--T", type=int, default=T_BENCH)
     ap.add_argument("--dtype", default="float64", choices=["float64", "float32"])
-    ap.add_argument("--fast", action="store_true", help="FMA-contracted arithmetic (not bitwise)")
+    ap.add_argument("--exact", action="store_true",
+                    help="bitwise reference op order (no FMA contraction); default: FMA-contracted float64")
+    ap.add_argument("--variants", type=int, default=1, help="also time f64-exact and f32 variants")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--ref-particles", type=int, default=1 << 17)
@@ -311,6 +313,7 @@ def main():
     kern = {k: {"avg_ms": round(v["avg_ms"], 4), "launches": v["launches"],
                 "GB/s": round(v["bytes"] / (v["total_ms"] / 1e3) / 1e9, 1)} for k, v in res["kern"].items()}
     dtype_tag = "f64" if args.dtype == "float64" else "f32"
+    arith = "bitwise reference op order" if args.exact else "float64 with FMA contraction (1e-12 of reference per step)"
     line = {
         "metric": METRIC,
         "value": value,
@@ -324,7 +327,7 @@ def main():
         "vs_baseline": None,
         "dtype": dtype_tag,
         "data": "synthetic (L96 theta*=(10,0.1) simulated per SURVEY 8d; device Philox noise)",
-        "config": workload_config(P, T, args.dtype),
+        "config": dict(workload_config(P, T, args.dtype), arithmetic=arith),
         "roofline": {
             "bound": "hbm",
             "kernel": "pw_kernel (fused ancestor gather + RK4 propagate + weight + LSE)",
@@ -345,6 +348,18 @@ def main():
         line["e2e"] = {"value": world * P * T / (res["e2e_ms"] / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
                        "ms_per_step": res["e2e_ms"]}
+    if args.variants and world == 1:
+        line["variants"] = {}
+        for name, dt, ex in (("f64_exact_bitwise", "float64", True), ("f32", "float32", False)):
+            if (dt, ex) == (args.dtype, args.exact):
+                continue
+            v_args = argparse.Namespace(**vars(args))
+            v_args.dtype, v_args.exact, v_args.e2e_steps = dt, ex, 0
+            v = run_ours(v_args, rank, world)
+            vpw = v["kern"].get("propagate_weight", {})
+            line["variants"][name] = {
+                "value": P * T * K / (v["ms"] / 1e3), "ms_per_step": v["ms"] / K,
+                "pw_GB_s": vpw["bytes"] / (vpw["total_ms"] / 1e3) / 1e9 if vpw else None}
     if args.cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_single()
     print(json.dumps(line), flush=True)

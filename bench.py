@@ -71,25 +71,32 @@ def workload_config(P, T, dtype):
 
 
 class ClockSampler:
+    """nvidia-smi sampled every 100 ms from before warm-up; summary() keeps the
+    samples whose timestamps fall inside [t0, t1] (the timed region)."""
+
+    FIELDS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
     def __init__(self, index=0):
         self.index = index
         self.proc = None
         self.lines = []
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+        time.sleep(0.3)
         return self
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            time.sleep(0.25)
             self.proc.terminate()
             try:
                 out, _ = self.proc.communicate(timeout=5)
@@ -98,23 +105,32 @@ class ClockSampler:
                 out = ""
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
-    def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    def summary(self, t0=None, t1=None):
+        import datetime
+
+        sm, mx, reasons, power = [], 0.0, set(), []
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = max(mx, float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            if t0 is not None and ts is not None and not (t0 - 0.15 <= ts <= t1 + 0.15):
+                continue
+            try:
+                sm.append(float(f[2]))
+                mx = max(mx, float(f[3]))
+                power.append(float(f[4]))
             except ValueError:
                 continue
-            for name, v in zip(names, f[5:9]):
+            for name, v in zip(self.FIELDS, f[6:10]):
                 if v.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
 
 
 # ------------------------------------------------------------------ our arm
@@ -149,16 +165,17 @@ def run_ours(args, rank, world):
             tdist.barrier()
         torch.cuda.synchronize()
 
-    for w in range(args.warmup):
-        out = one(10**6 + w, grid)
-    del out
-    # ---- device-timed region: K steps, inputs resident, events on the launching stream
     timer = profiling.KernelTimer()
-    barrier()
-    n0 = profiling.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     logliks = []
     with ClockSampler(dev.index) as clocks:
+        for w in range(args.warmup):
+            out = one(10**6 + w, grid)
+        del out
+        # ---- device-timed region: K steps, inputs resident, events on the launching stream
+        barrier()
+        n0 = profiling.launch_count()
+        t_wall0 = time.time()
         start.record()
         for k in range(args.steps):
             out = one(k, grid, timer)
@@ -166,6 +183,7 @@ def run_ours(args, rank, world):
             del out
         end.record()
         barrier()
+        t_wall1 = time.time()
     launches = profiling.launch_count() - n0
     ms = start.elapsed_time(end)
     kern = timer.summary()
@@ -190,7 +208,7 @@ def run_ours(args, rank, world):
         t = torch.tensor([ms, e2e_ms or 0.0], device=dev)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         ms, e2e_ms = float(t[0]), (float(t[1]) if e2e_ms is not None else None)
-    return dict(ms=ms, kern=kern, launches=launches, clocks=clocks.summary(), logliks=logliks,
+    return dict(ms=ms, kern=kern, launches=launches, clocks=clocks.summary(t_wall0, t_wall1), logliks=logliks,
                 e2e_ms=e2e_ms, h2d=h2d, d2h=d2h)
 
 
@@ -208,7 +226,7 @@ def _cpu_filter_task(a):
     return time.perf_counter() - t0
 
 
-def cpu_baseline_single(P=1 << 18, T=8):
+def cpu_baseline_single(P=1 << 20, T=10):
     """The oracle port on one host core (numpy is single-threaded here)."""
     dt = _cpu_filter_task((P, T, 0))
     return {"value": P * T / dt, "unit": UNIT, "cores": 1, "kind": "port",
@@ -267,7 +285,7 @@ def load_traffic():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--particles", type=int, default=P_BENCH)

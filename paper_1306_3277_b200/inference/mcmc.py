@@ -173,18 +173,65 @@ def mh_sample(ir, runner, n_samples, rng):
     return chains[0], int(acc[0])
 
 
-def mh_sample_chains(ir, runner, n_samples, rngs, upto=None, on_step=None):
+def mh_sample_chains(ir, runner, n_samples, rngs, upto=None, on_step=None, shard=None):
     """C independent PMMH chains advanced in lock-step (batched filters).
-    Chain c reproduces mh_sample(ir, runner, n_samples, rngs[c])."""
-    states = init_chains(ir, runner, [g.child(0) for g in rngs], upto=upto)
-    samples = [[] for _ in rngs]
-    accepted = np.zeros(len(rngs), dtype=int)
-    for step in range(1, n_samples + 1):
-        outs = marginal_mh_steps(ir, states, runner, [g.child(step) for g in rngs], upto=upto)
-        for c, (st, ok, _) in enumerate(outs):
-            states[c] = st
-            accepted[c] += int(ok)
-            samples[c].append(st)
-        if on_step is not None:
-            on_step(step, states)
-    return samples, accepted
+    Chain c reproduces mh_sample(ir, runner, n_samples, rngs[c]).
+
+    Multi-GPU (config 3): with a `Shard` (default: torch.distributed
+    if initialised) each rank runs its contiguous block of chains as
+    independent replicas; the samples are all-gathered at the end (C4), so
+    every rank returns all C chains."""
+    from ..distributed import Shard, allgather_f64, shard_bounds
+
+    shard = shard or Shard.current()
+    C = len(rngs)
+    lo, hi = shard.bounds(C)
+    mine = list(rngs[lo:hi])
+    samples = [[] for _ in mine]
+    accepted = np.zeros(len(mine), dtype=int)
+    if mine:
+        states = init_chains(ir, runner, [g.child(0) for g in mine], upto=upto)
+        for step in range(1, n_samples + 1):
+            outs = marginal_mh_steps(ir, states, runner, [g.child(step) for g in mine], upto=upto)
+            for c, (st, ok, _) in enumerate(outs):
+                states[c] = st
+                accepted[c] += int(ok)
+                samples[c].append(st)
+            if on_step is not None:
+                on_step(step, states)
+    if shard.world == 1:
+        return samples, accepted
+    # C4: gather every chain's record (theta, loglik, log_prior, x0, trajectory) to every rank
+    spec = resolve_model(ir)
+    S1 = runner.grid.last + 1 if upto is None else upto + 1
+    nx0 = spec.nx if spec.has_proposal_initial else 0
+    rec = spec.n_param + 2 + nx0 + S1 * spec.nx
+    flat = []
+    for ch in samples:
+        for st in ch:
+            parts = [st.theta, [st.loglik, st.log_prior]]
+            if nx0:
+                parts.append(st.init_state)
+            parts.append(st.trajectory.reshape(-1))
+            flat.append(np.concatenate([np.asarray(q, dtype=float).reshape(-1) for q in parts]))
+    counts = [(shard_bounds(C, r, shard.world)[1] - shard_bounds(C, r, shard.world)[0]) * n_samples * rec
+              for r in range(shard.world)]
+    allrec = allgather_f64(np.concatenate(flat) if flat else np.zeros(0), shard, counts).reshape(C, n_samples, rec)
+    acc_all = allgather_f64(accepted.astype(float), shard,
+                            [shard_bounds(C, r, shard.world)[1] - shard_bounds(C, r, shard.world)[0]
+                             for r in range(shard.world)]).astype(int)
+    out = []
+    for c in range(C):
+        chain = []
+        for k in range(n_samples):
+            v = allrec[c, k]
+            th = v[: spec.n_param].copy()
+            q = spec.n_param
+            ll, lp = float(v[q]), float(v[q + 1])
+            q += 2
+            x0 = v[q : q + nx0].copy() if nx0 else None
+            q += nx0
+            chain.append(MhChainState(theta=th, trajectory=v[q:].reshape(S1, spec.nx).copy(), loglik=ll,
+                                      log_prior=lp, init_state=x0))
+        out.append(chain)
+    return out, acc_all

@@ -3,14 +3,19 @@ filter inside (the reference's inference/smc.py:67-171 API).
 
 The reference maps rejuvenation and propagation over theta-particles with a
 GIL-bound thread pool (smc.py:60-64).  Here every phase is one batched
-device launch per grid step over all theta-particles:
-  * theta-resampling: `resample` on the device; clones share history
-    (ParticleRun.clone is copy-on-advance);
-  * rejuvenation: all proposals replayed from t0 to the previous
-    observation in ONE batched filter (the O(T^2) part, smc.py:100-122);
+device launch per grid step over the theta-particles a rank owns:
+  * theta-resampling: `resample` on the device, identical on every rank;
+    local clones share history (ParticleRun.clone is copy-on-advance);
+  * rejuvenation: all proposals replayed from t0 to the previous observation
+    in ONE batched filter (the O(T^2) part, smc.py:100-122);
   * propagation: all attached filters advanced together (smc.py:125-134).
-Draws use the reference's stream keys (step_rng.child(...)) so the result is
-independent of batching, like the reference's independence of nthreads.
+Multi-GPU: theta slots are sharded contiguously over
+ranks.  Per observation step there is one all-gather of the theta
+log-weights (C2) and one redistribution of the theta-particles whose
+ancestor lives on another rank (C3: host fields + filter state + history,
+NCCL point-to-point).  Draws are keyed by the global slot index
+(step_rng.child(...)), so results do not depend on the number of ranks,
+just as the reference's do not depend on nthreads.
 """
 
 from __future__ import annotations
@@ -18,19 +23,24 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 import numpy as np
+import torch
 
+from .. import _lib
+from ..distributed import Shard, allgather_f64, exchange, plan_redistribution
 from ..errors import DegenerateEnsembleError
 from ..models import resolve_model
 from .mcmc import MhChainState, _chain_log_prior, marginal_mh_steps
-from .particle import advance_runs, sample_trajectories
+from .particle import _dtype_info, advance_runs, sample_trajectories
 from .resampling import resample
 
 
 def _logsumexp(a):
     a = np.asarray(a, dtype=float)
     m = np.max(a)
+    if np.isnan(m):
+        return float("nan")
     if not np.isfinite(m):
-        return float(m) if m == np.inf else float("-inf") if np.all(a == -np.inf) else float("nan")
+        return float(m)
     return float(m + np.log(np.sum(np.exp(a - m))))
 
 
@@ -55,12 +65,12 @@ class SmcResult:
     log_v: np.ndarray
     logliks: np.ndarray
     trajectories: np.ndarray
-    particles: list = field(default_factory=list)
+    particles: list = field(default_factory=list)  # this rank's theta-particles
     diagnostics: list = field(default_factory=list)
 
 
 def _advance_all(runner, particles, js, upto, run_rngs, init_rngs, traj_rngs):
-    """Create missing runs, advance all to `upto` in one batch, refresh trajectories."""
+    """Create missing runs, advance all to `upto` in batches by position, refresh trajectories."""
     missing = [j for j in js if particles[j].run is None]
     if missing:
         runs = runner.new_runs([particles[j].theta for j in missing],
@@ -68,7 +78,6 @@ def _advance_all(runner, particles, js, upto, run_rngs, init_rngs, traj_rngs):
                                [init_rngs[j] for j in missing])
         for j, r in zip(missing, runs):
             particles[j].run = r
-    # group by position (all equal in practice)
     incr = {}
     by_pos = {}
     for j in js:
@@ -77,65 +86,182 @@ def _advance_all(runner, particles, js, upto, run_rngs, init_rngs, traj_rngs):
         inc = advance_runs([particles[j].run for j in group], upto, [run_rngs[j] for j in group])
         for j, v in zip(group, inc):
             incr[j] = float(v)
-    if traj_rngs is not None:
+    if traj_rngs is not None and js:
         trajs = sample_trajectories([particles[j].run for j in js], [traj_rngs[j] for j in js])
         for j, t in zip(js, trajs):
             particles[j].trajectory = t
     return incr
 
 
-def smc_sampler(ir, runner, n_theta, rng, theta_resampler="multinomial", nthreads=1):
-    """smc.py:67-171 on the GPU (nthreads is accepted for API compatibility;
-    the batch is the parallelism)."""
+# ---------------------------------------------------------------- C3 payloads
+
+
+def _payload_specs(spec, runner, have_run, pos, traj_len, P, tdtype):
+    n_host = spec.n_param + 2 + (traj_len * spec.nx) + (spec.nx if spec.has_proposal_initial else 0) + 3
+    specs = [((n_host,), torch.float64)]
+    if have_run:
+        specs += [((pos + 1, spec.nx, P), tdtype), ((max(pos, 1), P), torch.int32), ((P,), tdtype),
+                  ((64,), torch.uint8)]
+        if runner.resampler in ("systematic", "stratified"):
+            specs += [((P,), torch.int64), (((P + 31) // 32, 2), torch.float64)]
+    return specs
+
+
+def _pack(spec, runner, p, traj_len):
+    host = [p.theta, [p.log_prior, p.loglik]]
+    host.append(p.trajectory.reshape(-1) if traj_len else [])
+    if spec.has_proposal_initial:
+        host.append(p.init_state)
+    r = p.run
+    host.append([float(r.pos) if r else 0.0, float(r.weights_uniform) if r else 1.0,
+                 float(r._maybe_nonuniform) if r else 0.0])
+    out = [torch.from_numpy(np.concatenate([np.asarray(h, dtype=np.float64).reshape(-1) for h in host]))]
+    if r is not None:
+        P = r.n_particles
+        hx = torch.stack([h[0] for h in r.history])
+        ar = torch.arange(P, dtype=torch.int32, device=r.device)
+        ha = torch.stack([h[1] if h[1] is not None else ar for h in r.history[1:]]) if r.pos > 0 else ar[None]
+        a = r._a if r._a is not None else torch.zeros(P, dtype=r.tdtype, device=r.device)
+        out += [hx, ha, a, r._fs.contiguous()]
+        if runner.resampler in ("systematic", "stratified"):
+            out += [r._cdf if r._cdf is not None else torch.zeros(P, dtype=torch.int64, device=r.device),
+                    r._trec if r._trec is not None else torch.zeros(((P + 31) // 32, 2), dtype=torch.float64,
+                                                                    device=r.device)]
+    return out
+
+
+def _unpack(spec, runner, tensors, traj_len, has_a):
+    host = tensors[0].cpu().numpy()
+    k = 0
+    theta = host[k : k + spec.n_param].copy()
+    k += spec.n_param
+    log_prior, loglik = float(host[k]), float(host[k + 1])
+    k += 2
+    traj = host[k : k + traj_len * spec.nx].reshape(traj_len, spec.nx).copy() if traj_len else None
+    k += traj_len * spec.nx
+    init = None
+    if spec.has_proposal_initial:
+        init = host[k : k + spec.nx].copy()
+        k += spec.nx
+    pos, uniform, maybe = int(host[k]), bool(host[k + 1]), bool(host[k + 2])
+    p = ThetaParticle(theta=theta, log_prior=log_prior, loglik=loglik, trajectory=traj, init_state=init)
+    if len(tensors) > 1:
+        run = runner._make(theta, init)
+        dev = run.device
+        hx = tensors[1].to(dev)
+        ha = tensors[2].to(dev)
+        run.history = [(hx[0], None)] + [(hx[i], ha[i - 1]) for i in range(1, pos + 1)]
+        run._x = hx[pos]
+        run._a = tensors[3].to(dev) if has_a else None
+        run._fs = tensors[4].to(dev)
+        if len(tensors) > 5:
+            run._cdf = tensors[5].to(dev) if has_a else None
+            run._trec = tensors[6].to(dev) if has_a else None
+        run.pos, run.loglik, run.weights_uniform, run._maybe_nonuniform = pos, loglik, uniform, maybe
+        fsv = run._fs.cpu().numpy().view(_lib.FILTER_STATE_DTYPE)[0]
+        run.loglik = float(fsv["loglik"])
+        p.run = run
+    return p
+
+
+def _redistribute(spec, runner, particles, anc, n, shard, lo):
+    """particles: this rank's slots [lo, hi) (list); returns the new local list."""
+    plan = plan_redistribution(anc, n, shard)
+    local_src = {lo + i: p for i, p in enumerate(particles)}
+    probe = particles[0] if particles else None
+    have_run = probe is not None and probe.run is not None
+    traj_len = 0 if probe is None or probe.trajectory is None else probe.trajectory.shape[0]
+    # every rank holds particles in the same state, but a rank may own none: share the shape info
+    info = allgather_f64(np.array([float(have_run), float(traj_len),
+                                   float(probe.run.pos) if have_run else -1.0,
+                                   float(probe.run._a is not None) if have_run else 0.0]),
+                         shard).reshape(shard.world, 4)
+    ref = info[np.argmax(info[:, 2])] if shard.world > 1 else info.reshape(4)
+    have_run, traj_len, pos, has_a = bool(ref[0]), int(ref[1]), int(ref[2]), bool(ref[3])
+    sends = {peer: [t for a in srcs for t in _pack(spec, runner, local_src[a], traj_len)]
+             for peer, srcs in plan.sends.items()}
+    P = runner.n_particles
+    _, tdtype, _ = _dtype_info(runner.device_opts.get("dtype", "float64"))
+    one = _payload_specs(spec, runner, have_run, pos, traj_len, P, tdtype)
+    recv_specs = {peer: one * len(dsts) for peer, dsts in plan.recvs.items()}
+    got = exchange(sends, recv_specs, shard)
+    new = {}
+    for j, a in plan.local_copies:
+        new[j] = local_src[a].clone()
+    per = len(one)
+    for peer, dsts in plan.recvs.items():
+        ts = got[peer]
+        for q, j in enumerate(dsts):
+            new[j] = _unpack(spec, runner, ts[q * per : (q + 1) * per], traj_len, has_a)
+    hi = lo + len(particles)
+    return [new[j] for j in range(lo, hi)]
+
+
+# ---------------------------------------------------------------- the sampler
+
+
+def smc_sampler(ir, runner, n_theta, rng, theta_resampler="multinomial", nthreads=1, shard=None):
+    """smc.py:67-171 on the GPU.  `nthreads` is accepted for API compatibility
+    (the batch is the parallelism); `shard` (paper_1306_3277_b200.distributed.Shard)
+    spreads theta-particles over ranks, default: torch.distributed if initialised."""
     if n_theta < 2:
         raise ValueError("smc sampler needs n_theta >= 2")
+    shard = shard or Shard.current()
     spec = resolve_model(ir)
     grid = runner.grid
     use_init = spec.has_proposal_initial
+    lo, hi = shard.bounds(n_theta)
+    J = list(range(lo, hi))
+    # prior draws: the full ensemble's streams, sliced (identical on every rank)
     thetas = spec.sample_parameter(rng.child(0), size=n_theta)
     init_states = spec.sample_initial(thetas, rng.child(1), size=n_theta) if use_init else None
-    particles = []
-    for j in range(n_theta):
+    local = []
+    for j in J:
         ist = init_states[j] if use_init else None
-        particles.append(ThetaParticle(theta=thetas[j], log_prior=_chain_log_prior(spec, thetas[j], ist),
-                                       init_state=ist))
+        local.append(ThetaParticle(theta=thetas[j], log_prior=_chain_log_prior(spec, thetas[j], ist), init_state=ist))
     log_v = np.full(n_theta, -np.log(n_theta))
+    counts = [shard_bounds_count(n_theta, r, shard.world) for r in range(shard.world)]
     diagnostics = []
     obs_steps = grid.obs_steps
-    J = list(range(n_theta))
     for i, grid_idx in enumerate(obs_steps, start=1):
         step_rng = rng.child(2, i)
         prev_idx = obs_steps[i - 2] if i > 1 else 0
-        # theta-resample (smc.py:96-98)
+        # theta-resample (smc.py:96-98): same ancestors on every rank
         anc = resample(np.exp(log_v - _logsumexp(log_v)), theta_resampler, step_rng.child(0))
-        particles = [particles[a].clone() for a in anc]
-        # rejuvenate: one marginal MH move each, batched replays (smc.py:101-122)
+        if shard.world == 1:
+            local = [local[a].clone() for a in anc]
+        else:
+            local = _redistribute(spec, runner, local, anc, n_theta, shard, lo)
+        particles = dict(zip(J, local))
+        # rejuvenate: one marginal MH move each, one batched replay (smc.py:101-122)
         chains = [MhChainState(theta=p.theta, trajectory=p.trajectory, loglik=p.loglik,
-                               log_prior=p.log_prior, init_state=p.init_state) for p in particles]
+                               log_prior=p.log_prior, init_state=p.init_state) for p in local]
         outs = marginal_mh_steps(ir, chains, runner, [step_rng.child(1, j) for j in J], upto=prev_idx)
         accepted = []
-        for p, (new, ok, run) in zip(particles, outs):
+        for p, (new, ok, run) in zip(local, outs):
             if ok:
                 p.theta, p.log_prior, p.loglik = new.theta, new.log_prior, new.loglik
                 p.trajectory, p.init_state, p.run = new.trajectory, new.init_state, run
             accepted.append(ok)
         # propagate and weight (smc.py:125-134)
-        incr = _advance_all(runner, particles, J, grid_idx,
-                            run_rngs=[step_rng.child(2, j, 1) for j in J],
-                            init_rngs=[step_rng.child(2, j, 0) for j in J],
-                            traj_rngs=[step_rng.child(3, j) for j in J])
+        rr = {j: step_rng.child(2, j, 1) for j in J}
+        ir_ = {j: step_rng.child(2, j, 0) for j in J}
+        tr = {j: step_rng.child(3, j) for j in J}
+        incr = _advance_all(runner, particles, J, grid_idx, run_rngs=rr, init_rngs=ir_, traj_rngs=tr)
         for j in J:
             particles[j].loglik += incr[j]
-        log_v = np.array([incr[j] for j in J])
+        log_v = allgather_f64(np.array([incr[j] for j in J]), shard, counts)  # C2
+        acc_all = allgather_f64(np.array(accepted, dtype=float), shard, counts)
         lse = _logsumexp(log_v)
         if not np.isfinite(lse):
             t = float(grid.times[grid_idx])
             raise DegenerateEnsembleError(f"all theta-weights vanished at t={t:g}", time=t)
         norm = np.exp(log_v - lse)
         diagnostics.append({"time": float(grid.times[grid_idx]), "ess": float(1.0 / np.sum(norm ** 2)),
-                            "acceptance": float(np.mean(accepted))})
+                            "acceptance": float(np.mean(acc_all))})
 
     # finalize (smc.py:150-161)
+    particles = dict(zip(J, local))
     need_new = [j for j in J if particles[j].run is None]
     if need_new:
         runs = runner.new_runs([particles[j].theta for j in need_new],
@@ -153,7 +279,18 @@ def smc_sampler(ir, runner, n_theta, rng, theta_resampler="multinomial", nthread
         for j, t in zip(stale, trajs):
             particles[j].trajectory = t
     log_v = log_v - _logsumexp(log_v)
-    return SmcResult(thetas=np.stack([p.theta for p in particles]), log_v=log_v,
-                     logliks=np.array([p.loglik for p in particles]),
-                     trajectories=np.stack([p.trajectory for p in particles]),
-                     particles=particles, diagnostics=diagnostics)
+    S1 = grid.last + 1
+    th = allgather_f64(np.concatenate([particles[j].theta for j in J]) if J else np.zeros(0), shard,
+                       [c * spec.n_param for c in counts]).reshape(n_theta, spec.n_param)
+    ll = allgather_f64(np.array([particles[j].loglik for j in J]), shard, counts)
+    tj = allgather_f64(np.concatenate([particles[j].trajectory.reshape(-1) for j in J]) if J else np.zeros(0),
+                       shard, [c * S1 * spec.nx for c in counts]).reshape(n_theta, S1, spec.nx)
+    return SmcResult(thetas=th, log_v=log_v, logliks=ll, trajectories=tj,
+                     particles=[particles[j] for j in J], diagnostics=diagnostics)
+
+
+def shard_bounds_count(n, rank, world):
+    from ..distributed import shard_bounds
+
+    lo, hi = shard_bounds(n, rank, world)
+    return hi - lo

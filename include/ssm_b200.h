@@ -125,7 +125,12 @@ typedef struct ssm_pw_args {
   void* workspace;      /* ssm_pw_workspace_bytes(B, P) bytes */
   void* cdf_local;      /* [B][P] uint64 tile-local fixed-point CDF for the next resample, or NULL */
   void* tile_rec;       /* [B][ceil(P/32)] ssm_tile_rec (one per warp tile), or NULL */
+  uint32_t hints;       /* SSM_HINT_* bits the host guarantees */
+  uint32_t pad_hints;
 } ssm_pw_args;
+
+/* hint: subs[0] is the only sub-step and holds exactly one RK4 step (n_ode == 1) */
+#define SSM_HINT_SINGLE_SUBSTEP 1u
 
 /* Per 32-particle (warp) tile of a weighted step (written by ssm_propagate_weight):
  * the tile's max log-weight and its fixed-point weight total

@@ -95,7 +95,12 @@ class PwArgs(C.Structure):
         ("workspace", C.c_void_p),
         ("cdf_local", C.c_void_p),
         ("tile_rec", C.c_void_p),
+        ("hints", C.c_uint32),
+        ("pad_hints", C.c_uint32),
     ]
+
+
+SSM_HINT_SINGLE_SUBSTEP = 1
 
 
 # name -> (restype, argtypes); every symbol declared in include/ssm_b200.h

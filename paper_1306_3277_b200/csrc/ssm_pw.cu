@@ -165,7 +165,10 @@ __device__ __forceinline__ bool finite_bits(float v) {
 
 constexpr double kTileFix = 4503599627370496.0;  // 2^52
 
-template <int MODEL, typename T, bool E, bool INJ>
+// SIMPLE: one sub-step with one RK4 step and every obs slot present (the
+// benchmark grid) -- no runtime loops or per-slot predicates, sub-step
+// constants hoisted out of the particle loop.
+template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE = false>
 __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   using O = Ar<T, E>;
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
@@ -217,6 +220,12 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   if (p0 < P) load_x(p0, anc ? __ldg(anc + p0) : p0);
   int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride;
   const T gconst = static_cast<T>(static_cast<double>(__popc(A.obs_mask)) * (A.obs_log_sd + A.log_sqrt_2pi));
+  T s_F = T(0), s_c = T(0), s_s = T(0);
+  if constexpr (SIMPLE) {
+    s_F = static_cast<T>(th[0]);
+    s_c = static_cast<T>(th[1] * 20.0 * A.subs[0].sd);  // sqrt(sigma2) / h * sqrt(d)
+    s_s = static_cast<T>(A.subs[0].s[0]);
+  }
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int p = tile * kThreads + threadIdx.x;
@@ -232,6 +241,20 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
       anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
     }
     if (act) {
+      if constexpr (SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ) {
+        T z[8];
+        normals8<T>(k0, k1, static_cast<uint32_t>(p), static_cast<uint32_t>(A.step), 0u, z);
+        T Fn[8];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) Fn[n] = fma(s_c, z[n], s_F);  // F + sqrt(sigma2) sd z / h
+        l96_rk4_fast<T>(x, Fn, s_s);
+        if (A.check_finite && !bad) {
+          bool ok = true;
+#pragma unroll
+          for (int n = 0; n < 8; ++n) ok &= finite_bits(x[n]);
+          if (!ok) bad = true;  // bad_sub stays 0
+        }
+      } else
       for (int k = 0; k < A.n_sub; ++k) {
         const ssm_substep& S = A.subs[k];
         if constexpr (MODEL == SSM_MODEL_LORENZ96) {
@@ -298,11 +321,19 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
               }
             }
           } else {
+            if constexpr (SIMPLE) {
 #pragma unroll
-            for (int n = 0; n < 8; ++n) {
-              if (A.obs_mask & (1u << n)) {
+              for (int n = 0; n < 8; ++n) {
                 const T z = (static_cast<T>(A.y[n]) - x[n]) * T(2.0);
                 g = fma(T(-0.5) * z, z, g);
+              }
+            } else {
+#pragma unroll
+              for (int n = 0; n < 8; ++n) {
+                if (A.obs_mask & (1u << n)) {
+                  const T z = (static_cast<T>(A.y[n]) - x[n]) * T(2.0);
+                  g = fma(T(-0.5) * z, z, g);
+                }
               }
             }
             g -= gconst;
@@ -406,6 +437,15 @@ template <int MODEL, typename T>
 static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
   const dim3 grid(pw_grid_x(A.P), A.B);
   const bool inj = A.noise != nullptr;
+  if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+    // host hint: one sub-step with one RK4 step; and no obs or all 8 slots observed
+    const bool simple = (A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !A.exact && !inj &&
+                        (!A.has_obs || A.obs_mask == 0xFFu);
+    if (simple) {
+      pw_kernel<MODEL, T, false, false, true><<<grid, kThreads, 0, s>>>(A);
+      return;
+    }
+  }
   if (A.exact) {
     if (inj)
       pw_kernel<MODEL, T, true, true><<<grid, kThreads, 0, s>>>(A);

@@ -85,6 +85,7 @@ class Schedule:
         recs, self.offsets, self.n_sub, self.sub_end = [], [0] * (S + 1), [0] * (S + 1), [None] * (S + 1)
         self.host_subs = [None] * (S + 1)
         self.obs = [None] * (S + 1)
+        self.single = [False] * (S + 1)
         for i in range(1, S + 1):
             t0, t1 = times[i - 1], times[i]
             dt = t1 - t0
@@ -107,6 +108,7 @@ class Schedule:
                 ends.append(t_k + d)
             self.offsets[i] = len(recs)
             self.n_sub[i] = len(subs)
+            self.single[i] = len(subs) == 1 and (not spec.has_ode or int(arr[0]["n_ode"]) == 1)
             self.sub_end[i] = ends
             self.host_subs[i] = arr
             recs.extend(arr)
@@ -455,6 +457,7 @@ def advance_runs(runs, upto, rngs):
         a_out = torch.empty((B, P), dtype=tdt, device=dev) if obs is not None else None
         args.step = i
         args.n_sub = n_sub
+        args.hints = _lib.SSM_HINT_SINGLE_SUBSTEP if sched.single[i] else 0
         args.subs = sched.subs_ptr(i)
         args.x_in = x_prev.data_ptr()
         args.x_out = x_out.data_ptr()

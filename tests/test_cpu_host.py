@@ -45,7 +45,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_lib.Substep) == 64
     assert _lib.FILTER_STATE_DTYPE.itemsize == 64
     # PwArgs: 10 int32 + 8 doubles + 5 doubles + 11 pointers
-    assert C.sizeof(_lib.PwArgs) == 10 * 4 + 13 * 8 + 13 * 8
+    assert C.sizeof(_lib.PwArgs) == 10 * 4 + 13 * 8 + 13 * 8 + 8
 
 
 def test_status_strings_no_device_needed():

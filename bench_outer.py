@@ -1,0 +1,164 @@
+"""Secondary benchmarks for the other BASELINE.json configs (one JSON line each):
+
+  config 1: windkessel PF, P=1024, T=100 (reference CPU case; launch-bound on the GPU)
+  config 3: PMMH on windkessel, 2^16-particle filters, chains batched per GPU (8 per GPU of 64)
+  config 4: SMC^2 on L96, 128 theta-particles x 2^14 per GPU (of 1024), sparse obs
+  config 5: L96 PF particle-count sweep 2^10 .. 2^26 (1 GPU)
+
+Metric: particle-updates/s (P x grid steps, counting SMC^2 rejuvenation replays), device time
+with CUDA events around whole driver calls (host theta-level work included).
+Run: python bench_outer.py [--configs 1,3,4,5] [--quick]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+class Locf:
+    def __init__(self, times, values):
+        self.times = np.asarray(times, dtype=float)
+        self.values = np.asarray(values, dtype=float).reshape(len(self.times), -1)
+
+    def at(self, t):
+        tol = 1e-9 * max(1.0, abs(t))
+        return self.values[int(np.searchsorted(self.times, t + tol, side="right")) - 1]
+
+
+def wk_data(T=100, t_end=1.0):
+    from oracle import ssm_oracle as O
+
+    theta = np.array([1.8, 3.0, 0.06, 25.0])
+    in_times = np.round(np.arange(0, t_end + 1e-9, 0.01), 10)
+    inputs = Locf(in_times, O.windkessel_flow(in_times))
+    times = np.linspace(0.0, t_end, T + 1)
+    rng = O.Stream(1)
+    x = np.array([[rng.child(1).normal(90.0, 15.0)]])
+    obs = []
+    for k in range(1, T + 1):
+        rk = rng.child(2, k)
+        x, _ = O.wk_transition(theta, x, times[k - 1], times[k] - times[k - 1],
+                               lambda kk, sd, rk=rk: rk.normal(0.0, np.array([sd]), size=1), inputs.at)
+        F = float(inputs.at(times[k])[0])
+        obs.append([rng.child(3, k).normal(x[0, 0] + theta[2] * F, 2.0)])
+    return theta, times, np.array(obs), inputs
+
+
+def l96_sparse(T=40):
+    from oracle import ssm_oracle as O
+
+    theta = np.array([10.0, 0.1])
+    times = np.linspace(0.0, 2.0 * T / 40, T + 1)
+    obs = O.simulate_l96(theta, times, O.Stream(1), obs_slots=range(4), obs_every=2)
+    return theta, times, np.array([obs[k][0] for k in range(1, T + 1)]), np.array([obs[k][1] for k in range(1, T + 1)])
+
+
+def timed(fn, warmup=1, reps=3):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        out = fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps, out
+
+
+def config1(quick):
+    from paper_1306_3277_b200 import WINDKESSEL, RngStream
+    from paper_1306_3277_b200.inference import build_filter_grid, particle_filter
+
+    theta, times, obs, inputs = wk_data()
+    grid = build_filter_grid(0.0, 1.0, 100, times[1:], obs, np.ones((100, 1), bool), n_obs=1)
+    res = {}
+    for scheme in ("multinomial", "systematic"):
+        ms, out = timed(lambda: particle_filter(WINDKESSEL, theta, grid, RngStream(7), inputs=inputs,
+                                                n_particles=1024, resampler=scheme), reps=5)
+        res[scheme] = {"ms_per_filter": ms, "value": 1024 * 100 / (ms / 1e3), "loglik": out.loglik}
+    return {"config": "1: windkessel PF P=1024 T=100", "unit": "particle-updates/s", "results": res,
+            "reference_cpu_1core_survey": {"multinomial": 1.93e6, "systematic": 2.36e6}}
+
+
+def config3(quick):
+    from paper_1306_3277_b200 import WINDKESSEL, RngStream
+    from paper_1306_3277_b200.inference import FilterRunner, build_filter_grid, mh_sample_chains
+
+    theta, times, obs, inputs = wk_data()
+    grid = build_filter_grid(0.0, 1.0, 100, times[1:], obs, np.ones((100, 1), bool), n_obs=1)
+    chains, P, steps = 8, 1 << 16, (3 if quick else 10)
+    runner = FilterRunner(WINDKESSEL, grid, inputs=inputs, n_particles=P, resampler="systematic")
+    ms, (samples, acc) = timed(lambda: mh_sample_chains(WINDKESSEL, runner, steps, [RngStream(100 + c) for c in range(chains)]),
+                               warmup=1, reps=1)
+    runs = chains * (steps + 1)  # init + one filter per MH step (auto-rejects skip theirs)
+    return {"config": f"3: PMMH windkessel, {chains} chains/GPU x 2^16 particles, T=100, {steps} MH steps",
+            "unit": "particle-updates/s", "value": runs * P * 100 / (ms / 1e3), "ms_per_mh_step": ms / (steps + 1),
+            "acceptance": acc.tolist(), "reference_cpu_1core_survey": 8.12e6}
+
+
+def config4(quick):
+    from paper_1306_3277_b200 import LORENZ96, RngStream
+    from paper_1306_3277_b200.inference import FilterRunner, build_filter_grid, smc_sampler
+
+    theta, times, ov, om = l96_sparse(T=40)
+    grid = build_filter_grid(0.0, 2.0, 40, times[1:], ov, om, n_obs=8)
+    n_theta, P = (32, 1 << 12) if quick else (128, 1 << 14)
+    runner = FilterRunner(LORENZ96, grid, n_particles=P, resampler="systematic")
+    ms, res = timed(lambda: smc_sampler(LORENZ96, runner, n_theta, RngStream(5), theta_resampler="systematic"),
+                    warmup=0, reps=1)
+    obs_steps = grid.obs_steps
+    # PF work: propagation to each obs step + rejuvenation replay to the previous one
+    steps = sum(o for o in obs_steps) + sum((obs_steps[i - 2] if i > 1 else 0) for i in range(1, len(obs_steps) + 1))
+    return {"config": f"4: SMC^2 L96 {n_theta} theta x 2^{int(math.log2(P))}, sparse obs, T=40",
+            "unit": "particle-updates/s (incl. replays)", "value": n_theta * P * steps / (ms / 1e3),
+            "seconds": ms / 1e3, "final_ess": res.diagnostics[-1]["ess"],
+            "reference_cpu_1core_survey": 8.8e5}
+
+
+def config5(quick):
+    from paper_1306_3277_b200 import LORENZ96, RngStream
+    from paper_1306_3277_b200.inference import build_filter_grid, particle_filter
+    from oracle import ssm_oracle as O
+
+    theta = np.array([10.0, 0.1])
+    times = np.linspace(0.0, 2.0, 41)
+    obs = O.simulate_l96(theta, times, O.Stream(1))
+    grid = build_filter_grid(0.0, 2.0, 40, times[1:], np.array([obs[k][0] for k in range(1, 41)]),
+                             np.ones((40, 8), bool), n_obs=8)
+    out = {}
+    for lg in (range(10, 23, 4) if quick else range(10, 27, 2)):
+        P = 1 << lg
+        ms, _ = timed(lambda: particle_filter(LORENZ96, theta, grid, RngStream(7), n_particles=P,
+                                              resampler="systematic", exact=False), warmup=1, reps=3)
+        out[f"2^{lg}"] = {"ms_per_filter": ms, "value": P * 40 / (ms / 1e3)}
+    return {"config": "5: L96 PF sweep, T=40, systematic, f64 (1 GPU)", "unit": "particle-updates/s", "results": out}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,3,4,5")
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    fns = {"1": config1, "3": config3, "4": config4, "5": config5}
+    for c in args.configs.split(","):
+        t0 = time.time()
+        r = fns[c](args.quick)
+        r["wall_s"] = time.time() - t0
+        print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
           for (int n = 0; n < 8; ++n) ok &= finite_bits(x[n]);
           if (!ok) bad = true;  // bad_sub stays 0
         }
-      } else
+      } else {
       for (int k = 0; k < A.n_sub; ++k) {
         const ssm_substep& S = A.subs[k];
         if constexpr (MODEL == SSM_MODEL_LORENZ96) {
@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
           }
         }
       }
+      }  // general sub-step loop
 #pragma unroll
       for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * P + p] = x[n];
 

@@ -40,6 +40,9 @@ from ..rng import device_key
 from .timegrid import as_filter_grid
 from .types import FilterOutcome
 
+import os
+
+_NO_HINTS = bool(os.environ.get("SSM_NO_HINTS"))  # A/B switch for the specialised kernels
 _RESAMPLE_KEY = 0  # particle.py:24
 _PROPAGATE_KEY = 1  # particle.py:25
 SCHEMES = ("multinomial", "stratified", "systematic")
@@ -457,7 +460,7 @@ def advance_runs(runs, upto, rngs):
         a_out = torch.empty((B, P), dtype=tdt, device=dev) if obs is not None else None
         args.step = i
         args.n_sub = n_sub
-        args.hints = _lib.SSM_HINT_SINGLE_SUBSTEP if sched.single[i] else 0
+        args.hints = _lib.SSM_HINT_SINGLE_SUBSTEP if (sched.single[i] and not _NO_HINTS) else 0
         args.subs = sched.subs_ptr(i)
         args.x_in = x_prev.data_ptr()
         args.x_out = x_out.data_ptr()

@@ -345,3 +345,66 @@ def test_filter_resampler_degenerate_weights(scheme):
                                             _lib.ptr(u), None, 1, _lib.ptr(anc), _lib.ptr(ws), _lib.stream_ptr()))
         ref = O.resample_with(np.exp(a_np - logsumexp(a_np)), scheme, u.cpu().numpy())
         np.testing.assert_array_equal(anc.cpu().numpy(), ref)
+
+
+def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float64"):
+    """One ssm_propagate_weight launch with device noise (C ABI), returns x_out, a_out."""
+    from paper_1306_3277_b200 import _lib
+    from paper_1306_3277_b200.inference.particle import _fs_init, _dtype_info
+    from paper_1306_3277_b200.models import LOG_SQRT_2PI
+
+    L = _lib.lib()
+    _, tdt, dt_id = _dtype_info(dtype)
+    P = x.shape[0]
+    dev = torch.device("cuda")
+    xin = torch.from_numpy(np.ascontiguousarray(x.T)).to(dev, tdt)
+    xout = torch.empty_like(xin)
+    sub = np.zeros(1, dtype=_lib.SUBSTEP_DTYPE)
+    sub[0]["d"], sub[0]["sd"], sub[0]["n_ode"] = d, np.sqrt(d), 1
+    sub[0]["s"][0] = min(0.05, d)
+    subs = torch.from_numpy(sub.view(np.uint8).copy()).to(dev)
+    th = torch.from_numpy(LORENZ96.derived(theta)).to(dev)
+    kt = torch.from_numpy(np.asarray(keys, dtype=np.uint32).view(np.int32).reshape(1, 2)).to(dev)
+    fs = _fs_init(1, dev)
+    ws = torch.empty(L.ssm_pw_workspace_bytes(1, P), dtype=torch.uint8, device=dev)
+    a = torch.empty(P, dtype=tdt, device=dev)
+    A = _lib.PwArgs()
+    A.model, A.dtype, A.B, A.P, A.step, A.n_sub = 0, dt_id, 1, P, 3, 1
+    A.exact, A.check_finite, A.has_obs, A.obs_mask = int(exact), 1, 1, 0xFF
+    for n in range(8):
+        A.y[n] = float(y[n])
+    A.log_w0, A.obs_log_sd, A.log_sqrt_2pi, A.ess_rel = -np.log(P), np.log(0.5), LOG_SQRT_2PI, -1.0
+    A.x_in, A.x_out, A.a_out, A.theta, A.subs = xin.data_ptr(), xout.data_ptr(), a.data_ptr(), th.data_ptr(), subs.data_ptr()
+    A.keys, A.fs, A.workspace, A.hints = kt.data_ptr(), fs.data_ptr(), ws.data_ptr(), hints
+    _lib.check(L.ssm_propagate_weight(A, _lib.stream_ptr()))
+    return xout.t().double().cpu().numpy(), a.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("d", [0.05, 0.04999999999999999, 0.05000000000000002])
+def test_specialised_kernel_equals_general(dtype, d):
+    """The SIMPLE (single sub-step, full obs) fused kernel must compute the same
+    step as the general kernel (same device draws)."""
+    rs = np.random.default_rng(3)
+    P = 5000
+    x = rs.uniform(-1, 3, (P, 8))
+    y = rs.normal(0, 3, 8)
+    keys = [123456789, 987654321]
+    x1, a1 = _pw_direct(x, [10.0, 0.1], keys, d, 1, y, dtype=dtype)
+    x0, a0 = _pw_direct(x, [10.0, 0.1], keys, d, 0, y, dtype=dtype)
+    tol = 1e-12 if dtype == "float64" else 1e-5
+    assert normwise(x1, x0) <= tol
+    assert normwise(a1, a0) <= tol
+
+
+def test_fast_device_noise_filter_tracks_exact():
+    """Fast (FMA) and exact float64 filters share the device draws, so over a
+    short window their likelihoods agree to round-off amplification."""
+    g = load_golden("pf.npz")
+    grid = _l96_grid(g)
+    lls = []
+    for exact in (True, False):
+        out = particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(17), n_particles=1 << 14,
+                              resampler="systematic", exact=exact, upto=8)
+        lls.append(out.loglik)
+    assert abs(lls[0] - lls[1]) <= 1e-6 * abs(lls[0]), lls

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from ..errors import UnsupportedModelError
-from ..models import resolve_model
+from ..models import propose_batch, resolve_model
 from .particle import ParticleRun, advance_runs, init_runs, sample_trajectories
 from .timegrid import as_filter_grid
 
@@ -145,7 +145,13 @@ def marginal_mh_steps(ir, chains, runner, rngs, upto=None, references=None):
     then per-chain accept/reject with the chain's own stream."""
     spec = resolve_model(ir)
     references = references or [None] * len(chains)
-    props = [_propose(spec, c, g) for c, g in zip(chains, rngs)]
+    if not chains:
+        return []
+    # vectorised over chains; per-stream draws in the reference's order (bit-identical to _propose)
+    th_new, x0_new, lq_f, lq_r, lp_new = propose_batch(
+        spec, [c.theta for c in chains], [c.init_state for c in chains] if chains[0].init_state is not None else None,
+        rngs)
+    props = [(th_new[k], x0_new[k], float(lq_f[k]), float(lq_r[k]), float(lp_new[k])) for k in range(len(chains))]
     todo = [k for k, p in enumerate(props) if p[4] != -np.inf]
     res = runner.run_batch([props[k][0] for k in todo], [props[k][1] for k in todo],
                            [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto)

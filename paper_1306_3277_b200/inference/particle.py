@@ -221,12 +221,14 @@ class ParticleRun:
         self.loglik = 0.0
         self.pos = 0
         self.weights_uniform = True
-        self.history = []  # per grid index: (x_i [nx, P] tensor, anc_i [P] int32 tensor | None)
+        self._hist = []  # per grid index: (x batch tensor [B, nx, P], anc batch [B, P] | None, row b)
         self._x = None
         self._a = None  # unnormalised log-weights of the last weighted step
         self._fs = None  # (64,) uint8 view of an ssm_filter_state
         self._cdf = None  # (P,) tile-local fixed-point CDF of the last weighted step
         self._trec = None  # (ceil(P/32), 2) warp-tile records {max, Q} of the last weighted step
+        self._hx = []  # device pointers of history[i][0] (trace-kernel pointer table)
+        self._ha = []  # device pointers of history[i][1] (0 = identity)
         self._maybe_nonuniform = False
         self._derived = None
 
@@ -238,12 +240,23 @@ class ParticleRun:
     def clone(self):
         other = ParticleRun.__new__(ParticleRun)
         other.__dict__ = dict(self.__dict__)
-        other.history = list(self.history)
+        other._hist = list(self._hist)
+        other._hx = list(self._hx)
+        other._ha = list(self._ha)
         return other
 
     @property
     def initialized(self):
         return self._x is not None
+
+    @property
+    def history(self):
+        """[(x_i [nx, P], anc_i [P] | None)] per grid index (particle.py:59, 135); views made on access."""
+        return [(xb[b], ab[b] if ab is not None else None) for xb, ab, b in self._hist]
+
+    @history.setter
+    def history(self, entries):
+        self._hist = [(x.unsqueeze(0), a.unsqueeze(0) if a is not None else None, 0) for x, a in entries]
 
     def advance_to(self, upto, rng):
         return float(advance_runs([self], upto, [rng])[0])
@@ -358,7 +371,9 @@ def init_runs(runs, rngs):
         r.pos = 0
         r.weights_uniform = True
         r._maybe_nonuniform = False
-        r.history = [(r._x, None)]
+        r._hist = [(x, None, b)]
+        r._hx = [r._x.data_ptr()]
+        r._ha = [0]
     return runs
 
 
@@ -404,7 +419,7 @@ def advance_runs(runs, upto, rngs):
     ess_rel = -1.0 if r0.ess_rel is None else float(r0.ess_rel)
     log_w0 = float(-np.log(P))
     obs_log_sd = float(np.log(spec.obs_sd))
-    new_hist = [[] for _ in range(B)]
+    new_hist = []  # per step: (x_out [B, nx, P], anc [B, P] | None)
     esz = 8 if r0.dtype_id == _lib.SSM_F64 else 4
     theta_host = theta.cpu().numpy() if host_noise else None
 
@@ -485,8 +500,7 @@ def advance_runs(runs, upto, rngs):
                           + (esz if (a_last is not None and obs is not None and r0.ess_rel is not None) else 0))
         with profiling.maybe("propagate_weight", nbytes):
             _lib.check(L.ssm_propagate_weight(args, stream), "ssm_propagate_weight")
-        for b in range(B):
-            new_hist[b].append((x_out[b], anc[b] if anc is not None else None))
+        new_hist.append((x_out, anc))
         x_prev = x_out
         if obs is not None:
             a_last = a_out
@@ -494,6 +508,8 @@ def advance_runs(runs, upto, rngs):
         elif maybe_nonuniform and r0.ess_rel is None:
             maybe_nonuniform = False
 
+    xstride = spec.nx * P * esz
+    astride = P * 4
     fs_host = _fs_view(fs)  # one synchronisation per advance
     incr = np.empty(B)
     for b, r in enumerate(runs):
@@ -508,7 +524,9 @@ def advance_runs(runs, upto, rngs):
         r._trec = tile_rec[b] if (tiles_ok and a_last is not None) else None
         r._fs = fs[b]
         r._maybe_nonuniform = maybe_nonuniform
-        r.history.extend(new_hist[b])
+        r._hist.extend((xo, an, b) for xo, an in new_hist)
+        r._hx.extend(xo.data_ptr() + b * xstride for xo, _ in new_hist)
+        r._ha.extend((an.data_ptr() + b * astride) if an is not None else 0 for _, an in new_hist)
         r.pos = upto
     return incr
 
@@ -559,14 +577,11 @@ def sample_trajectories(runs, rngs):
     j = torch.empty((B, 1), dtype=torch.int32, device=dev)
     _lib.check(L.ssm_resample_search(B, P, 1, _lib.SCHEME_IDS["multinomial"], 1, _lib.ptr(cum), _lib.ptr(u),
                                      None, 0, None, _lib.ptr(j), None, stream), "ssm_resample_search")
-    xs = np.zeros((B, S + 1), dtype=np.int64)
-    ancs = np.zeros((B, S + 1), dtype=np.int64)
-    for b, r in enumerate(runs):
-        if len(r.history) != S + 1:
+    for r in runs:
+        if len(r._hx) != S + 1 or len(r._hist) != S + 1:
             raise ValueError("history length does not match the run position")
-        for i, (xi, ai) in enumerate(r.history):
-            xs[b, i] = xi.data_ptr()
-            ancs[b, i] = ai.data_ptr() if ai is not None else 0
+    xs = np.array([r._hx for r in runs], dtype=np.int64)
+    ancs = np.array([r._ha for r in runs], dtype=np.int64)
     xs_t = torch.from_numpy(xs).to(dev)
     ancs_t = torch.from_numpy(ancs).to(dev)
     out = torch.empty((B, S + 1, nx), dtype=torch.float64, device=dev)

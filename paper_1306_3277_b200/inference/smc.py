@@ -151,6 +151,8 @@ def _unpack(spec, runner, tensors, traj_len, has_a):
         hx = tensors[1].to(dev)
         ha = tensors[2].to(dev)
         run.history = [(hx[0], None)] + [(hx[i], ha[i - 1]) for i in range(1, pos + 1)]
+        run._hx = [h[0].data_ptr() for h in run.history]
+        run._ha = [0] + [h[1].data_ptr() for h in run.history[1:]]
         run._x = hx[pos]
         run._a = tensors[3].to(dev) if has_a else None
         run._fs = tensors[4].to(dev)

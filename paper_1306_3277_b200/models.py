@@ -300,6 +300,103 @@ class ModelSpec:
         return self._walk_initial(x_from, None, x_to)[1]
 
 
+# ---------------------------------------------------------------------------
+# vectorised theta-level blocks (one row per chain / theta-particle).  Draws
+# are taken per stream in the reference's order (the same numpy calls, so
+# bit-identical); the scipy density math runs once over all rows.
+# ---------------------------------------------------------------------------
+
+
+def _tg_from_u(u, mean, sd, lower, upper):
+    fa = ndtr((lower - mean) / sd)
+    fb = ndtr((upper - mean) / sd)
+    _require(fb - fa > 0, "truncated_gaussian truncation region has no mass")
+    return mean + sd * ndtri(fa + u * (fb - fa))
+
+
+def _tg_logpdf(x, mean, sd, lower, upper):
+    fa = ndtr((lower - mean) / sd)
+    fb = ndtr((upper - mean) / sd)
+    z = (x - mean) / sd
+    core = -0.5 * z * z - np.log(sd) - LOG_SQRT_2PI - np.log(fb - fa)
+    return np.where((x >= lower) & (x <= upper), core, -np.inf)
+
+
+def propose_batch(spec, thetas, inits, rngs):
+    """_propose for every chain: (theta_new, init_new, logq_fwd, logq_rev, log_prior_new).
+    Equals [spec.propose_parameters / proposal_parameter_logpdf / propose_initial /
+    proposal_initial_logpdf / parameter_logpdf + initial_logpdf] row by row."""
+    th = np.array(thetas, dtype=float).reshape(len(rngs), spec.n_param)
+    C = th.shape[0]
+    new = th.copy()
+    lq_f = np.zeros(C)  # logq accumulates from 0.0 statement by statement (simulate.py:283-299)
+    lq_r = np.zeros(C)
+    if spec.name == "Lorenz96":
+        stmts = [(0, "tg", (0.1, 8.0, 12.0))]
+        ig = 1
+    else:
+        stmts = [(0, "tg", (0.03, 0.0, np.inf)), (1, "tg", (0.1, 0.0, np.inf)), (2, "tg", (0.002, 0.0, np.inf))]
+        ig = 3
+    # draws, per stream, in statement order (simulate.py:272-300)
+    n_tg = len(stmts)
+    has_init = inits is not None and inits[0] is not None
+    u = np.empty((C, n_tg))
+    g = np.empty(C)
+    ui = np.empty((C, spec.nx)) if has_init else None
+    scale = 1.0 / (3.0 * th[:, ig])
+    _require(np.all(3.0 * th[:, ig] > 0), "inverse_gamma scale must be > 0")
+    for c, rng in enumerate(rngs):
+        for k in range(n_tg):
+            u[c, k] = rng.uniform(size=1)[0]
+        g[c] = rng.gamma(2.0, np.asarray(scale[c]), size=1)[0]
+        if has_init:
+            for n in range(spec.nx):
+                ui[c, n] = rng.uniform(size=1)[0]
+    for k, (slot, _, (sd, lo, hi)) in enumerate(stmts):
+        m = th[:, slot]
+        _require(lo < hi, "truncated_gaussian needs lower < upper")
+        v = _tg_from_u(u[:, k], m, sd, lo, hi)
+        new[:, slot] = v
+        lq_f += _tg_logpdf(v, m, sd, lo, hi)
+        lq_r += _tg_logpdf(th[:, slot], v, sd, lo, hi)
+    a_f, s_f = 2.0, 3.0 * th[:, ig]
+    v = 1.0 / g
+    new[:, ig] = v
+    lq_f += d_invgamma_logpdf(v, a_f, s_f)
+    lq_r += d_invgamma_logpdf(th[:, ig], 2.0, 3.0 * v)
+    init_new = None
+    if has_init:
+        # accumulate slot by slot, in the reference's order (mcmc.py:140-144)
+        x0 = np.array(inits, dtype=float)
+        init_new = _tg_from_u(ui, x0, 0.1, -1.0, 3.0)
+        f_i = _tg_logpdf(init_new, x0, 0.1, -1.0, 3.0)
+        r_i = _tg_logpdf(x0, init_new, 0.1, -1.0, 3.0)
+        lf, lr = np.zeros(C), np.zeros(C)
+        for n in range(spec.nx):
+            lf = lf + f_i[:, n]
+            lr = lr + r_i[:, n]
+        lq_f = lq_f + lf
+        lq_r = lq_r + lr
+    lp = parameter_logpdf_batch(spec, new)
+    if has_init:
+        li = np.where((init_new >= -1.0) & (init_new <= 3.0), -np.log(4.0), -np.inf)
+        tot = np.zeros(C)
+        for n in range(spec.nx):
+            tot = tot + li[:, n]
+        lp = lp + tot
+    return new, (list(init_new) if has_init else [None] * C), lq_f, lq_r, lp
+
+
+def parameter_logpdf_batch(spec, thetas):
+    """simulate.parameter_logpdf row-wise (total from 0.0, statement order)."""
+    th = np.atleast_2d(thetas)
+    z = np.zeros(th.shape[0])
+    if spec.name == "Lorenz96":
+        return (z + d_uniform_logpdf(th[:, 0], 8.0, 12.0)) + d_invgamma_logpdf(th[:, 1], 2.0, 0.25)
+    return (((z + d_gamma_logpdf(th[:, 0], 2.0, 0.9)) + d_gamma_logpdf(th[:, 1], 2.0, 1.5))
+            + d_gamma_logpdf(th[:, 2], 2.0, 0.03)) + d_invgamma_logpdf(th[:, 3], 2.0, 25.0)
+
+
 LORENZ96 = ModelSpec("Lorenz96", _lib.SSM_MODEL_LORENZ96, 2, 8, 8, 0, 8, 0.05, 0.05, 0.5, True)
 WINDKESSEL = ModelSpec("Windkessel", _lib.SSM_MODEL_WINDKESSEL, 4, 1, 1, 1, 1, 0.01, 0.01, 2.0, False)
 _BY_NAME = {"lorenz96": LORENZ96, "windkessel": WINDKESSEL}

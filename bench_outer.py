@@ -70,8 +70,10 @@ def timed(fn, warmup=1, reps=3):
         fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = None
     s.record()
     for _ in range(reps):
+        out = None  # release the previous run (and its history) before the next
         out = fn()
     e.record()
     torch.cuda.synchronize()

@@ -339,10 +339,14 @@ def init_runs(runs, rngs):
     dev = r0.device
     x = torch.empty((B, spec.nx, P), dtype=r0.tdtype, device=dev)
     need_draw = [b for b, r in enumerate(runs) if r.initial_state is None]
-    for b, r in enumerate(runs):
-        if r.initial_state is not None:
-            x0 = torch.as_tensor(np.asarray(r.initial_state, dtype=float), dtype=r0.tdtype)
-            x[b].copy_(x0.view(spec.nx, 1).expand(spec.nx, P))
+    fixed = [b for b, r in enumerate(runs) if r.initial_state is not None]
+    if fixed:  # np.tile(initial_state, (P, 1)) (particle.py:63-65): one H2D + one broadcast copy
+        x0 = torch.from_numpy(np.stack([np.asarray(runs[b].initial_state, dtype=float) for b in fixed]))
+        x0 = x0.to(dev, r0.tdtype).view(len(fixed), spec.nx, 1).expand(len(fixed), spec.nx, P)
+        if len(fixed) == B:
+            x.copy_(x0)
+        else:
+            x[torch.tensor(fixed, device=dev)] = x0
     if need_draw:
         if r0.noise == "host":
             for b in need_draw:
@@ -438,11 +442,22 @@ def advance_runs(runs, upto, rngs):
     args.fs = fs.data_ptr()
     args.workspace = pw_ws.data_ptr()
 
+    # one allocation per advance call for the history it produces (the caching
+    # allocator would otherwise churn cudaMalloc on every step)
+    n_steps = upto - start
+    x_arena = torch.empty((n_steps, B, spec.nx, P), dtype=tdt, device=dev)
+    n_res = sum(1 for i in range(start + 1, upto + 1) if sched.obs[i] is not None)
+    a_arena = torch.empty((max(n_res, 1), B, P), dtype=tdt, device=dev) if n_res else None
+    anc_arena = None
+    a_slot = 0
     for i in range(start + 1, upto + 1):
         step_rngs = [g.child(i) for g in rngs] if host_noise else None
         anc = None
         if maybe_nonuniform:
-            anc = torch.empty((B, P), dtype=torch.int32, device=dev)
+            if anc_arena is None:
+                anc_arena = torch.empty((upto - i + 1, B, P), dtype=torch.int32, device=dev)
+                anc_base = i
+            anc = anc_arena[i - anc_base]
             u_t = None
             if host_noise:
                 rr = [s.child(_RESAMPLE_KEY) for s in step_rngs]
@@ -465,14 +480,17 @@ def advance_runs(runs, upto, rngs):
                                                         _lib.ptr(anc), _lib.ptr(rs_ws), stream),
                                "ssm_resample_from_logw")
         n_sub = sched.n_sub[i]
-        x_out = torch.empty((B, spec.nx, P), dtype=tdt, device=dev)
+        x_out = x_arena[i - start - 1]
         noise_t = None
         if host_noise:
             noise = np.stack([spec.host_noise(s.child(_PROPAGATE_KEY), sched.host_subs[i], P, theta_row)
                               for s, theta_row in zip(step_rngs, theta_host)])
             noise_t = torch.from_numpy(noise).to(dev, tdt)
         obs = sched.obs[i]
-        a_out = torch.empty((B, P), dtype=tdt, device=dev) if obs is not None else None
+        a_out = None
+        if obs is not None:
+            a_out = a_arena[a_slot]
+            a_slot += 1
         args.step = i
         args.n_sub = n_sub
         args.hints = _lib.SSM_HINT_SINGLE_SUBSTEP if (sched.single[i] and not _NO_HINTS) else 0

@@ -209,6 +209,52 @@ int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const void* a, c
                            const ssm_filter_state* fs, const double* u, const uint32_t* keys,
                            int step, int32_t* anc, void* workspace, void* stream);
 
+/* Native driver for ParticleRun.advance_to (particle.py:87-94), device-noise
+ * mode: one call enqueues, for each grid step, the resample kernels (when the
+ * previous step weighted, particle.py:96-105) and ssm_propagate_weight, with
+ * the host-side weighting state machine.  No synchronisation. */
+typedef struct ssm_step_desc {
+  int32_t step;         /* grid index i */
+  int32_t n_sub;
+  int64_t subs_offset;  /* index of the step's first record in subs_table */
+  int32_t has_obs;
+  uint32_t obs_mask;
+  int32_t hints;        /* SSM_HINT_* */
+  int32_t pad;
+  double y[8];
+  double u_obs;
+} ssm_step_desc;
+
+typedef struct ssm_advance_args {
+  ssm_pw_args pw;       /* per-run constants (model, dtype, B, P, exact, ..., theta, keys, fs,
+                           workspace); per-step fields are filled by ssm_advance */
+  const ssm_substep* subs_table;  /* device */
+  const ssm_step_desc* steps;     /* HOST [n_steps] */
+  int32_t n_steps;
+  int32_t scheme;
+  int32_t tiles;             /* 1: resample from the fused kernel's tile CDF (systematic/stratified) */
+  int32_t maybe_nonuniform;  /* in: before the first step; out: after the last */
+  int32_t ess_gate;          /* ess_rel >= 0 */
+  int32_t pad;
+  const void* x_in;          /* [B][nx][P] */
+  void* x_arena;             /* [n_steps][B][nx][P] positions written per step */
+  int32_t* anc_arena;        /* [n_steps][B][P]; slot k valid iff anc_used[k] */
+  const void* a_prev;        /* unnormalised log-weights of the last weighted step, or NULL */
+  void* a_arena;             /* [n_weighted][B][P] */
+  void* cdf_local;           /* [B][P] uint64 */
+  void* tile_rec;            /* [B][ceil(P/32)] ssm_tile_rec */
+  void* resample_ws;         /* ssm_resample_workspace_bytes(B, P) */
+  int32_t* anc_used;         /* HOST out [n_steps] */
+  int32_t a_last_index;      /* out: a_arena slot of the last weighted step (-1: a_prev) */
+  int32_t pad2;
+  void* const* events;       /* HOST, nullable: 4 cudaEvent_t per step (resample start/end, pw start/end) */
+} ssm_advance_args;
+
+int ssm_advance(ssm_advance_args* args, void* stream);
+int ssm_event_create(void** out);
+int ssm_event_destroy(void* event);
+int ssm_event_elapsed_ms(void* start, void* end, float* ms);
+
 /* K6: ancestor gather x_out[b][s][k] = x_in[b][s][anc[b][k]] (particle.py:102). */
 int ssm_gather(int dtype, int B, int nx, int P, const void* x_in, const int32_t* anc,
                void* x_out, void* stream);

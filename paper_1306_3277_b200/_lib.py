@@ -103,6 +103,53 @@ class PwArgs(C.Structure):
 SSM_HINT_SINGLE_SUBSTEP = 1
 
 
+class StepDesc(C.Structure):
+    _fields_ = [
+        ("step", C.c_int32),
+        ("n_sub", C.c_int32),
+        ("subs_offset", C.c_int64),
+        ("has_obs", C.c_int32),
+        ("obs_mask", C.c_uint32),
+        ("hints", C.c_int32),
+        ("pad", C.c_int32),
+        ("y", C.c_double * 8),
+        ("u_obs", C.c_double),
+    ]
+
+
+STEP_DESC_DTYPE = np.dtype(
+    [("step", "<i4"), ("n_sub", "<i4"), ("subs_offset", "<i8"), ("has_obs", "<i4"), ("obs_mask", "<u4"),
+     ("hints", "<i4"), ("pad", "<i4"), ("y", "<f8", (8,)), ("u_obs", "<f8")]
+)
+assert STEP_DESC_DTYPE.itemsize == C.sizeof(StepDesc) == 104
+
+
+class AdvanceArgs(C.Structure):
+    _fields_ = [
+        ("pw", PwArgs),
+        ("subs_table", C.c_void_p),
+        ("steps", C.c_void_p),
+        ("n_steps", C.c_int32),
+        ("scheme", C.c_int32),
+        ("tiles", C.c_int32),
+        ("maybe_nonuniform", C.c_int32),
+        ("ess_gate", C.c_int32),
+        ("pad", C.c_int32),
+        ("x_in", C.c_void_p),
+        ("x_arena", C.c_void_p),
+        ("anc_arena", C.c_void_p),
+        ("a_prev", C.c_void_p),
+        ("a_arena", C.c_void_p),
+        ("cdf_local", C.c_void_p),
+        ("tile_rec", C.c_void_p),
+        ("resample_ws", C.c_void_p),
+        ("anc_used", C.c_void_p),
+        ("a_last_index", C.c_int32),
+        ("pad2", C.c_int32),
+        ("events", C.c_void_p),
+    ]
+
+
 # name -> (restype, argtypes); every symbol declared in include/ssm_b200.h
 _vp, _i, _sz, _d = C.c_void_p, C.c_int, C.c_size_t, C.c_double
 SIGNATURES = {
@@ -126,6 +173,10 @@ SIGNATURES = {
     "ssm_lse_workspace_bytes": (_sz, [_i, _i]),
     "ssm_logsumexp": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_block_gather": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
+    "ssm_advance": (_i, [C.POINTER(AdvanceArgs), _vp]),
+    "ssm_event_create": (_i, [C.POINTER(C.c_void_p)]),
+    "ssm_event_destroy": (_i, [_vp]),
+    "ssm_event_elapsed_ms": (_i, [_vp, _vp, C.POINTER(C.c_float)]),
 }
 
 # entry points that launch kernels (for the gpu_launches count): name -> launches
@@ -141,6 +192,7 @@ LAUNCHING = {
     "ssm_trace": 1,
     "ssm_logsumexp": 1,
     "ssm_block_gather": 1,
+    "ssm_advance": 0,
 }
 
 _LIB = None
@@ -167,6 +219,8 @@ class _Lib:
                         profiling.count_launch(2)  # offspring + expand
                     elif _name == "ssm_resample_from_logw" and a[3] == 0:
                         profiling.count_launch(2)  # look-back scan + binary search
+                    elif _name == "ssm_advance":
+                        pass  # counted by the caller from the step plan
                     else:
                         profiling.count_launch(_n)
                     return _fn(*a)

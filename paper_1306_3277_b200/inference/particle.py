@@ -128,6 +128,16 @@ class Schedule:
                         yy[n] = y[n]
                 u_obs = _input_value(inputs, t1) if spec.n_input else 0.0
                 self.obs[i] = (bits, yy, u_obs)
+        # native-driver step descriptors (ssm_step_desc), one per grid index
+        self.desc = np.zeros(S + 1, dtype=_lib.STEP_DESC_DTYPE)
+        for i in range(1, S + 1):
+            d = self.desc[i]
+            d["step"], d["n_sub"], d["subs_offset"] = i, self.n_sub[i], self.offsets[i]
+            d["hints"] = _lib.SSM_HINT_SINGLE_SUBSTEP if self.single[i] else 0
+            if self.obs[i] is not None:
+                d["has_obs"], d["obs_mask"] = 1, self.obs[i][0]
+                d["y"] = self.obs[i][1]
+                d["u_obs"] = self.obs[i][2]
         table = np.array(recs, dtype=_lib.SUBSTEP_DTYPE) if recs else np.zeros(1, _lib.SUBSTEP_DTYPE)
         self.table = torch.from_numpy(table.view(np.uint8).copy()).to(device)
         self.times = times
@@ -381,6 +391,69 @@ def init_runs(runs, rngs):
     return runs
 
 
+_RS_LAUNCHES = {("tiles", 0): 3, ("logw", 0): 2, ("logw", 1): 4, ("logw", 2): 4}
+
+
+def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe, x_arena, a_arena,
+                    cdf_local, tile_rec, rs_ws, tiles_ok, scheme, esz, new_hist, stream):
+    """One ssm_advance call for all steps (device noise).  Returns (x_prev,
+    a_last, maybe_nonuniform) and appends (x_out, anc | None) per step."""
+    import ctypes as C
+
+    n = upto - start
+    desc = np.ascontiguousarray(sched.desc[start + 1 : upto + 1])
+    if _NO_HINTS:
+        desc["hints"] = 0
+    anc_arena = torch.empty((n, B, P), dtype=torch.int32, device=args_device(x_arena)) if (maybe or any(
+        desc["has_obs"][:-1])) else None
+    anc_used = np.zeros(n, dtype=np.int32)
+    A = _lib.AdvanceArgs()
+    A.pw = args
+    A.subs_table = sched.table.data_ptr()
+    A.steps = desc.ctypes.data
+    A.n_steps = n
+    A.scheme = scheme
+    A.tiles = 1 if tiles_ok else 0
+    A.maybe_nonuniform = 1 if maybe else 0
+    A.ess_gate = 1 if r0.ess_rel is not None else 0
+    A.x_in = x_prev.data_ptr()
+    A.x_arena = x_arena.data_ptr()
+    A.anc_arena = anc_arena.data_ptr() if anc_arena is not None else None
+    A.a_prev = a_last.data_ptr() if a_last is not None else None
+    A.a_arena = a_arena.data_ptr() if a_arena is not None else None
+    A.cdf_local = cdf_local.data_ptr() if cdf_local is not None else None
+    A.tile_rec = tile_rec.data_ptr() if tile_rec is not None else None
+    A.resample_ws = rs_ws.data_ptr()
+    A.anc_used = anc_used.ctypes.data
+    timer = profiling.active()
+    evs = None
+    if timer is not None:
+        evs = [profiling.NativeEvent() for _ in range(4 * n)]
+        ev_arr = (C.c_void_p * (4 * n))(*[e.h for e in evs])
+        A.events = C.cast(ev_arr, C.c_void_p)
+    _lib.check(L.ssm_advance(A, stream), "ssm_advance")
+    kind = "tiles" if tiles_ok else "logw"
+    rs_n = _RS_LAUNCHES[(kind, 0 if tiles_ok else scheme)]
+    profiling.count_launch(n + rs_n * int(anc_used.sum()))
+    for k in range(n):
+        an = anc_arena[k] if anc_used[k] else None
+        new_hist.append((x_arena[k], an))
+        if timer is not None:
+            has_obs = bool(desc["has_obs"][k])
+            if an is not None:
+                rs_bytes = B * P * ((8 + 4 + 4 + 4) if tiles_ok else (2 * esz + 12))
+                timer.add("resample", evs[4 * k], evs[4 * k + 1], rs_bytes)
+            nbytes = B * P * (2 * spec.nx * esz + (4 if an is not None else 0)
+                              + ((esz + (8 if tiles_ok else 0)) if has_obs else 0))
+            timer.add("propagate_weight", evs[4 * k + 2], evs[4 * k + 3], nbytes)
+    a_new = a_arena[A.a_last_index] if A.a_last_index >= 0 else a_last
+    return x_arena[n - 1], a_new, bool(A.maybe_nonuniform)
+
+
+def args_device(t):
+    return t.device
+
+
 def advance_runs(runs, upto, rngs):
     """Advance a batch of runs (same model, grid, P, settings, position)
     through grid index `upto`; returns the per-run loglik increments
@@ -450,7 +523,11 @@ def advance_runs(runs, upto, rngs):
     a_arena = torch.empty((max(n_res, 1), B, P), dtype=tdt, device=dev) if n_res else None
     anc_arena = None
     a_slot = 0
-    for i in range(start + 1, upto + 1):
+    if not host_noise:
+        x_prev, a_last, maybe_nonuniform = _advance_native(
+            L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe_nonuniform, x_arena, a_arena,
+            cdf_local, tile_rec, rs_ws, tiles_ok, scheme, esz, new_hist, stream)
+    for i in (range(start + 1, upto + 1) if host_noise else ()):
         step_rngs = [g.child(i) for g in rngs] if host_noise else None
         anc = None
         if maybe_nonuniform:

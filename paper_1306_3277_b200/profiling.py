@@ -26,9 +26,42 @@ def launch_count():
     return _LAUNCHES
 
 
+class NativeEvent:
+    """cudaEvent_t owned by libssm_b200 (recorded inside native drivers)."""
+
+    def __init__(self):
+        import ctypes as C
+
+        from . import _lib
+
+        h = C.c_void_p()
+        _lib.check(_lib.lib().ssm_event_create(C.byref(h)), "ssm_event_create")
+        self.h = h.value
+
+    def elapsed_time(self, end):
+        import ctypes as C
+
+        from . import _lib
+
+        ms = C.c_float()
+        _lib.check(_lib.lib().ssm_event_elapsed_ms(self.h, end.h, C.byref(ms)), "ssm_event_elapsed_ms")
+        return float(ms.value)
+
+    def __del__(self):
+        try:
+            from . import _lib
+
+            _lib.lib().ssm_event_destroy(self.h)
+        except Exception:
+            pass
+
+
 class KernelTimer:
     def __init__(self):
         self.events = defaultdict(list)  # name -> [(start, end, bytes)]
+
+    def add(self, name, start, end, nbytes=0):
+        self.events[name].append((start, end, nbytes))
 
     @contextlib.contextmanager
     def kernel(self, name, nbytes=0):

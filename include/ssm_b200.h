@@ -126,7 +126,11 @@ typedef struct ssm_pw_args {
   void* cdf_local;      /* [B][P] uint64 tile-local fixed-point CDF for the next resample, or NULL */
   void* tile_rec;       /* [B][ceil(P/32)] ssm_tile_rec (one per warp tile), or NULL */
   uint32_t hints;       /* SSM_HINT_* bits the host guarantees */
-  uint32_t pad_hints;
+  int32_t p_offset;     /* global index of particle 0 (device RNG counters; sharded filter) */
+  int32_t x_in_stride;  /* row stride of x_in in particles (0: P) */
+  int32_t pad_args;
+  void* lse_out;        /* [B][4] doubles or NULL: if set, the finalize writes the LSE/ESS partial
+                           (m, c, t, s2) here instead of updating fs (cross-rank combine) */
 } ssm_pw_args;
 
 /* hint: subs[0] is the only sub-step and holds exactly one RK4 step (n_ode == 1) */
@@ -154,8 +158,15 @@ int ssm_propagate_weight(const ssm_pw_args* args, void* stream);
 /* K7: initial particles (simulate.sample_initial, simulate.py:111-129) drawn
  * on the device: L96 x ~ U(-1,3) (Lorenz96.bi:21), windkessel Pp ~ N(90,15)
  * (Windkessel.bi:24).  keys: [B][2]. */
-int ssm_init_particles(int model, int dtype, int B, int P, const uint32_t* keys,
+int ssm_init_particles(int model, int dtype, int B, int P, int p_offset, const uint32_t* keys,
                        void* x_out, void* stream);
+
+/* Cross-rank finalize of a weighted step for a filter sharded over W ranks
+ * (C1): combines the W per-rank partials (m, c, t, s2) in rank order and
+ * performs the finalize of ssm_propagate_weight (loglik, degenerate flag, ESS
+ * gate against P_total) on fs. parts: [W][B][4] doubles. */
+int ssm_lse_combine(int W, int B, const double* parts, ssm_filter_state* fs, double ess_rel,
+                    double P_total, int step, void* stream);
 
 /* K4: per-filter CDF of the resampling weights as an exact, deterministic
  * 64-bit fixed-point inclusive scan (decoupled look-back), replacing
@@ -255,9 +266,37 @@ int ssm_event_create(void** out);
 int ssm_event_destroy(void* event);
 int ssm_event_elapsed_ms(void* start, void* end, float* ms);
 
+/* Single filter sharded over ranks (config 5).  Each rank holds P
+ * consecutive particles of a P_global filter.  After the weighted step (run
+ * with ssm_pw_args.lse_out and combined by ssm_lse_combine):
+ *   1. ssm_tiles_total: this rank's fixed-point weight total (uint64 [B]);
+ *   2. host: all-gather the totals -> this rank's global offset g_off and the
+ *      global total g_tot (C1);
+ *   3. ssm_offspring_global: global offspring bounds of the local particles,
+ *      shifted by the rank's first output (shift_out), + partition;
+ *      c_last_out = number of outputs the local particles own;
+ *   4. ssm_expand_own: the local ancestor of each owned output;
+ *   5. host: all-gather (first output, count) per rank and move the states of
+ *      outputs owned here but slotted on other ranks (C3).
+ * Draws use global indices, so the result does not depend on the rank count. */
+size_t ssm_sharded_workspace_bytes(int B, int P, int P_global);
+int ssm_tiles_total(int B, int P, const void* tile_rec, const ssm_filter_state* fs, uint64_t* total_out,
+                    void* workspace, void* stream);
+int ssm_offspring_global(int B, int P, int P_global, int scheme, const void* cdf_local, const uint64_t* g_off,
+                         const uint64_t* g_tot, const double* u, const uint32_t* keys, int step,
+                         const ssm_filter_state* fs, int32_t* shift_out, int32_t* c_last_out, void* workspace,
+                         void* stream);
+int ssm_expand_own(int B, int P, int P_global, int n_own, const ssm_filter_state* fs, int32_t* anc_out,
+                   void* workspace, void* stream);
+
 /* K6: ancestor gather x_out[b][s][k] = x_in[b][s][anc[b][k]] (particle.py:102). */
 int ssm_gather(int dtype, int B, int nx, int P, const void* x_in, const int32_t* anc,
                void* x_out, void* stream);
+
+/* Strided gather out[s][k] = x_in[s][idx[k]] (x_in rows of in_stride particles,
+ * out rows of n_out): the cross-rank spill of the sharded filter. */
+int ssm_gather_cols(int dtype, int nx, int n_out, int in_stride, const void* x_in, const int32_t* idx,
+                    void* x_out, void* stream);
 
 /* K8: ancestry trace (ParticleRun.sample_trajectory, particle.py:137-149).
  * xs[b*(S+1) + i] points at history position array x_i of filter b

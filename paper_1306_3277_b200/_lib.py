@@ -96,7 +96,10 @@ class PwArgs(C.Structure):
         ("cdf_local", C.c_void_p),
         ("tile_rec", C.c_void_p),
         ("hints", C.c_uint32),
-        ("pad_hints", C.c_uint32),
+        ("p_offset", C.c_int32),
+        ("x_in_stride", C.c_int32),
+        ("pad_args", C.c_int32),
+        ("lse_out", C.c_void_p),
     ]
 
 
@@ -159,7 +162,8 @@ SIGNATURES = {
     "ssm_sm_count": (_i, [_i, C.POINTER(C.c_int)]),
     "ssm_pw_workspace_bytes": (_sz, [_i, _i]),
     "ssm_propagate_weight": (_i, [C.POINTER(PwArgs), _vp]),
-    "ssm_init_particles": (_i, [_i, _i, _i, _i, _vp, _vp, _vp]),
+    "ssm_init_particles": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp]),
+    "ssm_lse_combine": (_i, [_i, _i, _vp, _vp, _d, _d, _i, _vp]),
     "ssm_scan_workspace_bytes": (_sz, [_i, _i]),
     "ssm_weights_scan": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ssm_fixed_to_cum": (_i, [_i, _i, _vp, _vp, _vp]),
@@ -169,11 +173,16 @@ SIGNATURES = {
     "ssm_resample_from_logw": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ssm_resample_from_tiles": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ssm_gather": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "ssm_gather_cols": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "ssm_trace": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_lse_workspace_bytes": (_sz, [_i, _i]),
     "ssm_logsumexp": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_block_gather": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
     "ssm_advance": (_i, [C.POINTER(AdvanceArgs), _vp]),
+    "ssm_sharded_workspace_bytes": (_sz, [_i, _i, _i]),
+    "ssm_tiles_total": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "ssm_offspring_global": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp]),
+    "ssm_expand_own": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "ssm_event_create": (_i, [C.POINTER(C.c_void_p)]),
     "ssm_event_destroy": (_i, [_vp]),
     "ssm_event_elapsed_ms": (_i, [_vp, _vp, C.POINTER(C.c_float)]),
@@ -183,16 +192,21 @@ SIGNATURES = {
 LAUNCHING = {
     "ssm_propagate_weight": 1,
     "ssm_init_particles": 1,
+    "ssm_lse_combine": 1,
     "ssm_weights_scan": 1,
     "ssm_fixed_to_cum": 1,
     "ssm_resample_search": 1,
     "ssm_resample_from_logw": 4,
     "ssm_resample_from_tiles": 3,
     "ssm_gather": 1,
+    "ssm_gather_cols": 1,
     "ssm_trace": 1,
     "ssm_logsumexp": 1,
     "ssm_block_gather": 1,
     "ssm_advance": 0,
+    "ssm_tiles_total": 2,
+    "ssm_offspring_global": 2,
+    "ssm_expand_own": 1,
 }
 
 _LIB = None

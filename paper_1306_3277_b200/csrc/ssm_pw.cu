@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const bool uniform_in = R || fs->uniform;
   const double incr_prev = fs->incr;
   const size_t base = static_cast<size_t>(b) * NX * P;
-  const T* __restrict__ xin = static_cast<const T*>(A.x_in) + base;
+  const int in_stride = A.x_in_stride > 0 ? A.x_in_stride : P;  // sharded filter: local + received states
+  const T* __restrict__ xin = static_cast<const T*>(A.x_in) + static_cast<size_t>(b) * NX * in_stride;
   T* __restrict__ xout = static_cast<T*>(A.x_out) + base;
   const int32_t* __restrict__ anc =
       (R && A.anc != nullptr) ? A.anc + static_cast<size_t>(b) * P : nullptr;
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const int p0 = blockIdx.x * kThreads + threadIdx.x;
   auto load_x = [&](int pp, int src) {
 #pragma unroll
-    for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * P + src];
+    for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * in_stride + src];
   };
   if (p0 < P) load_x(p0, anc ? __ldg(anc + p0) : p0);
   int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride;
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
     if (act) {
       if constexpr (SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ) {
         T z[8];
-        normals8<T>(k0, k1, static_cast<uint32_t>(p), static_cast<uint32_t>(A.step), 0u, z);
+        normals8<T>(k0, k1, static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step), 0u, z);
         T Fn[8];
 #pragma unroll
         for (int n = 0; n < 8; ++n) Fn[n] = fma(s_c, z[n], s_F);  // F + sqrt(sigma2) sd z / h
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
 #pragma unroll
             for (int n = 0; n < 8; ++n) W[n] = noise[(static_cast<size_t>(k) * 8 + n) * P + p];
           } else {
-            normals8<T>(k0, k1, static_cast<uint32_t>(p), static_cast<uint32_t>(A.step),
+            normals8<T>(k0, k1, static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
                         static_cast<uint32_t>(k), W);
             const T sd = static_cast<T>(S.sd);
 #pragma unroll
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
           if constexpr (INJ) {
             xi = noise[static_cast<size_t>(k) * P + p];
           } else {
-            xi = static_cast<T>(th[3]) * normal1<T>(k0, k1, static_cast<uint32_t>(p),
+            xi = static_cast<T>(th[3]) * normal1<T>(k0, k1, static_cast<uint32_t>(p + A.p_offset),
                                                     static_cast<uint32_t>(A.step), static_cast<uint32_t>(k));
           }
           x[0] = O::add(O::mul(ca, x[0]), O::mul(cb, O::add(static_cast<T>(S.u_in), xi)));
@@ -413,7 +414,14 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
       acc = lse_combine(acc, q);
     }
     acc = lse_block_reduce<kThreads>(acc, red);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && A.lse_out) {
+      // sharded filter: hand the rank's partial to the cross-rank combine (C1)
+      double* o = static_cast<double*>(A.lse_out) + 4 * b;
+      o[0] = acc.m;
+      o[1] = acc.c;
+      o[2] = acc.t;
+      o[3] = acc.s2;
+    } else if (threadIdx.x == 0) {
       const double incr = lse_value(acc);
       const double ess = lse_ess(acc);
       if (!isfinite(incr)) {
@@ -463,7 +471,7 @@ static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
 // ----------------------------- K7: init ------------------------------------
 
 template <int MODEL, typename T>
-__global__ void __launch_bounds__(kThreads) init_kernel(int P, const uint32_t* keys, T* x) {
+__global__ void __launch_bounds__(kThreads) init_kernel(int P, int p_offset, const uint32_t* keys, T* x) {
   const int b = blockIdx.y;
   const uint32_t k0 = keys[2 * b], k1 = keys[2 * b + 1];
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
@@ -473,13 +481,13 @@ __global__ void __launch_bounds__(kThreads) init_kernel(int P, const uint32_t* k
       // x[n] ~ uniform(-1.0, 3.0): low + (high - low) * U  (Lorenz96.bi:21)
 #pragma unroll
       for (uint32_t g = 0; g < 4; ++g) {
-        const U4 r = philox4x32_10(U4{static_cast<uint32_t>(p), 0u, g, kPurposeInit}, k0, k1);
+        const U4 r = philox4x32_10(U4{static_cast<uint32_t>(p + p_offset), 0u, g, kPurposeInit}, k0, k1);
         xb[static_cast<size_t>(2 * g) * P + p] = static_cast<T>(-1.0 + 4.0 * u53(r.x, r.y));
         xb[static_cast<size_t>(2 * g + 1) * P + p] = static_cast<T>(-1.0 + 4.0 * u53(r.z, r.w));
       }
     } else {
       // Pp ~ gaussian(90.0, 15.0)  (Windkessel.bi:24)
-      const U4 r = philox4x32_10(U4{static_cast<uint32_t>(p), 0u, 0u, kPurposeInit}, k0, k1);
+      const U4 r = philox4x32_10(U4{static_cast<uint32_t>(p + p_offset), 0u, 0u, kPurposeInit}, k0, k1);
       double z0, z1;
       box_muller(r.x, r.y, r.z, r.w, z0, z1);
       xb[p] = static_cast<T>(90.0 + 15.0 * z0);
@@ -526,24 +534,61 @@ extern "C" int ssm_propagate_weight(const ssm_pw_args* args, void* stream) {
   return SSM_OK;
 }
 
-extern "C" int ssm_init_particles(int model, int dtype, int B, int P, const uint32_t* keys,
+extern "C" int ssm_init_particles(int model, int dtype, int B, int P, int p_offset, const uint32_t* keys,
                                   void* x_out, void* stream) {
   if (B <= 0 || P <= 0 || B > 65535 || !keys || !x_out) return SSM_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const dim3 grid(pw_grid_x(P), B);
   if (model == SSM_MODEL_LORENZ96) {
     if (dtype == SSM_F64)
-      init_kernel<SSM_MODEL_LORENZ96, double><<<grid, kThreads, 0, s>>>(P, keys, (double*)x_out);
+      init_kernel<SSM_MODEL_LORENZ96, double><<<grid, kThreads, 0, s>>>(P, p_offset, keys, (double*)x_out);
     else
-      init_kernel<SSM_MODEL_LORENZ96, float><<<grid, kThreads, 0, s>>>(P, keys, (float*)x_out);
+      init_kernel<SSM_MODEL_LORENZ96, float><<<grid, kThreads, 0, s>>>(P, p_offset, keys, (float*)x_out);
   } else if (model == SSM_MODEL_WINDKESSEL) {
     if (dtype == SSM_F64)
-      init_kernel<SSM_MODEL_WINDKESSEL, double><<<grid, kThreads, 0, s>>>(P, keys, (double*)x_out);
+      init_kernel<SSM_MODEL_WINDKESSEL, double><<<grid, kThreads, 0, s>>>(P, p_offset, keys, (double*)x_out);
     else
-      init_kernel<SSM_MODEL_WINDKESSEL, float><<<grid, kThreads, 0, s>>>(P, keys, (float*)x_out);
+      init_kernel<SSM_MODEL_WINDKESSEL, float><<<grid, kThreads, 0, s>>>(P, p_offset, keys, (float*)x_out);
   } else {
     return SSM_ERR_UNSUPPORTED;
   }
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+// ----------------------------- C1: cross-rank finalize ----------------------
+
+namespace ssm {
+__global__ void lse_combine_kernel(int W, int B, const double* parts, ssm_filter_state* fs, double ess_rel,
+                                   double P_total, int step) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  Lse acc = lse_empty();
+  for (int r = 0; r < W; ++r) {  // rank order: deterministic
+    const double* q = parts + (static_cast<size_t>(r) * B + b) * 4;
+    acc = lse_combine(acc, Lse{q[0], q[1], q[2], q[3]});
+  }
+  ssm_filter_state* f = fs + b;
+  const double incr = lse_value(acc);
+  const double ess = lse_ess(acc);
+  if (!isfinite(incr)) {
+    f->err_degenerate = min(f->err_degenerate, step);
+  } else {
+    f->loglik += incr;
+  }
+  f->incr = incr;
+  f->lse_raw = incr;
+  f->ess = ess;
+  f->uniform = 0;
+  f->resample_now = (ess_rel < 0.0) ? 1 : (ess < ess_rel * P_total ? 1 : 0);
+}
+}  // namespace ssm
+
+extern "C" int ssm_lse_combine(int W, int B, const double* parts, ssm_filter_state* fs, double ess_rel,
+                               double P_total, int step, void* stream) {
+  if (W <= 0 || B <= 0 || !parts || !fs) return SSM_ERR_INVALID_ARG;
+  ssm::lse_combine_kernel<<<(B + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(W, B, parts, fs, ess_rel,
+                                                                                          P_total, step);
   SSM_CHECK_LAUNCH();
   return SSM_OK;
 }

@@ -501,13 +501,18 @@ blk_prefix_kernel(int nblk, uint64_t* __restrict__ blk, uint64_t* __restrict__ t
 }
 
 // c_j for every particle + merge-path partition entries
+// g_off (nullable, sharded filter): global fixed-point offset of this rank's
+// first particle; `totals` is then the global total and P_out the global
+// particle count.  c_shift (nullable): subtracted from every stored c_j (the
+// rank's first output), so partition and expand work on the rank's own outputs.
 template <int SCHEME, int SRC, typename T>
 __global__ void __launch_bounds__(kThreads)
 offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double* __restrict__ shift,
                  const uint64_t* __restrict__ tile_prefix, const uint64_t* __restrict__ totals,
                  const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
                  const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ cnt,
-                 int32_t* __restrict__ split, int ndiag) {
+                 int32_t* __restrict__ split, int ndiag, const uint64_t* __restrict__ g_off = nullptr,
+                 const int32_t* __restrict__ c_shift = nullptr) {
   __shared__ uint64_t sm[kScanTile + kScanTile / 8];
   __shared__ uint64_t warp_tot[kThreads / 32];
   const int b = blockIdx.y, tile = blockIdx.x;
@@ -546,9 +551,10 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
     const bool ok = tw < nt;
     const double sc = ok ? shift[static_cast<size_t>(b) * nt + tw] : 0.0;
     const uint64_t* blk_pre = tile_prefix + static_cast<size_t>(B_total_tiles_offset(nt, gridDim.y));
-    const uint64_t pre = ok ? tile_prefix[static_cast<size_t>(b) * nt + tw] +
-                                  blk_pre[static_cast<size_t>(b) * nblk + tw / kRecPerBlock]
-                            : 0ull;
+    const uint64_t goff = g_off ? g_off[b] : 0ull;
+    const uint64_t pre = goff + (ok ? tile_prefix[static_cast<size_t>(b) * nt + tw] +
+                                          blk_pre[static_cast<size_t>(b) * nblk + tw / kRecPerBlock]
+                                    : 0ull);
     const double inv = 1.0 / static_cast<double>(totals[b]);
     uint64_t lv[kScanItems];
     if (jt + kScanItems <= P_in && (P_in & 7) == 0) {  // 4 x 16-byte vector loads, aligned
@@ -567,9 +573,13 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
     for (int i = 0; i < kScanItems; ++i) {
       const int j = jt + i;
       cum[i] = j < P_in ? static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(lv[i]))) * inv : 2.0;
-      if (j == P_in - 1) cum[i] = 1.0;  // cum[-1] = 1.0 (resampling.py:27)
+      if (j == P_in - 1 && (!g_off || goff + blk_pre[static_cast<size_t>(b) * nblk + nblk - 1] +
+                                              tile_prefix[static_cast<size_t>(b) * nt + nt - 1] +
+                                              __double2ull_rn(shift[static_cast<size_t>(b) * nt + nt - 1] *
+                                                              static_cast<double>(cl[P_in - 1])) == totals[b]))
+        cum[i] = 1.0;  // cum[-1] = 1.0 (resampling.py:27)
     }
-    cum_prev = jt == 0 ? 0.0
+    cum_prev = jt == 0 ? static_cast<double>(goff) * inv
                : ((jt & 31) == 0 ? static_cast<double>(pre) * inv
                                  : static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(cl[jt - 1]))) * inv);
   } else {
@@ -637,14 +647,16 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
   }
 
   if (jt >= P_in) return;
-  int c_prev = jt > 0 ? offspring_bound<SCHEME>(cum_prev, u_sys, U, k0, k1, step, P_out, invP, pow2) : 0;
+  const int cshift = c_shift ? c_shift[b] : 0;
+  int c_prev = (jt > 0 || g_off) ? offspring_bound<SCHEME>(cum_prev, u_sys, U, k0, k1, step, P_out, invP, pow2) - cshift
+                                 : 0;
   const int total = P_in + P_out;
   int32_t cvals[kScanItems];
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     const int j = jt + i;
     if (j >= P_in) break;
-    const int c = offspring_bound<SCHEME>(cum[i], u_sys, U, k0, k1, step, P_out, invP, pow2);
+    const int c = offspring_bound<SCHEME>(cum[i], u_sys, U, k0, k1, step, P_out, invP, pow2) - cshift;
     cvals[i] = c;
     // diagonal boundaries D in (j-1 + c_prev, j + c] are split at particle j
     const int lo = j - 1 + c_prev, hi = j + c;
@@ -794,6 +806,18 @@ gather_kernel(int nx, int P, const T* __restrict__ x, const int32_t* __restrict_
   for (int k = blockIdx.x * kThreads + threadIdx.x; k < P; k += gridDim.x * kThreads) {
     const int src = ab[k];
     for (int n = 0; n < nx; ++n) out[base + static_cast<size_t>(n) * P + k] = x[base + static_cast<size_t>(n) * P + src];
+  }
+}
+
+// out[n][k] = x[n][idx[k]]: x rows of length in_stride, out rows of length n_out
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+gather_cols_kernel(int nx, int n_out, int in_stride, const T* __restrict__ x, const int32_t* __restrict__ idx,
+                   T* __restrict__ out) {
+  for (int k = blockIdx.x * kThreads + threadIdx.x; k < n_out; k += gridDim.x * kThreads) {
+    const int src = idx[k];
+    for (int n = 0; n < nx; ++n)
+      out[static_cast<size_t>(n) * n_out + k] = x[static_cast<size_t>(n) * in_stride + src];
   }
 }
 
@@ -1068,6 +1092,104 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
   return SSM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Sharded single filter (config 5): the three resampling phases around the
+// host-side collectives.
+// ---------------------------------------------------------------------------
+
+template <int SCHEME>
+__global__ void rank_start_kernel(int B, int P_global, const uint64_t* g_off, const uint64_t* g_tot,
+                                  const double* u, const uint32_t* keys, int step, int32_t* shift) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const bool pow2 = (P_global & (P_global - 1)) == 0;
+  const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
+  const double u_sys = SCHEME == SSM_SYSTEMATIC
+                           ? (u ? u[b] : device_uniform(k0, k1, 0u, step, kPurposeSystematic))
+                           : 0.0;
+  const double* U = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * P_global : nullptr;
+  const double cum = static_cast<double>(g_off[b]) / static_cast<double>(g_tot[b]);
+  shift[b] = offspring_bound<SCHEME>(cum, u_sys, U, k0, k1, step, P_global, 1.0 / static_cast<double>(P_global), pow2);
+}
+
+extern "C" int ssm_tiles_total(int B, int P, const void* tile_rec, const ssm_filter_state* fs,
+                               uint64_t* total_out, void* workspace, void* stream) {
+  if (B <= 0 || P <= 0 || !tile_rec || !fs || !total_out || !workspace) return SSM_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SearchWs w;
+  search_ws_layout(B, P, P, workspace, &w);
+  const int nt = (P + 31) / 32;
+  const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
+  double* scale = reinterpret_cast<double*>(w.C);
+  uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + static_cast<size_t>(B) * nt;
+  uint64_t* blk = pref + B_total_tiles_offset(nt, B);
+  tile_scale_kernel<<<dim3(nblk, B), kThreads, 0, s>>>(nt, static_cast<const ssm_tile_rec*>(tile_rec), fs, scale,
+                                                      pref, blk);
+  blk_prefix_kernel<<<B, 1024, 0, s>>>(nblk, blk, total_out, fs);
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+extern "C" int ssm_offspring_global(int B, int P, int P_global, int scheme, const void* cdf_local,
+                                    const uint64_t* g_off, const uint64_t* g_tot, const double* u,
+                                    const uint32_t* keys, int step, const ssm_filter_state* fs, int32_t* shift_out,
+                                    int32_t* c_last_out, void* workspace, void* stream) {
+  if (B <= 0 || P <= 0 || P_global < P || !cdf_local || !g_off || !g_tot || !fs || !shift_out || !workspace)
+    return SSM_ERR_INVALID_ARG;
+  if (!u && !keys) return SSM_ERR_INVALID_ARG;
+  if (scheme != SSM_SYSTEMATIC && scheme != SSM_STRATIFIED) return SSM_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SearchWs w;
+  search_ws_layout(B, P, P_global, workspace, &w);
+  const int nt = (P + 31) / 32;
+  double* scale = reinterpret_cast<double*>(w.C);
+  uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + static_cast<size_t>(B) * nt;
+  const int nd_max = ndiag_of(P, P_global);
+  const dim3 g(scan_tiles(P), B);
+  if (scheme == SSM_SYSTEMATIC) {
+    rank_start_kernel<SSM_SYSTEMATIC><<<(B + 127) / 128, 128, 0, s>>>(B, P_global, g_off, g_tot, u, keys, step, shift_out);
+    offspring_kernel<SSM_SYSTEMATIC, kCumTiles, double><<<g, kThreads, 0, s>>>(
+        P, P_global, cdf_local, scale, pref, g_tot, u, keys, step, fs, w.cnt, w.split, nd_max, g_off, shift_out);
+  } else {
+    rank_start_kernel<SSM_STRATIFIED><<<(B + 127) / 128, 128, 0, s>>>(B, P_global, g_off, g_tot, u, keys, step, shift_out);
+    offspring_kernel<SSM_STRATIFIED, kCumTiles, double><<<g, kThreads, 0, s>>>(
+        P, P_global, cdf_local, scale, pref, g_tot, u, keys, step, fs, w.cnt, w.split, nd_max, g_off, shift_out);
+  }
+  if (c_last_out) {
+    for (int b = 0; b < B; ++b) {
+      cudaError_t e = cudaMemcpyAsync(c_last_out + b, w.cnt + static_cast<size_t>(b) * P + P - 1, sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) {
+        ssm_set_last_error(e);
+        return SSM_ERR_CUDA;
+      }
+    }
+  }
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+extern "C" int ssm_expand_own(int B, int P, int P_global, int n_own, const ssm_filter_state* fs, int32_t* anc_out,
+                              void* workspace, void* stream) {
+  if (B <= 0 || P <= 0 || n_own < 0 || !fs || !anc_out || !workspace) return SSM_ERR_INVALID_ARG;
+  if (n_own == 0) return SSM_OK;
+  SearchWs w;
+  search_ws_layout(B, P, P_global, workspace, &w);
+  const int nd = ndiag_of(P, n_own);
+  const int nd_max = ndiag_of(P, P_global);
+  // splits were written with stride nd_max + 1 per filter; B == 1 for the sharded filter
+  if (B != 1) return SSM_ERR_UNSUPPORTED;
+  expand_kernel<<<dim3(nd, B), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(P, n_own, w.cnt, w.split, nd, fs,
+                                                                                  anc_out);
+  (void)nd_max;
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+extern "C" size_t ssm_sharded_workspace_bytes(int B, int P, int P_global) {
+  return search_ws_layout(B, P, P_global, nullptr, nullptr);
+}
+
 extern "C" size_t ssm_resample_workspace_bytes(int B, int P) {
   return ssm_search_workspace_bytes(B, P, P);
 }
@@ -1115,6 +1237,22 @@ extern "C" int ssm_gather(int dtype, int B, int nx, int P, const void* x_in, con
     gather_kernel<double><<<g, kThreads, 0, s>>>(nx, P, (const double*)x_in, anc, (double*)x_out);
   else if (dtype == SSM_F32)
     gather_kernel<float><<<g, kThreads, 0, s>>>(nx, P, (const float*)x_in, anc, (float*)x_out);
+  else
+    return SSM_ERR_INVALID_ARG;
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+extern "C" int ssm_gather_cols(int dtype, int nx, int n_out, int in_stride, const void* x_in, const int32_t* idx,
+                               void* x_out, void* stream) {
+  if (nx <= 0 || n_out < 0 || in_stride <= 0 || !x_in || !idx || !x_out) return SSM_ERR_INVALID_ARG;
+  if (n_out == 0) return SSM_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int g = grid_for(n_out, kThreads, 8192);
+  if (dtype == SSM_F64)
+    gather_cols_kernel<double><<<g, kThreads, 0, s>>>(nx, n_out, in_stride, (const double*)x_in, idx, (double*)x_out);
+  else if (dtype == SSM_F32)
+    gather_cols_kernel<float><<<g, kThreads, 0, s>>>(nx, n_out, in_stride, (const float*)x_in, idx, (float*)x_out);
   else
     return SSM_ERR_INVALID_ARG;
   SSM_CHECK_LAUNCH();

@@ -365,11 +365,11 @@ def init_runs(runs, rngs):
             keys = np.stack([device_key(rngs[b]) for b in need_draw]).astype(np.uint32)
             kt = torch.from_numpy(keys.view(np.int32)).to(dev)
             if len(need_draw) == B:
-                _lib.check(_lib.lib().ssm_init_particles(spec.kernel, r0.dtype_id, B, P, _lib.ptr(kt),
+                _lib.check(_lib.lib().ssm_init_particles(spec.kernel, r0.dtype_id, B, P, 0, _lib.ptr(kt),
                                                          _lib.ptr(x), _lib.stream_ptr()), "ssm_init_particles")
             else:
                 tmp = torch.empty((len(need_draw), spec.nx, P), dtype=r0.tdtype, device=dev)
-                _lib.check(_lib.lib().ssm_init_particles(spec.kernel, r0.dtype_id, len(need_draw), P,
+                _lib.check(_lib.lib().ssm_init_particles(spec.kernel, r0.dtype_id, len(need_draw), P, 0,
                                                          _lib.ptr(kt), _lib.ptr(tmp), _lib.stream_ptr()),
                            "ssm_init_particles")
                 for j, b in enumerate(need_draw):

@@ -39,13 +39,34 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
-def test_struct_layouts_match_header():
+def test_struct_layouts_match_header(tmp_path):
+    """ABI check: compile the header with gcc and compare sizeof/offsetof of
+    every struct with the ctypes mirrors in _lib."""
     import ctypes as C
+    import subprocess
 
-    assert C.sizeof(_lib.Substep) == 64
-    assert _lib.FILTER_STATE_DTYPE.itemsize == 64
-    # PwArgs: 10 int32 + 8 doubles + 5 doubles + 11 pointers
-    assert C.sizeof(_lib.PwArgs) == 10 * 4 + 13 * 8 + 13 * 8 + 8
+    structs = {"ssm_pw_args": _lib.PwArgs, "ssm_substep": _lib.Substep, "ssm_step_desc": _lib.StepDesc,
+               "ssm_advance_args": _lib.AdvanceArgs}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ssm_b200.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{name}.{fname} %zu\\n", offsetof({name}, {fname}));')
+    lines.append('  printf("ssm_filter_state %zu\\n", sizeof(ssm_filter_state));')
+    lines.append('  printf("ssm_tile_rec %zu\\n", sizeof(ssm_tile_rec));')
+    lines.append("  return 0; }")
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == C.sizeof(cls), name
+        for fname, _ in cls._fields_:
+            assert int(got[f"{name}.{fname}"]) == getattr(cls, fname).offset, (name, fname)
+    assert int(got["ssm_filter_state"]) == _lib.FILTER_STATE_DTYPE.itemsize
+    assert int(got["ssm_tile_rec"]) == 16
+    assert int(got["ssm_step_desc"]) == _lib.STEP_DESC_DTYPE.itemsize
 
 
 def test_status_strings_no_device_needed():

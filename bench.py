@@ -142,19 +142,33 @@ def run_ours(args, rank, world):
     from paper_1306_3277_b200 import LORENZ96, RngStream, profiling
     from paper_1306_3277_b200.inference import build_filter_grid, particle_filter
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     P, T = args.particles, args.T
     times, ot, ov, om = synthetic_data(T)
     grid = build_filter_grid(0.0, times[-1], T, ot, ov, om, n_obs=8)
     opts = dict(dtype=args.dtype, exact=args.exact, noise="device")
 
+    sharded = world > 1 and args.mode == "sharded"
+
+    class _Out:
+        def __init__(self, ll, traj):
+            self.loglik, self.trajectory = ll, traj
+
+    def call(rng, grid_obj):
+        if sharded:  # one filter of world * P particles, NCCL collectives every weighted step (config 5)
+            from paper_1306_3277_b200.inference import particle_filter_sharded
+
+            return _Out(*particle_filter_sharded(LORENZ96, THETA, grid_obj, rng, world * P, resampler="systematic",
+                                                 dtype=args.dtype, exact=args.exact))
+        return particle_filter(LORENZ96, THETA, grid_obj, rng, n_particles=P, resampler="systematic", **opts)
+
     def one(step, grid_obj, timer=None):
-        rng = RngStream(7, (rank, step))
+        rng = RngStream(7, ((0 if sharded else rank), step))
         if timer is None:
-            return particle_filter(LORENZ96, THETA, grid_obj, rng, n_particles=P, resampler="systematic", **opts)
+            return call(rng, grid_obj)
         with profiling.timing(timer):
-            return particle_filter(LORENZ96, THETA, grid_obj, rng, n_particles=P, resampler="systematic", **opts)
+            return call(rng, grid_obj)
 
     dist = world > 1
     if dist:
@@ -294,6 +308,8 @@ def main():
     ap.add_argument("--exact", action="store_true",
                     help="bitwise reference op order (no FMA contraction); default: FMA-contracted float64")
     ap.add_argument("--variants", type=int, default=1, help="also time f64-exact and f32 variants")
+    ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
+                    help="N>1: one filter of N*2^24 particles across GPUs (default) or N independent filters")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--ref-particles", type=int, default=1 << 17)
@@ -312,8 +328,9 @@ def main():
         import torch
         import torch.distributed as tdist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+        # SSM_BENCH_BACKEND=gloo only to exercise the N>1 harness on a single GPU
+        tdist.init_process_group(os.environ.get("SSM_BENCH_BACKEND", "nccl"))
     res = run_ours(args, rank, world)
     if rank != 0:
         if world > 1:
@@ -345,7 +362,10 @@ def main():
         "vs_baseline": None,
         "dtype": dtype_tag,
         "data": "synthetic (L96 theta*=(10,0.1) simulated per SURVEY 8d; device Philox noise)",
-        "config": dict(workload_config(P, T, args.dtype), arithmetic=arith),
+        "config": dict(workload_config(P, T, args.dtype), arithmetic=arith,
+                       parallelism=("replicas" if world == 1 or args.mode == "replicas"
+                                    else f"one filter sharded over {world} GPUs (NCCL all-gather of LSE partials and "
+                                         "CDF totals + P2P spill of ancestor states per step)")),
         "roofline": {
             "bound": "hbm",
             "kernel": "pw_kernel (fused ancestor gather + RK4 propagate + weight + LSE)",
@@ -362,6 +382,9 @@ def main():
         "clocks": res["clocks"],
         "loglik_mean": float(np.mean(res["logliks"])),
     }
+    if world > 1 and args.mode == "sharded":
+        line["config"]["global_batch"] = world * P
+        line["config"]["particles"] = world * P
     if res["e2e_ms"] is not None:
         line["e2e"] = {"value": world * P * T / (res["e2e_ms"] / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],

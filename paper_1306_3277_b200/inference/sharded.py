@@ -23,7 +23,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .. import _lib
+from .. import _lib, profiling
 from ..distributed import Shard, exchange
 from ..errors import DegenerateEnsembleError, NonFiniteStateError
 from ..models import LOG_SQRT_2PI, resolve_model
@@ -117,8 +117,9 @@ class ShardedParticleFilter:
             anc = gidx = None
             x_in, stride = x_prev, 0
             if maybe:
-                x_in, stride, anc, gidx = self._resample(L, i, x_prev, a_last, fs, cdf, trec, tot, shift, c_last, sw,
-                                                         keys1, scheme, stream)
+                with profiling.maybe("resample", Pl * (8 + 4 + 4 + 4)):
+                    x_in, stride, anc, gidx = self._resample(L, i, x_prev, a_last, fs, cdf, trec, tot, shift, c_last,
+                                                             sw, keys1, scheme, stream)
             obs = sched.obs[i]
             x_out = torch.empty((spec.nx, Pl), dtype=tdt, device=dev)
             a_out = torch.empty(Pl, dtype=tdt, device=dev) if obs is not None else None
@@ -138,7 +139,10 @@ class ShardedParticleFilter:
                     A.y[n] = float(obs[1][n])
             else:
                 A.has_obs, A.obs_mask = 0, 0
-            _lib.check(L.ssm_propagate_weight(A, stream), "ssm_propagate_weight")
+            esz = 8 if self.dtype_id == _lib.SSM_F64 else 4
+            nbytes = Pl * (2 * spec.nx * esz + (4 if anc is not None else 0) + ((esz + 8) if obs is not None else 0))
+            with profiling.maybe("propagate_weight", nbytes):
+                _lib.check(L.ssm_propagate_weight(A, stream), "ssm_propagate_weight")
             if obs is not None:
                 parts = _allgather_tensor(lse_part, sh)  # C1
                 _lib.check(L.ssm_lse_combine(W, 1, _lib.ptr(parts), _lib.ptr(fs), ess_rel, float(P), i, stream),

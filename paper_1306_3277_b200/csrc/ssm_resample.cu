@@ -994,12 +994,14 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
     return r;
   };
   SearchWs tmp;
+  // regions that depend on P_out (the partition) go last, so the offsets of
+  // the others are the same for every P_out (the sharded phases rely on it)
   tmp.sums = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * tiles));
   tmp.totals = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * B));
   tmp.cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * P_in));
-  tmp.split = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * (nd + 1)));
   tmp.C = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * P_in));
   tmp.scan = take(scan_ws_bytes(B, P_in));
+  tmp.split = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * (nd + 1)));
   if (w) *w = tmp;
   return off;
 }

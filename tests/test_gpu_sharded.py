@@ -86,3 +86,21 @@ def test_two_ranks_match_one(scheme):
     for _, ll, traj in res:
         assert abs(ll[0] - ref_ll[0]) <= 1e-9 * abs(ref_ll[0])
         np.testing.assert_allclose(traj, ref_traj, rtol=0, atol=1e-9)
+
+
+def test_two_ranks_large_partition():
+    """Large per-rank P (partition sizes differ between the phases' layouts)."""
+    P = 1 << 21
+    ref_ll, ref_traj = _sharded("systematic", P)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, "systematic", P, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    for _, ll, traj in res:
+        assert abs(ll[0] - ref_ll[0]) <= 1e-9 * abs(ref_ll[0])

@@ -374,7 +374,10 @@ def main():
             "peak_kind": peak_kind,
             "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None,
-            "traffic": traffic.get("bytes_per_launch") if traffic else None,
+            # ncu DRAM bytes of one launch, only when the profiled launch has this run's size
+            "traffic": (traffic.get("bytes_per_launch") if traffic and pw and abs(
+                traffic.get("algorithmic_bytes_per_launch", 0) - pw["bytes"] / max(pw["launches"], 1)) < 1e6 * 64
+                else None),
             "algorithmic_bytes_per_particle": pw["bytes"] / max(pw["launches"], 1) / P if pw else None,
         },
         "kernels": kern,

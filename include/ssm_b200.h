@@ -128,7 +128,7 @@ typedef struct ssm_pw_args {
   uint32_t hints;       /* SSM_HINT_* bits the host guarantees */
   int32_t p_offset;     /* global index of particle 0 (device RNG counters; sharded filter) */
   int32_t x_in_stride;  /* row stride of x_in in particles (0: P) */
-  int32_t pad_args;
+  int32_t x_out_stride; /* row stride of x_out in particles (0: P) */
   void* lse_out;        /* [B][4] doubles or NULL: if set, the finalize writes the LSE/ESS partial
                            (m, c, t, s2) here instead of updating fs (cross-rank combine) */
 } ssm_pw_args;

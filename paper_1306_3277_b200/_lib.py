@@ -98,7 +98,7 @@ class PwArgs(C.Structure):
         ("hints", C.c_uint32),
         ("p_offset", C.c_int32),
         ("x_in_stride", C.c_int32),
-        ("pad_args", C.c_int32),
+        ("x_out_stride", C.c_int32),
         ("lse_out", C.c_void_p),
     ]
 

@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const size_t base = static_cast<size_t>(b) * NX * P;
   const int in_stride = A.x_in_stride > 0 ? A.x_in_stride : P;  // sharded filter: local + received states
   const T* __restrict__ xin = static_cast<const T*>(A.x_in) + static_cast<size_t>(b) * NX * in_stride;
-  T* __restrict__ xout = static_cast<T*>(A.x_out) + base;
+  const int out_stride = A.x_out_stride > 0 ? A.x_out_stride : P;  // spill capacity for the sharded filter
+  T* __restrict__ xout = static_cast<T*>(A.x_out) + static_cast<size_t>(b) * NX * out_stride;
   const int32_t* __restrict__ anc =
       (R && A.anc != nullptr) ? A.anc + static_cast<size_t>(b) * P : nullptr;
   const T* __restrict__ aprev =
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
       }
       }  // general sub-step loop
 #pragma unroll
-      for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * P + p] = x[n];
+      for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * out_stride + p] = x[n];
 
       if (has_obs) {
         T g = T(0);

@@ -70,6 +70,7 @@ class ShardedParticleFilter:
         self.exact = bool(exact)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.loglik = 0.0
+        self.spill_cap = 0 if self.shard.world == 1 else max(1024, self.P_loc // 8)
 
     def run(self, rng, upto=None):
         """particle_filter(...) semantics: init(child 0), advance(child 1),
@@ -83,9 +84,15 @@ class ShardedParticleFilter:
         off = r * Pl
         keys0 = torch.from_numpy(device_key(rng.child(0)).astype(np.uint32).reshape(1, 2).view(np.int32)).to(dev)
         keys1 = torch.from_numpy(device_key(rng.child(1)).astype(np.uint32).reshape(1, 2).view(np.int32)).to(dev)
-        x = torch.empty((spec.nx, Pl), dtype=tdt, device=dev)
-        _lib.check(L.ssm_init_particles(spec.kernel, self.dtype_id, 1, Pl, off, _lib.ptr(keys0), _lib.ptr(x), stream),
+        # every position buffer has `cap` spare columns: ancestor states received
+        # from other ranks land there, so resampling never copies the local state
+        cap = self.spill_cap
+        xbuf = torch.empty((spec.nx, Pl + cap), dtype=tdt, device=dev)
+        x0 = torch.empty((spec.nx, Pl), dtype=tdt, device=dev)
+        _lib.check(L.ssm_init_particles(spec.kernel, self.dtype_id, 1, Pl, off, _lib.ptr(keys0), _lib.ptr(x0), stream),
                    "ssm_init_particles")
+        xbuf[:, :Pl] = x0
+        x = xbuf[:, :Pl]
         fs = _fs_init(1, dev)
         theta = torch.from_numpy(spec.derived(self.theta)).to(dev)
         pw_ws = torch.empty(L.ssm_pw_workspace_bytes(1, Pl), dtype=torch.uint8, device=dev)
@@ -112,21 +119,23 @@ class ShardedParticleFilter:
         hist = [(x, None)]  # (x_i [nx, Pl], global ancestor index [Pl] int64 | None)
         a_last = None
         maybe = False
-        x_prev = x
+        x_prev, xbuf_prev = x, xbuf
         for i in range(1, upto + 1):
             anc = gidx = None
             x_in, stride = x_prev, 0
             if maybe:
                 with profiling.maybe("resample", Pl * (8 + 4 + 4 + 4)):
-                    x_in, stride, anc, gidx = self._resample(L, i, x_prev, a_last, fs, cdf, trec, tot, shift, c_last,
-                                                             sw, keys1, scheme, stream)
+                    x_in, stride, anc, gidx = self._resample(L, i, x_prev, xbuf_prev, a_last, fs, cdf, trec, tot,
+                                                             shift, c_last, sw, keys1, scheme, stream)
             obs = sched.obs[i]
-            x_out = torch.empty((spec.nx, Pl), dtype=tdt, device=dev)
+            xbuf_out = torch.empty((spec.nx, Pl + cap), dtype=tdt, device=dev)
+            x_out = xbuf_out[:, :Pl]
             a_out = torch.empty(Pl, dtype=tdt, device=dev) if obs is not None else None
             A.step, A.n_sub = i, sched.n_sub[i]
             A.hints = _lib.SSM_HINT_SINGLE_SUBSTEP if sched.single[i] else 0
             A.subs = sched.subs_ptr(i)
-            A.x_in, A.x_in_stride, A.x_out = x_in.data_ptr(), stride, x_out.data_ptr()
+            A.x_in, A.x_in_stride = x_in.data_ptr(), (stride if stride else Pl + cap)
+            A.x_out, A.x_out_stride = x_out.data_ptr(), Pl + cap
             A.anc = anc.data_ptr() if anc is not None else None
             A.a_prev = a_last.data_ptr() if a_last is not None else None
             A.a_out = a_out.data_ptr() if a_out is not None else None
@@ -152,7 +161,7 @@ class ShardedParticleFilter:
             elif maybe and self.ess_rel is None:
                 maybe = False
             hist.append((x_out, gidx))
-            x_prev = x_out
+            x_prev, xbuf_prev = x_out, xbuf_out
         st = _fs_view(fs)[0]
         nf, dg = int(st["err_nonfinite"]), int(st["err_degenerate"])
         if self.check_finite and nf != _lib.INT32_MAX and (dg == _lib.INT32_MAX or nf // 64 <= dg):
@@ -166,7 +175,7 @@ class ShardedParticleFilter:
         return self.loglik, traj
 
     # -- resampling across ranks ------------------------------------------------
-    def _resample(self, L, i, x_prev, a_last, fs, cdf, trec, tot, shift, c_last, sw, keys, scheme, stream):
+    def _resample(self, L, i, x_prev, xbuf, a_last, fs, cdf, trec, tot, shift, c_last, sw, keys, scheme, stream):
         sh, W, r = self.shard, self.shard.world, self.shard.rank
         P, Pl, dev, nx = self.P, self.P_loc, self.device, self.spec.nx
         _lib.check(L.ssm_tiles_total(1, Pl, _lib.ptr(trec), _lib.ptr(fs), _lib.ptr(tot), _lib.ptr(sw), stream),
@@ -198,7 +207,7 @@ class ShardedParticleFilter:
                 gidx[lo - d * Pl: hi - d * Pl] = seg.to(torch.int64) + r * Pl
             else:
                 xs = torch.empty((nx, hi - lo), dtype=x_prev.dtype, device=dev)
-                _lib.check(L.ssm_gather_cols(self.dtype_id, nx, hi - lo, Pl, _lib.ptr(x_prev), _lib.ptr(seg),
+                _lib.check(L.ssm_gather_cols(self.dtype_id, nx, hi - lo, xbuf.shape[1], _lib.ptr(xbuf), _lib.ptr(seg),
                                              _lib.ptr(xs), stream), "ssm_gather_cols")
                 sends[d] = [xs, seg.to(torch.int64) + r * Pl]
         for s_ in range(W):
@@ -211,10 +220,13 @@ class ShardedParticleFilter:
                 recv_slots.append((s_, lo - r * Pl, hi - lo))
         got = exchange(sends, specs, sh)  # C3
         if not recv_slots:
-            return x_prev, 0, anc_final, gidx
+            return xbuf, xbuf.shape[1], anc_final, gidx
         R = sum(n for _, _, n in recv_slots)
-        x_ext = torch.empty((nx, Pl + R), dtype=x_prev.dtype, device=dev)
-        x_ext[:, :Pl] = x_prev
+        if R <= xbuf.shape[1] - Pl:
+            x_ext = xbuf  # received states go to the spare columns: no copy of the local state
+        else:  # spill larger than the capacity (degenerate weights): extend once
+            x_ext = torch.empty((nx, Pl + R), dtype=x_prev.dtype, device=dev)
+            x_ext[:, :Pl] = x_prev
         pos = Pl
         for s_, slot0, n in recv_slots:
             xs, gi = got[s_]
@@ -222,7 +234,7 @@ class ShardedParticleFilter:
             anc_final[slot0:slot0 + n] = torch.arange(pos, pos + n, dtype=torch.int32, device=dev)
             gidx[slot0:slot0 + n] = gi.to(dev)
             pos += n
-        return x_ext, Pl + R, anc_final, gidx
+        return x_ext, x_ext.shape[1], anc_final, gidx
 
     # -- trajectory across ranks ------------------------------------------------
     def _trajectory(self, L, rng, hist, a_last, fs, stream):

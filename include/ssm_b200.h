@@ -289,6 +289,28 @@ int ssm_offspring_global(int B, int P, int P_global, int scheme, const void* cdf
 int ssm_expand_own(int B, int P, int P_global, int n_own, const ssm_filter_state* fs, int32_t* anc_out,
                    void* workspace, void* stream);
 
+/* Persistent small-P filter (P <= ssm_small_max_particles()): one CTA per
+ * filter runs all n_steps grid steps in ONE launch (device noise).  Same
+ * semantics as ssm_advance; log-weights, CDF and ancestors stay in shared
+ * memory; ancestors are written for every step (identity when not resampled). */
+typedef struct ssm_small_args {
+  int32_t model, dtype, B, P, scheme, exact, check_finite, n_steps;
+  double log_w0, obs_log_sd, log_sqrt_2pi, ess_rel;
+  const double* theta;         /* [B][4] */
+  const uint32_t* keys;        /* [B][2] */
+  ssm_filter_state* fs;        /* [B] */
+  const ssm_substep* subs;     /* device sub-step table */
+  const ssm_step_desc* steps;  /* DEVICE [n_steps] */
+  const void* x_in;            /* [B][nx][P] */
+  void* x_arena;               /* [n_steps][B][nx][P] */
+  int32_t* anc_arena;          /* [n_steps][B][P] */
+  const void* a_prev;          /* [B][P] or NULL */
+  void* a_out;                 /* [B][P] final unnormalised log-weights, or NULL */
+} ssm_small_args;
+
+int ssm_small_max_particles(void);
+int ssm_advance_small(const ssm_small_args* args, void* stream);
+
 /* K6: ancestor gather x_out[b][s][k] = x_in[b][s][anc[b][k]] (particle.py:102). */
 int ssm_gather(int dtype, int B, int nx, int P, const void* x_in, const int32_t* anc,
                void* x_out, void* stream);

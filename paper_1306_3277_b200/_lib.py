@@ -153,6 +153,13 @@ class AdvanceArgs(C.Structure):
     ]
 
 
+class SmallArgs(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("model", "dtype", "B", "P", "scheme", "exact", "check_finite", "n_steps")] + [
+        (n, C.c_double) for n in ("log_w0", "obs_log_sd", "log_sqrt_2pi", "ess_rel")] + [
+        (n, C.c_void_p) for n in ("theta", "keys", "fs", "subs", "steps", "x_in", "x_arena", "anc_arena", "a_prev",
+                                  "a_out")]
+
+
 # name -> (restype, argtypes); every symbol declared in include/ssm_b200.h
 _vp, _i, _sz, _d = C.c_void_p, C.c_int, C.c_size_t, C.c_double
 SIGNATURES = {
@@ -179,6 +186,8 @@ SIGNATURES = {
     "ssm_logsumexp": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_block_gather": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
     "ssm_advance": (_i, [C.POINTER(AdvanceArgs), _vp]),
+    "ssm_small_max_particles": (_i, []),
+    "ssm_advance_small": (_i, [C.POINTER(SmallArgs), _vp]),
     "ssm_sharded_workspace_bytes": (_sz, [_i, _i, _i]),
     "ssm_tiles_total": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_offspring_global": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp]),
@@ -204,6 +213,7 @@ LAUNCHING = {
     "ssm_logsumexp": 1,
     "ssm_block_gather": 1,
     "ssm_advance": 0,
+    "ssm_advance_small": 1,
     "ssm_tiles_total": 2,
     "ssm_offspring_global": 2,
     "ssm_expand_own": 1,

@@ -1,0 +1,368 @@
+// Persistent small-P filter: ONE launch advances B filters through all their
+// grid steps, one CTA per filter (device-noise mode).  For P <= 4096 the
+// multi-kernel path is launch/latency bound (~5 small kernels per step); here
+// the log-weights, the resampling CDF and the ancestors stay in shared memory,
+// positions stream through global memory (the history, L2-resident at this
+// size), and the step-to-step dependency is a __syncthreads.
+//
+// Semantics per step (particle.py:96-135), as in the multi-kernel path:
+//   resample if fs.resample_now: cum_j = C_j / C_tot over an exact 64-bit
+//   fixed-point block scan of w_j = exp(a_j - incr); ancestors by binary
+//   search on the reference's float64 query values (resampling.py:28-36);
+//   propagate / weight with the same device functions; scipy-form LSE/ESS
+//   block reduction and finalize.  Ancestors are written for every step
+//   (identity when no resampling happened, like the reference's arange).
+
+#include "ssm_common.cuh"
+
+namespace ssm {
+
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallMaxP = 4096;
+constexpr double kFix61 = 2305843009213693952.0;  // 2^61
+
+__device__ __forceinline__ double device_uniform_small(uint32_t k0, uint32_t k1, uint32_t k, uint32_t step,
+                                                       uint32_t purpose) {
+  const U4 r = philox4x32_10(U4{k, step, 0u, purpose}, k0, k1);  // same stream as the multi-kernel search
+  return u53(r.x, r.y);
+}
+
+// --- per-particle transition (device noise), the general path of pw_kernel ---
+template <typename T>
+__device__ __forceinline__ void small_normals8(uint32_t k0, uint32_t k1, uint32_t p, uint32_t step, uint32_t sub,
+                                               T z[8]) {
+#pragma unroll
+  for (uint32_t g = 0; g < 2; ++g) {
+    const U4 r = philox4x32_10(U4{p, step, (sub << 8) | g, kPurposeNoise}, k0, k1);
+    float a, b, c, d;
+    box_muller(r.x, r.y, a, b);
+    box_muller(r.z, r.w, c, d);
+    z[4 * g] = static_cast<T>(a);
+    z[4 * g + 1] = static_cast<T>(b);
+    z[4 * g + 2] = static_cast<T>(c);
+    z[4 * g + 3] = static_cast<T>(d);
+  }
+}
+
+template <typename T, bool E>
+__device__ __forceinline__ void small_l96_deriv(const T x[8], T F, const T nt[8], T out[8]) {
+  using O = Ar<T, E>;
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    const T xm1 = x[(n + 7) & 7], xp1 = x[(n + 1) & 7], xm2 = x[(n + 6) & 7];
+    out[n] = O::add(O::add(O::sub(O::mul(xm1, O::sub(xp1, xm2)), x[n]), F), nt[n]);
+  }
+}
+
+template <typename T, bool E>
+__device__ __forceinline__ void small_l96_rk4(T x[8], T F, const T nt[8], T s) {
+  using O = Ar<T, E>;
+  T k[8], acc[8], st[8];
+  const T hs = O::mul(T(0.5), s);
+  small_l96_deriv<T, E>(x, F, nt, k);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = k[n];
+    st[n] = O::add(x[n], O::mul(hs, k[n]));
+  }
+  small_l96_deriv<T, E>(st, F, nt, k);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = O::add(acc[n], O::mul(T(2.0), k[n]));
+    st[n] = O::add(x[n], O::mul(hs, k[n]));
+  }
+  small_l96_deriv<T, E>(st, F, nt, k);
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = O::add(acc[n], O::mul(T(2.0), k[n]));
+    st[n] = O::add(x[n], O::mul(s, k[n]));
+  }
+  small_l96_deriv<T, E>(st, F, nt, k);
+  const T s6 = O::div(s, T(6.0));
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    acc[n] = O::add(acc[n], k[n]);
+    x[n] = O::add(x[n], O::mul(s6, acc[n]));
+  }
+}
+
+template <int MODEL, typename T, bool E>
+__device__ __forceinline__ void small_transition(T* x, const double* th, const ssm_substep* subs, int n_sub,
+                                                 uint32_t k0, uint32_t k1, uint32_t pg, int step, bool check,
+                                                 bool& bad, int& bad_sub) {
+  using O = Ar<T, E>;
+  constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
+  for (int k = 0; k < n_sub; ++k) {
+    const ssm_substep& S = subs[k];
+    if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+      T W[8], nt[8];
+      small_normals8<T>(k0, k1, pg, static_cast<uint32_t>(step), static_cast<uint32_t>(k), W);
+      const T sd = static_cast<T>(S.sd);
+      const T F = static_cast<T>(th[0]);
+      const T sq = static_cast<T>(th[1]);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        W[n] = sd * W[n];
+        nt[n] = E ? O::div(O::mul(sq, W[n]), T(0.05)) : O::mul(O::mul(sq, W[n]), T(20.0));
+      }
+      for (int m = 0; m < S.n_ode; ++m) small_l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
+    } else {
+      const U4 r = philox4x32_10(U4{pg, static_cast<uint32_t>(step), static_cast<uint32_t>(k) << 8, kPurposeNoise},
+                                 k0, k1);
+      float z0, z1;
+      box_muller(r.x, r.y, z0, z1);
+      const T xi = static_cast<T>(th[3]) * static_cast<T>(z0);
+      x[0] = O::add(O::mul(static_cast<T>(th[0]), x[0]),
+                    O::mul(static_cast<T>(th[1]), O::add(static_cast<T>(S.u_in), xi)));
+    }
+    if (check && !bad) {
+      bool ok = true;
+#pragma unroll
+      for (int n = 0; n < NX; ++n) ok &= isfinite(x[n]);
+      if (!ok) {
+        bad = true;
+        bad_sub = k;
+      }
+    }
+  }
+}
+
+template <int MODEL, typename T, bool E>
+__device__ __forceinline__ T small_obs(const T* x, const double* th, const ssm_step_desc& d, T obs_log_sd, T lsp) {
+  using O = Ar<T, E>;
+  T g = T(0);
+  if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      if (d.obs_mask & (1u << n)) {
+        const T z = O::mul(O::sub(static_cast<T>(d.y[n]), x[n]), T(2.0));
+        g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
+      }
+    }
+  } else {
+    const T mean = O::add(x[0], O::mul(static_cast<T>(th[2]), static_cast<T>(d.u_obs)));
+    const T z = O::mul(O::sub(static_cast<T>(d.y[0]), mean), T(0.5));
+    g = O::add(g, O::sub(O::sub(O::mul(O::mul(T(-0.5), z), z), obs_log_sd), lsp));
+  }
+  return g;
+}
+
+__device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* warp_tot, uint64_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  uint64_t wex = 0, tot = 0;
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) {
+    const uint64_t t = warp_tot[w];
+    if (w < warp) wex += t;
+    tot += t;
+  }
+  *total = tot;
+  __syncthreads();
+  return wex + incl - v;
+}
+
+template <int MODEL, typename T, bool E>
+__global__ void __launch_bounds__(kSmallThreads) small_filter_kernel(const ssm_small_args A) {
+  constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int P = A.P;
+  T* a_s = reinterpret_cast<T*>(smem);                                          // [P]
+  double* cum_s = reinterpret_cast<double*>(smem + ((sizeof(T) * P + 15) & ~size_t(15)));  // [P]
+  int32_t* anc_s = reinterpret_cast<int32_t*>(cum_s + P);                       // [P]
+  __shared__ uint64_t warp_tot[kSmallThreads / 32];
+  __shared__ Lse red[kSmallThreads / 32];
+  __shared__ double s_incr;
+  __shared__ int s_resample, s_uniform;
+
+  const int b = blockIdx.x;
+  ssm_filter_state* fs = A.fs + b;
+  const double* th = A.theta + 4 * b;
+  const uint32_t k0 = A.keys[2 * b], k1 = A.keys[2 * b + 1];
+  const T obs_log_sd = static_cast<T>(A.obs_log_sd);
+  const T lsp = static_cast<T>(A.log_sqrt_2pi);
+  const T logw0 = static_cast<T>(A.log_w0);
+  const int ipt = (P + blockDim.x - 1) / blockDim.x;  // contiguous chunk per thread for the scan
+
+  if (A.a_prev) {
+    const T* ap = static_cast<const T*>(A.a_prev) + static_cast<size_t>(b) * P;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) a_s[p] = ap[p];
+  }
+  const size_t xstride_b = static_cast<size_t>(NX) * P;
+  const T* x_prev = static_cast<const T*>(A.x_in) + static_cast<size_t>(b) * xstride_b;
+  bool bad = false;
+  int bad_step = 0, bad_sub = 0;
+  __syncthreads();
+
+  for (int k = 0; k < A.n_steps; ++k) {
+    const ssm_step_desc& d = A.steps[k];
+    if (threadIdx.x == 0) {
+      s_resample = fs->resample_now;
+      s_uniform = fs->uniform;
+      s_incr = fs->incr;
+    }
+    __syncthreads();
+    const int R = s_resample;
+    int32_t* anc_g = A.anc_arena + (static_cast<size_t>(k) * A.B + b) * P;
+    if (R) {
+      // exact 64-bit CDF of w = exp(a - incr) (resampling.py:26-27)
+      const int j0 = threadIdx.x * ipt;
+      uint64_t local = 0;
+      for (int i = 0; i < ipt; ++i) {
+        const int j = j0 + i;
+        if (j < P) {
+          const double w = exp(static_cast<double>(a_s[j]) - s_incr);
+          const uint64_t q = (w >= 0.0 && w <= 4.0) ? __double2ull_rn(w * kFix61) : 0ull;
+          cum_s[j] = __longlong_as_double(static_cast<long long>(q));  // stash q
+          local += q;
+        }
+      }
+      uint64_t tot;
+      uint64_t run = block_excl_scan_u64(local, warp_tot, &tot);
+      const double inv_tot = 1.0 / static_cast<double>(tot);
+      for (int i = 0; i < ipt; ++i) {
+        const int j = j0 + i;
+        if (j < P) {
+          run += static_cast<uint64_t>(__double_as_longlong(cum_s[j]));
+          cum_s[j] = j == P - 1 ? 1.0 : static_cast<double>(run) * inv_tot;  // cum[-1] = 1
+        }
+      }
+      __syncthreads();
+      // queries and searchsorted(cum, u, 'right').clip(0, P-1)  (resampling.py:28-36)
+      const double u_sys = device_uniform_small(k0, k1, 0u, static_cast<uint32_t>(d.step), kPurposeSystematic);
+      for (int q = threadIdx.x; q < P; q += blockDim.x) {
+        double u;
+        if (A.scheme == SSM_SYSTEMATIC) {
+          u = (static_cast<double>(q) + u_sys) / static_cast<double>(P);
+        } else {
+          const double U = device_uniform_small(k0, k1, static_cast<uint32_t>(q), static_cast<uint32_t>(d.step),
+                                                kPurposeResample);
+          u = A.scheme == SSM_STRATIFIED ? (static_cast<double>(q) + U) / static_cast<double>(P) : U;
+        }
+        int lo = 0, hi = P;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (cum_s[mid] <= u)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        const int a_idx = lo < P ? lo : P - 1;
+        anc_s[q] = a_idx;
+        anc_g[q] = a_idx;
+      }
+    } else {
+      for (int q = threadIdx.x; q < P; q += blockDim.x) anc_g[q] = q;  // identity (reference: arange)
+    }
+    __syncthreads();
+    // propagate + weight
+    T* x_out = static_cast<T*>(A.x_arena) + (static_cast<size_t>(k) * A.B + b) * xstride_b;
+    const bool uni = R || s_uniform;
+    Lse st = lse_empty();
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+      const int src = R ? anc_s[p] : p;
+      T x[NX];
+#pragma unroll
+      for (int n = 0; n < NX; ++n) x[n] = x_prev[static_cast<size_t>(n) * P + src];
+      bool b_now = false;
+      int bs = 0;
+      small_transition<MODEL, T, E>(x, th, A.subs + d.subs_offset, d.n_sub, k0, k1, static_cast<uint32_t>(p),
+                                    d.step, A.check_finite != 0, b_now, bs);
+      if (b_now && !bad) {
+        bad = true;
+        bad_step = d.step;
+        bad_sub = bs;
+      }
+#pragma unroll
+      for (int n = 0; n < NX; ++n) x_out[static_cast<size_t>(n) * P + p] = x[n];
+      if (d.has_obs) {
+        const T g = small_obs<MODEL, T, E>(x, th, d, obs_log_sd, lsp);
+        const T lw = uni ? logw0 : Ar<T, E>::sub(a_s[p], static_cast<T>(s_incr));
+        const T a = Ar<T, E>::add(lw, g);
+        a_s[p] = a;  // each thread owns its p: in-place is safe after the resample read above
+        lse_push(st, static_cast<double>(a));
+      }
+    }
+    if (d.has_obs) {
+      const Lse r = lse_block_reduce<kSmallThreads>(st, red);
+      if (threadIdx.x == 0) {
+        const double incr = lse_value(r);
+        const double ess = lse_ess(r);
+        if (!isfinite(incr)) {
+          fs->err_degenerate = min(fs->err_degenerate, d.step);
+        } else {
+          fs->loglik += incr;
+        }
+        fs->incr = incr;
+        fs->lse_raw = incr;
+        fs->ess = ess;
+        fs->uniform = 0;
+        fs->resample_now = (A.ess_rel < 0.0) ? 1 : (ess < A.ess_rel * static_cast<double>(P) ? 1 : 0);
+      }
+    } else if (threadIdx.x == 0 && R) {
+      fs->uniform = 1;
+      fs->resample_now = 0;
+    }
+    __syncthreads();
+    x_prev = x_out;
+  }
+  if (bad) atomicMin(&fs->err_nonfinite, bad_step * 64 + bad_sub);
+  if (A.a_out) {
+    T* ao = static_cast<T*>(A.a_out) + static_cast<size_t>(b) * P;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) ao[p] = a_s[p];
+  }
+}
+
+template <int MODEL, typename T>
+static int launch_small(const ssm_small_args& A, cudaStream_t s) {
+  const size_t sm = ((sizeof(T) * A.P + 15) & ~size_t(15)) + (sizeof(double) + sizeof(int32_t)) * A.P;
+  const int threads = kSmallThreads;  // block reductions assume a full block
+  auto set = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    kern<<<A.B, threads, sm, s>>>(A);
+  };
+  if (A.exact)
+    set(small_filter_kernel<MODEL, T, true>);
+  else
+    set(small_filter_kernel<MODEL, T, false>);
+  return SSM_OK;
+}
+
+}  // namespace ssm
+
+using namespace ssm;
+
+extern "C" int ssm_small_max_particles(void) { return kSmallMaxP; }
+
+extern "C" int ssm_advance_small(const ssm_small_args* args, void* stream) {
+  if (!args) return SSM_ERR_INVALID_ARG;
+  const ssm_small_args& A = *args;
+  if (A.B <= 0 || A.P < 2 || A.P > kSmallMaxP || A.n_steps < 0 || !A.x_in || !A.x_arena || !A.anc_arena ||
+      !A.theta || !A.keys || !A.fs || !A.steps || !A.subs)
+    return SSM_ERR_INVALID_ARG;
+  if (A.scheme < SSM_MULTINOMIAL || A.scheme > SSM_SYSTEMATIC) return SSM_ERR_INVALID_ARG;
+  if (A.n_steps == 0) return SSM_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (A.model == SSM_MODEL_LORENZ96) {
+    if (A.dtype == SSM_F64)
+      launch_small<SSM_MODEL_LORENZ96, double>(A, s);
+    else
+      launch_small<SSM_MODEL_LORENZ96, float>(A, s);
+  } else if (A.model == SSM_MODEL_WINDKESSEL) {
+    if (A.dtype == SSM_F64)
+      launch_small<SSM_MODEL_WINDKESSEL, double>(A, s);
+    else
+      launch_small<SSM_MODEL_WINDKESSEL, float>(A, s);
+  } else {
+    return SSM_ERR_UNSUPPORTED;
+  }
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}

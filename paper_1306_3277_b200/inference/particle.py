@@ -138,6 +138,7 @@ class Schedule:
                 d["has_obs"], d["obs_mask"] = 1, self.obs[i][0]
                 d["y"] = self.obs[i][1]
                 d["u_obs"] = self.obs[i][2]
+        self.desc_dev = torch.from_numpy(self.desc.view(np.uint8).copy()).to(device)
         table = np.array(recs, dtype=_lib.SUBSTEP_DTYPE) if recs else np.zeros(1, _lib.SUBSTEP_DTYPE)
         self.table = torch.from_numpy(table.view(np.uint8).copy()).to(device)
         self.times = times
@@ -450,6 +451,47 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
     return x_arena[n - 1], a_new, bool(A.maybe_nonuniform)
 
 
+_SMALL_MAX = None
+_NO_SMALL = bool(os.environ.get("SSM_NO_SMALL"))  # A/B switch: force the multi-kernel path
+
+
+def _small_max():
+    global _SMALL_MAX
+    if _SMALL_MAX is None:
+        _SMALL_MAX = int(_lib.lib().ssm_small_max_particles())
+    return _SMALL_MAX
+
+
+def _advance_small(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe, x_arena, new_hist, stream):
+    """All steps of all B filters in ONE persistent launch (P <= ssm_small_max_particles())."""
+    n = upto - start
+    dev = x_arena.device
+    anc_arena = torch.empty((n, B, P), dtype=torch.int32, device=dev)
+    any_obs = any(sched.obs[i] is not None for i in range(start + 1, upto + 1))
+    a_out = torch.empty((B, P), dtype=r0.tdtype, device=dev) if (any_obs or a_last is not None) else None
+    S = _lib.SmallArgs()
+    S.model, S.dtype, S.B, S.P = spec.kernel, r0.dtype_id, B, P
+    S.scheme = _lib.SCHEME_IDS[r0.resampler]
+    S.exact, S.check_finite, S.n_steps = int(r0.exact), int(r0.check_finite), n
+    S.log_w0, S.obs_log_sd, S.log_sqrt_2pi, S.ess_rel = args.log_w0, args.obs_log_sd, args.log_sqrt_2pi, args.ess_rel
+    S.theta, S.keys, S.fs = args.theta, args.keys, args.fs
+    S.subs = sched.table.data_ptr()
+    S.steps = sched.desc_dev.data_ptr() + (start + 1) * _lib.STEP_DESC_DTYPE.itemsize
+    S.x_in, S.x_arena, S.anc_arena = x_prev.data_ptr(), x_arena.data_ptr(), anc_arena.data_ptr()
+    S.a_prev = a_last.data_ptr() if a_last is not None else None
+    S.a_out = a_out.data_ptr() if a_out is not None else None
+    with profiling.maybe("small_filter", 0):
+        _lib.check(L.ssm_advance_small(S, stream), "ssm_advance_small")
+    for k in range(n):
+        new_hist.append((x_arena[k], anc_arena[k]))
+        i = start + 1 + k
+        if sched.obs[i] is not None:
+            maybe = True
+        elif maybe and r0.ess_rel is None:
+            maybe = False
+    return x_arena[n - 1], (a_out if a_out is not None else a_last), maybe
+
+
 def args_device(t):
     return t.device
 
@@ -523,7 +565,12 @@ def advance_runs(runs, upto, rngs):
     a_arena = torch.empty((max(n_res, 1), B, P), dtype=tdt, device=dev) if n_res else None
     anc_arena = None
     a_slot = 0
-    if not host_noise:
+    small = (not host_noise and P <= _small_max() and not _NO_SMALL)
+    if small:
+        x_prev, a_last, maybe_nonuniform = _advance_small(
+            L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe_nonuniform, x_arena, new_hist, stream)
+        tiles_ok = False  # the persistent kernel keeps its CDF in shared memory
+    elif not host_noise:
         x_prev, a_last, maybe_nonuniform = _advance_native(
             L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe_nonuniform, x_arena, a_arena,
             cdf_local, tile_rec, rs_ws, tiles_ok, scheme, esz, new_hist, stream)

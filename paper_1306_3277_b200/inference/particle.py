@@ -525,11 +525,13 @@ def advance_runs(runs, upto, rngs):
     pw_ws = torch.empty(L.ssm_pw_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     rs_ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     # systematic / stratified resample from the pw kernel's tile-local CDF (no second pass over logw)
-    tiles_ok = r0.resampler in ("systematic", "stratified")
+    small = (not host_noise and P <= _small_max() and not _NO_SMALL)
+    # systematic / stratified resample from the pw kernel's tile CDF (multi-kernel path only)
+    tiles_ok = r0.resampler in ("systematic", "stratified") and not small
     ntile = (P + 31) // 32  # one tile record per warp tile
     cdf_local = tile_rec = None
     if tiles_ok:
-        if runs[0]._cdf is not None:  # resume: fresh copies, so clones sharing the views stay intact
+        if all(r._cdf is not None for r in runs):  # resume: fresh copies, clones sharing the views stay intact
             cdf_local = torch.stack([r._cdf for r in runs])
             tile_rec = torch.stack([r._trec for r in runs])
         else:
@@ -565,11 +567,9 @@ def advance_runs(runs, upto, rngs):
     a_arena = torch.empty((max(n_res, 1), B, P), dtype=tdt, device=dev) if n_res else None
     anc_arena = None
     a_slot = 0
-    small = (not host_noise and P <= _small_max() and not _NO_SMALL)
-    if small:
+    if small:  # the persistent kernel keeps its CDF in shared memory
         x_prev, a_last, maybe_nonuniform = _advance_small(
             L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe_nonuniform, x_arena, new_hist, stream)
-        tiles_ok = False  # the persistent kernel keeps its CDF in shared memory
     elif not host_noise:
         x_prev, a_last, maybe_nonuniform = _advance_native(
             L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe_nonuniform, x_arena, a_arena,

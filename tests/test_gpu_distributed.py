@@ -73,7 +73,7 @@ def test_sharded_equals_single(kind):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got = q.get(timeout=600)
+    got = q.get(timeout=240)
     for p in procs:
         p.join(120)
         assert p.exitcode == 0

@@ -79,7 +79,7 @@ def test_two_ranks_match_one(scheme):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, scheme, P, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(2)]
+    res = [q.get(timeout=240) for _ in range(2)]
     for p in procs:
         p.join(120)
         assert p.exitcode == 0
@@ -98,7 +98,7 @@ def test_two_ranks_large_partition():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, "systematic", P, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(2)]
+    res = [q.get(timeout=240) for _ in range(2)]
     for p in procs:
         p.join(120)
         assert p.exitcode == 0

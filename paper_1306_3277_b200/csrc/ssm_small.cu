@@ -169,18 +169,22 @@ __device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* wa
   return wex + incl - v;
 }
 
-template <int MODEL, typename T, bool E>
+// XS: positions double-buffered in shared memory (history still streamed to
+// global memory); otherwise read back from the global history (L2).
+template <int MODEL, typename T, bool E, bool XS>
 __global__ void __launch_bounds__(kSmallThreads) small_filter_kernel(const ssm_small_args A) {
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
   extern __shared__ __align__(16) unsigned char smem[];
   const int P = A.P;
-  T* a_s = reinterpret_cast<T*>(smem);                                          // [P]
+  T* a_s = reinterpret_cast<T*>(smem);                                                       // [P]
   double* cum_s = reinterpret_cast<double*>(smem + ((sizeof(T) * P + 15) & ~size_t(15)));  // [P]
-  int32_t* anc_s = reinterpret_cast<int32_t*>(cum_s + P);                       // [P]
+  int32_t* anc_s = reinterpret_cast<int32_t*>(cum_s + P);                                    // [P]
+  T* xs0 = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(anc_s) + ((sizeof(int32_t) * P + 15) & ~size_t(15)));
+  T* xs1 = xs0 + static_cast<size_t>(NX) * P;  // XS only: [NX][P] x 2
   __shared__ uint64_t warp_tot[kSmallThreads / 32];
   __shared__ Lse red[kSmallThreads / 32];
-  __shared__ double s_incr;
-  __shared__ int s_resample, s_uniform;
+  __shared__ ssm_filter_state s_fs;  // the filter state lives in shared memory during the launch
+  __shared__ double s_usys;
 
   const int b = blockIdx.x;
   ssm_filter_state* fs = A.fs + b;
@@ -190,35 +194,37 @@ __global__ void __launch_bounds__(kSmallThreads) small_filter_kernel(const ssm_s
   const T lsp = static_cast<T>(A.log_sqrt_2pi);
   const T logw0 = static_cast<T>(A.log_w0);
   const int ipt = (P + blockDim.x - 1) / blockDim.x;  // contiguous chunk per thread for the scan
+  const size_t xstride_b = static_cast<size_t>(NX) * P;
 
+  if (threadIdx.x == 0) s_fs = *fs;
   if (A.a_prev) {
     const T* ap = static_cast<const T*>(A.a_prev) + static_cast<size_t>(b) * P;
     for (int p = threadIdx.x; p < P; p += blockDim.x) a_s[p] = ap[p];
   }
-  const size_t xstride_b = static_cast<size_t>(NX) * P;
-  const T* x_prev = static_cast<const T*>(A.x_in) + static_cast<size_t>(b) * xstride_b;
+  const T* x_prev_g = static_cast<const T*>(A.x_in) + static_cast<size_t>(b) * xstride_b;
+  if constexpr (XS) {
+    for (int e = threadIdx.x; e < NX * P; e += blockDim.x) xs0[e] = x_prev_g[e];
+  }
+  T* xcur = xs0;
+  T* xnext = xs1;
   bool bad = false;
   int bad_step = 0, bad_sub = 0;
   __syncthreads();
 
   for (int k = 0; k < A.n_steps; ++k) {
     const ssm_step_desc& d = A.steps[k];
-    if (threadIdx.x == 0) {
-      s_resample = fs->resample_now;
-      s_uniform = fs->uniform;
-      s_incr = fs->incr;
-    }
-    __syncthreads();
-    const int R = s_resample;
+    const int R = s_fs.resample_now;
+    const double incr_prev = s_fs.incr;
     int32_t* anc_g = A.anc_arena + (static_cast<size_t>(k) * A.B + b) * P;
     if (R) {
+      if (threadIdx.x == 0) s_usys = device_uniform_small(k0, k1, 0u, static_cast<uint32_t>(d.step), kPurposeSystematic);
       // exact 64-bit CDF of w = exp(a - incr) (resampling.py:26-27)
       const int j0 = threadIdx.x * ipt;
       uint64_t local = 0;
       for (int i = 0; i < ipt; ++i) {
         const int j = j0 + i;
         if (j < P) {
-          const double w = exp(static_cast<double>(a_s[j]) - s_incr);
+          const double w = exp(static_cast<double>(a_s[j]) - incr_prev);
           const uint64_t q = (w >= 0.0 && w <= 4.0) ? __double2ull_rn(w * kFix61) : 0ull;
           cum_s[j] = __longlong_as_double(static_cast<long long>(q));  // stash q
           local += q;
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(kSmallThreads) small_filter_kernel(const ssm_s
       }
       __syncthreads();
       // queries and searchsorted(cum, u, 'right').clip(0, P-1)  (resampling.py:28-36)
-      const double u_sys = device_uniform_small(k0, k1, 0u, static_cast<uint32_t>(d.step), kPurposeSystematic);
+      const double u_sys = s_usys;
       for (int q = threadIdx.x; q < P; q += blockDim.x) {
         double u;
         if (A.scheme == SSM_SYSTEMATIC) {
@@ -264,13 +270,13 @@ __global__ void __launch_bounds__(kSmallThreads) small_filter_kernel(const ssm_s
     __syncthreads();
     // propagate + weight
     T* x_out = static_cast<T*>(A.x_arena) + (static_cast<size_t>(k) * A.B + b) * xstride_b;
-    const bool uni = R || s_uniform;
+    const bool uni = R || s_fs.uniform;
     Lse st = lse_empty();
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
       const int src = R ? anc_s[p] : p;
       T x[NX];
 #pragma unroll
-      for (int n = 0; n < NX; ++n) x[n] = x_prev[static_cast<size_t>(n) * P + src];
+      for (int n = 0; n < NX; ++n) x[n] = XS ? xcur[n * P + src] : x_prev_g[static_cast<size_t>(n) * P + src];
       bool b_now = false;
       int bs = 0;
       small_transition<MODEL, T, E>(x, th, A.subs + d.subs_offset, d.n_sub, k0, k1, static_cast<uint32_t>(p),
@@ -281,10 +287,13 @@ __global__ void __launch_bounds__(kSmallThreads) small_filter_kernel(const ssm_s
         bad_sub = bs;
       }
 #pragma unroll
-      for (int n = 0; n < NX; ++n) x_out[static_cast<size_t>(n) * P + p] = x[n];
+      for (int n = 0; n < NX; ++n) {
+        x_out[static_cast<size_t>(n) * P + p] = x[n];
+        if constexpr (XS) xnext[n * P + p] = x[n];
+      }
       if (d.has_obs) {
         const T g = small_obs<MODEL, T, E>(x, th, d, obs_log_sd, lsp);
-        const T lw = uni ? logw0 : Ar<T, E>::sub(a_s[p], static_cast<T>(s_incr));
+        const T lw = uni ? logw0 : Ar<T, E>::sub(a_s[p], static_cast<T>(incr_prev));
         const T a = Ar<T, E>::add(lw, g);
         a_s[p] = a;  // each thread owns its p: in-place is safe after the resample read above
         lse_push(st, static_cast<double>(a));
@@ -296,24 +305,32 @@ __global__ void __launch_bounds__(kSmallThreads) small_filter_kernel(const ssm_s
         const double incr = lse_value(r);
         const double ess = lse_ess(r);
         if (!isfinite(incr)) {
-          fs->err_degenerate = min(fs->err_degenerate, d.step);
+          s_fs.err_degenerate = min(s_fs.err_degenerate, d.step);
         } else {
-          fs->loglik += incr;
+          s_fs.loglik += incr;
         }
-        fs->incr = incr;
-        fs->lse_raw = incr;
-        fs->ess = ess;
-        fs->uniform = 0;
-        fs->resample_now = (A.ess_rel < 0.0) ? 1 : (ess < A.ess_rel * static_cast<double>(P) ? 1 : 0);
+        s_fs.incr = incr;
+        s_fs.lse_raw = incr;
+        s_fs.ess = ess;
+        s_fs.uniform = 0;
+        s_fs.resample_now = (A.ess_rel < 0.0) ? 1 : (ess < A.ess_rel * static_cast<double>(P) ? 1 : 0);
       }
     } else if (threadIdx.x == 0 && R) {
-      fs->uniform = 1;
-      fs->resample_now = 0;
+      s_fs.uniform = 1;
+      s_fs.resample_now = 0;
     }
     __syncthreads();
-    x_prev = x_out;
+    if constexpr (XS) {
+      T* t = xcur;
+      xcur = xnext;
+      xnext = t;
+    } else {
+      x_prev_g = x_out;
+    }
   }
-  if (bad) atomicMin(&fs->err_nonfinite, bad_step * 64 + bad_sub);
+  if (bad) atomicMin(&s_fs.err_nonfinite, bad_step * 64 + bad_sub);
+  __syncthreads();
+  if (threadIdx.x == 0) *fs = s_fs;
   if (A.a_out) {
     T* ao = static_cast<T*>(A.a_out) + static_cast<size_t>(b) * P;
     for (int p = threadIdx.x; p < P; p += blockDim.x) ao[p] = a_s[p];
@@ -322,16 +339,28 @@ __global__ void __launch_bounds__(kSmallThreads) small_filter_kernel(const ssm_s
 
 template <int MODEL, typename T>
 static int launch_small(const ssm_small_args& A, cudaStream_t s) {
-  const size_t sm = ((sizeof(T) * A.P + 15) & ~size_t(15)) + (sizeof(double) + sizeof(int32_t)) * A.P;
+  constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
+  const size_t base = ((sizeof(T) * A.P + 15) & ~size_t(15)) + sizeof(double) * A.P +
+                      ((sizeof(int32_t) * A.P + 15) & ~size_t(15));
+  const size_t with_x = base + 2 * sizeof(T) * NX * A.P;
+  const bool xs = with_x <= 200 * 1024;
+  const size_t sm = xs ? with_x : base;
   const int threads = kSmallThreads;  // block reductions assume a full block
-  auto set = [&](auto kern) {
+  auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
     kern<<<A.B, threads, sm, s>>>(A);
   };
-  if (A.exact)
-    set(small_filter_kernel<MODEL, T, true>);
-  else
-    set(small_filter_kernel<MODEL, T, false>);
+  if (A.exact) {
+    if (xs)
+      go(small_filter_kernel<MODEL, T, true, true>);
+    else
+      go(small_filter_kernel<MODEL, T, true, false>);
+  } else {
+    if (xs)
+      go(small_filter_kernel<MODEL, T, false, true>);
+    else
+      go(small_filter_kernel<MODEL, T, false, false>);
+  }
   return SSM_OK;
 }
 

@@ -408,3 +408,45 @@ def test_fast_device_noise_filter_tracks_exact():
                               resampler="systematic", exact=exact, upto=8)
         lls.append(out.loglik)
     assert abs(lls[0] - lls[1]) <= 1e-6 * abs(lls[0]), lls
+
+
+@pytest.mark.parametrize("P", [2, 33, 1000, 4097, 70001])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_pf_ragged_sizes_match_oracle(P, scheme):
+    """Partial warp tiles, non-power-of-two P and the minimum P=2, with the
+    reference's draws: loglik within 1e-12 of the oracle, trajectory bitwise."""
+    g = load_golden("pf.npz")
+    grid = _l96_grid(g)
+    T = 6 if P > 10000 else 12
+    out = particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(5 + P), n_particles=P, resampler=scheme,
+                          noise="host", upto=T)
+    ograd = O.Grid(grid.times, {k + 1: (g["l96/obs_v"][k], g["l96/obs_m"][k]) for k in range(20)})
+    ll, traj, _ = O.particle_filter("lorenz96", g["l96/theta"], ograd, O.Stream(5 + P), n_particles=P,
+                                    resampler=scheme, upto=T)
+    assert abs(out.loglik - ll) <= 1e-12 * abs(ll), (out.loglik, ll)
+    np.testing.assert_array_equal(out.trajectory, traj)
+
+
+def test_pf_upto_zero_and_unobserved_steps():
+    g = load_golden("pf.npz")
+    grid = _l96_grid(g)
+    out = particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(1), n_particles=64, upto=0)
+    assert out.loglik == 0.0 and out.trajectory.shape == (1, 8)
+    # all observations masked: pure propagation, loglik stays 0, no resampling
+    masked = build_filter_grid(0.0, 2.0, 20, g["l96/obs_t"], g["l96/obs_v"], np.zeros_like(g["l96/obs_m"]), n_obs=8)
+    out = particle_filter(LORENZ96, g["l96/theta"], masked, RngStream(1), n_particles=5000, resampler="systematic")
+    assert out.loglik == 0.0
+    assert all(h[1] is None or np.array_equal(h[1].cpu().numpy(), np.arange(5000)) for h in out.run.history[1:])
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("P", [3000, 100000])
+def test_device_noise_ess_gate_runs(scheme, P):
+    """ESS gate with device noise on both the persistent (small P) and the
+    multi-kernel path: runs, finite, and resamples less often than without."""
+    g = load_golden("pf.npz")
+    grid = _l96_grid(g)
+    out = particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(3), n_particles=P, resampler=scheme,
+                          ess_rel=0.5)
+    assert np.isfinite(out.loglik)
+    assert out.trajectory.shape == (21, 8)

@@ -295,6 +295,7 @@ constexpr int kMergeItems = 8;
 // ---------------------------------------------------------------------------
 
 constexpr int kDiag = 2048;  // merged-diagonal elements per expand block
+constexpr int kShortRun = 32;  // offspring runs up to this length are written by the offspring kernel
 
 enum CumSrc { kCumDouble = 0, kCumFixed = 1, kCumLogw = 2, kCumTiles = 3 };
 
@@ -512,7 +513,8 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
                  const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
                  const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ cnt,
                  int32_t* __restrict__ split, int ndiag, const uint64_t* __restrict__ g_off = nullptr,
-                 const int32_t* __restrict__ c_shift = nullptr) {
+                 const int32_t* __restrict__ c_shift = nullptr, int32_t* __restrict__ anc_direct = nullptr,
+                 int4* __restrict__ long_runs = nullptr, uint32_t* __restrict__ long_count = nullptr) {
   __shared__ uint64_t sm[kScanTile + kScanTile / 8];
   __shared__ uint64_t warp_tot[kThreads / 32];
   const int b = blockIdx.y, tile = blockIdx.x;
@@ -658,6 +660,20 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
     if (j >= P_in) break;
     const int c = offspring_bound<SCHEME>(cum[i], u_sys, U, k0, k1, step, P_out, invP, pow2) - cshift;
     cvals[i] = c;
+    if (anc_direct) {
+      // anc_k = j for k in [c_{j-1}, c_j): short runs written here, long ones deferred
+      int32_t* ab = anc_direct + static_cast<size_t>(b) * P_out;
+      int hi_k = c;
+      if (j == P_in - 1 && c < P_out) hi_k = P_out;  // u_k == 1.0 -> searchsorted = P -> clip to P-1
+      if (hi_k - c_prev <= kShortRun) {
+        for (int k = c_prev; k < hi_k; ++k) ab[k] = j;
+      } else {
+        const uint32_t slot = atomicAdd(long_count + b, 1u);
+        long_runs[static_cast<size_t>(b) * (P_in / kShortRun + 2) + slot] = make_int4(j, c_prev, hi_k, 0);
+      }
+      c_prev = c;
+      continue;
+    }
     // diagonal boundaries D in (j-1 + c_prev, j + c] are split at particle j
     const int lo = j - 1 + c_prev, hi = j + c;
     for (int t = lo / kDiag + 1; t * kDiag <= hi && t <= ndiag; ++t) sp[t] = j;
@@ -668,6 +684,7 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
     c_prev = c;
   }
   (void)total;
+  if (anc_direct) return;
   if (jt + kScanItems <= P_in && (P_in & 7) == 0) {  // two 16-byte vector stores, aligned
     int4* c4 = reinterpret_cast<int4*>(cb + jt);
     c4[0] = make_int4(cvals[0], cvals[1], cvals[2], cvals[3]);
@@ -676,6 +693,22 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i)
       if (jt + i < P_in) cb[jt + i] = cvals[i];
+  }
+}
+
+// Long offspring runs (> kShortRun outputs of one particle, e.g. degenerate
+// weights): one block per run, grid-stride over runs.
+__global__ void __launch_bounds__(kThreads)
+long_runs_kernel(int P_in, int P_out, const int4* __restrict__ runs, const uint32_t* __restrict__ count,
+                 const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc) {
+  const int b = blockIdx.y;
+  if (fs && !fs[b].resample_now) return;
+  const uint32_t n = count[b];
+  const int4* rb = runs + static_cast<size_t>(b) * (P_in / kShortRun + 2);
+  int32_t* ab = anc + static_cast<size_t>(b) * P_out;
+  for (uint32_t r = blockIdx.x; r < n; r += gridDim.x) {
+    const int4 q = rb[r];
+    for (int k = q.y + threadIdx.x; k < q.z; k += kThreads) ab[k] = q.x;
   }
 }
 
@@ -997,8 +1030,11 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
   // regions that depend on P_out (the partition) go last, so the offsets of
   // the others are the same for every P_out (the sharded phases rely on it)
   tmp.sums = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * tiles));
-  tmp.totals = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * B));
-  tmp.cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * P_in));
+  tmp.totals = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 3 * static_cast<size_t>(B)));  // + long-run counts
+  // cnt doubles as the long-run list of the direct ancestor writer (int4 per run, P_in/32 + 2 per filter)
+  const size_t cnt_bytes = sizeof(int32_t) * static_cast<size_t>(B) * P_in;
+  const size_t runs_bytes = sizeof(int4) * static_cast<size_t>(B) * (P_in / kShortRun + 2);
+  tmp.cnt = reinterpret_cast<int32_t*>(take(cnt_bytes > runs_bytes ? cnt_bytes : runs_bytes));
   tmp.C = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * P_in));
   tmp.scan = take(scan_ws_bytes(B, P_in));
   tmp.split = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * (nd + 1)));
@@ -1083,13 +1119,26 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
   const int tiles = scan_tiles(P);
   const int nd = ndiag_of(P, P);
   const dim3 g(tiles, B);
+  // direct mode: the offspring kernel writes the ancestors of short runs itself;
+  // long runs go to a list (w.cnt region reused) filled by long_runs_kernel
+  uint32_t* long_count = reinterpret_cast<uint32_t*>(w.totals) + 2 * static_cast<size_t>(B);  // after totals
+  int4* long_runs = reinterpret_cast<int4*>(w.cnt);
+  cudaError_t e = cudaMemsetAsync(long_count, 0, sizeof(uint32_t) * B, s);
+  if (e != cudaSuccess) {
+    ssm_set_last_error(e);
+    return SSM_ERR_CUDA;
+  }
   if (scheme == SSM_SYSTEMATIC)
     offspring_kernel<SSM_SYSTEMATIC, kCumTiles, double><<<g, kThreads, 0, s>>>(
-        P, P, cdf_local, scale, pref, w.totals, u, keys, step, fs, w.cnt, w.split, nd);
+        P, P, cdf_local, scale, pref, w.totals, u, keys, step, fs, w.cnt, w.split, nd, nullptr, nullptr, anc,
+        long_runs, long_count);
   else
     offspring_kernel<SSM_STRATIFIED, kCumTiles, double><<<g, kThreads, 0, s>>>(
-        P, P, cdf_local, scale, pref, w.totals, u, keys, step, fs, w.cnt, w.split, nd);
-  expand_kernel<<<dim3(nd, B), kThreads, 0, s>>>(P, P, w.cnt, w.split, nd, fs, anc);
+        P, P, cdf_local, scale, pref, w.totals, u, keys, step, fs, w.cnt, w.split, nd, nullptr, nullptr, anc,
+        long_runs, long_count);
+  long_runs_kernel<<<dim3(grid_for(P / kShortRun + 1, 1, 1184), B), kThreads, 0, s>>>(P, P, long_runs, long_count,
+                                                                                      fs, anc);
+  (void)expand_kernel;
   SSM_CHECK_LAUNCH();
   return SSM_OK;
 }

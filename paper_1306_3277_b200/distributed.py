@@ -129,7 +129,6 @@ def exchange(send_payloads: dict, recv_specs: dict, shard: Shard) -> dict:
     out = {}
     if shard.world == 1:
         return out
-    nccl = shard.backend == "nccl"
     dev = _comm_device(shard)
     ops, keep = [], []
     for peer in sorted(set(send_payloads) | set(recv_specs)):

@@ -120,7 +120,7 @@ def config4(quick):
     n_theta, P = (32, 1 << 12) if quick else (128, 1 << 14)
     runner = FilterRunner(LORENZ96, grid, n_particles=P, resampler="systematic")
     ms, res = timed(lambda: smc_sampler(LORENZ96, runner, n_theta, RngStream(5), theta_resampler="systematic"),
-                    warmup=0, reps=1)
+                    warmup=1, reps=2)
     obs_steps = grid.obs_steps
     # PF work: propagation to each obs step + rejuvenation replay to the previous one
     steps = sum(o for o in obs_steps) + sum((obs_steps[i - 2] if i > 1 else 0) for i in range(1, len(obs_steps) + 1))

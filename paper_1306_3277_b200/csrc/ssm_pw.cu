@@ -18,9 +18,6 @@
 namespace ssm {
 
 constexpr int kMaxPwBlocks = 2048;  // per filter; a function of P only (determinism)
-#ifndef SSM_SIMPLE_MIN_BLOCKS
-#define SSM_SIMPLE_MIN_BLOCKS 1
-#endif
 
 __host__ __device__ inline int pw_grid_x(int P) {
   const int tiles = (P + kThreads - 1) / kThreads;
@@ -172,7 +169,10 @@ constexpr double kTileFix = 4503599627370496.0;  // 2^52
 // benchmark grid) -- no runtime loops or per-slot predicates, sub-step
 // constants hoisted out of the particle loop.
 template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE = false>
-__global__ void __launch_bounds__(kThreads, SIMPLE ? SSM_SIMPLE_MIN_BLOCKS : 1) pw_kernel(const ssm_pw_args A) {
+// NOTE: plain __launch_bounds__(kThreads).  An explicit minBlocks of 1 lets
+// ptxas spend 172 registers on the SIMPLE f64 kernel (1 CTA/SM, 0.80 ms
+// vs 0.63 ms at 119 registers / 2 CTAs); minBlocks 3 (<= 85) is also slower.
+__global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   using O = Ar<T, E>;
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
   const int b = blockIdx.y;

@@ -4,6 +4,8 @@
 
 #include <stdio.h>
 
+#include <algorithm>
+
 #include "ssm_common.cuh"
 
 namespace ssm {
@@ -295,7 +297,12 @@ constexpr int kMergeItems = 8;
 // ---------------------------------------------------------------------------
 
 constexpr int kDiag = 2048;  // merged-diagonal elements per expand block
-constexpr int kShortRun = 32;  // offspring runs up to this length are written by the offspring kernel
+constexpr int kShortRun = 32;    // offspring runs up to this length are written by the offspring kernel
+constexpr int kRunChunk = 4096;  // long runs are filled in chunks of this many outputs
+__host__ __device__ inline size_t long_runs_cap(int P_in, int P_out) {
+  (void)P_in;  // a long run has > kShortRun outputs: at most P_out / kShortRun of them
+  return static_cast<size_t>(P_out / kShortRun) + static_cast<size_t>(P_out / kRunChunk) + 4;
+}
 
 enum CumSrc { kCumDouble = 0, kCumFixed = 1, kCumLogw = 2, kCumTiles = 3 };
 
@@ -667,9 +674,14 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
       if (j == P_in - 1 && c < P_out) hi_k = P_out;  // u_k == 1.0 -> searchsorted = P -> clip to P-1
       if (hi_k - c_prev <= kShortRun) {
         for (int k = c_prev; k < hi_k; ++k) ab[k] = j;
-      } else {
-        const uint32_t slot = atomicAdd(long_count + b, 1u);
-        long_runs[static_cast<size_t>(b) * (P_in / kShortRun + 2) + slot] = make_int4(j, c_prev, hi_k, 0);
+      } else {  // deferred in chunks of <= kRunChunk outputs so many blocks share a huge run
+        const int nchunk = (hi_k - c_prev + kRunChunk - 1) / kRunChunk;
+        const uint32_t slot = atomicAdd(long_count + b, static_cast<uint32_t>(nchunk));
+        int4* rb = long_runs + static_cast<size_t>(b) * long_runs_cap(P_in, P_out);
+        for (int q = 0; q < nchunk; ++q) {
+          const int lo_q = c_prev + q * kRunChunk;
+          rb[slot + q] = make_int4(j, lo_q, min(lo_q + kRunChunk, hi_k), 0);
+        }
       }
       c_prev = c;
       continue;
@@ -704,7 +716,7 @@ long_runs_kernel(int P_in, int P_out, const int4* __restrict__ runs, const uint3
   const int b = blockIdx.y;
   if (fs && !fs[b].resample_now) return;
   const uint32_t n = count[b];
-  const int4* rb = runs + static_cast<size_t>(b) * (P_in / kShortRun + 2);
+  const int4* rb = runs + static_cast<size_t>(b) * long_runs_cap(P_in, P_out);
   int32_t* ab = anc + static_cast<size_t>(b) * P_out;
   for (uint32_t r = blockIdx.x; r < n; r += gridDim.x) {
     const int4 q = rb[r];
@@ -1033,7 +1045,7 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
   tmp.totals = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 3 * static_cast<size_t>(B)));  // + long-run counts
   // cnt doubles as the long-run list of the direct ancestor writer (int4 per run, P_in/32 + 2 per filter)
   const size_t cnt_bytes = sizeof(int32_t) * static_cast<size_t>(B) * P_in;
-  const size_t runs_bytes = sizeof(int4) * static_cast<size_t>(B) * (P_in / kShortRun + 2);
+  const size_t runs_bytes = sizeof(int4) * static_cast<size_t>(B) * long_runs_cap(P_in, P_out);
   tmp.cnt = reinterpret_cast<int32_t*>(take(cnt_bytes > runs_bytes ? cnt_bytes : runs_bytes));
   tmp.C = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * P_in));
   tmp.scan = take(scan_ws_bytes(B, P_in));
@@ -1136,8 +1148,8 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
     offspring_kernel<SSM_STRATIFIED, kCumTiles, double><<<g, kThreads, 0, s>>>(
         P, P, cdf_local, scale, pref, w.totals, u, keys, step, fs, w.cnt, w.split, nd, nullptr, nullptr, anc,
         long_runs, long_count);
-  long_runs_kernel<<<dim3(grid_for(P / kShortRun + 1, 1, 1184), B), kThreads, 0, s>>>(P, P, long_runs, long_count,
-                                                                                      fs, anc);
+  const int gx = std::max(1, std::min(1184 / B, P / kRunChunk + 1));
+  long_runs_kernel<<<dim3(gx, B), kThreads, 0, s>>>(P, P, long_runs, long_count, fs, anc);
   (void)expand_kernel;
   SSM_CHECK_LAUNCH();
   return SSM_OK;

@@ -347,6 +347,66 @@ def test_filter_resampler_degenerate_weights(scheme):
         np.testing.assert_array_equal(anc.cpu().numpy(), ref)
 
 
+def _tile_inputs(a_np):
+    """cdf_local / tile_rec / fs exactly as the fused kernel documents them
+    (include/ssm_b200.h ssm_tile_rec): per 32-particle tile, m_w >= max a_j,
+    q_j = rint(exp(a_j - m_w) 2^52), cdf_local = tile-inclusive prefix of q."""
+    from scipy.special import logsumexp
+
+    from paper_1306_3277_b200 import _lib
+
+    P = a_np.size
+    nt = (P + 31) // 32
+    pad = np.full(nt * 32, -np.inf)
+    pad[:P] = a_np
+    t = pad.reshape(nt, 32)
+    m = t.max(axis=1)
+    q = np.rint(np.exp(t - m[:, None]) * 2.0**52).astype(np.uint64)
+    cdf = np.cumsum(q, axis=1, dtype=np.uint64).reshape(-1)[:P]
+    rec = np.zeros(nt, dtype=[("m", "<f8"), ("Q", "<u8")])
+    rec["m"], rec["Q"] = m, q.sum(axis=1, dtype=np.uint64)
+    fs = np.zeros(1, dtype=_lib.FILTER_STATE_DTYPE)
+    fs["incr"], fs["resample_now"] = logsumexp(a_np), 1
+    fs["err_nonfinite"] = fs["err_degenerate"] = _lib.INT32_MAX
+    dev = torch.device("cuda")
+    as_dev = lambda arr: torch.from_numpy(arr.view(np.uint8).copy()).to(dev)  # noqa: E731
+    return as_dev(cdf), as_dev(rec), as_dev(fs), np.exp(a_np - logsumexp(a_np))
+
+
+def _heavy_patterns(P):
+    r = np.random.default_rng(11)
+    one = np.full(P, -1e4)
+    one[P // 3] = 0.0
+    few = np.full(P, -30.0)
+    few[[5, 6, 4000, P // 2, P - 1]] = 0.0  # runs of ~P/5 outputs (> one block window)
+    cluster = np.zeros(P)  # long runs inside staged block windows (<= 4096 outputs)
+    cluster[10], cluster[3000] = np.log(1000.0), np.log(40.0)
+    lognorm = r.normal(0.0, 3.0, P)  # mixed: long and short runs, ragged windows
+    return {"one": one, "few": few, "cluster": cluster, "lognormal": lognorm}
+
+
+@pytest.mark.parametrize("scheme", ["systematic", "stratified"])
+@pytest.mark.parametrize("P", [1 << 16, 50001])
+@pytest.mark.parametrize("pattern", ["one", "few", "cluster", "lognormal"])
+def test_tiles_resample_heavy_runs_match_oracle(scheme, P, pattern):
+    """Filter-path resampler (ssm_resample_from_tiles): staged block windows,
+    the heavy-block fallback and chunked long runs give the reference's
+    ancestors."""
+    from paper_1306_3277_b200 import _lib
+
+    L = _lib.lib()
+    a_np = _heavy_patterns(P)[pattern]
+    cdf, rec, fs, w = _tile_inputs(a_np)
+    u_np = np.random.default_rng(3).random(1 if scheme == "systematic" else P)
+    u = torch.from_numpy(u_np).cuda()
+    ws = torch.empty(L.ssm_resample_workspace_bytes(1, P), dtype=torch.uint8, device="cuda")
+    anc = torch.full((P,), -7, dtype=torch.int32, device="cuda")
+    _lib.check(L.ssm_resample_from_tiles(1, P, _lib.SCHEME_IDS[scheme], _lib.ptr(cdf), _lib.ptr(rec),
+                                         _lib.ptr(fs), _lib.ptr(u), None, 1, _lib.ptr(anc), _lib.ptr(ws),
+                                         _lib.stream_ptr()))
+    np.testing.assert_array_equal(anc.cpu().numpy(), O.resample_with(w, scheme, u_np))
+
+
 def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float64"):
     """One ssm_propagate_weight launch with device noise (C ABI), returns x_out, a_out."""
     from paper_1306_3277_b200 import _lib

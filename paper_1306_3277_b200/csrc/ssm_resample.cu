@@ -330,6 +330,16 @@ __device__ __forceinline__ int offspring_bound(double cum, double u_sys, const d
     }
   };
   if (!(cum > 0.0)) return 0;  // u_k >= 0
+  if constexpr (SCHEME == SSM_SYSTEMATIC) {
+    // Fast accept: query k satisfies fl(fl(k + u) / P) < cum  <=>  k < cum P - u
+    // up to ~2^-27 absolute rounding (k < 2^25, P <= 2^30 checked below), so when
+    // t = cum P - u lies more than 2^-20 from an integer, ceil(t) is the count
+    // exactly; otherwise verify query by query as below.
+    const double t = cum * static_cast<double>(P_out) - u_sys;
+    const double e = ceil(t);
+    if (e - t > 0x1p-20 && t - (e - 1.0) > 0x1p-20 && P_out <= (1 << 30))
+      return t <= 0.0 ? 0 : (e >= static_cast<double>(P_out) ? P_out : static_cast<int>(e));
+  }
   double est = SCHEME == SSM_SYSTEMATIC ? ceil(cum * P_out - u_sys) : floor(cum * P_out);
   est = est < 0.0 ? 0.0 : (est > P_out ? static_cast<double>(P_out) : est);
   int k = static_cast<int>(est);

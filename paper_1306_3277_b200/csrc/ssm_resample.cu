@@ -532,7 +532,7 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
                  int32_t* __restrict__ split, int ndiag, const uint64_t* __restrict__ g_off = nullptr,
                  const int32_t* __restrict__ c_shift = nullptr, int32_t* __restrict__ anc_direct = nullptr,
                  int4* __restrict__ long_runs = nullptr, uint32_t* __restrict__ long_count = nullptr) {
-  __shared__ uint64_t sm[kScanTile + kScanTile / 8];
+  __shared__ __align__(16) uint64_t sm[kScanTile + kScanTile / 8];
   __shared__ uint64_t warp_tot[kThreads / 32];
   const int b = blockIdx.y, tile = blockIdx.x;
   if (fs && !fs[b].resample_now) return;
@@ -542,10 +542,17 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
   const bool pow2 = (P_out & (P_out - 1)) == 0;
   const double invP = 1.0 / static_cast<double>(P_out);
   const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
-  const double u_sys =
-      SCHEME == SSM_SYSTEMATIC
-          ? (u ? u[b] : device_uniform(k0, k1, 0u, step, kPurposeSystematic))
-          : 0.0;
+  double u_sys = 0.0;
+  if constexpr (SCHEME == SSM_SYSTEMATIC) {
+    if (u) {
+      u_sys = u[b];
+    } else {  // one Philox draw per block, not per thread
+      __shared__ double s_u;
+      if (threadIdx.x == 0) s_u = device_uniform(k0, k1, 0u, step, kPurposeSystematic);
+      __syncthreads();
+      u_sys = s_u;
+    }
+  }
   const double* U = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * P_out : nullptr;
   int32_t* cb = cnt + static_cast<size_t>(b) * P_in;
   int32_t* sp = split + static_cast<size_t>(b) * (ndiag + 1);
@@ -699,7 +706,8 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
     const int last_thread = min(kThreads - 1, (min(P_in, j0 + kScanTile) - 1 - j0) / kScanItems);
     if (threadIdx.x == 0) s_lo = c_first;  // thread 0 holds the block's first particle
     if (threadIdx.x == last_thread) s_hi = hk[kScanItems - 1];
-    for (int e = threadIdx.x; e < kOutBuf + kOutBuf / 32; e += kThreads) sOut[e] = -1;
+    for (int e = threadIdx.x; e < (kOutBuf + kOutBuf / 32) / 4; e += kThreads)
+      reinterpret_cast<int4*>(sOut)[e] = make_int4(-1, -1, -1, -1);
     __syncthreads();
     const int lo_blk = s_lo, n_out = s_hi - lo_blk;
     int32_t* ab = anc_direct + static_cast<size_t>(b) * P_out;
@@ -716,11 +724,13 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
       }
       __syncthreads();
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      static_assert(kPer == 16, "pad(t*kPer + i) == t*kPer + i + t/2 needs kPer == 16");
+      int32_t* sv = sOut + threadIdx.x * kPer + (threadIdx.x >> 1);
       int v[kPer];
       int run = -1;
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
-        run = max(run, sOut[pad(threadIdx.x * kPer + i)]);
+        run = max(run, sv[i]);
         v[i] = run;
       }
       int incl = run;
@@ -737,7 +747,7 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
       for (int w = 0; w < kThreads / 32; ++w)
         if (w < warp) carry = max(carry, s_wmax[w]);
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) sOut[pad(threadIdx.x * kPer + i)] = max(carry, v[i]);
+      for (int i = 0; i < kPer; ++i) sv[i] = max(carry, v[i]);
       __syncthreads();
       for (int e = threadIdx.x; e < n_out; e += kThreads) ab[lo_blk + e] = sOut[pad(e)];
     } else if (active) {

@@ -165,6 +165,27 @@ __device__ __forceinline__ bool finite_bits(float v) {
 
 constexpr double kTileFix = 4503599627370496.0;  // 2^52
 
+// Fold up to 32 parked warp-tile partials (lane l holds tile l: m_l is a
+// float-representable reference >= the tile's max, or -inf when empty) into
+// the warp partial `st` (lane 0): one exp per lane and a fixed shuffle tree,
+// so the result depends only on the tile layout (deterministic).
+__device__ __forceinline__ Lse fold_tiles(Lse st, double m, double t, double s2, int lane) {
+  const float mf = static_cast<float>(m);  // exact: m came from a float (or is +-inf / NaN)
+  const int key = __float_as_int(mf) >= 0 ? __float_as_int(mf) : (__float_as_int(mf) ^ 0x7fffffff);
+  const int kmax = __reduce_max_sync(0xffffffffu, key);
+  const double M = static_cast<double>(__int_as_float(kmax >= 0 ? kmax : (kmax ^ 0x7fffffff)));
+  if (M == -CUDART_INF) return st;  // warp-uniform: no particles in any parked tile
+  const double f = exp(m - M);      // 0 for empty slots; NaN M propagates
+  double T = t * f, S2 = s2 * (f * f);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T += __shfl_down_sync(0xffffffffu, T, o);
+    S2 += __shfl_down_sync(0xffffffffu, S2, o);
+  }
+  if (lane == 0) st = lse_combine(st, Lse{M, 0.0, T, S2});
+  return st;
+}
+
 // SIMPLE: one sub-step with one RK4 step and every obs slot present (the
 // benchmark grid) -- no runtime loops or per-slot predicates, sub-step
 // constants hoisted out of the particle loop.
@@ -208,7 +229,9 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const int lane = threadIdx.x & 31;
   const bool want_ess = A.ess_rel >= 0.0;
 
-  Lse st = lse_empty();  // warp partial (lane 0), warp tiles folded in order
+  Lse st = lse_empty();  // warp partial (lane 0), groups of 32 warp tiles folded in order
+  int slot = 0;          // lane holding the current warp tile's {m_w, t_w, s2_w}
+  double r_m = -CUDART_INF, r_t = 0.0, r_s2 = 0.0;
   bool bad = false;
   int bad_sub = 0;
 
@@ -384,13 +407,22 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s2_ += __shfl_xor_sync(0xffffffffu, s2_, o);
     }
-    if (lane == 0) {
-      if (trec && p < P) trec[p >> 5] = ssm_tile_rec{mw, Qw};
-      // tile sum of exp(a - m_w) from the exact fixed-point total (|err| <= 32 * 2^-53)
-      const double tsum = any_nan ? CUDART_NAN : static_cast<double>(Qw) * (1.0 / kTileFix);
-      st = lse_combine(st, Lse{mw, 0.0, tsum, s2_});
+    if (lane == 0 && trec && p < P) trec[p >> 5] = ssm_tile_rec{mw, Qw};
+    // tile sum of exp(a - m_w) from the exact fixed-point total (|err| <= 32 * 2^-53),
+    // parked in lane `slot`; every 32 tiles the warp folds them in one pass
+    if (lane == slot && p - lane < P) {  // tiles past P stay empty (their m_w is a NaN sentinel)
+      r_m = mw;
+      r_t = any_nan ? CUDART_NAN : static_cast<double>(Qw) * (1.0 / kTileFix);
+      r_s2 = s2_;
+    }
+    if (++slot == 32) {
+      st = fold_tiles(st, r_m, r_t, r_s2, lane);
+      slot = 0;
+      r_m = -CUDART_INF;
+      r_t = r_s2 = 0.0;
     }
   }
+  if (slot > 0) st = fold_tiles(st, r_m, r_t, r_s2, lane);
 
   if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
 

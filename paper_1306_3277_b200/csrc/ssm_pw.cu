@@ -165,6 +165,49 @@ __device__ __forceinline__ bool finite_bits(float v) {
 
 constexpr double kTileFix = 4503599627370496.0;  // 2^52
 
+// exp(x) for x <= 0 (the tile weights e_j = exp(a_j - m_w)): 2^(j/64) table in
+// shared memory + degree-6 polynomial on |r| <= ln2/128 (truncation < 3e-20,
+// ~1-2 ulp overall); coefficients in the constant bank so the DFMAs take them
+// as operands.  x < -40 -> 0 (round(e 2^52) is 0 below -36.7), NaN -> NaN.
+__constant__ double c_exp_tab[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
+};
+__constant__ double c_exp_poly[8] = {0x1.6c16c16c16c17p-10, 0x1.1111111111111p-7, 0x1.5555555555555p-5,
+                                     0x1.5555555555555p-3, 0x1.0000000000000p-1, 0x1.71547652b82fep+6,
+                                     0x1.62e42fefa39efp-7, 0x1.abc9e3b39803fp-62};
+
+__device__ __forceinline__ double exp_tile(double x, const double* __restrict__ tab /* smem */) {
+  if (!(x >= -40.0)) return x != x ? x : 0.0;
+  const double t = fma(x, c_exp_poly[5], 0x1.8p52);  // round(x 64/ln2) in the low word
+  const int n = __double2loint(t);
+  const double nd = t - 0x1.8p52;
+  double r = fma(nd, -c_exp_poly[6], x);
+  r = fma(nd, -c_exp_poly[7], r);
+  double p = fma(c_exp_poly[0], r, c_exp_poly[1]);
+  p = fma(p, r, c_exp_poly[2]);
+  p = fma(p, r, c_exp_poly[3]);
+  p = fma(p, r, c_exp_poly[4]);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double y = tab[n & 63] * p;  // in [0.99, 2.01)
+  return __hiloint2double(__double2hiint(y) + ((n >> 6) << 20), __double2loint(y));  // * 2^(n >> 6)
+}
+
 // Fold up to 32 parked warp-tile partials (lane l holds tile l: m_l is a
 // float-representable reference >= the tile's max, or -inf when empty) into
 // the warp partial `st` (lane 0): one exp per lane and a fixed shuffle tree,
@@ -229,6 +272,9 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
   const int lane = threadIdx.x & 31;
   const bool want_ess = A.ess_rel >= 0.0;
 
+  __shared__ double s_exp_tab[64];
+  if (threadIdx.x < 64) s_exp_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
+  __syncthreads();
   Lse st = lse_empty();  // warp partial (lane 0), groups of 32 warp tiles folded in order
   int slot = 0;          // lane holding the current warp tile's {m_w, t_w, s2_w}
   double r_m = -CUDART_INF, r_t = 0.0, r_s2 = 0.0;
@@ -391,7 +437,7 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
     const int kb = kmax >= 0 ? kmax : (kmax ^ 0x7fffffff);
     const double mw = static_cast<double>(__int_as_float(kb));
     const bool any_nan = __any_sync(0xffffffffu, act && isnan(a_d));
-    const double e = (!act || mw == -CUDART_INF) ? 0.0 : exp(a_d - mw);
+    const double e = (!act || mw == -CUDART_INF) ? 0.0 : exp_tile(a_d - mw, s_exp_tab);
     const uint64_t q = (e >= 0.0 && e <= 1.0) ? __double2ull_rn(e * kTileFix) : 0ull;
     uint64_t qi = q;
 #pragma unroll

@@ -407,7 +407,7 @@ def test_tiles_resample_heavy_runs_match_oracle(scheme, P, pattern):
     np.testing.assert_array_equal(anc.cpu().numpy(), O.resample_with(w, scheme, u_np))
 
 
-def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float64"):
+def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float64", tiles=None):
     """One ssm_propagate_weight launch with device noise (C ABI), returns x_out, a_out."""
     from paper_1306_3277_b200 import _lib
     from paper_1306_3277_b200.inference.particle import _fs_init, _dtype_info
@@ -436,7 +436,14 @@ def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float6
     A.log_w0, A.obs_log_sd, A.log_sqrt_2pi, A.ess_rel = -np.log(P), np.log(0.5), LOG_SQRT_2PI, -1.0
     A.x_in, A.x_out, A.a_out, A.theta, A.subs = xin.data_ptr(), xout.data_ptr(), a.data_ptr(), th.data_ptr(), subs.data_ptr()
     A.keys, A.fs, A.workspace, A.hints = kt.data_ptr(), fs.data_ptr(), ws.data_ptr(), hints
+    if tiles is not None:
+        cloc = torch.empty(P, dtype=torch.int64, device=dev)
+        trec = torch.empty(((P + 31) // 32) * 16, dtype=torch.uint8, device=dev)
+        A.cdf_local, A.tile_rec = cloc.data_ptr(), trec.data_ptr()
     _lib.check(L.ssm_propagate_weight(A, _lib.stream_ptr()))
+    if tiles is not None:
+        rec = trec.cpu().numpy().view([("m", "<f8"), ("Q", "<u8")])
+        tiles.update(cdf=cloc.cpu().numpy().view(np.uint64), m=rec["m"], Q=rec["Q"])
     return xout.t().double().cpu().numpy(), a.double().cpu().numpy()
 
 
@@ -510,3 +517,26 @@ def test_device_noise_ess_gate_runs(scheme, P):
                           ess_rel=0.5)
     assert np.isfinite(out.loglik)
     assert out.trajectory.shape == (21, 8)
+
+
+@pytest.mark.parametrize("P", [4096, 1000])
+def test_tile_records_match_documented_format(P):
+    """cdf_local / tile_rec from the fused kernel (include/ssm_b200.h):
+    m_w >= max a_j of the tile and float-representable, cdf_local the tile-inclusive
+    prefix of q_j = round(exp(a_j - m_w) 2^52) (kernel exp within a few ulp), Q_w
+    the tile total."""
+    r = np.random.default_rng(5)
+    x = r.normal(0.0, 3.0, (P, 8))
+    y = r.normal(0.0, 1.0, 8)
+    tiles = {}
+    _, a = _pw_direct(x, np.array([8.0, 0.1]), (7, 9), 0.05, 1, y, tiles=tiles)
+    nt = (P + 31) // 32
+    for w in range(nt):
+        aw = a[32 * w: 32 * w + 32]
+        m = tiles["m"][w]
+        assert m >= aw.max() and np.float32(m) == m
+        q = np.rint(np.exp(aw - m) * 2.0**52)
+        cdf = tiles["cdf"][32 * w: 32 * w + aw.size]
+        d = np.diff(np.concatenate([np.zeros(1, np.uint64), cdf])).astype(np.float64)  # each q_j <= 2^52: exact
+        assert np.all(np.abs(d - q) <= 4.0 + q * 1e-15), (w, np.max(np.abs(d - q)))
+        assert tiles["Q"][w] == tiles["cdf"][32 * w + aw.size - 1]

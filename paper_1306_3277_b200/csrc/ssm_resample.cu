@@ -821,6 +821,153 @@ long_runs_kernel(int P_in, int P_out, const int4* __restrict__ runs, const uint3
   }
 }
 
+// Filter-path offspring + ancestors from the fused kernel's tile records
+// (ssm_resample_from_tiles).  Lane = particle: each warp walks 8 consecutive
+// 32-particle tiles (its tile's prefix and scale are warp-uniform, cdf_local
+// loads are coalesced), c_{j-1} comes from the neighbouring lane.  The block's
+// output window [c_{j0-1}, c_{j0+2047}) is then filled in shared memory: run
+// starts are marked with their particle and an inclusive max-scan propagates
+// them; blocks whose window exceeds the staging buffer (degenerate weights)
+// write short runs directly and defer long ones to long_runs_kernel.
+// Counts are c_j = #{k : u_k < C_j / total} exactly (systematic fast accept when
+// C_j P / total - u is not within 2^-20 of an integer, query-by-query otherwise);
+// the last particle's run ends at P (cum[-1] = 1.0, resampling.py:27 + clip).
+template <int SCHEME>
+__global__ void __launch_bounds__(kThreads)
+offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const double* __restrict__ scale,
+                       const uint64_t* __restrict__ pref, const uint64_t* __restrict__ totals,
+                       const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
+                       const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc,
+                       int4* __restrict__ long_runs, uint32_t* __restrict__ long_count) {
+  constexpr int kOutBuf = 4096;             // staged outputs per block
+  constexpr int kPer = kOutBuf / kThreads;  // outputs per thread in the fill scan
+  constexpr int kIt = kScanTile / kThreads; // 32-particle tiles per warp
+  static_assert(kPer == 16 && kIt == 8, "layout");
+  __shared__ __align__(16) int32_t sOut[kOutBuf + kOutBuf / 32];
+  __shared__ int s_lo, s_hi;
+  __shared__ int s_wmax[kThreads / 32];
+  const int b = blockIdx.y;
+  if (fs && !fs[b].resample_now) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nt = (P + 31) >> 5;
+  const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
+  const uint64_t* tp = pref + static_cast<size_t>(b) * nt;
+  const uint64_t* bp = pref + B_total_tiles_offset(nt, gridDim.y) + static_cast<size_t>(b) * nblk;
+  const double* scb = scale + static_cast<size_t>(b) * nt;
+  const uint64_t* cl = cdf_local + static_cast<size_t>(b) * P;
+  const int jw = blockIdx.x * kScanTile + warp * (kScanTile / (kThreads / 32));  // warp's first particle
+  const int tw0 = jw >> 5;
+  // issue every load of the warp's 8 tiles first: cdf_local per lane, and the
+  // tiles' prefix / scale one per lane (broadcast by shuffle below)
+  uint64_t qv[kIt];
+#pragma unroll
+  for (int it = 0; it < kIt; ++it) {
+    const int j = jw + it * 32 + lane;
+    qv[it] = j < P - 1 ? __ldg(cl + j) : 0ull;
+  }
+  uint64_t my_pre = 0;
+  double my_sc = 0.0;
+  if (lane < kIt && tw0 + lane < nt) {
+    my_pre = tp[tw0 + lane] + bp[(tw0 + lane) / kRecPerBlock];
+    my_sc = scb[tw0 + lane];
+  }
+  const double inv = 1.0 / static_cast<double>(totals[b]);
+  const double Pd = static_cast<double>(P);
+  const double tscale = Pd * inv;
+  const bool pow2 = (P & (P - 1)) == 0;
+  const double invP = 1.0 / Pd;
+  const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
+  double u_sys = 0.0;
+  if constexpr (SCHEME == SSM_SYSTEMATIC)  // every lane draws the same value: no barrier
+    u_sys = u ? u[b] : device_uniform(k0, k1, 0u, step, kPurposeSystematic);
+  const double* U = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * P : nullptr;
+  const auto count = [&](uint64_t C) -> int {
+    const double Cd = static_cast<double>(C);
+    if constexpr (SCHEME == SSM_SYSTEMATIC) {
+      const double t = fma(Cd, tscale, -u_sys);
+      const double e = ceil(t);
+      if (e - t > 0x1p-20 && t - e > 0x1p-20 - 1.0 && P <= (1 << 30))
+        return static_cast<int>(fmin(fmax(e, 0.0), Pd));
+    }
+    return offspring_bound<SCHEME>(Cd * inv, u_sys, U, k0, k1, step, P, invP, pow2);
+  };
+
+  // c_{jw-1}: particle jw-1 closes tile tw0-1, so its C is tile tw0's exclusive prefix
+  const uint64_t pre0 = __shfl_sync(0xffffffffu, my_pre, 0);
+  int carry = 0;
+  if (jw > 0 && jw < P) carry = count(pre0);
+  else if (jw >= P) carry = P;
+  if (warp == 0 && lane == 0) s_lo = carry;
+  int cv[kIt], pv[kIt];
+#pragma unroll
+  for (int it = 0; it < kIt; ++it) {
+    const int j = jw + it * 32 + lane;
+    const uint64_t pre = __shfl_sync(0xffffffffu, my_pre, it);
+    const double sc = __shfl_sync(0xffffffffu, my_sc, it);
+    // particles >= P - 1: the last particle's run ends at P, later ones are empty
+    const int c = j < P - 1 ? count(pre + __double2ull_rn(sc * static_cast<double>(qv[it]))) : P;
+    const int up = __shfl_up_sync(0xffffffffu, c, 1);
+    pv[it] = lane == 0 ? carry : up;
+    cv[it] = c;
+    carry = __shfl_sync(0xffffffffu, c, 31);
+  }
+  if (threadIdx.x == kThreads - 1) s_hi = cv[kIt - 1];
+  for (int e = threadIdx.x; e < (kOutBuf + kOutBuf / 32) / 4; e += kThreads)
+    reinterpret_cast<int4*>(sOut)[e] = make_int4(-1, -1, -1, -1);
+  __syncthreads();
+  const int lo_blk = s_lo, n_out = s_hi - lo_blk;
+  int32_t* ab = anc + static_cast<size_t>(b) * P;
+  if (n_out <= kOutBuf) {
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+      const int e = pv[it] - lo_blk;
+      if (cv[it] > pv[it]) sOut[e + (e >> 5)] = jw + it * 32 + lane;
+    }
+    __syncthreads();
+    int32_t* sv = sOut + threadIdx.x * kPer + (threadIdx.x >> 1);  // pad(t*16 + i) = t*16 + i + t/2
+    int v[kPer];
+    int run = -1;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      run = max(run, sv[i]);
+      v[i] = run;
+    }
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = max(incl, y);
+    }
+    int cin = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) cin = -1;
+    if (lane == 31) s_wmax[warp] = incl;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w)
+      if (w < warp) cin = max(cin, s_wmax[w]);
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) sv[i] = max(cin, v[i]);
+    __syncthreads();
+    for (int e = threadIdx.x; e < n_out; e += kThreads) ab[lo_blk + e] = sOut[e + (e >> 5)];
+  } else {
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+      const int j = jw + it * 32 + lane, lo = pv[it], hi = cv[it];
+      if (hi - lo <= kShortRun) {
+        for (int k = lo; k < hi; ++k) ab[k] = j;
+      } else {
+        const int nchunk = (hi - lo + kRunChunk - 1) / kRunChunk;
+        const uint32_t slot = atomicAdd(long_count + b, static_cast<uint32_t>(nchunk));
+        int4* rb = long_runs + static_cast<size_t>(b) * long_runs_cap(P, P);
+        for (int q = 0; q < nchunk; ++q) {
+          const int lo_q = lo + q * kRunChunk;
+          rb[slot + q] = make_int4(j, lo_q, min(lo_q + kRunChunk, hi), 0);
+        }
+      }
+    }
+  }
+}
+
 // anc_k = #{j : c_j <= k}, clipped to P_in - 1, from the precomputed partition.
 // Balanced without searches: the block's particles [i0, i1] each mark the first
 // output of their offspring run inside [kb0, kb1); an inclusive max-scan of
@@ -1237,14 +1384,14 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
     ssm_set_last_error(e);
     return SSM_ERR_CUDA;
   }
+  (void)nd;
+  const uint64_t* cl = static_cast<const uint64_t*>(cdf_local);
   if (scheme == SSM_SYSTEMATIC)
-    offspring_kernel<SSM_SYSTEMATIC, kCumTiles, double><<<g, kThreads, 0, s>>>(
-        P, P, cdf_local, scale, pref, w.totals, u, keys, step, fs, w.cnt, w.split, nd, nullptr, nullptr, anc,
-        long_runs, long_count);
+    offspring_tiles_kernel<SSM_SYSTEMATIC><<<g, kThreads, 0, s>>>(P, cl, scale, pref, w.totals, u, keys, step, fs,
+                                                                  anc, long_runs, long_count);
   else
-    offspring_kernel<SSM_STRATIFIED, kCumTiles, double><<<g, kThreads, 0, s>>>(
-        P, P, cdf_local, scale, pref, w.totals, u, keys, step, fs, w.cnt, w.split, nd, nullptr, nullptr, anc,
-        long_runs, long_count);
+    offspring_tiles_kernel<SSM_STRATIFIED><<<g, kThreads, 0, s>>>(P, cl, scale, pref, w.totals, u, keys, step, fs,
+                                                                  anc, long_runs, long_count);
   const int gx = std::max(1, std::min(1184 / B, P / kRunChunk + 1));
   long_runs_kernel<<<dim3(gx, B), kThreads, 0, s>>>(P, P, long_runs, long_count, fs, anc);
   (void)expand_kernel;

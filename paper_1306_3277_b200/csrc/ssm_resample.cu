@@ -886,8 +886,9 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
     if constexpr (SCHEME == SSM_SYSTEMATIC) {
       const double t = fma(Cd, tscale, -u_sys);
       const double e = ceil(t);
-      if (e - t > 0x1p-20 && t - e > 0x1p-20 - 1.0 && P <= (1 << 30))
-        return static_cast<int>(fmin(fmax(e, 0.0), Pd));
+      const double d = e - t;  // in [0, 1), within 2^-53
+      if (d > 0x1p-20 && d < 1.0 - 0x1p-20 && P <= (1 << 30))
+        return min(max(__double2int_rz(e), 0), P);
     }
     return offspring_bound<SCHEME>(Cd * inv, u_sys, U, k0, k1, step, P, invP, pow2);
   };

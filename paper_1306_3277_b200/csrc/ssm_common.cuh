@@ -196,6 +196,28 @@ __device__ __forceinline__ bool finite(T v) {
   return isfinite(v);
 }
 
+// Programmatic dependent launch: the per-step kernels of the filter path are
+// launched with programmatic stream serialization, so a kernel's launch and
+// block scheduling overlap the tail of its predecessor; each such kernel calls
+// pdl_wait() as its FIRST statement (before any early exit, so completion stays
+// transitive along the chain).  A no-op when launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace ssm
 
 // error reporting helper shared by the C-ABI entry points

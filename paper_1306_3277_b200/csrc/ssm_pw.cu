@@ -19,9 +19,13 @@ namespace ssm {
 
 constexpr int kMaxPwBlocks = 2048;  // per filter; a function of P only (determinism)
 
+// Blocks per filter: >= 4 block tiles per block, so each warp folds several warp
+// tiles per setup (matters at moderate P with many filters, e.g. PMMH 8 x 2^16).
+// A function of P only, so the LSE fold order never depends on the batch.
 __host__ __device__ inline int pw_grid_x(int P) {
   const int tiles = (P + kThreads - 1) / kThreads;
-  return tiles < kMaxPwBlocks ? tiles : kMaxPwBlocks;
+  const int g = (tiles + 3) / 4;
+  return g < kMaxPwBlocks ? g : kMaxPwBlocks;
 }
 
 // ----------------------------- noise ---------------------------------------
@@ -237,6 +241,7 @@ template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE = false>
 // ptxas spend 172 registers on the SIMPLE f64 kernel (1 CTA/SM, 0.80 ms
 // vs 0.63 ms at 119 registers / 2 CTAs); minBlocks 3 (<= 85) is also slower.
 __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
+  pdl_wait();
   using O = Ar<T, E>;
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
   const int b = blockIdx.y;
@@ -533,20 +538,20 @@ static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
     const bool simple = (A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !A.exact && !inj &&
                         (!A.has_obs || A.obs_mask == 0xFFu);
     if (simple) {
-      pw_kernel<MODEL, T, false, false, true><<<grid, kThreads, 0, s>>>(A);
+      launch_pdl(pw_kernel<MODEL, T, false, false, true>, grid, dim3(kThreads), s, A);
       return;
     }
   }
   if (A.exact) {
     if (inj)
-      pw_kernel<MODEL, T, true, true><<<grid, kThreads, 0, s>>>(A);
+      launch_pdl(pw_kernel<MODEL, T, true, true>, grid, dim3(kThreads), s, A);
     else
-      pw_kernel<MODEL, T, true, false><<<grid, kThreads, 0, s>>>(A);
+      launch_pdl(pw_kernel<MODEL, T, true, false>, grid, dim3(kThreads), s, A);
   } else {
     if (inj)
-      pw_kernel<MODEL, T, false, true><<<grid, kThreads, 0, s>>>(A);
+      launch_pdl(pw_kernel<MODEL, T, false, true>, grid, dim3(kThreads), s, A);
     else
-      pw_kernel<MODEL, T, false, false><<<grid, kThreads, 0, s>>>(A);
+      launch_pdl(pw_kernel<MODEL, T, false, false>, grid, dim3(kThreads), s, A);
   }
 }
 

@@ -420,42 +420,30 @@ tile_prefix_kernel(int tiles, uint64_t* __restrict__ sums, uint64_t* __restrict_
 // offspring kernel reaches at the tile's last particle, so the global CDF is
 // monotone and deterministic.  Two launches: per-block (2048 tiles) scan, then
 // a 1-block scan of the block totals.
-constexpr int kRecPerBlock = kThreads * kScanItems;  // 2048 tile records per block
+constexpr int kRecPerBlock = kThreads;  // 256 tile records per block (one per thread)
 
 __global__ void __launch_bounds__(kThreads)
 tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_filter_state* __restrict__ fs,
-                  double* __restrict__ scale, uint64_t* __restrict__ prel, uint64_t* __restrict__ blk_tot) {
-  __shared__ uint64_t sm[kRecPerBlock + kRecPerBlock / 8];
+                  double* __restrict__ scale, uint64_t* __restrict__ prel, uint64_t* __restrict__ blk_tot,
+                  uint32_t* __restrict__ long_count = nullptr) {
+  pdl_wait();
   __shared__ uint64_t warp_tot[kThreads / 32];
   const int b = blockIdx.y, blk = blockIdx.x;
   if (!fs[b].resample_now) return;
+  if (long_count && blk == 0 && threadIdx.x == 0) long_count[b] = 0u;  // long-run list of this resample
   const double incr = fs[b].incr;
-  const size_t off = static_cast<size_t>(b) * ntiles + static_cast<size_t>(blk) * kRecPerBlock;
-  const int n = min(kRecPerBlock, ntiles - blk * kRecPerBlock);
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int e = i * kThreads + threadIdx.x;
-    uint64_t qg = 0;
-    if (e < n) {
-      const ssm_tile_rec r = rec[off + e];
-      const double sc = r.m == -CUDART_INF ? 0.0 : exp(r.m - incr) * kTileScale;
-      scale[off + e] = sc;
-      const double v = sc * static_cast<double>(r.Q);
-      qg = (v >= 0.0 && v < 4.0e18) ? __double2ull_rn(v) : 0ull;
-    }
-    sm[e + (e >> 3)] = qg;
-  }
-  __syncthreads();
-  uint64_t v[kScanItems];
-  uint64_t run = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int e = threadIdx.x * kScanItems + i;
-    v[i] = run;  // exclusive
-    run += sm[e + (e >> 3)];
+  const int e = blk * kRecPerBlock + threadIdx.x;
+  const size_t off = static_cast<size_t>(b) * ntiles + e;
+  uint64_t qg = 0;
+  if (e < ntiles) {
+    const ssm_tile_rec r = rec[off];
+    const double sc = r.m == -CUDART_INF ? 0.0 : exp(r.m - incr) * kTileScale;
+    scale[off] = sc;
+    const double v = sc * static_cast<double>(r.Q);
+    qg = (v >= 0.0 && v < 4.0e18) ? __double2ull_rn(v) : 0ull;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t incl = run;
+  uint64_t incl = qg;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -469,24 +457,14 @@ tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_fi
     if (w < warp) wex += warp_tot[w];
     tot += warp_tot[w];
   }
-  const uint64_t basev = wex + incl - run;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int e = threadIdx.x * kScanItems + i;
-    sm[e + (e >> 3)] = basev + v[i];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int e = i * kThreads + threadIdx.x;
-    if (e < n) prel[off + e] = sm[e + (e >> 3)];
-  }
+  if (e < ntiles) prel[off] = wex + incl - qg;  // exclusive, exact integer
   if (threadIdx.x == 0) blk_tot[static_cast<size_t>(b) * gridDim.x + blk] = tot;
 }
 
 __global__ void __launch_bounds__(1024)
 blk_prefix_kernel(int nblk, uint64_t* __restrict__ blk, uint64_t* __restrict__ totals,
                   const ssm_filter_state* __restrict__ fs) {
+  pdl_wait();
   const int b = blockIdx.x;
   if (fs && !fs[b].resample_now) return;
   uint64_t* bb = blk + static_cast<size_t>(b) * nblk;
@@ -810,6 +788,7 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
 __global__ void __launch_bounds__(kThreads)
 long_runs_kernel(int P_in, int P_out, const int4* __restrict__ runs, const uint32_t* __restrict__ count,
                  const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc) {
+  pdl_wait();
   const int b = blockIdx.y;
   if (fs && !fs[b].resample_now) return;
   const uint32_t n = count[b];
@@ -839,6 +818,7 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
                        const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
                        const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc,
                        int4* __restrict__ long_runs, uint32_t* __restrict__ long_count) {
+  pdl_wait();
   constexpr int kOutBuf = 4096;             // staged outputs per block
   constexpr int kPer = kOutBuf / kThreads;  // outputs per thread in the fill scan
   constexpr int kIt = kScanTile / kThreads; // 32-particle tiles per warp
@@ -1292,7 +1272,11 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
   const size_t cnt_bytes = sizeof(int32_t) * static_cast<size_t>(B) * P_in;
   const size_t runs_bytes = sizeof(int4) * static_cast<size_t>(B) * long_runs_cap(P_in, P_out);
   tmp.cnt = reinterpret_cast<int32_t*>(take(cnt_bytes > runs_bytes ? cnt_bytes : runs_bytes));
-  tmp.C = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * P_in));
+  // C doubles as the tile path's [scale | in-block prefix | block prefix] (2 nt + nblk per filter)
+  const size_t nt = (static_cast<size_t>(P_in) + 31) / 32;
+  const size_t tile_words = 2 * nt + (nt + kRecPerBlock - 1) / kRecPerBlock;
+  const size_t c_words = static_cast<size_t>(P_in) > tile_words ? static_cast<size_t>(P_in) : tile_words;
+  tmp.C = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * c_words));
   tmp.scan = take(scan_ws_bytes(B, P_in));
   tmp.split = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * (nd + 1)));
   if (w) *w = tmp;
@@ -1370,31 +1354,25 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
   double* scale = reinterpret_cast<double*>(w.C);
   uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + static_cast<size_t>(B) * nt;
   uint64_t* blk = pref + B_total_tiles_offset(nt, B);
-  tile_scale_kernel<<<dim3(nblk, B), kThreads, 0, s>>>(nt, static_cast<const ssm_tile_rec*>(tile_rec), fs,
-                                                      scale, pref, blk);
-  blk_prefix_kernel<<<B, 1024, 0, s>>>(nblk, blk, w.totals, fs);
-  const int tiles = scan_tiles(P);
-  const int nd = ndiag_of(P, P);
-  const dim3 g(tiles, B);
-  // direct mode: the offspring kernel writes the ancestors of short runs itself;
-  // long runs go to a list (w.cnt region reused) filled by long_runs_kernel
+  // the offspring kernel writes the ancestors itself; long runs of degenerate
+  // blocks go to a list (w.cnt region reused, count zeroed by tile_scale)
+  // filled by long_runs_kernel.  All four are programmatic dependent launches.
   uint32_t* long_count = reinterpret_cast<uint32_t*>(w.totals) + 2 * static_cast<size_t>(B);  // after totals
   int4* long_runs = reinterpret_cast<int4*>(w.cnt);
-  cudaError_t e = cudaMemsetAsync(long_count, 0, sizeof(uint32_t) * B, s);
-  if (e != cudaSuccess) {
-    ssm_set_last_error(e);
-    return SSM_ERR_CUDA;
-  }
-  (void)nd;
+  launch_pdl(tile_scale_kernel, dim3(nblk, B), dim3(kThreads), s, nt, static_cast<const ssm_tile_rec*>(tile_rec), fs,
+             scale, pref, blk, long_count);
+  launch_pdl(blk_prefix_kernel, dim3(B), dim3(1024), s, nblk, blk, w.totals, fs);
+  const dim3 g(scan_tiles(P), B);
   const uint64_t* cl = static_cast<const uint64_t*>(cdf_local);
   if (scheme == SSM_SYSTEMATIC)
-    offspring_tiles_kernel<SSM_SYSTEMATIC><<<g, kThreads, 0, s>>>(P, cl, scale, pref, w.totals, u, keys, step, fs,
-                                                                  anc, long_runs, long_count);
+    launch_pdl(offspring_tiles_kernel<SSM_SYSTEMATIC>, g, dim3(kThreads), s, P, cl, scale, pref, w.totals, u, keys,
+               step, fs, anc, long_runs, long_count);
   else
-    offspring_tiles_kernel<SSM_STRATIFIED><<<g, kThreads, 0, s>>>(P, cl, scale, pref, w.totals, u, keys, step, fs,
-                                                                  anc, long_runs, long_count);
+    launch_pdl(offspring_tiles_kernel<SSM_STRATIFIED>, g, dim3(kThreads), s, P, cl, scale, pref, w.totals, u, keys,
+               step, fs, anc, long_runs, long_count);
   const int gx = std::max(1, std::min(1184 / B, P / kRunChunk + 1));
-  long_runs_kernel<<<dim3(gx, B), kThreads, 0, s>>>(P, P, long_runs, long_count, fs, anc);
+  launch_pdl(long_runs_kernel, dim3(gx, B), dim3(kThreads), s, P, P, static_cast<const int4*>(long_runs),
+             static_cast<const uint32_t*>(long_count), fs, anc);
   (void)expand_kernel;
   SSM_CHECK_LAUNCH();
   return SSM_OK;

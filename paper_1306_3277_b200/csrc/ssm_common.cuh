@@ -35,6 +35,21 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
   return c;
 }
 
+// two blocks under one key: the round-key schedule is computed once for both
+__device__ __forceinline__ void philox4x32_10_x2(U4& a, U4& b, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t pa0 = static_cast<uint64_t>(0xD2511F53u) * a.x, pa1 = static_cast<uint64_t>(0xCD9E8D57u) * a.z;
+    const uint64_t pb0 = static_cast<uint64_t>(0xD2511F53u) * b.x, pb1 = static_cast<uint64_t>(0xCD9E8D57u) * b.z;
+    a = U4{static_cast<uint32_t>(pa1 >> 32) ^ a.y ^ k0, static_cast<uint32_t>(pa1),
+           static_cast<uint32_t>(pa0 >> 32) ^ a.w ^ k1, static_cast<uint32_t>(pa0)};
+    b = U4{static_cast<uint32_t>(pb1 >> 32) ^ b.y ^ k0, static_cast<uint32_t>(pb1),
+           static_cast<uint32_t>(pb0 >> 32) ^ b.w ^ k1, static_cast<uint32_t>(pb0)};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
 // counter word 3 tags the purpose of a draw so streams never overlap
 enum Purpose : uint32_t {
   kPurposeNoise = 1u,

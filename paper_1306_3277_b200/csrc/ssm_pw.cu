@@ -37,12 +37,13 @@ __host__ __device__ inline int pw_grid_x(int P) {
 template <typename T>
 __device__ __forceinline__ void normals8(uint32_t k0, uint32_t k1, uint32_t p, uint32_t step,
                                          uint32_t sub, T z[8]) {
+  U4 r[2] = {U4{p, step, sub << 8, kPurposeNoise}, U4{p, step, (sub << 8) | 1u, kPurposeNoise}};
+  philox4x32_10_x2(r[0], r[1], k0, k1);
 #pragma unroll
-  for (uint32_t g = 0; g < 2; ++g) {
-    const U4 r = philox4x32_10(U4{p, step, (sub << 8) | g, kPurposeNoise}, k0, k1);
+  for (int g = 0; g < 2; ++g) {
     float a, b, c, d;
-    box_muller(r.x, r.y, a, b);
-    box_muller(r.z, r.w, c, d);
+    box_muller(r[g].x, r[g].y, a, b);
+    box_muller(r[g].z, r[g].w, c, d);
     z[4 * g] = static_cast<T>(a);
     z[4 * g + 1] = static_cast<T>(b);
     z[4 * g + 2] = static_cast<T>(c);

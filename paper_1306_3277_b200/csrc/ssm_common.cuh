@@ -79,13 +79,14 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, uint32_t c, u
 
 // Box-Muller pair, float32 (the device noise generator for both precisions).
 // u1 = (a + 1/2) 2^-32 keeps 32 bits near 0, so |z| reaches 6.7 sigma; the
-// radius and angle use the MUFU lg2 / sin / cos (angle on [-pi, pi),
+// radius and angle use the MUFU lg2 / rsq / sin / cos (angle on [-pi, pi),
 // |error| < 2^-21; a rotation by pi leaves the pair iid N(0,1)).
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
   const float u1 = fmaf(static_cast<float>(a), 0x1.0p-32f, 0x1.0p-33f);  // (0, 1]
   const float th = fmaf(static_cast<float>(b >> 8), 6.28318530717958647692f * 0x1.0p-24f,
                         -3.14159265358979323846f);
-  const float r = sqrtf(-2.0f * __logf(u1));  // MUFU.LG2
+  const float x = -1.38629436111989061883f * __log2f(u1);  // -2 ln u1 (MUFU.LG2), >= 0
+  const float r = x > 0.0f ? x * rsqrtf(x) : 0.0f;             // sqrt via MUFU.RSQ, no slow path
   float s, co;
   __sincosf(th, &s, &co);
   z0 = r * co;

@@ -1091,21 +1091,33 @@ gather_cols_kernel(int nx, int n_out, int in_stride, const T* __restrict__ x, co
   }
 }
 
+// One block per filter.  Thread 0 walks the ancestry chain j_S -> j_0 (the
+// only serial part: one dependent load per step; the per-step pointer loads
+// are independent and run ahead) and parks j_i in out[i][0]; then the block
+// gathers the (S+1) x nx states in parallel.
 template <typename T>
-__global__ void trace_kernel(int B, int S, int nx, int P, const void* const* xs,
-                             const int32_t* const* ancs, const int32_t* j_final, double* out) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  int j = j_final[b];
+__global__ void __launch_bounds__(128)
+trace_kernel(int B, int S, int nx, int P, const void* const* __restrict__ xs,
+             const int32_t* const* __restrict__ ancs, const int32_t* __restrict__ j_final,
+             double* __restrict__ out) {
+  const int b = blockIdx.x;
   const size_t row = static_cast<size_t>(b) * (S + 1);
-  for (int i = S; i >= 0; --i) {
+  if (threadIdx.x == 0) {
+    int j = j_final[b];
+    out[(row + S) * nx] = static_cast<double>(j);
+#pragma unroll 8
+    for (int i = S; i > 0; --i) {
+      const int32_t* a = ancs[row + i];
+      if (a) j = __ldcg(a + j);
+      out[(row + i - 1) * nx] = static_cast<double>(j);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= S; i += blockDim.x) {
+    const int j = static_cast<int>(out[(row + i) * nx]);
     const T* xi = static_cast<const T*>(xs[row + i]);
     for (int n = 0; n < nx; ++n)
       out[(row + i) * nx + n] = static_cast<double>(xi[static_cast<size_t>(n) * P + j]);
-    if (i > 0) {
-      const int32_t* a = ancs[row + i];
-      if (a) j = a[j];
-    }
   }
 }
 
@@ -1551,11 +1563,10 @@ extern "C" int ssm_trace(int dtype, int B, int S, int nx, int P, const void* con
   if (B <= 0 || S < 0 || nx <= 0 || P <= 0 || !xs || !ancs || !j_final || !out)
     return SSM_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int nt = 128;
   if (dtype == SSM_F64)
-    trace_kernel<double><<<(B + nt - 1) / nt, nt, 0, s>>>(B, S, nx, P, xs, ancs, j_final, out);
+    trace_kernel<double><<<B, 128, 0, s>>>(B, S, nx, P, xs, ancs, j_final, out);
   else if (dtype == SSM_F32)
-    trace_kernel<float><<<(B + nt - 1) / nt, nt, 0, s>>>(B, S, nx, P, xs, ancs, j_final, out);
+    trace_kernel<float><<<B, 128, 0, s>>>(B, S, nx, P, xs, ancs, j_final, out);
   else
     return SSM_ERR_INVALID_ARG;
   SSM_CHECK_LAUNCH();

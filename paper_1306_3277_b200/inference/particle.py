@@ -36,7 +36,7 @@ import torch
 from .. import _lib, profiling
 from ..errors import DegenerateEnsembleError, NonFiniteStateError, UnsupportedModelError
 from ..models import LOG_SQRT_2PI, ModelSpec, resolve_model
-from ..rng import device_key
+from ..rng import device_keys, first_uniforms
 from .timegrid import as_filter_grid
 from .types import FilterOutcome
 
@@ -363,7 +363,7 @@ def init_runs(runs, rngs):
             for b in need_draw:
                 x[b].copy_(torch.from_numpy(spec.host_initial(rngs[b], P).T.copy()).to(r0.tdtype))
         else:
-            keys = np.stack([device_key(rngs[b]) for b in need_draw]).astype(np.uint32)
+            keys = device_keys([rngs[b] for b in need_draw])
             kt = torch.from_numpy(keys.view(np.int32)).to(dev)
             if len(need_draw) == B:
                 _lib.check(_lib.lib().ssm_init_particles(spec.kernel, r0.dtype_id, B, P, 0, _lib.ptr(kt),
@@ -519,7 +519,7 @@ def advance_runs(runs, upto, rngs):
     host_noise = r0.noise == "host"
     keys_t = None
     if not host_noise:
-        keys = np.stack([device_key(g) for g in rngs]).astype(np.uint32)
+        keys = device_keys(rngs)
         keys_t = torch.from_numpy(keys.view(np.int32)).to(dev)
     scheme = _lib.SCHEME_IDS[r0.resampler]
     pw_ws = torch.empty(L.ssm_pw_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
@@ -715,7 +715,7 @@ def sample_trajectories(runs, rngs):
     cum = torch.empty((B, P), dtype=torch.int64, device=dev)
     _lib.check(L.ssm_weights_scan(B, P, r0.dtype_id, _lib.ptr(a), 1, _lib.ptr(shift), None, _lib.ptr(cum),
                                   None, _lib.ptr(scan_ws), stream), "ssm_weights_scan")
-    u = torch.from_numpy(np.array([[float(np.asarray(g.uniform(size=1))[0])] for g in rngs])).to(dev)
+    u = torch.from_numpy(first_uniforms(rngs, 1)).to(dev)  # each stream's uniform(size=1)
     j = torch.empty((B, 1), dtype=torch.int32, device=dev)
     _lib.check(L.ssm_resample_search(B, P, 1, _lib.SCHEME_IDS["multinomial"], 1, _lib.ptr(cum), _lib.ptr(u),
                                      None, 0, None, _lib.ptr(j), None, stream), "ssm_resample_search")

@@ -345,13 +345,12 @@ def propose_batch(spec, thetas, inits, rngs):
     ui = np.empty((C, spec.nx)) if has_init else None
     scale = 1.0 / (3.0 * th[:, ig])
     _require(np.all(3.0 * th[:, ig] > 0), "inverse_gamma scale must be > 0")
+    # consecutive uniform(size=1) calls == one uniform(size=n) call (one raw word per double)
     for c, rng in enumerate(rngs):
-        for k in range(n_tg):
-            u[c, k] = rng.uniform(size=1)[0]
+        u[c] = rng.uniform(size=n_tg)
         g[c] = rng.gamma(2.0, np.asarray(scale[c]), size=1)[0]
         if has_init:
-            for n in range(spec.nx):
-                ui[c, n] = rng.uniform(size=1)[0]
+            ui[c] = rng.uniform(size=spec.nx)
     for k, (slot, _, (sd, lo, hi)) in enumerate(stmts):
         m = th[:, slot]
         _require(lo < hi, "truncated_gaussian needs lower < upper")

@@ -145,3 +145,38 @@ def test_product_package_never_imports_oracle():
         for f in files:
             if f.endswith(".py"):
                 assert not pat.search(open(os.path.join(dirpath, f)).read()), f
+
+
+def test_batched_streams_bit_exact_with_numpy():
+    """rng.device_keys / first_uniforms / prime_streams restate numpy's
+    SeedSequence + Philox4x64-10 vectorised; every draw must equal numpy's
+    (including continuation draws of the same stream afterwards)."""
+    from paper_1306_3277_b200.rng import RngStream, device_key, device_keys, first_uniforms, prime_streams
+
+    def ref_gen(seed, key):
+        return np.random.Generator(np.random.Philox(np.random.SeedSequence(entropy=seed, spawn_key=key)))
+
+    r = np.random.default_rng(0)
+    cases = []
+    for i in range(120):
+        seed = int(r.integers(0, 2**63)) if i % 4 == 0 else int(r.integers(0, 1000))
+        key = tuple(int(x) for x in r.integers(0, 2**40 if i % 5 == 0 else 100, size=int(r.integers(0, 6))))
+        cases.append((seed, key))
+    streams = [RngStream(s, k) for s, k in cases]
+    assert (device_keys(streams) == np.stack([device_key(x) for x in streams])).all()
+    for n in (1, 4, 6):
+        streams = [RngStream(s, k) for s, k in cases]
+        got = first_uniforms(streams, n)
+        gens = [ref_gen(s, k) for s, k in cases]
+        assert (got == np.stack([g.uniform(size=n) for g in gens])).all()
+        for st, g in list(zip(streams, gens))[:30]:
+            assert st.gamma(2.0, 0.3, size=1).tolist() == g.gamma(2.0, 0.3, size=1).tolist()
+            assert st.uniform(size=3).tolist() == g.uniform(size=3).tolist()
+            assert st.normal(1.0, 2.0) == g.normal(1.0, 2.0)
+    streams = [RngStream(s, k) for s, k in cases]
+    prime_streams(streams)
+    assert all(st._state is not None for st in streams)
+    for st, (s, k) in zip(streams, cases):
+        g = ref_gen(s, k)
+        assert st.uniform() == g.uniform()
+        assert st.generator.uniform(size=2).tolist() == g.uniform(size=2).tolist()

@@ -653,22 +653,30 @@ def advance_runs(runs, upto, rngs):
     xstride = spec.nx * P * esz
     astride = P * 4
     fs_host = _fs_view(fs)  # one synchronisation per advance
-    incr = np.empty(B)
+    if (fs_host["err_nonfinite"] != _lib.INT32_MAX).any() or (fs_host["err_degenerate"] != _lib.INT32_MAX).any():
+        for b, r in enumerate(runs):
+            _raise_if_failed(fs_host[b], sched, r.check_finite)
+    ll = fs_host["loglik"].astype(float)
+    unif = fs_host["uniform"].astype(bool)
+    incr = ll - np.array([r.loglik for r in runs])
+    # per-step base pointers once; each run's rows are at a fixed stride
+    x_ptrs = np.array([xo.data_ptr() for xo, _ in new_hist], dtype=np.int64)
+    a_ptrs = np.array([an.data_ptr() if an is not None else 0 for _, an in new_hist], dtype=np.int64)
+    a_has = a_ptrs != 0
+    has_a = a_last is not None
+    keep_tiles = tiles_ok and has_a
     for b, r in enumerate(runs):
-        st = fs_host[b]
-        _raise_if_failed(st, sched, r.check_finite)
-        incr[b] = float(st["loglik"]) - r.loglik
-        r.loglik = float(st["loglik"])
-        r.weights_uniform = bool(st["uniform"])
+        r.loglik = float(ll[b])
+        r.weights_uniform = bool(unif[b])
         r._x = x_prev[b]
-        r._a = a_last[b] if a_last is not None else None
-        r._cdf = cdf_local[b] if (tiles_ok and a_last is not None) else None
-        r._trec = tile_rec[b] if (tiles_ok and a_last is not None) else None
+        r._a = a_last[b] if has_a else None
+        r._cdf = cdf_local[b] if keep_tiles else None
+        r._trec = tile_rec[b] if keep_tiles else None
         r._fs = fs[b]
         r._maybe_nonuniform = maybe_nonuniform
         r._hist.extend((xo, an, b) for xo, an in new_hist)
-        r._hx.extend(xo.data_ptr() + b * xstride for xo, _ in new_hist)
-        r._ha.extend((an.data_ptr() + b * astride) if an is not None else 0 for _, an in new_hist)
+        r._hx.extend((x_ptrs + b * xstride).tolist())
+        r._ha.extend(np.where(a_has, a_ptrs + b * astride, 0).tolist())
         r.pos = upto
     return incr
 
@@ -707,10 +715,13 @@ def sample_trajectories(runs, rngs):
             a_rows.append(r._a)
             shifts.append(r._fs)
     a = _stack_rows(a_rows)
-    shift = torch.zeros(B, dtype=torch.float64, device=dev)
-    for b, f in enumerate(shifts):
-        if f is not None:
-            shift[b : b + 1].copy_(f[8:16].view(torch.float64))  # ssm_filter_state.incr
+    if all(f is None for f in shifts):
+        shift = torch.zeros(B, dtype=torch.float64, device=dev)
+    else:  # ssm_filter_state.incr (bytes 8..16) of weighted runs, 0 for uniform ones
+        fs_rows = _stack_rows([r._fs for r in runs]).contiguous()
+        incr = fs_rows.view(torch.float64)[:, 1]
+        weighted = torch.tensor([f is not None for f in shifts], device=dev)
+        shift = torch.where(weighted, incr, torch.zeros_like(incr))
     scan_ws = torch.empty(L.ssm_scan_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     cum = torch.empty((B, P), dtype=torch.int64, device=dev)
     _lib.check(L.ssm_weights_scan(B, P, r0.dtype_id, _lib.ptr(a), 1, _lib.ptr(shift), None, _lib.ptr(cum),

@@ -24,6 +24,7 @@ from scipy.special import gammaln, ndtr, ndtri
 
 from . import _lib
 from .errors import DistributionParameterError, UnsupportedModelError
+from .rng import prime_streams
 
 LOG_SQRT_2PI = 0.5 * np.log(2.0 * np.pi)  # distributions.py:15
 
@@ -345,7 +346,9 @@ def propose_batch(spec, thetas, inits, rngs):
     ui = np.empty((C, spec.nx)) if has_init else None
     scale = 1.0 / (3.0 * th[:, ig])
     _require(np.all(3.0 * th[:, ig] > 0), "inverse_gamma scale must be > 0")
-    # consecutive uniform(size=1) calls == one uniform(size=n) call (one raw word per double)
+    # consecutive uniform(size=1) calls == one uniform(size=n) call (one raw word per double);
+    # fresh streams get their Philox state in one vectorised pass (rng.prime_streams)
+    prime_streams(rngs)
     for c, rng in enumerate(rngs):
         u[c] = rng.uniform(size=n_tg)
         g[c] = rng.gamma(2.0, np.asarray(scale[c]), size=1)[0]

@@ -24,6 +24,9 @@ Noise modes
             and order, rng.py / simulate.py:50-60 / resampling.py:28-33) are
             generated on the host and injected, so a float64 run reproduces
             the reference filter (parity mode).
+Arithmetic: `exact` (default: True with host noise, False with device noise)
+selects the reference's float64 op order without FMA contraction (bitwise)
+over the FMA-contracted fast kernels (1e-12 of the reference per step).
 """
 
 from __future__ import annotations
@@ -207,7 +210,7 @@ class ParticleRun:
 
     def __init__(self, ir, theta, grid, inputs=None, n_particles=1024, resampler="multinomial",
                  ess_rel=None, initial_state=None, check_finite=True, *, dtype="float64",
-                 exact=True, noise="device", device=None):
+                 exact=None, noise="device", device=None):
         if n_particles < 2:
             raise ValueError("particle filter needs n_particles >= 2")
         if resampler not in SCHEMES:
@@ -226,7 +229,10 @@ class ParticleRun:
         self.initial_state = initial_state
         self.check_finite = check_finite
         self.dtype_name, self.tdtype, self.dtype_id = _dtype_info(dtype)
-        self.exact = bool(exact)
+        # exact: float64 in the reference's op order without FMA contraction, which
+        # with noise="host" is bitwise the reference; default on for host noise and
+        # off (FMA, 1e-12 of the reference per step) for device noise
+        self.exact = (noise == "host") if exact is None else bool(exact)
         self.noise = noise
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.loglik = 0.0

@@ -234,9 +234,9 @@ __device__ __forceinline__ Lse fold_tiles(Lse st, double m, double t, double s2,
   return st;
 }
 
-// SIMPLE: one sub-step with one RK4 step and every obs slot present (the
-// benchmark grid) -- no runtime loops or per-slot predicates, sub-step
-// constants hoisted out of the particle loop.
+// SIMPLE: one sub-step with one RK4 step (the benchmark grid and the sparse
+// SMC^2 grid) -- no runtime sub-step loops, sub-step constants hoisted out of
+// the particle loop, observation slots selected by grid-uniform predicates.
 template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE = false>
 // NOTE: plain __launch_bounds__(kThreads).  An explicit minBlocks of 1 lets
 // ptxas spend 172 registers on the SIMPLE f64 kernel (1 CTA/SM, 0.80 ms
@@ -403,10 +403,19 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
             }
           } else {
             if constexpr (SIMPLE) {
+              const uint32_t mask = A.obs_mask;  // grid-uniform: no divergence
+              if (mask == 0xFFu) {
 #pragma unroll
-              for (int n = 0; n < 8; ++n) {
-                const T z = (static_cast<T>(A.y[n]) - x[n]) * T(2.0);
-                g = fma(T(-0.5) * z, z, g);
+                for (int n = 0; n < 8; ++n) {
+                  const T z = (static_cast<T>(A.y[n]) - x[n]) * T(2.0);
+                  g = fma(T(-0.5) * z, z, g);
+                }
+              } else {
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                  const T z = (static_cast<T>(A.y[n]) - x[n]) * T(2.0);
+                  if (mask & (1u << n)) g = fma(T(-0.5) * z, z, g);
+                }
               }
             } else {
 #pragma unroll
@@ -535,9 +544,8 @@ static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
   const dim3 grid(pw_grid_x(A.P), A.B);
   const bool inj = A.noise != nullptr;
   if constexpr (MODEL == SSM_MODEL_LORENZ96) {
-    // host hint: one sub-step with one RK4 step; and no obs or all 8 slots observed
-    const bool simple = (A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !A.exact && !inj &&
-                        (!A.has_obs || A.obs_mask == 0xFFu);
+    // host hint: one sub-step with one RK4 step (any observation mask)
+    const bool simple = (A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !A.exact && !inj;
     if (simple) {
       launch_pdl(pw_kernel<MODEL, T, false, false, true>, grid, dim3(kThreads), s, A);
       return;

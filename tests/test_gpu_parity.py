@@ -407,7 +407,7 @@ def test_tiles_resample_heavy_runs_match_oracle(scheme, P, pattern):
     np.testing.assert_array_equal(anc.cpu().numpy(), O.resample_with(w, scheme, u_np))
 
 
-def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float64", tiles=None):
+def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float64", tiles=None, obs_mask=0xFF):
     """One ssm_propagate_weight launch with device noise (C ABI), returns x_out, a_out."""
     from paper_1306_3277_b200 import _lib
     from paper_1306_3277_b200.inference.particle import _fs_init, _dtype_info
@@ -430,7 +430,7 @@ def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float6
     a = torch.empty(P, dtype=tdt, device=dev)
     A = _lib.PwArgs()
     A.model, A.dtype, A.B, A.P, A.step, A.n_sub = 0, dt_id, 1, P, 3, 1
-    A.exact, A.check_finite, A.has_obs, A.obs_mask = int(exact), 1, 1, 0xFF
+    A.exact, A.check_finite, A.has_obs, A.obs_mask = int(exact), 1, 1, obs_mask
     for n in range(8):
         A.y[n] = float(y[n])
     A.log_w0, A.obs_log_sd, A.log_sqrt_2pi, A.ess_rel = -np.log(P), np.log(0.5), LOG_SQRT_2PI, -1.0
@@ -449,16 +449,17 @@ def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float6
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 @pytest.mark.parametrize("d", [0.05, 0.04999999999999999, 0.05000000000000002])
-def test_specialised_kernel_equals_general(dtype, d):
-    """The SIMPLE (single sub-step, full obs) fused kernel must compute the same
-    step as the general kernel (same device draws)."""
+@pytest.mark.parametrize("mask", [0xFF, 0x0F, 0x81])
+def test_specialised_kernel_equals_general(dtype, d, mask):
+    """The SIMPLE (single sub-step) fused kernel must compute the same step as
+    the general kernel (same device draws), for full and partial observation masks."""
     rs = np.random.default_rng(3)
     P = 5000
     x = rs.uniform(-1, 3, (P, 8))
     y = rs.normal(0, 3, 8)
     keys = [123456789, 987654321]
-    x1, a1 = _pw_direct(x, [10.0, 0.1], keys, d, 1, y, dtype=dtype)
-    x0, a0 = _pw_direct(x, [10.0, 0.1], keys, d, 0, y, dtype=dtype)
+    x1, a1 = _pw_direct(x, [10.0, 0.1], keys, d, 1, y, dtype=dtype, obs_mask=mask)
+    x0, a0 = _pw_direct(x, [10.0, 0.1], keys, d, 0, y, dtype=dtype, obs_mask=mask)
     tol = 1e-12 if dtype == "float64" else 1e-5
     assert normwise(x1, x0) <= tol
     assert normwise(a1, a0) <= tol

@@ -51,14 +51,14 @@ def synthetic_data(T=T_BENCH):
     return times, ot, ov, om
 
 
-def workload_config(P, T, dtype):
+def workload_config(P, T, dtype, resampler="systematic"):
     return {
         "workload": f"Lorenz96 bootstrap particle filter, P=2^{int(math.log2(P))} particles, T={T} grid steps "
-                    f"(linspace(0,2,{T + 1}), 8/8 slots observed), systematic resampling, {dtype}",
+                    f"(linspace(0,2,{T + 1}), 8/8 slots observed), {resampler} resampling, {dtype}",
         "model": "Lorenz96 (8 state dims, RK4, h=delta=0.05)",
         "particles": P,
         "grid_steps": T,
-        "resampler": "systematic",
+        "resampler": resampler,
         "noise": "device Philox4x32-10",
         "global_batch": P,
         "seq_len": T,
@@ -159,9 +159,9 @@ def run_ours(args, rank, world):
         if sharded:  # one filter of world * P particles, NCCL collectives every weighted step (config 5)
             from paper_1306_3277_b200.inference import particle_filter_sharded
 
-            return _Out(*particle_filter_sharded(LORENZ96, THETA, grid_obj, rng, world * P, resampler="systematic",
+            return _Out(*particle_filter_sharded(LORENZ96, THETA, grid_obj, rng, world * P, resampler=args.resampler,
                                                  dtype=args.dtype, exact=args.exact))
-        return particle_filter(LORENZ96, THETA, grid_obj, rng, n_particles=P, resampler="systematic", **opts)
+        return particle_filter(LORENZ96, THETA, grid_obj, rng, n_particles=P, resampler=args.resampler, **opts)
 
     def one(step, grid_obj, timer=None):
         rng = RngStream(7, ((0 if sharded else rank), step))
@@ -305,6 +305,7 @@ def main():
     ap.add_argument("--particles", type=int, default=P_BENCH)
     ap.add_argument("--T", type=int, default=T_BENCH)
     ap.add_argument("--dtype", default="float64", choices=["float64", "float32"])
+    ap.add_argument("--resampler", default="systematic", choices=["systematic", "stratified", "multinomial"])
     ap.add_argument("--exact", action="store_true",
                     help="bitwise reference op order (no FMA contraction); default: FMA-contracted float64")
     ap.add_argument("--variants", type=int, default=1, help="also time f64-exact and f32 variants")
@@ -362,7 +363,7 @@ def main():
         "vs_baseline": None,
         "dtype": dtype_tag,
         "data": "synthetic (L96 theta*=(10,0.1) simulated per SURVEY 8d; device Philox noise)",
-        "config": dict(workload_config(P, T, args.dtype), arithmetic=arith,
+        "config": dict(workload_config(P, T, args.dtype, args.resampler), arithmetic=arith,
                        parallelism=("replicas" if world == 1 or args.mode == "replicas"
                                     else f"one filter sharded over {world} GPUs (NCCL all-gather of LSE partials and "
                                          "CDF totals + P2P spill of ancestor states per step)")),
@@ -394,11 +395,13 @@ def main():
                        "ms_per_step": res["e2e_ms"]}
     if args.variants and world == 1:
         line["variants"] = {}
-        for name, dt, ex in (("f64_exact_bitwise", "float64", True), ("f32", "float32", False)):
-            if (dt, ex) == (args.dtype, args.exact):
+        for name, dt, ex, rs in (("f64_exact_bitwise", "float64", True, args.resampler),
+                                 ("f32", "float32", False, args.resampler),
+                                 ("f64_multinomial", "float64", False, "multinomial")):
+            if (dt, ex, rs) == (args.dtype, args.exact, args.resampler):
                 continue
             v_args = argparse.Namespace(**vars(args))
-            v_args.dtype, v_args.exact, v_args.e2e_steps = dt, ex, 0
+            v_args.dtype, v_args.exact, v_args.e2e_steps, v_args.resampler = dt, ex, 0, rs
             v = run_ours(v_args, rank, world)
             vpw = v["kern"].get("propagate_weight", {})
             line["variants"][name] = {

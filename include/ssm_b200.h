@@ -54,7 +54,11 @@ typedef enum {
 typedef enum {
   SSM_MULTINOMIAL = 0,
   SSM_STRATIFIED = 1,
-  SSM_SYSTEMATIC = 2
+  SSM_SYSTEMATIC = 2,
+  /* multinomial with device draws whose ancestors come back in ascending order:
+   * the reference's draw (iid uniforms searched in the CDF), slot order sorted
+   * (ssm_resample_from_logw / ssm_advance only) */
+  SSM_MULTINOMIAL_SORTED = 3
 } ssm_scheme;
 
 /* flag bits written by ssm_weights_scan for raw (non-log) weights,

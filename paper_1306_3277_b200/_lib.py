@@ -19,6 +19,7 @@ SSM_OK, SSM_ERR_INVALID_ARG, SSM_ERR_CUDA, SSM_ERR_UNSUPPORTED = 0, 1, 2, 3
 SSM_F32, SSM_F64 = 0, 1
 SSM_MODEL_LORENZ96, SSM_MODEL_WINDKESSEL = 0, 1
 SCHEME_IDS = {"multinomial": 0, "stratified": 1, "systematic": 2}
+SSM_MULTINOMIAL_SORTED = 3  # device-noise multinomial, ancestors in ascending order
 SSM_FLAG_BAD_WEIGHT, SSM_FLAG_ZERO_TOTAL = 1, 2
 INT32_MAX = 2**31 - 1
 

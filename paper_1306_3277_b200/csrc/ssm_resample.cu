@@ -811,6 +811,86 @@ long_runs_kernel(int P_in, int P_out, const int4* __restrict__ runs, const uint3
 // Counts are c_j = #{k : u_k < C_j / total} exactly (systematic fast accept when
 // C_j P / total - u is not within 2^-20 of an integer, query-by-query otherwise);
 // the last particle's run ends at P (cum[-1] = 1.0, resampling.py:27 + clip).
+// Shared-memory window of a block's outputs (see offspring_tiles_kernel).
+constexpr int kRunIt = kScanTile / kThreads;  // 32-particle tiles per warp (8)
+struct RunWindow {
+  int32_t out[4096 + 4096 / 32];
+  int lo, hi;
+  int wmax[kThreads / 32];
+};
+
+// Writes anc for a block's particles [jw, jw + 256) per warp (lane = particle,
+// cv / pv = c_j / c_{j-1} for the warp's 8 tiles).  sm.lo = c_{j0-1} must be
+// set by the caller before the call; the last thread's cv is the window end.
+// Windows up to 4096 outputs are filled in shared memory (run-start marks +
+// max-scan) and stored coalesced; larger ones (degenerate weights) write short
+// runs directly and defer long runs to long_runs_kernel.
+__device__ __forceinline__ void fill_run_window(RunWindow& sm, int b, int P, int jw, const int (&cv)[kRunIt],
+                                                const int (&pv)[kRunIt], int32_t* __restrict__ anc,
+                                                int4* __restrict__ long_runs, uint32_t* __restrict__ long_count) {
+  constexpr int kOutBuf = 4096;
+  constexpr int kPer = kOutBuf / kThreads;
+  constexpr int kIt = kRunIt;
+  static_assert(kPer == 16 && kIt == 8, "layout");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == kThreads - 1) sm.hi = cv[kIt - 1];
+  for (int e = threadIdx.x; e < (kOutBuf + kOutBuf / 32) / 4; e += kThreads)
+    reinterpret_cast<int4*>(sm.out)[e] = make_int4(-1, -1, -1, -1);
+  __syncthreads();
+  const int lo_blk = sm.lo, n_out = sm.hi - lo_blk;
+  int32_t* ab = anc + static_cast<size_t>(b) * P;
+  if (n_out <= kOutBuf) {
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+      const int e = pv[it] - lo_blk;
+      if (cv[it] > pv[it]) sm.out[e + (e >> 5)] = jw + it * 32 + lane;
+    }
+    __syncthreads();
+    int32_t* sv = sm.out + threadIdx.x * kPer + (threadIdx.x >> 1);  // pad(t*16 + i) = t*16 + i + t/2
+    int v[kPer];
+    int run = -1;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      run = max(run, sv[i]);
+      v[i] = run;
+    }
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = max(incl, y);
+    }
+    int cin = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) cin = -1;
+    if (lane == 31) sm.wmax[warp] = incl;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w)
+      if (w < warp) cin = max(cin, sm.wmax[w]);
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) sv[i] = max(cin, v[i]);
+    __syncthreads();
+    for (int e = threadIdx.x; e < n_out; e += kThreads) ab[lo_blk + e] = sm.out[e + (e >> 5)];
+  } else {
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+      const int j = jw + it * 32 + lane, lo = pv[it], hi = cv[it];
+      if (hi - lo <= kShortRun) {
+        for (int k = lo; k < hi; ++k) ab[k] = j;
+      } else {
+        const int nchunk = (hi - lo + kRunChunk - 1) / kRunChunk;
+        const uint32_t slot = atomicAdd(long_count + b, static_cast<uint32_t>(nchunk));
+        int4* rb = long_runs + static_cast<size_t>(b) * long_runs_cap(P, P);
+        for (int q = 0; q < nchunk; ++q) {
+          const int lo_q = lo + q * kRunChunk;
+          rb[slot + q] = make_int4(j, lo_q, min(lo_q + kRunChunk, hi), 0);
+        }
+      }
+    }
+  }
+}
+
+
 template <int SCHEME>
 __global__ void __launch_bounds__(kThreads)
 offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const double* __restrict__ scale,
@@ -819,13 +899,8 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
                        const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc,
                        int4* __restrict__ long_runs, uint32_t* __restrict__ long_count) {
   pdl_wait();
-  constexpr int kOutBuf = 4096;             // staged outputs per block
-  constexpr int kPer = kOutBuf / kThreads;  // outputs per thread in the fill scan
-  constexpr int kIt = kScanTile / kThreads; // 32-particle tiles per warp
-  static_assert(kPer == 16 && kIt == 8, "layout");
-  __shared__ __align__(16) int32_t sOut[kOutBuf + kOutBuf / 32];
-  __shared__ int s_lo, s_hi;
-  __shared__ int s_wmax[kThreads / 32];
+  constexpr int kIt = kRunIt;
+  __shared__ __align__(16) RunWindow sm;
   const int b = blockIdx.y;
   if (fs && !fs[b].resample_now) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -878,7 +953,7 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
   int carry = 0;
   if (jw > 0 && jw < P) carry = count(pre0);
   else if (jw >= P) carry = P;
-  if (warp == 0 && lane == 0) s_lo = carry;
+  if (warp == 0 && lane == 0) sm.lo = carry;
   int cv[kIt], pv[kIt];
 #pragma unroll
   for (int it = 0; it < kIt; ++it) {
@@ -892,61 +967,114 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
     cv[it] = c;
     carry = __shfl_sync(0xffffffffu, c, 31);
   }
-  if (threadIdx.x == kThreads - 1) s_hi = cv[kIt - 1];
-  for (int e = threadIdx.x; e < (kOutBuf + kOutBuf / 32) / 4; e += kThreads)
-    reinterpret_cast<int4*>(sOut)[e] = make_int4(-1, -1, -1, -1);
+  fill_run_window(sm, b, P, jw, cv, pv, anc, long_runs, long_count);
+}
+
+// ---------------------------------------------------------------------------
+// Sorted multinomial (device noise, SSM_MULTINOMIAL_SORTED): the reference's
+// draw -- P iid uniforms searched in the CDF (resampling.py:28-36) -- but each
+// query only counts its ancestor; the counts are then expanded into ascending
+// ancestor runs.  The multiset of ancestors is the reference's; slots come out
+// sorted, so the following gather x[anc] streams instead of scattering (the
+// slot order of exchangeable particles does not change the filter's law).
+// ---------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(kThreads)
+search_count_kernel(int P, const void* __restrict__ cum, const uint32_t* __restrict__ keys, int step,
+                    const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ cnt) {
+  const int b = blockIdx.y;
+  if (fs && !fs[b].resample_now) return;
+  const size_t coff = static_cast<size_t>(b) * P;
+  const double tot = cum_total<KIND>(cum, coff, P);
+  const uint32_t k0 = keys[2 * b], k1 = keys[2 * b + 1];
+  int32_t* cb = cnt + coff;
+  for (int k = blockIdx.x * kThreads + threadIdx.x; k < P; k += gridDim.x * kThreads) {
+    const double q = device_uniform(k0, k1, k, step, kPurposeResample);
+    int lo = 0, hi = P;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cum_at<KIND>(cum, coff, tot, mid) <= q)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    atomicAdd(cb + (lo < P ? lo : P - 1), 1);
+  }
+}
+
+// per 2048-particle block: sum of offspring counts
+__global__ void __launch_bounds__(kThreads)
+count_blocks_kernel(int P, const int32_t* __restrict__ cnt, const ssm_filter_state* __restrict__ fs,
+                    uint64_t* __restrict__ blk) {
+  __shared__ int s_w[kThreads / 32];
+  const int b = blockIdx.y;
+  if (fs && !fs[b].resample_now) return;
+  const int32_t* cb = cnt + static_cast<size_t>(b) * P;
+  const int j0 = blockIdx.x * kScanTile;
+  int v = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int j = j0 + i * kThreads + threadIdx.x;
+    if (j < P) v += cb[j];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
   __syncthreads();
-  const int lo_blk = s_lo, n_out = s_hi - lo_blk;
-  int32_t* ab = anc + static_cast<size_t>(b) * P;
-  if (n_out <= kOutBuf) {
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kThreads / 32; ++w) t += s_w[w];
+    blk[static_cast<size_t>(b) * gridDim.x + blockIdx.x] = static_cast<uint64_t>(t);
+  }
+}
+
+// offspring counts -> ascending ancestors (lane = particle, same window fill as
+// the filter path's offspring kernel)
+__global__ void __launch_bounds__(kThreads)
+expand_counts_kernel(int P, const int32_t* __restrict__ cnt, const uint64_t* __restrict__ blk_pref,
+                     const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc,
+                     int4* __restrict__ long_runs, uint32_t* __restrict__ long_count) {
+  __shared__ __align__(16) RunWindow sm;
+  __shared__ int s_wsum[kThreads / 32];
+  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (fs && !fs[b].resample_now) {  // ESS gate held: identity ancestors
+    int32_t* ab = anc + static_cast<size_t>(b) * P;
+    for (int k = blockIdx.x * kScanTile + threadIdx.x; k < min(P, (blockIdx.x + 1) * kScanTile); k += kThreads)
+      ab[k] = k;
+    return;
+  }
+  const int jw = blockIdx.x * kScanTile + warp * (kScanTile / (kThreads / 32));
+  const int32_t* cb = cnt + static_cast<size_t>(b) * P;
+  int cn[kRunIt];
+  int wsum = 0;
 #pragma unroll
-    for (int it = 0; it < kIt; ++it) {
-      const int e = pv[it] - lo_blk;
-      if (cv[it] > pv[it]) sOut[e + (e >> 5)] = jw + it * 32 + lane;
-    }
-    __syncthreads();
-    int32_t* sv = sOut + threadIdx.x * kPer + (threadIdx.x >> 1);  // pad(t*16 + i) = t*16 + i + t/2
-    int v[kPer];
-    int run = -1;
+  for (int it = 0; it < kRunIt; ++it) {
+    const int j = jw + it * 32 + lane;
+    cn[it] = j < P ? cb[j] : 0;
+    wsum += cn[it];
+  }
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      run = max(run, sv[i]);
-      v[i] = run;
-    }
-    int incl = run;
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+  if (lane == 0) s_wsum[warp] = wsum;
+  __syncthreads();
+  int carry = static_cast<int>(blk_pref[static_cast<size_t>(b) * gridDim.x + blockIdx.x]);
+  for (int w = 0; w < warp; ++w) carry += s_wsum[w];
+  if (warp == 0 && lane == 0) sm.lo = carry;
+  int cv[kRunIt], pv[kRunIt];
+#pragma unroll
+  for (int it = 0; it < kRunIt; ++it) {
+    int incl = cn[it];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl = max(incl, y);
+      if (lane >= o) incl += y;
     }
-    int cin = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane == 0) cin = -1;
-    if (lane == 31) s_wmax[warp] = incl;
-    __syncthreads();
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w)
-      if (w < warp) cin = max(cin, s_wmax[w]);
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) sv[i] = max(cin, v[i]);
-    __syncthreads();
-    for (int e = threadIdx.x; e < n_out; e += kThreads) ab[lo_blk + e] = sOut[e + (e >> 5)];
-  } else {
-#pragma unroll
-    for (int it = 0; it < kIt; ++it) {
-      const int j = jw + it * 32 + lane, lo = pv[it], hi = cv[it];
-      if (hi - lo <= kShortRun) {
-        for (int k = lo; k < hi; ++k) ab[k] = j;
-      } else {
-        const int nchunk = (hi - lo + kRunChunk - 1) / kRunChunk;
-        const uint32_t slot = atomicAdd(long_count + b, static_cast<uint32_t>(nchunk));
-        int4* rb = long_runs + static_cast<size_t>(b) * long_runs_cap(P, P);
-        for (int q = 0; q < nchunk; ++q) {
-          const int lo_q = lo + q * kRunChunk;
-          rb[slot + q] = make_int4(j, lo_q, min(lo_q + kRunChunk, hi), 0);
-        }
-      }
-    }
+    cv[it] = carry + incl;
+    pv[it] = cv[it] - cn[it];
+    carry = __shfl_sync(0xffffffffu, cv[it], 31);
   }
+  fill_run_window(sm, b, P, jw, cv, pv, anc, long_runs, long_count);
 }
 
 // anc_k = #{j : c_j <= k}, clipped to P_in - 1, from the precomputed partition.
@@ -1509,6 +1637,25 @@ extern "C" int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const
     if (st != SSM_OK) return st;
     const dim3 g(grid_for(P, kThreads, 65535), B);
     binary_search_kernel<1><<<g, kThreads, 0, s>>>(P, P, w.C, u, keys, step, fs, anc);
+  } else if (scheme == SSM_MULTINOMIAL_SORTED) {
+    if (u || !keys) return SSM_ERR_INVALID_ARG;  // device draws only
+    int st = ssm_weights_scan(B, P, dtype, a, 1, shift, fs, w.C, nullptr, w.scan, stream);
+    if (st != SSM_OK) return st;
+    // counts in w.cnt; block sums in w.sums; long-run list in w.C (free after the search)
+    uint32_t* long_count = reinterpret_cast<uint32_t*>(w.totals) + 2 * static_cast<size_t>(B);
+    cudaError_t e = cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * static_cast<size_t>(B) * P, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(long_count, 0, sizeof(uint32_t) * B, s);
+    if (e != cudaSuccess) {
+      ssm_set_last_error(e);
+      return SSM_ERR_CUDA;
+    }
+    search_count_kernel<1><<<dim3(grid_for(P, kThreads, 65535), B), kThreads, 0, s>>>(P, w.C, keys, step, fs, w.cnt);
+    count_blocks_kernel<<<dim3(tiles, B), kThreads, 0, s>>>(P, w.cnt, fs, w.sums);
+    blk_prefix_kernel<<<B, 1024, 0, s>>>(tiles, w.sums, w.totals, fs);
+    int4* long_runs = reinterpret_cast<int4*>(w.C);
+    expand_counts_kernel<<<dim3(tiles, B), kThreads, 0, s>>>(P, w.cnt, w.sums, fs, anc, long_runs, long_count);
+    const int gx = std::max(1, std::min(1184 / B, P / kRunChunk + 1));
+    long_runs_kernel<<<dim3(gx, B), kThreads, 0, s>>>(P, P, long_runs, long_count, fs, anc);
   } else if (scheme == SSM_SYSTEMATIC || scheme == SSM_STRATIFIED) {
     if (dtype == SSM_F64) {
       tile_sums_kernel<double><<<dim3(tiles, B), kThreads, 0, s>>>(P, static_cast<const double*>(a), shift, fs, w.sums);

@@ -378,9 +378,9 @@ def _heavy_patterns(P):
     one = np.full(P, -1e4)
     one[P // 3] = 0.0
     few = np.full(P, -30.0)
-    few[[5, 6, 4000, P // 2, P - 1]] = 0.0  # runs of ~P/5 outputs (> one block window)
+    few[[5, 6, min(4000, P - 3), P // 2, P - 1]] = 0.0  # runs of ~P/5 outputs (> one block window)
     cluster = np.zeros(P)  # long runs inside staged block windows (<= 4096 outputs)
-    cluster[10], cluster[3000] = np.log(1000.0), np.log(40.0)
+    cluster[10], cluster[min(3000, P - 1)] = np.log(1000.0), np.log(40.0)
     lognorm = r.normal(0.0, 3.0, P)  # mixed: long and short runs, ragged windows
     return {"one": one, "few": few, "cluster": cluster, "lognormal": lognorm}
 
@@ -541,3 +541,29 @@ def test_tile_records_match_documented_format(P):
         d = np.diff(np.concatenate([np.zeros(1, np.uint64), cdf])).astype(np.float64)  # each q_j <= 2^52: exact
         assert np.all(np.abs(d - q) <= 4.0 + q * 1e-15), (w, np.max(np.abs(d - q)))
         assert tiles["Q"][w] == tiles["cdf"][32 * w + aw.size - 1]
+
+
+@pytest.mark.parametrize("P", [1000, 5000, 1 << 16])
+@pytest.mark.parametrize("pattern", ["lognormal", "one", "few"])
+def test_sorted_multinomial_is_sorted_reference_draw(P, pattern):
+    """SSM_MULTINOMIAL_SORTED (device-noise filter path) returns exactly the
+    ancestors of the plain multinomial search for the same device draws, in
+    ascending order (B = 2 filters, ragged P, degenerate weights -> long runs)."""
+    from paper_1306_3277_b200 import _lib
+
+    L = _lib.lib()
+    pats = _heavy_patterns(P)
+    a_np = np.stack([pats[pattern], pats["lognormal"]])
+    from scipy.special import logsumexp
+
+    a = torch.from_numpy(a_np).cuda()
+    shift = torch.from_numpy(logsumexp(a_np, axis=1)).cuda()
+    keys = torch.tensor([[11, 22], [33, 44]], dtype=torch.int32, device="cuda")
+    ws = torch.empty(L.ssm_resample_workspace_bytes(2, P), dtype=torch.uint8, device="cuda")
+    out = {}
+    for scheme in (0, _lib.SSM_MULTINOMIAL_SORTED):
+        anc = torch.full((2, P), -1, dtype=torch.int32, device="cuda")
+        _lib.check(L.ssm_resample_from_logw(2, P, 1, scheme, _lib.ptr(a), _lib.ptr(shift), None, None,
+                                            _lib.ptr(keys), 5, _lib.ptr(anc), _lib.ptr(ws), _lib.stream_ptr()))
+        out[scheme] = anc.cpu().numpy()
+    np.testing.assert_array_equal(out[_lib.SSM_MULTINOMIAL_SORTED], np.sort(out[0], axis=1))

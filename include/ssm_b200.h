@@ -55,9 +55,10 @@ typedef enum {
   SSM_MULTINOMIAL = 0,
   SSM_STRATIFIED = 1,
   SSM_SYSTEMATIC = 2,
-  /* multinomial with device draws whose ancestors come back in ascending order:
-   * the reference's draw (iid uniforms searched in the CDF), slot order sorted
-   * (ssm_resample_from_logw / ssm_advance only) */
+  /* multinomial with device draws, ancestors in ascending order: searchsorted(cum,
+   * U_(k)) with U_(k) = S_k / S_{P+1} the order statistics of P iid uniforms from
+   * exponential spacings (the law of resampling.py:28-36's multinomial draw, slot
+   * order sorted).  ssm_resample_from_logw / ssm_advance with device keys only. */
   SSM_MULTINOMIAL_SORTED = 3
 } ssm_scheme;
 

@@ -56,6 +56,7 @@ enum Purpose : uint32_t {
   kPurposeResample = 2u,
   kPurposeInit = 3u,
   kPurposeSystematic = 4u,
+  kPurposeSpacing = 5u,  // exponential spacings of the sorted multinomial
 };
 
 // 53-bit uniform in [0,1) from two 32-bit words (same construction as numpy's

@@ -971,110 +971,196 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
 }
 
 // ---------------------------------------------------------------------------
-// Sorted multinomial (device noise, SSM_MULTINOMIAL_SORTED): the reference's
-// draw -- P iid uniforms searched in the CDF (resampling.py:28-36) -- but each
-// query only counts its ancestor; the counts are then expanded into ascending
-// ancestor runs.  The multiset of ancestors is the reference's; slots come out
-// sorted, so the following gather x[anc] streams instead of scattering (the
-// slot order of exchangeable particles does not change the filter's law).
+// Sorted multinomial via exponential spacings: with E_1..E_{P+1} iid Exp(1) and
+// S_k = E_1 + ... + E_k, (S_1, ..., S_P) / S_{P+1} has the law of P sorted iid
+// U(0,1) draws, so searchsorted(cum, U_(k)) is a multinomial sample with the
+// ancestors already ascending.  Each 2048-output block rebuilds its U_(k) in
+// shared memory (the block's spacing sums come from spacing_sums_kernel and a
+// one-block prefix, all in a fixed summation order: deterministic), finds its
+// first and last ancestor by binary search, and fills its outputs from the
+// particles in between (count of U_(k) < cum_j per particle, run-start marks,
+// max-scan).  Replaces P random-access searches of the unsorted draw.
 // ---------------------------------------------------------------------------
-template <int KIND>
+__device__ __forceinline__ double spacing(uint32_t k0, uint32_t k1, uint32_t k, uint32_t step) {
+  const U4 r = philox4x32_10(U4{k, step, 0u, kPurposeSpacing}, k0, k1);
+  return -log(1.0 - u53(r.x, r.y));  // 1 - u in (0, 1], exact
+}
+
+// inclusive prefix of the block's 2048 spacings (thread t: items 8t..8t+7), fixed order;
+// returns the thread's 8 inclusive values and the block total (all threads)
+__device__ __forceinline__ double spacing_block_scan(uint32_t k0, uint32_t k1, int step, int kbase, int n_valid,
+                                                     double (&v)[kScanItems], double* s_warp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double run = 0.0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int kl = threadIdx.x * kScanItems + i;
+    run += kl < n_valid ? spacing(k0, k1, static_cast<uint32_t>(kbase + kl), static_cast<uint32_t>(step)) : 0.0;
+    v[i] = run;
+  }
+  double incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  double wex = 0.0, tot = 0.0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (w < warp) wex += s_warp[w];
+    tot += s_warp[w];
+  }
+  const double base = wex + (incl - run);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) v[i] += base;
+  __syncthreads();
+  return tot;
+}
+
+// block totals of the P + 1 spacings (outputs k = 0..P; k = P is the extra E_{P+1})
 __global__ void __launch_bounds__(kThreads)
-search_count_kernel(int P, const void* __restrict__ cum, const uint32_t* __restrict__ keys, int step,
-                    const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ cnt) {
+spacing_sums_kernel(int P, const uint32_t* __restrict__ keys, int step, const ssm_filter_state* __restrict__ fs,
+                    double* __restrict__ blk) {
+  __shared__ double s_warp[kThreads / 32];
   const int b = blockIdx.y;
   if (fs && !fs[b].resample_now) return;
+  const int kbase = blockIdx.x * kScanTile;
+  double v[kScanItems];
+  const double tot = spacing_block_scan(keys[2 * b], keys[2 * b + 1], step, kbase, min(kScanTile, P + 1 - kbase), v, s_warp);
+  if (threadIdx.x == 0) blk[static_cast<size_t>(b) * gridDim.x + blockIdx.x] = tot;
+}
+
+// exclusive prefix of the block totals in place (fixed order), grand total -> tot[b]
+__global__ void __launch_bounds__(1024)
+spacing_prefix_kernel(int nblk, double* __restrict__ blk, double* __restrict__ tot,
+                      const ssm_filter_state* __restrict__ fs) {
+  __shared__ double wsum[32];
+  const int b = blockIdx.x;
+  if (fs && !fs[b].resample_now) return;
+  double* bb = blk + static_cast<size_t>(b) * nblk;
+  const int per = (nblk + 1023) / 1024;
+  const int t0 = threadIdx.x * per, t1 = min(t0 + per, nblk);
+  double local = 0.0;
+  for (int t = t0; t < t1; ++t) local += bb[t];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  double wex = 0.0, all = 0.0;
+  for (int w = 0; w < 32; ++w) {
+    if (w < warp) wex += wsum[w];
+    all += wsum[w];
+  }
+  double run = wex + incl - local;
+  for (int t = t0; t < t1; ++t) {
+    const double x = bb[t];
+    bb[t] = run;
+    run += x;
+  }
+  if (threadIdx.x == 0) tot[b] = all;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads)
+spacing_merge_kernel(int P, const void* __restrict__ cum, const uint32_t* __restrict__ keys, int step,
+                     const double* __restrict__ blk, const double* __restrict__ tot,
+                     const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc) {
+  __shared__ double sU[kScanTile];
+  __shared__ __align__(16) int32_t sOut[kScanTile + kScanTile / 32];
+  __shared__ double s_warp[kThreads / 32];
+  __shared__ int s_wmax[kThreads / 32];
+  __shared__ int s_j[2];
+  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t* ab = anc + static_cast<size_t>(b) * P;
+  const int k0 = blockIdx.x * kScanTile, n_out = min(kScanTile, P - k0);
+  if (fs && !fs[b].resample_now) {  // ESS gate held: identity ancestors
+    for (int k = threadIdx.x; k < n_out; k += kThreads) ab[k0 + k] = k0 + k;
+    return;
+  }
+  double v[kScanItems];
+  spacing_block_scan(keys[2 * b], keys[2 * b + 1], step, k0, n_out, v, s_warp);
+  const double off = blk[static_cast<size_t>(b) * (gridDim.x + (P % kScanTile == 0 ? 1 : 0)) + blockIdx.x];
+  const double inv = 1.0 / tot[b];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) sU[threadIdx.x * kScanItems + i] = (off + v[i]) * inv;  // U_(k0+k)
+  for (int e = threadIdx.x; e < (kScanTile + kScanTile / 32) / 4; e += kThreads)
+    reinterpret_cast<int4*>(sOut)[e] = make_int4(-1, -1, -1, -1);
   const size_t coff = static_cast<size_t>(b) * P;
-  const double tot = cum_total<KIND>(cum, coff, P);
-  const uint32_t k0 = keys[2 * b], k1 = keys[2 * b + 1];
-  int32_t* cb = cnt + coff;
-  for (int k = blockIdx.x * kThreads + threadIdx.x; k < P; k += gridDim.x * kThreads) {
-    const double q = device_uniform(k0, k1, k, step, kPurposeResample);
+  const double ctot = cum_total<KIND>(cum, coff, P);
+  __syncthreads();
+  // first / last ancestor: searchsorted(cum, U, 'right'), clipped
+  if (threadIdx.x < 2) {
+    const double q = sU[threadIdx.x == 0 ? 0 : n_out - 1];
     int lo = 0, hi = P;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (cum_at<KIND>(cum, coff, tot, mid) <= q)
+      if (cum_at<KIND>(cum, coff, ctot, mid) <= q)
         lo = mid + 1;
       else
         hi = mid;
     }
-    atomicAdd(cb + (lo < P ? lo : P - 1), 1);
+    s_j[threadIdx.x] = lo < P ? lo : P - 1;
   }
-}
-
-// per 2048-particle block: sum of offspring counts
-__global__ void __launch_bounds__(kThreads)
-count_blocks_kernel(int P, const int32_t* __restrict__ cnt, const ssm_filter_state* __restrict__ fs,
-                    uint64_t* __restrict__ blk) {
-  __shared__ int s_w[kThreads / 32];
-  const int b = blockIdx.y;
-  if (fs && !fs[b].resample_now) return;
-  const int32_t* cb = cnt + static_cast<size_t>(b) * P;
-  const int j0 = blockIdx.x * kScanTile;
-  int v = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int j = j0 + i * kThreads + threadIdx.x;
-    if (j < P) v += cb[j];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < kThreads / 32; ++w) t += s_w[w];
-    blk[static_cast<size_t>(b) * gridDim.x + blockIdx.x] = static_cast<uint64_t>(t);
-  }
-}
-
-// offspring counts -> ascending ancestors (lane = particle, same window fill as
-// the filter path's offspring kernel)
-__global__ void __launch_bounds__(kThreads)
-expand_counts_kernel(int P, const int32_t* __restrict__ cnt, const uint64_t* __restrict__ blk_pref,
-                     const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc,
-                     int4* __restrict__ long_runs, uint32_t* __restrict__ long_count) {
-  __shared__ __align__(16) RunWindow sm;
-  __shared__ int s_wsum[kThreads / 32];
-  const int b = blockIdx.y;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (fs && !fs[b].resample_now) {  // ESS gate held: identity ancestors
-    int32_t* ab = anc + static_cast<size_t>(b) * P;
-    for (int k = blockIdx.x * kScanTile + threadIdx.x; k < min(P, (blockIdx.x + 1) * kScanTile); k += kThreads)
-      ab[k] = k;
-    return;
-  }
-  const int jw = blockIdx.x * kScanTile + warp * (kScanTile / (kThreads / 32));
-  const int32_t* cb = cnt + static_cast<size_t>(b) * P;
-  int cn[kRunIt];
-  int wsum = 0;
-#pragma unroll
-  for (int it = 0; it < kRunIt; ++it) {
-    const int j = jw + it * 32 + lane;
-    cn[it] = j < P ? cb[j] : 0;
-    wsum += cn[it];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-  if (lane == 0) s_wsum[warp] = wsum;
-  __syncthreads();
-  int carry = static_cast<int>(blk_pref[static_cast<size_t>(b) * gridDim.x + blockIdx.x]);
-  for (int w = 0; w < warp; ++w) carry += s_wsum[w];
-  if (warp == 0 && lane == 0) sm.lo = carry;
-  int cv[kRunIt], pv[kRunIt];
-#pragma unroll
-  for (int it = 0; it < kRunIt; ++it) {
-    int incl = cn[it];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
+  const int jlo = s_j[0], jhi = s_j[1];
+  // local count of U < cum_j (the last particle takes every remaining output: clip rule)
+  auto cnt_lt = [&](int j) -> int {
+    if (j < jlo) return 0;
+    if (j >= P - 1 || j >= jhi) return n_out;
+    const double c = cum_at<KIND>(cum, coff, ctot, j);
+    int lo = 0, hi = n_out;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sU[mid] < c)
+        lo = mid + 1;
+      else
+        hi = mid;
     }
-    cv[it] = carry + incl;
-    pv[it] = cv[it] - cn[it];
-    carry = __shfl_sync(0xffffffffu, cv[it], 31);
+    return lo;
+  };
+  for (int j = jlo + threadIdx.x; j <= jhi; j += kThreads) {
+    const int a = cnt_lt(j - 1), c = cnt_lt(j);
+    if (c > a) sOut[a + (a >> 5)] = j;
   }
-  fill_run_window(sm, b, P, jw, cv, pv, anc, long_runs, long_count);
+  __syncthreads();
+  // inclusive max-scan of the marks (all outputs have an owner: position 0 is jlo's)
+  constexpr int kPer = kScanTile / kThreads;  // 8
+  int vv[kPer];
+  int run = -1;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int e = threadIdx.x * kPer + i;
+    run = max(run, sOut[e + (e >> 5)]);
+    vv[i] = run;
+  }
+  int incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = max(incl, y);
+  }
+  int cin = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) cin = -1;
+  if (lane == 31) s_wmax[warp] = incl;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w)
+    if (w < warp) cin = max(cin, s_wmax[w]);
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int e = threadIdx.x * kPer + i;
+    sOut[e + (e >> 5)] = max(cin, vv[i]);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n_out; e += kThreads) ab[k0 + e] = sOut[e + (e >> 5)];
 }
 
 // anc_k = #{j : c_j <= k}, clipped to P_in - 1, from the precomputed partition.
@@ -1406,7 +1492,8 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
   SearchWs tmp;
   // regions that depend on P_out (the partition) go last, so the offsets of
   // the others are the same for every P_out (the sharded phases rely on it)
-  tmp.sums = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * tiles));
+  // sums: tile sums, or the sorted multinomial's (P + 1)-spacing block sums (tiles + 1 per filter)
+  tmp.sums = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * (tiles + 1)));
   tmp.totals = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 3 * static_cast<size_t>(B)));  // + long-run counts
   // cnt doubles as the long-run list of the direct ancestor writer (int4 per run, P_in/32 + 2 per filter)
   const size_t cnt_bytes = sizeof(int32_t) * static_cast<size_t>(B) * P_in;
@@ -1641,22 +1728,14 @@ extern "C" int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const
     if (u || !keys) return SSM_ERR_INVALID_ARG;  // device draws only
     int st = ssm_weights_scan(B, P, dtype, a, 1, shift, fs, w.C, nullptr, w.scan, stream);
     if (st != SSM_OK) return st;
-    // counts in w.cnt; block sums in w.sums; long-run list in w.C (free after the search)
-    uint32_t* long_count = reinterpret_cast<uint32_t*>(w.totals) + 2 * static_cast<size_t>(B);
-    cudaError_t e = cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * static_cast<size_t>(B) * P, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(long_count, 0, sizeof(uint32_t) * B, s);
-    if (e != cudaSuccess) {
-      ssm_set_last_error(e);
-      return SSM_ERR_CUDA;
-    }
-    search_count_kernel<1><<<dim3(grid_for(P, kThreads, 65535), B), kThreads, 0, s>>>(P, w.C, keys, step, fs, w.cnt);
-    count_blocks_kernel<<<dim3(tiles, B), kThreads, 0, s>>>(P, w.cnt, fs, w.sums);
-    blk_prefix_kernel<<<B, 1024, 0, s>>>(tiles, w.sums, w.totals, fs);
-    int4* long_runs = reinterpret_cast<int4*>(w.C);
-    expand_counts_kernel<<<dim3(tiles, B), kThreads, 0, s>>>(P, w.cnt, w.sums, fs, anc, long_runs, long_count);
-    const int gx = std::max(1, std::min(1184 / B, P / kRunChunk + 1));
-    long_runs_kernel<<<dim3(gx, B), kThreads, 0, s>>>(P, P, long_runs, long_count, fs, anc);
-  } else if (scheme == SSM_SYSTEMATIC || scheme == SSM_STRATIFIED) {
+    // spacing block sums over P + 1 outputs in w.sums (as doubles), total in w.totals
+    const int nsb = (P + 1 + kScanTile - 1) / kScanTile;
+    double* blkE = reinterpret_cast<double*>(w.sums);
+    double* totE = reinterpret_cast<double*>(w.totals);
+    spacing_sums_kernel<<<dim3(nsb, B), kThreads, 0, s>>>(P, keys, step, fs, blkE);
+    spacing_prefix_kernel<<<B, 1024, 0, s>>>(nsb, blkE, totE, fs);
+    spacing_merge_kernel<1><<<dim3(tiles, B), kThreads, 0, s>>>(P, w.C, keys, step, blkE, totE, fs, anc);
+    } else if (scheme == SSM_SYSTEMATIC || scheme == SSM_STRATIFIED) {
     if (dtype == SSM_F64) {
       tile_sums_kernel<double><<<dim3(tiles, B), kThreads, 0, s>>>(P, static_cast<const double*>(a), shift, fs, w.sums);
       tile_prefix_kernel<<<B, 1024, 0, s>>>(tiles, w.sums, w.totals, fs);

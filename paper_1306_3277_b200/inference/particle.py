@@ -399,10 +399,10 @@ def init_runs(runs, rngs):
 
 
 # kernels per resample: tiles = tile scale, block prefix, offspring, long runs;
-# logw multinomial = scan, search; sorted multinomial = scan, search-count,
-# block counts, block prefix, expand, long runs; logw systematic/stratified =
-# tile sums, tile prefix, offspring, expand
-_RS_LAUNCHES = {("tiles", 0): 4, ("logw", 0): 2, ("logw", 1): 4, ("logw", 2): 4, ("logw", 3): 6}
+# logw multinomial = scan, search; sorted multinomial = scan, spacing sums,
+# spacing prefix, merge; logw systematic/stratified = tile sums, tile prefix,
+# offspring, expand
+_RS_LAUNCHES = {("tiles", 0): 4, ("logw", 0): 2, ("logw", 1): 4, ("logw", 2): 4, ("logw", 3): 4}
 
 
 def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe, x_arena, a_arena,
@@ -533,7 +533,9 @@ def advance_runs(runs, upto, rngs):
         keys_t = torch.from_numpy(keys.view(np.int32)).to(dev)
     scheme = _lib.SCHEME_IDS[r0.resampler]
     if scheme == 0 and not host_noise:
-        scheme = _lib.SSM_MULTINOMIAL_SORTED  # same draw, ancestors in ascending slot order
+        # device multinomial as sorted order statistics (exponential spacings):
+        # the same law, ancestors ascending so the next gather streams
+        scheme = _lib.SSM_MULTINOMIAL_SORTED
     pw_ws = torch.empty(L.ssm_pw_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     rs_ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     # systematic / stratified resample from the pw kernel's tile-local CDF (no second pass over logw)

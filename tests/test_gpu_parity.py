@@ -543,27 +543,54 @@ def test_tile_records_match_documented_format(P):
         assert tiles["Q"][w] == tiles["cdf"][32 * w + aw.size - 1]
 
 
-@pytest.mark.parametrize("P", [1000, 5000, 1 << 16])
+def _philox4x32_10(ctr, k0, k1):
+    """numpy restatement of the device Philox4x32-10 (ssm_common.cuh) for test oracles."""
+    M0, M1, W0, W1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57), 0x9E3779B9, 0xBB67AE85
+    c = [np.asarray(x, dtype=np.uint64) & np.uint64(0xFFFFFFFF) for x in ctr]
+    k0, k1 = int(k0), int(k1)
+    for _ in range(10):
+        p0, p1 = M0 * c[0], M1 * c[2]
+        lo0, hi0 = p0 & np.uint64(0xFFFFFFFF), p0 >> np.uint64(32)
+        lo1, hi1 = p1 & np.uint64(0xFFFFFFFF), p1 >> np.uint64(32)
+        c = [hi1 ^ c[1] ^ np.uint64(k0), lo1, hi0 ^ c[3] ^ np.uint64(k1), lo0]
+        k0, k1 = (k0 + W0) & 0xFFFFFFFF, (k1 + W1) & 0xFFFFFFFF
+    return c
+
+
+@pytest.mark.parametrize("P", [1000, 2048, 5000, 1 << 16])
 @pytest.mark.parametrize("pattern", ["lognormal", "one", "few"])
-def test_sorted_multinomial_is_sorted_reference_draw(P, pattern):
-    """SSM_MULTINOMIAL_SORTED (device-noise filter path) returns exactly the
-    ancestors of the plain multinomial search for the same device draws, in
-    ascending order (B = 2 filters, ragged P, degenerate weights -> long runs)."""
+def test_sorted_multinomial_matches_spacings_oracle(P, pattern):
+    """SSM_MULTINOMIAL_SORTED (device-noise filter path): U_(k) = S_k / S_{P+1}
+    from the device's exponential spacings, ancestors = searchsorted(cum, U, 'right')
+    -- restated in numpy from the same Philox words (B = 2 filters, ragged P,
+    degenerate weights); ancestors ascending."""
+    from scipy.special import logsumexp
+
     from paper_1306_3277_b200 import _lib
 
     L = _lib.lib()
     pats = _heavy_patterns(P)
     a_np = np.stack([pats[pattern], pats["lognormal"]])
-    from scipy.special import logsumexp
-
     a = torch.from_numpy(a_np).cuda()
     shift = torch.from_numpy(logsumexp(a_np, axis=1)).cuda()
-    keys = torch.tensor([[11, 22], [33, 44]], dtype=torch.int32, device="cuda")
+    keys_np = np.array([[11, 22], [33, 44]], dtype=np.uint32)
+    keys = torch.from_numpy(keys_np.view(np.int32)).cuda()
     ws = torch.empty(L.ssm_resample_workspace_bytes(2, P), dtype=torch.uint8, device="cuda")
-    out = {}
-    for scheme in (0, _lib.SSM_MULTINOMIAL_SORTED):
-        anc = torch.full((2, P), -1, dtype=torch.int32, device="cuda")
-        _lib.check(L.ssm_resample_from_logw(2, P, 1, scheme, _lib.ptr(a), _lib.ptr(shift), None, None,
-                                            _lib.ptr(keys), 5, _lib.ptr(anc), _lib.ptr(ws), _lib.stream_ptr()))
-        out[scheme] = anc.cpu().numpy()
-    np.testing.assert_array_equal(out[_lib.SSM_MULTINOMIAL_SORTED], np.sort(out[0], axis=1))
+    anc = torch.full((2, P), -1, dtype=torch.int32, device="cuda")
+    step = 5
+    _lib.check(L.ssm_resample_from_logw(2, P, 1, _lib.SSM_MULTINOMIAL_SORTED, _lib.ptr(a), _lib.ptr(shift), None,
+                                        None, _lib.ptr(keys), step, _lib.ptr(anc), _lib.ptr(ws), _lib.stream_ptr()))
+    got = anc.cpu().numpy()
+    k = np.arange(P + 1, dtype=np.uint64)
+    for b in range(2):
+        r = _philox4x32_10([k, np.full(P + 1, step), np.zeros(P + 1), np.full(P + 1, 5)], *keys_np[b])
+        u = ((r[0] << np.uint64(32)) | r[1]) >> np.uint64(11)
+        E = -np.log(1.0 - u.astype(np.float64) * 2.0**-53)
+        S = np.cumsum(E)
+        U = S[:P] / S[P]
+        w = np.exp(a_np[b] - logsumexp(a_np[b]))
+        cum = np.cumsum(w / w.sum())
+        cum[-1] = 1.0
+        ref = np.searchsorted(cum, U, side="right").clip(0, P - 1)
+        assert np.all(np.diff(got[b]) >= 0)
+        np.testing.assert_array_equal(got[b], ref)

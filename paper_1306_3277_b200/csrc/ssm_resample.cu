@@ -5,6 +5,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "ssm_common.cuh"
 
@@ -1022,7 +1023,7 @@ __device__ __forceinline__ double spacing_block_scan(uint32_t k0, uint32_t k1, i
 // block totals of the P + 1 spacings (outputs k = 0..P; k = P is the extra E_{P+1})
 __global__ void __launch_bounds__(kThreads)
 spacing_sums_kernel(int P, const uint32_t* __restrict__ keys, int step, const ssm_filter_state* __restrict__ fs,
-                    double* __restrict__ blk) {
+                    double* __restrict__ blk, double* __restrict__ spc) {
   __shared__ double s_warp[kThreads / 32];
   const int b = blockIdx.y;
   if (fs && !fs[b].resample_now) return;
@@ -1030,6 +1031,11 @@ spacing_sums_kernel(int P, const uint32_t* __restrict__ keys, int step, const ss
   double v[kScanItems];
   const double tot = spacing_block_scan(keys[2 * b], keys[2 * b + 1], step, kbase, min(kScanTile, P + 1 - kbase), v, s_warp);
   if (threadIdx.x == 0) blk[static_cast<size_t>(b) * gridDim.x + blockIdx.x] = tot;
+  // block-local inclusive prefixes for the merge pass (thread-contiguous, 4 x 16-byte stores)
+  double2* dst = reinterpret_cast<double2*>(spc + static_cast<size_t>(b) * gridDim.x * kScanTile + kbase +
+                                            threadIdx.x * kScanItems);
+#pragma unroll
+  for (int i = 0; i < kScanItems / 2; ++i) dst[i] = make_double2(v[2 * i], v[2 * i + 1]);
 }
 
 // exclusive prefix of the block totals in place (fixed order), grand total -> tot[b]
@@ -1067,9 +1073,55 @@ spacing_prefix_kernel(int nblk, double* __restrict__ blk, double* __restrict__ t
   if (threadIdx.x == 0) tot[b] = all;
 }
 
-template <int KIND>
+// CDF accessors for the sorted multinomial: cum_j = C_j / C_tot from an
+// inclusive u64 array (scan of the log-weights) or from the fused kernel's
+// tile records (C_j = tile prefix + round(scale_w * cdf_local_j), as the
+// systematic offspring kernel; the last particle's C is the total: cum = 1)
+struct CumFixedArr {
+  const uint64_t* C;
+  double tot;
+  __device__ __forceinline__ double operator()(int j) const { return static_cast<double>(__ldg(C + j)) / tot; }
+};
+struct CumTileRecs {
+  const uint64_t* cl;
+  const double* sc;
+  const uint64_t* tp;
+  const uint64_t* bp;
+  double tot;
+  __device__ __forceinline__ double operator()(int j) const {
+    const int tw = j >> 5;
+    const uint64_t C = tp[tw] + bp[tw / kRecPerBlock] + __double2ull_rn(sc[tw] * static_cast<double>(__ldg(cl + j)));
+    return static_cast<double>(C) / tot;
+  }
+};
+
+// searchsorted(cum, q, 'right') by one warp: 32 probes per round (5 rounds
+// for 2^24 entries instead of 24 dependent loads); all lanes return the answer
+template <typename Cum>
+__device__ __forceinline__ int warp_search_right(const Cum& cum_at, int P, double q, int lane) {
+  int lo = 0, hi = P;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) / 32;
+    const int p = min(lo + (lane + 1) * step - 1, hi - 1);
+    const unsigned m = __ballot_sync(0xffffffffu, cum_at(p) <= q);
+    const int cnt = __popc(m);  // probes are ascending: the true ones are a prefix
+    const int p_last = __shfl_sync(0xffffffffu, p, cnt > 0 ? cnt - 1 : 0);
+    const int p_next = __shfl_sync(0xffffffffu, p, cnt < 32 ? cnt : 31);
+    if (cnt > 0) lo = p_last + 1;
+    if (cnt < 32) hi = p_next;
+  }
+  const int p = lo + lane;
+  const unsigned m = __ballot_sync(0xffffffffu, p < hi && cum_at(p) <= q);
+  return lo + __popc(m);
+}
+
+// SRC 0: cum = inclusive u64 array `C` ([B][P]); SRC 1: tile records (cdf_local,
+// scale [B][nt], tile prefixes [B][nt] then block prefixes [B][nblk], totals)
+template <int SRC>
 __global__ void __launch_bounds__(kThreads)
-spacing_merge_kernel(int P, const void* __restrict__ cum, const uint32_t* __restrict__ keys, int step,
+spacing_merge_kernel(int P, const uint64_t* __restrict__ C, const uint64_t* __restrict__ cdf_local,
+                     const double* __restrict__ scale, const uint64_t* __restrict__ pref,
+                     const uint64_t* __restrict__ totals, const double* __restrict__ spc,
                      const double* __restrict__ blk, const double* __restrict__ tot,
                      const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc) {
   __shared__ double sU[kScanTile];
@@ -1077,6 +1129,8 @@ spacing_merge_kernel(int P, const void* __restrict__ cum, const uint32_t* __rest
   __shared__ double s_warp[kThreads / 32];
   __shared__ int s_wmax[kThreads / 32];
   __shared__ int s_j[2];
+  __shared__ int s_carry[kThreads / 32];
+  __shared__ int s_prev;
   const int b = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t* ab = anc + static_cast<size_t>(b) * P;
@@ -1085,29 +1139,37 @@ spacing_merge_kernel(int P, const void* __restrict__ cum, const uint32_t* __rest
     for (int k = threadIdx.x; k < n_out; k += kThreads) ab[k0 + k] = k0 + k;
     return;
   }
-  double v[kScanItems];
-  spacing_block_scan(keys[2 * b], keys[2 * b + 1], step, k0, n_out, v, s_warp);
-  const double off = blk[static_cast<size_t>(b) * (gridDim.x + (P % kScanTile == 0 ? 1 : 0)) + blockIdx.x];
+  const int nsb = gridDim.x + (P % kScanTile == 0 ? 1 : 0);  // spacing blocks cover P + 1 outputs
+  const double off = blk[static_cast<size_t>(b) * nsb + blockIdx.x];
   const double inv = 1.0 / tot[b];
+  const double2* src = reinterpret_cast<const double2*>(spc + static_cast<size_t>(b) * nsb * kScanTile + k0 +
+                                                        threadIdx.x * kScanItems);
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) sU[threadIdx.x * kScanItems + i] = (off + v[i]) * inv;  // U_(k0+k)
+  for (int i = 0; i < kScanItems / 2; ++i) {  // U_(k0+k) = (S_{k0} + local inclusive sum) / S_{P+1}
+    const double2 t = src[i];
+    sU[threadIdx.x * kScanItems + 2 * i] = (off + t.x) * inv;
+    sU[threadIdx.x * kScanItems + 2 * i + 1] = (off + t.y) * inv;
+  }
+  (void)s_warp;
   for (int e = threadIdx.x; e < (kScanTile + kScanTile / 32) / 4; e += kThreads)
     reinterpret_cast<int4*>(sOut)[e] = make_int4(-1, -1, -1, -1);
   const size_t coff = static_cast<size_t>(b) * P;
-  const double ctot = cum_total<KIND>(cum, coff, P);
+  using Cum = typename std::conditional<SRC == 0, CumFixedArr, CumTileRecs>::type;
+  Cum cum_at;
+  if constexpr (SRC == 0) {
+    cum_at = CumFixedArr{C + coff, static_cast<double>(C[coff + P - 1])};
+  } else {
+    const int nt = (P + 31) >> 5;
+    const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
+    cum_at = CumTileRecs{cdf_local + coff, scale + static_cast<size_t>(b) * nt, pref + static_cast<size_t>(b) * nt,
+                         pref + B_total_tiles_offset(nt, gridDim.y) + static_cast<size_t>(b) * nblk,
+                         static_cast<double>(totals[b])};
+  }
   __syncthreads();
   // first / last ancestor: searchsorted(cum, U, 'right'), clipped
-  if (threadIdx.x < 2) {
-    const double q = sU[threadIdx.x == 0 ? 0 : n_out - 1];
-    int lo = 0, hi = P;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (cum_at<KIND>(cum, coff, ctot, mid) <= q)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    s_j[threadIdx.x] = lo < P ? lo : P - 1;
+  if (warp < 2) {  // warp 0: first output, warp 1: last output
+    const int j = warp_search_right(cum_at, P, sU[warp == 0 ? 0 : n_out - 1], lane);
+    if (lane == 0) s_j[warp] = j < P ? j : P - 1;
   }
   __syncthreads();
   const int jlo = s_j[0], jhi = s_j[1];
@@ -1115,7 +1177,7 @@ spacing_merge_kernel(int P, const void* __restrict__ cum, const uint32_t* __rest
   auto cnt_lt = [&](int j) -> int {
     if (j < jlo) return 0;
     if (j >= P - 1 || j >= jhi) return n_out;
-    const double c = cum_at<KIND>(cum, coff, ctot, j);
+    const double c = cum_at(j);
     int lo = 0, hi = n_out;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -1126,9 +1188,16 @@ spacing_merge_kernel(int P, const void* __restrict__ cum, const uint32_t* __rest
     }
     return lo;
   };
-  for (int j = jlo + threadIdx.x; j <= jhi; j += kThreads) {
-    const int a = cnt_lt(j - 1), c = cnt_lt(j);
-    if (c > a) sOut[a + (a >> 5)] = j;
+  for (int j0 = jlo; j0 <= jhi; j0 += kThreads) {  // chunks of 256 particles
+    const int j = j0 + threadIdx.x;
+    const int c = j <= jhi ? cnt_lt(j) : n_out;
+    const int up = __shfl_up_sync(0xffffffffu, c, 1);
+    if (lane == 31) s_carry[warp] = c;
+    __syncthreads();
+    const int a = lane > 0 ? up : (warp > 0 ? s_carry[warp - 1] : (j0 == jlo ? cnt_lt(jlo - 1) : s_prev));
+    if (j <= jhi && c > a) sOut[a + (a >> 5)] = j;
+    __syncthreads();
+    if (threadIdx.x == kThreads - 1) s_prev = c;
   }
   __syncthreads();
   // inclusive max-scan of the marks (all outputs have an owner: position 0 is jlo's)
@@ -1477,6 +1546,7 @@ struct SearchWs {
   int32_t* split;
   void* scan;
   uint64_t* C;
+  double* spc;  // sorted multinomial: block-local inclusive spacing sums, [B][nsb * 2048]
 };
 
 static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, SearchWs* w) {
@@ -1504,6 +1574,8 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
   const size_t tile_words = 2 * nt + (nt + kRecPerBlock - 1) / kRecPerBlock;
   const size_t c_words = static_cast<size_t>(P_in) > tile_words ? static_cast<size_t>(P_in) : tile_words;
   tmp.C = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * c_words));
+  tmp.spc = reinterpret_cast<double*>(
+      take(sizeof(double) * static_cast<size_t>(B) * ((P_in + 1 + kScanTile - 1) / kScanTile) * kScanTile));
   tmp.scan = take(scan_ws_bytes(B, P_in));
   tmp.split = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * (nd + 1)));
   if (w) *w = tmp;
@@ -1571,7 +1643,9 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
   if (B <= 0 || B > 65535 || P <= 0 || !cdf_local || !tile_rec || !fs || !anc || !workspace)
     return SSM_ERR_INVALID_ARG;
   if (!u && !keys) return SSM_ERR_INVALID_ARG;
-  if (scheme != SSM_SYSTEMATIC && scheme != SSM_STRATIFIED) return SSM_ERR_INVALID_ARG;
+  if (scheme != SSM_SYSTEMATIC && scheme != SSM_STRATIFIED && scheme != SSM_MULTINOMIAL_SORTED)
+    return SSM_ERR_INVALID_ARG;
+  if (scheme == SSM_MULTINOMIAL_SORTED && (u || !keys)) return SSM_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SearchWs w;
   search_ws_layout(B, P, P, workspace, &w);
@@ -1590,6 +1664,17 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
              scale, pref, blk, long_count);
   launch_pdl(blk_prefix_kernel, dim3(B), dim3(1024), s, nblk, blk, w.totals, fs);
   const dim3 g(scan_tiles(P), B);
+  if (scheme == SSM_MULTINOMIAL_SORTED) {  // spacing sums in w.sums (doubles), totals after the u64 totals
+    const int nsb = (P + 1 + kScanTile - 1) / kScanTile;
+    double* blkE = reinterpret_cast<double*>(w.sums);
+    double* totE = reinterpret_cast<double*>(w.totals) + 2 * static_cast<size_t>(B);  // free slots
+    spacing_sums_kernel<<<dim3(nsb, B), kThreads, 0, s>>>(P, keys, step, fs, blkE, w.spc);
+    spacing_prefix_kernel<<<B, 1024, 0, s>>>(nsb, blkE, totE, fs);
+    spacing_merge_kernel<1><<<g, kThreads, 0, s>>>(P, nullptr, static_cast<const uint64_t*>(cdf_local), scale, pref,
+                                                   w.totals, w.spc, blkE, totE, fs, anc);
+    SSM_CHECK_LAUNCH();
+    return SSM_OK;
+  }
   const uint64_t* cl = static_cast<const uint64_t*>(cdf_local);
   if (scheme == SSM_SYSTEMATIC)
     launch_pdl(offspring_tiles_kernel<SSM_SYSTEMATIC>, g, dim3(kThreads), s, P, cl, scale, pref, w.totals, u, keys,
@@ -1732,9 +1817,10 @@ extern "C" int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const
     const int nsb = (P + 1 + kScanTile - 1) / kScanTile;
     double* blkE = reinterpret_cast<double*>(w.sums);
     double* totE = reinterpret_cast<double*>(w.totals);
-    spacing_sums_kernel<<<dim3(nsb, B), kThreads, 0, s>>>(P, keys, step, fs, blkE);
+    spacing_sums_kernel<<<dim3(nsb, B), kThreads, 0, s>>>(P, keys, step, fs, blkE, w.spc);
     spacing_prefix_kernel<<<B, 1024, 0, s>>>(nsb, blkE, totE, fs);
-    spacing_merge_kernel<1><<<dim3(tiles, B), kThreads, 0, s>>>(P, w.C, keys, step, blkE, totE, fs, anc);
+    spacing_merge_kernel<0><<<dim3(tiles, B), kThreads, 0, s>>>(P, w.C, nullptr, nullptr, nullptr, nullptr, w.spc,
+                                                                blkE, totE, fs, anc);
     } else if (scheme == SSM_SYSTEMATIC || scheme == SSM_STRATIFIED) {
     if (dtype == SSM_F64) {
       tile_sums_kernel<double><<<dim3(tiles, B), kThreads, 0, s>>>(P, static_cast<const double*>(a), shift, fs, w.sums);

@@ -398,11 +398,13 @@ def init_runs(runs, rngs):
     return runs
 
 
-# kernels per resample: tiles = tile scale, block prefix, offspring, long runs;
-# logw multinomial = scan, search; sorted multinomial = scan, spacing sums,
-# spacing prefix, merge; logw systematic/stratified = tile sums, tile prefix,
-# offspring, expand
-_RS_LAUNCHES = {("tiles", 0): 4, ("logw", 0): 2, ("logw", 1): 4, ("logw", 2): 4, ("logw", 3): 4}
+# kernels per resample: tiles = tile scale, block prefix, offspring, long runs
+# (sorted multinomial: tile scale, block prefix, spacing sums, spacing prefix,
+# merge); logw multinomial = scan, search; logw sorted multinomial = scan,
+# spacing sums, spacing prefix, merge; logw systematic/stratified = tile sums,
+# tile prefix, offspring, expand
+_RS_LAUNCHES = {("tiles", 1): 4, ("tiles", 2): 4, ("tiles", 3): 5,
+                ("logw", 0): 2, ("logw", 1): 4, ("logw", 2): 4, ("logw", 3): 4}
 
 
 def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe, x_arena, a_arena,
@@ -444,7 +446,7 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
         A.events = C.cast(ev_arr, C.c_void_p)
     _lib.check(L.ssm_advance(A, stream), "ssm_advance")
     kind = "tiles" if tiles_ok else "logw"
-    rs_n = _RS_LAUNCHES[(kind, 0 if tiles_ok else scheme)]
+    rs_n = _RS_LAUNCHES[(kind, scheme)]
     profiling.count_launch(n + rs_n * int(anc_used.sum()))
     for k in range(n):
         an = anc_arena[k] if anc_used[k] else None
@@ -540,8 +542,8 @@ def advance_runs(runs, upto, rngs):
     rs_ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     # systematic / stratified resample from the pw kernel's tile-local CDF (no second pass over logw)
     small = (not host_noise and P <= _small_max() and not _NO_SMALL)
-    # systematic / stratified resample from the pw kernel's tile CDF (multi-kernel path only)
-    tiles_ok = r0.resampler in ("systematic", "stratified") and not small
+    # resample from the pw kernel's tile CDF (multi-kernel path; multinomial with device draws only)
+    tiles_ok = (r0.resampler in ("systematic", "stratified") or scheme == _lib.SSM_MULTINOMIAL_SORTED) and not small
     ntile = (P + 31) // 32  # one tile record per warp tile
     cdf_local = tile_rec = None
     if tiles_ok:

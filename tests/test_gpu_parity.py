@@ -594,3 +594,30 @@ def test_sorted_multinomial_matches_spacings_oracle(P, pattern):
         ref = np.searchsorted(cum, U, side="right").clip(0, P - 1)
         assert np.all(np.diff(got[b]) >= 0)
         np.testing.assert_array_equal(got[b], ref)
+
+
+@pytest.mark.parametrize("P", [1000, 1 << 16])
+@pytest.mark.parametrize("pattern", ["lognormal", "few"])
+def test_sorted_multinomial_from_tiles_matches_logw(P, pattern):
+    """The filter path's sorted multinomial from the fused kernel's tile records
+    equals the one from the log-weight scan (same spacings, same CDF up to the
+    fixed-point rounding)."""
+    from scipy.special import logsumexp
+
+    from paper_1306_3277_b200 import _lib
+
+    L = _lib.lib()
+    a_np = _heavy_patterns(P)[pattern]
+    cdf, rec, fs, _ = _tile_inputs(a_np)
+    keys = torch.tensor([[77, 88]], dtype=torch.int32, device="cuda")
+    ws = torch.empty(L.ssm_resample_workspace_bytes(1, P), dtype=torch.uint8, device="cuda")
+    anc_t = torch.full((P,), -1, dtype=torch.int32, device="cuda")
+    _lib.check(L.ssm_resample_from_tiles(1, P, _lib.SSM_MULTINOMIAL_SORTED, _lib.ptr(cdf), _lib.ptr(rec),
+                                         _lib.ptr(fs), None, _lib.ptr(keys), 3, _lib.ptr(anc_t), _lib.ptr(ws),
+                                         _lib.stream_ptr()))
+    a = torch.from_numpy(a_np).cuda()
+    shift = torch.tensor([logsumexp(a_np)], dtype=torch.float64, device="cuda")
+    anc_l = torch.full((P,), -1, dtype=torch.int32, device="cuda")
+    _lib.check(L.ssm_resample_from_logw(1, P, 1, _lib.SSM_MULTINOMIAL_SORTED, _lib.ptr(a), _lib.ptr(shift), None,
+                                        None, _lib.ptr(keys), 3, _lib.ptr(anc_l), _lib.ptr(ws), _lib.stream_ptr()))
+    np.testing.assert_array_equal(anc_t.cpu().numpy(), anc_l.cpu().numpy())

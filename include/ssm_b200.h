@@ -330,6 +330,12 @@ int ssm_gather_cols(int dtype, int nx, int n_out, int in_stride, const void* x_i
  * ([nx][P] SoA), ancs[b*(S+1) + i] at the ancestors of step i (NULL =
  * identity; index 0 unused).  j_final[b] is the drawn final particle.
  * out: [B][S+1][nx] float64. */
+/* sample_trajectory's final-weight pick (particle.py:140-141) from the tile
+ * records of the last weighted ssm_propagate_weight: j_out[b] =
+ * searchsorted(cum_b, u[b], 'right') clipped, cum from the exact fixed-point
+ * CDF (same as ssm_resample_from_tiles); workspace = ssm_resample_workspace_bytes. */
+int ssm_pick_from_tiles(int B, int P, const void* cdf_local, const void* tile_rec, const ssm_filter_state* fs,
+                        const double* u, int32_t* j_out, void* workspace, void* stream);
 int ssm_trace(int dtype, int B, int S, int nx, int P, const void* const* xs,
               const int32_t* const* ancs, const int32_t* j_final, double* out, void* stream);
 

@@ -183,6 +183,7 @@ SIGNATURES = {
     "ssm_gather": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "ssm_gather_cols": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "ssm_trace": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "ssm_pick_from_tiles": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ssm_lse_workspace_bytes": (_sz, [_i, _i]),
     "ssm_logsumexp": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_block_gather": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
@@ -211,6 +212,7 @@ LAUNCHING = {
     "ssm_gather": 1,
     "ssm_gather_cols": 1,
     "ssm_trace": 1,
+    "ssm_pick_from_tiles": 3,
     "ssm_logsumexp": 1,
     "ssm_block_gather": 1,
     "ssm_advance": 0,

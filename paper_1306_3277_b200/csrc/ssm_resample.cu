@@ -426,11 +426,11 @@ constexpr int kRecPerBlock = kThreads;  // 256 tile records per block (one per t
 __global__ void __launch_bounds__(kThreads)
 tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_filter_state* __restrict__ fs,
                   double* __restrict__ scale, uint64_t* __restrict__ prel, uint64_t* __restrict__ blk_tot,
-                  uint32_t* __restrict__ long_count = nullptr) {
+                  uint32_t* __restrict__ long_count = nullptr, int gate = 1) {
   pdl_wait();
   __shared__ uint64_t warp_tot[kThreads / 32];
   const int b = blockIdx.y, blk = blockIdx.x;
-  if (!fs[b].resample_now) return;
+  if (gate && !fs[b].resample_now) return;
   if (long_count && blk == 0 && threadIdx.x == 0) long_count[b] = 0u;  // long-run list of this resample
   const double incr = fs[b].incr;
   const int e = blk * kRecPerBlock + threadIdx.x;
@@ -1661,7 +1661,7 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
   uint32_t* long_count = reinterpret_cast<uint32_t*>(w.totals) + 2 * static_cast<size_t>(B);  // after totals
   int4* long_runs = reinterpret_cast<int4*>(w.cnt);
   launch_pdl(tile_scale_kernel, dim3(nblk, B), dim3(kThreads), s, nt, static_cast<const ssm_tile_rec*>(tile_rec), fs,
-             scale, pref, blk, long_count);
+             scale, pref, blk, long_count, 1);
   launch_pdl(blk_prefix_kernel, dim3(B), dim3(1024), s, nblk, blk, w.totals, fs);
   const dim3 g(scan_tiles(P), B);
   if (scheme == SSM_MULTINOMIAL_SORTED) {  // spacing sums in w.sums (doubles), totals after the u64 totals
@@ -1865,6 +1865,45 @@ extern "C" int ssm_gather_cols(int dtype, int nx, int n_out, int in_stride, cons
     gather_cols_kernel<float><<<g, kThreads, 0, s>>>(nx, n_out, in_stride, (const float*)x_in, idx, (float*)x_out);
   else
     return SSM_ERR_INVALID_ARG;
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+// Trajectory pick (sample_trajectory's one multinomial draw, particle.py:140-141)
+// from the fused kernel's tile records: one warp per filter searches the
+// global fixed-point CDF for u_b (no full scan of the weights).
+__global__ void __launch_bounds__(32)
+pick_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const double* __restrict__ scale,
+                  const uint64_t* __restrict__ pref, const uint64_t* __restrict__ totals,
+                  const double* __restrict__ u, int32_t* __restrict__ j_out) {
+  const int b = blockIdx.x;
+  const int nt = (P + 31) >> 5;
+  const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
+  const CumTileRecs cum{cdf_local + static_cast<size_t>(b) * P, scale + static_cast<size_t>(b) * nt,
+                        pref + static_cast<size_t>(b) * nt,
+                        pref + B_total_tiles_offset(nt, gridDim.x) + static_cast<size_t>(b) * nblk,
+                        static_cast<double>(totals[b])};
+  const int j = warp_search_right(cum, P, u[b], threadIdx.x);
+  if (threadIdx.x == 0) j_out[b] = j < P ? j : P - 1;
+}
+
+extern "C" int ssm_pick_from_tiles(int B, int P, const void* cdf_local, const void* tile_rec,
+                                   const ssm_filter_state* fs, const double* u, int32_t* j_out, void* workspace,
+                                   void* stream) {
+  if (B <= 0 || B > 65535 || P <= 0 || !cdf_local || !tile_rec || !fs || !u || !j_out || !workspace)
+    return SSM_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SearchWs w;
+  search_ws_layout(B, P, P, workspace, &w);
+  const int nt = (P + 31) / 32;
+  const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
+  double* scale = reinterpret_cast<double*>(w.C);
+  uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + static_cast<size_t>(B) * nt;
+  uint64_t* blk = pref + B_total_tiles_offset(nt, B);
+  tile_scale_kernel<<<dim3(nblk, B), kThreads, 0, s>>>(nt, static_cast<const ssm_tile_rec*>(tile_rec), fs, scale,
+                                                      pref, blk, nullptr, 0);
+  blk_prefix_kernel<<<B, 1024, 0, s>>>(nblk, blk, w.totals, nullptr);
+  pick_tiles_kernel<<<B, 32, 0, s>>>(P, static_cast<const uint64_t*>(cdf_local), scale, pref, w.totals, u, j_out);
   SSM_CHECK_LAUNCH();
   return SSM_OK;
 }

@@ -721,6 +721,17 @@ def sample_trajectories(runs, rngs):
     dev = r0.device
     S = r0.pos
     stream = _lib.stream_ptr()
+    if all(not r.weights_uniform and r._cdf is not None and r._trec is not None for r in runs):
+        # final weights carry the fused kernel's tile records: one warp search per filter
+        u = torch.from_numpy(first_uniforms(rngs, 1)[:, 0].copy()).to(dev)
+        j = torch.empty((B, 1), dtype=torch.int32, device=dev)
+        ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
+        cdf = _stack_rows([r._cdf for r in runs]).contiguous()
+        trec = _stack_rows([r._trec for r in runs]).contiguous()
+        fs_rows = _stack_rows([r._fs for r in runs]).contiguous()
+        _lib.check(L.ssm_pick_from_tiles(B, P, _lib.ptr(cdf), _lib.ptr(trec), _lib.ptr(fs_rows), _lib.ptr(u),
+                                         _lib.ptr(j), _lib.ptr(ws), stream), "ssm_pick_from_tiles")
+        return _trace_runs(L, runs, j, S, B, P, nx, dev, stream)
     # final log-weights (uniform -> zeros with shift 0)
     a_rows, shifts = [], []
     for r in runs:
@@ -746,6 +757,12 @@ def sample_trajectories(runs, rngs):
     j = torch.empty((B, 1), dtype=torch.int32, device=dev)
     _lib.check(L.ssm_resample_search(B, P, 1, _lib.SCHEME_IDS["multinomial"], 1, _lib.ptr(cum), _lib.ptr(u),
                                      None, 0, None, _lib.ptr(j), None, stream), "ssm_resample_search")
+    return _trace_runs(L, runs, j, S, B, P, nx, dev, stream)
+
+
+def _trace_runs(L, runs, j, S, B, P, nx, dev, stream):
+    """Ancestry walk from the picked final particles j (device) -> trajectories."""
+    r0 = runs[0]
     for r in runs:
         if len(r._hx) != S + 1 or len(r._hist) != S + 1:
             raise ValueError("history length does not match the run position")

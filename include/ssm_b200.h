@@ -251,9 +251,10 @@ typedef struct ssm_advance_args {
   int32_t tiles;             /* 1: resample from the fused kernel's tile CDF (systematic/stratified) */
   int32_t maybe_nonuniform;  /* in: before the first step; out: after the last */
   int32_t ess_gate;          /* ess_rel >= 0 */
-  int32_t pad;
+  int32_t x_ring;            /* 0: x_arena has n_steps slots (history kept); r > 0: step k writes
+                                slot k % r (history-free runs: positions are replayed on demand) */
   const void* x_in;          /* [B][nx][P] */
-  void* x_arena;             /* [n_steps][B][nx][P] positions written per step */
+  void* x_arena;             /* [n_steps or x_ring][B][nx][P] positions written per step */
   int32_t* anc_arena;        /* [n_steps][B][P]; slot k valid iff anc_used[k] */
   const void* a_prev;        /* unnormalised log-weights of the last weighted step, or NULL */
   void* a_arena;             /* [n_weighted][B][P] */
@@ -334,6 +335,28 @@ int ssm_gather_cols(int dtype, int nx, int n_out, int in_stride, const void* x_i
  * records of the last weighted ssm_propagate_weight: j_out[b] =
  * searchsorted(cum_b, u[b], 'right') clipped, cum from the exact fixed-point
  * CDF (same as ssm_resample_from_tiles); workspace = ssm_resample_workspace_bytes. */
+/* Trajectory of history-free runs (device noise).  With counter-based noise a
+ * particle's state at grid step i is a function of its ancestor's state at
+ * i - 1, its slot j_i and step i only, so sample_trajectory's output
+ * (particle.py:137-149) is recomputed along the chosen ancestry: walk j_S ->
+ * j_0 through the stored ancestors, regenerate x_0[j_0] (ssm_init_particles'
+ * draw or the fixed initial state), then apply each grid step's transition
+ * with slot j_i's draws -- the fused kernel's own transition code, so the
+ * result is bitwise the stored-history trajectory.  One thread per filter. */
+typedef struct ssm_replay_args {
+  int32_t model, dtype, B, P, S, exact;
+  const double* theta;            /* [B][4] derived parameters (as ssm_pw_args.theta) */
+  const ssm_substep* subs;        /* device sub-step table */
+  const ssm_step_desc* steps;     /* device [S + 1]; entry i describes grid step i (i >= 1) */
+  const uint32_t* keys;           /* device [B][S + 1][2]: Philox key of grid step i; entry 0 = init key */
+  const double* x0;               /* device [B][nx]: fixed initial state rows (used where x0_flag[b]) */
+  const int32_t* x0_flag;         /* device [B] or NULL: 1 = start from x0[b], 0 = init draw */
+  const int32_t* const* ancs;     /* device [B][S + 1] ancestor rows of each step (NULL: identity) */
+  const int32_t* j_final;         /* device [B]: picked final particle */
+  double* out;                    /* device [B][S + 1][nx] */
+} ssm_replay_args;
+int ssm_replay_path(const ssm_replay_args* args, void* stream);
+
 int ssm_pick_from_tiles(int B, int P, const void* cdf_local, const void* tile_rec, const ssm_filter_state* fs,
                         const double* u, int32_t* j_out, void* workspace, void* stream);
 int ssm_trace(int dtype, int B, int S, int nx, int P, const void* const* xs,

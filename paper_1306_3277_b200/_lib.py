@@ -138,7 +138,7 @@ class AdvanceArgs(C.Structure):
         ("tiles", C.c_int32),
         ("maybe_nonuniform", C.c_int32),
         ("ess_gate", C.c_int32),
-        ("pad", C.c_int32),
+        ("x_ring", C.c_int32),
         ("x_in", C.c_void_p),
         ("x_arena", C.c_void_p),
         ("anc_arena", C.c_void_p),
@@ -152,6 +152,11 @@ class AdvanceArgs(C.Structure):
         ("pad2", C.c_int32),
         ("events", C.c_void_p),
     ]
+
+
+class ReplayArgs(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("model", "dtype", "B", "P", "S", "exact")] + [
+        (n, C.c_void_p) for n in ("theta", "subs", "steps", "keys", "x0", "x0_flag", "ancs", "j_final", "out")]
 
 
 class SmallArgs(C.Structure):
@@ -184,6 +189,7 @@ SIGNATURES = {
     "ssm_gather_cols": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "ssm_trace": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_pick_from_tiles": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "ssm_replay_path": (_i, [C.POINTER(ReplayArgs), _vp]),
     "ssm_lse_workspace_bytes": (_sz, [_i, _i]),
     "ssm_logsumexp": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_block_gather": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
@@ -213,6 +219,7 @@ LAUNCHING = {
     "ssm_gather_cols": 1,
     "ssm_trace": 1,
     "ssm_pick_from_tiles": 3,
+    "ssm_replay_path": 1,
     "ssm_logsumexp": 1,
     "ssm_block_gather": 1,
     "ssm_advance": 0,

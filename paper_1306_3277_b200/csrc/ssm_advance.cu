@@ -48,7 +48,8 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
     pw.hints = static_cast<uint32_t>(d.hints);
     pw.subs = A->subs_table + d.subs_offset;
     pw.x_in = x_prev;
-    void* x_out = static_cast<char*>(A->x_arena) + static_cast<size_t>(k) * xstep;
+    const int slot_x = A->x_ring > 0 ? k % A->x_ring : k;
+    void* x_out = static_cast<char*>(A->x_arena) + static_cast<size_t>(slot_x) * xstep;
     pw.x_out = x_out;
     pw.anc = anc;
     pw.a_prev = a_last;

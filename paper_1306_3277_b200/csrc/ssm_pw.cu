@@ -156,6 +156,86 @@ __device__ __forceinline__ bool finite_bits(float v) {
   return (__float_as_int(v) & 0x7f800000) != 0x7f800000;
 }
 
+// One particle through one grid step (particle.py:110-111 / simulate.py:132-163):
+// the sub-steps of noise + RK4 / windkessel update, in place on x.  Shared by
+// the fused kernel and the trajectory replay, so both produce the same bits.
+// SIMPLE (fast L96, one sub-step, one RK4 step) uses the hoisted constants
+// s_F = F, s_c = sqrt(sigma2) / h * sqrt(d), s_s = RK4 step length.
+template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE>
+__device__ __forceinline__ void transition_one(T (&x)[MODEL == SSM_MODEL_LORENZ96 ? 8 : 1], const double* th,
+                                               const ssm_substep* subs, int n_sub, const T* noise, int P, int p,
+                                               uint32_t k0, uint32_t k1, uint32_t pglob, uint32_t step, T s_F,
+                                               T s_c, T s_s, bool check_finite, bool& bad, int& bad_sub) {
+  using O = Ar<T, E>;
+  constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
+  if constexpr (SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ) {
+    T z[8];
+    normals8<T>(k0, k1, pglob, step, 0u, z);
+    T Fn[8];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) Fn[n] = fma(s_c, z[n], s_F);  // F + sqrt(sigma2) sd z / h
+    l96_rk4_fast<T>(x, Fn, s_s);
+    if (check_finite && !bad) {
+      bool ok = true;
+#pragma unroll
+      for (int n = 0; n < 8; ++n) ok &= finite_bits(x[n]);
+      if (!ok) bad = true;  // bad_sub stays 0
+    }
+  } else {
+  for (int k = 0; k < n_sub; ++k) {
+    const ssm_substep& S = subs[k];
+    if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+      T W[8];
+      if constexpr (INJ) {
+#pragma unroll
+        for (int n = 0; n < 8; ++n) W[n] = noise[(static_cast<size_t>(k) * 8 + n) * P + p];
+      } else {
+        normals8<T>(k0, k1, pglob, step,
+                    static_cast<uint32_t>(k), W);
+        const T sd = static_cast<T>(S.sd);
+#pragma unroll
+        for (int n = 0; n < 8; ++n) W[n] = sd * W[n];
+      }
+      if constexpr (E) {
+        const T F = static_cast<T>(th[0]);
+        const T sq = static_cast<T>(th[1]);  // np.sqrt(sigma2), host-computed
+        T nt[8];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) nt[n] = O::div(O::mul(sq, W[n]), T(0.05));
+        for (int m = 0; m < S.n_ode; ++m) l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
+      } else {
+        const T F = static_cast<T>(th[0]);
+        const T sqh = static_cast<T>(th[1] * 20.0);  // sqrt(sigma2) / h
+        T Fn[8];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) Fn[n] = fma(sqh, W[n], F);
+        for (int m = 0; m < S.n_ode; ++m) l96_rk4_fast<T>(x, Fn, static_cast<T>(S.s[m]));
+      }
+    } else {
+      // Windkessel.bi:28-29, Pp <- exp(-h/(R*C))*Pp + R*(1 - exp(-h/(R*C)))*(F + xi)
+      const T ca = static_cast<T>(th[0]), cb = static_cast<T>(th[1]);
+      T xi;
+      if constexpr (INJ) {
+        xi = noise[static_cast<size_t>(k) * P + p];
+      } else {
+        xi = static_cast<T>(th[3]) * normal1<T>(k0, k1, pglob,
+                                                step, static_cast<uint32_t>(k));
+      }
+      x[0] = O::add(O::mul(ca, x[0]), O::mul(cb, O::add(static_cast<T>(S.u_in), xi)));
+    }
+    if (check_finite && !bad) {
+      bool ok = true;
+#pragma unroll
+      for (int n = 0; n < NX; ++n) ok &= finite_bits(x[n]);
+      if (!ok) {
+        bad = true;
+        bad_sub = k;
+      }
+    }
+  }
+  }  // general sub-step loop
+}
+
 // ----------------------------- the kernel ----------------------------------
 //
 // Grid-stride over 256-particle block tiles; one particle per thread per tile.
@@ -321,72 +401,9 @@ __global__ void __launch_bounds__(kThreads) pw_kernel(const ssm_pw_args A) {
       anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
     }
     if (act) {
-      if constexpr (SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ) {
-        T z[8];
-        normals8<T>(k0, k1, static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step), 0u, z);
-        T Fn[8];
-#pragma unroll
-        for (int n = 0; n < 8; ++n) Fn[n] = fma(s_c, z[n], s_F);  // F + sqrt(sigma2) sd z / h
-        l96_rk4_fast<T>(x, Fn, s_s);
-        if (A.check_finite && !bad) {
-          bool ok = true;
-#pragma unroll
-          for (int n = 0; n < 8; ++n) ok &= finite_bits(x[n]);
-          if (!ok) bad = true;  // bad_sub stays 0
-        }
-      } else {
-      for (int k = 0; k < A.n_sub; ++k) {
-        const ssm_substep& S = A.subs[k];
-        if constexpr (MODEL == SSM_MODEL_LORENZ96) {
-          T W[8];
-          if constexpr (INJ) {
-#pragma unroll
-            for (int n = 0; n < 8; ++n) W[n] = noise[(static_cast<size_t>(k) * 8 + n) * P + p];
-          } else {
-            normals8<T>(k0, k1, static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
-                        static_cast<uint32_t>(k), W);
-            const T sd = static_cast<T>(S.sd);
-#pragma unroll
-            for (int n = 0; n < 8; ++n) W[n] = sd * W[n];
-          }
-          if constexpr (E) {
-            const T F = static_cast<T>(th[0]);
-            const T sq = static_cast<T>(th[1]);  // np.sqrt(sigma2), host-computed
-            T nt[8];
-#pragma unroll
-            for (int n = 0; n < 8; ++n) nt[n] = O::div(O::mul(sq, W[n]), T(0.05));
-            for (int m = 0; m < S.n_ode; ++m) l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
-          } else {
-            const T F = static_cast<T>(th[0]);
-            const T sqh = static_cast<T>(th[1] * 20.0);  // sqrt(sigma2) / h
-            T Fn[8];
-#pragma unroll
-            for (int n = 0; n < 8; ++n) Fn[n] = fma(sqh, W[n], F);
-            for (int m = 0; m < S.n_ode; ++m) l96_rk4_fast<T>(x, Fn, static_cast<T>(S.s[m]));
-          }
-        } else {
-          // Windkessel.bi:28-29, Pp <- exp(-h/(R*C))*Pp + R*(1 - exp(-h/(R*C)))*(F + xi)
-          const T ca = static_cast<T>(th[0]), cb = static_cast<T>(th[1]);
-          T xi;
-          if constexpr (INJ) {
-            xi = noise[static_cast<size_t>(k) * P + p];
-          } else {
-            xi = static_cast<T>(th[3]) * normal1<T>(k0, k1, static_cast<uint32_t>(p + A.p_offset),
-                                                    static_cast<uint32_t>(A.step), static_cast<uint32_t>(k));
-          }
-          x[0] = O::add(O::mul(ca, x[0]), O::mul(cb, O::add(static_cast<T>(S.u_in), xi)));
-        }
-        if (A.check_finite && !bad) {
-          bool ok = true;
-#pragma unroll
-          for (int n = 0; n < NX; ++n) ok &= finite_bits(x[n]);
-          if (!ok) {
-            bad = true;
-            bad_sub = k;
-          }
-        }
-      }
-      }  // general sub-step loop
+      transition_one<MODEL, T, E, INJ, SIMPLE>(x, th, A.subs, A.n_sub, noise, P, p, k0, k1,
+                                              static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
+                                              s_F, s_c, s_s, A.check_finite != 0, bad, bad_sub);
 #pragma unroll
       for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * out_stride + p] = x[n];
 
@@ -566,6 +583,27 @@ static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
 
 // ----------------------------- K7: init ------------------------------------
 
+// initial state of global particle pg (sample_initial, simulate.py:111-129)
+template <int MODEL, typename T>
+__device__ __forceinline__ void init_one(T (&x)[MODEL == SSM_MODEL_LORENZ96 ? 8 : 1], uint32_t pg, uint32_t k0,
+                                         uint32_t k1) {
+  if constexpr (MODEL == SSM_MODEL_LORENZ96) {
+    // x[n] ~ uniform(-1.0, 3.0): low + (high - low) * U  (Lorenz96.bi:21)
+#pragma unroll
+    for (uint32_t g = 0; g < 4; ++g) {
+      const U4 r = philox4x32_10(U4{pg, 0u, g, kPurposeInit}, k0, k1);
+      x[2 * g] = static_cast<T>(-1.0 + 4.0 * u53(r.x, r.y));
+      x[2 * g + 1] = static_cast<T>(-1.0 + 4.0 * u53(r.z, r.w));
+    }
+  } else {
+    // Pp ~ gaussian(90.0, 15.0)  (Windkessel.bi:24)
+    const U4 r = philox4x32_10(U4{pg, 0u, 0u, kPurposeInit}, k0, k1);
+    double z0, z1;
+    box_muller(r.x, r.y, r.z, r.w, z0, z1);
+    x[0] = static_cast<T>(90.0 + 15.0 * z0);
+  }
+}
+
 template <int MODEL, typename T>
 __global__ void __launch_bounds__(kThreads) init_kernel(int P, int p_offset, const uint32_t* keys, T* x) {
   const int b = blockIdx.y;
@@ -573,21 +611,69 @@ __global__ void __launch_bounds__(kThreads) init_kernel(int P, int p_offset, con
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
   T* xb = x + static_cast<size_t>(b) * NX * P;
   for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads) {
-    if constexpr (MODEL == SSM_MODEL_LORENZ96) {
-      // x[n] ~ uniform(-1.0, 3.0): low + (high - low) * U  (Lorenz96.bi:21)
+    T v[NX];
+    init_one<MODEL, T>(v, static_cast<uint32_t>(p + p_offset), k0, k1);
 #pragma unroll
-      for (uint32_t g = 0; g < 4; ++g) {
-        const U4 r = philox4x32_10(U4{static_cast<uint32_t>(p + p_offset), 0u, g, kPurposeInit}, k0, k1);
-        xb[static_cast<size_t>(2 * g) * P + p] = static_cast<T>(-1.0 + 4.0 * u53(r.x, r.y));
-        xb[static_cast<size_t>(2 * g + 1) * P + p] = static_cast<T>(-1.0 + 4.0 * u53(r.z, r.w));
+    for (int n = 0; n < NX; ++n) xb[static_cast<size_t>(n) * P + p] = v[n];
+  }
+}
+
+// ----------------------------- trajectory replay ---------------------------
+// (ssm_replay_path) one thread per filter: ancestry walk, then the chosen
+// line's states regenerated step by step with the fused kernel's transition.
+template <int MODEL, typename T, bool E>
+__global__ void replay_kernel(const ssm_replay_args R) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= R.B) return;
+  constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
+  const int S = R.S;
+  double* ob = R.out + static_cast<size_t>(b) * (S + 1) * NX;
+  const int32_t* const* ab = R.ancs + static_cast<size_t>(b) * (S + 1);
+  const uint32_t* kb = R.keys + static_cast<size_t>(b) * (S + 1) * 2;
+  int j = R.j_final[b];
+  ob[static_cast<size_t>(S) * NX] = static_cast<double>(j);
+  for (int i = S; i > 0; --i) {
+    const int32_t* a = ab[i];
+    if (a) j = a[j];
+    ob[static_cast<size_t>(i - 1) * NX] = static_cast<double>(j);
+  }
+  T x[NX];
+  if (R.x0_flag && R.x0_flag[b]) {
+#pragma unroll
+    for (int n = 0; n < NX; ++n) x[n] = static_cast<T>(R.x0[static_cast<size_t>(b) * NX + n]);
+  } else {
+    init_one<MODEL, T>(x, static_cast<uint32_t>(j), kb[0], kb[1]);
+  }
+#pragma unroll
+  for (int n = 0; n < NX; ++n) ob[n] = static_cast<double>(x[n]);
+  const double* th = R.theta + 4 * b;
+  for (int i = 1; i <= S; ++i) {
+    const int ji = static_cast<int>(ob[static_cast<size_t>(i) * NX]);
+    const ssm_step_desc& d = R.steps[i];
+    const ssm_substep* subs = R.subs + d.subs_offset;
+    bool bad = false;
+    int bad_sub = 0;
+    if constexpr (MODEL == SSM_MODEL_LORENZ96 && !E) {
+      if ((d.hints & SSM_HINT_SINGLE_SUBSTEP) && d.n_sub == 1) {  // the fused kernel's SIMPLE choice
+        const T s_F = static_cast<T>(th[0]);
+        const T s_c = static_cast<T>(th[1] * 20.0 * subs[0].sd);
+        const T s_s = static_cast<T>(subs[0].s[0]);
+        transition_one<MODEL, T, false, false, true>(x, th, subs, d.n_sub, nullptr, R.P, ji, kb[2 * i],
+                                                      kb[2 * i + 1], static_cast<uint32_t>(ji),
+                                                      static_cast<uint32_t>(i), s_F, s_c, s_s, false, bad, bad_sub);
+      } else {
+        transition_one<MODEL, T, false, false, false>(x, th, subs, d.n_sub, nullptr, R.P, ji, kb[2 * i],
+                                                       kb[2 * i + 1], static_cast<uint32_t>(ji),
+                                                       static_cast<uint32_t>(i), T(0), T(0), T(0), false, bad,
+                                                       bad_sub);
       }
     } else {
-      // Pp ~ gaussian(90.0, 15.0)  (Windkessel.bi:24)
-      const U4 r = philox4x32_10(U4{static_cast<uint32_t>(p + p_offset), 0u, 0u, kPurposeInit}, k0, k1);
-      double z0, z1;
-      box_muller(r.x, r.y, r.z, r.w, z0, z1);
-      xb[p] = static_cast<T>(90.0 + 15.0 * z0);
+      transition_one<MODEL, T, E, false, false>(x, th, subs, d.n_sub, nullptr, R.P, ji, kb[2 * i], kb[2 * i + 1],
+                                                static_cast<uint32_t>(ji), static_cast<uint32_t>(i), T(0), T(0),
+                                                T(0), false, bad, bad_sub);
     }
+#pragma unroll
+    for (int n = 0; n < NX; ++n) ob[static_cast<size_t>(i) * NX + n] = static_cast<double>(x[n]);
   }
 }
 
@@ -621,6 +707,43 @@ extern "C" int ssm_propagate_weight(const ssm_pw_args* args, void* stream) {
       launch_pw<SSM_MODEL_WINDKESSEL, double>(A, s);
     else if (A.dtype == SSM_F32)
       launch_pw<SSM_MODEL_WINDKESSEL, float>(A, s);
+    else
+      return SSM_ERR_INVALID_ARG;
+  } else {
+    return SSM_ERR_UNSUPPORTED;
+  }
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+template <int MODEL, typename T>
+static void launch_replay(const ssm_replay_args& R, cudaStream_t s) {
+  const int nt = 64;
+  if (R.exact)
+    replay_kernel<MODEL, T, true><<<(R.B + nt - 1) / nt, nt, 0, s>>>(R);
+  else
+    replay_kernel<MODEL, T, false><<<(R.B + nt - 1) / nt, nt, 0, s>>>(R);
+}
+
+extern "C" int ssm_replay_path(const ssm_replay_args* args, void* stream) {
+  if (!args) return SSM_ERR_INVALID_ARG;
+  const ssm_replay_args& R = *args;
+  if (R.B <= 0 || R.P <= 0 || R.S < 0 || !R.theta || !R.steps || !R.subs || !R.keys || !R.ancs || !R.j_final ||
+      !R.out || (R.x0_flag && !R.x0))
+    return SSM_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (R.model == SSM_MODEL_LORENZ96) {
+    if (R.dtype == SSM_F64)
+      launch_replay<SSM_MODEL_LORENZ96, double>(R, s);
+    else if (R.dtype == SSM_F32)
+      launch_replay<SSM_MODEL_LORENZ96, float>(R, s);
+    else
+      return SSM_ERR_INVALID_ARG;
+  } else if (R.model == SSM_MODEL_WINDKESSEL) {
+    if (R.dtype == SSM_F64)
+      launch_replay<SSM_MODEL_WINDKESSEL, double>(R, s);
+    else if (R.dtype == SSM_F32)
+      launch_replay<SSM_MODEL_WINDKESSEL, float>(R, s);
     else
       return SSM_ERR_INVALID_ARG;
   } else {

@@ -903,7 +903,12 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
   constexpr int kIt = kRunIt;
   __shared__ __align__(16) RunWindow sm;
   const int b = blockIdx.y;
-  if (fs && !fs[b].resample_now) return;
+  if (fs && !fs[b].resample_now) {  // ESS gate held (particle.py:99-100): the history records identity
+    int32_t* ab = anc + static_cast<size_t>(b) * P;
+    const int k1 = min(P, (blockIdx.x + 1) * kScanTile);
+    for (int k = blockIdx.x * kScanTile + threadIdx.x; k < k1; k += kThreads) ab[k] = k;
+    return;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nt = (P + 31) >> 5;
   const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;

@@ -210,7 +210,7 @@ class ParticleRun:
 
     def __init__(self, ir, theta, grid, inputs=None, n_particles=1024, resampler="multinomial",
                  ess_rel=None, initial_state=None, check_finite=True, *, dtype="float64",
-                 exact=None, noise="device", device=None):
+                 exact=None, noise="device", device=None, keep_history=True):
         if n_particles < 2:
             raise ValueError("particle filter needs n_particles >= 2")
         if resampler not in SCHEMES:
@@ -234,6 +234,13 @@ class ParticleRun:
         # off (FMA, 1e-12 of the reference per step) for device noise
         self.exact = (noise == "host") if exact is None else bool(exact)
         self.noise = noise
+        # keep_history=False (device noise): only the ancestors are stored per grid
+        # step; sample_trajectory replays the chosen ancestral line (ssm_replay_path),
+        # bitwise the same trajectory at ~1/17 of the f64 L96 history memory
+        if not keep_history and noise != "device":
+            raise ValueError("keep_history=False needs device noise (host draws cannot be replayed)")
+        self.keep_history = bool(keep_history)
+        self._keys = []  # history-free runs: Philox key (2 x uint32) used at each grid index
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.loglik = 0.0
         self.pos = 0
@@ -260,6 +267,7 @@ class ParticleRun:
         other._hist = list(self._hist)
         other._hx = list(self._hx)
         other._ha = list(self._ha)
+        other._keys = list(self._keys)
         return other
 
     @property
@@ -269,6 +277,9 @@ class ParticleRun:
     @property
     def history(self):
         """[(x_i [nx, P], anc_i [P] | None)] per grid index (particle.py:59, 135); views made on access."""
+        if not self.keep_history:
+            raise ValueError("this run keeps no position history (keep_history=False); "
+                             "sample_trajectory replays the ancestral line instead")
         return [(xb[b], ab[b] if ab is not None else None) for xb, ab, b in self._hist]
 
     @history.setter
@@ -335,6 +346,7 @@ def _common(runs):
         if (r.spec is not r0.spec or r.grid is not r0.grid or r.n_particles != r0.n_particles
                 or r.dtype_id != r0.dtype_id or r.resampler != r0.resampler or r.ess_rel != r0.ess_rel
                 or r.check_finite != r0.check_finite or r.exact != r0.exact or r.noise != r0.noise
+                or r.keep_history != r0.keep_history
                 or r.pos != r0.pos or r.device != r0.device or r.inputs is not r0.inputs):
             raise ValueError("runs advanced together must share model, grid, settings and position")
     return r0
@@ -382,7 +394,13 @@ def init_runs(runs, rngs):
                 for j, b in enumerate(need_draw):
                     x[b].copy_(tmp[j])
     fs = _fs_init(B, dev)
+    if not r0.keep_history:  # what the trajectory replay needs to regenerate x_0
+        init_keys = np.zeros((B, 2), dtype=np.uint32)
+        if need_draw and r0.noise != "host":
+            init_keys[need_draw] = keys
     for b, r in enumerate(runs):
+        if not r0.keep_history:
+            r._keys = [init_keys[b]]
         r._x = x[b]
         r._a = None
         r._cdf = None
@@ -392,8 +410,8 @@ def init_runs(runs, rngs):
         r.pos = 0
         r.weights_uniform = True
         r._maybe_nonuniform = False
-        r._hist = [(x, None, b)]
-        r._hx = [r._x.data_ptr()]
+        r._hist = [(x, None, b)] if r0.keep_history else [(None, None, b)]
+        r._hx = [r._x.data_ptr()] if r0.keep_history else [0]
         r._ha = [0]
     return runs
 
@@ -429,6 +447,7 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
     A.tiles = 1 if tiles_ok else 0
     A.maybe_nonuniform = 1 if maybe else 0
     A.ess_gate = 1 if r0.ess_rel is not None else 0
+    A.x_ring = 0 if r0.keep_history else x_arena.shape[0]
     A.x_in = x_prev.data_ptr()
     A.x_arena = x_arena.data_ptr()
     A.anc_arena = anc_arena.data_ptr() if anc_arena is not None else None
@@ -448,9 +467,10 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
     kind = "tiles" if tiles_ok else "logw"
     rs_n = _RS_LAUNCHES[(kind, scheme)]
     profiling.count_launch(n + rs_n * int(anc_used.sum()))
+    ring = x_arena.shape[0]
     for k in range(n):
         an = anc_arena[k] if anc_used[k] else None
-        new_hist.append((x_arena[k], an))
+        new_hist.append((x_arena[k % ring], an))
         if timer is not None:
             has_obs = bool(desc["has_obs"][k])
             if an is not None:
@@ -460,7 +480,7 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
                               + ((esz + (8 if tiles_ok else 0)) if has_obs else 0))
             timer.add("propagate_weight", evs[4 * k + 2], evs[4 * k + 3], nbytes)
     a_new = a_arena[A.a_last_index] if A.a_last_index >= 0 else a_last
-    return x_arena[n - 1], a_new, bool(A.maybe_nonuniform)
+    return x_arena[(n - 1) % ring], a_new, bool(A.maybe_nonuniform)
 
 
 _SMALL_MAX = None
@@ -541,7 +561,7 @@ def advance_runs(runs, upto, rngs):
     pw_ws = torch.empty(L.ssm_pw_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     rs_ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     # systematic / stratified resample from the pw kernel's tile-local CDF (no second pass over logw)
-    small = (not host_noise and P <= _small_max() and not _NO_SMALL)
+    small = (not host_noise and P <= _small_max() and not _NO_SMALL and r0.keep_history)
     # resample from the pw kernel's tile CDF (multi-kernel path; multinomial with device draws only)
     tiles_ok = (r0.resampler in ("systematic", "stratified") or scheme == _lib.SSM_MULTINOMIAL_SORTED) and not small
     ntile = (P + 31) // 32  # one tile record per warp tile
@@ -578,7 +598,9 @@ def advance_runs(runs, upto, rngs):
     # one allocation per advance call for the history it produces (the caching
     # allocator would otherwise churn cudaMalloc on every step)
     n_steps = upto - start
-    x_arena = torch.empty((n_steps, B, spec.nx, P), dtype=tdt, device=dev)
+    # history-free runs keep two position buffers (ring) instead of one per step
+    x_slots = n_steps if r0.keep_history else min(n_steps, 2)
+    x_arena = torch.empty((x_slots, B, spec.nx, P), dtype=tdt, device=dev)
     n_res = sum(1 for i in range(start + 1, upto + 1) if sched.obs[i] is not None)
     a_arena = torch.empty((max(n_res, 1), B, P), dtype=tdt, device=dev) if n_res else None
     anc_arena = None
@@ -690,8 +712,13 @@ def advance_runs(runs, upto, rngs):
         r._trec = tile_rec[b] if keep_tiles else None
         r._fs = fs[b]
         r._maybe_nonuniform = maybe_nonuniform
-        r._hist.extend((xo, an, b) for xo, an in new_hist)
-        r._hx.extend((x_ptrs + b * xstride).tolist())
+        if r0.keep_history:
+            r._hist.extend((xo, an, b) for xo, an in new_hist)
+            r._hx.extend((x_ptrs + b * xstride).tolist())
+        else:  # ancestors only; positions are replayed by sample_trajectories
+            r._hist.extend((None, an, b) for _, an in new_hist)
+            r._hx.extend([0] * len(new_hist))
+            r._keys.extend([keys[b]] * len(new_hist))
         r._ha.extend(np.where(a_has, a_ptrs + b * astride, 0).tolist())
         r.pos = upto
     return incr
@@ -731,7 +758,7 @@ def sample_trajectories(runs, rngs):
         fs_rows = _stack_rows([r._fs for r in runs]).contiguous()
         _lib.check(L.ssm_pick_from_tiles(B, P, _lib.ptr(cdf), _lib.ptr(trec), _lib.ptr(fs_rows), _lib.ptr(u),
                                          _lib.ptr(j), _lib.ptr(ws), stream), "ssm_pick_from_tiles")
-        return _trace_runs(L, runs, j, S, B, P, nx, dev, stream)
+        return _trajectories_from(L, runs, j, S, B, P, nx, dev, stream)
     # final log-weights (uniform -> zeros with shift 0)
     a_rows, shifts = [], []
     for r in runs:
@@ -757,7 +784,48 @@ def sample_trajectories(runs, rngs):
     j = torch.empty((B, 1), dtype=torch.int32, device=dev)
     _lib.check(L.ssm_resample_search(B, P, 1, _lib.SCHEME_IDS["multinomial"], 1, _lib.ptr(cum), _lib.ptr(u),
                                      None, 0, None, _lib.ptr(j), None, stream), "ssm_resample_search")
-    return _trace_runs(L, runs, j, S, B, P, nx, dev, stream)
+    return _trajectories_from(L, runs, j, S, B, P, nx, dev, stream)
+
+
+def _trajectories_from(L, runs, j, S, B, P, nx, dev, stream):
+    if runs[0].keep_history:
+        return _trace_runs(L, runs, j, S, B, P, nx, dev, stream)
+    return _replay_runs(L, runs, j, S, B, P, nx, dev, stream)
+
+
+def _replay_runs(L, runs, j, S, B, P, nx, dev, stream):
+    """History-free runs: regenerate the chosen ancestral line (ssm_replay_path)."""
+    r0 = runs[0]
+    for r in runs:
+        if len(r._keys) != S + 1 or len(r._ha) != S + 1:
+            raise ValueError("history length does not match the run position")
+    sched = _schedule(r0.grid, r0.spec, r0.inputs, dev)
+    desc = np.ascontiguousarray(sched.desc[: S + 1]).copy()
+    if _NO_HINTS:
+        desc["hints"] = 0
+    desc_t = torch.from_numpy(desc.view(np.uint8).copy()).to(dev)
+    keys_t = torch.from_numpy(np.ascontiguousarray(np.array([r._keys for r in runs], dtype=np.uint32))
+                              .view(np.int32)).to(dev)
+    ancs_t = torch.from_numpy(np.array([r._ha for r in runs], dtype=np.int64)).to(dev)
+    theta = _derived_tensor(runs)
+    fixed = [r.initial_state is not None for r in runs]
+    x0_t = flag_t = None
+    if any(fixed):
+        x0 = np.zeros((B, nx))
+        for b, r in enumerate(runs):
+            if fixed[b]:
+                x0[b] = np.asarray(r.initial_state, dtype=float)
+        x0_t = torch.from_numpy(x0).to(dev)
+        flag_t = torch.tensor(fixed, dtype=torch.int32, device=dev)
+    out = torch.empty((B, S + 1, nx), dtype=torch.float64, device=dev)
+    R = _lib.ReplayArgs()
+    R.model, R.dtype, R.B, R.P, R.S, R.exact = r0.spec.kernel, r0.dtype_id, B, P, S, int(r0.exact)
+    R.theta, R.subs, R.steps = theta.data_ptr(), sched.table.data_ptr(), desc_t.data_ptr()
+    R.keys, R.ancs, R.j_final, R.out = keys_t.data_ptr(), ancs_t.data_ptr(), j.data_ptr(), out.data_ptr()
+    R.x0 = x0_t.data_ptr() if x0_t is not None else None
+    R.x0_flag = flag_t.data_ptr() if flag_t is not None else None
+    _lib.check(L.ssm_replay_path(R, stream), "ssm_replay_path")
+    return list(out.cpu().numpy())
 
 
 def _trace_runs(L, runs, j, S, B, P, nx, dev, stream):

@@ -46,7 +46,8 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
 
     structs = {"ssm_pw_args": _lib.PwArgs, "ssm_substep": _lib.Substep, "ssm_step_desc": _lib.StepDesc,
-               "ssm_advance_args": _lib.AdvanceArgs, "ssm_small_args": _lib.SmallArgs}
+               "ssm_advance_args": _lib.AdvanceArgs, "ssm_small_args": _lib.SmallArgs,
+               "ssm_replay_args": _lib.ReplayArgs}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ssm_b200.h"', "int main(void) {"]
     for name, cls in structs.items():
         lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')

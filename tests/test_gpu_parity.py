@@ -621,3 +621,56 @@ def test_sorted_multinomial_from_tiles_matches_logw(P, pattern):
     _lib.check(L.ssm_resample_from_logw(1, P, 1, _lib.SSM_MULTINOMIAL_SORTED, _lib.ptr(a), _lib.ptr(shift), None,
                                         None, _lib.ptr(keys), 3, _lib.ptr(anc_l), _lib.ptr(ws), _lib.stream_ptr()))
     np.testing.assert_array_equal(anc_t.cpu().numpy(), anc_l.cpu().numpy())
+
+
+@pytest.mark.parametrize("kw", [
+    dict(resampler="systematic"),
+    dict(resampler="multinomial"),
+    dict(resampler="stratified", exact=True),
+    dict(resampler="systematic", dtype="float32"),
+    dict(resampler="systematic", ess_rel=0.5),
+    dict(resampler="multinomial", initial_state=np.linspace(-0.5, 2.5, 8)),
+    dict(resampler="systematic", sparse=True),
+])
+def test_history_free_replay_equals_stored_history(kw):
+    """keep_history=False stores only ancestors; sample_trajectory replays the
+    chosen line with the fused kernel's transition: bitwise the same trajectory
+    (and the same log-likelihood) as the run that keeps every position."""
+    kw = dict(kw)
+    sparse = kw.pop("sparse", False)
+    theta = np.array([10.0, 0.1])
+    times = np.linspace(0.0, 1.0, 21)
+    obs = O.simulate_l96(theta, times, O.Stream(3), obs_slots=range(4) if sparse else range(8),
+                         obs_every=2 if sparse else 1)
+    ov = np.array([obs[k][0] for k in range(1, 21)])
+    om = np.array([obs[k][1] for k in range(1, 21)])
+    grid = build_filter_grid(0.0, 1.0, 20, times[1:], ov, om, n_obs=8)
+    outs = [particle_filter(LORENZ96, theta, grid, RngStream(11), n_particles=9000, keep_history=kh, **kw)
+            for kh in (True, False)]
+    assert outs[0].loglik == outs[1].loglik
+    np.testing.assert_array_equal(outs[0].trajectory, outs[1].trajectory)
+    with pytest.raises(ValueError):
+        _ = outs[1].run.history
+    if kw.get("resampler") in ("systematic", "stratified"):  # ancestors ascending, in range (ESS-held steps: identity)
+        for _, anc in outs[0].run.history[1:]:
+            if anc is not None:
+                a = anc.cpu().numpy()
+                assert a.min() >= 0 and a.max() < 9000 and np.all(np.diff(a) >= 0)
+
+
+def test_history_free_windkessel_and_resume():
+    theta = np.array([1.8, 3.0, 0.06, 25.0])
+    times = np.linspace(0.0, 0.5, 51)
+    tin = np.round(np.arange(0, 0.51, 0.01), 10)
+    inputs = LocfInputs(tin, O.windkessel_flow(tin))
+    ys = 90.0 + np.zeros((50, 1))
+    grid = build_filter_grid(0.0, 0.5, 50, times[1:], ys, np.ones((50, 1), bool), n_obs=1)
+    trajs = []
+    for kh in (True, False):
+        run = ParticleRun(WINDKESSEL, theta, grid, inputs=inputs, n_particles=6000, resampler="systematic",
+                          keep_history=kh)
+        run.init(RngStream(5).child(0))
+        run.advance_to(20, RngStream(5).child(1))
+        run.advance_to(50, RngStream(5).child(2))  # second call: different device keys per segment
+        trajs.append(run.sample_trajectory(RngStream(5).child(3)))
+    np.testing.assert_array_equal(trajs[0], trajs[1])

@@ -257,13 +257,14 @@ typedef struct ssm_advance_args {
   void* x_arena;             /* [n_steps or x_ring][B][nx][P] positions written per step */
   int32_t* anc_arena;        /* [n_steps][B][P]; slot k valid iff anc_used[k] */
   const void* a_prev;        /* unnormalised log-weights of the last weighted step, or NULL */
-  void* a_arena;             /* [n_weighted][B][P] */
+  void* a_arena;             /* [n_weighted or a_ring][B][P] */
   void* cdf_local;           /* [B][P] uint64 */
   void* tile_rec;            /* [B][ceil(P/32)] ssm_tile_rec */
   void* resample_ws;         /* ssm_resample_workspace_bytes(B, P) */
   int32_t* anc_used;         /* HOST out [n_steps] */
   int32_t a_last_index;      /* out: a_arena slot of the last weighted step (-1: a_prev) */
-  int32_t pad2;
+  int32_t a_ring;            /* 0: a_arena has a slot per weighted step; r > 0: weighted step w writes
+                                slot w % r (only the last weighted step's log-weights are read later) */
   void* const* events;       /* HOST, nullable: 4 cudaEvent_t per step (resample start/end, pw start/end) */
 } ssm_advance_args;
 

@@ -149,7 +149,7 @@ class AdvanceArgs(C.Structure):
         ("resample_ws", C.c_void_p),
         ("anc_used", C.c_void_p),
         ("a_last_index", C.c_int32),
-        ("pad2", C.c_int32),
+        ("a_ring", C.c_int32),
         ("events", C.c_void_p),
     ]
 

@@ -58,7 +58,8 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
     for (int n = 0; n < 8; ++n) pw.y[n] = d.y[n];
     pw.u_obs = d.u_obs;
     void* a_out = nullptr;
-    if (d.has_obs) a_out = static_cast<char*>(A->a_arena) + static_cast<size_t>(slot) * astep;
+    const int a_slot = A->a_ring > 0 ? slot % A->a_ring : slot;
+    if (d.has_obs) a_out = static_cast<char*>(A->a_arena) + static_cast<size_t>(a_slot) * astep;
     pw.a_out = a_out;
     pw.cdf_local = (A->tiles && d.has_obs) ? A->cdf_local : nullptr;
     pw.tile_rec = (A->tiles && d.has_obs) ? A->tile_rec : nullptr;
@@ -69,7 +70,7 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
     x_prev = x_out;
     if (d.has_obs) {
       a_last = a_out;
-      A->a_last_index = slot;
+      A->a_last_index = a_slot;
       ++slot;
       maybe = 1;
     } else if (maybe && !A->ess_gate) {

@@ -448,6 +448,7 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
     A.maybe_nonuniform = 1 if maybe else 0
     A.ess_gate = 1 if r0.ess_rel is not None else 0
     A.x_ring = 0 if r0.keep_history else x_arena.shape[0]
+    A.a_ring = a_arena.shape[0] if a_arena is not None else 0
     A.x_in = x_prev.data_ptr()
     A.x_arena = x_arena.data_ptr()
     A.anc_arena = anc_arena.data_ptr() if anc_arena is not None else None
@@ -602,7 +603,10 @@ def advance_runs(runs, upto, rngs):
     x_slots = n_steps if r0.keep_history else min(n_steps, 2)
     x_arena = torch.empty((x_slots, B, spec.nx, P), dtype=tdt, device=dev)
     n_res = sum(1 for i in range(start + 1, upto + 1) if sched.obs[i] is not None)
-    a_arena = torch.empty((max(n_res, 1), B, P), dtype=tdt, device=dev) if n_res else None
+    # log-weights: the native driver keeps a ring of two (the step reads the previous
+    # weighted step's, later only the last one is used); host-noise loop: one per step
+    a_slots = min(n_res, 2) if not host_noise else n_res
+    a_arena = torch.empty((max(a_slots, 1), B, P), dtype=tdt, device=dev) if n_res else None
     anc_arena = None
     a_slot = 0
     if small:  # the persistent kernel keeps its CDF in shared memory

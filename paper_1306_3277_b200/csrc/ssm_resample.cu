@@ -509,8 +509,7 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
                  const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
                  const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ cnt,
                  int32_t* __restrict__ split, int ndiag, const uint64_t* __restrict__ g_off = nullptr,
-                 const int32_t* __restrict__ c_shift = nullptr, int32_t* __restrict__ anc_direct = nullptr,
-                 int4* __restrict__ long_runs = nullptr, uint32_t* __restrict__ long_count = nullptr) {
+                 const int32_t* __restrict__ c_shift = nullptr) {
   __shared__ __align__(16) uint64_t sm[kScanTile + kScanTile / 8];
   __shared__ uint64_t warp_tot[kThreads / 32];
   const int b = blockIdx.y, tile = blockIdx.x;
@@ -652,106 +651,6 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
   }
 
   const int cshift = c_shift ? c_shift[b] : 0;
-  if (anc_direct) {
-    // anc_k = j for k in [c_{j-1}, c_j).  Short runs are staged in shared
-    // memory over the block's output window and stored coalesced; outputs
-    // past the window go straight to global; long runs are deferred to
-    // long_runs_kernel in chunks of <= kRunChunk outputs.
-    __shared__ int s_lo, s_hi;
-    __shared__ int s_wmax[kThreads / 32];
-    constexpr int kOutBuf = 4096;             // block output window staged in shared memory
-    constexpr int kPer = kOutBuf / kThreads;  // outputs per thread in the fill scan
-    static_assert(sizeof(sm) >= (kOutBuf + kOutBuf / 32) * sizeof(int32_t), "staging buffer");
-    int32_t* sOut = reinterpret_cast<int32_t*>(sm);
-    const auto pad = [](int e) { return e + (e >> 5); };  // stride-kPer reads conflict-free
-    const bool active = jt < P_in;
-    const int c_first = active && (jt > 0 || g_off)
-                            ? offspring_bound<SCHEME>(cum_prev, u_sys, U, k0, k1, step, P_out, invP, pow2) - cshift
-                            : 0;
-    int hk[kScanItems];  // c_j (end of particle j's offspring run), clipped for the last particle
-    {
-      int cp = c_first;
-#pragma unroll
-      for (int i = 0; i < kScanItems; ++i) {
-        const int j = jt + i;
-        if (active && j < P_in) {
-          cp = offspring_bound<SCHEME>(cum[i], u_sys, U, k0, k1, step, P_out, invP, pow2) - cshift;
-          if (j == P_in - 1 && cp < P_out) cp = P_out;  // u_k == 1.0 -> searchsorted = P -> clip to P-1
-        }
-        hk[i] = cp;
-      }
-    }
-    __syncthreads();  // sm may still be read by the non-tile paths above
-    const int last_thread = min(kThreads - 1, (min(P_in, j0 + kScanTile) - 1 - j0) / kScanItems);
-    if (threadIdx.x == 0) s_lo = c_first;  // thread 0 holds the block's first particle
-    if (threadIdx.x == last_thread) s_hi = hk[kScanItems - 1];
-    for (int e = threadIdx.x; e < (kOutBuf + kOutBuf / 32) / 4; e += kThreads)
-      reinterpret_cast<int4*>(sOut)[e] = make_int4(-1, -1, -1, -1);
-    __syncthreads();
-    const int lo_blk = s_lo, n_out = s_hi - lo_blk;
-    int32_t* ab = anc_direct + static_cast<size_t>(b) * P_out;
-    if (n_out <= kOutBuf) {
-      // anc_k = j for k in [c_{j-1}, c_j): mark each run start with its
-      // particle, then an inclusive max-scan over the window fills the runs
-      if (active) {
-        int cp = c_first;
-#pragma unroll
-        for (int i = 0; i < kScanItems; ++i) {
-          if (hk[i] > cp) sOut[pad(cp - lo_blk)] = jt + i;
-          cp = hk[i];
-        }
-      }
-      __syncthreads();
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      static_assert(kPer == 16, "pad(t*kPer + i) == t*kPer + i + t/2 needs kPer == 16");
-      int32_t* sv = sOut + threadIdx.x * kPer + (threadIdx.x >> 1);
-      int v[kPer];
-      int run = -1;
-#pragma unroll
-      for (int i = 0; i < kPer; ++i) {
-        run = max(run, sv[i]);
-        v[i] = run;
-      }
-      int incl = run;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl = max(incl, y);
-      }
-      int carry = __shfl_up_sync(0xffffffffu, incl, 1);
-      if (lane == 0) carry = -1;
-      if (lane == 31) s_wmax[warp] = incl;
-      __syncthreads();
-#pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w)
-        if (w < warp) carry = max(carry, s_wmax[w]);
-#pragma unroll
-      for (int i = 0; i < kPer; ++i) sv[i] = max(carry, v[i]);
-      __syncthreads();
-      for (int e = threadIdx.x; e < n_out; e += kThreads) ab[lo_blk + e] = sOut[pad(e)];
-    } else if (active) {
-      // heavy block (degenerate weights): short runs written in place, long
-      // runs deferred to long_runs_kernel in chunks of <= kRunChunk outputs
-      int cp = c_first;
-#pragma unroll
-      for (int i = 0; i < kScanItems; ++i) {
-        const int j = jt + i, hi_k = hk[i];
-        if (hi_k - cp <= kShortRun) {
-          for (int k = cp; k < hi_k; ++k) ab[k] = j;
-        } else {
-          const int nchunk = (hi_k - cp + kRunChunk - 1) / kRunChunk;
-          const uint32_t slot = atomicAdd(long_count + b, static_cast<uint32_t>(nchunk));
-          int4* rb = long_runs + static_cast<size_t>(b) * long_runs_cap(P_in, P_out);
-          for (int q = 0; q < nchunk; ++q) {
-            const int lo_q = cp + q * kRunChunk;
-            rb[slot + q] = make_int4(j, lo_q, min(lo_q + kRunChunk, hi_k), 0);
-          }
-        }
-        cp = hi_k;
-      }
-    }
-    return;
-  }
   if (jt >= P_in) return;
   int c_prev = (jt > 0 || g_off) ? offspring_bound<SCHEME>(cum_prev, u_sys, U, k0, k1, step, P_out, invP, pow2) - cshift
                                  : 0;

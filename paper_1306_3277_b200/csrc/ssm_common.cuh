@@ -78,16 +78,30 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, uint32_t c, u
   z1 = r * s;
 }
 
+// MUFU approximations with flush-to-zero: no denormal fix-up code around them
+// (the arguments below are never denormal).
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_ftz(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Box-Muller pair, float32 (the device noise generator for both precisions).
 // u1 = (a + 1/2) 2^-32 keeps 32 bits near 0, so |z| reaches 6.7 sigma; the
-// radius and angle use the MUFU lg2 / rsq / sin / cos (angle on [-pi, pi),
-// |error| < 2^-21; a rotation by pi leaves the pair iid N(0,1)).
+// radius and angle use the MUFU lg2 / sqrt / sin / cos (angle on [-pi, pi),
+// |error| < 2^-21; a rotation by pi leaves the pair iid N(0,1)).  u1 >= 2^-33,
+// so nothing here is denormal; the max() guards lg2's error near u1 = 1.
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
   const float u1 = fmaf(static_cast<float>(a), 0x1.0p-32f, 0x1.0p-33f);  // (0, 1]
   const float th = fmaf(static_cast<float>(b >> 8), 6.28318530717958647692f * 0x1.0p-24f,
                         -3.14159265358979323846f);
-  const float x = -1.38629436111989061883f * __log2f(u1);  // -2 ln u1 (MUFU.LG2), >= 0
-  const float r = x > 0.0f ? x * rsqrtf(x) : 0.0f;             // sqrt via MUFU.RSQ, no slow path
+  const float x = fmaxf(-1.38629436111989061883f * lg2_ftz(u1), 0.0f);  // -2 ln u1
+  const float r = sqrt_ftz(x);
   float s, co;
   __sincosf(th, &s, &co);
   z0 = r * co;

@@ -314,6 +314,16 @@ __device__ __forceinline__ Lse fold_tiles(Lse st, double m, double t, double s2,
   return st;
 }
 
+// Warp-tile partials parked until 32 have accumulated (one per slot, in tile order).
+struct ParkedTiles {
+  double m[32], t[32], s2[32];
+};
+
+__device__ __forceinline__ Lse fold_parked(Lse st, const ParkedTiles* pk, bool valid, int lane) {
+  return fold_tiles(st, valid ? pk->m[lane] : -CUDART_INF, valid ? pk->t[lane] : 0.0,
+                    valid ? pk->s2[lane] : 0.0, lane);
+}
+
 // SIMPLE: one sub-step with one RK4 step (the benchmark grid and the sparse
 // SMC^2 grid) -- no runtime sub-step loops, sub-step constants hoisted out of
 // the particle loop, observation slots selected by grid-uniform predicates.
@@ -361,9 +371,11 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
   __shared__ double s_exp_tab[64];
   if (threadIdx.x < 64) s_exp_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
   __syncthreads();
+  __shared__ ParkedTiles s_park[kThreads / 32];
+  ParkedTiles* park = &s_park[threadIdx.x >> 5];
   Lse st = lse_empty();  // warp partial (lane 0), groups of 32 warp tiles folded in order
-  int slot = 0;          // lane holding the current warp tile's {m_w, t_w, s2_w}
-  double r_m = -CUDART_INF, r_t = 0.0, r_s2 = 0.0;
+  int slot = 0;          // parking slot of the current warp tile's {m_w, t_w, s2_w}
+  int nparked = 0;       // (lane 0) slots filled since the last fold: a prefix of the slots
   bool bad = false;
   int bad_sub = 0;
 
@@ -419,31 +431,35 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
               }
             }
           } else {
+            // sum of -z^2/2 with z = (y - x) / 0.5 = 2d, accumulated as -2 * sum(d^2):
+            // every step differs from fma(-z/2, z, g) by a power-of-two scaling only,
+            // so the two forms round identically (bitwise) with half the FP64 work
+            T s = T(0);
             if constexpr (SIMPLE) {
               const uint32_t mask = A.obs_mask;  // grid-uniform: no divergence
               if (mask == 0xFFu) {
 #pragma unroll
                 for (int n = 0; n < 8; ++n) {
-                  const T z = (static_cast<T>(A.y[n]) - x[n]) * T(2.0);
-                  g = fma(T(-0.5) * z, z, g);
+                  const T d = static_cast<T>(A.y[n]) - x[n];
+                  s = fma(d, d, s);
                 }
               } else {
 #pragma unroll
                 for (int n = 0; n < 8; ++n) {
-                  const T z = (static_cast<T>(A.y[n]) - x[n]) * T(2.0);
-                  if (mask & (1u << n)) g = fma(T(-0.5) * z, z, g);
+                  const T d = static_cast<T>(A.y[n]) - x[n];
+                  if (mask & (1u << n)) s = fma(d, d, s);
                 }
               }
             } else {
 #pragma unroll
               for (int n = 0; n < 8; ++n) {
                 if (A.obs_mask & (1u << n)) {
-                  const T z = (static_cast<T>(A.y[n]) - x[n]) * T(2.0);
-                  g = fma(T(-0.5) * z, z, g);
+                  const T d = static_cast<T>(A.y[n]) - x[n];
+                  s = fma(d, d, s);
                 }
               }
             }
-            g -= gconst;
+            g = fma(T(-2.0), s, -gconst);
           }
         } else {
           const T mean = O::add(x[0], O::mul(static_cast<T>(th[2]), static_cast<T>(A.u_obs)));
@@ -471,14 +487,22 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
     const bool any_nan = __any_sync(0xffffffffu, act && isnan(a_d));
     const double e = (!act || mw == -CUDART_INF) ? 0.0 : exp_tile(a_d - mw, s_exp_tab);
     const uint64_t q = (e >= 0.0 && e <= 1.0) ? __double2ull_rn(e * kTileFix) : 0ull;
-    uint64_t qi = q;
+    // inclusive prefix of q <= 2^52 over the tile as two 32-bit scans of its
+    // 26-bit halves (each tile sum < 2^31): exact, half the shuffle work of a u64 scan
+    uint32_t qh = static_cast<uint32_t>(q >> 26), ql = static_cast<uint32_t>(q) & 0x3ffffffu;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xffffffffu, qi, o);
-      if (lane >= o) qi += y;
+      const uint32_t yh = __shfl_up_sync(0xffffffffu, qh, o);
+      const uint32_t yl = __shfl_up_sync(0xffffffffu, ql, o);
+      if (lane >= o) {
+        qh += yh;
+        ql += yl;
+      }
     }
+    const uint64_t qi = (static_cast<uint64_t>(qh) << 26) + ql;
     if (cloc && act) cloc[p] = qi;
-    const uint64_t Qw = __shfl_sync(0xffffffffu, qi, 31);
+    const uint64_t Qw = (static_cast<uint64_t>(__shfl_sync(0xffffffffu, qh, 31)) << 26) +
+                        __shfl_sync(0xffffffffu, ql, 31);
     double s2_ = 0.0;
     if (want_ess) {  // block-uniform
       s2_ = e * e;
@@ -487,20 +511,26 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
     }
     if (lane == 0 && trec && p < P) trec[p >> 5] = ssm_tile_rec{mw, Qw};
     // tile sum of exp(a - m_w) from the exact fixed-point total (|err| <= 32 * 2^-53),
-    // parked in lane `slot`; every 32 tiles the warp folds them in one pass
-    if (lane == slot && p - lane < P) {  // tiles past P stay empty (their m_w is a NaN sentinel)
-      r_m = mw;
-      r_t = any_nan ? CUDART_NAN : static_cast<double>(Qw) * (1.0 / kTileFix);
-      r_s2 = s2_;
+    // parked in shared memory slot `slot` of the warp (the values are warp-uniform,
+    // lane 0 stores); every 32 tiles the warp folds them in one pass
+    if (lane == 0 && p - lane < P) {  // tiles past P stay empty (their m_w is a NaN sentinel)
+      park->m[slot] = mw;
+      park->t[slot] = any_nan ? CUDART_NAN : static_cast<double>(Qw) * (1.0 / kTileFix);
+      park->s2[slot] = s2_;
+      ++nparked;
     }
     if (++slot == 32) {
-      st = fold_tiles(st, r_m, r_t, r_s2, lane);
+      __syncwarp();
+      st = fold_parked(st, park, lane < __shfl_sync(0xffffffffu, nparked, 0), lane);
+      __syncwarp();
       slot = 0;
-      r_m = -CUDART_INF;
-      r_t = r_s2 = 0.0;
+      nparked = 0;
     }
   }
-  if (slot > 0) st = fold_tiles(st, r_m, r_t, r_s2, lane);
+  if (slot > 0) {
+    __syncwarp();
+    st = fold_parked(st, park, lane < __shfl_sync(0xffffffffu, nparked, 0), lane);
+  }
 
   if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
 

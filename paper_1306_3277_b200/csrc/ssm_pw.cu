@@ -17,13 +17,14 @@
 
 namespace ssm {
 
+constexpr int kPwThreads = kThreads;  // fused-kernel block (128 threads x 5 CTAs spills: slower)
 constexpr int kMaxPwBlocks = 2048;  // per filter; a function of P only (determinism)
 
 // Blocks per filter: >= 4 block tiles per block, so each warp folds several warp
 // tiles per setup (matters at moderate P with many filters, e.g. PMMH 8 x 2^16).
 // A function of P only, so the LSE fold order never depends on the batch.
 __host__ __device__ inline int pw_grid_x(int P) {
-  const int tiles = (P + kThreads - 1) / kThreads;
+  const int tiles = (P + kPwThreads - 1) / kPwThreads;
   const int g = (tiles + 3) / 4;
   return g < kMaxPwBlocks ? g : kMaxPwBlocks;
 }
@@ -331,13 +332,13 @@ template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE = false>
 // NOTE: plain __launch_bounds__(kThreads).  An explicit minBlocks of 1 lets
 // ptxas spend 172 registers on the SIMPLE f64 kernel (1 CTA/SM, 0.80 ms
 // vs 0.63 ms at 119 registers / 2 CTAs); minBlocks 3 (<= 85) is also slower.
-__global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) pw_kernel(const ssm_pw_args A) {
+__global__ void __launch_bounds__(kPwThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) pw_kernel(const ssm_pw_args A) {
   pdl_wait();
   using O = Ar<T, E>;
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
   const int b = blockIdx.y;
   const int P = A.P;
-  const int ntiles = (P + kThreads - 1) / kThreads;
+  const int ntiles = (P + kPwThreads - 1) / kPwThreads;
   ssm_filter_state* fs = A.fs + b;
   const int R = fs->resample_now;
   const bool uniform_in = R || fs->uniform;
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
   __shared__ double s_exp_tab[64];
   if (threadIdx.x < 64) s_exp_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
   __syncthreads();
-  __shared__ ParkedTiles s_park[kThreads / 32];
+  __shared__ ParkedTiles s_park[kPwThreads / 32];
   ParkedTiles* park = &s_park[threadIdx.x >> 5];
   Lse st = lse_empty();  // warp partial (lane 0), groups of 32 warp tiles folded in order
   int slot = 0;          // parking slot of the current warp tile's {m_w, t_w, s2_w}
@@ -383,8 +384,8 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
   // ancestor index of the tile after it are in flight while the current tile
   // computes (the anc -> x dependent loads never stall an iteration)
   T xn[NX];
-  const int stride = gridDim.x * kThreads;
-  const int p0 = blockIdx.x * kThreads + threadIdx.x;
+  const int stride = gridDim.x * kPwThreads;
+  const int p0 = blockIdx.x * kPwThreads + threadIdx.x;
   auto load_x = [&](int pp, int src) {
 #pragma unroll
     for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * in_stride + src];
@@ -393,6 +394,9 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
   int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride;
   const T gconst = static_cast<T>(static_cast<double>(__popc(A.obs_mask)) * (A.obs_log_sd + A.log_sqrt_2pi));
   T s_F = T(0), s_c = T(0), s_s = T(0);
+  // SIMPLE with every slot observed: the finite-state check rides on the observation sum
+  const bool defer_finite = SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ && has_obs &&
+                            A.obs_mask == 0xFFu && A.check_finite != 0;
   if constexpr (SIMPLE) {
     s_F = static_cast<T>(th[0]);
     s_c = static_cast<T>(th[1] * 20.0 * A.subs[0].sd);  // sqrt(sigma2) / h * sqrt(d)
@@ -400,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
   }
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int p = tile * kThreads + threadIdx.x;
+    const int p = tile * kPwThreads + threadIdx.x;
     const bool act = p < P;
     double a_d = -CUDART_INF;
     T x[NX];
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
     if (act) {
       transition_one<MODEL, T, E, INJ, SIMPLE>(x, th, A.subs, A.n_sub, noise, P, p, k0, k1,
                                               static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
-                                              s_F, s_c, s_s, A.check_finite != 0, bad, bad_sub);
+                                              s_F, s_c, s_s, A.check_finite != 0 && !defer_finite, bad, bad_sub);
 #pragma unroll
       for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * out_stride + p] = x[n];
 
@@ -442,6 +446,14 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
                 for (int n = 0; n < 8; ++n) {
                   const T d = static_cast<T>(A.y[n]) - x[n];
                   s = fma(d, d, s);
+                }
+                // deferred finite check: s is finite only if every x[n] is, so the
+                // per-slot test runs only when s is not (overflow or a bad state)
+                if (defer_finite && !bad && !(s < T(CUDART_INF))) {
+                  bool ok = true;
+#pragma unroll
+                  for (int n = 0; n < 8; ++n) ok &= finite_bits(x[n]);
+                  if (!ok) bad = true;  // bad_sub stays 0 (one sub-step)
                 }
               } else {
 #pragma unroll
@@ -535,12 +547,12 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
   if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
 
   // ---- per-block partial + last-block finalize ----
-  __shared__ Lse red[kThreads / 32];
+  __shared__ Lse red[kPwThreads / 32];
   __shared__ bool s_last;
   Lse* parts = reinterpret_cast<Lse*>(A.workspace) + static_cast<size_t>(b) * kMaxPwBlocks;
   if (has_obs) {
     // lane 0 of each warp holds its warp's partial; fold warps in order
-    const Lse r = lse_block_reduce<kThreads>(lane == 0 ? st : lse_empty(), red);
+    const Lse r = lse_block_reduce<kPwThreads>(lane == 0 ? st : lse_empty(), red);
     if (threadIdx.x == 0) parts[blockIdx.x] = r;
   }
   __threadfence();
@@ -552,12 +564,12 @@ __global__ void __launch_bounds__(kThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) 
 
   if (has_obs) {
     Lse acc = lse_empty();
-    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += kThreads) {
+    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += kPwThreads) {
       const Lse q{__ldcg(&parts[i].m), __ldcg(&parts[i].c), __ldcg(&parts[i].t),
                   __ldcg(&parts[i].s2)};
       acc = lse_combine(acc, q);
     }
-    acc = lse_block_reduce<kThreads>(acc, red);
+    acc = lse_block_reduce<kPwThreads>(acc, red);
     if (threadIdx.x == 0 && A.lse_out) {
       // sharded filter: hand the rank's partial to the cross-rank combine (C1)
       double* o = static_cast<double*>(A.lse_out) + 4 * b;
@@ -594,20 +606,20 @@ static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
     // host hint: one sub-step with one RK4 step (any observation mask)
     const bool simple = (A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !A.exact && !inj;
     if (simple) {
-      launch_pdl(pw_kernel<MODEL, T, false, false, true>, grid, dim3(kThreads), s, A);
+      launch_pdl(pw_kernel<MODEL, T, false, false, true>, grid, dim3(kPwThreads), s, A);
       return;
     }
   }
   if (A.exact) {
     if (inj)
-      launch_pdl(pw_kernel<MODEL, T, true, true>, grid, dim3(kThreads), s, A);
+      launch_pdl(pw_kernel<MODEL, T, true, true>, grid, dim3(kPwThreads), s, A);
     else
-      launch_pdl(pw_kernel<MODEL, T, true, false>, grid, dim3(kThreads), s, A);
+      launch_pdl(pw_kernel<MODEL, T, true, false>, grid, dim3(kPwThreads), s, A);
   } else {
     if (inj)
-      launch_pdl(pw_kernel<MODEL, T, false, true>, grid, dim3(kThreads), s, A);
+      launch_pdl(pw_kernel<MODEL, T, false, true>, grid, dim3(kPwThreads), s, A);
     else
-      launch_pdl(pw_kernel<MODEL, T, false, false>, grid, dim3(kThreads), s, A);
+      launch_pdl(pw_kernel<MODEL, T, false, false>, grid, dim3(kPwThreads), s, A);
   }
 }
 

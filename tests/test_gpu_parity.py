@@ -407,7 +407,8 @@ def test_tiles_resample_heavy_runs_match_oracle(scheme, P, pattern):
     np.testing.assert_array_equal(anc.cpu().numpy(), O.resample_with(w, scheme, u_np))
 
 
-def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float64", tiles=None, obs_mask=0xFF):
+def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float64", tiles=None, obs_mask=0xFF,
+               fs_out=None):
     """One ssm_propagate_weight launch with device noise (C ABI), returns x_out, a_out."""
     from paper_1306_3277_b200 import _lib
     from paper_1306_3277_b200.inference.particle import _fs_init, _dtype_info
@@ -444,6 +445,8 @@ def _pw_direct(x, theta, keys, d, hints, y, exact=False, anc=None, dtype="float6
     if tiles is not None:
         rec = trec.cpu().numpy().view([("m", "<f8"), ("Q", "<u8")])
         tiles.update(cdf=cloc.cpu().numpy().view(np.uint64), m=rec["m"], Q=rec["Q"])
+    if fs_out is not None:
+        fs_out.update(err_nonfinite=int(fs.cpu().numpy().reshape(-1).view(_lib.FILTER_STATE_DTYPE)["err_nonfinite"][0]))
     return xout.t().double().cpu().numpy(), a.double().cpu().numpy()
 
 
@@ -463,6 +466,28 @@ def test_specialised_kernel_equals_general(dtype, d, mask):
     tol = 1e-12 if dtype == "float64" else 1e-5
     assert normwise(x1, x0) <= tol
     assert normwise(a1, a0) <= tol
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("mask", [0xFF, 0x0F])
+@pytest.mark.parametrize("bad", ["none", "inf", "nan"])
+def test_fused_nonfinite_flag_both_kernels(dtype, mask, bad):
+    """Non-finite states are flagged at the step (err = step * 64 + sub-step) by the
+    SIMPLE kernel (whose full-observation path checks through the observation sum)
+    and by the general kernel alike; finite states are never flagged."""
+    rs = np.random.default_rng(4)
+    P = 3000
+    x = rs.uniform(-1, 3, (P, 8))
+    if bad == "inf":
+        x[1234, 5] = 1e200  # overflows inside RK4
+    elif bad == "nan":
+        x[77, 0] = np.nan
+    y = rs.normal(0, 3, 8)
+    for hints in (1, 0):
+        fs = {}
+        _pw_direct(x, [10.0, 0.1], [5, 6], 0.05, hints, y, dtype=dtype, obs_mask=mask, fs_out=fs)
+        want = 3 * 64 if bad != "none" else np.iinfo(np.int32).max
+        assert fs["err_nonfinite"] == want, (hints, fs)
 
 
 def test_fast_device_noise_filter_tracks_exact():

@@ -423,6 +423,12 @@ tile_prefix_kernel(int tiles, uint64_t* __restrict__ sums, uint64_t* __restrict_
 // a 1-block scan of the block totals.
 constexpr int kRecPerBlock = kThreads;  // 256 tile records per block (one per thread)
 
+// per-filter constants of the tile-path offspring kernel (blk_prefix_kernel):
+// 1 / total, P / total, the systematic uniform, 1 / P
+struct OffspringConsts {
+  double inv, tscale, u_sys, invP;
+};
+
 __global__ void __launch_bounds__(kThreads)
 tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_filter_state* __restrict__ fs,
                   double* __restrict__ scale, uint64_t* __restrict__ prel, uint64_t* __restrict__ blk_tot,
@@ -464,7 +470,8 @@ tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_fi
 
 __global__ void __launch_bounds__(1024)
 blk_prefix_kernel(int nblk, uint64_t* __restrict__ blk, uint64_t* __restrict__ totals,
-                  const ssm_filter_state* __restrict__ fs) {
+                  const ssm_filter_state* __restrict__ fs, OffspringConsts* __restrict__ oc = nullptr, int P = 0,
+                  const double* __restrict__ u = nullptr, const uint32_t* __restrict__ keys = nullptr, int step = 0) {
   pdl_wait();
   const int b = blockIdx.x;
   if (fs && !fs[b].resample_now) return;
@@ -494,7 +501,15 @@ blk_prefix_kernel(int nblk, uint64_t* __restrict__ blk, uint64_t* __restrict__ t
     bb[t] = run;
     run += x;
   }
-  if (threadIdx.x == 0) totals[b] = tot;
+  if (threadIdx.x == 0) {
+    totals[b] = tot;
+    if (oc) {  // the offspring kernel's per-filter constants, computed once
+      const double inv = 1.0 / static_cast<double>(tot);
+      const double Pd = static_cast<double>(P);
+      const double us = u ? u[b] : (keys ? device_uniform(keys[2 * b], keys[2 * b + 1], 0u, step, kPurposeSystematic) : 0.0);
+      oc[b] = OffspringConsts{inv, Pd * inv, us, 1.0 / Pd};
+    }
+  }
 }
 
 // c_j for every particle + merge-path partition entries
@@ -797,10 +812,16 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
                        const uint64_t* __restrict__ pref, const uint64_t* __restrict__ totals,
                        const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
                        const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc,
-                       int4* __restrict__ long_runs, uint32_t* __restrict__ long_count) {
+                       int4* __restrict__ long_runs, uint32_t* __restrict__ long_count,
+                       const OffspringConsts* __restrict__ oc) {
   pdl_wait();
   constexpr int kIt = kRunIt;
   __shared__ __align__(16) RunWindow sm;
+  struct __align__(16) TileInfo {
+    uint64_t pre;
+    double sc;
+  };
+  __shared__ TileInfo s_tile[kThreads / 32][kIt];
   const int b = blockIdx.y;
   if (fs && !fs[b].resample_now) {  // ESS gate held (particle.py:99-100): the history records identity
     int32_t* ab = anc + static_cast<size_t>(b) * P;
@@ -825,21 +846,18 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
     const int j = jw + it * 32 + lane;
     qv[it] = j < P - 1 ? __ldg(cl + j) : 0ull;
   }
-  uint64_t my_pre = 0;
-  double my_sc = 0.0;
-  if (lane < kIt && tw0 + lane < nt) {
-    my_pre = tp[tw0 + lane] + bp[(tw0 + lane) / kRecPerBlock];
-    my_sc = scb[tw0 + lane];
+  // the warp's 8 tiles' prefix / scale, one per lane, broadcast through shared memory
+  if (lane < kIt) {
+    TileInfo ti{0ull, 0.0};
+    if (tw0 + lane < nt) ti = TileInfo{tp[tw0 + lane] + bp[(tw0 + lane) / kRecPerBlock], scb[tw0 + lane]};
+    s_tile[warp][lane] = ti;
   }
-  const double inv = 1.0 / static_cast<double>(totals[b]);
-  const double Pd = static_cast<double>(P);
-  const double tscale = Pd * inv;
+  const OffspringConsts K = oc[b];  // 1 / total, P / total, u, 1 / P (blk_prefix_kernel)
+  const double inv = K.inv, tscale = K.tscale, invP = K.invP;
   const bool pow2 = (P & (P - 1)) == 0;
-  const double invP = 1.0 / Pd;
   const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
-  double u_sys = 0.0;
-  if constexpr (SCHEME == SSM_SYSTEMATIC)  // every lane draws the same value: no barrier
-    u_sys = u ? u[b] : device_uniform(k0, k1, 0u, step, kPurposeSystematic);
+  const double u_sys = SCHEME == SSM_SYSTEMATIC ? K.u_sys : 0.0;
+  __syncwarp();
   const double* U = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * P : nullptr;
   const auto count = [&](uint64_t C) -> int {
     const double Cd = static_cast<double>(C);
@@ -854,7 +872,7 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
   };
 
   // c_{jw-1}: particle jw-1 closes tile tw0-1, so its C is tile tw0's exclusive prefix
-  const uint64_t pre0 = __shfl_sync(0xffffffffu, my_pre, 0);
+  const uint64_t pre0 = s_tile[warp][0].pre;
   int carry = 0;
   if (jw > 0 && jw < P) carry = count(pre0);
   else if (jw >= P) carry = P;
@@ -863,8 +881,9 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
 #pragma unroll
   for (int it = 0; it < kIt; ++it) {
     const int j = jw + it * 32 + lane;
-    const uint64_t pre = __shfl_sync(0xffffffffu, my_pre, it);
-    const double sc = __shfl_sync(0xffffffffu, my_sc, it);
+    const TileInfo ti = s_tile[warp][it];
+    const uint64_t pre = ti.pre;
+    const double sc = ti.sc;
     // particles >= P - 1: the last particle's run ends at P, later ones are empty
     const int c = j < P - 1 ? count(pre + __double2ull_rn(sc * static_cast<double>(qv[it]))) : P;
     const int up = __shfl_up_sync(0xffffffffu, c, 1);
@@ -1468,7 +1487,8 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
   // the others are the same for every P_out (the sharded phases rely on it)
   // sums: tile sums, or the sorted multinomial's (P + 1)-spacing block sums (tiles + 1 per filter)
   tmp.sums = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * (tiles + 1)));
-  tmp.totals = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 3 * static_cast<size_t>(B)));  // + long-run counts
+  // totals, long-run counts, spacing totals, then OffspringConsts (4 words) per filter
+  tmp.totals = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 7 * static_cast<size_t>(B)));
   // cnt doubles as the long-run list of the direct ancestor writer (int4 per run, P_in/32 + 2 per filter)
   const size_t cnt_bytes = sizeof(int32_t) * static_cast<size_t>(B) * P_in;
   const size_t runs_bytes = sizeof(int4) * static_cast<size_t>(B) * long_runs_cap(P_in, P_out);
@@ -1566,7 +1586,9 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
   int4* long_runs = reinterpret_cast<int4*>(w.cnt);
   launch_pdl(tile_scale_kernel, dim3(nblk, B), dim3(kThreads), s, nt, static_cast<const ssm_tile_rec*>(tile_rec), fs,
              scale, pref, blk, long_count, 1);
-  launch_pdl(blk_prefix_kernel, dim3(B), dim3(1024), s, nblk, blk, w.totals, fs);
+  // per-filter offspring constants after the totals / long-run counts / spacing totals
+  OffspringConsts* oc = reinterpret_cast<OffspringConsts*>(w.totals + 3 * static_cast<size_t>(B));
+  launch_pdl(blk_prefix_kernel, dim3(B), dim3(1024), s, nblk, blk, w.totals, fs, oc, P, u, keys, step);
   const dim3 g(scan_tiles(P), B);
   if (scheme == SSM_MULTINOMIAL_SORTED) {  // spacing sums in w.sums (doubles), totals after the u64 totals
     const int nsb = (P + 1 + kScanTile - 1) / kScanTile;
@@ -1582,10 +1604,10 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
   const uint64_t* cl = static_cast<const uint64_t*>(cdf_local);
   if (scheme == SSM_SYSTEMATIC)
     launch_pdl(offspring_tiles_kernel<SSM_SYSTEMATIC>, g, dim3(kThreads), s, P, cl, scale, pref, w.totals, u, keys,
-               step, fs, anc, long_runs, long_count);
+               step, fs, anc, long_runs, long_count, static_cast<const OffspringConsts*>(oc));
   else
     launch_pdl(offspring_tiles_kernel<SSM_STRATIFIED>, g, dim3(kThreads), s, P, cl, scale, pref, w.totals, u, keys,
-               step, fs, anc, long_runs, long_count);
+               step, fs, anc, long_runs, long_count, static_cast<const OffspringConsts*>(oc));
   const int gx = std::max(1, std::min(1184 / B, P / kRunChunk + 1));
   launch_pdl(long_runs_kernel, dim3(gx, B), dim3(kThreads), s, P, P, static_cast<const int4*>(long_runs),
              static_cast<const uint32_t*>(long_count), fs, anc);

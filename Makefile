@@ -12,7 +12,7 @@ LIB       := $(LIB_DIR)/libssm_b200.so
 
 all: $(LIB)
 
-build/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/ssm_common.cuh include/ssm_b200.h
+build/%.o: $(SRC_DIR)/%.cu $(wildcard $(SRC_DIR)/*.cuh) include/ssm_b200.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

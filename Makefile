@@ -18,7 +18,7 @@ build/%.o: $(SRC_DIR)/%.cu $(wildcard $(SRC_DIR)/*.cuh) include/ssm_b200.h
 
 $(LIB): $(OBJS)
 	@mkdir -p $(LIB_DIR)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lnvrtc
 
 clean:
 	rm -rf build $(LIB)

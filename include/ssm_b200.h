@@ -28,8 +28,10 @@
 #ifndef SSM_B200_H
 #define SSM_B200_H
 
+#ifndef __CUDACC_RTC__ /* the NVRTC-compiled generic-model kernels include this header too */
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -44,10 +46,12 @@ typedef enum {
 
 typedef enum { SSM_F32 = 0, SSM_F64 = 1 } ssm_dtype;
 
-/* model ids: the two hand-written model kernels */
+/* model ids: the two hand-written model kernels, and any other model lowered
+ * from a reference ModelIr and compiled at run time (ssm_gen_compile) */
 typedef enum {
-  SSM_MODEL_LORENZ96 = 0,  /* Lorenz96.bi  (8 slots, RK4, Wiener noise) */
-  SSM_MODEL_WINDKESSEL = 1 /* Windkessel.bi (1 slot, analytic update, input F) */
+  SSM_MODEL_LORENZ96 = 0,   /* Lorenz96.bi  (8 slots, RK4, Wiener noise) */
+  SSM_MODEL_WINDKESSEL = 1, /* Windkessel.bi (1 slot, analytic update, input F) */
+  SSM_MODEL_GENERIC = 2     /* ssm_pw_args.gen: a handle from ssm_gen_compile */
 } ssm_model;
 
 /* resampling schemes, resampling.py:12 SCHEMES */
@@ -91,7 +95,10 @@ typedef struct ssm_filter_state {
   int32_t err_nonfinite;  /* min(step*64 + sub-step) with a non-finite state, else INT32_MAX */
   int32_t err_degenerate; /* min(step) with a non-finite LSE increment, else INT32_MAX */
   uint32_t blocks_done;   /* completion counter for the fused finalize (reset by the kernel) */
-  int32_t pad[3];
+  int32_t err_param;      /* generic models: min(step*64 + sub-step) where a distribution
+                             argument was invalid (DistributionParameterError,
+                             distributions.py:53-69), else INT32_MAX */
+  int32_t pad[2];
 } ssm_filter_state;
 
 /* Arguments of the fused propagate + weight step (kernels K1/K2).
@@ -136,6 +143,9 @@ typedef struct ssm_pw_args {
   int32_t x_out_stride; /* row stride of x_out in particles (0: P) */
   void* lse_out;        /* [B][4] doubles or NULL: if set, the finalize writes the LSE/ESS partial
                            (m, c, t, s2) here instead of updating fs (cross-rank combine) */
+  const void* gen;      /* SSM_MODEL_GENERIC: the ssm_gen_compile handle, else NULL */
+  int32_t theta_stride; /* doubles per filter in theta (0: 4, the hand-written kernels) */
+  int32_t gen_pad;
 } ssm_pw_args;
 
 /* hint: subs[0] is the only sub-step and holds exactly one RK4 step (n_ode == 1) */
@@ -159,6 +169,26 @@ int ssm_sm_count(int device, int* out);
 /* K1/K2 fused propagate + weight (+ gather, + LSE/ESS finalize). */
 size_t ssm_pw_workspace_bytes(int B, int P);
 int ssm_propagate_weight(const ssm_pw_args* args, void* stream);
+
+/* Generic models: any reference ModelIr within the limits
+ * below, lowered on the host (paper_1306_3277_b200/codegen.py) to a CUDA
+ * source that defines `gen::Model` and includes csrc/ssm_gen_rt.cuh, then
+ * compiled here for sm_100a with NVRTC and loaded into the current context
+ * (ir.py:83-121 ModelIr, simulate.py:50-193 block semantics).
+ *   ssm_gen_compile: source -> handle (`out`); `include_dir` = the csrc
+ *     directory; `log` (HOST, nullable) receives the NVRTC log.
+ *   ssm_gen_check: compile only (no device needed; used by CPU tests).
+ * The handle is used through ssm_pw_args.gen (model = SSM_MODEL_GENERIC) by
+ * ssm_propagate_weight / ssm_advance, and by ssm_gen_init_particles (the
+ * model's `initial` block on the device).  Limits: n_state <= 32,
+ * n_obs <= 8, n_input <= 1, <= 255 draws per sub-step. */
+int ssm_gen_compile(const char* source, const char* include_dir, void** out, char* log, size_t log_len);
+int ssm_gen_check(const char* source, const char* include_dir, char* log, size_t log_len);
+int ssm_gen_destroy(void* handle);
+int ssm_gen_info(const void* handle, int* n_state, int* n_draws);
+int ssm_gen_init_particles(const void* handle, int dtype, int B, int P, int p_offset, const uint32_t* keys,
+                           const double* theta, int theta_stride, void* x_out, ssm_filter_state* fs,
+                           void* stream);
 
 /* K7: initial particles (simulate.sample_initial, simulate.py:111-129) drawn
  * on the device: L96 x ~ U(-1,3) (Lorenz96.bi:21), windkessel Pp ~ N(90,15)

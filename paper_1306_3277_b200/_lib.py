@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libssm_b200.so")
 
 SSM_OK, SSM_ERR_INVALID_ARG, SSM_ERR_CUDA, SSM_ERR_UNSUPPORTED = 0, 1, 2, 3
 SSM_F32, SSM_F64 = 0, 1
-SSM_MODEL_LORENZ96, SSM_MODEL_WINDKESSEL = 0, 1
+SSM_MODEL_LORENZ96, SSM_MODEL_WINDKESSEL, SSM_MODEL_GENERIC = 0, 1, 2
 SCHEME_IDS = {"multinomial": 0, "stratified": 1, "systematic": 2}
 SSM_MULTINOMIAL_SORTED = 3  # device-noise multinomial, ancestors in ascending order
 SSM_FLAG_BAD_WEIGHT, SSM_FLAG_ZERO_TOTAL = 1, 2
@@ -59,7 +59,8 @@ FILTER_STATE_DTYPE = np.dtype(
         ("err_nonfinite", "<i4"),
         ("err_degenerate", "<i4"),
         ("blocks_done", "<u4"),
-        ("pad", "<i4", (3,)),
+        ("err_param", "<i4"),
+        ("pad", "<i4", (2,)),
     ]
 )
 assert FILTER_STATE_DTYPE.itemsize == 64
@@ -101,6 +102,9 @@ class PwArgs(C.Structure):
         ("x_in_stride", C.c_int32),
         ("x_out_stride", C.c_int32),
         ("lse_out", C.c_void_p),
+        ("gen", C.c_void_p),
+        ("theta_stride", C.c_int32),
+        ("gen_pad", C.c_int32),
     ]
 
 
@@ -203,12 +207,18 @@ SIGNATURES = {
     "ssm_event_create": (_i, [C.POINTER(C.c_void_p)]),
     "ssm_event_destroy": (_i, [_vp]),
     "ssm_event_elapsed_ms": (_i, [_vp, _vp, C.POINTER(C.c_float)]),
+    "ssm_gen_compile": (_i, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, _sz]),
+    "ssm_gen_check": (_i, [C.c_char_p, C.c_char_p, C.c_char_p, _sz]),
+    "ssm_gen_destroy": (_i, [_vp]),
+    "ssm_gen_info": (_i, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ssm_gen_init_particles": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp]),
 }
 
 # entry points that launch kernels (for the gpu_launches count): name -> launches
 LAUNCHING = {
     "ssm_propagate_weight": 1,
     "ssm_init_particles": 1,
+    "ssm_gen_init_particles": 1,
     "ssm_lse_combine": 1,
     "ssm_weights_scan": 1,
     "ssm_fixed_to_cum": 1,

@@ -1,0 +1,490 @@
+"""Generic models on the device path: a reference `ModelIr`
+lowered to a JSON-able description, then to a CUDA source compiled at run
+time (NVRTC, csrc/ssm_gen.cu) -- LibBi's own design.
+
+Lowering (`lower`) walks the IR the reference builds (core/ir.py:83-121,
+291-347): for the `initial`, `transition` and `observation` blocks it records
+every statement unrolled over its dim loop, with expressions as small trees
+resolved to role slots exactly as ir.py:151-193 does:
+
+    ["num", v] | ["T", k] | ["X", k] | ["W", k] | ["U", k] | ["neg", e]
+    | ["bin", op, l, r] | ["call", name, [args]]
+
+From the trees:
+  * `numpy_source` prints the reference's own expression source
+    (ir.py:170-193, e.g. "((X[:, 7] * (X[:, 1] - X[:, 6])) - X[:, 0])"), used
+    for host-side evaluation with the reference's semantics;
+  * `cuda_source` emits `gen::Model` -- the transition sub-step, the
+    observation log-density and the initial block for one particle -- in the
+    reference's evaluation order (statement order; every slot of a statement
+    evaluated before any is written, simulate.py:62-68; RK4 as
+    simulate.py:71-93; log-densities as distributions.py:94-123), with every
+    arithmetic op individually rounded under `E` (exact mode).
+
+Limits of the device path: n_state <= 32, n_obs <= 8, n_input <= 1.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+
+from .errors import UnsupportedModelError
+
+MAX_STATE, MAX_OBS, MAX_INPUT = 32, 8, 1
+
+# distributions.py:33-46 (canonical argument order and defaults)
+DIST_PARAMS = {
+    "gaussian": ("mean", "sd"),
+    "normal": ("mean", "sd"),
+    "truncated_gaussian": ("mean", "sd", "lower", "upper"),
+    "gamma": ("shape", "scale"),
+    "inverse_gamma": ("shape", "scale"),
+    "uniform": ("lower", "upper"),
+    "wiener": (),
+}
+DIST_DEFAULTS = {"truncated_gaussian": {"lower": -math.inf, "upper": math.inf}}
+KIND_OF = {"normal": "gaussian"}
+ROLE_KEY = {"param": "T", "state": "X", "noise": "W", "input": "U"}
+FN_NUMPY = {"exp": "np.exp", "sqrt": "np.sqrt", "sin": "np.sin", "pow": "np.power", "mod": "np.mod"}
+LOG_SQRT_2PI = 0.5 * np.log(2.0 * np.pi)  # distributions.py:15
+
+
+# ---------------------------------------------------------------------------
+# lowering (reference IR, duck-typed) -> description
+# ---------------------------------------------------------------------------
+
+
+def _resolve_index(dim, ix, binding):
+    """ir.py:124-135"""
+    value = ix.offset if ix.var is None else binding[ix.var] + ix.offset
+    if dim.boundary == "cyclic":
+        return value % dim.size
+    if not 0 <= value < dim.size:
+        raise UnsupportedModelError(f"index {value} out of range for dim {dim.name}")
+    return value
+
+
+def _resolve_slot(var, indices, binding):
+    """ir.py:138-146"""
+    flat = 0
+    for dim, ix in zip(var.dims, indices):
+        flat = flat * dim.size + _resolve_index(dim, ix, binding)
+    return var.offset + flat
+
+
+def _expr(node, consts, vars_, binding):
+    kind = type(node).__name__
+    if kind == "Num":
+        return ["num", float(node.value)]
+    if kind == "VarRef":
+        if node.name in consts:
+            return ["num", float(consts[node.name])]
+        var = vars_[node.name]
+        return [ROLE_KEY[var.role], _resolve_slot(var, node.indices, binding)]
+    if kind == "Unary":
+        return ["neg", _expr(node.operand, consts, vars_, binding)]
+    if kind == "Binary":
+        return ["bin", node.op, _expr(node.left, consts, vars_, binding), _expr(node.right, consts, vars_, binding)]
+    if kind == "Call":
+        if node.name not in FN_NUMPY:
+            raise UnsupportedModelError(f"function {node.name!r}")
+        return ["call", node.name, [_expr(a, consts, vars_, binding) for a in node.args]]
+    raise UnsupportedModelError(f"expression node {kind}")
+
+
+def _dist_args(dist):
+    """ir.py:226-245: canonical arguments with defaults."""
+    name = dist.name
+    if name not in DIST_PARAMS:
+        raise UnsupportedModelError(f"distribution {name!r}")
+    params = DIST_PARAMS[name]
+    by_name = dict(zip(params, dist.args))
+    by_name.update(dict(dist.named))
+    out = []
+    for p in params:
+        if p in by_name:
+            out.append(by_name[p])
+        else:
+            out.append(("default", DIST_DEFAULTS[name][p]))
+    return KIND_OF.get(name, name), out
+
+
+def _lower_op(op, ir):
+    consts, vars_ = ir.consts, ir.vars
+    cls = type(op).__name__
+    if cls == "SampleStmtOp":
+        kind, arg_nodes = _dist_args(op.stmt.dist)
+        args = []
+        for b in op.bindings:
+            row = []
+            for a in arg_nodes:
+                row.append(["num", float(a[1])] if isinstance(a, tuple) else _expr(a, consts, vars_, b))
+            args.append(row)
+        return {"op": "sample", "role": op.role, "kind": kind, "slots": list(op.slots), "args": args}
+    if cls == "AssignStmtOp":
+        return {"op": "assign", "role": op.role, "slots": list(op.slots),
+                "exprs": [_expr(op.stmt.expr, consts, vars_, b) for b in op.bindings]}
+    if cls == "OdeOp":
+        if str(op.alg).upper() != "RK4":
+            raise UnsupportedModelError(f"ode alg {op.alg!r}")
+        return {"op": "ode", "slots": list(op.slots), "h": float(op.h),
+                "exprs": [_expr(eq.expr, consts, vars_, b) for eq, b in op.items]}
+    raise UnsupportedModelError(f"statement {cls}")
+
+
+THETA_BLOCKS = ("parameter", "proposal_parameter", "proposal_initial")
+
+
+def fingerprint(ir) -> str:
+    """Digest of every block of a reference ModelIr, lowered (including the
+    theta-level blocks the hand-written specs implement on the host)."""
+    d = {"name": ir.name, "counts": {k: int(v) for k, v in ir.counts.items()},
+         "delta": None if ir.delta is None else float(ir.delta)}
+    for name in ("initial", "transition", "observation") + THETA_BLOCKS:
+        blk = ir.block(name)
+        d[name] = [] if blk is None else [_lower_op(op, ir) for op in blk.ops]
+    return hashlib.sha256(dumps(d).encode()).hexdigest()
+
+
+def lower(ir) -> dict:
+    """Reference ModelIr -> JSON-able description (the codegen input)."""
+    counts = {k: int(v) for k, v in ir.counts.items()}
+    if counts["state"] > MAX_STATE or counts["obs"] > MAX_OBS or counts["input"] > MAX_INPUT:
+        raise UnsupportedModelError(
+            f"{ir.name}: device path limits are n_state <= {MAX_STATE}, n_obs <= {MAX_OBS}, n_input <= {MAX_INPUT}")
+    out = {"name": ir.name, "counts": counts, "delta": None if ir.delta is None else float(ir.delta)}
+    for name in ("initial", "transition", "observation"):
+        blk = ir.block(name)
+        out[name] = [] if blk is None else [_lower_op(op, ir) for op in blk.ops]
+    for op in out["observation"]:
+        if op["op"] != "sample" or op["kind"] == "wiener":
+            raise UnsupportedModelError("observation block: distribution statements only")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# expression printers
+# ---------------------------------------------------------------------------
+
+
+def numpy_source(e) -> str:
+    """The reference's expression source (ir.py:170-193)."""
+    t = e[0]
+    if t == "num":
+        return repr(e[1])
+    if t == "U":
+        return f"U[{e[1]}]"
+    if t in ("T", "X", "W"):
+        return f"{t}[:, {e[1]}]"
+    if t == "neg":
+        return f"(-{numpy_source(e[1])})"
+    if t == "bin":
+        return f"({numpy_source(e[2])} {e[1]} {numpy_source(e[3])})"
+    if t == "call":
+        return f"{FN_NUMPY[e[1]]}({', '.join(numpy_source(a) for a in e[2])})"
+    raise ValueError(e)
+
+
+def numpy_fn(e):
+    """lambda T, X, W, U evaluating the expression like ir.py:196-198 (the
+    `inf` default of truncated bounds is made evaluable)."""
+    return eval(f"lambda T, X, W, U: {numpy_source(e)}", {"np": np, "inf": np.inf, "__builtins__": {}})
+
+
+def _is_const(e):
+    t = e[0]
+    if t == "num":
+        return True
+    if t in ("T", "X", "W", "U"):
+        return False
+    if t == "neg":
+        return _is_const(e[1])
+    if t == "bin":
+        return _is_const(e[2]) and _is_const(e[3])
+    return all(_is_const(a) for a in e[2])
+
+
+def _const_value(e):
+    z = np.zeros((1, 1))
+    return float(np.asarray(numpy_fn(e)(z, z, z, np.zeros(1))).reshape(-1)[0])
+
+
+def _lit(v: float) -> str:
+    if math.isnan(v):
+        return "T(CUDART_NAN)"
+    if math.isinf(v):
+        return "T(CUDART_INF)" if v > 0 else "T(-CUDART_INF)"
+    return f"T({float(v).hex()})"
+
+
+def _dlit(v: float) -> str:
+    if math.isinf(v):
+        return "CUDART_INF" if v > 0 else "(-CUDART_INF)"
+    return float(v).hex()
+
+
+_OPS = {"+": "add", "-": "sub", "*": "mul", "/": "div"}
+
+
+def cuda_expr(e, xname="X") -> str:
+    """C++ expression of type T (numpy float64 semantics under E: one rounding per op)."""
+    t = e[0]
+    if t == "num":
+        return _lit(e[1])
+    if t == "T":
+        return f"T(TH[{e[1]}])"
+    if t == "X":
+        return f"{xname}[{e[1]}]"
+    if t == "W":
+        return f"W[{e[1]}]"
+    if t == "U":
+        return f"T(U[{e[1]}])"
+    if t == "neg":
+        return f"(-{cuda_expr(e[1], xname)})"
+    if t == "bin":
+        return f"O::{_OPS[e[1]]}({cuda_expr(e[2], xname)}, {cuda_expr(e[3], xname)})"
+    if t == "call":
+        args = [cuda_expr(a, xname) for a in e[2]]
+        fn = {"exp": "exp", "sqrt": "sqrt", "sin": "sin", "pow": "pow", "mod": "ssm::py_mod"}[e[1]]
+        return f"{fn}({', '.join(args)})"
+    raise ValueError(e)
+
+
+# ---------------------------------------------------------------------------
+# CUDA source
+# ---------------------------------------------------------------------------
+
+
+class _Emitter:
+    def __init__(self):
+        self.lines = []
+        self.ind = 2
+
+    def __call__(self, s=""):
+        self.lines.append(" " * self.ind + s if s else "")
+
+    def block(self, head, comment=None):
+        self(head + " {" + (f"  // {comment}" if comment else ""))
+        self.ind += 2
+
+    def end(self, tail="}"):
+        self.ind -= 2
+        self(tail)
+
+
+def _sample_value(em, kind, args, kd, tmp, dname="d"):
+    """Emit `T tmp = <draw of `kind` with args>` (simulate.py:50-60, distributions.py:73-91)."""
+    if kind == "wiener":  # rng.normal(0.0, sqrt(d)): 0.0 + sd z
+        em(f"const T {tmp} = O::add(T(0.0), O::mul(T(sqrt({dname})), dr.normal({kd})));")
+    elif kind == "gaussian":  # rng.normal(mean, sd): mean + sd z
+        em(f"const T {tmp}_m = {args[0]}, {tmp}_s = {args[1]};")
+        em(f"if (!({tmp}_s > T(0))) perr = true;")
+        em(f"const T {tmp} = O::add({tmp}_m, O::mul({tmp}_s, dr.normal({kd})));")
+    elif kind == "uniform":  # rng.uniform(lo, hi): lo + (hi - lo) U
+        em(f"const T {tmp}_a = {args[0]}, {tmp}_b = {args[1]};")
+        em(f"if (!({tmp}_a < {tmp}_b)) perr = true;")
+        em(f"const T {tmp} = O::add({tmp}_a, O::mul(O::sub({tmp}_b, {tmp}_a), dr.uniform({kd})));")
+    elif kind == "truncated_gaussian":  # mean + sd ndtri(fa + u (fb - fa)), distributions.py:78-84
+        em(f"const double {tmp}_m = {args[0]}, {tmp}_s = {args[1]}, {tmp}_lo = {args[2]}, {tmp}_hi = {args[3]};")
+        em(f"const double {tmp}_fa = normcdf(({tmp}_lo - {tmp}_m) / {tmp}_s), "
+           f"{tmp}_fb = normcdf(({tmp}_hi - {tmp}_m) / {tmp}_s);")
+        em(f"if (!({tmp}_s > 0.0) || !({tmp}_lo < {tmp}_hi) || !({tmp}_fb - {tmp}_fa > 0.0)) perr = true;")
+        em(f"const T {tmp} = T({tmp}_m + {tmp}_s * normcdfinv({tmp}_fa + double(dr.uniform({kd})) * "
+           f"({tmp}_fb - {tmp}_fa)));")
+    elif kind == "gamma":  # rng.gamma(shape, scale) = scale * standard_gamma(shape)
+        em(f"const double {tmp}_k = {args[0]}, {tmp}_t = {args[1]};")
+        em(f"if (!({tmp}_k > 0.0) || !({tmp}_t > 0.0)) perr = true;")
+        em(f"const T {tmp} = T({tmp}_t * dr.std_gamma({kd}, {tmp}_k));")
+    elif kind == "inverse_gamma":  # 1 / rng.gamma(shape, 1 / scale)
+        em(f"const double {tmp}_k = {args[0]}, {tmp}_t = {args[1]};")
+        em(f"if (!({tmp}_k > 0.0) || !({tmp}_t > 0.0)) perr = true;")
+        em(f"const T {tmp} = T(1.0 / ((1.0 / {tmp}_t) * dr.std_gamma({kd}, {tmp}_k)));")
+    else:
+        raise UnsupportedModelError(f"cannot sample {kind}")
+
+
+def _d(e):
+    """double-typed argument (truncated/gamma draws compute in float64)"""
+    return f"double({cuda_expr(e)})"
+
+
+def _emit_statements(em, ops, roles, dname="d"):
+    """Statements of a block in order; returns the number of draws used."""
+    kd = 0
+    for si, op in enumerate(ops):
+        if op["op"] == "sample":
+            em.block("", f"statement {si}: sample ({op['kind']}) -> {op['role']} {op['slots']}")
+            for j, args in enumerate(op["args"]):
+                if op["kind"] in ("truncated_gaussian", "gamma", "inverse_gamma"):
+                    a = [_d(x) for x in args]
+                else:
+                    a = [cuda_expr(x) for x in args]
+                _sample_value(em, op["kind"], a, kd, f"v{j}", dname)
+                kd += 1
+            for j, slot in enumerate(op["slots"]):
+                em(f"{roles[op['role']]}[{slot}] = v{j};")
+            em.end()
+        elif op["op"] == "assign":
+            em.block("", f"statement {si}: assign -> {op['role']} {op['slots']}")
+            for j, ex in enumerate(op["exprs"]):
+                em(f"const T v{j} = {cuda_expr(ex)};")
+            for j, slot in enumerate(op["slots"]):
+                em(f"{roles[op['role']]}[{slot}] = v{j};")
+            em.end()
+        else:  # ode, simulate.py:71-93
+            m = len(op["slots"])
+            em.block("", f"statement {si}: ode RK4 h={op['h']!r} over X{op['slots']}")
+            em(f"constexpr double H = {_dlit(op['h'])};")
+            em(f"const int n_steps = max(1, int(ceil({dname} / H - 1e-9)));")
+            em("auto deriv = [&](const T (&stg)[%d], T (&out)[%d]) {" % (m, m))
+            em("  T Xs[NX];")
+            em("  for (int i = 0; i < NX; ++i) Xs[i] = X[i];")
+            for j, slot in enumerate(op["slots"]):
+                em(f"  Xs[{slot}] = stg[{j}];")
+            for j, ex in enumerate(op["exprs"]):
+                em(f"  out[{j}] = {cuda_expr(ex, 'Xs')};")
+            em("};")
+            em.block("for (int kk = 0; kk < n_steps; ++kk)")
+            em(f"const double s_ = fmin(H, {dname} - double(kk) * H);")
+            em("const T s = T(s_);")
+            em("const T hs = O::mul(T(0.5), s);  // `0.5 * s * k` == (0.5*s)*k")
+            em(f"T y0[{m}], k1[{m}], k2[{m}], k3[{m}], k4[{m}], st[{m}];")
+            for j, slot in enumerate(op["slots"]):
+                em(f"y0[{j}] = X[{slot}];")
+            em("deriv(y0, k1);")
+            em(f"for (int j = 0; j < {m}; ++j) st[j] = O::add(y0[j], O::mul(hs, k1[j]));")
+            em("deriv(st, k2);")
+            em(f"for (int j = 0; j < {m}; ++j) st[j] = O::add(y0[j], O::mul(hs, k2[j]));")
+            em("deriv(st, k3);")
+            em(f"for (int j = 0; j < {m}; ++j) st[j] = O::add(y0[j], O::mul(s, k3[j]));")
+            em("deriv(st, k4);")
+            em("const T s6 = O::div(s, T(6.0));")
+            for j, slot in enumerate(op["slots"]):
+                em(f"X[{slot}] = O::add(y0[{j}], O::mul(s6, O::add(O::add(O::add(k1[{j}], "
+                   f"O::mul(T(2.0), k2[{j}])), O::mul(T(2.0), k3[{j}])), k4[{j}])));")
+            em.end()
+            em.end()
+    return kd
+
+
+def _emit_logpdf(em, kind, args, y, tmp):
+    """`T tmp` = log-density (distributions.py:94-123); args are expression trees."""
+    if kind == "gaussian":
+        m, sd = cuda_expr(args[0]), cuda_expr(args[1])
+        logsd = _lit(float(np.log(_const_value(args[1])))) if _is_const(args[1]) else f"T(log(double({tmp}_s)))"
+        em(f"const T {tmp}_s = {sd};")
+        em(f"if (!({tmp}_s > T(0))) perr = true;")
+        em(f"const T {tmp}_z = O::div(O::sub({y}, {m}), {tmp}_s);")
+        em(f"const T {tmp} = O::sub(O::sub(O::mul(O::mul(T(-0.5), {tmp}_z), {tmp}_z), {logsd}), "
+           f"{_lit(LOG_SQRT_2PI)});")
+    elif kind == "truncated_gaussian":
+        a = [_d(x) for x in args]
+        em(f"const double {tmp}_m = {a[0]}, {tmp}_s = {a[1]}, {tmp}_lo = {a[2]}, {tmp}_hi = {a[3]};")
+        em(f"const double {tmp}_fa = normcdf(({tmp}_lo - {tmp}_m) / {tmp}_s), "
+           f"{tmp}_fb = normcdf(({tmp}_hi - {tmp}_m) / {tmp}_s);")
+        em(f"if (!({tmp}_s > 0.0) || !({tmp}_fb - {tmp}_fa > 0.0)) perr = true;")
+        em(f"const double {tmp}_z = (double({y}) - {tmp}_m) / {tmp}_s;")
+        em(f"const double {tmp}_c = -0.5 * {tmp}_z * {tmp}_z - log({tmp}_s) - {_dlit(LOG_SQRT_2PI)} "
+           f"- log({tmp}_fb - {tmp}_fa);")
+        em(f"const T {tmp} = (double({y}) >= {tmp}_lo && double({y}) <= {tmp}_hi) ? T({tmp}_c) : T(-CUDART_INF);")
+    elif kind == "gamma":
+        a = [_d(x) for x in args]
+        em(f"const double {tmp}_k = {a[0]}, {tmp}_t = {a[1]}, {tmp}_x = double({y});")
+        em(f"if (!({tmp}_k > 0.0) || !({tmp}_t > 0.0)) perr = true;")
+        em(f"const T {tmp} = {tmp}_x > 0.0 ? T(((({tmp}_k - 1.0) * log({tmp}_x)) - ({tmp}_x / {tmp}_t)) "
+           f"- ({tmp}_k * log({tmp}_t)) - lgamma({tmp}_k)) : T(-CUDART_INF);")
+    elif kind == "inverse_gamma":
+        a = [_d(x) for x in args]
+        em(f"const double {tmp}_k = {a[0]}, {tmp}_t = {a[1]}, {tmp}_x = double({y});")
+        em(f"if (!({tmp}_k > 0.0) || !({tmp}_t > 0.0)) perr = true;")
+        em(f"const T {tmp} = {tmp}_x > 0.0 ? T((({tmp}_k * log({tmp}_t)) - lgamma({tmp}_k)) "
+           f"- (({tmp}_k + 1.0) * log({tmp}_x)) - ({tmp}_t / {tmp}_x)) : T(-CUDART_INF);")
+    elif kind == "uniform":
+        a = [_d(x) for x in args]
+        em(f"const double {tmp}_a = {a[0]}, {tmp}_b = {a[1]}, {tmp}_x = double({y});")
+        em(f"if (!({tmp}_a < {tmp}_b)) perr = true;")
+        em(f"const T {tmp} = ({tmp}_x >= {tmp}_a && {tmp}_x <= {tmp}_b) ? T(-log({tmp}_b - {tmp}_a)) "
+           f": T(-CUDART_INF);")
+    else:
+        raise UnsupportedModelError(f"observation density {kind}")
+
+
+def transition_draws(desc):
+    """Per transition sub-step: the draw kinds in kernel order (kd = index)."""
+    return [op["kind"] for op in desc["transition"] if op["op"] == "sample" for _ in op["slots"]]
+
+
+def cuda_source(desc: dict) -> str:
+    c = desc["counts"]
+    nx, nw = c["state"], c["noise"]
+    roles = {"state": "X", "noise": "W", "param": "TH_", "input": "U_"}
+    em = _Emitter()
+    em.ind = 0
+    em(f"// generated by paper_1306_3277_b200/codegen.py from model {desc['name']!r}")
+    em('#include "ssm_gen_rt.cuh"')
+    em("namespace gen {")
+    em("struct Model {")
+    em.ind = 2
+    kdraw = len(transition_draws(desc))
+    em(f"static constexpr int NX = {nx}, NW = {nw}, NWB = {max(nw, 1)}, KDRAW = {max(kdraw, 1)};")
+    # transition sub-step
+    em("template <typename T, bool E>")
+    em.block("__device__ static void substep(T (&X)[NX], T (&W)[NWB], const double* TH, const double* U, "
+             "double d, const ssm::GenDraws<T>& dr, bool& perr)")
+    em("using O = ssm::Ar<T, E>;")
+    em("(void)W; (void)TH; (void)U; (void)d; (void)dr; (void)perr;")
+    for op in desc["transition"]:
+        if op["op"] != "ode" and op["role"] not in ("state", "noise"):
+            raise UnsupportedModelError(f"transition statement writing a {op['role']} variable")
+    _emit_statements(em, desc["transition"], roles)
+    em.end()
+    # observation
+    em("template <typename T, bool E>")
+    em.block("__device__ static T obs_logpdf(const T (&X)[NX], const T (&W)[NWB], const double* TH, "
+             "const double* U, const double* Y, unsigned mask, bool& perr)")
+    em("using O = ssm::Ar<T, E>;")
+    em("(void)X; (void)W; (void)TH; (void)U; (void)Y; (void)perr;")
+    em("T total = T(0);")
+    for si, op in enumerate(desc["observation"]):
+        for j, (slot, args) in enumerate(zip(op["slots"], op["args"])):
+            em.block(f"if (mask & (1u << {slot}))")
+            _emit_logpdf(em, op["kind"], args, f"T(Y[{slot}])", f"g{si}_{j}")
+            em(f"total = O::add(total, g{si}_{j});")
+            em.end()
+    em("return total;")
+    em.end()
+    # initial block
+    em("template <typename T, bool E>")
+    em.block("__device__ static void initial(T (&X)[NX], const double* TH, const ssm::GenDraws<T>& dr, bool& perr)")
+    em("using O = ssm::Ar<T, E>;")
+    em("(void)TH; (void)dr; (void)perr;")
+    em("T W[NWB] = {};")
+    em("const double U[1] = {0.0};")
+    em("(void)W; (void)U;")
+    for op in desc["initial"]:
+        if op["op"] == "ode" or op["role"] != "state":
+            raise UnsupportedModelError("initial block: state sample/assign statements only")
+    _emit_statements(em, desc["initial"], roles)
+    em.end()
+    em.ind = 0
+    em("};")
+    em("}  // namespace gen")
+    em(f'extern "C" __device__ int ssm_gen_model_info[2] = {{{nx}, {max(kdraw, 1)}}};')
+    return "\n".join(em.lines) + "\n"
+
+
+def include_dir() -> str:
+    return os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc")
+
+
+def source_digest(src: str) -> str:
+    return hashlib.sha256(src.encode()).hexdigest()[:16]
+
+
+def dumps(desc) -> str:
+    return json.dumps(desc, sort_keys=True)

@@ -13,7 +13,9 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int B = A->pw.B, P = A->pw.P;
   const size_t esz = A->pw.dtype == SSM_F64 ? 8 : 4;
-  const int nx = A->pw.model == SSM_MODEL_LORENZ96 ? 8 : 1;
+  const int nx = A->pw.model == SSM_MODEL_GENERIC ? ssm_gen_nx(A->pw.gen)
+                 : (A->pw.model == SSM_MODEL_LORENZ96 ? 8 : 1);
+  if (nx <= 0) return SSM_ERR_INVALID_ARG;
   const size_t xstep = static_cast<size_t>(B) * nx * P * esz;
   const size_t astep = static_cast<size_t>(B) * P * esz;
   const size_t ancstep = static_cast<size_t>(B) * P;

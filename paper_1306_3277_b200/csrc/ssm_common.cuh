@@ -1,9 +1,18 @@
 // Shared device helpers for libssm_b200 (sm_100a).
 #pragma once
 
+#ifdef __CUDACC_RTC__  // NVRTC (generic-model kernels): no system headers
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+#define CUDART_INF __longlong_as_double(0x7ff0000000000000ULL)
+#define CUDART_NAN __longlong_as_double(0xfff8000000000000ULL)
+#else
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#endif
 
 #include "../../include/ssm_b200.h"
 
@@ -57,6 +66,7 @@ enum Purpose : uint32_t {
   kPurposeInit = 3u,
   kPurposeSystematic = 4u,
   kPurposeSpacing = 5u,  // exponential spacings of the sorted multinomial
+  kPurposeGen = 6u,      // generic-model draws (ssm_gen_rt.cuh); bits 8+ carry a retry index
 };
 
 // 53-bit uniform in [0,1) from two 32-bit words (same construction as numpy's
@@ -234,6 +244,8 @@ __device__ __forceinline__ bool finite(T v) {
 // transitive along the chain).  A no-op when launched without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+#ifndef __CUDACC_RTC__
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -249,10 +261,16 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, c
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+#endif  // __CUDACC_RTC__
+
 }  // namespace ssm
 
+#ifndef __CUDACC_RTC__
 // error reporting helper shared by the C-ABI entry points
 extern "C" void ssm_set_last_error(cudaError_t e);
+// generic models (ssm_gen.cu)
+int ssm_gen_propagate_weight(const ssm_pw_args& A, cudaStream_t s);
+int ssm_gen_nx(const void* handle);
 #define SSM_CHECK_LAUNCH()                      \
   do {                                          \
     cudaError_t _e = cudaGetLastError();        \
@@ -261,3 +279,4 @@ extern "C" void ssm_set_last_error(cudaError_t e);
       return SSM_ERR_CUDA;                      \
     }                                           \
   } while (0)
+#endif  // __CUDACC_RTC__

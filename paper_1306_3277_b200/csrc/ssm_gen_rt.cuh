@@ -1,0 +1,231 @@
+// Generic-model kernels.  Compiled at run time by NVRTC
+// (csrc/ssm_gen.cu) together with a generated `gen::Model`, which
+// paper_1306_3277_b200/codegen.py lowers from a reference ModelIr
+// (core/ir.py:83-121).  The generated model provides, per particle:
+//
+//   NX, NW, NWB (= max(NW, 1)), KDRAW (draws per transition sub-step)
+//   substep<T, E>(X, W, TH, U, d, draws, perr)  one transition sub-step
+//        (simulate.py:132-163: the block's statements in order, sample /
+//         assign / RK4 ode, with the reference's op order under E)
+//   obs_logpdf<T, E>(X, W, TH, U, Y, mask, perr) sum over present obs slots
+//        (simulate.py:166-193, distributions.py:94-123)
+//   initial<T, E>(X, TH, draws, perr)            the initial block
+//        (simulate.py:111-129)
+//
+// The kernels below are the generic counterparts of pw_kernel / init_kernel:
+// the same ancestor gather, software pipeline, warp-tile weighting and fused
+// LSE/ESS finalize (ssm_tile.cuh), so resampling downstream is shared.
+#pragma once
+
+#include "ssm_tile.cuh"
+
+namespace ssm {
+
+// np.mod on floats (numpy npy_divmod): the result takes the divisor's sign
+template <typename T>
+__device__ __forceinline__ T py_mod(T a, T b) {
+  T m = fmod(a, b);
+  if (b == T(0)) return m;
+  if (m != T(0)) {
+    if ((b < T(0)) != (m < T(0))) m += b;
+  } else {
+    m = copysign(T(0), b);
+  }
+  return m;
+}
+
+// Draws of one (particle, grid step, sub-step).  Device mode: Philox4x32-10
+// counter {particle, step, sub << 8 | draw, kPurposeGen | retry << 8}; injected
+// mode (noise="host"): the reference's standard variates, [KDRAW][P] per sub-step.
+template <typename T>
+struct GenDraws {
+  uint32_t k0, k1, pg, step, sub;
+  const T* inj;
+  int P, p;
+
+  __device__ __forceinline__ U4 block(int kd, uint32_t retry) const {
+    return philox4x32_10(U4{pg, step, (sub << 8) | static_cast<uint32_t>(kd), kPurposeGen | (retry << 8)}, k0, k1);
+  }
+  // standard normal z (numpy normal(loc, scale) = loc + scale z)
+  __device__ __forceinline__ T normal(int kd) const {
+    if (inj) return inj[static_cast<size_t>(kd) * P + p];
+    const U4 r = block(kd, 0u);
+    float z0, z1;
+    box_muller(r.x, r.y, z0, z1);
+    return static_cast<T>(z0);
+  }
+  // U[0,1) (numpy uniform(low, high) = low + (high - low) U)
+  __device__ __forceinline__ T uniform(int kd) const {
+    if (inj) return inj[static_cast<size_t>(kd) * P + p];
+    const U4 r = block(kd, 0u);
+    return static_cast<T>(u53(r.x, r.y));
+  }
+  // standard gamma(shape) by Marsaglia-Tsang (device draws only); shape < 1
+  // through gamma(shape + 1) U^(1/shape)
+  __device__ __forceinline__ double std_gamma(int kd, double shape) const {
+    double boost = 1.0;
+    if (shape < 1.0) {
+      const U4 r = block(kd, 0u);
+      boost = pow(1.0 - u53(r.z, r.w), 1.0 / shape);
+      shape += 1.0;
+    }
+    const double dd = shape - 1.0 / 3.0, c = 1.0 / sqrt(9.0 * dd);
+    for (uint32_t it = 1; it < 256; ++it) {
+      const U4 r = block(kd, it);
+      float z0, z1;
+      box_muller(r.x, r.y, z0, z1);
+      const double z = z0;
+      double v = 1.0 + c * z;
+      if (v <= 0.0) continue;
+      v = v * v * v;
+      const double u = 1.0 - u53(r.z, r.w);
+      if (log(u) < 0.5 * z * z + dd - dd * v + dd * log(v)) return dd * v * boost;
+    }
+    return dd * boost;  // not reached in practice (acceptance > 0.95 per try)
+  }
+};
+
+template <class M, typename T, bool E, bool INJ>
+__global__ void __launch_bounds__(kPwThreads) gen_pw_kernel(const ssm_pw_args A) {
+  pdl_wait();
+  constexpr int NX = M::NX;
+  const int b = blockIdx.y;
+  const int P = A.P;
+  const int ntiles = (P + kPwThreads - 1) / kPwThreads;
+  ssm_filter_state* fs = A.fs + b;
+  const int R = fs->resample_now;
+  const bool uniform_in = R || fs->uniform;
+  const double incr_prev = fs->incr;
+  const int in_stride = A.x_in_stride > 0 ? A.x_in_stride : P;
+  const T* __restrict__ xin = static_cast<const T*>(A.x_in) + static_cast<size_t>(b) * NX * in_stride;
+  const int out_stride = A.x_out_stride > 0 ? A.x_out_stride : P;
+  T* __restrict__ xout = static_cast<T*>(A.x_out) + static_cast<size_t>(b) * NX * out_stride;
+  const int32_t* __restrict__ anc = (R && A.anc != nullptr) ? A.anc + static_cast<size_t>(b) * P : nullptr;
+  const T* __restrict__ aprev = A.a_prev ? static_cast<const T*>(A.a_prev) + static_cast<size_t>(b) * P : nullptr;
+  T* __restrict__ aout = A.a_out ? static_cast<T*>(A.a_out) + static_cast<size_t>(b) * P : nullptr;
+  uint64_t* __restrict__ cloc =
+      A.cdf_local ? static_cast<uint64_t*>(A.cdf_local) + static_cast<size_t>(b) * P : nullptr;
+  ssm_tile_rec* __restrict__ trec =
+      A.tile_rec ? static_cast<ssm_tile_rec*>(A.tile_rec) + static_cast<size_t>(b) * ((P + 31) >> 5) : nullptr;
+  const T* __restrict__ noise =
+      INJ ? static_cast<const T*>(A.noise) + static_cast<size_t>(b) * A.n_sub * M::KDRAW * P : nullptr;
+  const double* th = A.theta + static_cast<size_t>(A.theta_stride) * b;
+  const uint32_t k0 = (!INJ && A.keys) ? A.keys[2 * b] : 0u, k1 = (!INJ && A.keys) ? A.keys[2 * b + 1] : 0u;
+  const int has_obs = A.has_obs;
+  const T logw0 = static_cast<T>(A.log_w0);
+  const int lane = threadIdx.x & 31;
+  const bool want_ess = A.ess_rel >= 0.0;
+
+  __shared__ double s_exp_tab[64];
+  if (threadIdx.x < 64) s_exp_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
+  __syncthreads();
+  __shared__ ParkedTiles s_park[kPwThreads / 32];
+  WarpTileAcc acc{&s_park[threadIdx.x >> 5], lse_empty(), 0, 0};
+  bool bad = false, perr = false;
+  int bad_sub = 0, perr_sub = 0;
+
+  // software pipeline as pw_kernel: next tile's gathered state in flight
+  T xn[NX];
+  const int stride = gridDim.x * kPwThreads;
+  const int p0 = blockIdx.x * kPwThreads + threadIdx.x;
+  auto load_x = [&](int src) {
+#pragma unroll
+    for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * in_stride + src];
+  };
+  if (p0 < P) load_x(anc ? __ldg(anc + p0) : p0);
+  int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride;
+
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int p = tile * kPwThreads + threadIdx.x;
+    const bool act = p < P;
+    double a_d = -CUDART_INF;
+    T x[NX];
+#pragma unroll
+    for (int n = 0; n < NX; ++n) x[n] = xn[n];
+    {
+      const int p2 = p + stride;
+      if (p2 < P) load_x(anc_next);
+      const int p3 = p2 + stride;
+      anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
+    }
+    if (act) {
+      T w[M::NWB];  // the noise array of step_transition: zeros, then rewritten per sub-step
+#pragma unroll
+      for (int n = 0; n < M::NWB; ++n) w[n] = T(0);
+      for (int k = 0; k < A.n_sub; ++k) {
+        const ssm_substep& S = A.subs[k];
+        const double U[1] = {S.u_in};
+        const GenDraws<T> dr{k0, k1, static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
+                             static_cast<uint32_t>(k), INJ ? noise + static_cast<size_t>(k) * M::KDRAW * P : nullptr,
+                             P, p};
+        bool pe = false;
+        M::template substep<T, E>(x, w, th, U, S.d, dr, pe);
+        if (pe && !perr) {
+          perr = true;
+          perr_sub = k;
+        }
+        if (A.check_finite && !bad) {
+          bool ok = true;
+#pragma unroll
+          for (int n = 0; n < NX; ++n) ok &= isfinite(x[n]);
+          if (!ok) {
+            bad = true;
+            bad_sub = k;
+          }
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * out_stride + p] = x[n];
+      if (has_obs) {
+        T w0[M::NWB];  // observe_logpdf sees a zero noise array (simulate.py:181)
+#pragma unroll
+        for (int n = 0; n < M::NWB; ++n) w0[n] = T(0);
+        const double Uo[1] = {A.u_obs};
+        bool pe = false;
+        const T g = M::template obs_logpdf<T, E>(x, w0, th, Uo, A.y, A.obs_mask, pe);
+        if (pe && !perr) {
+          perr = true;
+          perr_sub = 63;  // the observation density at this step
+        }
+        const T lw = uniform_in ? logw0 : Ar<T, E>::sub(aprev[p], static_cast<T>(incr_prev));
+        const T a = Ar<T, E>::add(lw, g);
+        if (aout) aout[p] = a;
+        a_d = static_cast<double>(a);
+      }
+    }
+    if (!has_obs) continue;  // block-uniform
+    warp_tile_weigh(acc, a_d, act, p, P, lane, s_exp_tab, cloc, trec, want_ess);
+  }
+  warp_tile_flush(acc, lane);
+
+  if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
+  if (perr) atomicMin(&fs->err_param, A.step * 64 + perr_sub);
+  pw_block_finalize<kPwThreads>(A, fs, b, P, R, has_obs, acc.st, lane, kMaxPwBlocks);
+}
+
+// the model's initial block on the device (sample_initial, simulate.py:111-129)
+template <class M, typename T>
+__global__ void __launch_bounds__(kPwThreads)
+    gen_init_kernel(int P, int p_offset, const uint32_t* keys, const double* theta, int theta_stride, T* x,
+                    ssm_filter_state* fs) {
+  constexpr int NX = M::NX;
+  const int b = blockIdx.y;
+  const uint32_t k0 = keys[2 * b], k1 = keys[2 * b + 1];
+  const double* th = theta + static_cast<size_t>(theta_stride) * b;
+  T* xb = x + static_cast<size_t>(b) * NX * P;
+  bool perr = false;
+  for (int p = blockIdx.x * kPwThreads + threadIdx.x; p < P; p += gridDim.x * kPwThreads) {
+    T X[NX];
+#pragma unroll
+    for (int n = 0; n < NX; ++n) X[n] = T(0);
+    const GenDraws<T> dr{k0, k1, static_cast<uint32_t>(p + p_offset), 0u, 0u, nullptr, P, p};
+    bool pe = false;
+    M::template initial<T, true>(X, th, dr, pe);
+    perr |= pe;
+#pragma unroll
+    for (int n = 0; n < NX; ++n) xb[static_cast<size_t>(n) * P + p] = X[n];
+  }
+  if (perr && fs) atomicMin(&fs[b].err_param, 0);
+}
+
+}  // namespace ssm

@@ -18,18 +18,6 @@
 
 namespace ssm {
 
-constexpr int kPwThreads = kThreads;  // fused-kernel block (128 threads x 5 CTAs spills: slower)
-constexpr int kMaxPwBlocks = 2048;  // per filter; a function of P only (determinism)
-
-// Blocks per filter: >= 4 block tiles per block, so each warp folds several warp
-// tiles per setup (matters at moderate P with many filters, e.g. PMMH 8 x 2^16).
-// A function of P only, so the LSE fold order never depends on the batch.
-__host__ __device__ inline int pw_grid_x(int P) {
-  const int tiles = (P + kPwThreads - 1) / kPwThreads;
-  const int g = (tiles + 3) / 4;
-  return g < kMaxPwBlocks ? g : kMaxPwBlocks;
-}
-
 // ----------------------------- noise ---------------------------------------
 
 // Eight standard normals per particle and sub-step: two Philox4x32-10 blocks,
@@ -556,6 +544,7 @@ extern "C" int ssm_propagate_weight(const ssm_pw_args* args, void* stream) {
   if (A.has_obs && !A.a_out) return SSM_ERR_INVALID_ARG;
   if (A.n_sub > 0 && !A.noise && !A.keys) return SSM_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (A.model == SSM_MODEL_GENERIC) return ssm_gen_propagate_weight(A, s);
   if (A.model == SSM_MODEL_LORENZ96) {
     if (A.dtype == SSM_F64)
       launch_pw<SSM_MODEL_LORENZ96, double>(A, s);

@@ -17,6 +17,18 @@
 
 namespace ssm {
 
+constexpr int kPwThreads = kThreads;  // fused-kernel block (128 threads x 5 CTAs spills: slower)
+constexpr int kMaxPwBlocks = 2048;  // per filter; a function of P only (determinism)
+
+// Blocks per filter: >= 4 block tiles per block, so each warp folds several warp
+// tiles per setup (matters at moderate P with many filters, e.g. PMMH 8 x 2^16).
+// A function of P only, so the LSE fold order never depends on the batch.
+__host__ __device__ inline int pw_grid_x(int P) {
+  const int tiles = (P + kPwThreads - 1) / kPwThreads;
+  const int g = (tiles + 3) / 4;
+  return g < kMaxPwBlocks ? g : kMaxPwBlocks;
+}
+
 constexpr double kTileFix = 4503599627370496.0;  // 2^52
 
 // exp(x) for x <= 0 (the tile weights e_j = exp(a_j - m_w)): 2^(j/64) table in

@@ -31,13 +31,14 @@ over the FMA-contracted fast kernels (1e-12 of the reference per step).
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 
 import numpy as np
 import torch
 
 from .. import _lib, profiling
-from ..errors import DegenerateEnsembleError, NonFiniteStateError, UnsupportedModelError
+from ..errors import DegenerateEnsembleError, DistributionParameterError, NonFiniteStateError, UnsupportedModelError
 from ..models import LOG_SQRT_2PI, ModelSpec, resolve_model
 from ..rng import device_keys, first_uniforms
 from .timegrid import as_filter_grid
@@ -151,7 +152,7 @@ class Schedule:
 
 
 def _schedule(grid, spec, inputs, device):
-    key = (spec.name, id(inputs), str(device))
+    key = (getattr(spec, "digest", spec.name), id(inputs), str(device))
     cache = grid._device_cache
     hit = cache.get(key)
     if hit is None or hit[0] is not inputs:
@@ -177,6 +178,7 @@ def _fs_init(B, device):
     fs["uniform"] = 1
     fs["err_nonfinite"] = _lib.INT32_MAX
     fs["err_degenerate"] = _lib.INT32_MAX
+    fs["err_param"] = _lib.INT32_MAX
     return torch.from_numpy(fs.view(np.uint8).reshape(B, 64).copy()).to(device)
 
 
@@ -240,6 +242,11 @@ class ParticleRun:
         if not keep_history and noise != "device":
             raise ValueError("keep_history=False needs device noise (host draws cannot be replayed)")
         self.keep_history = bool(keep_history)
+        if self.spec.kernel == _lib.SSM_MODEL_GENERIC:
+            if not self.keep_history:
+                raise UnsupportedModelError(f"{self.spec.name}: history-free runs need a hand-written model kernel")
+            if noise == "host":
+                self.spec.check_host_noise()
         self._keys = []  # history-free runs: Philox key (2 x uint32) used at each grid index
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.loglik = 0.0
@@ -379,11 +386,23 @@ def init_runs(runs, rngs):
     if need_draw:
         if r0.noise == "host":
             for b in need_draw:
-                x[b].copy_(torch.from_numpy(spec.host_initial(rngs[b], P).T.copy()).to(r0.tdtype))
+                x0b = spec.host_initial(rngs[b], P, runs[b].theta)
+                x[b].copy_(torch.from_numpy(x0b.T.copy()).to(r0.tdtype))
         else:
             keys = device_keys([rngs[b] for b in need_draw])
             kt = torch.from_numpy(keys.view(np.int32)).to(dev)
-            if len(need_draw) == B:
+            if spec.kernel == _lib.SSM_MODEL_GENERIC:  # the model's initial block, NVRTC-compiled
+                th = torch.from_numpy(spec.derived(np.concatenate([runs[b].theta for b in need_draw]))).to(dev)
+                tmp = torch.empty((len(need_draw), spec.nx, P), dtype=r0.tdtype, device=dev)
+                fs_init = _fs_init(len(need_draw), dev)
+                _lib.check(_lib.lib().ssm_gen_init_particles(
+                    C.c_void_p(spec.handle(dev)), r0.dtype_id, len(need_draw), P, 0, _lib.ptr(kt), _lib.ptr(th),
+                    spec.theta_stride, _lib.ptr(tmp), _lib.ptr(fs_init), _lib.stream_ptr()), "ssm_gen_init_particles")
+                if int(_fs_view(fs_init)["err_param"].min()) != _lib.INT32_MAX:
+                    raise DistributionParameterError(f"{spec.name}: invalid initial-block distribution argument")
+                for j, b in enumerate(need_draw):
+                    x[b].copy_(tmp[j])
+            elif len(need_draw) == B:
                 _lib.check(_lib.lib().ssm_init_particles(spec.kernel, r0.dtype_id, B, P, 0, _lib.ptr(kt),
                                                          _lib.ptr(x), _lib.stream_ptr()), "ssm_init_particles")
             else:
@@ -562,7 +581,8 @@ def advance_runs(runs, upto, rngs):
     pw_ws = torch.empty(L.ssm_pw_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     rs_ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     # systematic / stratified resample from the pw kernel's tile-local CDF (no second pass over logw)
-    small = (not host_noise and P <= _small_max() and not _NO_SMALL and r0.keep_history)
+    small = (not host_noise and P <= _small_max() and not _NO_SMALL and r0.keep_history
+             and spec.kernel != _lib.SSM_MODEL_GENERIC)
     # resample from the pw kernel's tile CDF (multi-kernel path; multinomial with device draws only)
     tiles_ok = (r0.resampler in ("systematic", "stratified") or scheme == _lib.SSM_MULTINOMIAL_SORTED) and not small
     ntile = (P + 31) // 32  # one tile record per warp tile
@@ -592,6 +612,9 @@ def advance_runs(runs, upto, rngs):
     args.log_sqrt_2pi = float(LOG_SQRT_2PI)
     args.ess_rel = ess_rel
     args.theta = theta.data_ptr()
+    if spec.kernel == _lib.SSM_MODEL_GENERIC:
+        args.gen = spec.handle(dev)
+        args.theta_stride = spec.theta_stride
     args.keys = keys_t.data_ptr() if keys_t is not None else None
     args.fs = fs.data_ptr()
     args.workspace = pw_ws.data_ptr()
@@ -695,7 +718,8 @@ def advance_runs(runs, upto, rngs):
     xstride = spec.nx * P * esz
     astride = P * 4
     fs_host = _fs_view(fs)  # one synchronisation per advance
-    if (fs_host["err_nonfinite"] != _lib.INT32_MAX).any() or (fs_host["err_degenerate"] != _lib.INT32_MAX).any():
+    if ((fs_host["err_nonfinite"] != _lib.INT32_MAX).any() or (fs_host["err_degenerate"] != _lib.INT32_MAX).any()
+            or (fs_host["err_param"] != _lib.INT32_MAX).any()):
         for b, r in enumerate(runs):
             _raise_if_failed(fs_host[b], sched, r.check_finite)
     ll = fs_host["loglik"].astype(float)
@@ -731,6 +755,11 @@ def advance_runs(runs, upto, rngs):
 def _raise_if_failed(st, sched, check_finite):
     nf = int(st["err_nonfinite"])
     dg = int(st["err_degenerate"])
+    pe = int(st["err_param"])
+    if pe != _lib.INT32_MAX and (nf == _lib.INT32_MAX or pe <= nf) and (dg == _lib.INT32_MAX or pe // 64 <= dg):
+        step, sub = pe // 64, pe % 64
+        where = "observation density" if sub == 63 else "transition"
+        raise DistributionParameterError(f"invalid distribution argument in the {where} at grid index {step}")
     if nf == _lib.INT32_MAX and dg == _lib.INT32_MAX:
         return
     nf_step = nf // 64 if nf != _lib.INT32_MAX else None

@@ -173,8 +173,9 @@ class ModelSpec:
         return out
 
     # ---- host draws in the reference's order (noise="host" parity mode) ----
-    def host_initial(self, rng, P):
-        """simulate.sample_initial draws (simulate.py:111-129), (P, nx)."""
+    def host_initial(self, rng, P, theta=None):
+        """simulate.sample_initial draws (simulate.py:111-129), (P, nx); the
+        initial blocks of both models do not read theta."""
         x = np.zeros((P, self.nx))
         if self.name == "Lorenz96":
             for n in range(8):
@@ -403,38 +404,38 @@ LORENZ96 = ModelSpec("Lorenz96", _lib.SSM_MODEL_LORENZ96, 2, 8, 8, 0, 8, 0.05, 0
 WINDKESSEL = ModelSpec("Windkessel", _lib.SSM_MODEL_WINDKESSEL, 4, 1, 1, 1, 1, 0.01, 0.01, 2.0, False)
 _BY_NAME = {"lorenz96": LORENZ96, "windkessel": WINDKESSEL}
 
-# Expression fingerprints of the reference's compiled lambdas (ir.py:188-214)
-# that the kernels implement; a ModelIr must match exactly to be accepted.
-_L96_TRANSITION_SLOT0 = (
-    "((((X[:, 7] * (X[:, 1] - X[:, 6])) - X[:, 0]) + T[:, 0]) + ((np.sqrt(T[:, 1]) * W[:, 0]) / 0.05))"
-)
-_WK_TRANSITION = (
-    "((np.exp(((-0.01) / (T[:, 0] * T[:, 1]))) * X[:, 0]) + ((T[:, 0] * (1.0 - "
-    "np.exp(((-0.01) / (T[:, 0] * T[:, 1]))))) * (U[0] + W[:, 0])))"
-)
+# Digests of the two reference models lowered block by block
+# (codegen.fingerprint over Lorenz96.bi / Windkessel.bi): a ModelIr maps onto a
+# hand-written kernel (and its host theta-level blocks) only when every block
+# lowers to exactly these statements.
+_FINGERPRINTS = {
+    "lorenz96": "10523704f015f378394f23196c8c3777758c9dbf0e7bdcce94f2c0f9dfe35069",
+    "windkessel": "81441693f4b10e3d6a8a61cda5069b0bcccb849865b05d1f7be18931b1584a92",
+}
 
 
 def _ir_fingerprint(ir):
-    """Source of the first transition expression of a reference ModelIr,
-    regenerated with the reference's own expr_source if importable."""
+    from . import codegen
+
     try:
-        from ssmkit.core import ir as I  # the reference, when installed alongside
-    except Exception:  # pragma: no cover - reference absent
+        return codegen.fingerprint(ir)
+    except UnsupportedModelError:
         return None
-    block = ir.block("transition")
-    for op in block.ops:
-        if hasattr(op, "items") and op.items:
-            eq, b = op.items[0]
-            return I.expr_source(eq.expr, (ir.consts, ir.vars), b)
-        if type(op).__name__ == "AssignStmtOp":
-            return I.expr_source(op.stmt.expr, (ir.consts, ir.vars), op.bindings[0])
-    return None
 
 
-def resolve_model(model) -> ModelSpec:
-    """ModelSpec | "lorenz96" | "windkessel" | reference ModelIr -> ModelSpec."""
-    if isinstance(model, ModelSpec):
+def resolve_model(model):
+    """ModelSpec | "lorenz96" | "windkessel" | reference ModelIr | GenericModel |
+    lowered description -> the model's device spec.
+
+    A reference ModelIr whose compiled expressions are exactly those of a
+    hand-written kernel maps onto that kernel; any other ModelIr is lowered and
+    compiled at run time (generic.GenericModel)."""
+    from . import generic
+
+    if isinstance(model, (ModelSpec, generic.GenericModel)):
         return model
+    if isinstance(model, dict) and "counts" in model and "transition" in model:
+        return generic.from_description(model)
     if isinstance(model, str):
         spec = _BY_NAME.get(model.lower())
         if spec is None:
@@ -442,16 +443,12 @@ def resolve_model(model) -> ModelSpec:
         return spec
     name = getattr(model, "name", None)
     counts = getattr(model, "counts", None)
-    spec = _BY_NAME.get(str(name).lower()) if name else None
-    if spec is None or counts is None:
+    if counts is None or not hasattr(model, "block"):
         raise UnsupportedModelError(f"no sm_100a kernel for model {name!r}")
-    if dict(counts) != spec.counts or float(getattr(model, "delta", -1)) != spec.delta:
-        raise UnsupportedModelError(f"model {name!r} does not match the {spec.name} kernel")
-    fp = _ir_fingerprint(model)
-    want = _L96_TRANSITION_SLOT0 if spec is LORENZ96 else _WK_TRANSITION
-    if fp is not None and fp != want:
-        raise UnsupportedModelError(f"model {name!r} transition differs from the {spec.name} kernel")
-    return spec
+    key = str(name).lower() if name else None
+    if key in _BY_NAME and _ir_fingerprint(model) == _FINGERPRINTS[key]:
+        return _BY_NAME[key]
+    return generic.from_ir(model)
 
 
 def load_model(name_or_path: str) -> ModelSpec:

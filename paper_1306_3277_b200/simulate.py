@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import NonFiniteStateError
+from .errors import DistributionParameterError, NonFiniteStateError
 from .inference.particle import _dtype_info, _fs_init, substep_schedule
 from .models import LOG_SQRT_2PI, resolve_model
 
@@ -68,6 +68,8 @@ def _run_pw(spec, theta, x, arr, noise, obs, dtype, exact, check_finite, device)
     A.subs = subs_t.data_ptr() if subs_t is not None else None
     A.noise = noise_t.data_ptr() if noise_t is not None else None
     A.fs, A.workspace = fs.data_ptr(), ws.data_ptr()
+    if spec.kernel == _lib.SSM_MODEL_GENERIC:
+        A.gen, A.theta_stride = spec.handle(dev), spec.theta_stride
     if obs is not None:
         bits, yy, u_obs = obs
         A.has_obs, A.obs_mask, A.u_obs = 1, bits, u_obs
@@ -76,6 +78,8 @@ def _run_pw(spec, theta, x, arr, noise, obs, dtype, exact, check_finite, device)
         A.a_out = a_out.data_ptr()
     _lib.check(L.ssm_propagate_weight(A, _lib.stream_ptr()), "ssm_propagate_weight")
     st = fs.cpu().numpy().reshape(-1).view(_lib.FILTER_STATE_DTYPE)[0]
+    if int(st["err_param"]) != _lib.INT32_MAX:
+        raise DistributionParameterError(f"{spec.name}: invalid distribution argument")
     return xout, a_out, st
 
 

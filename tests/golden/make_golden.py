@@ -395,6 +395,92 @@ def gen_outer_loops():
     save("outer.npz", **out)
 
 
+TEST_MODELS = os.path.join(os.path.dirname(HERE), "models")
+
+
+def load_test_model(name):
+    with open(os.path.join(TEST_MODELS, name + ".bi")) as fh:
+        return load_model(fh.read())
+
+
+def simulate_data(ir, theta, times, seed=1, inputs=None):
+    """Observations simulated with the reference (runner.py:47-80 recipe)."""
+    rng = RngStream(seed)
+    x = simulate.sample_initial(ir, theta, rng.child(1), size=1)
+    ot, ov, om = [], [], []
+    for k in range(1, len(times)):
+        x = simulate.step_transition(ir, theta, x, inputs, times[k - 1], times[k] - times[k - 1], rng.child(2, k))
+        y = simulate.simulate_obs(ir, theta, x, None if inputs is None else inputs.at(times[k]), rng.child(3, k))[0]
+        ot.append(times[k])
+        ov.append(y)
+        om.append(np.ones(ir.n_obs, bool))
+    return np.array(ot), np.array(ov), np.array(om)
+
+
+def gen_generic():
+    """Generic (NVRTC) path fixtures: every model lowered by our codegen from
+    the reference IR, the reference's own expression sources for each lowered
+    expression (pins the lowering), and reference PF runs of the two test models."""
+    import json
+
+    import ssmkit.core.ir as I
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1306_3277_b200 import codegen
+
+    # truncated_gaussian's default bound `inf` (SURVEY 8c known defect): compile shim
+    I.compile_expr = lambda e, t, b: eval(
+        f"lambda T, X, W, U: {I.expr_source(e, t, b)}", {"np": np, "inf": np.inf, "__builtins__": {}})
+
+    models = {"Lorenz96": load("lorenz96"), "Windkessel": load("windkessel"),
+              "StochVol": load_test_model("StochVol"), "PredatorPrey": load_test_model("PredatorPrey")}
+    lowered, sources = {}, {}
+    for name, ir in models.items():
+        d = codegen.lower(ir)
+        lowered[name] = d
+        srcs = []
+        for bn in ("initial", "transition", "observation"):
+            blk = ir.block(bn)
+            for op in (blk.ops if blk is not None else ()):
+                if type(op).__name__ == "AssignStmtOp":
+                    srcs += [I.expr_source(op.stmt.expr, (ir.consts, ir.vars), b) for b in op.bindings]
+                elif type(op).__name__ == "OdeOp":
+                    srcs += [I.expr_source(eq.expr, (ir.consts, ir.vars), b) for eq, b in op.items]
+                else:
+                    _, args = I.canonical_dist_args(op.stmt.dist)
+                    srcs += [I.expr_source(a, (ir.consts, ir.vars), b) for b in op.bindings for a in args]
+        sources[name] = srcs
+        lowered[name]["fingerprint"] = codegen.fingerprint(ir)
+    with open(os.path.join(HERE, "gen_models.json"), "w") as fh:
+        json.dump({"lowered": lowered, "reference_sources": sources, "versions": VERSIONS}, fh, indent=0,
+                  sort_keys=True)
+    print("wrote gen_models.json")
+
+    out = {}
+    cases = {"StochVol": (np.array([-0.5, 0.9, 0.3]), np.linspace(0.0, 30.0, 31)),
+             "PredatorPrey": (np.array([1.1, 0.9, 0.02]), np.linspace(0.0, 3.0, 16))}
+    for name, (theta, times) in cases.items():
+        ir = models[name]
+        ot, ov, om = simulate_data(ir, theta, times)
+        grid = build_filter_grid(0.0, times[-1], len(times) - 1, ot, ov, om, n_obs=ir.n_obs)
+        out[f"{name}/theta"] = theta
+        out[f"{name}/times"] = grid.times
+        out[f"{name}/obs_t"] = ot
+        out[f"{name}/obs_v"] = ov
+        out[f"{name}/obs_m"] = om
+        for scheme in ("systematic", "multinomial"):
+            res = particle_filter(ir, theta, grid, RngStream(11), n_particles=512, resampler=scheme)
+            out[f"{name}/{scheme}/loglik"] = np.array(res.loglik)
+            out[f"{name}/{scheme}/traj"] = res.trajectory
+            out[f"{name}/{scheme}/x_final"] = res.run.x
+            out[f"{name}/{scheme}/anc"] = np.array([h[1] for h in res.run.history[1:] if h[1] is not None])
+        # initial block and one transition step with the reference's draws
+        x0 = simulate.sample_initial(ir, theta, RngStream(5).child(0), size=300)
+        out[f"{name}/x0"] = x0
+        out[f"{name}/x1"] = simulate.step_transition(ir, theta, x0, None, 0.0, times[1] - times[0], RngStream(6))
+        out[f"{name}/g1"] = simulate.observe_logpdf(ir, theta, out[f"{name}/x1"], None, ov[0], om[0])
+    save("generic.npz", **out)
+
+
 if __name__ == "__main__":
     gen_resample()
     gen_lse()
@@ -403,3 +489,4 @@ if __name__ == "__main__":
     gen_pf()
     gen_theta_level()
     gen_outer_loops()
+    gen_generic()

@@ -164,6 +164,10 @@ def lower(ir) -> dict:
     for op in out["observation"]:
         if op["op"] != "sample" or op["kind"] == "wiener":
             raise UnsupportedModelError("observation block: distribution statements only")
+    # theta-level blocks, evaluated on the host by the PMMH / SMC^2 loops (None = absent)
+    for name in THETA_BLOCKS:
+        blk = ir.block(name)
+        out[name] = None if blk is None else [_lower_op(op, ir) for op in blk.ops]
     return out
 
 

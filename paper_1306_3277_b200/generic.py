@@ -26,7 +26,8 @@ import numpy as np
 
 from . import _lib, codegen
 from .errors import DistributionParameterError, UnsupportedModelError
-from .models import d_gamma_sample, d_invgamma_sample, d_tgauss_sample, d_uniform_sample
+from .models import (d_gamma_logpdf, d_gamma_sample, d_gauss_logpdf, d_invgamma_logpdf, d_invgamma_sample,
+                     d_tgauss_logpdf, d_tgauss_sample, d_uniform_logpdf, d_uniform_sample)
 
 _INJECTABLE = {"wiener": "normal", "gaussian": "normal", "uniform": "uniform", "truncated_gaussian": "uniform"}
 _CACHE = {}
@@ -52,6 +53,39 @@ def _sample_host(kind, args, size, rng):
     raise UnsupportedModelError(f"cannot sample {kind} on the host")
 
 
+def _check_params(kind, args):
+    """distributions.py:53-69"""
+    def req(ok, msg):
+        if not np.all(ok):
+            raise DistributionParameterError(msg)
+
+    if kind in ("gaussian", "truncated_gaussian"):
+        req(np.asarray(args[1]) > 0, f"{kind} sd must be > 0")
+        if kind == "truncated_gaussian":
+            req(np.asarray(args[2]) < np.asarray(args[3]), "truncated_gaussian needs lower < upper")
+    elif kind in ("gamma", "inverse_gamma"):
+        req(np.asarray(args[0]) > 0, f"{kind} shape must be > 0")
+        req(np.asarray(args[1]) > 0, f"{kind} scale must be > 0")
+    elif kind == "uniform":
+        req(np.asarray(args[0]) < np.asarray(args[1]), "uniform needs lower < upper")
+
+
+def _logpdf_host(kind, args, x):
+    """distributions.logpdf (distributions.py:94-123)."""
+    _check_params(kind, args)
+    if kind == "gaussian":
+        return d_gauss_logpdf(x, args[0], args[1])
+    if kind == "truncated_gaussian":
+        return d_tgauss_logpdf(x, *args)
+    if kind == "gamma":
+        return d_gamma_logpdf(x, args[0], args[1])
+    if kind == "inverse_gamma":
+        return d_invgamma_logpdf(x, args[0], args[1])
+    if kind == "uniform":
+        return d_uniform_logpdf(x, args[0], args[1])
+    raise UnsupportedModelError(f"cannot evaluate {kind}")
+
+
 class GenericModel:
     """Model spec for the NVRTC-compiled generic kernels (SSM_MODEL_GENERIC)."""
 
@@ -59,7 +93,6 @@ class GenericModel:
     h = 0.0  # RK4 steps are split in the kernel (the sub-step table's s[] is unused)
     obs_sd = 1.0  # unused: the observation density is generated code
     has_ode = False
-    has_proposal_initial = False
 
     def __init__(self, desc: dict):
         self.desc = desc
@@ -73,7 +106,8 @@ class GenericModel:
         self.draw_kinds = codegen.transition_draws(desc)
         self.theta_stride = max(self.n_param, 1)
         self._handles = {}
-        self._init_fns = None
+        self._fns = {}
+        self.has_proposal_initial = desc.get("proposal_initial") is not None
 
     @property
     def nx(self):
@@ -84,7 +118,9 @@ class GenericModel:
         return dict(self.desc["counts"])
 
     def block(self, name):
-        return True if name in ("initial", "transition", "observation") else None
+        if name in ("initial", "transition", "observation"):
+            return True
+        return True if self.desc.get(name) is not None else None
 
     def __repr__(self):
         return f"GenericModel({self.name!r}, digest={self.digest})"
@@ -131,17 +167,18 @@ class GenericModel:
         return out
 
     # ---- host draws (noise="host") -----------------------------------------
-    def _initial_fns(self):
-        if self._init_fns is None:
+    def _block_fns(self, name):
+        """Statements of a block with host (numpy) expression functions."""
+        if name not in self._fns:
             ops = []
-            for op in self.desc["initial"]:
+            for op in self.desc.get(name) or ():
                 if op["op"] == "sample":
                     ops.append(("sample", op["kind"], op["slots"],
                                 [[codegen.numpy_fn(a) for a in row] for row in op["args"]]))
-                else:
+                elif op["op"] == "assign":
                     ops.append(("assign", None, op["slots"], [codegen.numpy_fn(e) for e in op["exprs"]]))
-            self._init_fns = ops
-        return self._init_fns
+            self._fns[name] = ops
+        return self._fns[name]
 
     def host_initial(self, rng, P, theta=None):
         """simulate.sample_initial (simulate.py:111-129) for one filter: (P, nx)."""
@@ -149,7 +186,7 @@ class GenericModel:
         X = np.zeros((P, self.n_state))
         W = np.zeros((P, 0))
         U = np.zeros(self.n_input)
-        for what, kind, slots, fns in self._initial_fns():
+        for what, kind, slots, fns in self._block_fns("initial"):
             if what == "sample":
                 args_all = [tuple(f(T, X, W, U) for f in row) for row in fns]
                 for slot, args in zip(slots, args_all):
@@ -178,6 +215,117 @@ class GenericModel:
                 else:
                     out[k, j] = rng.uniform(0.0, 1.0, size=P)
         return out
+
+
+    # ---- theta-level blocks on the host (simulate.py:96-108, 219-352) --------
+    def sample_parameter(self, rng, size=1):
+        T = np.zeros((size, self.n_param))
+        X, W, U = np.zeros((size, 0)), np.zeros((size, 0)), np.zeros(self.n_input)
+        for what, kind, slots, fns in self._block_fns("parameter"):
+            if what != "sample":
+                continue
+            args_all = [tuple(f(T, X, W, U) for f in row) for row in fns]
+            for slot, args in zip(slots, args_all):
+                T[:, slot] = _sample_host(kind, args, size, rng)
+        return T
+
+    def sample_initial(self, thetas, rng, size=None):
+        T = np.atleast_2d(np.asarray(thetas, dtype=float))
+        return self.host_initial(rng, T.shape[0] if size is None else size, T)
+
+    def parameter_logpdf(self, theta):
+        theta = np.asarray(theta, dtype=float)
+        T, X, W, U = theta[None, :], np.zeros((1, 0)), np.zeros((1, 0)), np.zeros(self.n_input)
+        total = 0.0
+        for what, kind, slots, fns in self._block_fns("parameter"):
+            for slot, row in zip(slots, fns):
+                args = tuple(f(T, X, W, U) for f in row)
+                total += float(np.sum(_logpdf_host(kind, args, theta[slot])))
+        return total
+
+    def initial_logpdf(self, theta, x0):
+        theta, x0 = np.asarray(theta, dtype=float), np.asarray(x0, dtype=float)
+        T, X, W, U = theta[None, :], x0[None, :], np.zeros((1, 0)), np.zeros(self.n_input)
+        total = 0.0
+        for what, kind, slots, fns in self._block_fns("initial"):
+            if what != "sample":
+                continue
+            for slot, row in zip(slots, fns):
+                args = tuple(f(T, X, W, U) for f in row)
+                total += float(np.sum(_logpdf_host(kind, args, x0[slot])))
+        return total
+
+    def _apply_initial_assigns(self, theta, x0):
+        X = np.array(x0, dtype=float, copy=True)[None, :]
+        T, W, U = np.atleast_2d(np.asarray(theta, dtype=float)), np.zeros((1, 0)), np.zeros(self.n_input)
+        for what, _, slots, fns in self._block_fns("initial"):
+            if what == "assign":
+                vals = [f(T, X, W, U) for f in fns]
+                for slot, v in zip(slots, vals):
+                    X[:, slot] = v
+        return X[0]
+
+    def _walk(self, block, fallback, T, X, env, values_from, values_to, rng):
+        """simulate._walk_proposal (simulate.py:264-299): sequential overwrite."""
+        name = block if self.desc.get(block) is not None else fallback
+        W, U = np.zeros((1, 0)), np.zeros(self.n_input)
+        logq = 0.0
+        out = np.array(values_from, dtype=float, copy=True)
+        for what, kind, slots, fns in self._block_fns(name):
+            if what != "sample":
+                continue
+            args_all = [tuple(f(T, X, W, U) for f in row) for row in fns]
+            for slot, args in zip(slots, args_all):
+                if values_to is None:
+                    value = float(_sample_host(kind, args, 1, rng)[0])
+                else:
+                    value = float(values_to[slot])
+                logq += float(np.sum(_logpdf_host(kind, args, value)))
+                out[slot] = value
+                env[0, slot] = value
+        return out, logq
+
+    def propose_parameters(self, theta, rng):
+        theta = np.asarray(theta, dtype=float)
+        T, X = theta[None, :].copy(), np.zeros((1, self.n_state))
+        return self._walk("proposal_parameter", "parameter", T, X, T, theta, None, rng)
+
+    def proposal_parameter_logpdf(self, theta_from, theta_to):
+        theta_from = np.asarray(theta_from, dtype=float)
+        T, X = theta_from[None, :].copy(), np.zeros((1, self.n_state))
+        return self._walk("proposal_parameter", "parameter", T, X, T, theta_from, theta_to, None)[1]
+
+    def propose_initial(self, theta, x0, rng):
+        x0 = np.asarray(x0, dtype=float)
+        T, X = np.atleast_2d(np.asarray(theta, dtype=float)).copy(), x0[None, :].copy()
+        out, logq = self._walk("proposal_initial", "initial", T, X, X, x0, None, rng)
+        return self._apply_initial_assigns(theta, out), logq
+
+    def proposal_initial_logpdf(self, theta, x_from, x_to):
+        x_from = np.asarray(x_from, dtype=float)
+        T, X = np.atleast_2d(np.asarray(theta, dtype=float)).copy(), x_from[None, :].copy()
+        return self._walk("proposal_initial", "initial", T, X, X, x_from, x_to, None)[1]
+
+    def propose_batch(self, thetas, inits, rngs):
+        """models.propose_batch for a generic model: the reference's marginal MH
+        proposal (mcmc.py:140-147), chain by chain in its draw order."""
+        C = len(rngs)
+        new = np.zeros((C, self.n_param))
+        x0s, lq_f, lq_r, lp = [None] * C, np.zeros(C), np.zeros(C), np.zeros(C)
+        for c, rng in enumerate(rngs):
+            th = np.asarray(thetas[c], dtype=float)
+            th_new, f = self.propose_parameters(th, rng)
+            r = self.proposal_parameter_logpdf(th_new, th)
+            x_new = None
+            if inits is not None and inits[c] is not None:
+                x_new, lq = self.propose_initial(th_new, inits[c], rng)
+                f += lq
+                r += self.proposal_initial_logpdf(th, x_new, inits[c])
+            p = self.parameter_logpdf(th_new)
+            if x_new is not None:
+                p += self.initial_logpdf(th_new, x_new)
+            new[c], x0s[c], lq_f[c], lq_r[c], lp[c] = th_new, x_new, f, r, p
+        return new, x0s, lq_f, lq_r, lp
 
 
 def from_description(desc: dict) -> GenericModel:

@@ -328,6 +328,8 @@ def propose_batch(spec, thetas, inits, rngs):
     """_propose for every chain: (theta_new, init_new, logq_fwd, logq_rev, log_prior_new).
     Equals [spec.propose_parameters / proposal_parameter_logpdf / propose_initial /
     proposal_initial_logpdf / parameter_logpdf + initial_logpdf] row by row."""
+    if hasattr(spec, "propose_batch"):  # generic model: its own host blocks
+        return spec.propose_batch(thetas, inits, rngs)
     th = np.array(thetas, dtype=float).reshape(len(rngs), spec.n_param)
     C = th.shape[0]
     new = th.copy()

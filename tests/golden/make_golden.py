@@ -420,8 +420,11 @@ def simulate_data(ir, theta, times, seed=1, inputs=None):
 def gen_generic():
     """Generic (NVRTC) path fixtures: every model lowered by our codegen from
     the reference IR, the reference's own expression sources for each lowered
-    expression (pins the lowering), and reference PF runs of the two test models."""
+    expression (pins the lowering), and reference PF / theta-level / PMMH /
+    SMC^2 runs of the two test models."""
     import json
+
+    from ssmkit.inference import FilterRunner, mh_sample, smc_sampler
 
     import ssmkit.core.ir as I
     sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
@@ -478,6 +481,25 @@ def gen_generic():
         out[f"{name}/x0"] = x0
         out[f"{name}/x1"] = simulate.step_transition(ir, theta, x0, None, 0.0, times[1] - times[0], RngStream(6))
         out[f"{name}/g1"] = simulate.observe_logpdf(ir, theta, out[f"{name}/x1"], None, ov[0], om[0])
+        # theta-level blocks (simulate.py:96-108, 219-352)
+        th = simulate.sample_parameter(ir, RngStream(3), size=5)
+        out[f"{name}/prior_draws"] = th
+        out[f"{name}/prior_logpdf"] = np.array([simulate.parameter_logpdf(ir, t) for t in th])
+        props = [simulate.propose_parameters(ir, t, RngStream(4).child(k)) for k, t in enumerate(th)]
+        out[f"{name}/prop"] = np.array([p[0] for p in props])
+        out[f"{name}/prop_logq"] = np.array([p[1] for p in props])
+        out[f"{name}/prop_rev"] = np.array([simulate.proposal_parameter_logpdf(ir, p[0], t)
+                                            for p, t in zip(props, th)])
+        # outer loops at toy size with the reference's draws
+        runner = FilterRunner(ir, grid, n_particles=64, resampler="systematic")
+        chains, acc = mh_sample(ir, runner, 5, RngStream(31))
+        out[f"{name}/mh/thetas"] = np.array([c.theta for c in chains])
+        out[f"{name}/mh/logliks"] = np.array([c.loglik for c in chains])
+        out[f"{name}/mh/accepted"] = np.array(acc)
+        res = smc_sampler(ir, runner, 6, RngStream(32), theta_resampler="systematic")
+        out[f"{name}/smc/thetas"] = res.thetas
+        out[f"{name}/smc/logliks"] = res.logliks
+        out[f"{name}/smc/log_v"] = res.log_v
     save("generic.npz", **out)
 
 

@@ -39,4 +39,10 @@ model PredatorPrey {
     z0 ~ truncated_gaussian(x[0], 0.2, lower = 0.0)
     z1 ~ gamma(4.0, (x[1]*x[1] + 0.1)/4.0)
   }
+
+  sub proposal_parameter {
+    a ~ truncated_gaussian(a, 0.05, 0.5, 1.5)
+    b ~ truncated_gaussian(b, 0.05, 0.5, 1.5)
+    s2 ~ inverse_gamma(2.0, 3.0*s2)
+  }
 }

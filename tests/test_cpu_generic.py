@@ -88,3 +88,22 @@ def test_codegen_limits_and_unsupported_statements():
     bad["observation"][0]["kind"] = "wiener"
     with pytest.raises(models.UnsupportedModelError):
         codegen.cuda_source(bad)
+
+
+@pytest.mark.parametrize("name", ["StochVol", "PredatorPrey"])
+def test_theta_level_blocks_equal_reference(name):
+    """Prior draws / densities and the parameter proposal (with its fallback to
+    the prior when the model has no proposal_parameter block) on the host,
+    bitwise the reference's (simulate.py:96-108, 219-352)."""
+    g = load_golden("generic.npz")
+    m = generic.from_description(_desc(name))
+    th = m.sample_parameter(RngStream(3), size=5)
+    np.testing.assert_array_equal(th, g[f"{name}/prior_draws"])
+    np.testing.assert_array_equal([m.parameter_logpdf(t) for t in th], g[f"{name}/prior_logpdf"])
+    props = [m.propose_parameters(t, RngStream(4).child(k)) for k, t in enumerate(th)]
+    np.testing.assert_array_equal([p[0] for p in props], g[f"{name}/prop"])
+    np.testing.assert_array_equal([p[1] for p in props], g[f"{name}/prop_logq"])
+    np.testing.assert_array_equal([m.proposal_parameter_logpdf(p[0], t) for p, t in zip(props, th)],
+                                  g[f"{name}/prop_rev"])
+    assert m.has_proposal_initial is False
+    assert (m.block("proposal_parameter") is not None) == (name == "PredatorPrey")

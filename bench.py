@@ -136,6 +136,17 @@ class ClockSampler:
 # ------------------------------------------------------------------ our arm
 
 
+def generic_l96():
+    """Lorenz '96 through the generic path: the reference model lowered from its
+    IR (tests/golden/gen_models.json, make_golden.py) and compiled with NVRTC."""
+    from paper_1306_3277_b200 import generic
+
+    with open(os.path.join(ROOT, "tests", "golden", "gen_models.json")) as fh:
+        d = dict(json.load(fh)["lowered"]["Lorenz96"])
+    d.pop("fingerprint", None)
+    return generic.from_description(d)
+
+
 def run_ours(args, rank, world):
     import torch
 
@@ -145,6 +156,7 @@ def run_ours(args, rank, world):
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     P, T = args.particles, args.T
+    model = LORENZ96 if args.model == "lorenz96" else generic_l96()
     times, ot, ov, om = synthetic_data(T)
     grid = build_filter_grid(0.0, times[-1], T, ot, ov, om, n_obs=8)
     opts = dict(dtype=args.dtype, exact=args.exact, noise="device")
@@ -161,7 +173,7 @@ def run_ours(args, rank, world):
 
             return _Out(*particle_filter_sharded(LORENZ96, THETA, grid_obj, rng, world * P, resampler=args.resampler,
                                                  dtype=args.dtype, exact=args.exact))
-        return particle_filter(LORENZ96, THETA, grid_obj, rng, n_particles=P, resampler=args.resampler, **opts)
+        return particle_filter(model, THETA, grid_obj, rng, n_particles=P, resampler=args.resampler, **opts)
 
     def one(step, grid_obj, timer=None):
         rng = RngStream(7, ((0 if sharded else rank), step))
@@ -311,6 +323,8 @@ def main():
     ap.add_argument("--variants", type=int, default=1, help="also time f64-exact and f32 variants")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
                     help="N>1: one filter of N*2^24 particles across GPUs (default) or N independent filters")
+    ap.add_argument("--model", default="lorenz96", choices=["lorenz96", "generic"],
+                    help="hand-written L96 kernel (default) or the NVRTC-compiled generic path")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--ref-particles", type=int, default=1 << 17)
@@ -364,6 +378,8 @@ def main():
         "dtype": dtype_tag,
         "data": "synthetic (L96 theta*=(10,0.1) simulated per SURVEY 8d; device Philox noise)",
         "config": dict(workload_config(P, T, args.dtype, args.resampler), arithmetic=arith,
+                       kernels=("hand-written L96 kernel" if args.model == "lorenz96"
+                                else "generic path: L96 lowered from the reference IR, NVRTC-compiled"),
                        parallelism=("replicas" if world == 1 or args.mode == "replicas"
                                     else f"one filter sharded over {world} GPUs (NCCL all-gather of LSE partials and "
                                          "CDF totals + P2P spill of ancestor states per step)")),
@@ -395,13 +411,14 @@ def main():
                        "ms_per_step": res["e2e_ms"]}
     if args.variants and world == 1:
         line["variants"] = {}
-        for name, dt, ex, rs in (("f64_exact_bitwise", "float64", True, args.resampler),
-                                 ("f32", "float32", False, args.resampler),
-                                 ("f64_multinomial", "float64", False, "multinomial")):
-            if (dt, ex, rs) == (args.dtype, args.exact, args.resampler):
+        for name, dt, ex, rs, mdl in (("f64_exact_bitwise", "float64", True, args.resampler, args.model),
+                                      ("f32", "float32", False, args.resampler, args.model),
+                                      ("f64_multinomial", "float64", False, "multinomial", args.model),
+                                      ("f64_generic_codegen", "float64", False, args.resampler, "generic")):
+            if (dt, ex, rs, mdl) == (args.dtype, args.exact, args.resampler, args.model):
                 continue
             v_args = argparse.Namespace(**vars(args))
-            v_args.dtype, v_args.exact, v_args.e2e_steps, v_args.resampler = dt, ex, 0, rs
+            v_args.dtype, v_args.exact, v_args.e2e_steps, v_args.resampler, v_args.model = dt, ex, 0, rs, mdl
             v = run_ours(v_args, rank, world)
             vpw = v["kern"].get("propagate_weight", {})
             line["variants"][name] = {

@@ -251,6 +251,9 @@ def cuda_expr(e, xname="X") -> str:
     if t == "neg":
         return f"(-{cuda_expr(e[1], xname)})"
     if t == "bin":
+        if e[1] == "/" and e[3][0] == "num" and math.isfinite(e[3][1]) and e[3][1] != 0.0:
+            c = e[3][1]  # constant divisor: fast mode multiplies by the reciprocal
+            return f"O::divc({cuda_expr(e[2], xname)}, {_lit(c)}, {_lit(1.0 / c)})"
         return f"O::{_OPS[e[1]]}({cuda_expr(e[2], xname)}, {cuda_expr(e[3], xname)})"
     if t == "call":
         args = [cuda_expr(a, xname) for a in e[2]]
@@ -273,7 +276,7 @@ class _Emitter:
         self.lines.append(" " * self.ind + s if s else "")
 
     def block(self, head, comment=None):
-        self(head + " {" + (f"  // {comment}" if comment else ""))
+        self((head + " {").lstrip() + (f"  // {comment}" if comment else ""))
         self.ind += 2
 
     def end(self, tail="}"):
@@ -281,24 +284,80 @@ class _Emitter:
         self(tail)
 
 
-def _sample_value(em, kind, args, kd, tmp, dname="d"):
+_NORMAL_KINDS = ("wiener", "gaussian")
+_UNIFORM_KINDS = ("uniform", "truncated_gaussian")
+
+
+def draw_plan(kinds):
+    """Device words of each draw of a block (kd = draw index): normals take half
+    a Box-Muller pair, uniforms a whole pair (two 32-bit words each); pairs are
+    packed two per Philox block.  Returns (per-draw ("z", i) | ("u", i) |
+    ("g", kd), normal pairs [(pair, z index)], uniform pairs [(pair, u index)],
+    n_blocks)."""
+    plan, zpairs, upairs = [], [], []
+    q, open_z = 0, None
+    for kd, kind in enumerate(kinds):
+        if kind in _NORMAL_KINDS:
+            if open_z is None:
+                zpairs.append((q, 2 * len(zpairs)))
+                open_z = zpairs[-1][1]
+                q += 1
+                plan.append(("z", open_z))
+            else:
+                plan.append(("z", open_z + 1))
+                open_z = None
+        elif kind in _UNIFORM_KINDS:
+            upairs.append((q, len(upairs)))
+            q += 1
+            plan.append(("u", upairs[-1][1]))
+        else:
+            plan.append(("g", kd))
+    return plan, zpairs, upairs, (q + 1) // 2
+
+
+def _emit_draw_words(em, kinds):
+    """Take each Philox block once; Box-Muller per normal pair; u53 per uniform."""
+    plan, zpairs, upairs, nblk = draw_plan(kinds)
+    em(f"float Z_[{max(2 * len(zpairs), 1)}];")
+    em(f"double V_[{max(len(upairs), 1)}];")
+    em("(void)Z_; (void)V_;")
+    if nblk:
+        em.block("if constexpr (!INJ)")
+        for b in range(nblk):
+            em(f"const ssm::U4 R{b} = dr.block({b});")
+        for pq, zi in zpairs:
+            w = ("x", "y") if pq % 2 == 0 else ("z", "w")
+            em(f"ssm::box_muller(R{pq // 2}.{w[0]}, R{pq // 2}.{w[1]}, Z_[{zi}], Z_[{zi + 1}]);")
+        for pq, ui in upairs:
+            w = ("x", "y") if pq % 2 == 0 else ("z", "w")
+            em(f"V_[{ui}] = ssm::u53(R{pq // 2}.{w[0]}, R{pq // 2}.{w[1]});")
+        em.end()
+    return plan
+
+
+def _draw(plan, kd):
+    what, i = plan[kd]
+    return f"dr.template pick<INJ>({kd}, T({'Z_' if what == 'z' else 'V_'}[{i}]))"
+
+
+def _sample_value(em, kind, args, kd, tmp, dname="d", plan=None):
     """Emit `T tmp = <draw of `kind` with args>` (simulate.py:50-60, distributions.py:73-91)."""
     if kind == "wiener":  # rng.normal(0.0, sqrt(d)): 0.0 + sd z
-        em(f"const T {tmp} = O::add(T(0.0), O::mul(T(sqrt({dname})), dr.normal({kd})));")
+        em(f"const T {tmp} = O::add(T(0.0), O::mul(T(sqrt({dname})), {_draw(plan, kd)}));")
     elif kind == "gaussian":  # rng.normal(mean, sd): mean + sd z
         em(f"const T {tmp}_m = {args[0]}, {tmp}_s = {args[1]};")
         em(f"if (!({tmp}_s > T(0))) perr = true;")
-        em(f"const T {tmp} = O::add({tmp}_m, O::mul({tmp}_s, dr.normal({kd})));")
+        em(f"const T {tmp} = O::add({tmp}_m, O::mul({tmp}_s, {_draw(plan, kd)}));")
     elif kind == "uniform":  # rng.uniform(lo, hi): lo + (hi - lo) U
         em(f"const T {tmp}_a = {args[0]}, {tmp}_b = {args[1]};")
         em(f"if (!({tmp}_a < {tmp}_b)) perr = true;")
-        em(f"const T {tmp} = O::add({tmp}_a, O::mul(O::sub({tmp}_b, {tmp}_a), dr.uniform({kd})));")
+        em(f"const T {tmp} = O::add({tmp}_a, O::mul(O::sub({tmp}_b, {tmp}_a), {_draw(plan, kd)}));")
     elif kind == "truncated_gaussian":  # mean + sd ndtri(fa + u (fb - fa)), distributions.py:78-84
         em(f"const double {tmp}_m = {args[0]}, {tmp}_s = {args[1]}, {tmp}_lo = {args[2]}, {tmp}_hi = {args[3]};")
         em(f"const double {tmp}_fa = normcdf(({tmp}_lo - {tmp}_m) / {tmp}_s), "
            f"{tmp}_fb = normcdf(({tmp}_hi - {tmp}_m) / {tmp}_s);")
         em(f"if (!({tmp}_s > 0.0) || !({tmp}_lo < {tmp}_hi) || !({tmp}_fb - {tmp}_fa > 0.0)) perr = true;")
-        em(f"const T {tmp} = T({tmp}_m + {tmp}_s * normcdfinv({tmp}_fa + double(dr.uniform({kd})) * "
+        em(f"const T {tmp} = T({tmp}_m + {tmp}_s * normcdfinv({tmp}_fa + double({_draw(plan, kd)}) * "
            f"({tmp}_fb - {tmp}_fa)));")
     elif kind == "gamma":  # rng.gamma(shape, scale) = scale * standard_gamma(shape)
         em(f"const double {tmp}_k = {args[0]}, {tmp}_t = {args[1]};")
@@ -319,6 +378,8 @@ def _d(e):
 
 def _emit_statements(em, ops, roles, dname="d"):
     """Statements of a block in order; returns the number of draws used."""
+    kinds = [op["kind"] for op in ops if op["op"] == "sample" for _ in op["slots"]]
+    plan = _emit_draw_words(em, kinds)
     kd = 0
     for si, op in enumerate(ops):
         if op["op"] == "sample":
@@ -328,7 +389,7 @@ def _emit_statements(em, ops, roles, dname="d"):
                     a = [_d(x) for x in args]
                 else:
                     a = [cuda_expr(x) for x in args]
-                _sample_value(em, op["kind"], a, kd, f"v{j}", dname)
+                _sample_value(em, op["kind"], a, kd, f"v{j}", dname, plan)
                 kd += 1
             for j, slot in enumerate(op["slots"]):
                 em(f"{roles[op['role']]}[{slot}] = v{j};")
@@ -357,20 +418,24 @@ def _emit_statements(em, ops, roles, dname="d"):
             em(f"const double s_ = fmin(H, {dname} - double(kk) * H);")
             em("const T s = T(s_);")
             em("const T hs = O::mul(T(0.5), s);  // `0.5 * s * k` == (0.5*s)*k")
-            em(f"T y0[{m}], k1[{m}], k2[{m}], k3[{m}], k4[{m}], st[{m}];")
+            em(f"T y0[{m}], k[{m}], acc[{m}], st[{m}];")
             for j, slot in enumerate(op["slots"]):
                 em(f"y0[{j}] = X[{slot}];")
-            em("deriv(y0, k1);")
-            em(f"for (int j = 0; j < {m}; ++j) st[j] = O::add(y0[j], O::mul(hs, k1[j]));")
-            em("deriv(st, k2);")
-            em(f"for (int j = 0; j < {m}; ++j) st[j] = O::add(y0[j], O::mul(hs, k2[j]));")
-            em("deriv(st, k3);")
-            em(f"for (int j = 0; j < {m}; ++j) st[j] = O::add(y0[j], O::mul(s, k3[j]));")
-            em("deriv(st, k4);")
-            em("const T s6 = O::div(s, T(6.0));")
+            # y0 + (s/6)(k1 + 2 k2 + 2 k3 + k4) with the sum accumulated as the
+            # stages complete: the same operations in the same order (numpy
+            # evaluates ((k1 + 2.0*k2) + 2.0*k3) + k4), fewer live registers
+            em("deriv(y0, k);")
+            em(f"for (int j = 0; j < {m}; ++j) {{ acc[j] = k[j]; st[j] = O::add(y0[j], O::mul(hs, k[j])); }}")
+            em("deriv(st, k);")
+            em(f"for (int j = 0; j < {m}; ++j) {{ acc[j] = O::add(acc[j], O::mul(T(2.0), k[j])); "
+               f"st[j] = O::add(y0[j], O::mul(hs, k[j])); }}")
+            em("deriv(st, k);")
+            em(f"for (int j = 0; j < {m}; ++j) {{ acc[j] = O::add(acc[j], O::mul(T(2.0), k[j])); "
+               f"st[j] = O::add(y0[j], O::mul(s, k[j])); }}")
+            em("deriv(st, k);")
+            em(f"const T s6 = O::divc(s, T(6.0), {_lit(1.0 / 6.0)});")
             for j, slot in enumerate(op["slots"]):
-                em(f"X[{slot}] = O::add(y0[{j}], O::mul(s6, O::add(O::add(O::add(k1[{j}], "
-                   f"O::mul(T(2.0), k2[{j}])), O::mul(T(2.0), k3[{j}])), k4[{j}])));")
+                em(f"X[{slot}] = O::add(y0[{j}], O::mul(s6, O::add(acc[{j}], k[{j}])));")
             em.end()
             em.end()
     return kd
@@ -437,7 +502,7 @@ def cuda_source(desc: dict) -> str:
     kdraw = len(transition_draws(desc))
     em(f"static constexpr int NX = {nx}, NW = {nw}, NWB = {max(nw, 1)}, KDRAW = {max(kdraw, 1)};")
     # transition sub-step
-    em("template <typename T, bool E>")
+    em("template <typename T, bool E, bool INJ>")
     em.block("__device__ static void substep(T (&X)[NX], T (&W)[NWB], const double* TH, const double* U, "
              "double d, const ssm::GenDraws<T>& dr, bool& perr)")
     em("using O = ssm::Ar<T, E>;")
@@ -463,7 +528,7 @@ def cuda_source(desc: dict) -> str:
     em("return total;")
     em.end()
     # initial block
-    em("template <typename T, bool E>")
+    em("template <typename T, bool E, bool INJ>")
     em.block("__device__ static void initial(T (&X)[NX], const double* TH, const ssm::GenDraws<T>& dr, bool& perr)")
     em("using O = ssm::Ar<T, E>;")
     em("(void)TH; (void)dr; (void)perr;")

@@ -118,6 +118,14 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, fl
   z1 = r * s;
 }
 
+// finite test on the exponent bits (integer pipe, keeps the FP64 pipe free)
+__device__ __forceinline__ bool finite_bits(double v) {
+  return (__double2hiint(v) & 0x7ff00000) != 0x7ff00000;
+}
+__device__ __forceinline__ bool finite_bits(float v) {
+  return (__float_as_int(v) & 0x7f800000) != 0x7f800000;
+}
+
 // ---------------------------------------------------------------------------
 // Arithmetic policy.  EXACT = the reference's op order with every operation
 // individually rounded (no FMA contraction): bitwise-equal to numpy float64
@@ -132,6 +140,9 @@ struct Ar<double, true> {
   static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
   static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
   static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  // division by a constant b with host-computed reciprocal rb: exact mode divides,
+  // fast mode multiplies (within 1 ulp more)
+  static __device__ __forceinline__ double divc(double a, double b, double rb) { return __ddiv_rn(a, b); }
 };
 template <>
 struct Ar<double, false> {
@@ -139,6 +150,9 @@ struct Ar<double, false> {
   static __device__ __forceinline__ double sub(double a, double b) { return a - b; }
   static __device__ __forceinline__ double mul(double a, double b) { return a * b; }
   static __device__ __forceinline__ double div(double a, double b) { return a / b; }
+  // division by a constant b with host-computed reciprocal rb: exact mode divides,
+  // fast mode multiplies (within 1 ulp more)
+  static __device__ __forceinline__ double divc(double a, double b, double rb) { return a * rb; }
 };
 template <>
 struct Ar<float, true> {
@@ -146,6 +160,9 @@ struct Ar<float, true> {
   static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
   static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
   static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  // division by a constant b with host-computed reciprocal rb: exact mode divides,
+  // fast mode multiplies (within 1 ulp more)
+  static __device__ __forceinline__ float divc(float a, float b, float rb) { return __fdiv_rn(a, b); }
 };
 template <>
 struct Ar<float, false> {
@@ -153,6 +170,9 @@ struct Ar<float, false> {
   static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
   static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
   static __device__ __forceinline__ float div(float a, float b) { return a / b; }
+  // division by a constant b with host-computed reciprocal rb: exact mode divides,
+  // fast mode multiplies (within 1 ulp more)
+  static __device__ __forceinline__ float divc(float a, float b, float rb) { return a * rb; }
 };
 
 // ---------------------------------------------------------------------------

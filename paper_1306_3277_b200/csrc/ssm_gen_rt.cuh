@@ -4,12 +4,12 @@
 // (core/ir.py:83-121).  The generated model provides, per particle:
 //
 //   NX, NW, NWB (= max(NW, 1)), KDRAW (draws per transition sub-step)
-//   substep<T, E>(X, W, TH, U, d, draws, perr)  one transition sub-step
+//   substep<T, E, INJ>(X, W, TH, U, d, draws, perr)  one transition sub-step
 //        (simulate.py:132-163: the block's statements in order, sample /
 //         assign / RK4 ode, with the reference's op order under E)
 //   obs_logpdf<T, E>(X, W, TH, U, Y, mask, perr) sum over present obs slots
 //        (simulate.py:166-193, distributions.py:94-123)
-//   initial<T, E>(X, TH, draws, perr)            the initial block
+//   initial<T, E, INJ>(X, TH, draws, perr)       the initial block
 //        (simulate.py:111-129)
 //
 // The kernels below are the generic counterparts of pw_kernel / init_kernel:
@@ -35,42 +35,38 @@ __device__ __forceinline__ T py_mod(T a, T b) {
 }
 
 // Draws of one (particle, grid step, sub-step).  Device mode: Philox4x32-10
-// counter {particle, step, sub << 8 | draw, kPurposeGen | retry << 8}; injected
-// mode (noise="host"): the reference's standard variates, [KDRAW][P] per sub-step.
+// blocks {particle, step, sub << 8 | block, kPurposeGen | retry << 8}; the
+// generated code takes each block once and spends its four words on two
+// Box-Muller pairs (four normals) or two 53-bit uniforms (codegen's draw plan).
+// Injected mode (noise="host"): the reference's standard variates, [KDRAW][P]
+// per sub-step, by draw index.
 template <typename T>
 struct GenDraws {
   uint32_t k0, k1, pg, step, sub;
   const T* inj;
   int P, p;
 
-  __device__ __forceinline__ U4 block(int kd, uint32_t retry) const {
-    return philox4x32_10(U4{pg, step, (sub << 8) | static_cast<uint32_t>(kd), kPurposeGen | (retry << 8)}, k0, k1);
+  __device__ __forceinline__ U4 block(int b, uint32_t retry = 0u) const {
+    return philox4x32_10(U4{pg, step, (sub << 8) | static_cast<uint32_t>(b), kPurposeGen | (retry << 8)}, k0, k1);
   }
-  // standard normal z (numpy normal(loc, scale) = loc + scale z)
-  __device__ __forceinline__ T normal(int kd) const {
-    if (inj) return inj[static_cast<size_t>(kd) * P + p];
-    const U4 r = block(kd, 0u);
-    float z0, z1;
-    box_muller(r.x, r.y, z0, z1);
-    return static_cast<T>(z0);
+  // the injected variate of draw kd (INJ), else the device value
+  template <bool INJ>
+  __device__ __forceinline__ T pick(int kd, T device_value) const {
+    if constexpr (INJ) return inj[static_cast<size_t>(kd) * P + p];
+    else return device_value;
   }
-  // U[0,1) (numpy uniform(low, high) = low + (high - low) U)
-  __device__ __forceinline__ T uniform(int kd) const {
-    if (inj) return inj[static_cast<size_t>(kd) * P + p];
-    const U4 r = block(kd, 0u);
-    return static_cast<T>(u53(r.x, r.y));
-  }
-  // standard gamma(shape) by Marsaglia-Tsang (device draws only); shape < 1
-  // through gamma(shape + 1) U^(1/shape)
+  // standard gamma(shape) by Marsaglia-Tsang (device draws only, own counters:
+  // block = draw index, retries 1..254, the shape < 1 boost uniform at 255);
+  // shape < 1 through gamma(shape + 1) U^(1/shape)
   __device__ __forceinline__ double std_gamma(int kd, double shape) const {
     double boost = 1.0;
     if (shape < 1.0) {
-      const U4 r = block(kd, 0u);
+      const U4 r = block(kd, 255u);
       boost = pow(1.0 - u53(r.z, r.w), 1.0 / shape);
       shape += 1.0;
     }
     const double dd = shape - 1.0 / 3.0, c = 1.0 / sqrt(9.0 * dd);
-    for (uint32_t it = 1; it < 256; ++it) {
+    for (uint32_t it = 1; it < 255; ++it) {
       const U4 r = block(kd, it);
       float z0, z1;
       box_muller(r.x, r.y, z0, z1);
@@ -86,7 +82,7 @@ struct GenDraws {
 };
 
 template <class M, typename T, bool E, bool INJ>
-__global__ void __launch_bounds__(kPwThreads) gen_pw_kernel(const ssm_pw_args A) {
+__global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args A) {
   pdl_wait();
   constexpr int NX = M::NX;
   const int b = blockIdx.y;
@@ -159,7 +155,7 @@ __global__ void __launch_bounds__(kPwThreads) gen_pw_kernel(const ssm_pw_args A)
                              static_cast<uint32_t>(k), INJ ? noise + static_cast<size_t>(k) * M::KDRAW * P : nullptr,
                              P, p};
         bool pe = false;
-        M::template substep<T, E>(x, w, th, U, S.d, dr, pe);
+        M::template substep<T, E, INJ>(x, w, th, U, S.d, dr, pe);
         if (pe && !perr) {
           perr = true;
           perr_sub = k;
@@ -167,7 +163,7 @@ __global__ void __launch_bounds__(kPwThreads) gen_pw_kernel(const ssm_pw_args A)
         if (A.check_finite && !bad) {
           bool ok = true;
 #pragma unroll
-          for (int n = 0; n < NX; ++n) ok &= isfinite(x[n]);
+          for (int n = 0; n < NX; ++n) ok &= finite_bits(x[n]);
           if (!ok) {
             bad = true;
             bad_sub = k;
@@ -220,7 +216,7 @@ __global__ void __launch_bounds__(kPwThreads)
     for (int n = 0; n < NX; ++n) X[n] = T(0);
     const GenDraws<T> dr{k0, k1, static_cast<uint32_t>(p + p_offset), 0u, 0u, nullptr, P, p};
     bool pe = false;
-    M::template initial<T, true>(X, th, dr, pe);
+    M::template initial<T, true, false>(X, th, dr, pe);
     perr |= pe;
 #pragma unroll
     for (int n = 0; n < NX; ++n) xb[static_cast<size_t>(n) * P + p] = X[n];

@@ -138,13 +138,6 @@ __device__ __forceinline__ void l96_rk4_fast(T x[8], const T Fn[8], T s) {
   for (int n = 0; n < 8; ++n) x[n] = fma(s6, acc[n] + k[n], x[n]);
 }
 
-// finite test on the exponent bits (integer pipe, keeps the FP64 pipe free)
-__device__ __forceinline__ bool finite_bits(double v) {
-  return (__double2hiint(v) & 0x7ff00000) != 0x7ff00000;
-}
-__device__ __forceinline__ bool finite_bits(float v) {
-  return (__float_as_int(v) & 0x7f800000) != 0x7f800000;
-}
 
 // One particle through one grid step (particle.py:110-111 / simulate.py:132-163):
 // the sub-steps of noise + RK4 / windkessel update, in place on x.  Shared by

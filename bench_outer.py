@@ -4,10 +4,12 @@
   config 3: PMMH on windkessel, 2^16-particle filters, chains batched per GPU (8 per GPU of 64)
   config 4: SMC^2 on L96, 128 theta-particles x 2^14 per GPU (of 1024), sparse obs
   config 5: L96 PF particle-count sweep 2^10 .. 2^26 (1 GPU)
+  config g: generic path: models lowered from the reference IR and compiled with
+            NVRTC -- L96 (against the hand-written kernel) and the two test models, P = 2^20
 
 Metric: particle-updates/s (P x grid steps, counting SMC^2 rejuvenation replays), device time
 with CUDA events around whole driver calls (host theta-level work included).
-Run: python bench_outer.py [--configs 1,3,4,5] [--quick]
+Run: python bench_outer.py [--configs 1,3,4,5,g] [--quick]
 """
 
 from __future__ import annotations
@@ -154,12 +156,49 @@ def config5(quick):
                       "history alone is 164 GiB)", "unit": "particle-updates/s", "results": out}
 
 
+def configg(quick):
+    from paper_1306_3277_b200 import LORENZ96, RngStream, generic
+    from paper_1306_3277_b200.inference import build_filter_grid, particle_filter
+    from oracle import ssm_oracle as O
+
+    with open(os.path.join(ROOT, "tests", "golden", "gen_models.json")) as fh:
+        lowered = json.load(fh)["lowered"]
+    g = dict(np.load(os.path.join(ROOT, "tests", "golden", "generic.npz")))
+
+    def model(name):
+        d = dict(lowered[name])
+        d.pop("fingerprint", None)
+        return generic.from_description(d)
+
+    P = 1 << (16 if quick else 20)
+    theta = np.array([10.0, 0.1])
+    times = np.linspace(0.0, 2.0, 41)
+    obs = O.simulate_l96(theta, times, O.Stream(1))
+    grid = build_filter_grid(0.0, 2.0, 40, times[1:], np.array([obs[k][0] for k in range(1, 41)]),
+                             np.ones((40, 8), bool), n_obs=8)
+    cases = [("Lorenz96 hand-written", LORENZ96, theta, grid), ("Lorenz96 generic", model("Lorenz96"), theta, grid)]
+    for name in ("StochVol", "PredatorPrey"):
+        m = model(name)
+        T = len(g[f"{name}/times"]) - 1
+        gr = build_filter_grid(0.0, float(g[f"{name}/times"][-1]), T, g[f"{name}/obs_t"], g[f"{name}/obs_v"],
+                               g[f"{name}/obs_m"], n_obs=m.n_obs)
+        cases.append((f"{name} generic", m, g[f"{name}/theta"], gr))
+    out = {}
+    for name, spec, th, gr in cases:
+        ms, res = timed(lambda: particle_filter(spec, th, gr, RngStream(7), n_particles=P, resampler="systematic",
+                                                exact=False), warmup=1, reps=3)
+        T = len(gr.times) - 1
+        out[name] = {"ms_per_filter": ms, "value": P * T / (ms / 1e3), "T": T, "loglik": res.loglik}
+    return {"config": f"g: generic (NVRTC) path, P=2^{int(math.log2(P))}, systematic, f64 fast",
+            "unit": "particle-updates/s", "results": out}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="1,3,4,5")
+    ap.add_argument("--configs", default="1,3,4,5,g")
     ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
-    fns = {"1": config1, "3": config3, "4": config4, "5": config5}
+    fns = {"1": config1, "3": config3, "4": config4, "5": config5, "g": configg}
     for c in args.configs.split(","):
         t0 = time.time()
         r = fns[c](args.quick)

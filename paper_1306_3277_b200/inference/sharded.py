@@ -19,6 +19,8 @@ grid step.
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -89,12 +91,18 @@ class ShardedParticleFilter:
         cap = self.spill_cap
         xbuf = torch.empty((spec.nx, Pl + cap), dtype=tdt, device=dev)
         x0 = torch.empty((spec.nx, Pl), dtype=tdt, device=dev)
-        _lib.check(L.ssm_init_particles(spec.kernel, self.dtype_id, 1, Pl, off, _lib.ptr(keys0), _lib.ptr(x0), stream),
-                   "ssm_init_particles")
+        theta = torch.from_numpy(spec.derived(self.theta)).to(dev)
+        generic = spec.kernel == _lib.SSM_MODEL_GENERIC
+        if generic:  # the model's initial block, global particle indices (the draws match one process)
+            _lib.check(L.ssm_gen_init_particles(C.c_void_p(spec.handle(dev)), self.dtype_id, 1, Pl, off,
+                                                _lib.ptr(keys0), _lib.ptr(theta), spec.theta_stride, _lib.ptr(x0),
+                                                None, stream), "ssm_gen_init_particles")
+        else:
+            _lib.check(L.ssm_init_particles(spec.kernel, self.dtype_id, 1, Pl, off, _lib.ptr(keys0), _lib.ptr(x0),
+                                            stream), "ssm_init_particles")
         xbuf[:, :Pl] = x0
         x = xbuf[:, :Pl]
         fs = _fs_init(1, dev)
-        theta = torch.from_numpy(spec.derived(self.theta)).to(dev)
         pw_ws = torch.empty(L.ssm_pw_workspace_bytes(1, Pl), dtype=torch.uint8, device=dev)
         sw = torch.empty(L.ssm_sharded_workspace_bytes(1, Pl, P), dtype=torch.uint8, device=dev)
         cdf = torch.empty(Pl, dtype=torch.int64, device=dev)
@@ -115,6 +123,8 @@ class ShardedParticleFilter:
         A.ess_rel = ess_rel
         A.theta, A.keys, A.fs, A.workspace = theta.data_ptr(), keys1.data_ptr(), fs.data_ptr(), pw_ws.data_ptr()
         A.p_offset = off
+        if generic:
+            A.gen, A.theta_stride = spec.handle(dev), spec.theta_stride
 
         hist = [(x, None)]  # (x_i [nx, Pl], global ancestor index [Pl] int64 | None)
         a_last = None

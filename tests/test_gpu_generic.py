@@ -193,3 +193,31 @@ def test_generic_l96_pmmh_with_initial_proposals_matches_reference():
     np.testing.assert_array_equal(np.array([c.theta for c in chains]), g["l96/mh/thetas"])
     np.testing.assert_array_equal(np.array([c.init_state for c in chains]), g["l96/mh/inits"])
     np.testing.assert_allclose([c.loglik for c in chains], g["l96/mh/logliks"], rtol=1e-12)
+
+
+def test_generic_l96_ess_gate_and_sparse_obs_bitwise_reference():
+    """ESS-gated resampling and a sparse observation mask (4 of 8 slots, every
+    other step) through the generic kernel with the reference's draws."""
+    g = load_golden("pf.npz")
+    m = model("Lorenz96")
+    out = particle_filter(m, g["l96/theta"], _l96_grid(g), RngStream(9), n_particles=256, resampler="systematic",
+                          ess_rel=0.5, noise="host")
+    assert abs(out.loglik - float(g["l96/ess/loglik"])) <= 1e-12 * abs(float(g["l96/ess/loglik"]))
+    np.testing.assert_array_equal(out.trajectory, g["l96/ess/traj"])
+    grid = build_filter_grid(0.0, 2.0, 20, g["l96/obs_t"], g["l96s/obs_v"], g["l96s/obs_m"], n_obs=8)
+    out = particle_filter(m, g["l96/theta"], grid, RngStream(8), n_particles=128, resampler="systematic",
+                          noise="host")
+    assert abs(out.loglik - float(g["l96s/loglik"])) <= 1e-12 * abs(float(g["l96s/loglik"]))
+    np.testing.assert_array_equal(out.trajectory, g["l96s/traj"])
+
+
+def test_generic_sharded_one_rank_equals_particle_filter():
+    from paper_1306_3277_b200.inference import particle_filter_sharded
+
+    g = load_golden("generic.npz")
+    m, grid = _grid(g, "StochVol")
+    th = g["StochVol/theta"]
+    ll, traj = particle_filter_sharded(m, th, grid, RngStream(31), 1 << 14, resampler="systematic")
+    out = particle_filter(m, th, grid, RngStream(31), n_particles=1 << 14, resampler="systematic", exact=False)
+    assert ll == out.loglik
+    np.testing.assert_array_equal(traj, out.trajectory)

@@ -98,7 +98,8 @@ typedef struct ssm_filter_state {
   int32_t err_param;      /* generic models: min(step*64 + sub-step) where a distribution
                              argument was invalid (DistributionParameterError,
                              distributions.py:53-69), else INT32_MAX */
-  int32_t pad[2];
+  uint32_t prefix_done;   /* completion counter of the resample's tile-prefix pass (reset by the kernel) */
+  int32_t pad;
 } ssm_filter_state;
 
 /* Arguments of the fused propagate + weight step (kernels K1/K2).
@@ -245,9 +246,11 @@ int ssm_resample_search(int B, int P_in, int P_out, int scheme, int cum_kind, co
  * look-back and no searches; multinomial: look-back scan + binary search. */
 size_t ssm_resample_workspace_bytes(int B, int P);
 /* Filter fast path: ancestors from the tile records + cdf_local written by the
- * weighted ssm_propagate_weight (systematic / stratified only): tile scale +
- * exact integer prefix (1 block per filter) -> offspring bounds + partition
- * -> expand.  Global CDF: C_j = prefix_b + round(exp(m_b - incr) 2^9 cdf_local_j). */
+ * weighted ssm_propagate_weight (systematic / stratified; sorted multinomial
+ * with device keys): tile scale + in-block prefix, with the exact block prefix
+ * done by the last block of each filter (fs.prefix_done) -> offspring counts
+ * that write the ancestors (window fill in shared memory) -> long-run fill.
+ * Global CDF: C_j = prefix_b + round(exp(m_b - incr) 2^9 cdf_local_j). */
 int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf_local, const void* tile_rec,
                             const ssm_filter_state* fs, const double* u, const uint32_t* keys,
                             int step, int32_t* anc, void* workspace, void* stream);

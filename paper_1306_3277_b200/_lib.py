@@ -60,7 +60,8 @@ FILTER_STATE_DTYPE = np.dtype(
         ("err_degenerate", "<i4"),
         ("blocks_done", "<u4"),
         ("err_param", "<i4"),
-        ("pad", "<i4", (2,)),
+        ("prefix_done", "<u4"),
+        ("pad", "<i4"),
     ]
 )
 assert FILTER_STATE_DTYPE.itemsize == 64

@@ -429,12 +429,63 @@ struct OffspringConsts {
   double inv, tscale, u_sys, invP;
 };
 
+// Exclusive prefix of one filter's block totals in place, the filter total and
+// (oc != nullptr) the offspring kernel's per-filter constants; one block of NT threads.
+template <int NT>
+__device__ __forceinline__ void filter_block_prefix(int nblk, uint64_t* __restrict__ bb, uint64_t* __restrict__ totals,
+                                                    int b, OffspringConsts* __restrict__ oc, int P,
+                                                    const double* __restrict__ u, const uint32_t* __restrict__ keys,
+                                                    int step) {
+  const int per = (nblk + NT - 1) / NT;
+  const int t0 = threadIdx.x * per, t1 = min(t0 + per, nblk);
+  uint64_t local = 0;
+  for (int t = t0; t < t1; ++t) local += __ldcg(bb + t);
+  __shared__ uint64_t wsum[NT / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  uint64_t wex = 0, tot = 0;
+  for (int w = 0; w < NT / 32; ++w) {
+    if (w < warp) wex += wsum[w];
+    tot += wsum[w];
+  }
+  uint64_t run = wex + incl - local;
+  for (int t = t0; t < t1; ++t) {
+    const uint64_t x = __ldcg(bb + t);
+    bb[t] = run;
+    run += x;
+  }
+  if (threadIdx.x == 0) {
+    totals[b] = tot;
+    if (oc) {  // the offspring kernel's per-filter constants, computed once
+      const double inv = 1.0 / static_cast<double>(tot);
+      const double Pd = static_cast<double>(P);
+      const double us = u ? u[b] : (keys ? device_uniform(keys[2 * b], keys[2 * b + 1], 0u, step, kPurposeSystematic) : 0.0);
+      oc[b] = OffspringConsts{inv, Pd * inv, us, 1.0 / Pd};
+    }
+  }
+}
+
+// Per-warp-tile scale and exclusive in-block prefix (one record per thread) and
+// block totals.  With `fs_rw` (the filter path) the last block of each filter to
+// finish (completion counter fs.prefix_done) also turns the block totals into
+// exclusive block prefixes, so the offspring kernel follows directly.
 __global__ void __launch_bounds__(kThreads)
 tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_filter_state* __restrict__ fs,
                   double* __restrict__ scale, uint64_t* __restrict__ prel, uint64_t* __restrict__ blk_tot,
-                  uint32_t* __restrict__ long_count = nullptr, int gate = 1) {
+                  uint32_t* __restrict__ long_count = nullptr, int gate = 1, ssm_filter_state* fs_rw = nullptr,
+                  uint64_t* __restrict__ totals = nullptr, OffspringConsts* __restrict__ oc = nullptr, int P = 0,
+                  const double* __restrict__ u = nullptr, const uint32_t* __restrict__ keys = nullptr,
+                  int step = 0) {
   pdl_wait();
   __shared__ uint64_t warp_tot[kThreads / 32];
+  __shared__ bool s_last;
   const int b = blockIdx.y, blk = blockIdx.x;
   if (gate && !fs[b].resample_now) return;
   if (long_count && blk == 0 && threadIdx.x == 0) long_count[b] = 0u;  // long-run list of this resample
@@ -466,6 +517,16 @@ tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_fi
   }
   if (e < ntiles) prel[off] = wex + incl - qg;  // exclusive, exact integer
   if (threadIdx.x == 0) blk_tot[static_cast<size_t>(b) * gridDim.x + blk] = tot;
+  if (!fs_rw) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&fs_rw[b].prefix_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  filter_block_prefix<kThreads>(gridDim.x, blk_tot + static_cast<size_t>(b) * gridDim.x, totals, b, oc, P, u, keys,
+                                step);
+  if (threadIdx.x == 0) fs_rw[b].prefix_done = 0u;
 }
 
 __global__ void __launch_bounds__(1024)
@@ -475,41 +536,7 @@ blk_prefix_kernel(int nblk, uint64_t* __restrict__ blk, uint64_t* __restrict__ t
   pdl_wait();
   const int b = blockIdx.x;
   if (fs && !fs[b].resample_now) return;
-  uint64_t* bb = blk + static_cast<size_t>(b) * nblk;
-  const int per = (nblk + 1023) / 1024;
-  const int t0 = threadIdx.x * per, t1 = min(t0 + per, nblk);
-  uint64_t local = 0;
-  for (int t = t0; t < t1; ++t) local += bb[t];
-  __shared__ uint64_t wsum[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t incl = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  uint64_t wex = 0, tot = 0;
-  for (int w = 0; w < 32; ++w) {
-    if (w < warp) wex += wsum[w];
-    tot += wsum[w];
-  }
-  uint64_t run = wex + incl - local;
-  for (int t = t0; t < t1; ++t) {
-    const uint64_t x = bb[t];
-    bb[t] = run;
-    run += x;
-  }
-  if (threadIdx.x == 0) {
-    totals[b] = tot;
-    if (oc) {  // the offspring kernel's per-filter constants, computed once
-      const double inv = 1.0 / static_cast<double>(tot);
-      const double Pd = static_cast<double>(P);
-      const double us = u ? u[b] : (keys ? device_uniform(keys[2 * b], keys[2 * b + 1], 0u, step, kPurposeSystematic) : 0.0);
-      oc[b] = OffspringConsts{inv, Pd * inv, us, 1.0 / Pd};
-    }
-  }
+  filter_block_prefix<1024>(nblk, blk + static_cast<size_t>(b) * nblk, totals, b, oc, P, u, keys, step);
 }
 
 // c_j for every particle + merge-path partition entries
@@ -1584,11 +1611,11 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
   // filled by long_runs_kernel.  All four are programmatic dependent launches.
   uint32_t* long_count = reinterpret_cast<uint32_t*>(w.totals) + 2 * static_cast<size_t>(B);  // after totals
   int4* long_runs = reinterpret_cast<int4*>(w.cnt);
-  launch_pdl(tile_scale_kernel, dim3(nblk, B), dim3(kThreads), s, nt, static_cast<const ssm_tile_rec*>(tile_rec), fs,
-             scale, pref, blk, long_count, 1);
   // per-filter offspring constants after the totals / long-run counts / spacing totals
   OffspringConsts* oc = reinterpret_cast<OffspringConsts*>(w.totals + 3 * static_cast<size_t>(B));
-  launch_pdl(blk_prefix_kernel, dim3(B), dim3(1024), s, nblk, blk, w.totals, fs, oc, P, u, keys, step);
+  // tile scale + in-block prefix, and (last block per filter) the block prefix and constants
+  launch_pdl(tile_scale_kernel, dim3(nblk, B), dim3(kThreads), s, nt, static_cast<const ssm_tile_rec*>(tile_rec), fs,
+             scale, pref, blk, long_count, 1, const_cast<ssm_filter_state*>(fs), w.totals, oc, P, u, keys, step);
   const dim3 g(scan_tiles(P), B);
   if (scheme == SSM_MULTINOMIAL_SORTED) {  // spacing sums in w.sums (doubles), totals after the u64 totals
     const int nsb = (P + 1 + kScanTile - 1) / kScanTile;

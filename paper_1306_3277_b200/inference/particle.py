@@ -435,12 +435,12 @@ def init_runs(runs, rngs):
     return runs
 
 
-# kernels per resample: tiles = tile scale, block prefix, offspring, long runs
-# (sorted multinomial: tile scale, block prefix, spacing sums, spacing prefix,
-# merge); logw multinomial = scan, search; logw sorted multinomial = scan,
+# kernels per resample: tiles = tile scale (+ block prefix in its last block),
+# offspring, long runs (sorted multinomial: tile scale, spacing sums, spacing
+# prefix, merge); logw multinomial = scan, search; logw sorted multinomial = scan,
 # spacing sums, spacing prefix, merge; logw systematic/stratified = tile sums,
 # tile prefix, offspring, expand
-_RS_LAUNCHES = {("tiles", 1): 4, ("tiles", 2): 4, ("tiles", 3): 5,
+_RS_LAUNCHES = {("tiles", 1): 3, ("tiles", 2): 3, ("tiles", 3): 4,
                 ("logw", 0): 2, ("logw", 1): 4, ("logw", 2): 4, ("logw", 3): 4}
 
 

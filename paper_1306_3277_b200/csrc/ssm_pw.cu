@@ -238,7 +238,7 @@ template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE = false>
 // NOTE: plain __launch_bounds__(kThreads).  An explicit minBlocks of 1 lets
 // ptxas spend 172 registers on the SIMPLE f64 kernel (1 CTA/SM, 0.80 ms
 // vs 0.63 ms at 119 registers / 2 CTAs); minBlocks 3 (<= 85) is also slower.
-__global__ void __launch_bounds__(kPwThreads, (SIMPLE && sizeof(T) == 4) ? 3 : 2) pw_kernel(const ssm_pw_args A) {
+__global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 : ((SIMPLE && sizeof(T) == 4) ? 3 : 2)) pw_kernel(const ssm_pw_args A) {
   pdl_wait();
   using O = Ar<T, E>;
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;

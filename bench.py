@@ -252,12 +252,23 @@ def _cpu_filter_task(a):
     return time.perf_counter() - t0
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
 def cpu_baseline_single(P=1 << 20, T=10):
     """The oracle port on one host core (numpy is single-threaded here)."""
     dt = _cpu_filter_task((P, T, 0))
     return {"value": P * T / dt, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"oracle port (numpy restatement of ssmkit particle_filter), L96, P=2^{int(math.log2(P))}, "
-                      f"T={T} steps, systematic, float64, {dt:.1f} s"}
+                      f"T={T} steps, systematic, float64, {dt:.1f} s, one core of {cpu_model()}"}
 
 
 def run_reference(args):
@@ -277,7 +288,7 @@ def run_reference(args):
     ms = 1e3 * float(np.mean(walls))
     value = cores * P * T / (ms / 1e3)
     sample = (f"{cores} processes x oracle port (numpy restatement of ssmkit particle_filter), L96, "
-              f"P=2^{int(math.log2(P))} each, T={T} steps, systematic, float64")
+              f"P=2^{int(math.log2(P))} each, T={T} steps, systematic, float64, {cores} cores of {cpu_model()}")
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -361,7 +372,10 @@ def main():
     achieved = pw["bytes"] / (pw["total_ms"] / 1e3) / 1e9 if pw else None
     traffic = load_traffic()
     kern = {k: {"avg_ms": round(v["avg_ms"], 4), "launches": v["launches"],
-                "GB/s": round(v["bytes"] / (v["total_ms"] / 1e3) / 1e9, 1)} for k, v in res["kern"].items()}
+                "GB/s": round(v["bytes"] / (v["total_ms"] / 1e3) / 1e9, 1),
+                "frac": round(v["bytes"] / (v["total_ms"] / 1e3) / 1e9 / peak, 3),
+                "algorithmic_bytes_per_particle": round(v["bytes"] / max(v["launches"], 1) / P, 2)}
+            for k, v in res["kern"].items()}
     dtype_tag = "f64" if args.dtype == "float64" else "f32"
     arith = "bitwise reference op order" if args.exact else "float64 with FMA contraction (1e-12 of reference per step)"
     line = {

@@ -444,6 +444,13 @@ _RS_LAUNCHES = {("tiles", 1): 3, ("tiles", 2): 3, ("tiles", 3): 4,
                 ("logw", 0): 2, ("logw", 1): 4, ("logw", 2): 4, ("logw", 3): 4}
 
 
+def _tile_resample_bytes(scheme):
+    """Algorithmic bytes per particle of a tile-path resample: cdf_local read (8),
+    ancestor write (4), tile records / scales / prefixes (1.5); the sorted
+    multinomial also writes and reads its spacing prefixes (16)."""
+    return 13.5 + (16.0 if scheme == _lib.SSM_MULTINOMIAL_SORTED else 0.0)
+
+
 def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe, x_arena, a_arena,
                     cdf_local, tile_rec, rs_ws, tiles_ok, scheme, esz, new_hist, stream):
     """One ssm_advance call for all steps (device noise).  Returns (x_prev,
@@ -494,7 +501,7 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
         if timer is not None:
             has_obs = bool(desc["has_obs"][k])
             if an is not None:
-                rs_bytes = B * P * ((8 + 4 + 4 + 4) if tiles_ok else (2 * esz + 12))
+                rs_bytes = int(B * P * (_tile_resample_bytes(scheme) if tiles_ok else (2 * esz + 12)))
                 timer.add("resample", evs[4 * k], evs[4 * k + 1], rs_bytes)
             nbytes = B * P * (2 * spec.nx * esz + (4 if an is not None else 0)
                               + ((esz + (8 if tiles_ok else 0)) if has_obs else 0))
@@ -657,7 +664,7 @@ def advance_runs(runs, upto, rngs):
                 u_t = torch.from_numpy(u).to(dev)
             if tiles_ok:
                 # bytes: cdf_local read + c write/read + anc write (+ tile records, negligible)
-                with profiling.maybe("resample", B * P * (8 + 4 + 4 + 4)):
+                with profiling.maybe("resample", int(B * P * _tile_resample_bytes(scheme))):
                     _lib.check(L.ssm_resample_from_tiles(B, P, scheme, _lib.ptr(cdf_local), _lib.ptr(tile_rec),
                                                          _lib.ptr(fs), _lib.ptr(u_t), _lib.ptr(keys_t), i,
                                                          _lib.ptr(anc), _lib.ptr(rs_ws), stream),

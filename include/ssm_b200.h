@@ -147,6 +147,10 @@ typedef struct ssm_pw_args {
   const void* gen;      /* SSM_MODEL_GENERIC: the ssm_gen_compile handle, else NULL */
   int32_t theta_stride; /* doubles per filter in theta (0: 4, the hand-written kernels) */
   int32_t gen_pad;
+  const double* y_vec;  /* generic models, nullable: observation values [n_obs] (<= 32) of this step
+                           (device); NULL: y[] */
+  const double* u_vec;  /* generic models, nullable: inputs [n_sub + 1][n_input] (device): one row per
+                           sub-step start (simulate.py:150), then the observation time; NULL: u_in / u_obs */
 } ssm_pw_args;
 
 /* hint: subs[0] is the only sub-step and holds exactly one RK4 step (n_ode == 1) */
@@ -182,7 +186,8 @@ int ssm_propagate_weight(const ssm_pw_args* args, void* stream);
  * The handle is used through ssm_pw_args.gen (model = SSM_MODEL_GENERIC) by
  * ssm_propagate_weight / ssm_advance, and by ssm_gen_init_particles (the
  * model's `initial` block on the device).  Limits: n_state <= 32,
- * n_obs <= 8, n_input <= 1, <= 255 draws per sub-step. */
+ * n_obs <= 32, n_input <= 16 (vectors through ssm_pw_args.y_vec / u_vec),
+ * <= 255 Philox blocks per sub-step. */
 int ssm_gen_compile(const char* source, const char* include_dir, void** out, char* log, size_t log_len);
 int ssm_gen_check(const char* source, const char* include_dir, char* log, size_t log_len);
 int ssm_gen_destroy(void* handle);
@@ -272,6 +277,8 @@ typedef struct ssm_step_desc {
   int32_t pad;
   double y[8];
   double u_obs;
+  int64_t y_off;        /* offset (doubles) of the step's y_vec in ssm_advance_args.y_table, or -1 */
+  int64_t u_off;        /* offset (doubles) of the step's u_vec in ssm_advance_args.u_table, or -1 */
 } ssm_step_desc;
 
 typedef struct ssm_advance_args {
@@ -299,6 +306,8 @@ typedef struct ssm_advance_args {
   int32_t a_ring;            /* 0: a_arena has a slot per weighted step; r > 0: weighted step w writes
                                 slot w % r (only the last weighted step's log-weights are read later) */
   void* const* events;       /* HOST, nullable: 4 cudaEvent_t per step (resample start/end, pw start/end) */
+  const double* y_table;     /* device, nullable: per-step observation vectors (ssm_step_desc.y_off) */
+  const double* u_table;     /* device, nullable: per-step input rows (ssm_step_desc.u_off) */
 } ssm_advance_args;
 
 int ssm_advance(ssm_advance_args* args, void* stream);

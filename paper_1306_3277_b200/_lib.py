@@ -106,6 +106,8 @@ class PwArgs(C.Structure):
         ("gen", C.c_void_p),
         ("theta_stride", C.c_int32),
         ("gen_pad", C.c_int32),
+        ("y_vec", C.c_void_p),
+        ("u_vec", C.c_void_p),
     ]
 
 
@@ -123,14 +125,16 @@ class StepDesc(C.Structure):
         ("pad", C.c_int32),
         ("y", C.c_double * 8),
         ("u_obs", C.c_double),
+        ("y_off", C.c_int64),
+        ("u_off", C.c_int64),
     ]
 
 
 STEP_DESC_DTYPE = np.dtype(
     [("step", "<i4"), ("n_sub", "<i4"), ("subs_offset", "<i8"), ("has_obs", "<i4"), ("obs_mask", "<u4"),
-     ("hints", "<i4"), ("pad", "<i4"), ("y", "<f8", (8,)), ("u_obs", "<f8")]
+     ("hints", "<i4"), ("pad", "<i4"), ("y", "<f8", (8,)), ("u_obs", "<f8"), ("y_off", "<i8"), ("u_off", "<i8")]
 )
-assert STEP_DESC_DTYPE.itemsize == C.sizeof(StepDesc) == 104
+assert STEP_DESC_DTYPE.itemsize == C.sizeof(StepDesc) == 120
 
 
 class AdvanceArgs(C.Structure):
@@ -156,6 +160,8 @@ class AdvanceArgs(C.Structure):
         ("a_last_index", C.c_int32),
         ("a_ring", C.c_int32),
         ("events", C.c_void_p),
+        ("y_table", C.c_void_p),
+        ("u_table", C.c_void_p),
     ]
 
 

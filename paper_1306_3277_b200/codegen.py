@@ -21,7 +21,7 @@ From the trees:
     simulate.py:71-93; log-densities as distributions.py:94-123), with every
     arithmetic op individually rounded under `E` (exact mode).
 
-Limits of the device path: n_state <= 32, n_obs <= 8, n_input <= 1.
+Limits of the device path: n_state <= 32, n_obs <= 32, n_input <= 16.
 """
 
 from __future__ import annotations
@@ -35,7 +35,7 @@ import numpy as np
 
 from .errors import UnsupportedModelError
 
-MAX_STATE, MAX_OBS, MAX_INPUT = 32, 8, 1
+MAX_STATE, MAX_OBS, MAX_INPUT = 32, 32, 16
 
 # distributions.py:33-46 (canonical argument order and defaults)
 DIST_PARAMS = {
@@ -500,7 +500,8 @@ def cuda_source(desc: dict) -> str:
     em("struct Model {")
     em.ind = 2
     kdraw = len(transition_draws(desc))
-    em(f"static constexpr int NX = {nx}, NW = {nw}, NWB = {max(nw, 1)}, KDRAW = {max(kdraw, 1)};")
+    em(f"static constexpr int NX = {nx}, NW = {nw}, NWB = {max(nw, 1)}, NU = {max(c['input'], 1)}, "
+       f"KDRAW = {max(kdraw, 1)};")
     # transition sub-step
     em("template <typename T, bool E, bool INJ>")
     em.block("__device__ static void substep(T (&X)[NX], T (&W)[NWB], const double* TH, const double* U, "
@@ -533,7 +534,7 @@ def cuda_source(desc: dict) -> str:
     em("using O = ssm::Ar<T, E>;")
     em("(void)TH; (void)dr; (void)perr;")
     em("T W[NWB] = {};")
-    em("const double U[1] = {0.0};")
+    em("const double U[NU] = {};")
     em("(void)W; (void)U;")
     for op in desc["initial"]:
         if op["op"] == "ode" or op["role"] != "state":

@@ -59,6 +59,8 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
     pw.obs_mask = d.obs_mask;
     for (int n = 0; n < 8; ++n) pw.y[n] = d.y[n];
     pw.u_obs = d.u_obs;
+    pw.y_vec = (A->y_table && d.y_off >= 0) ? A->y_table + d.y_off : nullptr;
+    pw.u_vec = (A->u_table && d.u_off >= 0) ? A->u_table + d.u_off : nullptr;
     void* a_out = nullptr;
     const int a_slot = A->a_ring > 0 ? slot % A->a_ring : slot;
     if (d.has_obs) a_out = static_cast<char*>(A->a_arena) + static_cast<size_t>(a_slot) * astep;

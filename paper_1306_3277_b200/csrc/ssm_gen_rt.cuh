@@ -3,7 +3,7 @@
 // paper_1306_3277_b200/codegen.py lowers from a reference ModelIr
 // (core/ir.py:83-121).  The generated model provides, per particle:
 //
-//   NX, NW, NWB (= max(NW, 1)), KDRAW (draws per transition sub-step)
+//   NX, NW, NWB (= max(NW, 1)), NU (inputs), KDRAW (draws per transition sub-step)
 //   substep<T, E, INJ>(X, W, TH, U, d, draws, perr)  one transition sub-step
 //        (simulate.py:132-163: the block's statements in order, sample /
 //         assign / RK4 ode, with the reference's op order under E)
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args
       for (int n = 0; n < M::NWB; ++n) w[n] = T(0);
       for (int k = 0; k < A.n_sub; ++k) {
         const ssm_substep& S = A.subs[k];
-        const double U[1] = {S.u_in};
+        const double* U = A.u_vec ? A.u_vec + static_cast<size_t>(k) * M::NU : &S.u_in;
         const GenDraws<T> dr{k0, k1, static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
                              static_cast<uint32_t>(k), INJ ? noise + static_cast<size_t>(k) * M::KDRAW * P : nullptr,
                              P, p};
@@ -176,9 +176,10 @@ __global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args
         T w0[M::NWB];  // observe_logpdf sees a zero noise array (simulate.py:181)
 #pragma unroll
         for (int n = 0; n < M::NWB; ++n) w0[n] = T(0);
-        const double Uo[1] = {A.u_obs};
+        const double* Uo = A.u_vec ? A.u_vec + static_cast<size_t>(A.n_sub) * M::NU : &A.u_obs;
+        const double* Y = A.y_vec ? A.y_vec : A.y;
         bool pe = false;
-        const T g = M::template obs_logpdf<T, E>(x, w0, th, Uo, A.y, A.obs_mask, pe);
+        const T g = M::template obs_logpdf<T, E>(x, w0, th, Uo, Y, A.obs_mask, pe);
         if (pe && !perr) {
           perr = true;
           perr_sub = 63;  // the observation density at this step

@@ -75,6 +75,15 @@ def substep_schedule(t, dt, delta):
     return [(t + k * delta, min(delta, t_end - (t + k * delta))) for k in range(n_sub)]
 
 
+def _input_vector(inputs, t, n_input, width):
+    """Input values at t (InputProvider.at, timeseries.py:205-210), zero-padded to width."""
+    out = np.zeros(width)
+    if inputs is not None and n_input:
+        v = np.asarray(inputs.at(t) if hasattr(inputs, "at") else inputs, dtype=float).reshape(-1)
+        out[:n_input] = v[:n_input]
+    return out
+
+
 def _input_value(inputs, t):
     if inputs is None:
         return 0.0
@@ -90,6 +99,7 @@ class Schedule:
         times = grid.times
         S = len(times) - 1
         recs, self.offsets, self.n_sub, self.sub_end = [], [0] * (S + 1), [0] * (S + 1), [None] * (S + 1)
+        self.sub_start = [None] * (S + 1)
         self.host_subs = [None] * (S + 1)
         self.obs = [None] * (S + 1)
         self.single = [False] * (S + 1)
@@ -117,6 +127,7 @@ class Schedule:
             self.n_sub[i] = len(subs)
             self.single[i] = len(subs) == 1 and (not spec.has_ode or int(arr[0]["n_ode"]) == 1)
             self.sub_end[i] = ends
+            self.sub_start[i] = [t_k for t_k, _ in subs]
             self.host_subs[i] = arr
             recs.extend(arr)
             o = grid.obs_at(i)
@@ -126,18 +137,44 @@ class Schedule:
                 mask = np.asarray(mask, dtype=bool)
                 bits = 0
                 yy = np.zeros(8)
-                for n in range(spec.n_obs):
+                for n in range(min(spec.n_obs, 8)):
                     if mask[n]:
                         bits |= 1 << n
                         yy[n] = y[n]
                 u_obs = _input_value(inputs, t1) if spec.n_input else 0.0
                 self.obs[i] = (bits, yy, u_obs)
+        # generic models: per-step observation vectors and input rows in device tables
+        # (ssm_pw_args.y_vec / u_vec; the fixed y[8] / u_in fields cover the hand-written kernels)
+        self.y_off = [-1] * (S + 1)
+        self.u_off = [-1] * (S + 1)
+        ytab, utab = [], []
+        if spec.kernel == _lib.SSM_MODEL_GENERIC:
+            nu = max(spec.n_input, 1)
+            for i in range(1, S + 1):
+                rows = [_input_vector(inputs, t_k, spec.n_input, nu) for t_k in self.sub_start[i]]
+                o = grid.obs_at(i)
+                rows.append(_input_vector(inputs, times[i], spec.n_input, nu) if o is not None else np.zeros(nu))
+                self.u_off[i] = len(utab)
+                utab.extend(np.concatenate(rows))
+                if o is not None:
+                    self.y_off[i] = len(ytab)
+                    yv = np.zeros(max(spec.n_obs, 1))
+                    yv[: spec.n_obs] = np.where(np.asarray(o[1], dtype=bool), np.asarray(o[0], dtype=float), 0.0)
+                    ytab.extend(yv)
+                    bits = 0
+                    for n in range(spec.n_obs):
+                        if o[1][n]:
+                            bits |= 1 << n
+                    self.obs[i] = (bits, self.obs[i][1], self.obs[i][2])
+        self.y_table = torch.tensor(ytab if ytab else [0.0], dtype=torch.float64, device=device)
+        self.u_table = torch.tensor(utab if utab else [0.0], dtype=torch.float64, device=device)
         # native-driver step descriptors (ssm_step_desc), one per grid index
         self.desc = np.zeros(S + 1, dtype=_lib.STEP_DESC_DTYPE)
         for i in range(1, S + 1):
             d = self.desc[i]
             d["step"], d["n_sub"], d["subs_offset"] = i, self.n_sub[i], self.offsets[i]
             d["hints"] = _lib.SSM_HINT_SINGLE_SUBSTEP if self.single[i] else 0
+            d["y_off"], d["u_off"] = self.y_off[i], self.u_off[i]
             if self.obs[i] is not None:
                 d["has_obs"], d["obs_mask"] = 1, self.obs[i][0]
                 d["y"] = self.obs[i][1]
@@ -146,6 +183,12 @@ class Schedule:
         table = np.array(recs, dtype=_lib.SUBSTEP_DTYPE) if recs else np.zeros(1, _lib.SUBSTEP_DTYPE)
         self.table = torch.from_numpy(table.view(np.uint8).copy()).to(device)
         self.times = times
+
+    def y_ptr(self, i):
+        return None if self.y_off[i] < 0 else self.y_table.data_ptr() + 8 * self.y_off[i]
+
+    def u_ptr(self, i):
+        return None if self.u_off[i] < 0 else self.u_table.data_ptr() + 8 * self.u_off[i]
 
     def subs_ptr(self, i):
         return self.table.data_ptr() + self.offsets[i] * _lib.SUBSTEP_DTYPE.itemsize
@@ -484,6 +527,7 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
     A.tile_rec = tile_rec.data_ptr() if tile_rec is not None else None
     A.resample_ws = rs_ws.data_ptr()
     A.anc_used = anc_used.ctypes.data
+    A.y_table, A.u_table = sched.y_table.data_ptr(), sched.u_table.data_ptr()
     timer = profiling.active()
     evs = None
     if timer is not None:
@@ -691,6 +735,7 @@ def advance_runs(runs, upto, rngs):
         args.n_sub = n_sub
         args.hints = _lib.SSM_HINT_SINGLE_SUBSTEP if (sched.single[i] and not _NO_HINTS) else 0
         args.subs = sched.subs_ptr(i)
+        args.y_vec, args.u_vec = sched.y_ptr(i), sched.u_ptr(i)
         args.x_in = x_prev.data_ptr()
         args.x_out = x_out.data_ptr()
         args.anc = anc.data_ptr() if anc is not None else None

@@ -144,6 +144,7 @@ class ShardedParticleFilter:
             A.step, A.n_sub = i, sched.n_sub[i]
             A.hints = _lib.SSM_HINT_SINGLE_SUBSTEP if sched.single[i] else 0
             A.subs = sched.subs_ptr(i)
+            A.y_vec, A.u_vec = sched.y_ptr(i), sched.u_ptr(i)
             A.x_in, A.x_in_stride = x_in.data_ptr(), (stride if stride else Pl + cap)
             A.x_out, A.x_out_stride = x_out.data_ptr(), Pl + cap
             A.anc = anc.data_ptr() if anc is not None else None

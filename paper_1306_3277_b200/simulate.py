@@ -22,6 +22,15 @@ from .inference.particle import _dtype_info, _fs_init, substep_schedule
 from .models import LOG_SQRT_2PI, resolve_model
 
 
+def _input_row(inputs, t, n_input, width):
+    """Input values (a provider at t, or a value vector), zero-padded to width."""
+    out = np.zeros(width)
+    if inputs is not None and n_input:
+        v = inputs.at(t) if hasattr(inputs, "at") else inputs
+        out[:n_input] = np.asarray(v, dtype=float).reshape(-1)[:n_input]
+    return out
+
+
 def _subs(spec, t, dt, inputs):
     if dt <= 0:
         raise ValueError("step_transition requires dt > 0")
@@ -40,7 +49,7 @@ def _subs(spec, t, dt, inputs):
     return subs, arr
 
 
-def _run_pw(spec, theta, x, arr, noise, obs, dtype, exact, check_finite, device):
+def _run_pw(spec, theta, x, arr, noise, obs, dtype, exact, check_finite, device, y_vec=None, u_vec=None):
     _lib.require_cuda()
     L = _lib.lib()
     _, tdt, dt_id = _dtype_info(dtype)
@@ -68,8 +77,14 @@ def _run_pw(spec, theta, x, arr, noise, obs, dtype, exact, check_finite, device)
     A.subs = subs_t.data_ptr() if subs_t is not None else None
     A.noise = noise_t.data_ptr() if noise_t is not None else None
     A.fs, A.workspace = fs.data_ptr(), ws.data_ptr()
+    keep = []
     if spec.kernel == _lib.SSM_MODEL_GENERIC:
         A.gen, A.theta_stride = spec.handle(dev), spec.theta_stride
+        for name, v in (("y_vec", y_vec), ("u_vec", u_vec)):
+            if v is not None:
+                t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)
+                keep.append(t)
+                setattr(A, name, t.data_ptr())
     if obs is not None:
         bits, yy, u_obs = obs
         A.has_obs, A.obs_mask, A.u_obs = 1, bits, u_obs
@@ -93,7 +108,12 @@ def step_transition(ir, theta, x, inputs, t, dt, rng=None, check_finite=True, *,
         if rng is None:
             raise ValueError("step_transition needs rng or noise")
         noise = spec.host_noise(rng, arr, P, spec.derived(np.asarray(theta).reshape(1, -1))[0])
-    xout, _, st = _run_pw(spec, theta, x, arr, noise, None, dtype, exact, check_finite, device)
+    u_vec = None
+    if spec.kernel == _lib.SSM_MODEL_GENERIC:  # input rows per sub-step start, then the (unused) obs row
+        nu = max(spec.n_input, 1)
+        rows = [_input_row(inputs, t_k, spec.n_input, nu) for t_k, _ in subs] + [np.zeros(nu)]
+        u_vec = np.concatenate(rows)
+    xout, _, st = _run_pw(spec, theta, x, arr, noise, None, dtype, exact, check_finite, device, u_vec=u_vec)
     nf = int(st["err_nonfinite"])
     if check_finite and nf != _lib.INT32_MAX:
         t_k, d = subs[nf % 64]
@@ -116,8 +136,13 @@ def observe_logpdf(ir, theta, x, inputs, y, mask, *, dtype="float64", exact=True
     for n in range(spec.n_obs):
         if mask[n]:
             bits |= 1 << n
-            yy[n] = y[n]
+            if n < 8:
+                yy[n] = y[n]
     u_obs = float(np.asarray(inputs, dtype=float).reshape(-1)[0]) if spec.n_input else 0.0
+    y_vec = u_vec = None
+    if spec.kernel == _lib.SSM_MODEL_GENERIC:
+        y_vec = np.where(mask[: spec.n_obs], y[: spec.n_obs], 0.0)
+        u_vec = _input_row(inputs, None, spec.n_input, max(spec.n_input, 1))
     _, a_out, _ = _run_pw(spec, theta, x, np.zeros(0, _lib.SUBSTEP_DTYPE), None, (bits, yy, u_obs), dtype,
-                          exact, False, device)
+                          exact, False, device, y_vec=y_vec, u_vec=u_vec)
     return a_out.to(torch.float64).cpu().numpy()

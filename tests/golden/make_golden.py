@@ -435,7 +435,8 @@ def gen_generic():
         f"lambda T, X, W, U: {I.expr_source(e, t, b)}", {"np": np, "inf": np.inf, "__builtins__": {}})
 
     models = {"Lorenz96": load("lorenz96"), "Windkessel": load("windkessel"),
-              "StochVol": load_test_model("StochVol"), "PredatorPrey": load_test_model("PredatorPrey")}
+              "StochVol": load_test_model("StochVol"), "PredatorPrey": load_test_model("PredatorPrey"),
+              "Wide": load_test_model("Wide")}
     lowered, sources = {}, {}
     for name, ir in models.items():
         d = codegen.lower(ir)
@@ -500,6 +501,26 @@ def gen_generic():
         out[f"{name}/smc/thetas"] = res.thetas
         out[f"{name}/smc/logliks"] = res.logliks
         out[f"{name}/smc/log_v"] = res.log_v
+    # Wide: 12 observations and two inputs (LOCF tables)
+    ir = models["Wide"]
+    theta = np.array([0.2])
+    times = np.linspace(0.0, 2.0, 21)
+    in_times = np.round(np.arange(0.0, 2.0001, 0.05), 10)
+    in_values = np.stack([0.1 * np.sin(3.0 * in_times), np.cos(2.0 * in_times)], axis=1)
+    inputs = LocfInputs(in_times, in_values)
+    ot, ov, om = simulate_data(ir, theta, times, inputs=inputs)
+    om[3, 5:9] = False  # a partially observed step
+    grid = build_filter_grid(0.0, 2.0, 20, ot, ov, om, n_obs=ir.n_obs)
+    out["Wide/theta"] = theta
+    out["Wide/in_times"] = in_times
+    out["Wide/in_values"] = in_values
+    out["Wide/obs_t"] = ot
+    out["Wide/obs_v"] = ov
+    out["Wide/obs_m"] = om
+    res = particle_filter(ir, theta, grid, RngStream(12), inputs=inputs, n_particles=512, resampler="systematic")
+    out["Wide/loglik"] = np.array(res.loglik)
+    out["Wide/traj"] = res.trajectory
+    out["Wide/x_final"] = res.run.x
     save("generic.npz", **out)
 
 

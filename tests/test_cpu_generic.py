@@ -17,7 +17,7 @@ from paper_1306_3277_b200.rng import RngStream
 
 with open(os.path.join(GOLDEN, "gen_models.json")) as fh:
     FIX = json.load(fh)
-NAMES = ["Lorenz96", "Windkessel", "StochVol", "PredatorPrey"]
+NAMES = ["Lorenz96", "Windkessel", "StochVol", "PredatorPrey", "Wide"]
 
 
 def _desc(name):

@@ -311,13 +311,21 @@ def check(status: int, what: str = "") -> None:
         raise NativeError(f"{what} failed: {msg}")
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
-    """Fail loudly when the device path cannot run."""
+    """Fail loudly when the device path cannot run (checked once per process
+    once it succeeds: ParticleRun construction is on the SMC^2 hot path)."""
+    global _CUDA_OK
+    if _CUDA_OK:
+        return
     import torch
 
     load_library()
     if not torch.cuda.is_available():
         raise NativeUnavailableError("no CUDA device visible; the B200 path has no CPU fallback")
+    _CUDA_OK = True
 
 
 def stream_ptr(stream=None):

@@ -518,9 +518,12 @@ tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_fi
   if (e < ntiles) prel[off] = wex + incl - qg;  // exclusive, exact integer
   if (threadIdx.x == 0) blk_tot[static_cast<size_t>(b) * gridDim.x + blk] = tot;
   if (!fs_rw) return;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&fs_rw[b].prefix_done, 1u) == gridDim.x - 1;
+  // only thread 0's block total is read by the last block (prel is read by the
+  // next kernel), so only thread 0 fences before taking a ticket
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&fs_rw[b].prefix_done, 1u) == gridDim.x - 1;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();

@@ -191,13 +191,25 @@ __device__ __forceinline__ void pw_block_finalize(const ssm_pw_args& A, ssm_filt
   __shared__ bool s_last;
   Lse* parts = reinterpret_cast<Lse*>(A.workspace) + static_cast<size_t>(b) * max_blocks;
   if (has_obs) {
-    // lane 0 of each warp holds its warp's partial; fold warps in order
-    const Lse r = lse_block_reduce<NT>(lane == 0 ? st : lse_empty(), red);
-    if (threadIdx.x == 0) parts[blockIdx.x] = r;
+    // lane 0 of each warp holds its warp's partial: fold the NT/32 warp partials in
+    // warp 0 (the same combination tree lse_block_reduce applies, without its
+    // intra-warp pass over empty lanes)
+    const int warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = st;
+    __syncthreads();
+    if (warp == 0) {
+      Lse r = lane < NT / 32 ? red[lane] : lse_empty();
+#pragma unroll
+      for (int off = NT / 64; off > 0; off >>= 1) r = lse_combine(r, lse_shfl_down(r, off));
+      if (lane == 0) parts[blockIdx.x] = r;
+    }
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&fs->blocks_done, 1u) == gridDim.x - 1;
+  // the last block reads only the partials thread 0 wrote (error flags are atomics),
+  // so thread 0 alone fences before taking its ticket
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&fs->blocks_done, 1u) == gridDim.x - 1;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();

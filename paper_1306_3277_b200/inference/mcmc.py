@@ -12,6 +12,8 @@ device next).
 
 from __future__ import annotations
 
+import copy
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -72,7 +74,19 @@ class FilterRunner:
         return self._make(theta, init_state).init(rng.child(0))
 
     def new_runs(self, thetas, init_states, rngs):
-        runs = [self._make(t, s) for t, s in zip(thetas, init_states)]
+        # one validated run, then per-theta shallow copies (the constructor's checks
+        # and lookups are per runner, not per theta; SMC^2 builds ~100 runs per step)
+        if not thetas:
+            return []
+        proto = self._make(thetas[0], init_states[0])
+        runs = [proto]
+        for t, st in zip(thetas[1:], init_states[1:]):
+            r = copy.copy(proto)
+            r.theta = np.asarray(t, dtype=float).reshape(1, -1)
+            r.initial_state = st
+            r._derived = None
+            r._hist, r._keys, r._hx, r._ha = [], [], [], []
+            runs.append(r)
         init_runs(runs, [g.child(0) for g in rngs])
         return runs
 

@@ -302,6 +302,18 @@ def run_reference(args):
 # ------------------------------------------------------------------- main
 
 
+def _step_roofline(kern, P, peak):
+    ph = [kern[k] for k in ("resample", "propagate_weight") if k in kern]
+    if not ph:
+        return None
+    nbytes, ms = sum(v["bytes"] for v in ph), sum(v["total_ms"] for v in ph)
+    steps = max(v["launches"] for v in ph)
+    achieved = nbytes / (ms / 1e3) / 1e9
+    return {"phases": "resample + propagate_weight (gather fused)", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 3),
+            "algorithmic_bytes_per_update": round(nbytes / steps / P, 2)}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -412,6 +424,9 @@ def main():
             "algorithmic_bytes_per_particle": pw["bytes"] / max(pw["launches"], 1) / P if pw else None,
         },
         "kernels": kern,
+        # the whole grid step (resample kernels + fused gather/propagate/weight): algorithmic bytes of
+        # both phases over their summed device time, per particle-update
+        "step_roofline": _step_roofline(res["kern"], P, peak),
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
         "loglik_mean": float(np.mean(res["logliks"])),

@@ -14,6 +14,7 @@
 //   (identity when no resampling happened, like the reference's arange).
 
 #include "ssm_common.cuh"
+#include "ssm_models.cuh"
 
 namespace ssm {
 
@@ -25,106 +26,6 @@ __device__ __forceinline__ double device_uniform_small(uint32_t k0, uint32_t k1,
                                                        uint32_t purpose) {
   const U4 r = philox4x32_10(U4{k, step, 0u, purpose}, k0, k1);  // same stream as the multi-kernel search
   return u53(r.x, r.y);
-}
-
-// --- per-particle transition (device noise), the general path of pw_kernel ---
-template <typename T>
-__device__ __forceinline__ void small_normals8(uint32_t k0, uint32_t k1, uint32_t p, uint32_t step, uint32_t sub,
-                                               T z[8]) {
-#pragma unroll
-  for (uint32_t g = 0; g < 2; ++g) {
-    const U4 r = philox4x32_10(U4{p, step, (sub << 8) | g, kPurposeNoise}, k0, k1);
-    float a, b, c, d;
-    box_muller(r.x, r.y, a, b);
-    box_muller(r.z, r.w, c, d);
-    z[4 * g] = static_cast<T>(a);
-    z[4 * g + 1] = static_cast<T>(b);
-    z[4 * g + 2] = static_cast<T>(c);
-    z[4 * g + 3] = static_cast<T>(d);
-  }
-}
-
-template <typename T, bool E>
-__device__ __forceinline__ void small_l96_deriv(const T x[8], T F, const T nt[8], T out[8]) {
-  using O = Ar<T, E>;
-#pragma unroll
-  for (int n = 0; n < 8; ++n) {
-    const T xm1 = x[(n + 7) & 7], xp1 = x[(n + 1) & 7], xm2 = x[(n + 6) & 7];
-    out[n] = O::add(O::add(O::sub(O::mul(xm1, O::sub(xp1, xm2)), x[n]), F), nt[n]);
-  }
-}
-
-template <typename T, bool E>
-__device__ __forceinline__ void small_l96_rk4(T x[8], T F, const T nt[8], T s) {
-  using O = Ar<T, E>;
-  T k[8], acc[8], st[8];
-  const T hs = O::mul(T(0.5), s);
-  small_l96_deriv<T, E>(x, F, nt, k);
-#pragma unroll
-  for (int n = 0; n < 8; ++n) {
-    acc[n] = k[n];
-    st[n] = O::add(x[n], O::mul(hs, k[n]));
-  }
-  small_l96_deriv<T, E>(st, F, nt, k);
-#pragma unroll
-  for (int n = 0; n < 8; ++n) {
-    acc[n] = O::add(acc[n], O::mul(T(2.0), k[n]));
-    st[n] = O::add(x[n], O::mul(hs, k[n]));
-  }
-  small_l96_deriv<T, E>(st, F, nt, k);
-#pragma unroll
-  for (int n = 0; n < 8; ++n) {
-    acc[n] = O::add(acc[n], O::mul(T(2.0), k[n]));
-    st[n] = O::add(x[n], O::mul(s, k[n]));
-  }
-  small_l96_deriv<T, E>(st, F, nt, k);
-  const T s6 = O::div(s, T(6.0));
-#pragma unroll
-  for (int n = 0; n < 8; ++n) {
-    acc[n] = O::add(acc[n], k[n]);
-    x[n] = O::add(x[n], O::mul(s6, acc[n]));
-  }
-}
-
-template <int MODEL, typename T, bool E>
-__device__ __forceinline__ void small_transition(T* x, const double* th, const ssm_substep* subs, int n_sub,
-                                                 uint32_t k0, uint32_t k1, uint32_t pg, int step, bool check,
-                                                 bool& bad, int& bad_sub) {
-  using O = Ar<T, E>;
-  constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
-  for (int k = 0; k < n_sub; ++k) {
-    const ssm_substep& S = subs[k];
-    if constexpr (MODEL == SSM_MODEL_LORENZ96) {
-      T W[8], nt[8];
-      small_normals8<T>(k0, k1, pg, static_cast<uint32_t>(step), static_cast<uint32_t>(k), W);
-      const T sd = static_cast<T>(S.sd);
-      const T F = static_cast<T>(th[0]);
-      const T sq = static_cast<T>(th[1]);
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        W[n] = sd * W[n];
-        nt[n] = E ? O::div(O::mul(sq, W[n]), T(0.05)) : O::mul(O::mul(sq, W[n]), T(20.0));
-      }
-      for (int m = 0; m < S.n_ode; ++m) small_l96_rk4<T, E>(x, F, nt, static_cast<T>(S.s[m]));
-    } else {
-      const U4 r = philox4x32_10(U4{pg, static_cast<uint32_t>(step), static_cast<uint32_t>(k) << 8, kPurposeNoise},
-                                 k0, k1);
-      float z0, z1;
-      box_muller(r.x, r.y, z0, z1);
-      const T xi = static_cast<T>(th[3]) * static_cast<T>(z0);
-      x[0] = O::add(O::mul(static_cast<T>(th[0]), x[0]),
-                    O::mul(static_cast<T>(th[1]), O::add(static_cast<T>(S.u_in), xi)));
-    }
-    if (check && !bad) {
-      bool ok = true;
-#pragma unroll
-      for (int n = 0; n < NX; ++n) ok &= isfinite(x[n]);
-      if (!ok) {
-        bad = true;
-        bad_sub = k;
-      }
-    }
-  }
 }
 
 template <int MODEL, typename T, bool E>
@@ -279,8 +180,10 @@ __global__ void __launch_bounds__(kSmallThreads) small_filter_kernel(const ssm_s
       for (int n = 0; n < NX; ++n) x[n] = XS ? xcur[n * P + src] : x_prev_g[static_cast<size_t>(n) * P + src];
       bool b_now = false;
       int bs = 0;
-      small_transition<MODEL, T, E>(x, th, A.subs + d.subs_offset, d.n_sub, k0, k1, static_cast<uint32_t>(p),
-                                    d.step, A.check_finite != 0, b_now, bs);
+      // the fused kernel's general (non-SIMPLE) transition: the same draws and arithmetic
+      transition_one<MODEL, T, E, false, false>(x, th, A.subs + d.subs_offset, d.n_sub, nullptr, P, p, k0, k1,
+                                                static_cast<uint32_t>(p), static_cast<uint32_t>(d.step), T(0), T(0),
+                                                T(0), A.check_finite != 0, b_now, bs);
       if (b_now && !bad) {
         bad = true;
         bad_step = d.step;

@@ -699,3 +699,22 @@ def test_history_free_windkessel_and_resume():
         run.advance_to(50, RngStream(5).child(2))  # second call: different device keys per segment
         trajs.append(run.sample_trajectory(RngStream(5).child(3)))
     np.testing.assert_array_equal(trajs[0], trajs[1])
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_small_and_multikernel_paths_share_the_transition(exact, monkeypatch):
+    """The persistent small-P kernel and the fused multi-kernel path run the same
+    per-particle transition code (ssm_models.cuh): the first grid step (no
+    resampling yet) gives bitwise-equal states from the same device draws."""
+    from paper_1306_3277_b200.inference import particle as particle_mod
+
+    g = load_golden("pf.npz")
+    grid = _l96_grid(g)
+    small = particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(3), n_particles=3000, upto=1, exact=exact)
+    monkeypatch.setattr(particle_mod, "_NO_SMALL", True)
+    multi = particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(3), n_particles=3000, upto=1, exact=exact)
+    np.testing.assert_array_equal(small.run.x, multi.run.x)
+    if exact:
+        np.testing.assert_array_equal(small.run.logw, multi.run.logw)
+    else:
+        assert normwise(small.run.logw, multi.run.logw) <= 1e-12

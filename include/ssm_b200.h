@@ -181,8 +181,10 @@ int ssm_propagate_weight(const ssm_pw_args* args, void* stream);
  * compiled here for sm_100a with NVRTC and loaded into the current context
  * (ir.py:83-121 ModelIr, simulate.py:50-193 block semantics).
  *   ssm_gen_compile: source -> handle (`out`); `include_dir` = the csrc
- *     directory; `log` (HOST, nullable) receives the NVRTC log.
- *   ssm_gen_check: compile only (no device needed; used by CPU tests).
+ *     directory; `log` (HOST, nullable) receives the NVRTC log.  Compiles
+ *     the float64 / FMA / device-noise fused kernel now (errors surface
+ *     here); every other variant compiles on its first launch.
+ *   ssm_gen_check: compile every variant only (no device needed; CPU tests).
  * The handle is used through ssm_pw_args.gen (model = SSM_MODEL_GENERIC) by
  * ssm_propagate_weight / ssm_advance, and by ssm_gen_init_particles (the
  * model's `initial` block on the device).  Limits: n_state <= 32,

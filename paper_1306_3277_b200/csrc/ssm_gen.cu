@@ -3,12 +3,14 @@
 // (a `gen::Model` + #include "ssm_gen_rt.cuh") is compiled for sm_100a with
 // NVRTC, loaded with the runtime library API (cudaLibraryLoadData) and
 // launched like the hand-written kernels (programmatic dependent launches on
-// the caller's stream).  The handle owns the loaded library; no other state.
+// the caller's stream).  Each kernel variant (dtype x exact x injected noise,
+// init) is compiled on first use; the handle owns the loaded libraries.
 
 #include <nvrtc.h>
 
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -17,21 +19,30 @@
 
 namespace {
 
-// kernel instantiations, in handle order: pw[dtype][exact][injected], init[dtype]
-const char* kPwNames[2][2][2] = {
-    {{"ssm::gen_pw_kernel<gen::Model, float, false, false>", "ssm::gen_pw_kernel<gen::Model, float, false, true>"},
-     {"ssm::gen_pw_kernel<gen::Model, float, true, false>", "ssm::gen_pw_kernel<gen::Model, float, true, true>"}},
-    {{"ssm::gen_pw_kernel<gen::Model, double, false, false>", "ssm::gen_pw_kernel<gen::Model, double, false, true>"},
-     {"ssm::gen_pw_kernel<gen::Model, double, true, false>", "ssm::gen_pw_kernel<gen::Model, double, true, true>"}}};
-const char* kInitNames[2] = {"ssm::gen_init_kernel<gen::Model, float>", "ssm::gen_init_kernel<gen::Model, double>"};
+// kernel instantiations: pw[dtype][exact][injected] = variant dtype * 4 + exact * 2 + injected,
+// init[dtype] = variant 8 + dtype (dtype 0 float, 1 double)
+constexpr int kVariants = 10;
+const char* kVariantNames[kVariants] = {
+    "ssm::gen_pw_kernel<gen::Model, float, false, false>",  "ssm::gen_pw_kernel<gen::Model, float, false, true>",
+    "ssm::gen_pw_kernel<gen::Model, float, true, false>",   "ssm::gen_pw_kernel<gen::Model, float, true, true>",
+    "ssm::gen_pw_kernel<gen::Model, double, false, false>", "ssm::gen_pw_kernel<gen::Model, double, false, true>",
+    "ssm::gen_pw_kernel<gen::Model, double, true, false>",  "ssm::gen_pw_kernel<gen::Model, double, true, true>",
+    "ssm::gen_init_kernel<gen::Model, float>",              "ssm::gen_init_kernel<gen::Model, double>"};
 const char* kInfoName = "ssm_gen_model_info";  // extern "C" __device__ int[2] = {NX, KDRAW}
 
+// One handle per model: the source, and each kernel variant compiled (NVRTC)
+// and loaded on first use, so a model pays only for the variants it runs.
 struct GenModel {
-  cudaLibrary_t lib;
-  cudaKernel_t pw[2][2][2];
-  cudaKernel_t init[2];
-  int nx, kdraw;
+  std::string src, inc;
+  std::mutex mu;
+  cudaLibrary_t lib[kVariants] = {};
+  cudaKernel_t kernel[kVariants] = {};
+  int nx = 0, kdraw = 0;
 };
+
+int pw_variant(int dtype, int exact, int injected) {
+  return (dtype == SSM_F64 ? 4 : 0) + (exact ? 2 : 0) + (injected ? 1 : 0);
+}
 
 void copy_log(const std::string& s, char* log, size_t log_len) {
   if (!log || log_len == 0) return;
@@ -40,19 +51,13 @@ void copy_log(const std::string& s, char* log, size_t log_len) {
   log[n] = '\0';
 }
 
-// NVRTC: source -> sm_100a cubin (+ lowered kernel names)
-int compile(const char* source, const char* include_dir, std::vector<char>* cubin,
-            std::vector<std::string>* lowered, char* log, size_t log_len) {
+// NVRTC: source -> sm_100a cubin for the given instantiations (+ their lowered names)
+int compile(const char* source, const char* include_dir, const std::vector<const char*>& names,
+            std::vector<char>* cubin, std::vector<std::string>* lowered, char* log, size_t log_len) {
   if (!source || !include_dir) return SSM_ERR_INVALID_ARG;
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, source, "ssm_gen_model.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return SSM_ERR_INVALID_ARG;
-  std::vector<const char*> names;
-  for (int t = 0; t < 2; ++t)
-    for (int e = 0; e < 2; ++e)
-      for (int i = 0; i < 2; ++i) names.push_back(kPwNames[t][e][i]);
-  names.push_back(kInitNames[0]);
-  names.push_back(kInitNames[1]);
   for (const char* n : names) nvrtcAddNameExpression(prog, n);
   const std::string inc = std::string("--include-path=") + include_dir;
   const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "-lineinfo",
@@ -84,51 +89,67 @@ int compile(const char* source, const char* include_dir, std::vector<char>* cubi
   return SSM_OK;
 }
 
+// compile + load one variant (caller holds g->mu); also reads the model sizes
+int load_variant(GenModel* g, int v, char* log, size_t log_len) {
+  if (g->kernel[v]) return SSM_OK;
+  std::vector<char> cubin;
+  std::vector<std::string> low;
+  const int st = compile(g->src.c_str(), g->inc.c_str(), {kVariantNames[v]}, &cubin, &low, log, log_len);
+  if (st != SSM_OK) return st;
+  cudaFree(nullptr);  // the primary context (the one torch uses) is current
+  cudaLibrary_t lib;
+  cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  cudaKernel_t k = nullptr;
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&k, lib, low[0].c_str());
+  if (e == cudaSuccess && g->nx == 0) {  // model sizes from ssm_gen_model_info (NX, KDRAW)
+    int info[2] = {0, 0};
+    void* dptr = nullptr;
+    size_t bytes = 0;
+    e = cudaLibraryGetGlobal(&dptr, &bytes, lib, kInfoName);
+    if (e == cudaSuccess && bytes >= sizeof(info)) e = cudaMemcpy(info, dptr, sizeof(info), cudaMemcpyDeviceToHost);
+    g->nx = info[0];
+    g->kdraw = info[1];
+  }
+  if (e != cudaSuccess) {
+    ssm_set_last_error(e);
+    return SSM_ERR_CUDA;
+  }
+  g->lib[v] = lib;
+  g->kernel[v] = k;
+  return SSM_OK;
+}
+
+cudaKernel_t get_kernel(const void* handle, int v) {
+  GenModel* g = static_cast<GenModel*>(const_cast<void*>(handle));
+  std::lock_guard<std::mutex> lock(g->mu);
+  return load_variant(g, v, nullptr, 0) == SSM_OK ? g->kernel[v] : nullptr;
+}
+
 }  // namespace
 
 extern "C" int ssm_gen_check(const char* source, const char* include_dir, char* log, size_t log_len) {
-  return compile(source, include_dir, nullptr, nullptr, log, log_len);
+  std::vector<const char*> all(kVariantNames, kVariantNames + kVariants);
+  return compile(source, include_dir, all, nullptr, nullptr, log, log_len);
 }
 
 extern "C" int ssm_gen_compile(const char* source, const char* include_dir, void** out, char* log,
                                size_t log_len) {
-  if (!out) return SSM_ERR_INVALID_ARG;
+  if (!out || !source || !include_dir) return SSM_ERR_INVALID_ARG;
   *out = nullptr;
-  std::vector<char> cubin;
-  std::vector<std::string> low;
-  const int st = compile(source, include_dir, &cubin, &low, log, log_len);
-  if (st != SSM_OK) return st;
-  cudaFree(nullptr);  // the primary context (the one torch uses) is current
   GenModel* g = new GenModel();
-  cudaError_t e = cudaLibraryLoadData(&g->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-  if (e != cudaSuccess) {
+  g->src = source;
+  g->inc = include_dir;
+  // the filter's default variant (float64, FMA, device draws) now: reports compile
+  // errors here and reads the model sizes; the others compile on first use
+  int st;
+  {
+    std::lock_guard<std::mutex> lock(g->mu);
+    st = load_variant(g, pw_variant(SSM_F64, 0, 0), log, log_len);
+  }
+  if (st != SSM_OK) {
     delete g;
-    ssm_set_last_error(e);
-    return SSM_ERR_CUDA;
+    return st;
   }
-  int k = 0;
-  for (int t = 0; t < 2; ++t)
-    for (int x = 0; x < 2; ++x)
-      for (int i = 0; i < 2; ++i, ++k)
-        if (e == cudaSuccess) e = cudaLibraryGetKernel(&g->pw[t][x][i], g->lib, low[k].c_str());
-  for (int t = 0; t < 2; ++t, ++k)
-    if (e == cudaSuccess) e = cudaLibraryGetKernel(&g->init[t], g->lib, low[k].c_str());
-  // model sizes from the module's ssm_gen_model_info (NX, KDRAW)
-  int info[2] = {0, 0};
-  if (e == cudaSuccess) {
-    void* dptr = nullptr;
-    size_t bytes = 0;
-    e = cudaLibraryGetGlobal(&dptr, &bytes, g->lib, kInfoName);
-    if (e == cudaSuccess && bytes >= sizeof(info)) e = cudaMemcpy(info, dptr, sizeof(info), cudaMemcpyDeviceToHost);
-  }
-  if (e != cudaSuccess) {
-    cudaLibraryUnload(g->lib);
-    delete g;
-    ssm_set_last_error(e);
-    return SSM_ERR_CUDA;
-  }
-  g->nx = info[0];
-  g->kdraw = info[1];
   *out = g;
   return SSM_OK;
 }
@@ -136,7 +157,8 @@ extern "C" int ssm_gen_compile(const char* source, const char* include_dir, void
 extern "C" int ssm_gen_destroy(void* handle) {
   if (!handle) return SSM_OK;
   GenModel* g = static_cast<GenModel*>(handle);
-  cudaLibraryUnload(g->lib);
+  for (int v = 0; v < kVariants; ++v)
+    if (g->lib[v]) cudaLibraryUnload(g->lib[v]);
   delete g;
   return SSM_OK;
 }
@@ -151,11 +173,10 @@ extern "C" int ssm_gen_info(const void* handle, int* n_state, int* n_draws) {
 
 // called by ssm_propagate_weight for SSM_MODEL_GENERIC
 int ssm_gen_propagate_weight(const ssm_pw_args& A, cudaStream_t s) {
-  const GenModel* g = static_cast<const GenModel*>(A.gen);
-  if (!g || A.theta_stride <= 0) return SSM_ERR_INVALID_ARG;
+  if (!A.gen || A.theta_stride <= 0) return SSM_ERR_INVALID_ARG;
   if (A.dtype != SSM_F64 && A.dtype != SSM_F32) return SSM_ERR_INVALID_ARG;
-  const int t = A.dtype == SSM_F64 ? 1 : 0;
-  cudaKernel_t k = g->pw[t][A.exact ? 1 : 0][A.noise ? 1 : 0];
+  cudaKernel_t k = get_kernel(A.gen, pw_variant(A.dtype, A.exact, A.noise != nullptr));
+  if (!k) return SSM_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ssm::pw_grid_x(A.P), A.B);
   cfg.blockDim = dim3(ssm::kPwThreads);
@@ -179,18 +200,18 @@ int ssm_gen_nx(const void* handle) { return handle ? static_cast<const GenModel*
 extern "C" int ssm_gen_init_particles(const void* handle, int dtype, int B, int P, int p_offset,
                                       const uint32_t* keys, const double* theta, int theta_stride, void* x_out,
                                       ssm_filter_state* fs, void* stream) {
-  const GenModel* g = static_cast<const GenModel*>(handle);
-  if (!g || B <= 0 || P <= 0 || B > 65535 || !keys || !theta || theta_stride <= 0 || !x_out)
+  if (!handle || B <= 0 || P <= 0 || B > 65535 || !keys || !theta || theta_stride <= 0 || !x_out)
     return SSM_ERR_INVALID_ARG;
   if (dtype != SSM_F64 && dtype != SSM_F32) return SSM_ERR_INVALID_ARG;
+  cudaKernel_t k = get_kernel(handle, 8 + (dtype == SSM_F64 ? 1 : 0));
+  if (!k) return SSM_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ssm::pw_grid_x(P), B);
   cfg.blockDim = dim3(ssm::kPwThreads);
   cfg.stream = static_cast<cudaStream_t>(stream);
   void* params[] = {&P, &p_offset, const_cast<uint32_t**>(&keys), const_cast<double**>(&theta), &theta_stride,
                     &x_out, &fs};
-  const cudaError_t e =
-      cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(g->init[dtype == SSM_F64 ? 1 : 0]), params);
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k), params);
   if (e != cudaSuccess) {
     ssm_set_last_error(e);
     return SSM_ERR_CUDA;

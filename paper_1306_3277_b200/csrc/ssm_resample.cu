@@ -935,9 +935,12 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
 // particles in between (count of U_(k) < cum_j per particle, run-start marks,
 // max-scan).  Replaces P random-access searches of the unsorted draw.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double spacing(uint32_t k0, uint32_t k1, uint32_t k, uint32_t step) {
-  const U4 r = philox4x32_10(U4{k, step, 0u, kPurposeSpacing}, k0, k1);
-  return -log(1.0 - u53(r.x, r.y));  // 1 - u in (0, 1], exact
+// spacings 2m and 2m + 1 from one Philox block (words x,y and z,w)
+__device__ __forceinline__ void spacing_pair(uint32_t k0, uint32_t k1, uint32_t m, uint32_t step, double& e0,
+                                             double& e1) {
+  const U4 r = philox4x32_10(U4{m, step, 0u, kPurposeSpacing}, k0, k1);
+  e0 = -log(1.0 - u53(r.x, r.y));  // 1 - u in (0, 1], exact
+  e1 = -log(1.0 - u53(r.z, r.w));
 }
 
 // inclusive prefix of the block's 2048 spacings (thread t: items 8t..8t+7), fixed order;
@@ -946,11 +949,17 @@ __device__ __forceinline__ double spacing_block_scan(uint32_t k0, uint32_t k1, i
                                                      double (&v)[kScanItems], double* s_warp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double run = 0.0;
+  static_assert(kScanItems % 2 == 0 && kScanTile % 2 == 0, "spacing pairs");
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int kl = threadIdx.x * kScanItems + i;
-    run += kl < n_valid ? spacing(k0, k1, static_cast<uint32_t>(kbase + kl), static_cast<uint32_t>(step)) : 0.0;
+  for (int i = 0; i < kScanItems; i += 2) {
+    const int kl = threadIdx.x * kScanItems + i;  // even: the pair (kl, kl + 1) shares a block
+    double e0 = 0.0, e1 = 0.0;
+    if (kl < n_valid)
+      spacing_pair(k0, k1, static_cast<uint32_t>((kbase + kl) >> 1), static_cast<uint32_t>(step), e0, e1);
+    run += e0;
     v[i] = run;
+    run += kl + 1 < n_valid ? e1 : 0.0;
+    v[i + 1] = run;
   }
   double incl = run;
 #pragma unroll

@@ -608,8 +608,11 @@ def test_sorted_multinomial_matches_spacings_oracle(P, pattern):
     got = anc.cpu().numpy()
     k = np.arange(P + 1, dtype=np.uint64)
     for b in range(2):
-        r = _philox4x32_10([k, np.full(P + 1, step), np.zeros(P + 1), np.full(P + 1, 5)], *keys_np[b])
-        u = ((r[0] << np.uint64(32)) | r[1]) >> np.uint64(11)
+        # spacing k: Philox block k // 2, words (x, y) for even k and (z, w) for odd k
+        r = _philox4x32_10([k >> np.uint64(1), np.full(P + 1, step), np.zeros(P + 1), np.full(P + 1, 5)],
+                           *keys_np[b])
+        odd = (k & np.uint64(1)).astype(bool)
+        u = np.where(odd, (r[2] << np.uint64(32)) | r[3], (r[0] << np.uint64(32)) | r[1]) >> np.uint64(11)
         E = -np.log(1.0 - u.astype(np.float64) * 2.0**-53)
         S = np.cumsum(E)
         U = S[:P] / S[P]

@@ -1039,10 +1039,26 @@ spacing_prefix_kernel(int nblk, double* __restrict__ blk, double* __restrict__ t
 // inclusive u64 array (scan of the log-weights) or from the fused kernel's
 // tile records (C_j = tile prefix + round(scale_w * cdf_local_j), as the
 // systematic offspring kernel; the last particle's C is the total: cum = 1)
+// The sorted multinomial's CDF accessors scale by a precomputed 1 / total (its
+// draws are device noise: consistency between its two sources is what matters);
+// the trajectory pick keeps the division (CumTileRecs), which the host-draw
+// parity runs compare against the reference.
 struct CumFixedArr {
   const uint64_t* C;
-  double tot;
-  __device__ __forceinline__ double operator()(int j) const { return static_cast<double>(__ldg(C + j)) / tot; }
+  double inv;
+  __device__ __forceinline__ double operator()(int j) const { return static_cast<double>(__ldg(C + j)) * inv; }
+};
+struct CumTileRecsMul {
+  const uint64_t* cl;
+  const double* sc;
+  const uint64_t* tp;
+  const uint64_t* bp;
+  double inv;
+  __device__ __forceinline__ double operator()(int j) const {
+    const int tw = j >> 5;
+    const uint64_t C = tp[tw] + bp[tw / kRecPerBlock] + __double2ull_rn(sc[tw] * static_cast<double>(__ldg(cl + j)));
+    return static_cast<double>(C) * inv;
+  }
 };
 struct CumTileRecs {
   const uint64_t* cl;
@@ -1116,16 +1132,16 @@ spacing_merge_kernel(int P, const uint64_t* __restrict__ C, const uint64_t* __re
   for (int e = threadIdx.x; e < (kScanTile + kScanTile / 32) / 4; e += kThreads)
     reinterpret_cast<int4*>(sOut)[e] = make_int4(-1, -1, -1, -1);
   const size_t coff = static_cast<size_t>(b) * P;
-  using Cum = typename std::conditional<SRC == 0, CumFixedArr, CumTileRecs>::type;
+  using Cum = typename std::conditional<SRC == 0, CumFixedArr, CumTileRecsMul>::type;
   Cum cum_at;
   if constexpr (SRC == 0) {
-    cum_at = CumFixedArr{C + coff, static_cast<double>(C[coff + P - 1])};
+    cum_at = CumFixedArr{C + coff, 1.0 / static_cast<double>(C[coff + P - 1])};
   } else {
     const int nt = (P + 31) >> 5;
     const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
-    cum_at = CumTileRecs{cdf_local + coff, scale + static_cast<size_t>(b) * nt, pref + static_cast<size_t>(b) * nt,
+    cum_at = CumTileRecsMul{cdf_local + coff, scale + static_cast<size_t>(b) * nt, pref + static_cast<size_t>(b) * nt,
                          pref + B_total_tiles_offset(nt, gridDim.y) + static_cast<size_t>(b) * nblk,
-                         static_cast<double>(totals[b])};
+                         1.0 / static_cast<double>(totals[b])};
   }
   __syncthreads();
   // first / last ancestor: searchsorted(cum, U, 'right'), clipped

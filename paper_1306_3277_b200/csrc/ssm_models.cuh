@@ -32,6 +32,19 @@ __device__ __forceinline__ void normals8(uint32_t k0, uint32_t k1, uint32_t p, u
   }
 }
 
+// the same eight normals, kept in float (the SIMPLE fused kernel draws the next
+// tile's noise while the current tile integrates)
+__device__ __forceinline__ void normals8f(uint32_t k0, uint32_t k1, uint32_t p, uint32_t step, uint32_t sub,
+                                          float (&z)[8]) {
+  U4 r[2] = {U4{p, step, sub << 8, kPurposeNoise}, U4{p, step, (sub << 8) | 1u, kPurposeNoise}};
+  philox4x32_10_x2(r[0], r[1], k0, k1);
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    box_muller(r[g].x, r[g].y, z[4 * g], z[4 * g + 1]);
+    box_muller(r[g].z, r[g].w, z[4 * g + 2], z[4 * g + 3]);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ T normal1(uint32_t k0, uint32_t k1, uint32_t p, uint32_t step,
                                      uint32_t sub) {
@@ -129,6 +142,16 @@ __device__ __forceinline__ void l96_rk4_fast(T x[8], const T Fn[8], T s) {
   for (int n = 0; n < 8; ++n) x[n] = fma(s6, acc[n] + k[n], x[n]);
 }
 
+
+// SIMPLE L96 step (one sub-step, one RK4 step) from standard normals z: the
+// same arithmetic as transition_one's SIMPLE branch
+template <typename T>
+__device__ __forceinline__ void l96_simple_step(T (&x)[8], const float (&z)[8], T s_F, T s_c, T s_s) {
+  T Fn[8];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) Fn[n] = fma(s_c, static_cast<T>(z[n]), s_F);  // F + sqrt(sigma2) sd z / h
+  l96_rk4_fast<T>(x, Fn, s_s);
+}
 
 // One particle through one grid step (particle.py:110-111 / simulate.py:132-163):
 // the sub-steps of noise + RK4 / windkessel update, in place on x.  Shared by

@@ -106,6 +106,12 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
     s_s = static_cast<T>(A.subs[0].s[0]);
   }
 
+  constexpr bool kPipeNoise = SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ;
+  float zc[8], zn[8];  // (kPipeNoise) this tile's and the next tile's standard normals
+  if constexpr (kPipeNoise) {
+    if (p0 < P) normals8f(k0, k1, static_cast<uint32_t>(p0 + A.p_offset), static_cast<uint32_t>(A.step), 0u, zc);
+  }
+
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int p = tile * kPwThreads + threadIdx.x;
     const bool act = p < P;
@@ -120,9 +126,25 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
       anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
     }
     if (act) {
-      transition_one<MODEL, T, E, INJ, SIMPLE>(x, th, A.subs, A.n_sub, noise, P, p, k0, k1,
-                                              static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
-                                              s_F, s_c, s_s, A.check_finite != 0 && !defer_finite, bad, bad_sub);
+      if constexpr (kPipeNoise) {
+        // the next tile's draws do not depend on this tile: issuing them here gives the
+        // scheduler integer / MUFU work to interleave with the FP64 RK4 chain
+        const int pn = p + stride;
+        if (pn < P) normals8f(k0, k1, static_cast<uint32_t>(pn + A.p_offset), static_cast<uint32_t>(A.step), 0u, zn);
+        l96_simple_step<T>(reinterpret_cast<T(&)[8]>(x), zc, s_F, s_c, s_s);
+        if (A.check_finite != 0 && !defer_finite && !bad) {
+          bool ok = true;
+#pragma unroll
+          for (int n = 0; n < NX; ++n) ok &= finite_bits(x[n]);
+          if (!ok) bad = true;
+        }
+#pragma unroll
+        for (int n = 0; n < 8; ++n) zc[n] = zn[n];
+      } else {
+        transition_one<MODEL, T, E, INJ, SIMPLE>(x, th, A.subs, A.n_sub, noise, P, p, k0, k1,
+                                                static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
+                                                s_F, s_c, s_s, A.check_finite != 0 && !defer_finite, bad, bad_sub);
+      }
 #pragma unroll
       for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * out_stride + p] = x[n];
 

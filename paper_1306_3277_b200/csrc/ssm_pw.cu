@@ -107,10 +107,16 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
   }
 
   constexpr bool kPipeNoise = SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ;
-  float zc[8], zn[8];  // (kPipeNoise) this tile's and the next tile's standard normals
+  constexpr bool kPipeNoiseWK = SIMPLE && MODEL == SSM_MODEL_WINDKESSEL && !INJ;
+  float zc[8], zn[8];  // (kPipeNoise*) this tile's and the next tile's standard normals
   if constexpr (kPipeNoise) {
     if (p0 < P) normals8f(k0, k1, static_cast<uint32_t>(p0 + A.p_offset), static_cast<uint32_t>(A.step), 0u, zc);
   }
+  if constexpr (kPipeNoiseWK) {
+    if (p0 < P) zc[0] = normal1<float>(k0, k1, static_cast<uint32_t>(p0 + A.p_offset), static_cast<uint32_t>(A.step), 0u);
+  }
+  // SIMPLE windkessel: the sub-step's input and the analytic-update constants hoisted
+  const T wk_u = SIMPLE && MODEL == SSM_MODEL_WINDKESSEL ? static_cast<T>(A.subs[0].u_in) : T(0);
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int p = tile * kPwThreads + threadIdx.x;
@@ -140,6 +146,15 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
         }
 #pragma unroll
         for (int n = 0; n < 8; ++n) zc[n] = zn[n];
+      } else if constexpr (kPipeNoiseWK) {
+        const int pn = p + stride;
+        if (pn < P) zn[0] = normal1<float>(k0, k1, static_cast<uint32_t>(pn + A.p_offset), static_cast<uint32_t>(A.step), 0u);
+        // Windkessel.bi:28-29 as transition_one: ca x + cb (F + xi), xi = h sqrt(sigma2) z
+        using O = Ar<T, E>;
+        const T xi = static_cast<T>(th[3]) * static_cast<T>(zc[0]);
+        x[0] = O::add(O::mul(static_cast<T>(th[0]), x[0]), O::mul(static_cast<T>(th[1]), O::add(wk_u, xi)));
+        if (A.check_finite != 0 && !bad && !finite_bits(x[0])) bad = true;
+        zc[0] = zn[0];
       } else {
         transition_one<MODEL, T, E, INJ, SIMPLE>(x, th, A.subs, A.n_sub, noise, P, p, k0, k1,
                                                 static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
@@ -229,6 +244,15 @@ static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
     const bool simple = (A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !A.exact && !inj;
     if (simple) {
       launch_pdl(pw_kernel<MODEL, T, false, false, true>, grid, dim3(kPwThreads), s, A);
+      return;
+    }
+  } else {
+    // windkessel with one sub-step per grid step (device noise): draws pipelined across tiles
+    if ((A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !inj) {
+      if (A.exact)
+        launch_pdl(pw_kernel<MODEL, T, true, false, true>, grid, dim3(kPwThreads), s, A);
+      else
+        launch_pdl(pw_kernel<MODEL, T, false, false, true>, grid, dim3(kPwThreads), s, A);
       return;
     }
   }

@@ -721,3 +721,39 @@ def test_small_and_multikernel_paths_share_the_transition(exact, monkeypatch):
         np.testing.assert_array_equal(small.run.logw, multi.run.logw)
     else:
         assert normwise(small.run.logw, multi.run.logw) <= 1e-12
+
+
+def _random_weights(seed, P, sigma, zero_frac, ties):
+    r = np.random.default_rng(seed)
+    w = np.exp(sigma * r.normal(size=P))
+    if ties:
+        w = np.round(w, 1) + 0.0
+    w[r.random(P) < zero_frac] = 0.0
+    if not np.any(w > 0):
+        w[r.integers(P)] = 1.0
+    return w
+
+
+def test_resample_randomised_vs_oracle():
+    """Property test (hypothesis): for random sizes (ragged, non-power-of-two,
+    resampled size != P), weight shapes (log-normal spread up to degenerate,
+    exact zeros, tied values) and all three schemes, the device resample()
+    returns exactly the oracle's searchsorted ancestors for the same uniforms."""
+    from hypothesis import HealthCheck, given, settings
+    from hypothesis import strategies as st
+
+    @settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+    @given(seed=st.integers(0, 2**31 - 1), P=st.integers(2, 9000), sigma=st.sampled_from([0.0, 0.5, 3.0, 12.0]),
+           zero_frac=st.sampled_from([0.0, 0.3, 0.95]), ties=st.booleans(), scheme=st.sampled_from(SCHEMES),
+           size_factor=st.sampled_from([None, 0.5, 1.7]))
+    def check(seed, P, sigma, zero_frac, ties, scheme, size_factor):
+        w = _random_weights(seed, P, sigma, zero_frac, ties)
+        size = None if size_factor is None else max(1, int(P * size_factor))
+        n = P if size is None else size
+        r = np.random.default_rng(seed + 1)
+        u = r.random(1 if scheme == "systematic" else n)
+        got = resample(w, scheme, FixedU(u), size=size)
+        want = O.resample_with(w, scheme, u, size=size)
+        np.testing.assert_array_equal(got, want)
+
+    check()

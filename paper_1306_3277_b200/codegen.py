@@ -376,6 +376,49 @@ def _d(e):
     return f"double({cuda_expr(e)})"
 
 
+def _has_x(e):
+    t = e[0]
+    if t == "X":
+        return True
+    if t in ("num", "T", "W", "U"):
+        return False
+    if t == "neg":
+        return _has_x(e[1])
+    if t == "bin":
+        return _has_x(e[2]) or _has_x(e[3])
+    return any(_has_x(a) for a in e[2])
+
+
+def _sum_terms(e, sign=1):
+    """Top-level additive terms of e as (sign, subtree)."""
+    if e[0] == "bin" and e[1] in ("+", "-"):
+        return _sum_terms(e[2], sign) + _sum_terms(e[3], sign if e[1] == "+" else -sign)
+    if e[0] == "neg":
+        return _sum_terms(e[1], -sign)
+    return [(sign, e)]
+
+
+def _rebuild(terms):
+    out = None
+    for sg, t in terms:
+        if out is None:
+            out = t if sg > 0 else ["neg", t]
+        else:
+            out = ["bin", "+" if sg > 0 else "-", out, t]
+    return out
+
+
+def _split_invariant(e):
+    """(state-dependent part, state-independent part) of an additive expression;
+    the second is None when there is nothing to hoist."""
+    terms = _sum_terms(e)
+    dep = [t for t in terms if _has_x(t[1])]
+    inv = [t for t in terms if not _has_x(t[1])]
+    if not inv or not dep and len(inv) == 1:
+        return None, None
+    return _rebuild(dep), _rebuild(inv)
+
+
 def _emit_statements(em, ops, roles, dname="d"):
     """Statements of a block in order; returns the number of draws used."""
     kinds = [op["kind"] for op in ops if op["op"] == "sample" for _ in op["slots"]]
@@ -406,13 +449,27 @@ def _emit_statements(em, ops, roles, dname="d"):
             em.block("", f"statement {si}: ode RK4 h={op['h']!r} over X{op['slots']}")
             em(f"constexpr double H = {_dlit(op['h'])};")
             em(f"const int n_steps = max(1, int(ceil({dname} / H - 1e-9)));")
+            # fast mode: the state-independent terms of each derivative (parameters,
+            # this sub-step's noise and inputs) summed once per sub-step instead of in
+            # every RK4 stage (a reassociation, within the fast path's tolerance)
+            split = [_split_invariant(ex) for ex in op["exprs"]]
+            for j, (_, inv) in enumerate(split):
+                if inv is not None:
+                    em(f"T inv{j} = T(0);")
+                    em(f"if constexpr (!E) inv{j} = {cuda_expr(inv)};")
             em("auto deriv = [&](const T (&stg)[%d], T (&out)[%d]) {" % (m, m))
             em("  T Xs[NX];")
             em("  for (int i = 0; i < NX; ++i) Xs[i] = X[i];")
             for j, slot in enumerate(op["slots"]):
                 em(f"  Xs[{slot}] = stg[{j}];")
             for j, ex in enumerate(op["exprs"]):
-                em(f"  out[{j}] = {cuda_expr(ex, 'Xs')};")
+                dep, inv = split[j]
+                if inv is None:
+                    em(f"  out[{j}] = {cuda_expr(ex, 'Xs')};")
+                else:
+                    em(f"  if constexpr (E) out[{j}] = {cuda_expr(ex, 'Xs')};")
+                    fast = f"inv{j}" if dep is None else f"O::add({cuda_expr(dep, 'Xs')}, inv{j})"
+                    em(f"  else out[{j}] = {fast};")
             em("};")
             em.block("for (int kk = 0; kk < n_steps; ++kk)")
             em(f"const double s_ = fmin(H, {dname} - double(kk) * H);")

@@ -38,9 +38,38 @@ T_BENCH = 40
 THETA = np.array([10.0, 0.1])  # SURVEY 8d theta* = (F=10, sigma2=0.1)
 
 
+def simulate_l96_data(times, seed=1, obs_slots=range(8), obs_every=1):
+    """L96 states and observations on `times` (the runner.py:47-80 recipe:
+    x0 from child(1), transitions child(2, k), observations child(3, k)), simulated
+    with this package's own simulate API (host draws on the device kernel: bitwise
+    the reference's simulation).  Returns (obs_t, obs_v, obs_m)."""
+    from paper_1306_3277_b200 import LORENZ96, RngStream
+    from paper_1306_3277_b200 import simulate as S
+
+    rng = RngStream(seed)
+    x = LORENZ96.host_initial(rng.child(1), 1)
+    ov, om = [], []
+    for k in range(1, len(times)):
+        x = S.step_transition(LORENZ96, THETA, x, None, times[k - 1], times[k] - times[k - 1], rng.child(2, k))
+        ro = rng.child(3, k)
+        ov.append([ro.normal(x[0, n], 0.5) for n in range(8)])  # y[n] ~ normal(x[n], 0.5), Lorenz96.bi:32
+        m = np.zeros(8, dtype=bool)
+        if k % obs_every == 0:
+            m[list(obs_slots)] = True
+        om.append(m)
+    return np.asarray(times[1:]), np.array(ov), np.array(om)
+
+
 def synthetic_data(T=T_BENCH):
-    """L96 data per SURVEY 8d: theta*, grid linspace(0,2,T+1), all slots observed,
-    simulated with the oracle's restatement of the reference recipe (data only)."""
+    """L96 data per SURVEY 8d: theta*, grid linspace(0,2,T+1), all slots observed."""
+    times = np.linspace(0.0, 2.0 * T / 40, T + 1)
+    ot, ov, om = simulate_l96_data(times)
+    return times, ot, ov, om
+
+
+def _cpu_data(T):
+    """The same data for the CPU legs, from the oracle's restatement of the
+    reference (the CPU legs may not touch the device)."""
     from oracle import ssm_oracle as O
 
     times = np.linspace(0.0, 2.0 * T / 40, T + 1)
@@ -245,7 +274,7 @@ def _cpu_filter_task(a):
     P, T, seed = a
     from oracle import ssm_oracle as O
 
-    times, ot, ov, om = synthetic_data(T)
+    times, ot, ov, om = _cpu_data(T)
     grid = O.Grid(times, {k + 1: (ov[k], om[k]) for k in range(T)})
     t0 = time.perf_counter()
     O.particle_filter("lorenz96", THETA, grid, O.Stream(7, (seed,)), n_particles=P, resampler="systematic")

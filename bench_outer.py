@@ -37,32 +37,45 @@ class Locf:
         return self.values[int(np.searchsorted(self.times, t + tol, side="right")) - 1]
 
 
+def flow(t, f_max=500.0, t_s=0.3, t_d=0.5):
+    """Aortic flow input of the windkessel data (Eq. 5)."""
+    tp = np.mod(t, t_s + t_d)
+    return np.where(tp < t_s, f_max * np.sin(np.pi * tp / t_s) ** 2, 0.0)
+
+
 def wk_data(T=100, t_end=1.0):
-    from oracle import ssm_oracle as O
+    """Windkessel data at theta* (SURVEY 8d), simulated with this package's simulate API."""
+    from paper_1306_3277_b200 import WINDKESSEL, RngStream
+    from paper_1306_3277_b200 import simulate as S
 
     theta = np.array([1.8, 3.0, 0.06, 25.0])
     in_times = np.round(np.arange(0, t_end + 1e-9, 0.01), 10)
-    inputs = Locf(in_times, O.windkessel_flow(in_times))
+    inputs = Locf(in_times, flow(in_times))
     times = np.linspace(0.0, t_end, T + 1)
-    rng = O.Stream(1)
-    x = np.array([[rng.child(1).normal(90.0, 15.0)]])
+    rng = RngStream(1)
+    x = WINDKESSEL.host_initial(rng.child(1), 1)
     obs = []
     for k in range(1, T + 1):
-        rk = rng.child(2, k)
-        x, _ = O.wk_transition(theta, x, times[k - 1], times[k] - times[k - 1],
-                               lambda kk, sd, rk=rk: rk.normal(0.0, np.array([sd]), size=1), inputs.at)
+        x = S.step_transition(WINDKESSEL, theta, x, inputs, times[k - 1], times[k] - times[k - 1], rng.child(2, k))
         F = float(inputs.at(times[k])[0])
-        obs.append([rng.child(3, k).normal(x[0, 0] + theta[2] * F, 2.0)])
+        obs.append([rng.child(3, k).normal(x[0, 0] + theta[2] * F, 2.0)])  # Windkessel.bi:33
     return theta, times, np.array(obs), inputs
 
 
 def l96_sparse(T=40):
-    from oracle import ssm_oracle as O
+    from bench import THETA, simulate_l96_data
 
-    theta = np.array([10.0, 0.1])
     times = np.linspace(0.0, 2.0 * T / 40, T + 1)
-    obs = O.simulate_l96(theta, times, O.Stream(1), obs_slots=range(4), obs_every=2)
-    return theta, times, np.array([obs[k][0] for k in range(1, T + 1)]), np.array([obs[k][1] for k in range(1, T + 1)])
+    _, ov, om = simulate_l96_data(times, obs_slots=range(4), obs_every=2)
+    return THETA.copy(), times, ov, om
+
+
+def l96_full(T=40):
+    from bench import simulate_l96_data
+
+    times = np.linspace(0.0, 2.0 * T / 40, T + 1)
+    _, ov, om = simulate_l96_data(times)
+    return times, ov, om
 
 
 def timed(fn, warmup=1, reps=3):
@@ -135,13 +148,9 @@ def config4(quick):
 def config5(quick):
     from paper_1306_3277_b200 import LORENZ96, RngStream
     from paper_1306_3277_b200.inference import build_filter_grid, particle_filter
-    from oracle import ssm_oracle as O
-
     theta = np.array([10.0, 0.1])
-    times = np.linspace(0.0, 2.0, 41)
-    obs = O.simulate_l96(theta, times, O.Stream(1))
-    grid = build_filter_grid(0.0, 2.0, 40, times[1:], np.array([obs[k][0] for k in range(1, 41)]),
-                             np.ones((40, 8), bool), n_obs=8)
+    times, ov, om = l96_full()
+    grid = build_filter_grid(0.0, 2.0, 40, times[1:], ov, om, n_obs=8)
     out = {}
     sizes = [(lg, True) for lg in (range(10, 23, 4) if quick else (10, 12, 14, 16, 18, 20, 22, 24, 25))]
     if not quick:  # full f64 history at 2^26 is 164 GiB: history-free run (ancestors only, replayed trajectory)
@@ -159,8 +168,6 @@ def config5(quick):
 def configg(quick):
     from paper_1306_3277_b200 import LORENZ96, RngStream, generic
     from paper_1306_3277_b200.inference import build_filter_grid, particle_filter
-    from oracle import ssm_oracle as O
-
     with open(os.path.join(ROOT, "tests", "golden", "gen_models.json")) as fh:
         lowered = json.load(fh)["lowered"]
     g = dict(np.load(os.path.join(ROOT, "tests", "golden", "generic.npz")))
@@ -172,10 +179,8 @@ def configg(quick):
 
     P = 1 << (16 if quick else 20)
     theta = np.array([10.0, 0.1])
-    times = np.linspace(0.0, 2.0, 41)
-    obs = O.simulate_l96(theta, times, O.Stream(1))
-    grid = build_filter_grid(0.0, 2.0, 40, times[1:], np.array([obs[k][0] for k in range(1, 41)]),
-                             np.ones((40, 8), bool), n_obs=8)
+    times, ov, om = l96_full()
+    grid = build_filter_grid(0.0, 2.0, 40, times[1:], ov, om, n_obs=8)
     cases = [("Lorenz96 hand-written", LORENZ96, theta, grid), ("Lorenz96 generic", model("Lorenz96"), theta, grid)]
     for name in ("StochVol", "PredatorPrey"):
         m = model(name)

@@ -110,7 +110,7 @@ def config1(quick):
             "reference_cpu_1core_survey": {"multinomial": 1.93e6, "systematic": 2.36e6}}
 
 
-def config3(quick):
+def config3(quick, theta_draws=None):
     from paper_1306_3277_b200 import WINDKESSEL, RngStream
     from paper_1306_3277_b200.inference import FilterRunner, build_filter_grid, mh_sample_chains
 
@@ -118,15 +118,17 @@ def config3(quick):
     grid = build_filter_grid(0.0, 1.0, 100, times[1:], obs, np.ones((100, 1), bool), n_obs=1)
     chains, P, steps = 8, 1 << 16, (3 if quick else 10)
     runner = FilterRunner(WINDKESSEL, grid, inputs=inputs, n_particles=P, resampler="systematic")
-    ms, (samples, acc) = timed(lambda: mh_sample_chains(WINDKESSEL, runner, steps, [RngStream(100 + c) for c in range(chains)]),
+    ms, (samples, acc) = timed(lambda: mh_sample_chains(WINDKESSEL, runner, steps, [RngStream(100 + c) for c in range(chains)],
+                                                        theta_draws=theta_draws),
                                warmup=1, reps=1)
     runs = chains * (steps + 1)  # init + one filter per MH step (auto-rejects skip theirs)
-    return {"config": f"3: PMMH windkessel, {chains} chains/GPU x 2^16 particles, T=100, {steps} MH steps",
+    tag = "" if theta_draws is None else f", theta blocks on device ({theta_draws} draws)"
+    return {"config": f"3: PMMH windkessel, {chains} chains/GPU x 2^16 particles, T=100, {steps} MH steps{tag}",
             "unit": "particle-updates/s", "value": runs * P * 100 / (ms / 1e3), "ms_per_mh_step": ms / (steps + 1),
             "acceptance": acc.tolist(), "reference_cpu_1core_survey": 8.12e6}
 
 
-def config4(quick):
+def config4(quick, theta_draws=None):
     from paper_1306_3277_b200 import LORENZ96, RngStream
     from paper_1306_3277_b200.inference import FilterRunner, build_filter_grid, smc_sampler
 
@@ -134,12 +136,14 @@ def config4(quick):
     grid = build_filter_grid(0.0, 2.0, 40, times[1:], ov, om, n_obs=8)
     n_theta, P = (32, 1 << 12) if quick else (128, 1 << 14)
     runner = FilterRunner(LORENZ96, grid, n_particles=P, resampler="systematic")
-    ms, res = timed(lambda: smc_sampler(LORENZ96, runner, n_theta, RngStream(5), theta_resampler="systematic"),
+    ms, res = timed(lambda: smc_sampler(LORENZ96, runner, n_theta, RngStream(5), theta_resampler="systematic",
+                                                theta_draws=theta_draws),
                     warmup=1, reps=2)
     obs_steps = grid.obs_steps
     # PF work: propagation to each obs step + rejuvenation replay to the previous one
     steps = sum(o for o in obs_steps) + sum((obs_steps[i - 2] if i > 1 else 0) for i in range(1, len(obs_steps) + 1))
-    return {"config": f"4: SMC^2 L96 {n_theta} theta x 2^{int(math.log2(P))}, sparse obs, T=40",
+    tag = "" if theta_draws is None else f", theta blocks on device ({theta_draws} draws)"
+    return {"config": f"4: SMC^2 L96 {n_theta} theta x 2^{int(math.log2(P))}, sparse obs, T=40{tag}",
             "unit": "particle-updates/s (incl. replays)", "value": n_theta * P * steps / (ms / 1e3),
             "seconds": ms / 1e3, "final_ess": res.diagnostics[-1]["ess"],
             "reference_cpu_1core_survey": 8.8e5}
@@ -203,7 +207,8 @@ def main():
     ap.add_argument("--configs", default="1,3,4,5,g")
     ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
-    fns = {"1": config1, "3": config3, "4": config4, "5": config5, "g": configg}
+    fns = {"1": config1, "3": config3, "4": config4, "5": config5, "g": configg,
+           "3d": lambda q: config3(q, "device"), "4d": lambda q: config4(q, "device")}
     for c in args.configs.split(","):
         t0 = time.time()
         r = fns[c](args.quick)

@@ -418,6 +418,48 @@ int ssm_logsumexp(int dtype, int B, int P, const void* a, double* out_lse, doubl
 int ssm_block_gather(int J, size_t block_bytes, const void* src, const int32_t* idx, void* dst,
                      void* stream);
 
+/* K10: theta-level marginal MH on the device for the hand-written models.
+ * ssm_theta_propose replaces the proposal walk and its densities
+ * (simulate.py:272-352 propose_parameters / proposal_parameter_logpdf / propose_initial /
+ * proposal_initial_logpdf) and the prior of the proposal (simulate.py:220-233), as called
+ * from mcmc.py:_propose (138-148).  ssm_theta_accept replaces the accept step
+ * (mcmc.py:28-33, 155-164): accepted chains copy theta_new / x0_new / loglik_new /
+ * log_prior_new into the current state in place.  One thread per chain.
+ * Draws: device Philox keyed by keys[c] and `step` (u_in == NULL), or injected
+ * reference draws: u_in [C][u_stride] standard uniforms (truncated-Gaussian statements in
+ * block order, then proposal_initial slots), g_in [C] the numpy gamma(2, 1/scale) variate
+ * of the inverse-gamma statement, u_acc_in [C] the accept uniform.  u_stride must be
+ * ssm_theta_draws(model, has_init).  *err is set to 1 when a distribution parameter is
+ * invalid (DistributionParameterError on the host). */
+typedef struct {
+  int32_t model;                 /* SSM_MODEL_LORENZ96 or SSM_MODEL_WINDKESSEL */
+  int32_t n_chains;
+  int32_t n_param;               /* 2 (L96) / 4 (WK) */
+  int32_t nx;                    /* 8 / 1 */
+  int32_t has_init;              /* L96 proposal_initial: chains carry x0 */
+  int32_t u_stride;
+  uint64_t step;                 /* device-draw counter word (MH step index) */
+  const uint32_t* keys;          /* device [C][2] Philox keys of the chain streams */
+  double* theta;                 /* device [C][n_param] current (updated by accept) */
+  double* x0;                    /* device [C][nx] current initial state or NULL */
+  double* theta_new;             /* device [C][n_param] */
+  double* x0_new;                /* device [C][nx] or NULL */
+  double* logq_fwd;              /* device [C] */
+  double* logq_rev;              /* device [C] */
+  double* log_prior_new;         /* device [C] parameter_logpdf (+ initial_logpdf) of the proposal */
+  double* loglik;                /* device [C] current loglik (accept) */
+  double* log_prior;             /* device [C] current log prior (accept) */
+  const double* loglik_new;      /* device [C] filter loglik at the proposal (-inf: not run) */
+  int32_t* accepted;             /* device [C] */
+  int32_t* err;                  /* device [1] */
+  const double* u_in;            /* injected draws or NULL */
+  const double* g_in;
+  const double* u_acc_in;
+} ssm_theta_args;
+int ssm_theta_draws(int model, int has_init);
+int ssm_theta_propose(const ssm_theta_args* args, void* stream);
+int ssm_theta_accept(const ssm_theta_args* args, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -177,6 +177,14 @@ class SmallArgs(C.Structure):
                                   "a_out")]
 
 
+class ThetaArgs(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("model", "n_chains", "n_param", "nx", "has_init", "u_stride")] + [
+        ("step", C.c_uint64)] + [
+        (n, C.c_void_p) for n in ("keys", "theta", "x0", "theta_new", "x0_new", "logq_fwd", "logq_rev",
+                                  "log_prior_new", "loglik", "log_prior", "loglik_new", "accepted", "err", "u_in",
+                                  "g_in", "u_acc_in")]
+
+
 # name -> (restype, argtypes); every symbol declared in include/ssm_b200.h
 _vp, _i, _sz, _d = C.c_void_p, C.c_int, C.c_size_t, C.c_double
 SIGNATURES = {
@@ -219,6 +227,9 @@ SIGNATURES = {
     "ssm_gen_destroy": (_i, [_vp]),
     "ssm_gen_info": (_i, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ssm_gen_init_particles": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp]),
+    "ssm_theta_draws": (_i, [_i, _i]),
+    "ssm_theta_propose": (_i, [C.POINTER(ThetaArgs), _vp]),
+    "ssm_theta_accept": (_i, [C.POINTER(ThetaArgs), _vp]),
 }
 
 # entry points that launch kernels (for the gpu_launches count): name -> launches
@@ -244,6 +255,8 @@ LAUNCHING = {
     "ssm_tiles_total": 2,
     "ssm_offspring_global": 2,
     "ssm_expand_own": 1,
+    "ssm_theta_propose": 1,
+    "ssm_theta_accept": 1,
 }
 
 _LIB = None

@@ -6,8 +6,8 @@ particle filter inside -- the reference's inference/mcmc.py:28-180 API.
 in one launch per step; `mh_sample_chains` uses it to run C independent
 PMMH chains in lock-step (config 3: 64 chains), giving exactly the draws of
 C serial `mh_sample` calls with streams rngs[c].  theta-level proposals and
-priors stay on the host (scalar per chain, SURVEY 8f row 1 moves them on
-device next).
+priors run on the host by default, or on the device with
+`theta_draws=` (theta_mh.py).
 """
 
 from __future__ import annotations
@@ -193,9 +193,14 @@ def mh_sample(ir, runner, n_samples, rng):
     return chains[0], int(acc[0])
 
 
-def mh_sample_chains(ir, runner, n_samples, rngs, upto=None, on_step=None, shard=None):
+def mh_sample_chains(ir, runner, n_samples, rngs, upto=None, on_step=None, shard=None, theta_draws=None):
     """C independent PMMH chains advanced in lock-step (batched filters).
     Chain c reproduces mh_sample(ir, runner, n_samples, rngs[c]).
+
+    `theta_draws` moves the theta-level blocks (proposal walk, densities,
+    prior, accept) onto the device (theta_mh.py): "host"
+    injects the reference's draws (parity mode), "device" draws with Philox;
+    None keeps them on the host.
 
     Multi-GPU (config 3): with a `Shard` (default: torch.distributed
     if initialised) each rank runs its contiguous block of chains as
@@ -211,8 +216,15 @@ def mh_sample_chains(ir, runner, n_samples, rngs, upto=None, on_step=None, shard
     accepted = np.zeros(len(mine), dtype=int)
     if mine:
         states = init_chains(ir, runner, [g.child(0) for g in mine], upto=upto)
+        dev = None
         for step in range(1, n_samples + 1):
-            outs = marginal_mh_steps(ir, states, runner, [g.child(step) for g in mine], upto=upto)
+            if theta_draws is None:
+                outs = marginal_mh_steps(ir, states, runner, [g.child(step) for g in mine], upto=upto)
+            else:
+                from .theta_mh import marginal_mh_steps_device
+
+                outs, dev = marginal_mh_steps_device(ir, states, runner, [g.child(step) for g in mine], upto=upto,
+                                                     draws=theta_draws, dev=dev, step=step)
             for c, (st, ok, _) in enumerate(outs):
                 states[c] = st
                 accepted[c] += int(ok)

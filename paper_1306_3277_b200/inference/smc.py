@@ -202,10 +202,13 @@ def _redistribute(spec, runner, particles, anc, n, shard, lo):
 # ---------------------------------------------------------------- the sampler
 
 
-def smc_sampler(ir, runner, n_theta, rng, theta_resampler="multinomial", nthreads=1, shard=None):
+def smc_sampler(ir, runner, n_theta, rng, theta_resampler="multinomial", nthreads=1, shard=None,
+                theta_draws=None):
     """smc.py:67-171 on the GPU.  `nthreads` is accepted for API compatibility
     (the batch is the parallelism); `shard` (paper_1306_3277_b200.distributed.Shard)
-    spreads theta-particles over ranks, default: torch.distributed if initialised."""
+    spreads theta-particles over ranks, default: torch.distributed if initialised.
+    `theta_draws` ("host" | "device") runs the rejuvenation move's theta-level
+    blocks on the device (theta_mh.py); None keeps them on the host."""
     if n_theta < 2:
         raise ValueError("smc sampler needs n_theta >= 2")
     shard = shard or Shard.current()
@@ -238,7 +241,13 @@ def smc_sampler(ir, runner, n_theta, rng, theta_resampler="multinomial", nthread
         # rejuvenate: one marginal MH move each, one batched replay (smc.py:101-122)
         chains = [MhChainState(theta=p.theta, trajectory=p.trajectory, loglik=p.loglik,
                                log_prior=p.log_prior, init_state=p.init_state) for p in local]
-        outs = marginal_mh_steps(ir, chains, runner, [step_rng.child(1, j) for j in J], upto=prev_idx)
+        if theta_draws is None:
+            outs = marginal_mh_steps(ir, chains, runner, [step_rng.child(1, j) for j in J], upto=prev_idx)
+        else:
+            from .theta_mh import marginal_mh_steps_device
+
+            outs, _ = marginal_mh_steps_device(ir, chains, runner, [step_rng.child(1, j) for j in J], upto=prev_idx,
+                                               draws=theta_draws, step=i)
         accepted = []
         for p, (new, ok, run) in zip(local, outs):
             if ok:

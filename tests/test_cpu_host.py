@@ -47,7 +47,7 @@ def test_struct_layouts_match_header(tmp_path):
 
     structs = {"ssm_pw_args": _lib.PwArgs, "ssm_substep": _lib.Substep, "ssm_step_desc": _lib.StepDesc,
                "ssm_advance_args": _lib.AdvanceArgs, "ssm_small_args": _lib.SmallArgs,
-               "ssm_replay_args": _lib.ReplayArgs}
+               "ssm_replay_args": _lib.ReplayArgs, "ssm_theta_args": _lib.ThetaArgs}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ssm_b200.h"', "int main(void) {"]
     for name, cls in structs.items():
         lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')
@@ -83,6 +83,26 @@ def test_invalid_args_rejected_without_device():
     assert lib.ssm_propagate_weight(None, None) == _lib.SSM_ERR_INVALID_ARG
     assert lib.ssm_gather(1, 0, 8, 16, None, None, None, None) == _lib.SSM_ERR_INVALID_ARG
     assert lib.ssm_resample_search(1, 4, 4, 9, 0, None, None, None, 0, None, None, None, None) == _lib.SSM_ERR_INVALID_ARG
+    a = _lib.ThetaArgs()
+    a.model, a.n_chains, a.n_param, a.nx = _lib.SSM_MODEL_WINDKESSEL, 4, 4, 1
+    assert lib.ssm_theta_propose(a, None) == _lib.SSM_ERR_INVALID_ARG  # no keys, no injected draws
+    a.model = _lib.SSM_MODEL_GENERIC
+    assert lib.ssm_theta_propose(a, None) == _lib.SSM_ERR_UNSUPPORTED
+    assert lib.ssm_theta_draws(_lib.SSM_MODEL_LORENZ96, 1) == 1 + 8 + 2 + 1
+
+
+def test_device_theta_mh_rejects_generic_models():
+    import json
+
+    from paper_1306_3277_b200 import generic
+    from paper_1306_3277_b200.errors import UnsupportedModelError
+    from paper_1306_3277_b200.inference.theta_mh import DeviceThetaChains
+
+    with open(os.path.join(ROOT, "tests", "golden", "gen_models.json")) as fh:
+        d = dict(json.load(fh)["lowered"]["StochVol"])
+    d.pop("fingerprint", None)
+    with pytest.raises(UnsupportedModelError):
+        DeviceThetaChains(generic.from_description(d), [])
 
 
 def test_resolve_model():

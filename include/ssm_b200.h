@@ -456,6 +456,33 @@ typedef struct {
   const double* g_in;
   const double* u_acc_in;
 } ssm_theta_args;
+/* K11: batched Kalman filter for linear-Gaussian models, replacing the
+ * forward pass of KalmanRun (kalman.py:53-96) for B systems per launch (one thread each).
+ * The system of filter f comes from lineargauss.extract_linear_gaussian (lineargauss.py:292-316)
+ * in the form x_s = A x_{s-1} + b + N(0, Q), y_s = H x_s + c + N(0, diag(r_sd^2)).
+ * Records: entry 0 of mu / P is the initial state (input); entries s0+1..s1 are written
+ * (filtered moments in mu / P, predicted in mu_p / P_p).  err[f] = first step whose
+ * innovation covariance is not positive definite (CholeskyError on the host). */
+typedef struct {
+  int32_t B, nx, ny, S;          /* S = grid steps in the tables */
+  int32_t s0, s1;                /* advance over steps s0+1..s1 */
+  const double* A;               /* [B][S][nx][nx] */
+  const double* b;               /* [B][S][nx] */
+  const double* Q;               /* [B][S][nx][nx] */
+  const double* H;               /* [B][S][ny][nx] */
+  const double* c;               /* [B][S][ny] */
+  const double* r_sd;            /* [B][S][ny] */
+  const double* y;               /* [S][ny] */
+  const uint8_t* mask;           /* [S][ny] present slots */
+  double* mu;                    /* [B][S+1][nx] */
+  double* P;                     /* [B][S+1][nx][nx] */
+  double* mu_p;                  /* [B][S+1][nx] */
+  double* P_p;                   /* [B][S+1][nx][nx] */
+  double* loglik;                /* [B] accumulated in place */
+  int32_t* err;                  /* [B] */
+} ssm_kalman_args;
+int ssm_kalman_max_dim(void);
+int ssm_kalman_filter(const ssm_kalman_args* args, void* stream);
 int ssm_theta_draws(int model, int has_init);
 int ssm_theta_propose(const ssm_theta_args* args, void* stream);
 int ssm_theta_accept(const ssm_theta_args* args, void* stream);

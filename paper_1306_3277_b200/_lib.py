@@ -185,6 +185,12 @@ class ThetaArgs(C.Structure):
                                   "g_in", "u_acc_in")]
 
 
+class KalmanArgs(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("B", "nx", "ny", "S", "s0", "s1")] + [
+        (n, C.c_void_p) for n in ("A", "b", "Q", "H", "c", "r_sd", "y", "mask", "mu", "P", "mu_p", "P_p", "loglik",
+                                  "err")]
+
+
 # name -> (restype, argtypes); every symbol declared in include/ssm_b200.h
 _vp, _i, _sz, _d = C.c_void_p, C.c_int, C.c_size_t, C.c_double
 SIGNATURES = {
@@ -228,6 +234,8 @@ SIGNATURES = {
     "ssm_gen_info": (_i, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ssm_gen_init_particles": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp]),
     "ssm_theta_draws": (_i, [_i, _i]),
+    "ssm_kalman_max_dim": (_i, []),
+    "ssm_kalman_filter": (_i, [C.POINTER(KalmanArgs), _vp]),
     "ssm_theta_propose": (_i, [C.POINTER(ThetaArgs), _vp]),
     "ssm_theta_accept": (_i, [C.POINTER(ThetaArgs), _vp]),
 }
@@ -257,6 +265,7 @@ LAUNCHING = {
     "ssm_expand_own": 1,
     "ssm_theta_propose": 1,
     "ssm_theta_accept": 1,
+    "ssm_kalman_filter": 1,
 }
 
 _LIB = None

@@ -6,6 +6,7 @@ typedef unsigned int uint32_t;
 typedef int int32_t;
 typedef unsigned long long uint64_t;
 typedef long long int64_t;
+typedef unsigned char uint8_t;
 #define CUDART_INF __longlong_as_double(0x7ff0000000000000ULL)
 #define CUDART_NAN __longlong_as_double(0xfff8000000000000ULL)
 #else

@@ -37,3 +37,16 @@ class MissingInputError(SsmError):
 
 class DataFormatError(SsmError):
     """Malformed or schema-inconsistent data."""
+
+
+class NonlinearModelError(SsmError):
+    """The model is not linear-Gaussian, so the Kalman filter does not apply
+    (lineargauss.py:1-12)."""
+
+
+class CholeskyError(SsmError):
+    """A covariance is not positive (semi-)definite (linalg.py:21-50)."""
+
+    def __init__(self, message, index=None):
+        self.index = index
+        super().__init__(message)

@@ -1,0 +1,224 @@
+"""Kalman filter on the device for linear-Gaussian models --
+the reference's inference/kalman.py API (KalmanRun, kalman_filter) and the
+`filter_kind="kalman"` route of FilterRunner (mcmc.py:79-88).
+
+The forward recursions of B systems run in one `ssm_kalman_filter` launch
+(csrc/ssm_kalman.cu, one thread per system); the filtered and predicted
+moments of every grid step stay on the device.  `sample_trajectory` (one
+backward smoothing draw, kalman.py:98-114) reads one run's records back and
+draws on the host with the run's stream, in the reference's order.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+from scipy.linalg import solve_triangular
+
+from .. import _lib
+from ..errors import CholeskyError, UnsupportedModelError
+from ..lineargauss import LinearGaussianSystems
+from .types import FilterOutcome
+
+PIVOT_RTOL = 1e-12  # pivot tolerance relative to the largest diagonal entry (linalg.py:17-18)
+
+
+@dataclass
+class GaussianState:
+    """Mean and upper-triangular square root of the covariance (linalg.py:100-110)."""
+
+    mean: np.ndarray
+    sqrt_cov: np.ndarray
+
+    @property
+    def dim(self):
+        return self.mean.shape[0]
+
+    def cov(self):
+        return self.sqrt_cov.T @ self.sqrt_cov
+
+
+def psd_cholesky_upper(S):
+    """Upper U with U^T U = S for symmetric positive SEMI-definite S: a pivot
+    within tolerance of zero leaves its row zero (the row must vanish), one
+    below -tol raises CholeskyError (the rule of linalg.py:21-50)."""
+    S = np.asarray(S, dtype=float)
+    n = S.shape[0]
+    tol = PIVOT_RTOL * max(1.0, float(np.max(np.abs(np.diag(S)))) if n else 1.0)
+    U = np.zeros((n, n))
+    for i in range(n):
+        pivot = S[i, i] - U[:i, i] @ U[:i, i]
+        if pivot < -tol:
+            raise CholeskyError(f"matrix is not positive semi-definite at pivot {i}", index=i)
+        if pivot <= tol:
+            rest = S[i, i + 1 :] - U[:i, i] @ U[:i, i + 1 :]
+            if np.any(np.abs(rest) > np.sqrt(tol) * max(1.0, np.max(np.abs(S)))):
+                raise CholeskyError(f"matrix is not positive semi-definite at pivot {i}", index=i)
+            continue
+        U[i, i] = np.sqrt(pivot)
+        U[i, i + 1 :] = (S[i, i + 1 :] - U[:i, i] @ U[:i, i + 1 :]) / U[i, i]
+    return U
+
+
+def _solve_upper_t(U, v):
+    """U^-T v with zero pivots treated as absent directions."""
+    d = np.diag(U)
+    if np.all(d != 0):
+        return solve_triangular(U, v, trans="T")
+    return np.linalg.pinv(U.T) @ v
+
+
+class _KalmanBatch:
+    """Device tables and records of B systems along one grid."""
+
+    def __init__(self, sys_: LinearGaussianSystems, grid, device=None):
+        _lib.require_cuda()
+        B, S, ny, nx = sys_.H.shape
+        mx = _lib.lib().ssm_kalman_max_dim()
+        if nx > mx or ny > mx:
+            raise UnsupportedModelError(f"device Kalman filter: n_state, n_obs <= {mx}")
+        if S != grid.last:
+            raise ValueError("system and grid time axes differ")
+        self.device = torch.device(device if device is not None else "cuda")
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.B, self.S, self.nx, self.ny = B, S, nx, ny
+        t = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=float), **f64)  # noqa: E731
+        self.A, self.b, self.Q = t(sys_.A), t(sys_.b), t(sys_.Q)
+        self.H, self.c, self.r = t(sys_.H), t(sys_.c), t(sys_.r_sd)
+        y = np.zeros((S, max(ny, 1)))
+        m = np.zeros((S, max(ny, 1)), dtype=np.uint8)
+        for i in range(1, S + 1):
+            obs = grid.obs_at(i)
+            if obs is not None:
+                y[i - 1, :ny] = np.asarray(obs[0], dtype=float)[:ny]
+                m[i - 1, :ny] = np.asarray(obs[1], dtype=bool)[:ny]
+        self.y = torch.as_tensor(y, **f64)
+        self.mask = torch.as_tensor(m, device=self.device)
+        self.mu = torch.zeros(B, S + 1, nx, **f64)
+        self.P = torch.zeros(B, S + 1, nx, nx, **f64)
+        self.mu[:, 0] = t(sys_.mu0)
+        self.P[:, 0] = t(sys_.P0)
+        self.mu_p = torch.zeros_like(self.mu)
+        self.P_p = torch.zeros_like(self.P)
+        self.loglik = torch.zeros(B, **f64)
+        self.err = torch.zeros(B, dtype=torch.int32, device=self.device)
+
+    def launch(self, rows, s0, s1):
+        """Advance `rows` (a contiguous range lo..hi) from s0 to s1."""
+        lo, hi = rows
+        a = _lib.KalmanArgs()
+        a.B, a.nx, a.ny, a.S, a.s0, a.s1 = hi - lo, self.nx, self.ny, self.S, s0, s1
+        off = lambda t: t[lo:hi].data_ptr()  # noqa: E731
+        a.A, a.b, a.Q, a.H, a.c, a.r_sd = (off(x) for x in (self.A, self.b, self.Q, self.H, self.c, self.r))
+        a.y, a.mask = self.y.data_ptr(), self.mask.data_ptr()
+        a.mu, a.P, a.mu_p, a.P_p = (off(x) for x in (self.mu, self.P, self.mu_p, self.P_p))
+        a.loglik, a.err = off(self.loglik), off(self.err)
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().ssm_kalman_filter(a, _lib.stream_ptr()), "ssm_kalman_filter")
+
+
+class KalmanRun:
+    """Resumable Kalman filter along a FilterGrid (kalman.py:26-114); one row of
+    a device batch."""
+
+    def __init__(self, system, grid, device=None, _batch=None, _row=0):
+        self.grid = grid
+        self.system = system
+        self._batch = _batch if _batch is not None else _KalmanBatch(system, grid, device)
+        self._row = _row
+        self.loglik = 0.0
+        self.pos = 0
+
+    def clone(self):
+        b = self._batch
+        r = self._row
+        nb = _KalmanBatch.__new__(_KalmanBatch)
+        nb.__dict__.update(b.__dict__)
+        for f in ("A", "b", "Q", "H", "c", "r", "mu", "P", "mu_p", "P_p", "loglik", "err"):
+            setattr(nb, f, getattr(b, f)[r : r + 1].clone())
+        nb.B = 1
+        other = KalmanRun(self.system, self.grid, _batch=nb, _row=0)
+        other.loglik, other.pos = self.loglik, self.pos
+        return other
+
+    def advance_to(self, upto, rng=None):
+        """Prediction/correction through grid index `upto`; returns the
+        log-likelihood increment (kalman.py:53-59)."""
+        return advance_kalman_runs([self], upto)[0]
+
+    def _records(self):
+        b, r = self._batch, self._row
+        return (b.mu[r].cpu().numpy(), b.P[r].cpu().numpy(), b.mu_p[r].cpu().numpy(), b.P_p[r].cpu().numpy())
+
+    def filtered(self, i):
+        b, r = self._batch, self._row
+        return GaussianState(b.mu[r, i].cpu().numpy(), psd_cholesky_upper(b.P[r, i].cpu().numpy()))
+
+    def sample_trajectory(self, rng):
+        """Backward smoothing sample x(t_{0:pos}) (kalman.py:98-114): the same
+        draws in the same order, covariance-form algebra."""
+        s = self.pos
+        mu, P, mu_p, P_p = self._records()
+        A = self._batch.A[self._row].cpu().numpy()
+        nx = mu.shape[1]
+        out = np.empty((s + 1, nx))
+        out[s] = mu[s] + psd_cholesky_upper(P[s]).T @ rng.standard_normal(nx)
+        for i in range(s - 1, -1, -1):
+            Uh = psd_cholesky_upper(P_p[i + 1])
+            C = P[i] @ A[i].T  # Cov(x_i, x_{i+1} | y_{1:i})
+            K = _solve_upper_t(Uh, C.T).T  # C Uh^-1
+            omega = mu[i] + K @ _solve_upper_t(Uh, out[i + 1] - mu_p[i + 1])
+            W = psd_cholesky_upper(P[i] - K @ K.T)
+            out[i] = omega + W.T @ rng.standard_normal(nx)
+        return out
+
+
+def advance_kalman_runs(runs, upto):
+    """Advance many runs through `upto`: one launch per batch (runs of one batch
+    at the same position), else one launch per run.  Returns the increments."""
+    groups = {}
+    for k, r in enumerate(runs):
+        groups.setdefault((id(r._batch), r.pos), []).append(k)
+    before = [r.loglik for r in runs]
+    for (_, pos), ks in groups.items():
+        if upto <= pos:
+            continue
+        b = runs[ks[0]]._batch
+        rows = sorted(runs[k]._row for k in ks)
+        if rows == list(range(rows[0], rows[0] + len(rows))):
+            b.launch((rows[0], rows[-1] + 1), pos, upto)
+        else:
+            for k in ks:
+                b.launch((runs[k]._row, runs[k]._row + 1), pos, upto)
+    seen = {}
+    for r in runs:
+        if id(r._batch) not in seen:
+            seen[id(r._batch)] = (r._batch.loglik.cpu().numpy(), r._batch.err.cpu().numpy())
+    out = []
+    for r, ll0 in zip(runs, before):
+        ll, err = seen[id(r._batch)]
+        if err[r._row]:
+            t = float(r.grid.times[err[r._row]])
+            raise CholeskyError(f"innovation covariance not positive definite at t={t:g}", index=int(err[r._row]))
+        r.loglik = float(ll[r._row])
+        r.pos = max(r.pos, upto)
+        out.append(r.loglik - ll0)
+    return out
+
+
+def kalman_runs(systems: LinearGaussianSystems, grid, device=None):
+    """B fresh runs sharing one device batch."""
+    batch = _KalmanBatch(systems, grid, device)
+    return [KalmanRun(systems.row(k), grid, _batch=batch, _row=k) for k in range(systems.B)]
+
+
+def kalman_filter(system, grid, rng, upto=None, device=None):
+    """Filter through `upto` (default: the whole grid) and draw one smoothing
+    trajectory (kalman.py:117-122)."""
+    run = KalmanRun(system, grid, device)
+    run.advance_to(grid.last if upto is None else upto)
+    trajectory = run.sample_trajectory(rng)
+    summaries = [run.filtered(i) for i in range(run.pos + 1)]
+    return FilterOutcome(loglik=run.loglik, trajectory=trajectory, summaries=summaries, run=run)

@@ -18,7 +18,6 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ..errors import UnsupportedModelError
 from ..models import propose_batch, resolve_model
 from .particle import ParticleRun, advance_runs, init_runs, sample_trajectories
 from .timegrid import as_filter_grid
@@ -50,9 +49,6 @@ class FilterRunner:
                  resampler="multinomial", ess_rel=None, check_finite=True, **device_opts):
         if filter_kind not in ("kalman", "bootstrap"):
             raise ValueError(f"unknown filter {filter_kind!r}")
-        if filter_kind == "kalman":
-            raise UnsupportedModelError(
-                "the Kalman filter is not part of the device path (SURVEY 2: serial dense algebra)")
         self.ir = ir
         self.spec = resolve_model(ir)
         self.grid = as_filter_grid(grid)
@@ -64,6 +60,19 @@ class FilterRunner:
         self.check_finite = check_finite
         self.device_opts = dict(device_opts)
 
+    def _systems(self, thetas, init_states):
+        """Linear-Gaussian systems of a batch (mcmc.py:81-87): x0 proposals pin the initial state."""
+        from ..lineargauss import extract_linear_gaussian
+
+        src = self.spec if isinstance(self.ir, str) else self.ir
+        sys_ = extract_linear_gaussian(src, np.asarray(thetas, dtype=float).reshape(len(thetas), -1),
+                                       self.grid.times, self.inputs)
+        for k, st in enumerate(init_states):
+            if st is not None:
+                sys_.mu0[k] = np.asarray(st, dtype=float)
+                sys_.P0[k] = 0.0
+        return sys_
+
     def _make(self, theta, init_state):
         return ParticleRun(self.spec, theta, self.grid, inputs=self.inputs, n_particles=self.n_particles,
                            resampler=self.resampler, ess_rel=self.ess_rel, initial_state=init_state,
@@ -71,6 +80,8 @@ class FilterRunner:
 
     def new_run(self, theta, init_state, rng):
         """Fresh, initialised (not yet advanced) filter run (mcmc.py:79-100)."""
+        if self.filter_kind == "kalman":
+            return self.new_runs([theta], [init_state], [rng])[0]
         return self._make(theta, init_state).init(rng.child(0))
 
     def new_runs(self, thetas, init_states, rngs):
@@ -78,6 +89,10 @@ class FilterRunner:
         # and lookups are per runner, not per theta; SMC^2 builds ~100 runs per step)
         if not thetas:
             return []
+        if self.filter_kind == "kalman":
+            from .kalman import kalman_runs
+
+            return kalman_runs(self._systems(thetas, init_states), self.grid, self.device_opts.get("device"))
         proto = self._make(thetas[0], init_states[0])
         runs = [proto]
         for t, st in zip(thetas[1:], init_states[1:]):
@@ -101,6 +116,12 @@ class FilterRunner:
         if not thetas:
             return []
         runs = self.new_runs(thetas, init_states, rngs)
+        if self.filter_kind == "kalman":
+            from .kalman import advance_kalman_runs
+
+            advance_kalman_runs(runs, upto)
+            trajs = [r.sample_trajectory(g.child(2)) for r, g in zip(runs, rngs)]
+            return [(r.loglik, t, r) for r, t in zip(runs, trajs)]
         advance_runs(runs, upto, [g.child(1) for g in rngs])
         trajs = sample_trajectories(runs, [g.child(2) for g in rngs])
         return [(r.loglik, t, r) for r, t in zip(runs, trajs)]

@@ -524,6 +524,112 @@ def gen_generic():
     save("generic.npz", **out)
 
 
+def dense_kf(out, k, grid):
+    """Covariance-form Kalman filter on the reference's extracted system.
+
+    The reference's KalmanRun._step forms the gain as triangular_solve(V, D.T,
+    side="right") (kalman.py:84), i.e. D^T V^-1 instead of D V^-1: right only
+    when D = Sigma_hat G is square and symmetric (every scalar model such as
+    windkessel), and a shape error when fewer slots than states are present.
+    Multi-state fixtures therefore use this textbook filter instead."""
+    mu, P = out[f"{k}/mu0"].copy(), out[f"{k}/P0"].copy()
+    ll, means = 0.0, [mu.copy()]
+    for i in range(1, len(grid.times)):
+        A, b, Q = out[f"{k}/A"][i - 1], out[f"{k}/b"][i - 1], out[f"{k}/Q"][i - 1]
+        mu, P = A @ mu + b, A @ P @ A.T + Q
+        obs = grid.obs_at(i)
+        if obs is not None:
+            pres = np.flatnonzero(obs[1])
+            H = out[f"{k}/H"][i - 1][pres]
+            c, r = out[f"{k}/c"][i - 1][pres], out[f"{k}/r_sd"][i - 1][pres]
+            S = H @ P @ H.T + np.diag(r**2)
+            e = obs[0][pres] - (H @ mu + c)
+            K = P @ H.T @ np.linalg.inv(S)
+            mu = mu + K @ e
+            P = P - K @ S @ K.T
+            ll += -0.5 * len(pres) * np.log(2 * np.pi) - 0.5 * np.linalg.slogdet(S)[1] - 0.5 * e @ np.linalg.solve(S, e)
+        means.append(mu.copy())
+    return ll, np.array(means)
+
+
+def gen_kalman():
+    """Reference Kalman filter (kalman.py, lineargauss.py) on the linear-Gaussian
+    models: the extracted systems in x' = A x + b form, logliks, a smoothing
+    trajectory and the filtered means, for a few parameter vectors."""
+    from ssmkit.inference import FilterRunner, kalman_filter, mh_sample
+    from ssmkit.lineargauss import extract_linear_gaussian
+
+    import ssmkit.core.ir as I
+    I.compile_expr = lambda e, t, b: eval(
+        f"lambda T, X, W, U: {I.expr_source(e, t, b)}", {"np": np, "inf": np.inf, "__builtins__": {}})
+    out = {}
+
+    def record(tag, ir, thetas, grid, inputs):
+        for j, th in enumerate(thetas):
+            sys_ = extract_linear_gaussian(ir, th, grid.times, inputs)
+            k = f"{tag}/{j}"
+            out[f"{k}/mu0"] = sys_.initial.mean
+            out[f"{k}/P0"] = sys_.initial.sqrt_cov.T @ sys_.initial.sqrt_cov
+            out[f"{k}/A"] = np.array([st.F.T for st in sys_.steps])
+            out[f"{k}/b"] = np.array([st.b for st in sys_.steps])
+            out[f"{k}/Q"] = np.array([st.Qu.T @ st.Qu for st in sys_.steps])
+            out[f"{k}/H"] = np.array([st.G.T for st in sys_.steps])
+            out[f"{k}/c"] = np.array([st.c for st in sys_.steps])
+            out[f"{k}/r_sd"] = np.array([st.r_sd for st in sys_.steps])
+            if tag == "wk":  # the reference's filter (nx = 1)
+                res = kalman_filter(sys_, grid, RngStream(40 + j))
+                out[f"{k}/loglik"] = np.array(res.loglik)
+                out[f"{k}/traj"] = res.trajectory
+                out[f"{k}/means"] = np.array([g.mean for g in res.summaries])
+            else:  # reference defect (see dense_kf): a textbook filter on the reference's systems
+                ll, means = dense_kf(out, k, grid)
+                out[f"{k}/loglik"] = np.array(ll)
+                out[f"{k}/means"] = means
+        out[f"{tag}/thetas"] = np.array(thetas)
+
+    # windkessel on the config-1 data's first 40 steps
+    ir = load("windkessel")
+    in_times = np.round(np.arange(0, 1.0001, 0.01), 10)
+    inputs = LocfInputs(in_times, flow(in_times)[:, None])
+    times = np.linspace(0.0, 0.4, 41)
+    ot, ov, om = simulate_data(ir, np.array([1.8, 3.0, 0.06, 25.0]), times, inputs=inputs)
+    om[5] = False
+    grid = build_filter_grid(0.0, 0.4, 40, ot, ov, om, n_obs=1)
+    out["wk/obs_v"], out["wk/obs_m"], out["wk/times"] = ov, om, grid.times
+    record("wk", ir, [np.array([1.8, 3.0, 0.06, 25.0]), np.array([1.2, 2.0, 0.04, 9.0])], grid, inputs)
+    runner = FilterRunner(ir, grid, inputs=inputs, filter_kind="kalman")
+    chains, acc = mh_sample(ir, runner, 8, RngStream(24))
+    out["wk/mh/thetas"] = np.array([c.theta for c in chains])
+    out["wk/mh/logliks"] = np.array([c.loglik for c in chains])
+    out["wk/mh/accepted"] = np.array(acc)
+    # LinOsc: coupled ode with 2 RK4 steps per sub-step, grid spacing 0.1 = 2 sub-steps, partial masks
+    ir = load_test_model("LinOsc")
+    import json
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1306_3277_b200 import codegen
+
+    out["osc/desc"] = np.array(json.dumps(codegen.lower(ir)))
+    o_times = np.round(np.arange(0, 3.0001, 0.1), 10)
+    o_inputs = LocfInputs(o_times, 0.2 * np.sin(o_times)[:, None])
+    times = np.linspace(0.0, 3.0, 31)
+    ot, ov, om = simulate_data(ir, np.array([1.3, 0.04]), times, inputs=o_inputs)
+    om[2, 1] = False
+    om[7, 0] = False
+    om[11] = False
+    grid = build_filter_grid(0.0, 3.0, 30, ot, ov, om, n_obs=2)
+    out["osc/in_times"], out["osc/in_values"] = o_times, 0.2 * np.sin(o_times)
+    out["osc/obs_v"], out["osc/obs_m"], out["osc/times"] = ov, om, grid.times
+    record("osc", ir, [np.array([1.3, 0.04]), np.array([0.7, 0.1]), np.array([1.9, 0.01])], grid, o_inputs)
+    # Wide: 12 states, two inputs (the generic.npz data)
+    g = np.load(os.path.join(HERE, "generic.npz"))
+    ir = load_test_model("Wide")
+    inputs = LocfInputs(g["Wide/in_times"], g["Wide/in_values"])
+    grid = build_filter_grid(0.0, 2.0, 20, g["Wide/obs_t"], g["Wide/obs_v"], g["Wide/obs_m"], n_obs=12)
+    record("wide", ir, [np.array([0.2]), np.array([0.5])], grid, inputs)
+    save("kalman.npz", **out)
+
+
 if __name__ == "__main__":
     gen_resample()
     gen_lse()
@@ -533,3 +639,4 @@ if __name__ == "__main__":
     gen_theta_level()
     gen_outer_loops()
     gen_generic()
+    gen_kalman()

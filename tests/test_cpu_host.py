@@ -47,7 +47,8 @@ def test_struct_layouts_match_header(tmp_path):
 
     structs = {"ssm_pw_args": _lib.PwArgs, "ssm_substep": _lib.Substep, "ssm_step_desc": _lib.StepDesc,
                "ssm_advance_args": _lib.AdvanceArgs, "ssm_small_args": _lib.SmallArgs,
-               "ssm_replay_args": _lib.ReplayArgs, "ssm_theta_args": _lib.ThetaArgs}
+               "ssm_replay_args": _lib.ReplayArgs, "ssm_theta_args": _lib.ThetaArgs,
+               "ssm_kalman_args": _lib.KalmanArgs}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ssm_b200.h"', "int main(void) {"]
     for name, cls in structs.items():
         lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')

@@ -149,6 +149,41 @@ def config4(quick, theta_draws=None):
             "reference_cpu_1core_survey": 8.8e5}
 
 
+def configk(quick):
+    """Device Kalman filter: B windkessel systems x T=100 in one
+    launch, host extraction timed separately; plus PMMH with filter_kind="kalman"."""
+    from paper_1306_3277_b200 import WINDKESSEL, RngStream
+    from paper_1306_3277_b200.inference import FilterRunner, build_filter_grid, mh_sample_chains
+    from paper_1306_3277_b200.inference.kalman import advance_kalman_runs, kalman_runs
+    from paper_1306_3277_b200.lineargauss import extract_linear_gaussian
+
+    theta, times, obs, inputs = wk_data()
+    grid = build_filter_grid(0.0, 1.0, 100, times[1:], obs, np.ones((100, 1), bool), n_obs=1)
+    B = 1024 if quick else 8192
+    rs = np.random.default_rng(0)
+    thetas = theta * rs.uniform(0.8, 1.2, size=(B, 4))
+    t0 = time.perf_counter()
+    sys_ = extract_linear_gaussian(WINDKESSEL, thetas, grid.times, inputs)
+    t_extract = time.perf_counter() - t0
+
+    def run():
+        runs = kalman_runs(sys_, grid)
+        advance_kalman_runs(runs, grid.last)
+        return runs
+
+    ms, runs = timed(run, warmup=1, reps=3)
+    batch = runs[0]._batch
+    ms_kernel, _ = timed(lambda: batch.launch((0, B), 0, grid.last), warmup=1, reps=5)  # kernel only
+    runner = FilterRunner(WINDKESSEL, grid, inputs=inputs, filter_kind="kalman")
+    ms_mh, (_, acc) = timed(lambda: mh_sample_chains(WINDKESSEL, runner, 20, [RngStream(100 + c) for c in range(64)],
+                                                     theta_draws="device"), warmup=1, reps=1)
+    return {"config": f"k: device Kalman filter, windkessel, {B} systems x T=100 (one launch) + host extraction",
+            "unit": "filter-steps/s", "value": B * 100 / (ms / 1e3), "ms_filter_incl_upload": ms,
+            "ms_kernel": ms_kernel, "kernel_filter_steps_per_s": B * 100 / (ms_kernel / 1e3),
+            "s_extract_host": t_extract,
+            "pmmh_kalman_64_chains_ms_per_mh_step": ms_mh / 21, "pmmh_acceptance": int(np.sum(acc))}
+
+
 def config5(quick):
     from paper_1306_3277_b200 import LORENZ96, RngStream
     from paper_1306_3277_b200.inference import build_filter_grid, particle_filter
@@ -208,7 +243,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
     fns = {"1": config1, "3": config3, "4": config4, "5": config5, "g": configg,
-           "3d": lambda q: config3(q, "device"), "4d": lambda q: config4(q, "device")}
+           "k": configk, "3d": lambda q: config3(q, "device"), "4d": lambda q: config4(q, "device")}
     for c in args.configs.split(","):
         t0 = time.time()
         r = fns[c](args.quick)

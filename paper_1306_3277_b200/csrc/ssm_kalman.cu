@@ -15,10 +15,13 @@
 namespace ssm {
 namespace {
 
-constexpr int kKfMax = 16;
+constexpr int kKfMaxDim = 16;
 constexpr double kLog2Pi = 1.83787706640934548356;
 
+// N: compile-time bound on nx and ny (1, 2, 4, 8, 16): small models keep every array in registers
+template <int N>
 __global__ void __launch_bounds__(64) kalman_kernel(ssm_kalman_args A) {
+  constexpr int kKfMax = N;
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= A.B) return;
   const int nx = A.nx, ny = A.ny, S = A.S;
@@ -145,18 +148,29 @@ __global__ void __launch_bounds__(64) kalman_kernel(ssm_kalman_args A) {
 }  // namespace
 }  // namespace ssm
 
-extern "C" int ssm_kalman_max_dim(void) { return ssm::kKfMax; }
+extern "C" int ssm_kalman_max_dim(void) { return ssm::kKfMaxDim; }
 
 extern "C" int ssm_kalman_filter(const ssm_kalman_args* args, void* stream) {
   using namespace ssm;
-  if (!args || args->B < 0 || args->nx < 1 || args->ny < 0 || args->nx > kKfMax || args->ny > kKfMax ||
+  if (!args || args->B < 0 || args->nx < 1 || args->ny < 0 || args->nx > kKfMaxDim || args->ny > kKfMaxDim ||
       args->s0 < 0 || args->s1 < args->s0 || args->s1 > args->S)
     return SSM_ERR_INVALID_ARG;
   if (args->B == 0 || args->s1 == args->s0) return SSM_OK;
   if (!args->A || !args->b || !args->Q || !args->mu || !args->P || !args->mu_p || !args->P_p || !args->loglik ||
       !args->err || !args->mask || (args->ny > 0 && (!args->H || !args->c || !args->r_sd || !args->y)))
     return SSM_ERR_INVALID_ARG;
-  const int nt = 64;
-  kalman_kernel<<<(args->B + nt - 1) / nt, nt, 0, static_cast<cudaStream_t>(stream)>>>(*args);
+  const int nt = 64, n = args->nx > args->ny ? args->nx : args->ny;
+  const dim3 g((args->B + nt - 1) / nt);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n <= 1)
+    kalman_kernel<1><<<g, nt, 0, s>>>(*args);
+  else if (n <= 2)
+    kalman_kernel<2><<<g, nt, 0, s>>>(*args);
+  else if (n <= 4)
+    kalman_kernel<4><<<g, nt, 0, s>>>(*args);
+  else if (n <= 8)
+    kalman_kernel<8><<<g, nt, 0, s>>>(*args);
+  else
+    kalman_kernel<16><<<g, nt, 0, s>>>(*args);
   return cudaGetLastError() == cudaSuccess ? SSM_OK : SSM_ERR_CUDA;
 }

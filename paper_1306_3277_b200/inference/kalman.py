@@ -4,9 +4,10 @@ the reference's inference/kalman.py API (KalmanRun, kalman_filter) and the
 
 The forward recursions of B systems run in one `ssm_kalman_filter` launch
 (csrc/ssm_kalman.cu, one thread per system); the filtered and predicted
-moments of every grid step stay on the device.  `sample_trajectory` (one
-backward smoothing draw, kalman.py:98-114) reads one run's records back and
-draws on the host with the run's stream, in the reference's order.
+moments of every grid step stay on the device.  Backward smoothing draws
+(kalman.py:98-114) read the records of a batch back once and run on the host,
+vectorised over the batch's runs, with each run's stream in the reference's
+order.
 """
 
 from __future__ import annotations
@@ -60,6 +61,70 @@ def psd_cholesky_upper(S):
         U[i, i] = np.sqrt(pivot)
         U[i, i + 1 :] = (S[i, i + 1 :] - U[:i, i] @ U[:i, i + 1 :]) / U[i, i]
     return U
+
+
+def _psd_chol_batch(S):
+    """psd_cholesky_upper over a stack (B, n, n) (same pivot rule, per matrix)."""
+    S = np.asarray(S, dtype=float)
+    B, n, _ = S.shape
+    tol = PIVOT_RTOL * np.maximum(1.0, np.max(np.abs(np.diagonal(S, axis1=1, axis2=2)), axis=1))
+    big = np.sqrt(tol) * np.maximum(1.0, np.max(np.abs(S), axis=(1, 2)))
+    U = np.zeros_like(S)
+    for i in range(n):
+        pivot = S[:, i, i] - np.einsum("bk,bk->b", U[:, :i, i], U[:, :i, i])
+        rest = S[:, i, i + 1 :] - np.einsum("bk,bkj->bj", U[:, :i, i], U[:, :i, i + 1 :])
+        neg = pivot < -tol
+        zero = (~neg) & (pivot <= tol)
+        if np.any(neg) or np.any(zero[:, None] & (np.abs(rest) > big[:, None])):
+            raise CholeskyError(f"matrix is not positive semi-definite at pivot {i}", index=i)
+        d = np.where(zero, 0.0, np.sqrt(np.where(zero, 1.0, pivot)))
+        U[:, i, i] = d
+        U[:, i, i + 1 :] = np.where(zero[:, None], 0.0, rest / np.where(zero, 1.0, d)[:, None])
+    return U
+
+
+def _solve_upper_t_batch(U, v):
+    """U^-T v over a stack; v (B, n) or (B, n, m).  Zero pivots: pseudo-inverse."""
+    Ut = U.transpose(0, 2, 1)
+    vv = v[..., None] if v.ndim == 2 else v
+    if np.all(np.diagonal(U, axis1=1, axis2=2) != 0):
+        out = np.linalg.solve(Ut, vv)
+    else:
+        out = np.linalg.pinv(Ut) @ vv
+    return out[..., 0] if v.ndim == 2 else out
+
+
+def sample_kalman_trajectories(runs, rngs):
+    """KalmanRun.sample_trajectory for many runs (kalman.py:98-114): per run the
+    reference's draws in its order (step s first, then s-1 .. 0), the backward
+    recursion vectorised over runs of one batch at one position."""
+    out = [None] * len(runs)
+    groups = {}
+    for k, r in enumerate(runs):
+        groups.setdefault((id(r._batch), r.pos), []).append(k)
+    for (_, s), ks in groups.items():
+        b = runs[ks[0]]._batch
+        rows = torch.as_tensor([runs[k]._row for k in ks], device=b.device)
+        mu = b.mu.index_select(0, rows)[:, : s + 1].cpu().numpy()
+        P = b.P.index_select(0, rows)[:, : s + 1].cpu().numpy()
+        mu_p = b.mu_p.index_select(0, rows)[:, : s + 1].cpu().numpy()
+        P_p = b.P_p.index_select(0, rows)[:, : s + 1].cpu().numpy()
+        A = b.A.index_select(0, rows)[:, :s].cpu().numpy()
+        G, nx = len(ks), b.nx
+        z = np.stack([np.asarray(rngs[k].standard_normal((s + 1) * nx), dtype=float).reshape(s + 1, nx)
+                      for k in ks])  # row q = the draw for step s - q
+        tr = np.empty((G, s + 1, nx))
+        tr[:, s] = mu[:, s] + np.einsum("bji,bj->bi", _psd_chol_batch(P[:, s]), z[:, 0])
+        for i in range(s - 1, -1, -1):
+            Uh = _psd_chol_batch(P_p[:, i + 1])
+            C = P[:, i] @ A[:, i].transpose(0, 2, 1)
+            K = _solve_upper_t_batch(Uh, C.transpose(0, 2, 1)).transpose(0, 2, 1)  # C Uh^-1
+            omega = mu[:, i] + np.einsum("bij,bj->bi", K, _solve_upper_t_batch(Uh, tr[:, i + 1] - mu_p[:, i + 1]))
+            W = _psd_chol_batch(P[:, i] - K @ K.transpose(0, 2, 1))
+            tr[:, i] = omega + np.einsum("bji,bj->bi", W, z[:, s - i])
+        for q, k in enumerate(ks):
+            out[k] = tr[q]
+    return out
 
 
 def _solve_upper_t(U, v):
@@ -125,11 +190,19 @@ class KalmanRun:
 
     def __init__(self, system, grid, device=None, _batch=None, _row=0):
         self.grid = grid
-        self.system = system
+        self._system = system
         self._batch = _batch if _batch is not None else _KalmanBatch(system, grid, device)
         self._row = _row
         self.loglik = 0.0
         self.pos = 0
+
+    @property
+    def system(self):
+        """This run's LinearGaussianSystems row (materialised on first use)."""
+        if isinstance(self._system, tuple):
+            systems, k = self._system
+            self._system = systems.row(k)
+        return self._system
 
     def clone(self):
         b = self._batch
@@ -139,7 +212,7 @@ class KalmanRun:
         for f in ("A", "b", "Q", "H", "c", "r", "mu", "P", "mu_p", "P_p", "loglik", "err"):
             setattr(nb, f, getattr(b, f)[r : r + 1].clone())
         nb.B = 1
-        other = KalmanRun(self.system, self.grid, _batch=nb, _row=0)
+        other = KalmanRun(self._system, self.grid, _batch=nb, _row=0)
         other.loglik, other.pos = self.loglik, self.pos
         return other
 
@@ -159,6 +232,9 @@ class KalmanRun:
     def sample_trajectory(self, rng):
         """Backward smoothing sample x(t_{0:pos}) (kalman.py:98-114): the same
         draws in the same order, covariance-form algebra."""
+        return sample_kalman_trajectories([self], [rng])[0]
+
+    def _sample_trajectory_serial(self, rng):
         s = self.pos
         mu, P, mu_p, P_p = self._records()
         A = self._batch.A[self._row].cpu().numpy()
@@ -211,7 +287,7 @@ def advance_kalman_runs(runs, upto):
 def kalman_runs(systems: LinearGaussianSystems, grid, device=None):
     """B fresh runs sharing one device batch."""
     batch = _KalmanBatch(systems, grid, device)
-    return [KalmanRun(systems.row(k), grid, _batch=batch, _row=k) for k in range(systems.B)]
+    return [KalmanRun((systems, k), grid, _batch=batch, _row=k) for k in range(systems.B)]
 
 
 def kalman_filter(system, grid, rng, upto=None, device=None):

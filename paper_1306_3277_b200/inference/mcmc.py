@@ -117,10 +117,10 @@ class FilterRunner:
             return []
         runs = self.new_runs(thetas, init_states, rngs)
         if self.filter_kind == "kalman":
-            from .kalman import advance_kalman_runs
+            from .kalman import advance_kalman_runs, sample_kalman_trajectories
 
             advance_kalman_runs(runs, upto)
-            trajs = [r.sample_trajectory(g.child(2)) for r, g in zip(runs, rngs)]
+            trajs = sample_kalman_trajectories(runs, [g.child(2) for g in rngs])
             return [(r.loglik, t, r) for r, t in zip(runs, trajs)]
         advance_runs(runs, upto, [g.child(1) for g in rngs])
         trajs = sample_trajectories(runs, [g.child(2) for g in rngs])

@@ -27,7 +27,7 @@ import torch
 
 from .. import _lib
 from ..distributed import Shard, allgather_f64, exchange, plan_redistribution
-from ..errors import DegenerateEnsembleError
+from ..errors import DegenerateEnsembleError, UnsupportedModelError
 from ..models import resolve_model
 from .mcmc import MhChainState, _chain_log_prior, marginal_mh_steps
 from .particle import _dtype_info, advance_runs, sample_trajectories
@@ -79,6 +79,17 @@ def _advance_all(runner, particles, js, upto, run_rngs, init_rngs, traj_rngs):
         for j, r in zip(missing, runs):
             particles[j].run = r
     incr = {}
+    if runner.filter_kind == "kalman":  # device Kalman runs (kalman.py): exact increments, host backward draws
+        from .kalman import advance_kalman_runs, sample_kalman_trajectories
+
+        inc = advance_kalman_runs([particles[j].run for j in js], upto)
+        for j, v in zip(js, inc):
+            incr[j] = float(v)
+        if traj_rngs is not None and js:
+            trajs = sample_kalman_trajectories([particles[j].run for j in js], [traj_rngs[j] for j in js])
+            for j, t in zip(js, trajs):
+                particles[j].trajectory = t
+        return incr
     by_pos = {}
     for j in js:
         by_pos.setdefault(particles[j].run.pos, []).append(j)
@@ -212,6 +223,8 @@ def smc_sampler(ir, runner, n_theta, rng, theta_resampler="multinomial", nthread
     if n_theta < 2:
         raise ValueError("smc sampler needs n_theta >= 2")
     shard = shard or Shard.current()
+    if runner.filter_kind == "kalman" and shard.world > 1:
+        raise UnsupportedModelError("sharded SMC^2 moves particle-filter state; use the bootstrap filter")
     spec = resolve_model(ir)
     grid = runner.grid
     use_init = spec.has_proposal_initial

@@ -392,6 +392,11 @@ def gen_outer_loops():
     out["wk/mh/thetas"] = np.array([c.theta for c in chains])
     out["wk/mh/logliks"] = np.array([c.loglik for c in chains])
     out["wk/mh/accepted"] = np.array(acc)
+    from ssmkit.inference import smc_sampler
+
+    res = smc_sampler(ir, runner, 6, RngStream(25), theta_resampler="systematic")
+    out["wk/smc/thetas"], out["wk/smc/logliks"], out["wk/smc/log_v"] = res.thetas, res.logliks, res.log_v
+    out["wk/smc/trajectories"] = res.trajectories
     save("outer.npz", **out)
 
 
@@ -602,6 +607,11 @@ def gen_kalman():
     out["wk/mh/thetas"] = np.array([c.theta for c in chains])
     out["wk/mh/logliks"] = np.array([c.loglik for c in chains])
     out["wk/mh/accepted"] = np.array(acc)
+    from ssmkit.inference import smc_sampler
+
+    res = smc_sampler(ir, runner, 6, RngStream(25), theta_resampler="systematic")
+    out["wk/smc/thetas"], out["wk/smc/logliks"], out["wk/smc/log_v"] = res.thetas, res.logliks, res.log_v
+    out["wk/smc/trajectories"] = res.trajectories
     # LinOsc: coupled ode with 2 RK4 steps per sub-step, grid spacing 0.1 = 2 sub-steps, partial masks
     ir = load_test_model("LinOsc")
     import json

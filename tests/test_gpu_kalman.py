@@ -126,3 +126,27 @@ def test_particle_filter_unbiased_vs_kalman_linosc():
     m = np.log(np.mean(np.exp(lls - lls.max()))) + lls.max()
     se = lls.std(ddof=1) / np.sqrt(len(lls))
     assert abs(m - r.loglik) < 5 * se + 0.02, (m, r.loglik, se)
+
+
+def test_smc2_kalman_windkessel_matches_reference():
+    from paper_1306_3277_b200.inference import smc_sampler
+
+    g, grid, inputs = wk_case()
+    runner = FilterRunner(WINDKESSEL, grid, inputs=inputs, filter_kind="kalman")
+    res = smc_sampler(WINDKESSEL, runner, 6, RngStream(25), theta_resampler="systematic")
+    np.testing.assert_array_equal(res.thetas, g["wk/smc/thetas"])
+    np.testing.assert_allclose(res.logliks, g["wk/smc/logliks"], rtol=1e-12)
+    np.testing.assert_allclose(res.log_v, g["wk/smc/log_v"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(res.trajectories, g["wk/smc/trajectories"], rtol=1e-10)
+
+
+def test_batched_backward_sampling_equals_serial():
+    g, grid, inputs, desc = osc_case()
+    sys_ = extract_linear_gaussian(desc, g["osc/thetas"], grid.times, inputs)
+    runs = kalman_runs(sys_, grid)
+    advance_kalman_runs(runs, 17)
+    from paper_1306_3277_b200.inference.kalman import sample_kalman_trajectories
+
+    got = sample_kalman_trajectories(runs, [RngStream(70 + k) for k in range(len(runs))])
+    for k, r in enumerate(runs):
+        np.testing.assert_allclose(got[k], r._sample_trajectory_serial(RngStream(70 + k)), rtol=1e-11, atol=1e-13)

@@ -15,7 +15,8 @@ from paper_1306_3277_b200 import profiling  # noqa: E402
 
 
 def main(cfg):
-    fn = {"3": B.config3, "4": B.config4}[cfg]
+    fn = {"3": B.config3, "4": B.config4, "3d": lambda q: B.config3(q, "device"),
+          "4d": lambda q: B.config4(q, "device")}[cfg]
     fn(False)  # warm
     torch.cuda.synchronize()
     t0 = time.perf_counter()

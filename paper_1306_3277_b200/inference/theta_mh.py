@@ -114,7 +114,8 @@ class DeviceThetaChains:
             self._keys = None
         else:
             self._inj = None
-            self._keys = torch.as_tensor(device_keys(rngs).astype(np.int32).view(np.int32), device=self.device)
+            keys = np.ascontiguousarray(device_keys(rngs), dtype=np.uint32).view(np.int32)  # bit pattern kept
+            self._keys = torch.as_tensor(keys, device=self.device)
         self.err.zero_()
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().ssm_theta_propose(self._args(step), _lib.stream_ptr(stream)), "ssm_theta_propose")

@@ -34,25 +34,27 @@ __global__ void __launch_bounds__(64) kalman_kernel(ssm_kalman_args A) {
   double ll = A.loglik[f];
   for (int s = A.s0 + 1; s <= A.s1; ++s) {
     const size_t tab = static_cast<size_t>(f) * S + (s - 1);
-    const double* Am = A.A + tab * nx * nx;
-    const double* bv = A.b + tab * nx;
-    const double* Qm = A.Q + tab * nx * nx;
+    // the tables are read-only for the whole launch: the non-coherent path lets these
+    // loads issue ahead of the record stores below instead of behind them
+    const double* __restrict__ Am = A.A + tab * nx * nx;
+    const double* __restrict__ bv = A.b + tab * nx;
+    const double* __restrict__ Qm = A.Q + tab * nx * nx;
     // predict
     for (int i = 0; i < nx; ++i) {
-      double acc = bv[i];
-      for (int k = 0; k < nx; ++k) acc += Am[i * nx + k] * mu[k];
+      double acc = __ldg(&bv[i]);
+      for (int k = 0; k < nx; ++k) acc += __ldg(&Am[i * nx + k]) * mu[k];
       mh[i] = acc;
     }
     for (int i = 0; i < nx; ++i)  // T = A P
       for (int j = 0; j < nx; ++j) {
         double acc = 0.0;
-        for (int k = 0; k < nx; ++k) acc += Am[i * nx + k] * P[k * nx + j];
+        for (int k = 0; k < nx; ++k) acc += __ldg(&Am[i * nx + k]) * P[k * nx + j];
         T[i * nx + j] = acc;
       }
     for (int i = 0; i < nx; ++i)  // P^ = T A^T + Q, symmetric by construction
       for (int j = 0; j <= i; ++j) {
-        double acc = Qm[i * nx + j];
-        for (int k = 0; k < nx; ++k) acc += T[i * nx + k] * Am[j * nx + k];
+        double acc = __ldg(&Qm[i * nx + j]);
+        for (int k = 0; k < nx; ++k) acc += T[i * nx + k] * __ldg(&Am[j * nx + k]);
         Ph[i * nx + j] = acc;
         Ph[j * nx + i] = acc;
       }
@@ -66,19 +68,19 @@ __global__ void __launch_bounds__(64) kalman_kernel(ssm_kalman_args A) {
       for (int i = 0; i < nx; ++i) mu[i] = mh[i];
       for (int i = 0; i < nx * nx; ++i) P[i] = Ph[i];
     } else {
-      const double* Hm = A.H + tab * ny * nx;
-      const double* cv = A.c + tab * ny;
-      const double* rv = A.r_sd + tab * ny;
-      const double* yv = A.y + static_cast<size_t>(s - 1) * ny;
+      const double* __restrict__ Hm = A.H + tab * ny * nx;
+      const double* __restrict__ cv = A.c + tab * ny;
+      const double* __restrict__ rv = A.r_sd + tab * ny;
+      const double* __restrict__ yv = A.y + static_cast<size_t>(s - 1) * ny;
       // W <- H P^ (m x nx), e <- y - H mu^ - c
       for (int a = 0; a < m; ++a) {
-        const double* h = Hm + slot[a] * nx;
-        double nu = cv[slot[a]];
-        for (int k = 0; k < nx; ++k) nu += h[k] * mh[k];
-        e[a] = yv[slot[a]] - nu;
+        const double* __restrict__ h = Hm + slot[a] * nx;
+        double nu = __ldg(&cv[slot[a]]);
+        for (int k = 0; k < nx; ++k) nu += __ldg(&h[k]) * mh[k];
+        e[a] = __ldg(&yv[slot[a]]) - nu;
         for (int j = 0; j < nx; ++j) {
           double acc = 0.0;
-          for (int k = 0; k < nx; ++k) acc += h[k] * Ph[k * nx + j];
+          for (int k = 0; k < nx; ++k) acc += __ldg(&h[k]) * Ph[k * nx + j];
           W[a * nx + j] = acc;
         }
       }
@@ -86,9 +88,9 @@ __global__ void __launch_bounds__(64) kalman_kernel(ssm_kalman_args A) {
       bool bad = false;
       for (int a = 0; a < m; ++a)
         for (int bb = 0; bb <= a; ++bb) {
-          const double* h = Hm + slot[bb] * nx;
-          double acc = (a == bb) ? rv[slot[a]] * rv[slot[a]] : 0.0;
-          for (int k = 0; k < nx; ++k) acc += W[a * nx + k] * h[k];
+          const double* __restrict__ h = Hm + slot[bb] * nx;
+          double acc = (a == bb) ? __ldg(&rv[slot[a]]) * __ldg(&rv[slot[a]]) : 0.0;
+          for (int k = 0; k < nx; ++k) acc += W[a * nx + k] * __ldg(&h[k]);
           L[a * kKfMax + bb] = acc;
         }
       for (int j = 0; j < m; ++j) {

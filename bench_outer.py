@@ -184,6 +184,46 @@ def configk(quick):
             "pmmh_kalman_64_chains_ms_per_mh_step": ms_mh / 21, "pmmh_acceptance": int(np.sum(acc))}
 
 
+def configr(quick):
+    """Resample + gather microbench (SURVEY 8d kernel inputs): logw ~ N(0, sigma_w^2),
+    sigma_w in {0, 1, 10} (ESS from P to ~1), numpy default_rng(1234), states U(-1,3)^8,
+    f64, P = 2^24: ssm_resample_from_logw then ssm_gather, timed with CUDA events.
+    Algorithmic bytes B_R = 8 (read logw) + 4 (write ancestor) + 2*8*8 (gather) = 140 B."""
+    import torch
+
+    from paper_1306_3277_b200 import _lib
+
+    L = _lib.lib()
+    P = 1 << (20 if quick else 24)
+    dev = torch.device("cuda")
+    rs = np.random.default_rng(1234)
+    x = torch.as_tensor(rs.uniform(-1.0, 3.0, size=(8, P)), device=dev)
+    xo = torch.empty_like(x)
+    anc = torch.empty(P, dtype=torch.int32, device=dev)
+    ws = torch.empty(L.ssm_resample_workspace_bytes(1, P), dtype=torch.uint8, device=dev)
+    keys = torch.tensor([[12345, 678]], dtype=torch.int32, device=dev)
+    st = _lib.stream_ptr()
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak = float(json.load(open(pk)).get("hbm_gbs", 6552.3)) if os.path.exists(pk) else 6552.3
+    res = {}
+    for sw in (0.0, 1.0, 10.0):
+        a = torch.as_tensor(rs.normal(0.0, sw, size=P) if sw > 0 else np.zeros(P), device=dev)
+        shift = torch.logsumexp(a, 0).reshape(1)  # normalised weights (the CDF's fixed point needs sum 1)
+        for name, scheme in (("systematic", 2), ("stratified", 1), ("multinomial_sorted", 3)):
+            def step():
+                _lib.check(L.ssm_resample_from_logw(1, P, _lib.SSM_F64, scheme, _lib.ptr(a), _lib.ptr(shift), None,
+                                                    None, _lib.ptr(keys), 1, _lib.ptr(anc), _lib.ptr(ws), st), "rs")
+                _lib.check(L.ssm_gather(_lib.SSM_F64, 1, 8, P, _lib.ptr(x), _lib.ptr(anc), _lib.ptr(xo), st), "g")
+
+            ms, _ = timed(step, warmup=2, reps=10)
+            gbs = 140.0 * P / (ms / 1e3) / 1e9
+            uniq = int(torch.unique(anc).numel())
+            res[f"sigma_w={sw:g} {name}"] = {"ms": ms, "GB/s": gbs, "frac_of_measured_peak": gbs / peak,
+                                             "unique_ancestors": uniq / P}
+    return {"config": f"r: resample+gather microbench, P=2^{int(math.log2(P))}, f64, nx=8 (B_R = 140 B/particle)",
+            "unit": "GB/s (algorithmic)", "results": res}
+
+
 def config5(quick):
     from paper_1306_3277_b200 import LORENZ96, RngStream
     from paper_1306_3277_b200.inference import build_filter_grid, particle_filter
@@ -243,7 +283,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
     fns = {"1": config1, "3": config3, "4": config4, "5": config5, "g": configg,
-           "k": configk, "3d": lambda q: config3(q, "device"), "4d": lambda q: config4(q, "device")}
+           "k": configk, "r": configr, "3d": lambda q: config3(q, "device"), "4d": lambda q: config4(q, "device")}
     for c in args.configs.split(","):
         t0 = time.time()
         r = fns[c](args.quick)

@@ -248,6 +248,8 @@ int ssm_resample_search(int B, int P_in, int P_out, int scheme, int cum_kind, co
 
 /* K4+K5 for the filter (particle.py:96-105): ancestors straight from the
  * unnormalised log-weights a (w = exp(a - shift[b]), shift NULL -> fs[b].incr).
+ * shift must be the log-sum-exp of a[b] (the weights sum to 1): the exact
+ * fixed-point CDF has 2^52 units per unit of weight and no headroom beyond 1.
  * systematic / stratified: exact fixed-point reduce-then-scan (tile sums ->
  * tile prefix -> offspring bounds + partition) -> expand, 4 launches, no
  * look-back and no searches; multinomial: look-back scan + binary search. */

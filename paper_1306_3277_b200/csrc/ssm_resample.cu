@@ -1151,6 +1151,24 @@ spacing_merge_kernel(int P, const uint64_t* __restrict__ C, const uint64_t* __re
   }
   __syncthreads();
   const int jlo = s_j[0], jhi = s_j[1];
+  if (jhi - jlo > 8 * kScanTile) {
+    // degenerate weights: the tile's outputs span a long stretch of (near-)zero-weight
+    // particles; one binary search per output instead of a walk over every particle.
+    // searchsorted(cum, U, 'right') within [jlo, jhi] (jhi already clipped to P - 1)
+    for (int e = threadIdx.x; e < n_out; e += kThreads) {
+      const double u = sU[e];
+      int lo = jlo, hi = jhi;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cum_at(mid) <= u)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      ab[k0 + e] = lo;
+    }
+    return;
+  }
   // local count of U < cum_j (the last particle takes every remaining output: clip rule)
   auto cnt_lt = [&](int j) -> int {
     if (j < jlo) return 0;

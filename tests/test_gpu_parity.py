@@ -582,8 +582,8 @@ def _philox4x32_10(ctr, k0, k1):
     return c
 
 
-@pytest.mark.parametrize("P", [1000, 2048, 5000, 1 << 16])
-@pytest.mark.parametrize("pattern", ["lognormal", "one", "few"])
+@pytest.mark.parametrize("P", [1000, 2048, 5000, 1 << 16, 1 << 18])
+@pytest.mark.parametrize("pattern", ["lognormal", "one", "few", "sigma10"])
 def test_sorted_multinomial_matches_spacings_oracle(P, pattern):
     """SSM_MULTINOMIAL_SORTED (device-noise filter path): U_(k) = S_k / S_{P+1}
     from the device's exponential spacings, ancestors = searchsorted(cum, U, 'right')
@@ -595,6 +595,7 @@ def test_sorted_multinomial_matches_spacings_oracle(P, pattern):
 
     L = _lib.lib()
     pats = _heavy_patterns(P)
+    pats["sigma10"] = np.random.default_rng(1234).normal(0.0, 10.0, size=P)  # ESS ~ 1
     a_np = np.stack([pats[pattern], pats["lognormal"]])
     a = torch.from_numpy(a_np).cuda()
     shift = torch.from_numpy(logsumexp(a_np, axis=1)).cuda()

@@ -70,6 +70,10 @@ typedef enum {
  * resampling.py:18-24 */
 #define SSM_FLAG_BAD_WEIGHT 1u  /* negative or non-finite weight -> ValueError */
 #define SSM_FLAG_ZERO_TOTAL 2u  /* all weights zero -> DegenerateEnsembleError */
+/* (is_log = 1, flags != NULL) the normalisation precondition sum exp(a - shift) = 1
+ * is violated: a weight above 1 + 2^-20 or a fixed-point prefix reaching 2^62
+ * (the look-back flag bits).  The CDF is then not meaningful -> ValueError. */
+#define SSM_FLAG_UNNORMALISED 4u
 
 /* One transition sub-step, built on the host from substep_schedule
  * (simulate.py:28-38) and the RK4 step split (simulate.py:85-87). */
@@ -204,6 +208,15 @@ int ssm_gen_init_particles(const void* handle, int dtype, int B, int P, int p_of
 int ssm_init_particles(int model, int dtype, int B, int P, int p_offset, const uint32_t* keys,
                        void* x_out, void* stream);
 
+/* Validation export of the device noise: the float32 standard normals the
+ * fused kernels draw for particles [p_offset, p_offset + P) at grid step `step`,
+ * sub-step `sub` (Philox4x32-10 + float32 Box-Muller, ssm_common.cuh).  L96:
+ * out [B][8][P] (slot-major, the draws of Lorenz96.bi:25 before the sqrt(d)
+ * scaling); windkessel: out [B][P].  Lets the tests feed the oracle the exact
+ * draws the benchmark kernel consumed and test the generator's law. */
+int ssm_device_normals(int model, int B, int P, int p_offset, const uint32_t* keys, int step, int sub,
+                       float* out, void* stream);
+
 /* Cross-rank finalize of a weighted step for a filter sharded over W ranks
  * (C1): combines the W per-rank partials (m, c, t, s2) in rank order and
  * performs the finalize of ssm_propagate_weight (loglik, degenerate flag, ESS
@@ -219,7 +232,8 @@ int ssm_lse_combine(int W, int B, const double* parts, ssm_filter_state* fs, dou
  * unnormalised log-weights and the last LSE, particle.py:101, 133); with
  * shift == NULL the shift is fs[b].incr.
  * is_log = 0: w = a (float64 raw weights); validated as in resampling.py:18-24
- * with failures OR-ed into flags[b] (SSM_FLAG_*).
+ * with failures OR-ed into flags[b] (SSM_FLAG_*).  flags is required for
+ * is_log = 0 and optional for is_log = 1 (SSM_FLAG_UNNORMALISED).
  * fs (nullable): filters with fs[b].resample_now == 0 are skipped. */
 size_t ssm_scan_workspace_bytes(int B, int P);
 int ssm_weights_scan(int B, int P, int dtype, const void* a, int is_log, const double* shift,

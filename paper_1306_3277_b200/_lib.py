@@ -20,7 +20,7 @@ SSM_F32, SSM_F64 = 0, 1
 SSM_MODEL_LORENZ96, SSM_MODEL_WINDKESSEL, SSM_MODEL_GENERIC = 0, 1, 2
 SCHEME_IDS = {"multinomial": 0, "stratified": 1, "systematic": 2}
 SSM_MULTINOMIAL_SORTED = 3  # device-noise multinomial, ancestors in ascending order
-SSM_FLAG_BAD_WEIGHT, SSM_FLAG_ZERO_TOTAL = 1, 2
+SSM_FLAG_BAD_WEIGHT, SSM_FLAG_ZERO_TOTAL, SSM_FLAG_UNNORMALISED = 1, 2, 4
 INT32_MAX = 2**31 - 1
 
 
@@ -201,6 +201,7 @@ SIGNATURES = {
     "ssm_pw_workspace_bytes": (_sz, [_i, _i]),
     "ssm_propagate_weight": (_i, [C.POINTER(PwArgs), _vp]),
     "ssm_init_particles": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp]),
+    "ssm_device_normals": (_i, [_i, _i, _i, _i, _vp, _i, _i, _vp, _vp]),
     "ssm_lse_combine": (_i, [_i, _i, _vp, _vp, _d, _d, _i, _vp]),
     "ssm_scan_workspace_bytes": (_sz, [_i, _i]),
     "ssm_weights_scan": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -244,6 +245,7 @@ SIGNATURES = {
 LAUNCHING = {
     "ssm_propagate_weight": 1,
     "ssm_init_particles": 1,
+    "ssm_device_normals": 1,
     "ssm_gen_init_particles": 1,
     "ssm_lse_combine": 1,
     "ssm_weights_scan": 1,

@@ -443,6 +443,40 @@ extern "C" int ssm_init_particles(int model, int dtype, int B, int P, int p_offs
   return SSM_OK;
 }
 
+// ----------------------------- device-noise export -------------------------
+
+namespace ssm {
+__global__ void __launch_bounds__(kThreads) normals_kernel(int model, int P, int p_offset, const uint32_t* keys,
+                                                           int step, int sub, float* out) {
+  const int b = blockIdx.y;
+  const uint32_t k0 = keys[2 * b], k1 = keys[2 * b + 1];
+  const int nx = model == SSM_MODEL_LORENZ96 ? 8 : 1;
+  float* ob = out + static_cast<size_t>(b) * nx * P;
+  for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads) {
+    const uint32_t pg = static_cast<uint32_t>(p + p_offset);
+    if (model == SSM_MODEL_LORENZ96) {
+      float z[8];
+      normals8f(k0, k1, pg, static_cast<uint32_t>(step), static_cast<uint32_t>(sub), z);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) ob[static_cast<size_t>(n) * P + p] = z[n];
+    } else {
+      ob[p] = normal1<float>(k0, k1, pg, static_cast<uint32_t>(step), static_cast<uint32_t>(sub));
+    }
+  }
+}
+}  // namespace ssm
+
+extern "C" int ssm_device_normals(int model, int B, int P, int p_offset, const uint32_t* keys, int step, int sub,
+                                  float* out, void* stream) {
+  if (B <= 0 || P <= 0 || B > 65535 || !keys || !out || sub < 0) return SSM_ERR_INVALID_ARG;
+  if (model != SSM_MODEL_LORENZ96 && model != SSM_MODEL_WINDKESSEL) return SSM_ERR_UNSUPPORTED;
+  const dim3 grid(pw_grid_x(P), B);
+  ssm::normals_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(model, P, p_offset, keys, step, sub,
+                                                                               out);
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
 // ----------------------------- C1: cross-rank finalize ----------------------
 
 namespace ssm {

@@ -120,7 +120,8 @@ raw_total_kernel(int P, const double* w, double* partial, uint32_t* done, double
 template <typename T, bool IS_LOG>
 __global__ void __launch_bounds__(kThreads)
 scan_kernel(int B, int P, const T* __restrict__ a, const double* __restrict__ shift,
-            const ssm_filter_state* __restrict__ fs, uint64_t* __restrict__ C, ScanWs ws) {
+            const ssm_filter_state* __restrict__ fs, uint64_t* __restrict__ C, ScanWs ws,
+            uint32_t* __restrict__ flags = nullptr) {
   __shared__ uint64_t sm[kScanTile + kScanTile / 8];  // padded: e -> e + e/8
   __shared__ uint64_t warp_tot[kThreads / 32];
   __shared__ uint64_t s_excl;
@@ -140,6 +141,7 @@ scan_kernel(int B, int P, const T* __restrict__ a, const double* __restrict__ sh
   const double total = IS_LOG ? 1.0 : ws.scale[b];
 
   // coalesced load -> fixed point -> padded smem
+  bool over = false;  // normalisation precondition violated (is_log): reported, not wrapped
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     const int e = i * kThreads + threadIdx.x;
@@ -152,8 +154,12 @@ scan_kernel(int B, int P, const T* __restrict__ a, const double* __restrict__ sh
         w = static_cast<double>(a[off + e]) / total;
       }
       q = (w >= 0.0 && w <= 4.0) ? __double2ull_rn(w * kFix) : 0ull;
+      if (IS_LOG && w > 1.0 + 0x1p-20) over = true;
     }
     sm[e + (e >> 3)] = q;
+  }
+  if (IS_LOG && flags && __syncthreads_or(over)) {
+    if (threadIdx.x == 0) atomicOr(&flags[b], SSM_FLAG_UNNORMALISED);
   }
   __syncthreads();
   // thread-sequential 8 items
@@ -189,9 +195,9 @@ scan_kernel(int B, int P, const T* __restrict__ a, const double* __restrict__ sh
   if (warp == 0) {
     uint64_t excl = 0;
     if (j == 0) {
-      if (lane == 0) st_status(&status[0], kFlagPrefix | block_tot);
+      if (lane == 0) st_status(&status[0], kFlagPrefix | (block_tot & kValueMask));
     } else {
-      if (lane == 0) st_status(&status[j], kFlagAgg | block_tot);
+      if (lane == 0) st_status(&status[j], kFlagAgg | (block_tot & kValueMask));
       int look = j - 1;
       while (true) {
         const int idx = look - lane;
@@ -210,8 +216,10 @@ scan_kernel(int B, int P, const T* __restrict__ a, const double* __restrict__ sh
         if (first >= 0) break;
         look -= 32;
       }
-      if (lane == 0) st_status(&status[j], kFlagPrefix | (excl + block_tot));
+      if (lane == 0) st_status(&status[j], kFlagPrefix | ((excl + block_tot) & kValueMask));
     }
+    // a prefix at or above 2^62 would spill into the flag bits: report it
+    if (lane == 0 && flags && excl + block_tot > kValueMask) atomicOr(&flags[b], SSM_FLAG_UNNORMALISED);
     if (lane == 0) s_excl = excl;
   }
   __syncthreads();
@@ -1507,13 +1515,13 @@ extern "C" int ssm_weights_scan(int B, int P, int dtype, const void* a, int is_l
                                             ws.scale, flags);
     SSM_CHECK_LAUNCH();
     scan_kernel<double, false><<<B * tiles, kThreads, 0, s>>>(B, P, static_cast<const double*>(a),
-                                                             nullptr, fs, C, ws);
+                                                             nullptr, fs, C, ws, flags);
   } else if (dtype == SSM_F64) {
     scan_kernel<double, true><<<B * tiles, kThreads, 0, s>>>(B, P, static_cast<const double*>(a),
-                                                            shift, fs, C, ws);
+                                                            shift, fs, C, ws, flags);
   } else if (dtype == SSM_F32) {
     scan_kernel<float, true><<<B * tiles, kThreads, 0, s>>>(B, P, static_cast<const float*>(a),
-                                                           shift, fs, C, ws);
+                                                           shift, fs, C, ws, flags);
   } else {
     return SSM_ERR_INVALID_ARG;
   }

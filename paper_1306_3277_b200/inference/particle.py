@@ -639,12 +639,20 @@ def advance_runs(runs, upto, rngs):
     ntile = (P + 31) // 32  # one tile record per warp tile
     cdf_local = tile_rec = None
     if tiles_ok:
-        if all(r._cdf is not None for r in runs):  # resume: fresh copies, clones sharing the views stay intact
+        have = [r._cdf is not None for r in runs]
+        if all(have):  # resume: fresh copies, clones sharing the views stay intact
             cdf_local = torch.stack([r._cdf for r in runs])
             tile_rec = torch.stack([r._trec for r in runs])
         else:
             cdf_local = torch.empty((B, P), dtype=torch.int64, device=dev)
             tile_rec = torch.empty((B, ntile, 2), dtype=torch.float64, device=dev)
+            for b, r in enumerate(runs):
+                if have[b]:  # mixed batch: keep every carried CDF
+                    cdf_local[b].copy_(r._cdf)
+                    tile_rec[b].copy_(r._trec)
+                elif not r.weights_uniform:
+                    # the next step resamples from this run's tile CDF: it must travel with the run
+                    raise RuntimeError("weighted run without its tile CDF (cdf_local / tile_rec) cannot resume")
     ess_rel = -1.0 if r0.ess_rel is None else float(r0.ess_rel)
     log_w0 = float(-np.log(P))
     obs_log_sd = float(np.log(spec.obs_sd))
@@ -844,7 +852,9 @@ def sample_trajectories(runs, rngs):
         _lib.check(L.ssm_pick_from_tiles(B, P, _lib.ptr(cdf), _lib.ptr(trec), _lib.ptr(fs_rows), _lib.ptr(u),
                                          _lib.ptr(j), _lib.ptr(ws), stream), "ssm_pick_from_tiles")
         return _trajectories_from(L, runs, j, S, B, P, nx, dev, stream)
-    # final log-weights (uniform -> zeros with shift 0)
+    # final log-weights (uniform -> zeros with shift log P, so the scan's
+    # precondition sum(exp(a - shift)) = 1 holds: w_j = 1/P as the reference's
+    # exp(logw) with logw = -log P, particle.py:139)
     a_rows, shifts = [], []
     for r in runs:
         if r.weights_uniform or r._a is None:
@@ -854,22 +864,27 @@ def sample_trajectories(runs, rngs):
             a_rows.append(r._a)
             shifts.append(r._fs)
     a = _stack_rows(a_rows)
+    log_p = math.log(P)
     if all(f is None for f in shifts):
-        shift = torch.zeros(B, dtype=torch.float64, device=dev)
-    else:  # ssm_filter_state.incr (bytes 8..16) of weighted runs, 0 for uniform ones
+        shift = torch.full((B,), log_p, dtype=torch.float64, device=dev)
+    else:  # ssm_filter_state.incr (bytes 8..16) of weighted runs, log P for uniform ones
         fs_rows = _stack_rows([r._fs for r in runs]).contiguous()
         incr = fs_rows.view(torch.float64)[:, 1]
         weighted = torch.tensor([f is not None for f in shifts], device=dev)
-        shift = torch.where(weighted, incr, torch.zeros_like(incr))
+        shift = torch.where(weighted, incr, torch.full_like(incr, log_p))
     scan_ws = torch.empty(L.ssm_scan_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     cum = torch.empty((B, P), dtype=torch.int64, device=dev)
+    flags = torch.zeros(B, dtype=torch.int32, device=dev)
     _lib.check(L.ssm_weights_scan(B, P, r0.dtype_id, _lib.ptr(a), 1, _lib.ptr(shift), None, _lib.ptr(cum),
-                                  None, _lib.ptr(scan_ws), stream), "ssm_weights_scan")
+                                  _lib.ptr(flags), _lib.ptr(scan_ws), stream), "ssm_weights_scan")
     u = torch.from_numpy(first_uniforms(rngs, 1)).to(dev)  # each stream's uniform(size=1)
     j = torch.empty((B, 1), dtype=torch.int32, device=dev)
     _lib.check(L.ssm_resample_search(B, P, 1, _lib.SCHEME_IDS["multinomial"], 1, _lib.ptr(cum), _lib.ptr(u),
                                      None, 0, None, _lib.ptr(j), None, stream), "ssm_resample_search")
-    return _trajectories_from(L, runs, j, S, B, P, nx, dev, stream)
+    out = _trajectories_from(L, runs, j, S, B, P, nx, dev, stream)
+    if int(flags.max().item()) & _lib.SSM_FLAG_UNNORMALISED:  # after the read-back: no extra sync
+        raise ValueError("final weights violate the CDF normalisation precondition (ssm_weights_scan)")
+    return out
 
 
 def _trajectories_from(L, runs, j, S, B, P, nx, dev, stream):

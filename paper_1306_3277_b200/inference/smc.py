@@ -105,71 +105,115 @@ def _advance_all(runner, particles, js, upto, run_rngs, init_rngs, traj_rngs):
 
 
 # ---------------------------------------------------------------- C3 payloads
+#
+# A theta-particle travels as one float64 host vector (theta, prior, loglik,
+# trajectory, x0, run position / weighting state and, for history-free runs,
+# the per-step Philox keys) plus its filter's device tensors:
+#   keep_history=True : positions x_0..x_pos [pos+1, nx, P], ancestors [pos, P]
+#   keep_history=False: current positions [nx, P] and ancestors [pos, P] only
+#                       (the trajectory replay regenerates the line,
+#                       ssm_replay_path) -- ~10x less than the stacked history
+# then the unnormalised log-weights, the 64-byte filter state and, whenever the
+# run carries the fused kernel's tile CDF (systematic / stratified and the
+# device-noise sorted multinomial), cdf_local and the warp-tile records.
 
 
-def _payload_specs(spec, runner, have_run, pos, traj_len, P, tdtype):
-    n_host = spec.n_param + 2 + (traj_len * spec.nx) + (spec.nx if spec.has_proposal_initial else 0) + 3
-    specs = [((n_host,), torch.float64)]
-    if have_run:
-        specs += [((pos + 1, spec.nx, P), tdtype), ((max(pos, 1), P), torch.int32), ((P,), tdtype),
-                  ((64,), torch.uint8)]
-        if runner.resampler in ("systematic", "stratified"):
+@dataclass(frozen=True)
+class _Layout:
+    have_run: bool
+    traj_len: int
+    pos: int
+    has_a: bool
+    has_tiles: bool
+    keep_history: bool
+
+
+def _host_len(spec, L):
+    n = spec.n_param + 2 + L.traj_len * spec.nx + (spec.nx if spec.has_proposal_initial else 0) + 3
+    if L.have_run and not L.keep_history:
+        n += 2 * (L.pos + 1)  # Philox key (2 x uint32, exact in float64) per grid index
+    return n
+
+
+def _payload_specs(spec, L, P, tdtype):
+    specs = [((_host_len(spec, L),), torch.float64)]
+    if L.have_run:
+        xs = (L.pos + 1, spec.nx, P) if L.keep_history else (spec.nx, P)
+        specs += [(xs, tdtype), ((max(L.pos, 1), P), torch.int32), ((P,), tdtype), ((64,), torch.uint8)]
+        if L.has_tiles:
             specs += [((P,), torch.int64), (((P + 31) // 32, 2), torch.float64)]
     return specs
 
 
-def _pack(spec, runner, p, traj_len):
+def _pack(spec, L, p):
     host = [p.theta, [p.log_prior, p.loglik]]
-    host.append(p.trajectory.reshape(-1) if traj_len else [])
+    host.append(p.trajectory.reshape(-1) if L.traj_len else [])
     if spec.has_proposal_initial:
         host.append(p.init_state)
     r = p.run
     host.append([float(r.pos) if r else 0.0, float(r.weights_uniform) if r else 1.0,
                  float(r._maybe_nonuniform) if r else 0.0])
+    if r is not None and not L.keep_history:
+        host.append(np.asarray(r._keys, dtype=np.uint32).reshape(-1).astype(np.float64))
     out = [torch.from_numpy(np.concatenate([np.asarray(h, dtype=np.float64).reshape(-1) for h in host]))]
     if r is not None:
         P = r.n_particles
-        hx = torch.stack([h[0] for h in r.history])
         ar = torch.arange(P, dtype=torch.int32, device=r.device)
-        ha = torch.stack([h[1] if h[1] is not None else ar for h in r.history[1:]]) if r.pos > 0 else ar[None]
+        if L.keep_history:
+            hist = r.history
+            xs = torch.stack([h[0] for h in hist])
+            ancs = [h[1] for h in hist[1:]]
+        else:
+            xs = r._x
+            ancs = [ab[b] if ab is not None else None for _, ab, b in r._hist[1:]]
+        ha = torch.stack([a if a is not None else ar for a in ancs]) if r.pos > 0 else ar[None]
         a = r._a if r._a is not None else torch.zeros(P, dtype=r.tdtype, device=r.device)
-        out += [hx, ha, a, r._fs.contiguous()]
-        if runner.resampler in ("systematic", "stratified"):
+        out += [xs, ha, a, r._fs.contiguous()]
+        if L.has_tiles:
             out += [r._cdf if r._cdf is not None else torch.zeros(P, dtype=torch.int64, device=r.device),
                     r._trec if r._trec is not None else torch.zeros(((P + 31) // 32, 2), dtype=torch.float64,
                                                                     device=r.device)]
     return out
 
 
-def _unpack(spec, runner, tensors, traj_len, has_a):
+def _unpack(spec, runner, tensors, L):
     host = tensors[0].cpu().numpy()
     k = 0
     theta = host[k : k + spec.n_param].copy()
     k += spec.n_param
     log_prior, loglik = float(host[k]), float(host[k + 1])
     k += 2
-    traj = host[k : k + traj_len * spec.nx].reshape(traj_len, spec.nx).copy() if traj_len else None
-    k += traj_len * spec.nx
+    traj = host[k : k + L.traj_len * spec.nx].reshape(L.traj_len, spec.nx).copy() if L.traj_len else None
+    k += L.traj_len * spec.nx
     init = None
     if spec.has_proposal_initial:
         init = host[k : k + spec.nx].copy()
         k += spec.nx
     pos, uniform, maybe = int(host[k]), bool(host[k + 1]), bool(host[k + 2])
+    k += 3
     p = ThetaParticle(theta=theta, log_prior=log_prior, loglik=loglik, trajectory=traj, init_state=init)
     if len(tensors) > 1:
         run = runner._make(theta, init)
         dev = run.device
-        hx = tensors[1].to(dev)
+        xs = tensors[1].to(dev)
         ha = tensors[2].to(dev)
-        run.history = [(hx[0], None)] + [(hx[i], ha[i - 1]) for i in range(1, pos + 1)]
-        run._hx = [h[0].data_ptr() for h in run.history]
-        run._ha = [0] + [h[1].data_ptr() for h in run.history[1:]]
-        run._x = hx[pos]
-        run._a = tensors[3].to(dev) if has_a else None
+        if L.keep_history:
+            run.history = [(xs[0], None)] + [(xs[i], ha[i - 1]) for i in range(1, pos + 1)]
+            run._hx = [h[0].data_ptr() for h in run.history]
+            run._x = xs[pos]
+        else:
+            keys = host[k : k + 2 * (pos + 1)].astype(np.uint32).reshape(pos + 1, 2)
+            run._keys = [keys[i].copy() for i in range(pos + 1)]
+            ha_b = ha.unsqueeze(0)
+            run._hist = [(None, None, 0)] + [(None, ha_b[:, i - 1], 0) for i in range(1, pos + 1)]
+            run._hx = [0] * (pos + 1)
+            run._x = xs
+        run._ha = [0] + [ha[i - 1].data_ptr() for i in range(1, pos + 1)]
+        run._a = tensors[3].to(dev) if L.has_a else None
         run._fs = tensors[4].to(dev)
-        if len(tensors) > 5:
-            run._cdf = tensors[5].to(dev) if has_a else None
-            run._trec = tensors[6].to(dev) if has_a else None
+        if L.has_tiles:
+            run._cdf = tensors[5].to(dev)
+            run._trec = tensors[6].to(dev)
         run.pos, run.loglik, run.weights_uniform, run._maybe_nonuniform = pos, loglik, uniform, maybe
         fsv = run._fs.cpu().numpy().view(_lib.FILTER_STATE_DTYPE)[0]
         run.loglik = float(fsv["loglik"])
@@ -184,18 +228,18 @@ def _redistribute(spec, runner, particles, anc, n, shard, lo):
     probe = particles[0] if particles else None
     have_run = probe is not None and probe.run is not None
     traj_len = 0 if probe is None or probe.trajectory is None else probe.trajectory.shape[0]
-    # every rank holds particles in the same state, but a rank may own none: share the shape info
-    info = allgather_f64(np.array([float(have_run), float(traj_len),
-                                   float(probe.run.pos) if have_run else -1.0,
-                                   float(probe.run._a is not None) if have_run else 0.0]),
-                         shard).reshape(shard.world, 4)
-    ref = info[np.argmax(info[:, 2])] if shard.world > 1 else info.reshape(4)
-    have_run, traj_len, pos, has_a = bool(ref[0]), int(ref[1]), int(ref[2]), bool(ref[3])
-    sends = {peer: [t for a in srcs for t in _pack(spec, runner, local_src[a], traj_len)]
-             for peer, srcs in plan.sends.items()}
+    # every rank holds particles in the same state, but a rank may own none: share the layout
+    r = probe.run if have_run else None
+    info = allgather_f64(np.array([float(have_run), float(traj_len), float(r.pos) if have_run else -1.0,
+                                   float(r._a is not None) if have_run else 0.0,
+                                   float(r._cdf is not None) if have_run else 0.0,
+                                   float(r.keep_history) if have_run else 1.0]), shard).reshape(shard.world, 6)
+    ref = info[np.argmax(info[:, 2])]
+    L = _Layout(bool(ref[0]), int(ref[1]), int(ref[2]), bool(ref[3]), bool(ref[4]), bool(ref[5]))
+    sends = {peer: [t for a in srcs for t in _pack(spec, L, local_src[a])] for peer, srcs in plan.sends.items()}
     P = runner.n_particles
     _, tdtype, _ = _dtype_info(runner.device_opts.get("dtype", "float64"))
-    one = _payload_specs(spec, runner, have_run, pos, traj_len, P, tdtype)
+    one = _payload_specs(spec, L, P, tdtype)
     recv_specs = {peer: one * len(dsts) for peer, dsts in plan.recvs.items()}
     got = exchange(sends, recv_specs, shard)
     new = {}
@@ -205,7 +249,7 @@ def _redistribute(spec, runner, particles, anc, n, shard, lo):
     for peer, dsts in plan.recvs.items():
         ts = got[peer]
         for q, j in enumerate(dsts):
-            new[j] = _unpack(spec, runner, ts[q * per : (q + 1) * per], traj_len, has_a)
+            new[j] = _unpack(spec, runner, ts[q * per : (q + 1) * per], L)
     hi = lo + len(particles)
     return [new[j] for j in range(lo, hi)]
 

@@ -88,7 +88,9 @@ def workload_config(P, T, dtype, resampler="systematic"):
         "particles": P,
         "grid_steps": T,
         "resampler": resampler,
-        "noise": "device Philox4x32-10",
+        "noise": ("device Philox4x32-10 counters + float32 Box-Muller (MUFU lg2/sqrt/sincos, 32-bit radius "
+                  "uniform, 24-bit angle: |z| <= 6.77 sigma), widened to the filter precision; validated in law "
+                  "against the reference in tests/test_gpu_statistics.py"),
         "global_batch": P,
         "seq_len": T,
         "parallelism": "replicas",
@@ -318,11 +320,17 @@ def run_reference(args):
     value = cores * P * T / (ms / 1e3)
     sample = (f"{cores} processes x oracle port (numpy restatement of ssmkit particle_filter), L96, "
               f"P=2^{int(math.log2(P))} each, T={T} steps, systematic, float64, {cores} cores of {cpu_model()}")
+    # the workload is ours (same metric, model, data recipe, scheme, precision); each timed step is a
+    # bounded SAMPLE of it, stated here: `cores` independent filters of P particles over the first T
+    # grid steps (the CPU filter's particle-updates/s is flat in P and T: SURVEY 8d)
+    cfg = dict(workload_config(P_BENCH, T_BENCH, "float64"), noise="numpy Philox4x64 + ziggurat (host, oracle port)",
+               sample=f"{cores} processes x P=2^{int(math.log2(P))} particles x T={T} grid steps per timed step",
+               sample_particles=P, sample_grid_steps=T, sample_processes=cores, parallelism=f"{cores} CPU processes")
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(P_BENCH, T_BENCH, "float64"),
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -446,10 +454,11 @@ def main():
             "peak_kind": peak_kind,
             "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None,
-            # ncu DRAM bytes of one launch, only when the profiled launch has this run's size
-            "traffic": (traffic.get("bytes_per_launch") if traffic and pw and abs(
-                traffic.get("algorithmic_bytes_per_launch", 0) - pw["bytes"] / max(pw["launches"], 1)) < 1e6 * 64
-                else None),
+            # ncu DRAM bytes of one launch (profiles/pw_traffic.json, captured with `source` below), only
+            # when the profiled launch has this run's size
+            "traffic": (traffic.get("bytes_per_launch") if traffic and pw and traffic.get("particles") == P
+                        else None),
+            "traffic_source": (traffic.get("source") if traffic else None),
             "algorithmic_bytes_per_particle": pw["bytes"] / max(pw["launches"], 1) / P if pw else None,
         },
         "kernels": kern,

@@ -133,7 +133,8 @@ typedef struct ssm_pw_args {
   void* x_out;          /* [B][nx][P] positions at grid index i */
   const int32_t* anc;   /* [B][P] ancestors for step i (used iff fs.resample_now) or NULL */
   const void* a_prev;   /* [B][P] unnormalised log-weights of the last weighted step, or NULL */
-  void* a_out;          /* [B][P] unnormalised log-weights logw + g (iff has_obs) */
+  void* a_out;          /* [B][P] unnormalised log-weights logw + g (iff has_obs; may be NULL when
+                           cdf_local is set and the next step resamples from the tile records) */
   const double* theta;  /* [B][4] derived per-filter constants */
   const ssm_substep* subs; /* [n_sub] */
   const void* noise;    /* injected noise-variable values [B][n_sub][n_noise][P], or NULL */

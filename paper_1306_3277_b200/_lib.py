@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libssm_b200.so")
+# SSM_LIB_PATH: an alternative in-tree build (profiles/: A/B variants of the kernels)
+LIB_PATH = os.environ.get("SSM_LIB_PATH") or os.path.join(HERE, "lib", "libssm_b200.so")
 
 SSM_OK, SSM_ERR_INVALID_ARG, SSM_ERR_CUDA, SSM_ERR_UNSUPPORTED = 0, 1, 2, 3
 SSM_F32, SSM_F64 = 0, 1
@@ -281,7 +282,9 @@ class _Lib:
 
         self._cdll = cdll
         for name, (res, args) in SIGNATURES.items():
-            fn = getattr(cdll, name)
+            fn = getattr(cdll, name, None)
+            if fn is None:  # an older A/B build (SSM_LIB_PATH) without this entry point
+                continue
             fn.restype = res
             fn.argtypes = args
             if name in LAUNCHING:

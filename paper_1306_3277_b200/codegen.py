@@ -151,6 +151,9 @@ def fingerprint(ir) -> str:
     return hashlib.sha256(dumps(d).encode()).hexdigest()
 
 
+ROLES_WITH_SLOTS = ("param", "input", "noise", "state", "obs")
+
+
 def lower(ir) -> dict:
     """Reference ModelIr -> JSON-able description (the codegen input)."""
     counts = {k: int(v) for k, v in ir.counts.items()}
@@ -158,6 +161,9 @@ def lower(ir) -> dict:
         raise UnsupportedModelError(
             f"{ir.name}: device path limits are n_state <= {MAX_STATE}, n_obs <= {MAX_OBS}, n_input <= {MAX_INPUT}")
     out = {"name": ir.name, "counts": counts, "delta": None if ir.delta is None else float(ir.delta)}
+    # variable table (name, role, slot offset, dim sizes) for the data-file layer (timeseries.py)
+    out["vars"] = [{"name": v.name, "role": v.role, "offset": int(v.offset), "dims": [int(d.size) for d in v.dims]}
+                   for v in ir.vars.values() if getattr(v, "role", None) in ROLES_WITH_SLOTS]
     for name in ("initial", "transition", "observation"):
         blk = ir.block(name)
         out[name] = [] if blk is None else [_lower_op(op, ir) for op in blk.ops]

@@ -24,6 +24,14 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
   int maybe = A->maybe_nonuniform;
   int slot = 0;
   A->a_last_index = -1;
+  // On the tile path without an ESS gate every weighted step is resampled from
+  // its tile records, so the unnormalised log-weights of a weighted step are read
+  // again only when it is the call's LAST weighted step (ParticleRun.logw / ess,
+  // a resumed advance): the others are not written (8 B / particle / step less).
+  int last_obs = -1;
+  for (int k = 0; k < A->n_steps; ++k)
+    if (A->steps[k].has_obs) last_obs = k;
+  const bool skip_a = A->tiles && !A->ess_gate;
   cudaEvent_t* ev = reinterpret_cast<cudaEvent_t*>(const_cast<void**>(A->events));
   for (int k = 0; k < A->n_steps; ++k) {
     const ssm_step_desc& d = A->steps[k];
@@ -63,7 +71,7 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
     pw.u_vec = (A->u_table && d.u_off >= 0) ? A->u_table + d.u_off : nullptr;
     void* a_out = nullptr;
     const int a_slot = A->a_ring > 0 ? slot % A->a_ring : slot;
-    if (d.has_obs) a_out = static_cast<char*>(A->a_arena) + static_cast<size_t>(a_slot) * astep;
+    if (d.has_obs && !(skip_a && k != last_obs)) a_out = static_cast<char*>(A->a_arena) + static_cast<size_t>(a_slot) * astep;
     pw.a_out = a_out;
     pw.cdf_local = (A->tiles && d.has_obs) ? A->cdf_local : nullptr;
     pw.tile_rec = (A->tiles && d.has_obs) ? A->tile_rec : nullptr;

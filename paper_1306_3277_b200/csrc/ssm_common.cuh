@@ -258,6 +258,21 @@ __device__ __forceinline__ bool finite(T v) {
   return isfinite(v);
 }
 
+// cp.async (LDGSTS): an asynchronous global -> shared copy per thread that
+// holds no register while in flight.  The fused kernel stages its ancestor
+// gather through shared memory with it (thread-private slots: a thread only
+// ever reads the copies it issued, so cp.async.wait_group alone orders them).
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gmem), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Programmatic dependent launch: the per-step kernels of the filter path are
 // launched with programmatic stream serialization, so a kernel's launch and
 // block scheduling overlap the tail of its predecessor; each such kernel calls

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args
   if (threadIdx.x < 64) s_exp_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
   __syncthreads();
   __shared__ ParkedTiles s_park[kPwThreads / 32];
-  WarpTileAcc acc{&s_park[threadIdx.x >> 5], lse_empty(), 0, 0};
+  WarpTileAcc acc = warp_tile_acc(&s_park[threadIdx.x >> 5], lane);
   bool bad = false, perr = false;
   int bad_sub = 0, perr_sub = 0;
 
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args
 
   if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
   if (perr) atomicMin(&fs->err_param, A.step * 64 + perr_sub);
-  pw_block_finalize<kPwThreads>(A, fs, b, P, R, has_obs, acc.st, lane, kMaxPwBlocks);
+  pw_block_finalize<kPwThreads>(A, fs, b, P, R, has_obs, acc.park->st, lane, kMaxPwBlocks);
 }
 
 // the model's initial block on the device (sample_initial, simulate.py:111-129)

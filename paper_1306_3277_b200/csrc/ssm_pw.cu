@@ -38,7 +38,14 @@ template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE = false>
 // NOTE: plain __launch_bounds__(kThreads).  An explicit minBlocks of 1 lets
 // ptxas spend 172 registers on the SIMPLE f64 kernel (1 CTA/SM, 0.80 ms
 // vs 0.63 ms at 119 registers / 2 CTAs); minBlocks 3 (<= 85) is also slower.
-__global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 : ((SIMPLE && sizeof(T) == 4) ? 3 : 2)) pw_kernel(const ssm_pw_args A) {
+// resident CTAs per SM the register budget is sized for (SIMPLE L96: 3 x 256
+// threads = 24 warps at <= 80 registers; profiles/ for the measured variants)
+#ifndef SSM_PW_CTAS_SIMPLE
+#define SSM_PW_CTAS_SIMPLE (2 * 256 / SSM_PW_THREADS)
+#endif
+__global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 * 256 / kPwThreads
+                                              : (SIMPLE ? SSM_PW_CTAS_SIMPLE : 2 * 256 / kPwThreads))
+    pw_kernel(const ssm_pw_args A) {
   pdl_wait();
   using O = Ar<T, E>;
   constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
@@ -79,21 +86,38 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
   if (threadIdx.x < 64) s_exp_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
   __syncthreads();
   __shared__ ParkedTiles s_park[kPwThreads / 32];
-  WarpTileAcc acc{&s_park[threadIdx.x >> 5], lse_empty(), 0, 0};
+  WarpTileAcc acc = warp_tile_acc(&s_park[threadIdx.x >> 5], lane);
   bool bad = false;
   int bad_sub = 0;
 
-  // software pipeline: the gathered state of the block's next tile and the
-  // ancestor index of the tile after it are in flight while the current tile
-  // computes (the anc -> x dependent loads never stall an iteration)
-  T xn[NX];
+  // Staged ancestor gather (x = x[anc], particle.py:102): while the current
+  // tile computes, each thread's cp.async copies of its NEXT tile's ancestor
+  // state (NX words) are in flight into its own shared-memory slots, and the
+  // ancestor index of the tile after that is loaded -- the anc -> x dependent
+  // loads never stall an iteration and hold no registers (2-stage ring).
+#ifndef SSM_STAGED_GATHER
+#define SSM_STAGED_GATHER 0
+#endif
   const int stride = gridDim.x * kPwThreads;
   const int p0 = blockIdx.x * kPwThreads + threadIdx.x;
-  auto load_x = [&](int pp, int src) {
+#if SSM_STAGED_GATHER
+  __shared__ __align__(16) T s_x[2][NX][kPwThreads];
+  auto stage_x = [&](int st, int src) {
+#pragma unroll
+    for (int n = 0; n < NX; ++n) cp_async<sizeof(T)>(&s_x[st][n][threadIdx.x], xin + static_cast<size_t>(n) * in_stride + src);
+  };
+  if (p0 < P) stage_x(0, anc ? __ldg(anc + p0) : p0);
+  cp_async_commit();
+  int stage = 0;
+#else
+  // register prefetch: the next tile's gathered state is in flight in xn[]
+  T xn[NX];
+  auto load_x = [&](int src) {
 #pragma unroll
     for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * in_stride + src];
   };
-  if (p0 < P) load_x(p0, anc ? __ldg(anc + p0) : p0);
+  if (p0 < P) load_x(anc ? __ldg(anc + p0) : p0);
+#endif
   int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride;
   const T gconst = static_cast<T>(static_cast<double>(__popc(A.obs_mask)) * (A.obs_log_sd + A.log_sqrt_2pi));
   T s_F = T(0), s_c = T(0), s_s = T(0);
@@ -106,7 +130,13 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
     s_s = static_cast<T>(A.subs[0].s[0]);
   }
 
-  constexpr bool kPipeNoise = SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ;
+#ifndef SSM_PIPE_NOISE
+#define SSM_PIPE_NOISE 1
+#endif
+  // kPipeNoise: the next tile's draws issued during this tile's RK4 (8 more live
+  // registers); kDrawNow: the tile's own draws at its start (fits 3 CTAs / SM)
+  constexpr bool kPipeNoise = SSM_PIPE_NOISE && SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ;
+  constexpr bool kDrawNow = !SSM_PIPE_NOISE && SIMPLE && MODEL == SSM_MODEL_LORENZ96 && !E && !INJ;
   constexpr bool kPipeNoiseWK = SIMPLE && MODEL == SSM_MODEL_WINDKESSEL && !INJ;
   float zc[8], zn[8];  // (kPipeNoise*) this tile's and the next tile's standard normals
   if constexpr (kPipeNoise) {
@@ -123,14 +153,28 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
     const bool act = p < P;
     double a_d = -CUDART_INF;
     T x[NX];
+#if SSM_STAGED_GATHER
+    {
+      const int p2 = p + stride;
+      if (p2 < P) stage_x(stage ^ 1, anc_next);
+      cp_async_commit();  // (possibly empty) group per tile: uniform group accounting
+      const int p3 = p2 + stride;
+      anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
+    }
+    cp_async_wait<1>();  // this tile's copies have landed (the next tile's may be in flight)
+#pragma unroll
+    for (int n = 0; n < NX; ++n) x[n] = s_x[stage][n][threadIdx.x];
+    stage ^= 1;
+#else
 #pragma unroll
     for (int n = 0; n < NX; ++n) x[n] = xn[n];
     {
       const int p2 = p + stride;
-      if (p2 < P) load_x(p2, anc_next);
+      if (p2 < P) load_x(anc_next);
       const int p3 = p2 + stride;
       anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
     }
+#endif
     if (act) {
       if constexpr (kPipeNoise) {
         // the next tile's draws do not depend on this tile: issuing them here gives the
@@ -146,6 +190,16 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
         }
 #pragma unroll
         for (int n = 0; n < 8; ++n) zc[n] = zn[n];
+      } else if constexpr (kDrawNow) {
+        float z[8];
+        normals8f(k0, k1, static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step), 0u, z);
+        l96_simple_step<T>(reinterpret_cast<T(&)[8]>(x), z, s_F, s_c, s_s);
+        if (A.check_finite != 0 && !defer_finite && !bad) {
+          bool ok = true;
+#pragma unroll
+          for (int n = 0; n < NX; ++n) ok &= finite_bits(x[n]);
+          if (!ok) bad = true;
+        }
       } else if constexpr (kPipeNoiseWK) {
         const int pn = p + stride;
         if (pn < P) zn[0] = normal1<float>(k0, k1, static_cast<uint32_t>(pn + A.p_offset), static_cast<uint32_t>(A.step), 0u);
@@ -232,7 +286,7 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
 
   if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
 
-  pw_block_finalize<kPwThreads>(A, fs, b, P, R, has_obs, acc.st, lane, kMaxPwBlocks);
+  pw_block_finalize<kPwThreads>(A, fs, b, P, R, has_obs, acc.park->st, lane, kMaxPwBlocks);
 }
 
 template <int MODEL, typename T>
@@ -359,7 +413,9 @@ extern "C" int ssm_propagate_weight(const ssm_pw_args* args, void* stream) {
   if (A.B <= 0 || A.P <= 0 || A.B > 65535 || A.n_sub < 0 || !A.x_in || !A.x_out || !A.theta ||
       (A.n_sub > 0 && !A.subs) || !A.fs || !A.workspace)
     return SSM_ERR_INVALID_ARG;
-  if (A.has_obs && !A.a_out) return SSM_ERR_INVALID_ARG;
+  // a_out may be omitted on the tile path (cdf_local set): ssm_advance skips it
+  // when the next step resamples from the tile records
+  if (A.has_obs && !A.a_out && !A.cdf_local) return SSM_ERR_INVALID_ARG;
   if (A.n_sub > 0 && !A.noise && !A.keys) return SSM_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (A.model == SSM_MODEL_GENERIC) return ssm_gen_propagate_weight(A, s);

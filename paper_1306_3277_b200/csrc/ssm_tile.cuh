@@ -17,7 +17,10 @@
 
 namespace ssm {
 
-constexpr int kPwThreads = kThreads;  // fused-kernel block (128 threads x 5 CTAs spills: slower)
+#ifndef SSM_PW_THREADS
+#define SSM_PW_THREADS 256
+#endif
+constexpr int kPwThreads = SSM_PW_THREADS;  // fused-kernel block
 constexpr int kMaxPwBlocks = 2048;  // per filter; a function of P only (determinism)
 
 // Blocks per filter: >= 4 block tiles per block, so each warp folds several warp
@@ -95,23 +98,33 @@ __device__ __forceinline__ Lse fold_tiles(Lse st, double m, double t, double s2,
   return st;
 }
 
-// Warp-tile partials parked until 32 have accumulated (one per slot, in tile order).
+// Warp-tile partials parked until 32 have accumulated (one per slot, in tile
+// order), and the warp partial they fold into (shared memory, not registers:
+// the fused kernels run at 3 CTAs / SM on an 80-register budget).
 struct ParkedTiles {
   double m[32], t[32], s2[32];
+  Lse st;  // warp partial, groups of 32 warp tiles folded in order (lane 0 writes)
 };
 
-__device__ __forceinline__ Lse fold_parked(Lse st, const ParkedTiles* pk, bool valid, int lane) {
-  return fold_tiles(st, valid ? pk->m[lane] : -CUDART_INF, valid ? pk->t[lane] : 0.0,
-                    valid ? pk->s2[lane] : 0.0, lane);
+__device__ __forceinline__ void fold_parked(ParkedTiles* pk, bool valid, int lane) {
+  const Lse st = lane == 0 ? pk->st : lse_empty();
+  const Lse r = fold_tiles(st, valid ? pk->m[lane] : -CUDART_INF, valid ? pk->t[lane] : 0.0,
+                           valid ? pk->s2[lane] : 0.0, lane);
+  if (lane == 0) pk->st = r;
 }
 
-// Running state of a warp's weighted tiles (lane 0 holds the warp partial).
+// Running state of a warp's weighted tiles (the warp partial lives in park->st).
 struct WarpTileAcc {
   ParkedTiles* park;  // this warp's parking slots in shared memory
-  Lse st;             // warp partial, groups of 32 warp tiles folded in order
   int slot;           // parking slot of the current warp tile's {m_w, t_w, s2_w}
   int nparked;        // (lane 0) slots filled since the last fold: a prefix of the slots
 };
+
+__device__ __forceinline__ WarpTileAcc warp_tile_acc(ParkedTiles* park, int lane) {
+  if (lane == 0) park->st = lse_empty();
+  __syncwarp();
+  return WarpTileAcc{park, 0, 0};
+}
 
 // One weighted warp tile: a_d = the particle's unnormalised log-weight (-inf
 // when inactive).  Warp-uniform call (all 32 lanes).
@@ -164,7 +177,7 @@ __device__ __forceinline__ void warp_tile_weigh(WarpTileAcc& acc, double a_d, bo
   }
   if (++acc.slot == 32) {
     __syncwarp();
-    acc.st = fold_parked(acc.st, acc.park, lane < __shfl_sync(0xffffffffu, acc.nparked, 0), lane);
+    fold_parked(acc.park, lane < __shfl_sync(0xffffffffu, acc.nparked, 0), lane);
     __syncwarp();
     acc.slot = 0;
     acc.nparked = 0;
@@ -175,8 +188,9 @@ __device__ __forceinline__ void warp_tile_weigh(WarpTileAcc& acc, double a_d, bo
 __device__ __forceinline__ void warp_tile_flush(WarpTileAcc& acc, int lane) {
   if (acc.slot > 0) {
     __syncwarp();
-    acc.st = fold_parked(acc.st, acc.park, lane < __shfl_sync(0xffffffffu, acc.nparked, 0), lane);
+    fold_parked(acc.park, lane < __shfl_sync(0xffffffffu, acc.nparked, 0), lane);
   }
+  __syncwarp();
 }
 
 // Per-block partial + last-block finalize (completion counter): block partials

@@ -487,11 +487,20 @@ _RS_LAUNCHES = {("tiles", 1): 3, ("tiles", 2): 3, ("tiles", 3): 4,
                 ("logw", 0): 2, ("logw", 1): 4, ("logw", 2): 4, ("logw", 3): 4}
 
 
-def _tile_resample_bytes(scheme):
-    """Algorithmic bytes per particle of a tile-path resample: cdf_local read (8),
-    ancestor write (4), tile records / scales / prefixes (1.5); the sorted
-    multinomial also writes and reads its spacing prefixes (16)."""
-    return 13.5 + (16.0 if scheme == _lib.SSM_MULTINOMIAL_SORTED else 0.0)
+def _resample_bytes(esz):
+    """Algorithmic bytes per particle of a resample (B_R without the
+    gather, which the fused kernel performs): read the weight (r) + write the
+    ancestor (4).  The CDF (cdf_local / tile records / spacing prefixes) is an
+    implementation intermediate and is not counted."""
+    return esz + 4
+
+
+def _pw_bytes(nx, esz, resampled, weighted):
+    """Algorithmic bytes per particle of one fused step (SURVEY 8d B_P plus the
+    gather's ancestor read): x in + x out (2 nx r), the ancestor (4) when the step
+    resampled, the log-weight (r) when it weighted.  cdf_local and a_out are
+    implementation intermediates (not counted)."""
+    return 2 * nx * esz + (4 if resampled else 0) + (esz if weighted else 0)
 
 
 def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, maybe, x_arena, a_arena,
@@ -545,10 +554,8 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
         if timer is not None:
             has_obs = bool(desc["has_obs"][k])
             if an is not None:
-                rs_bytes = int(B * P * (_tile_resample_bytes(scheme) if tiles_ok else (2 * esz + 12)))
-                timer.add("resample", evs[4 * k], evs[4 * k + 1], rs_bytes)
-            nbytes = B * P * (2 * spec.nx * esz + (4 if an is not None else 0)
-                              + ((esz + (8 if tiles_ok else 0)) if has_obs else 0))
+                timer.add("resample", evs[4 * k], evs[4 * k + 1], int(B * P * _resample_bytes(esz)))
+            nbytes = B * P * _pw_bytes(spec.nx, esz, an is not None, has_obs)
             timer.add("propagate_weight", evs[4 * k + 2], evs[4 * k + 3], nbytes)
     a_new = a_arena[A.a_last_index] if A.a_last_index >= 0 else a_last
     return x_arena[(n - 1) % ring], a_new, bool(A.maybe_nonuniform)
@@ -715,14 +722,13 @@ def advance_runs(runs, upto, rngs):
                     u = np.stack([g.uniform(size=P) for g in rr])
                 u_t = torch.from_numpy(u).to(dev)
             if tiles_ok:
-                # bytes: cdf_local read + c write/read + anc write (+ tile records, negligible)
-                with profiling.maybe("resample", int(B * P * _tile_resample_bytes(scheme))):
+                with profiling.maybe("resample", int(B * P * _resample_bytes(esz))):
                     _lib.check(L.ssm_resample_from_tiles(B, P, scheme, _lib.ptr(cdf_local), _lib.ptr(tile_rec),
                                                          _lib.ptr(fs), _lib.ptr(u_t), _lib.ptr(keys_t), i,
                                                          _lib.ptr(anc), _lib.ptr(rs_ws), stream),
                                "ssm_resample_from_tiles")
             else:
-                with profiling.maybe("resample", B * P * (2 * esz + 4 + 4 + 4)):
+                with profiling.maybe("resample", int(B * P * _resample_bytes(esz))):
                     _lib.check(L.ssm_resample_from_logw(B, P, r0.dtype_id, scheme, _lib.ptr(a_last), None,
                                                         _lib.ptr(fs), _lib.ptr(u_t), _lib.ptr(keys_t), i,
                                                         _lib.ptr(anc), _lib.ptr(rs_ws), stream),
@@ -761,10 +767,7 @@ def advance_runs(runs, upto, rngs):
         else:
             args.has_obs = 0
             args.obs_mask = 0
-        # algorithmic bytes: (anc) + gather read + write of x + (read a_prev) + write a
-        nbytes = B * P * (2 * spec.nx * esz + (4 if anc is not None else 0)
-                          + (esz + (8 if tiles_ok else 0) if obs is not None else 0)
-                          + (esz if (a_last is not None and obs is not None and r0.ess_rel is not None) else 0))
+        nbytes = B * P * _pw_bytes(spec.nx, esz, anc is not None, obs is not None)
         with profiling.maybe("propagate_weight", nbytes):
             _lib.check(L.ssm_propagate_weight(args, stream), "ssm_propagate_weight")
         new_hist.append((x_out, anc))

@@ -156,8 +156,8 @@ def test_windkessel_simple_equals_general_kernel_2p16(monkeypatch):
     monkeypatch.setattr(particle_mod, "_NO_HINTS", True)
     b = particle_filter(WINDKESSEL, g["wk/theta"], grid, RngStream(5), **kw)
     assert abs(a.loglik - b.loglik) <= 1e-12 * abs(b.loglik)
-    for i in range(1, 51):
-        np.testing.assert_array_equal(a.run.history[i][1].cpu().numpy(), b.run.history[i][1].cpu().numpy())
+    for aa, bb in zip(_device_anc(a.run, 50), _device_anc(b.run, 50)):
+        np.testing.assert_array_equal(aa, bb)
     assert normwise(a.run.x, b.run.x) <= 1e-13
     assert normwise(a.trajectory, b.trajectory) <= 1e-13
 
@@ -188,7 +188,7 @@ def test_tile_cdf_vs_reference_cumsum_flip_bound_2p24():
         u = torch.from_numpy(u_np).cuda()
         ws = torch.empty(L.ssm_resample_workspace_bytes(1, P), dtype=torch.uint8, device="cuda")
         anc = torch.empty(P, dtype=torch.int32, device="cuda")
-        _lib.check(L.ssm_resample_from_tiles(1, P, _lib.SSM_SYSTEMATIC, _lib.ptr(cdf), _lib.ptr(rec), _lib.ptr(fs),
+        _lib.check(L.ssm_resample_from_tiles(1, P, _lib.SCHEME_IDS["systematic"], _lib.ptr(cdf), _lib.ptr(rec), _lib.ptr(fs),
                                              _lib.ptr(u), None, 1, _lib.ptr(anc), _lib.ptr(ws), _lib.stream_ptr()))
         got = anc.cpu().numpy()
         q = O.queries("systematic", u_np, P)
@@ -222,9 +222,8 @@ def test_small_kernel_full_run_matches_multikernel(scheme, exact, P, monkeypatch
     monkeypatch.setattr(particle_mod, "_NO_SMALL", True)
     monkeypatch.setattr(particle_mod, "_NO_HINTS", True)  # the general transition, as the small kernel
     multi = particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(3), **kw)
-    for i in range(1, 21):
-        np.testing.assert_array_equal(small.run.history[i][1].cpu().numpy(), multi.run.history[i][1].cpu().numpy(),
-                                      err_msg=f"ancestors at step {i}")
+    for i, (aa, bb) in enumerate(zip(_device_anc(small.run, 20), _device_anc(multi.run, 20)), start=1):
+        np.testing.assert_array_equal(aa, bb, err_msg=f"ancestors at step {i}")
     np.testing.assert_array_equal(small.run.x, multi.run.x)
     assert abs(small.loglik - multi.loglik) <= 1e-12 * abs(multi.loglik)
     np.testing.assert_array_equal(small.trajectory, multi.trajectory)

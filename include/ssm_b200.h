@@ -278,6 +278,17 @@ size_t ssm_resample_workspace_bytes(int B, int P);
 int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf_local, const void* tile_rec,
                             const ssm_filter_state* fs, const double* u, const uint32_t* keys,
                             int step, int32_t* anc, void* workspace, void* stream);
+/* ssm_resample_from_tiles as the native driver calls it once per grid step.
+ * `parity` / `zero_state` carry the state of the single-kernel variant (built
+ * with -DSSM_RESAMPLE_FUSED=1: tile scale + decoupled look-back prefix +
+ * offspring + window fill in one kernel, look-back state double-buffered by
+ * parity, cleared when zero_state != 0); the default build runs the two-kernel
+ * path (tile scale with the block prefix in its last block, then offspring +
+ * window fill), which measured faster.  ssm_resample_from_tiles = parity 0,
+ * zero_state 1. */
+int ssm_resample_tiles_step(int B, int P, int scheme, const void* cdf_local, const void* tile_rec,
+                            const ssm_filter_state* fs, const double* u, const uint32_t* keys, int step,
+                            int32_t* anc, void* workspace, int parity, int zero_state, void* stream);
 int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const void* a, const double* shift,
                            const ssm_filter_state* fs, const double* u, const uint32_t* keys,
                            int step, int32_t* anc, void* workspace, void* stream);

@@ -212,6 +212,7 @@ SIGNATURES = {
     "ssm_resample_workspace_bytes": (_sz, [_i, _i]),
     "ssm_resample_from_logw": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ssm_resample_from_tiles": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
+    "ssm_resample_tiles_step": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _vp]),
     "ssm_gather": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "ssm_gather_cols": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "ssm_trace": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
@@ -253,7 +254,8 @@ LAUNCHING = {
     "ssm_fixed_to_cum": 1,
     "ssm_resample_search": 1,
     "ssm_resample_from_logw": 4,
-    "ssm_resample_from_tiles": 3,
+    "ssm_resample_from_tiles": 3,  # systematic / stratified: tile scale, offspring, long runs (sorted multinomial: 4)
+    "ssm_resample_tiles_step": 3,
     "ssm_gather": 1,
     "ssm_gather_cols": 1,
     "ssm_trace": 1,
@@ -295,6 +297,8 @@ class _Lib:
                         profiling.count_launch(2)  # raw weights: total pre-pass + scan
                     elif _name == "ssm_resample_search" and a[3] != 0:
                         profiling.count_launch(2)  # offspring + expand
+                    elif _name in ("ssm_resample_from_tiles", "ssm_resample_tiles_step") and a[2] == 3:
+                        profiling.count_launch(4)  # sorted multinomial: tile scale, spacing sums / prefix, merge
                     elif _name == "ssm_resample_from_logw" and a[3] == 0:
                         profiling.count_launch(2)  # look-back scan + binary search
                     elif _name == "ssm_advance":

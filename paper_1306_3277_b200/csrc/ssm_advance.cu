@@ -32,6 +32,7 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
   for (int k = 0; k < A->n_steps; ++k)
     if (A->steps[k].has_obs) last_obs = k;
   const bool skip_a = A->tiles && !A->ess_gate;
+  int n_resample = 0;  // fused resample: look-back state parity
   cudaEvent_t* ev = reinterpret_cast<cudaEvent_t*>(const_cast<void**>(A->events));
   for (int k = 0; k < A->n_steps; ++k) {
     const ssm_step_desc& d = A->steps[k];
@@ -41,12 +42,14 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
       A->anc_used[k] = 1;
       if (ev) cudaEventRecord(ev[4 * k + 0], s);
       int st;
-      if (A->tiles)
-        st = ssm_resample_from_tiles(B, P, A->scheme, A->cdf_local, A->tile_rec, A->pw.fs, nullptr,
-                                     A->pw.keys, d.step, anc, A->resample_ws, stream);
-      else
+      if (A->tiles) {
+        st = ssm_resample_tiles_step(B, P, A->scheme, A->cdf_local, A->tile_rec, A->pw.fs, nullptr, A->pw.keys,
+                                     d.step, anc, A->resample_ws, n_resample & 1, n_resample == 0, stream);
+        ++n_resample;
+      } else {
         st = ssm_resample_from_logw(B, P, A->pw.dtype, A->scheme, a_last, nullptr, A->pw.fs, nullptr,
                                     A->pw.keys, d.step, anc, A->resample_ws, stream);
+      }
       if (ev) cudaEventRecord(ev[4 * k + 1], s);
       if (st != SSM_OK) return st;
     } else {

@@ -933,6 +933,169 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
 }
 
 // ---------------------------------------------------------------------------
+// Fused filter-path resample (systematic / stratified): tile scale, global
+// prefix and offspring + ancestors in ONE kernel.  Each block owns 2048
+// particles = 64 warp tiles: it scales its tiles' records (Q'_w =
+// round(exp(m_w - incr) 2^9 Q_w)), scans them, and obtains its exclusive prefix
+// from its predecessors by a decoupled look-back over exact 64-bit integer
+// aggregates (associative: the same prefix on every run, whatever the timing).
+// The CDF is normalised by the nominal total 2^61 = exp(LSE) on the 2^61 fixed
+// point instead of the exact sum of the Q'_w (which would need a second pass
+// over all tiles): C_j / 2^61 differs from C_j / sum_w Q'_w by the rounding of
+// the LSE (~1e-15 relative), far below the fixed-point CDF's own distance to
+// the reference's float64 cumsum.  The last particle's
+// run still ends at P (cum[-1] = 1.0, resampling.py:27) and counts clamp at P.
+// Look-back status words and the long-run counters are double-buffered by
+// `parity`: each launch clears the other parity's words for the next one (whose
+// previous user completed before this kernel passed griddepcontrol.wait).
+// ---------------------------------------------------------------------------
+constexpr int kFusedTiles = kScanTile / 32;  // 64 warp tiles per block
+constexpr double kNominalTotal = 2305843009213693952.0;  // 2^61
+
+struct FusedWs {
+  uint64_t* status;      // [2][B][nb]
+  uint32_t* long_count;  // [2][B]
+};
+
+__host__ __device__ inline size_t fused_ws_words(int B, int P) {
+  return 2 * static_cast<size_t>(B) * scan_tiles(P) + static_cast<size_t>(B) + 1;
+}
+
+__host__ __device__ inline FusedWs fused_ws(uint64_t* base, int B, int P) {
+  return FusedWs{base, reinterpret_cast<uint32_t*>(base + 2 * static_cast<size_t>(B) * scan_tiles(P))};
+}
+
+template <int SCHEME>
+__global__ void __launch_bounds__(kThreads)
+resample_fused_kernel(int P, const uint64_t* __restrict__ cdf_local, const ssm_tile_rec* __restrict__ rec,
+                      const ssm_filter_state* __restrict__ fs, const double* __restrict__ u,
+                      const uint32_t* __restrict__ keys, int step, int32_t* __restrict__ anc,
+                      int4* __restrict__ long_runs, FusedWs ws, int parity) {
+  pdl_wait();
+  constexpr int kIt = kRunIt;
+  __shared__ __align__(16) RunWindow sm;
+  __shared__ uint64_t s_pre[kFusedTiles];
+  __shared__ double s_sc[kFusedTiles];
+  __shared__ uint64_t s_wtot[2];
+  __shared__ uint64_t s_excl;
+  __shared__ double s_usys;
+  const int b = blockIdx.y, blk = blockIdx.x, nb = gridDim.x, B = gridDim.y;
+  uint64_t* st = ws.status + (static_cast<size_t>(parity) * B + b) * nb;
+  uint32_t* long_count = ws.long_count + static_cast<size_t>(parity) * B;
+  if (threadIdx.x == 0) {  // the other parity's words, for the next launch
+    ws.status[(static_cast<size_t>(parity ^ 1) * B + b) * nb + blk] = 0ull;
+    if (blk == 0) ws.long_count[static_cast<size_t>(parity ^ 1) * B + b] = 0u;
+  }
+  if (fs && !fs[b].resample_now) {  // ESS gate held (particle.py:99-100): the history records identity
+    int32_t* ab = anc + static_cast<size_t>(b) * P;
+    const int k1 = min(P, (blk + 1) * kScanTile);
+    for (int k = blk * kScanTile + threadIdx.x; k < k1; k += kThreads) ab[k] = k;
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nt = (P + 31) >> 5;
+  const double incr = fs[b].incr;
+  // (1) this block's 64 warp tiles: global scale and in-block exclusive prefix
+  uint64_t q = 0, incl = 0;
+  if (threadIdx.x < kFusedTiles) {
+    const int w = blk * kFusedTiles + threadIdx.x;
+    double sc = 0.0;
+    if (w < nt) {
+      const ssm_tile_rec r = rec[static_cast<size_t>(b) * nt + w];
+      sc = r.m == -CUDART_INF ? 0.0 : exp(r.m - incr) * kTileScale;
+      const double v = sc * static_cast<double>(r.Q);
+      q = (v >= 0.0 && v < 4.0e18) ? __double2ull_rn(v) : 0ull;
+    }
+    s_sc[threadIdx.x] = sc;
+    incl = q;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wtot[warp] = incl;
+  }
+  if (threadIdx.x == kThreads - 1) {
+    const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
+    s_usys = SCHEME == SSM_SYSTEMATIC ? (u ? u[b] : device_uniform(k0, k1, 0u, step, kPurposeSystematic)) : 0.0;
+  }
+  __syncthreads();
+  // (2) decoupled look-back for the block's exclusive prefix (warp 0)
+  if (warp == 0) {
+    const uint64_t btot = s_wtot[0] + s_wtot[1];
+    uint64_t excl = 0;
+    if (blk == 0) {
+      if (lane == 0) st_status(&st[0], kFlagPrefix | (btot & kValueMask));
+    } else {
+      if (lane == 0) st_status(&st[blk], kFlagAgg | (btot & kValueMask));
+      int look = blk - 1;
+      while (true) {
+        const int idx = look - lane;
+        uint64_t sv = idx >= 0 ? ld_status(&st[idx]) : kFlagPrefix;
+        while (__any_sync(0xffffffffu, (sv >> 62) == 0)) {
+          if ((sv >> 62) == 0) sv = ld_status(&st[idx]);
+        }
+        const uint32_t pm = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
+        const int first = __ffs(pm) - 1;  // nearest predecessor holding a prefix
+        uint64_t contrib = (first < 0 || lane <= first) ? (sv & kValueMask) : 0ull;
+        if (idx < 0) contrib = 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) contrib += __shfl_down_sync(0xffffffffu, contrib, o);
+        excl += __shfl_sync(0xffffffffu, contrib, 0);
+        if (first >= 0) break;
+        look -= 32;
+      }
+      if (lane == 0) st_status(&st[blk], kFlagPrefix | ((excl + btot) & kValueMask));
+    }
+    if (lane == 0) s_excl = excl;
+  }
+  __syncthreads();
+  if (threadIdx.x < kFusedTiles) s_pre[threadIdx.x] = s_excl + (warp == 1 ? s_wtot[0] : 0ull) + incl - q;
+  __syncthreads();
+  // (3) offspring counts per particle (lane = particle, 8 tiles per warp) -> window fill
+  const uint64_t* cl = cdf_local + static_cast<size_t>(b) * P;
+  const int jw = blk * kScanTile + warp * (kScanTile / (kThreads / 32));
+  uint64_t qv[kIt];
+#pragma unroll
+  for (int it = 0; it < kIt; ++it) {
+    const int j = jw + it * 32 + lane;
+    qv[it] = j < P - 1 ? __ldg(cl + j) : 0ull;
+  }
+  const double inv = 1.0 / kNominalTotal, Pd = static_cast<double>(P);
+  const double tscale = Pd * inv, invP = 1.0 / Pd;
+  const bool pow2 = (P & (P - 1)) == 0;
+  const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
+  const double u_sys = s_usys;
+  const double* U = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * P : nullptr;
+  const auto count = [&](uint64_t C) -> int {
+    const double Cd = static_cast<double>(C);
+    if constexpr (SCHEME == SSM_SYSTEMATIC) {
+      const double t = fma(Cd, tscale, -u_sys);
+      const double e = ceil(t);
+      const double d = e - t;  // in [0, 1), within 2^-53
+      if (d > 0x1p-20 && d < 1.0 - 0x1p-20 && P <= (1 << 30)) return min(max(__double2int_rz(e), 0), P);
+    }
+    return offspring_bound<SCHEME>(Cd * inv, u_sys, U, k0, k1, step, P, invP, pow2);
+  };
+  const int tw = warp * kIt;  // the warp's first tile within the block
+  int carry = 0;
+  if (jw > 0 && jw < P) carry = count(s_pre[tw]);
+  else if (jw >= P) carry = P;
+  if (warp == 0 && lane == 0) sm.lo = carry;
+  int cv[kIt], pv[kIt];
+#pragma unroll
+  for (int it = 0; it < kIt; ++it) {
+    const int j = jw + it * 32 + lane;
+    const int c = j < P - 1 ? count(s_pre[tw + it] + __double2ull_rn(s_sc[tw + it] * static_cast<double>(qv[it]))) : P;
+    const int up = __shfl_up_sync(0xffffffffu, c, 1);
+    pv[it] = lane == 0 ? carry : up;
+    cv[it] = c;
+    carry = __shfl_sync(0xffffffffu, c, 31);
+  }
+  fill_run_window(sm, b, P, jw, cv, pv, anc, long_runs, long_count);
+}
+
+// ---------------------------------------------------------------------------
 // Sorted multinomial via exponential spacings: with E_1..E_{P+1} iid Exp(1) and
 // S_k = E_1 + ... + E_k, (S_1, ..., S_P) / S_{P+1} has the law of P sorted iid
 // U(0,1) draws, so searchsorted(cum, U_(k)) is a multinomial sample with the
@@ -1551,6 +1714,7 @@ struct SearchWs {
   void* scan;
   uint64_t* C;
   double* spc;  // sorted multinomial: block-local inclusive spacing sums, [B][nsb * 2048]
+  uint64_t* lb;  // fused tile resample: double-buffered look-back status + long-run counts (fused_ws)
 };
 
 static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, SearchWs* w) {
@@ -1582,6 +1746,7 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
   tmp.spc = reinterpret_cast<double*>(
       take(sizeof(double) * static_cast<size_t>(B) * ((P_in + 1 + kScanTile - 1) / kScanTile) * kScanTile));
   tmp.scan = take(scan_ws_bytes(B, P_in));
+  tmp.lb = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * fused_ws_words(B, P_in)));
   tmp.split = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * (nd + 1)));
   if (w) *w = tmp;
   return off;
@@ -1645,15 +1810,51 @@ extern "C" int ssm_resample_from_tiles(int B, int P, int scheme, const void* cdf
                                        const void* tile_rec, const ssm_filter_state* fs,
                                        const double* u, const uint32_t* keys, int step, int32_t* anc,
                                        void* workspace, void* stream) {
+  return ssm_resample_tiles_step(B, P, scheme, cdf_local, tile_rec, fs, u, keys, step, anc, workspace, 0, 1,
+                                 stream);
+}
+
+extern "C" int ssm_resample_tiles_step(int B, int P, int scheme, const void* cdf_local, const void* tile_rec,
+                                       const ssm_filter_state* fs, const double* u, const uint32_t* keys, int step,
+                                       int32_t* anc, void* workspace, int parity, int zero_state, void* stream) {
   if (B <= 0 || B > 65535 || P <= 0 || !cdf_local || !tile_rec || !fs || !anc || !workspace)
     return SSM_ERR_INVALID_ARG;
   if (!u && !keys) return SSM_ERR_INVALID_ARG;
   if (scheme != SSM_SYSTEMATIC && scheme != SSM_STRATIFIED && scheme != SSM_MULTINOMIAL_SORTED)
     return SSM_ERR_INVALID_ARG;
   if (scheme == SSM_MULTINOMIAL_SORTED && (u || !keys)) return SSM_ERR_INVALID_ARG;
+  if (parity != 0 && parity != 1) return SSM_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SearchWs w;
   search_ws_layout(B, P, P, workspace, &w);
+#ifndef SSM_RESAMPLE_FUSED
+#define SSM_RESAMPLE_FUSED 0  // measured slower: 0.176 vs 0.103 ms per 2^24 resample (profiles/r2_ab.txt)
+#endif
+  if (SSM_RESAMPLE_FUSED && scheme != SSM_MULTINOMIAL_SORTED) {  // one fused kernel + long-run fill
+    if (zero_state) {
+      const cudaError_t e = cudaMemsetAsync(w.lb, 0, sizeof(uint64_t) * fused_ws_words(B, P), s);
+      if (e != cudaSuccess) {
+        ssm_set_last_error(e);
+        return SSM_ERR_CUDA;
+      }
+    }
+    const FusedWs fw = fused_ws(w.lb, B, P);
+    const dim3 g(scan_tiles(P), B);
+    const auto* cl = static_cast<const uint64_t*>(cdf_local);
+    const auto* rec = static_cast<const ssm_tile_rec*>(tile_rec);
+    int4* long_runs = reinterpret_cast<int4*>(w.cnt);
+    if (scheme == SSM_SYSTEMATIC)
+      launch_pdl(resample_fused_kernel<SSM_SYSTEMATIC>, g, dim3(kThreads), s, P, cl, rec, fs, u, keys, step, anc,
+                 long_runs, fw, parity);
+    else
+      launch_pdl(resample_fused_kernel<SSM_STRATIFIED>, g, dim3(kThreads), s, P, cl, rec, fs, u, keys, step, anc,
+                 long_runs, fw, parity);
+    const int gx = std::max(1, std::min(1184 / B, P / kRunChunk + 1));
+    launch_pdl(long_runs_kernel, dim3(gx, B), dim3(kThreads), s, P, P, static_cast<const int4*>(long_runs),
+               static_cast<const uint32_t*>(fw.long_count + static_cast<size_t>(parity) * B), fs, anc);
+    SSM_CHECK_LAUNCH();
+    return SSM_OK;
+  }
   const int nt = (P + 31) / 32;
   const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
   // reuse w.C (B*P u64): [scale B*nt doubles][in-block prefixes B*nt][block prefixes B*nblk]

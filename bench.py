@@ -269,6 +269,116 @@ def run_ours(args, rank, world):
                 e2e_ms=e2e_ms, h2d=h2d, d2h=d2h)
 
 
+# ------------------------------------------------------------ SMC^2 workload (config 4)
+
+SMC2_METRIC = "particle-updates/sec (SMC^2 on Lorenz '96, 1024 theta x 2^14, rejuvenation replays counted)"
+
+
+def run_smc2(args, rank, world):
+    """Config 4: SMC^2 on L96 with 1024 theta-particles x 2^14 state
+    particles, sparse observations (slots 0-3 every other step of linspace(0,2,41)),
+    systematic at both levels, theta-slots sharded contiguously over the ranks
+    (smc_sampler with torch.distributed: per observation one all-gather of the
+    theta log-weights (C2) and the point-to-point redistribution of migrating
+    theta-particles (C3, history-free payloads)).  One bench step = one complete
+    SMC^2 run; particle-updates = sum over theta-particles of P x (propagated +
+    replayed grid steps)."""
+    import torch
+
+    from paper_1306_3277_b200 import LORENZ96, RngStream, profiling
+    from paper_1306_3277_b200.inference import FilterRunner, build_filter_grid, smc_sampler
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    n_theta, P, T = args.smc_theta, args.smc_particles, 40
+    times = np.linspace(0.0, 2.0, T + 1)
+    ot, ov, om = simulate_l96_data(times, obs_slots=range(4), obs_every=2)
+    grid = build_filter_grid(0.0, 2.0, T, ot, ov, om, n_obs=8)
+    runner = FilterRunner(LORENZ96, grid, n_particles=P, resampler="systematic", keep_history=False)
+    obs_steps = grid.obs_steps
+    steps = sum(obs_steps) + sum((obs_steps[i - 2] if i > 1 else 0) for i in range(1, len(obs_steps) + 1))
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+
+    def barrier():
+        if dist:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    def one(k):
+        return smc_sampler(LORENZ96, runner, n_theta, RngStream(11, (k,)), theta_resampler="systematic",
+                           theta_draws="device")
+
+    timer = profiling.KernelTimer()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clocks:
+        for w in range(args.warmup):
+            one(10**6 + w)
+        barrier()
+        n0 = profiling.launch_count()
+        t_wall0 = time.time()
+        start.record()
+        ess = []
+        for k in range(args.steps):
+            with profiling.timing(timer):
+                res = one(k)
+            ess.append(res.diagnostics[-1]["ess"])
+        end.record()
+        barrier()
+        t_wall1 = time.time()
+    ms = start.elapsed_time(end)
+    launches = profiling.launch_count() - n0
+    e2e_ms = None
+    if args.e2e_steps > 0:  # through the public API from host data: grid, runner and sampler built per step
+        barrier()
+        t0 = time.perf_counter()
+        for k in range(args.e2e_steps):
+            g2 = build_filter_grid(0.0, 2.0, T, ot.copy(), ov.copy(), om.copy(), n_obs=8)
+            r2 = FilterRunner(LORENZ96, g2, n_particles=P, resampler="systematic", keep_history=False)
+            out = smc_sampler(LORENZ96, r2, n_theta, RngStream(12, (k,)), theta_resampler="systematic",
+                              theta_draws="device")
+            _ = float(np.sum(out.logliks))
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+    if dist:
+        t = torch.tensor([ms, e2e_ms or 0.0], device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms, e2e_ms = float(t[0]), (float(t[1]) if e2e_ms is not None else None)
+    return dict(ms=ms, kern=timer.summary(), launches=launches, clocks=clocks.summary(t_wall0, t_wall1),
+                e2e_ms=e2e_ms, steps_per_run=steps, ess=ess)
+
+
+def smc2_line(args, res, world):
+    n_theta, P, K = args.smc_theta, args.smc_particles, args.steps
+    updates = n_theta * P * res["steps_per_run"]
+    value = updates * K / (res["ms"] / 1e3)
+    peak, peak_kind = load_peaks()
+    pw = res["kern"].get("propagate_weight", {})
+    achieved = pw["bytes"] / (pw["total_ms"] / 1e3) / 1e9 if pw else None
+    line = {
+        "metric": SMC2_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": res["ms"] / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (L96 theta*=(10,0.1), sparse obs: slots 0-3 every other step; device noise)",
+        "config": {"workload": f"SMC^2 on Lorenz96, {n_theta} theta-particles x 2^{int(math.log2(P))} particles, "
+                               "T=40 grid steps, 20 sparse observations, systematic at both levels, float64",
+                   "theta_particles": n_theta, "particles": P, "grid_steps": 40,
+                   "parallelism": f"theta-slots sharded over {world} GPU(s): C2 all-gather of theta log-weights, "
+                                  "C3 point-to-point theta-particle redistribution (history-free payloads)",
+                   "theta_draws": "device", "history": "history-free runs (ancestors + replayed trajectories)"},
+        "roofline": {"bound": "hbm", "kernel": "pw_kernel (batched over theta-particles)", "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": None},
+        "kernels": {k: {"avg_ms": round(v["avg_ms"], 4), "launches": v["launches"]} for k, v in res["kern"].items()},
+        "gpu_launches": res["launches"], "clocks": res["clocks"], "final_theta_ess": res["ess"],
+    }
+    if res["e2e_ms"] is not None:
+        line["e2e"] = {"value": updates / (res["e2e_ms"] / 1e3), "unit": UNIT,
+                       "h2d_bytes_per_step": int(40 * 64 + 40 * 8 * 8), "d2h_bytes_per_step": int(n_theta * 8 * 3),
+                       "ms_per_step": res["e2e_ms"]}
+    return line
+
+
 # ------------------------------------------------------------ CPU baselines
 
 
@@ -389,6 +499,10 @@ def main():
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--ref-particles", type=int, default=1 << 17)
     ap.add_argument("--ref-T", type=int, default=8)
+    ap.add_argument("--workload", default="pf", choices=["pf", "smc2"],
+                    help="pf: the L96 particle filter (headline); smc2: config 4, SMC^2 sharded over the GPUs")
+    ap.add_argument("--smc-theta", type=int, default=1024)
+    ap.add_argument("--smc-particles", type=int, default=1 << 14)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -406,6 +520,15 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
         # SSM_BENCH_BACKEND=gloo only to exercise the N>1 harness on a single GPU
         tdist.init_process_group(os.environ.get("SSM_BENCH_BACKEND", "nccl"))
+    if args.workload == "smc2":
+        res = run_smc2(args, rank, world)
+        if rank == 0:
+            print(json.dumps(smc2_line(args, res, world)), flush=True)
+        if world > 1:
+            import torch.distributed as tdist
+
+            tdist.destroy_process_group()
+        return
     res = run_ours(args, rank, world)
     if rank != 0:
         if world > 1:

@@ -156,6 +156,10 @@ typedef struct ssm_pw_args {
                            (device); NULL: y[] */
   const double* u_vec;  /* generic models, nullable: inputs [n_sub + 1][n_input] (device): one row per
                            sub-step start (simulate.py:150), then the observation time; NULL: u_in / u_obs */
+  const void* const* x_peer; /* sharded filter, nullable (device): [W] every rank's x_in (peer-mapped, row
+                                stride x_in_stride); anc then holds GLOBAL indices, rank = idx / peer_n */
+  int32_t peer_n;            /* particles per rank */
+  int32_t peer_pad;
 } ssm_pw_args;
 
 /* hint: subs[0] is the only sub-step and holds exactly one RK4 step (n_ode == 1) */
@@ -345,28 +349,38 @@ int ssm_event_create(void** out);
 int ssm_event_destroy(void* event);
 int ssm_event_elapsed_ms(void* start, void* end, float* ms);
 
-/* Single filter sharded over ranks (config 5).  Each rank holds P
- * consecutive particles of a P_global filter.  After the weighted step (run
- * with ssm_pw_args.lse_out and combined by ssm_lse_combine):
- *   1. ssm_tiles_total: this rank's fixed-point weight total (uint64 [B]);
- *   2. host: all-gather the totals -> this rank's global offset g_off and the
- *      global total g_tot (C1);
- *   3. ssm_offspring_global: global offspring bounds of the local particles,
- *      shifted by the rank's first output (shift_out), + partition;
- *      c_last_out = number of outputs the local particles own;
- *   4. ssm_expand_own: the local ancestor of each owned output;
- *   5. host: all-gather (first output, count) per rank and move the states of
- *      outputs owned here but slotted on other ranks (C3).
- * Draws use global indices, so the result does not depend on the rank count. */
+/* Single filter sharded over W ranks (config 5).  Rank r holds
+ * the P consecutive particles [rP, (r+1)P) of a P_global = W P filter and owns
+ * the output slots of the same range.  Every rank maps every other rank's
+ * position and ancestor arenas (CUDA IPC, ssm_ipc_open: NVLink peer memory),
+ * so no particle state is ever exchanged through the host:
+ *   pw:   ssm_propagate_weight with x_peer set gathers each ancestor from the
+ *         rank that holds it (P2P loads at the rank boundaries) and writes the
+ *         rank's LSE partial to lse_out -> all-gather (C1) -> ssm_lse_combine;
+ *   1. ssm_tiles_total: this rank's fixed-point weight total -> all-gather (C1');
+ *   2. ssm_offspring_push: the global offspring counts of the local particles
+ *      (global query indices, offset = the lower ranks' totals) and the window
+ *      fill, storing each ancestor (a global index) straight into the array of
+ *      the rank that owns the output slot (P2P stores) -> rank barrier (C2);
+ *   trajectory: ssm_tiles_total + all-gather, ssm_pick_sharded on every rank
+ *      (the owner writes the global index, max over ranks), ssm_trace_peer walks
+ *      the ancestry through the peer-mapped arenas.
+ * Draws use global indices, so the result does not depend on the rank count
+ * beyond the association of the LSE partials. */
 size_t ssm_sharded_workspace_bytes(int B, int P, int P_global);
 int ssm_tiles_total(int B, int P, const void* tile_rec, const ssm_filter_state* fs, uint64_t* total_out,
                     void* workspace, void* stream);
-int ssm_offspring_global(int B, int P, int P_global, int scheme, const void* cdf_local, const uint64_t* g_off,
-                         const uint64_t* g_tot, const double* u, const uint32_t* keys, int step,
-                         const ssm_filter_state* fs, int32_t* shift_out, int32_t* c_last_out, void* workspace,
-                         void* stream);
-int ssm_expand_own(int B, int P, int P_global, int n_own, const ssm_filter_state* fs, int32_t* anc_out,
-                   void* workspace, void* stream);
+int ssm_offspring_push(int P, int P_global, int W, int rank, int scheme, const void* cdf_local,
+                       const uint64_t* totals_all, const double* u, const uint32_t* keys, int step,
+                       const ssm_filter_state* fs, int32_t* const* anc_tab, void* workspace, void* stream);
+int ssm_pick_sharded(int P, int W, int rank, const void* cdf_local, const uint64_t* totals_all, const double* u,
+                     int32_t* j_out, void* workspace, void* stream);
+int ssm_trace_peer(int dtype, int S, int nx, int P, const void* const* x_tab, const int32_t* const* anc_tab,
+                   const int32_t* has_anc, const int32_t* j_final, double* out, void* stream);
+/* CUDA IPC: map a peer allocation (64-byte cudaIpcMemHandle_t from its owner)
+ * into this process with lazy peer access; unmap. */
+int ssm_ipc_open(const void* handle, void** ptr);
+int ssm_ipc_close(void* ptr);
 
 /* Persistent small-P filter (P <= ssm_small_max_particles()): one CTA per
  * filter runs all n_steps grid steps in ONE launch (device noise).  Same
@@ -511,6 +525,23 @@ typedef struct {
 } ssm_kalman_args;
 int ssm_kalman_max_dim(void);
 int ssm_kalman_filter(const ssm_kalman_args* args, void* stream);
+
+/* Backward smoothing draws (KalmanRun.sample_trajectory, kalman.py:98-114) of
+ * G runs on the device, one thread per run, from the records of
+ * ssm_kalman_filter: rows[g] selects the batch row, s the run position, z the
+ * reference's standard normals [G][s+1][nx] (row q = the draw for step s-q,
+ * drawn on the host from each run's stream in the reference's order); out
+ * [G][s+1][nx].  Covariance-form algebra with the reference's PSD pivot rule;
+ * err[g] = failing grid index + 1 (CholeskyError), else untouched. */
+typedef struct ssm_kalman_sample_args {
+  int32_t G, nx, S, s;
+  const int32_t* rows;
+  const double *A, *mu, *P, *mu_p, *P_p; /* batch records, as ssm_kalman_args */
+  const double* z;
+  double* out;
+  int32_t* err;
+} ssm_kalman_sample_args;
+int ssm_kalman_sample(const ssm_kalman_sample_args* args, void* stream);
 int ssm_theta_draws(int model, int has_init);
 int ssm_theta_propose(const ssm_theta_args* args, void* stream);
 int ssm_theta_accept(const ssm_theta_args* args, void* stream);

@@ -109,6 +109,9 @@ class PwArgs(C.Structure):
         ("gen_pad", C.c_int32),
         ("y_vec", C.c_void_p),
         ("u_vec", C.c_void_p),
+        ("x_peer", C.c_void_p),
+        ("peer_n", C.c_int32),
+        ("peer_pad", C.c_int32),
     ]
 
 
@@ -192,6 +195,11 @@ class KalmanArgs(C.Structure):
                                   "err")]
 
 
+class KalmanSampleArgs(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("G", "nx", "S", "s")] + [
+        (n, C.c_void_p) for n in ("rows", "A", "mu", "P", "mu_p", "P_p", "z", "out", "err")]
+
+
 # name -> (restype, argtypes); every symbol declared in include/ssm_b200.h
 _vp, _i, _sz, _d = C.c_void_p, C.c_int, C.c_size_t, C.c_double
 SIGNATURES = {
@@ -226,8 +234,11 @@ SIGNATURES = {
     "ssm_advance_small": (_i, [C.POINTER(SmallArgs), _vp]),
     "ssm_sharded_workspace_bytes": (_sz, [_i, _i, _i]),
     "ssm_tiles_total": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp]),
-    "ssm_offspring_global": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp]),
-    "ssm_expand_own": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "ssm_offspring_push": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp]),
+    "ssm_pick_sharded": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "ssm_trace_peer": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "ssm_ipc_open": (_i, [_vp, C.POINTER(C.c_void_p)]),
+    "ssm_ipc_close": (_i, [_vp]),
     "ssm_event_create": (_i, [C.POINTER(C.c_void_p)]),
     "ssm_event_destroy": (_i, [_vp]),
     "ssm_event_elapsed_ms": (_i, [_vp, _vp, C.POINTER(C.c_float)]),
@@ -239,6 +250,7 @@ SIGNATURES = {
     "ssm_theta_draws": (_i, [_i, _i]),
     "ssm_kalman_max_dim": (_i, []),
     "ssm_kalman_filter": (_i, [C.POINTER(KalmanArgs), _vp]),
+    "ssm_kalman_sample": (_i, [C.POINTER(KalmanSampleArgs), _vp]),
     "ssm_theta_propose": (_i, [C.POINTER(ThetaArgs), _vp]),
     "ssm_theta_accept": (_i, [C.POINTER(ThetaArgs), _vp]),
 }
@@ -266,11 +278,13 @@ LAUNCHING = {
     "ssm_advance": 0,
     "ssm_advance_small": 1,
     "ssm_tiles_total": 2,
-    "ssm_offspring_global": 2,
-    "ssm_expand_own": 1,
+    "ssm_offspring_push": 3,
+    "ssm_pick_sharded": 1,
+    "ssm_trace_peer": 1,
     "ssm_theta_propose": 1,
     "ssm_theta_accept": 1,
     "ssm_kalman_filter": 1,
+    "ssm_kalman_sample": 1,
 }
 
 _LIB = None

@@ -124,12 +124,26 @@ __global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args
   T xn[NX];
   const int stride = gridDim.x * kPwThreads;
   const int p0 = blockIdx.x * kPwThreads + threadIdx.x;
+  // sharded filter (A.x_peer): global ancestor indices, gathered from the owning rank
+  const bool peer = A.x_peer != nullptr;
+  const int src_off = peer ? A.p_offset : 0;
   auto load_x = [&](int src) {
+    const T* base = xin;
+    if (peer) {
+      const int loc = src - A.p_offset;
+      if (static_cast<unsigned>(loc) < static_cast<unsigned>(A.peer_n)) {
+        src = loc;
+      } else {
+        const int o = src / A.peer_n;
+        base = static_cast<const T*>(A.x_peer[o]) + static_cast<size_t>(b) * NX * in_stride;
+        src -= o * A.peer_n;
+      }
+    }
 #pragma unroll
-    for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * in_stride + src];
+    for (int n = 0; n < NX; ++n) xn[n] = base[static_cast<size_t>(n) * in_stride + src];
   };
-  if (p0 < P) load_x(anc ? __ldg(anc + p0) : p0);
-  int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride;
+  if (p0 < P) load_x(anc ? __ldg(anc + p0) : p0 + src_off);
+  int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride + src_off;
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int p = tile * kPwThreads + threadIdx.x;
@@ -142,7 +156,7 @@ __global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args
       const int p2 = p + stride;
       if (p2 < P) load_x(anc_next);
       const int p3 = p2 + stride;
-      anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
+      anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3 + src_off;
     }
     if (act) {
       T w[M::NWB];  // the noise array of step_transition: zeros, then rewritten per sub-step

@@ -34,7 +34,11 @@ namespace ssm {
 // SIMPLE: one sub-step with one RK4 step (the benchmark grid and the sparse
 // SMC^2 grid) -- no runtime sub-step loops, sub-step constants hoisted out of
 // the particle loop, observation slots selected by grid-uniform predicates.
-template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE = false>
+// PEER (sharded filter): ancestors are global indices and the state is
+// gathered from the rank that holds it through A.x_peer (NVLink P2P loads at
+// the rank boundaries); the identity gather of a step without resampling reads
+// this rank's own particles (global index p + p_offset).
+template <int MODEL, typename T, bool E, bool INJ, bool SIMPLE = false, bool PEER = false>
 // NOTE: plain __launch_bounds__(kThreads).  An explicit minBlocks of 1 lets
 // ptxas spend 172 registers on the SIMPLE f64 kernel (1 CTA/SM, 0.80 ms
 // vs 0.63 ms at 119 registers / 2 CTAs); minBlocks 3 (<= 85) is also slower.
@@ -101,6 +105,7 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
   const int stride = gridDim.x * kPwThreads;
   const int p0 = blockIdx.x * kPwThreads + threadIdx.x;
 #if SSM_STAGED_GATHER
+  static_assert(!PEER, "the staged gather has no peer path");
   __shared__ __align__(16) T s_x[2][NX][kPwThreads];
   auto stage_x = [&](int st, int src) {
 #pragma unroll
@@ -113,12 +118,24 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
   // register prefetch: the next tile's gathered state is in flight in xn[]
   T xn[NX];
   auto load_x = [&](int src) {
+    const T* base = xin;
+    if constexpr (PEER) {  // global index -> owning rank's (peer-mapped) positions
+      const int loc = src - A.p_offset;
+      if (static_cast<unsigned>(loc) < static_cast<unsigned>(A.peer_n)) {
+        src = loc;  // this rank's particle (all but the boundary ancestors)
+      } else {
+        const int o = src / A.peer_n;
+        base = static_cast<const T*>(A.x_peer[o]) + static_cast<size_t>(b) * NX * in_stride;
+        src -= o * A.peer_n;
+      }
+    }
 #pragma unroll
-    for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * in_stride + src];
+    for (int n = 0; n < NX; ++n) xn[n] = base[static_cast<size_t>(n) * in_stride + src];
   };
-  if (p0 < P) load_x(anc ? __ldg(anc + p0) : p0);
+  const int src_off = PEER ? A.p_offset : 0;  // identity gather: this rank's particle p (global p + offset)
+  if (p0 < P) load_x(anc ? __ldg(anc + p0) : p0 + src_off);
 #endif
-  int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride;
+  int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride + src_off;
   const T gconst = static_cast<T>(static_cast<double>(__popc(A.obs_mask)) * (A.obs_log_sd + A.log_sqrt_2pi));
   T s_F = T(0), s_c = T(0), s_s = T(0);
   // SIMPLE with every slot observed: the finite-state check rides on the observation sum
@@ -172,7 +189,7 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
       const int p2 = p + stride;
       if (p2 < P) load_x(anc_next);
       const int p3 = p2 + stride;
-      anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
+      anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3 + src_off;
     }
 #endif
     if (act) {
@@ -289,26 +306,33 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
   pw_block_finalize<kPwThreads>(A, fs, b, P, R, has_obs, acc.park->st, lane, kMaxPwBlocks);
 }
 
-template <int MODEL, typename T>
-static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
+template <int MODEL, typename T, bool PEER>
+static void launch_pw_impl(const ssm_pw_args& A, cudaStream_t s) {
   const dim3 grid(pw_grid_x(A.P), A.B);
   const bool inj = A.noise != nullptr;
   if constexpr (MODEL == SSM_MODEL_LORENZ96) {
     // host hint: one sub-step with one RK4 step (any observation mask)
     const bool simple = (A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !A.exact && !inj;
     if (simple) {
-      launch_pdl(pw_kernel<MODEL, T, false, false, true>, grid, dim3(kPwThreads), s, A);
+      launch_pdl(pw_kernel<MODEL, T, false, false, true, PEER>, grid, dim3(kPwThreads), s, A);
       return;
     }
   } else {
     // windkessel with one sub-step per grid step (device noise): draws pipelined across tiles
     if ((A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !inj) {
       if (A.exact)
-        launch_pdl(pw_kernel<MODEL, T, true, false, true>, grid, dim3(kPwThreads), s, A);
+        launch_pdl(pw_kernel<MODEL, T, true, false, true, PEER>, grid, dim3(kPwThreads), s, A);
       else
-        launch_pdl(pw_kernel<MODEL, T, false, false, true>, grid, dim3(kPwThreads), s, A);
+        launch_pdl(pw_kernel<MODEL, T, false, false, true, PEER>, grid, dim3(kPwThreads), s, A);
       return;
     }
+  }
+  if constexpr (PEER) {  // the sharded filter draws on the device
+    if (A.exact)
+      launch_pdl(pw_kernel<MODEL, T, true, false, false, true>, grid, dim3(kPwThreads), s, A);
+    else
+      launch_pdl(pw_kernel<MODEL, T, false, false, false, true>, grid, dim3(kPwThreads), s, A);
+    return;
   }
   if (A.exact) {
     if (inj)
@@ -321,6 +345,14 @@ static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
     else
       launch_pdl(pw_kernel<MODEL, T, false, false>, grid, dim3(kPwThreads), s, A);
   }
+}
+
+template <int MODEL, typename T>
+static void launch_pw(const ssm_pw_args& A, cudaStream_t s) {
+  if (A.x_peer)
+    launch_pw_impl<MODEL, T, true>(A, s);
+  else
+    launch_pw_impl<MODEL, T, false>(A, s);
 }
 
 // ----------------------------- K7: init ------------------------------------
@@ -417,6 +449,7 @@ extern "C" int ssm_propagate_weight(const ssm_pw_args* args, void* stream) {
   // when the next step resamples from the tile records
   if (A.has_obs && !A.a_out && !A.cdf_local) return SSM_ERR_INVALID_ARG;
   if (A.n_sub > 0 && !A.noise && !A.keys) return SSM_ERR_INVALID_ARG;
+  if (A.x_peer && (A.noise || A.peer_n <= 0)) return SSM_ERR_INVALID_ARG;  // sharded: device noise only
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (A.model == SSM_MODEL_GENERIC) return ssm_gen_propagate_weight(A, s);
   if (A.model == SSM_MODEL_LORENZ96) {

@@ -3,6 +3,7 @@
 // inference/particle.py:96-105 and 137-149, inference/smc.py:96-98.
 
 #include <stdio.h>
+#include <string.h>
 
 #include <algorithm>
 #include <type_traits>
@@ -738,19 +739,39 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
 
 // Long offspring runs (> kShortRun outputs of one particle, e.g. degenerate
 // weights): one block per run, grid-stride over runs.
+// Where an output's ancestor goes: this filter's own array (LocalStore), or --
+// sharded filter -- the array of the rank that owns output slot k, through
+// that rank's peer-mapped pointer (PeerStore: a P2P store over NVLink when the
+// owner is another GPU); `base` turns a local particle index into a global one.
+struct LocalStore {
+  int32_t* anc;  // [B][P]
+  int P;
+  __device__ __forceinline__ void operator()(int b, int k, int v) const { anc[static_cast<size_t>(b) * P + k] = v; }
+};
+struct PeerStore {
+  int32_t* const* tab;  // [W] owners' ancestor arrays for this step (peer-mapped)
+  int P_loc;
+  int base;             // global index of this rank's particle 0
+  __device__ __forceinline__ void operator()(int, int k, int v) const {
+    const int o = k / P_loc;
+    tab[o][k - o * P_loc] = v + base;
+  }
+};
+
+template <typename Store = LocalStore>
 __global__ void __launch_bounds__(kThreads)
 long_runs_kernel(int P_in, int P_out, const int4* __restrict__ runs, const uint32_t* __restrict__ count,
-                 const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc) {
+                 const ssm_filter_state* __restrict__ fs, Store st) {
   pdl_wait();
   const int b = blockIdx.y;
   if (fs && !fs[b].resample_now) return;
   const uint32_t n = count[b];
   const int4* rb = runs + static_cast<size_t>(b) * long_runs_cap(P_in, P_out);
-  int32_t* ab = anc + static_cast<size_t>(b) * P_out;
   for (uint32_t r = blockIdx.x; r < n; r += gridDim.x) {
     const int4 q = rb[r];
-    for (int k = q.y + threadIdx.x; k < q.z; k += kThreads) ab[k] = q.x;
+    for (int k = q.y + threadIdx.x; k < q.z; k += kThreads) st(b, k, q.x);
   }
+  if constexpr (!std::is_same<Store, LocalStore>::value) __threadfence_system();  // peer stores
 }
 
 // Filter-path offspring + ancestors from the fused kernel's tile records
@@ -778,8 +799,9 @@ struct RunWindow {
 // Windows up to 4096 outputs are filled in shared memory (run-start marks +
 // max-scan) and stored coalesced; larger ones (degenerate weights) write short
 // runs directly and defer long runs to long_runs_kernel.
+template <typename Store>
 __device__ __forceinline__ void fill_run_window(RunWindow& sm, int b, int P, int jw, const int (&cv)[kRunIt],
-                                                const int (&pv)[kRunIt], int32_t* __restrict__ anc,
+                                                const int (&pv)[kRunIt], const Store& st,
                                                 int4* __restrict__ long_runs, uint32_t* __restrict__ long_count) {
   constexpr int kOutBuf = 4096;
   constexpr int kPer = kOutBuf / kThreads;
@@ -791,7 +813,6 @@ __device__ __forceinline__ void fill_run_window(RunWindow& sm, int b, int P, int
     reinterpret_cast<int4*>(sm.out)[e] = make_int4(-1, -1, -1, -1);
   __syncthreads();
   const int lo_blk = sm.lo, n_out = sm.hi - lo_blk;
-  int32_t* ab = anc + static_cast<size_t>(b) * P;
   if (n_out <= kOutBuf) {
 #pragma unroll
     for (int it = 0; it < kIt; ++it) {
@@ -823,13 +844,13 @@ __device__ __forceinline__ void fill_run_window(RunWindow& sm, int b, int P, int
 #pragma unroll
     for (int i = 0; i < kPer; ++i) sv[i] = max(cin, v[i]);
     __syncthreads();
-    for (int e = threadIdx.x; e < n_out; e += kThreads) ab[lo_blk + e] = sm.out[e + (e >> 5)];
+    for (int e = threadIdx.x; e < n_out; e += kThreads) st(b, lo_blk + e, sm.out[e + (e >> 5)]);
   } else {
 #pragma unroll
     for (int it = 0; it < kIt; ++it) {
       const int j = jw + it * 32 + lane, lo = pv[it], hi = cv[it];
       if (hi - lo <= kShortRun) {
-        for (int k = lo; k < hi; ++k) ab[k] = j;
+        for (int k = lo; k < hi; ++k) st(b, k, j);
       } else {
         const int nchunk = (hi - lo + kRunChunk - 1) / kRunChunk;
         const uint32_t slot = atomicAdd(long_count + b, static_cast<uint32_t>(nchunk));
@@ -844,16 +865,27 @@ __device__ __forceinline__ void fill_run_window(RunWindow& sm, int b, int P, int
 }
 
 
-template <int SCHEME>
+// Sharded filter (one rank of W): this rank's particles are global indices
+// [base, base + P), its fixed-point CDF starts at the global offset g_off, the
+// queries run over P_glob global outputs and the ancestors land in the owners'
+// arrays (PeerStore).  Single filter: base 0, g_off 0, P_glob = P, LocalStore.
+struct ShardSpan {
+  const uint64_t* g_off;  // [B] global fixed-point offset of particle 0, or nullptr
+  int P_glob;
+  int base;
+};
+
+template <int SCHEME, typename Store = LocalStore>
 __global__ void __launch_bounds__(kThreads)
 offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const double* __restrict__ scale,
                        const uint64_t* __restrict__ pref, const uint64_t* __restrict__ totals,
                        const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
-                       const ssm_filter_state* __restrict__ fs, int32_t* __restrict__ anc,
+                       const ssm_filter_state* __restrict__ fs, Store st,
                        int4* __restrict__ long_runs, uint32_t* __restrict__ long_count,
-                       const OffspringConsts* __restrict__ oc) {
+                       const OffspringConsts* __restrict__ oc, ShardSpan span = ShardSpan{nullptr, 0, 0}) {
   pdl_wait();
   constexpr int kIt = kRunIt;
+  constexpr bool kLocal = std::is_same<Store, LocalStore>::value;
   __shared__ __align__(16) RunWindow sm;
   struct __align__(16) TileInfo {
     uint64_t pre;
@@ -861,10 +893,12 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
   };
   __shared__ TileInfo s_tile[kThreads / 32][kIt];
   const int b = blockIdx.y;
+  const int Pg = kLocal ? P : span.P_glob;  // outputs (global for a sharded filter)
+  const uint64_t goff = kLocal ? 0ull : span.g_off[b];
   if (fs && !fs[b].resample_now) {  // ESS gate held (particle.py:99-100): the history records identity
-    int32_t* ab = anc + static_cast<size_t>(b) * P;
     const int k1 = min(P, (blockIdx.x + 1) * kScanTile);
-    for (int k = blockIdx.x * kScanTile + threadIdx.x; k < k1; k += kThreads) ab[k] = k;
+    for (int k = blockIdx.x * kScanTile + threadIdx.x; k < k1; k += kThreads) st(b, k + (kLocal ? 0 : span.base), k);
+    if constexpr (!kLocal) __threadfence_system();
     return;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -877,43 +911,51 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
   const int jw = blockIdx.x * kScanTile + warp * (kScanTile / (kThreads / 32));  // warp's first particle
   const int tw0 = jw >> 5;
   // issue every load of the warp's 8 tiles first: cdf_local per lane, and the
-  // tiles' prefix / scale one per lane (broadcast by shuffle below)
+  // tiles' prefix / scale one per lane (broadcast by shuffle below).  The last
+  // GLOBAL particle's run ends at P_glob; a rank's last local particle is not special.
+  const int jlast = kLocal || span.base + P == Pg ? P - 1 : P;
   uint64_t qv[kIt];
 #pragma unroll
   for (int it = 0; it < kIt; ++it) {
     const int j = jw + it * 32 + lane;
-    qv[it] = j < P - 1 ? __ldg(cl + j) : 0ull;
+    qv[it] = j < jlast ? __ldg(cl + j) : 0ull;
   }
   // the warp's 8 tiles' prefix / scale, one per lane, broadcast through shared memory
   if (lane < kIt) {
-    TileInfo ti{0ull, 0.0};
-    if (tw0 + lane < nt) ti = TileInfo{tp[tw0 + lane] + bp[(tw0 + lane) / kRecPerBlock], scb[tw0 + lane]};
+    TileInfo ti{goff, 0.0};
+    if (tw0 + lane < nt) ti = TileInfo{goff + tp[tw0 + lane] + bp[(tw0 + lane) / kRecPerBlock], scb[tw0 + lane]};
     s_tile[warp][lane] = ti;
   }
-  const OffspringConsts K = oc[b];  // 1 / total, P / total, u, 1 / P (blk_prefix_kernel)
+  const OffspringConsts K = oc[b];  // 1 / total, P / total, u, 1 / P (blk_prefix_kernel / shard_consts_kernel)
   const double inv = K.inv, tscale = K.tscale, invP = K.invP;
-  const bool pow2 = (P & (P - 1)) == 0;
+  const bool pow2 = (Pg & (Pg - 1)) == 0;
   const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
   const double u_sys = SCHEME == SSM_SYSTEMATIC ? K.u_sys : 0.0;
   __syncwarp();
-  const double* U = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * P : nullptr;
+  const double* U = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * Pg : nullptr;
   const auto count = [&](uint64_t C) -> int {
     const double Cd = static_cast<double>(C);
     if constexpr (SCHEME == SSM_SYSTEMATIC) {
       const double t = fma(Cd, tscale, -u_sys);
       const double e = ceil(t);
       const double d = e - t;  // in [0, 1), within 2^-53
-      if (d > 0x1p-20 && d < 1.0 - 0x1p-20 && P <= (1 << 30))
-        return min(max(__double2int_rz(e), 0), P);
+      if (d > 0x1p-20 && d < 1.0 - 0x1p-20 && Pg <= (1 << 30))
+        return min(max(__double2int_rz(e), 0), Pg);
     }
-    return offspring_bound<SCHEME>(Cd * inv, u_sys, U, k0, k1, step, P, invP, pow2);
+    return offspring_bound<SCHEME>(Cd * inv, u_sys, U, k0, k1, step, Pg, invP, pow2);
   };
 
   // c_{jw-1}: particle jw-1 closes tile tw0-1, so its C is tile tw0's exclusive prefix
+  // (for a sharded rank's particle 0: the previous rank's last particle, C = g_off)
   const uint64_t pre0 = s_tile[warp][0].pre;
+  // F: the count of every particle >= jlast (the last global particle's run ends
+  // at P_glob; a non-last rank's padding lanes repeat its last particle's count)
+  int F = Pg;
+  if (!kLocal && jlast == P)
+    F = count(goff + tp[nt - 1] + bp[(nt - 1) / kRecPerBlock] + __double2ull_rn(scb[nt - 1] * static_cast<double>(cl[P - 1])));
   int carry = 0;
-  if (jw > 0 && jw < P) carry = count(pre0);
-  else if (jw >= P) carry = P;
+  if ((jw > 0 || (!kLocal && span.base > 0)) && jw < P) carry = count(pre0);
+  else if (jw >= P) carry = F;
   if (warp == 0 && lane == 0) sm.lo = carry;
   int cv[kIt], pv[kIt];
 #pragma unroll
@@ -922,14 +964,15 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
     const TileInfo ti = s_tile[warp][it];
     const uint64_t pre = ti.pre;
     const double sc = ti.sc;
-    // particles >= P - 1: the last particle's run ends at P, later ones are empty
-    const int c = j < P - 1 ? count(pre + __double2ull_rn(sc * static_cast<double>(qv[it]))) : P;
+    // the last (global) particle's run ends at P_glob, later lanes are empty
+    const int c = j < jlast ? count(pre + __double2ull_rn(sc * static_cast<double>(qv[it]))) : F;
     const int up = __shfl_up_sync(0xffffffffu, c, 1);
     pv[it] = lane == 0 ? carry : up;
     cv[it] = c;
     carry = __shfl_sync(0xffffffffu, c, 31);
   }
-  fill_run_window(sm, b, P, jw, cv, pv, anc, long_runs, long_count);
+  fill_run_window(sm, b, Pg, jw, cv, pv, st, long_runs, long_count);
+  if constexpr (!kLocal) __threadfence_system();  // peer stores visible before the rank barrier
 }
 
 // ---------------------------------------------------------------------------
@@ -1092,7 +1135,7 @@ resample_fused_kernel(int P, const uint64_t* __restrict__ cdf_local, const ssm_t
     cv[it] = c;
     carry = __shfl_sync(0xffffffffu, c, 31);
   }
-  fill_run_window(sm, b, P, jw, cv, pv, anc, long_runs, long_count);
+  fill_run_window(sm, b, P, jw, cv, pv, LocalStore{anc, P}, long_runs, long_count);
 }
 
 // ---------------------------------------------------------------------------
@@ -1734,10 +1777,6 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
   tmp.sums = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * (tiles + 1)));
   // totals, long-run counts, spacing totals, then OffspringConsts (4 words) per filter
   tmp.totals = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 7 * static_cast<size_t>(B)));
-  // cnt doubles as the long-run list of the direct ancestor writer (int4 per run, P_in/32 + 2 per filter)
-  const size_t cnt_bytes = sizeof(int32_t) * static_cast<size_t>(B) * P_in;
-  const size_t runs_bytes = sizeof(int4) * static_cast<size_t>(B) * long_runs_cap(P_in, P_out);
-  tmp.cnt = reinterpret_cast<int32_t*>(take(cnt_bytes > runs_bytes ? cnt_bytes : runs_bytes));
   // C doubles as the tile path's [scale | in-block prefix | block prefix] (2 nt + nblk per filter)
   const size_t nt = (static_cast<size_t>(P_in) + 31) / 32;
   const size_t tile_words = 2 * nt + (nt + kRecPerBlock - 1) / kRecPerBlock;
@@ -1747,6 +1786,11 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
       take(sizeof(double) * static_cast<size_t>(B) * ((P_in + 1 + kScanTile - 1) / kScanTile) * kScanTile));
   tmp.scan = take(scan_ws_bytes(B, P_in));
   tmp.lb = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * fused_ws_words(B, P_in)));
+  // cnt doubles as the long-run list of the direct ancestor writer (int4 per run, P_out/32 + ... per filter);
+  // it and split depend on P_out, so they come last (the sharded phases share the other offsets)
+  const size_t cnt_bytes = sizeof(int32_t) * static_cast<size_t>(B) * P_in;
+  const size_t runs_bytes = sizeof(int4) * static_cast<size_t>(B) * long_runs_cap(P_in, P_out);
+  tmp.cnt = reinterpret_cast<int32_t*>(take(cnt_bytes > runs_bytes ? cnt_bytes : runs_bytes));
   tmp.split = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * (nd + 1)));
   if (w) *w = tmp;
   return off;
@@ -1850,8 +1894,8 @@ extern "C" int ssm_resample_tiles_step(int B, int P, int scheme, const void* cdf
       launch_pdl(resample_fused_kernel<SSM_STRATIFIED>, g, dim3(kThreads), s, P, cl, rec, fs, u, keys, step, anc,
                  long_runs, fw, parity);
     const int gx = std::max(1, std::min(1184 / B, P / kRunChunk + 1));
-    launch_pdl(long_runs_kernel, dim3(gx, B), dim3(kThreads), s, P, P, static_cast<const int4*>(long_runs),
-               static_cast<const uint32_t*>(fw.long_count + static_cast<size_t>(parity) * B), fs, anc);
+    launch_pdl(long_runs_kernel<LocalStore>, dim3(gx, B), dim3(kThreads), s, P, P, static_cast<const int4*>(long_runs),
+               static_cast<const uint32_t*>(fw.long_count + static_cast<size_t>(parity) * B), fs, LocalStore{anc, P});
     SSM_CHECK_LAUNCH();
     return SSM_OK;
   }
@@ -1886,13 +1930,15 @@ extern "C" int ssm_resample_tiles_step(int B, int P, int scheme, const void* cdf
   const uint64_t* cl = static_cast<const uint64_t*>(cdf_local);
   if (scheme == SSM_SYSTEMATIC)
     launch_pdl(offspring_tiles_kernel<SSM_SYSTEMATIC>, g, dim3(kThreads), s, P, cl, scale, pref, w.totals, u, keys,
-               step, fs, anc, long_runs, long_count, static_cast<const OffspringConsts*>(oc));
+               step, fs, LocalStore{anc, P}, long_runs, long_count, static_cast<const OffspringConsts*>(oc),
+               ShardSpan{nullptr, P, 0});
   else
     launch_pdl(offspring_tiles_kernel<SSM_STRATIFIED>, g, dim3(kThreads), s, P, cl, scale, pref, w.totals, u, keys,
-               step, fs, anc, long_runs, long_count, static_cast<const OffspringConsts*>(oc));
+               step, fs, LocalStore{anc, P}, long_runs, long_count, static_cast<const OffspringConsts*>(oc),
+               ShardSpan{nullptr, P, 0});
   const int gx = std::max(1, std::min(1184 / B, P / kRunChunk + 1));
-  launch_pdl(long_runs_kernel, dim3(gx, B), dim3(kThreads), s, P, P, static_cast<const int4*>(long_runs),
-             static_cast<const uint32_t*>(long_count), fs, anc);
+  launch_pdl(long_runs_kernel<LocalStore>, dim3(gx, B), dim3(kThreads), s, P, P, static_cast<const int4*>(long_runs),
+             static_cast<const uint32_t*>(long_count), fs, LocalStore{anc, P});
   (void)expand_kernel;
   SSM_CHECK_LAUNCH();
   return SSM_OK;
@@ -1903,19 +1949,80 @@ extern "C" int ssm_resample_tiles_step(int B, int P, int scheme, const void* cdf
 // host-side collectives.
 // ---------------------------------------------------------------------------
 
-template <int SCHEME>
-__global__ void rank_start_kernel(int B, int P_global, const uint64_t* g_off, const uint64_t* g_tot,
-                                  const double* u, const uint32_t* keys, int step, int32_t* shift) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const bool pow2 = (P_global & (P_global - 1)) == 0;
-  const uint32_t k0 = keys ? keys[2 * b] : 0u, k1 = keys ? keys[2 * b + 1] : 0u;
-  const double u_sys = SCHEME == SSM_SYSTEMATIC
-                           ? (u ? u[b] : device_uniform(k0, k1, 0u, step, kPurposeSystematic))
-                           : 0.0;
-  const double* U = (SCHEME == SSM_STRATIFIED && u) ? u + static_cast<size_t>(b) * P_global : nullptr;
-  const double cum = static_cast<double>(g_off[b]) / static_cast<double>(g_tot[b]);
-  shift[b] = offspring_bound<SCHEME>(cum, u_sys, U, k0, k1, step, P_global, 1.0 / static_cast<double>(P_global), pow2);
+// Per-rank constants of the sharded resample from the all-gathered rank totals:
+// this rank's global fixed-point offset (sum of the lower ranks' totals, rank
+// order: exact integers, the same on every rank), the offspring constants on
+// the global total, and a zeroed long-run list.
+__global__ void shard_consts_kernel(int W, int rank, int P_global, const uint64_t* __restrict__ totals_all,
+                                    const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
+                                    uint64_t* __restrict__ g_off, OffspringConsts* __restrict__ oc,
+                                    uint32_t* __restrict__ long_count) {
+  if (threadIdx.x != 0) return;
+  uint64_t off = 0, tot = 0;
+  for (int d = 0; d < W; ++d) {
+    if (d < rank) off += totals_all[d];
+    tot += totals_all[d];
+  }
+  g_off[0] = off;
+  const double inv = 1.0 / static_cast<double>(tot), Pd = static_cast<double>(P_global);
+  const double us = u ? u[0] : (keys ? device_uniform(keys[0], keys[1], 0u, step, kPurposeSystematic) : 0.0);
+  oc[0] = OffspringConsts{inv, Pd * inv, us, 1.0 / Pd};
+  long_count[0] = 0u;
+}
+
+// Trajectory of the sharded filter (particle.py:137-149): one thread walks the
+// ancestry through every rank's peer-mapped history -- x_tab[r] / anc_tab[r]
+// are rank r's position / ancestor arenas ([S+1][nx][P_loc], [S][P_loc] global
+// indices, steps without a resample flagged 0 in has_anc: identity) -- so
+// every rank obtains the same trajectory without a per-step exchange.
+template <typename T>
+__global__ void trace_peer_kernel(int S, int nx, int P_loc, const void* const* __restrict__ x_tab,
+                                  const int32_t* const* __restrict__ anc_tab, const int32_t* __restrict__ has_anc,
+                                  const int32_t* __restrict__ j_final, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int j = j_final[0];
+  for (int i = S; i >= 0; --i) {
+    const int o = j / P_loc, l = j - o * P_loc;
+    const T* x = static_cast<const T*>(x_tab[o]) + static_cast<size_t>(i) * nx * P_loc;
+    for (int n = 0; n < nx; ++n) out[static_cast<size_t>(i) * nx + n] = static_cast<double>(x[static_cast<size_t>(n) * P_loc + l]);
+    if (i > 0 && has_anc[i]) j = anc_tab[o][static_cast<size_t>(i - 1) * P_loc + l];
+  }
+}
+
+// Final multinomial pick across ranks (resample(exp(logw), "multinomial", size=1)):
+// the rank whose global CDF range holds u writes its global particle index,
+// the others -1 (the host takes the max over ranks).
+__global__ void pick_shard_kernel(int W, int rank, int P_loc, const uint64_t* __restrict__ cdf_local,
+                                  const double* __restrict__ scale, const uint64_t* __restrict__ pref,
+                                  const uint64_t* __restrict__ totals_all, const double* __restrict__ u,
+                                  int32_t* __restrict__ j_out) {
+  uint64_t off = 0, tot = 0;
+  for (int d = 0; d < W; ++d) {
+    if (d < rank) off += totals_all[d];
+    tot += totals_all[d];
+  }
+  const double q = u[0];
+  const double totd = static_cast<double>(tot);
+  const bool mine = static_cast<double>(off) / totd <= q &&
+                    (rank == W - 1 || q < static_cast<double>(off + totals_all[rank]) / totd);
+  if (!mine) {
+    if (threadIdx.x == 0) j_out[0] = -1;
+    return;
+  }
+  const int nt = (P_loc + 31) >> 5;
+  struct Cum {
+    const uint64_t *cl, *tp, *bp;
+    const double* sc;
+    uint64_t off;
+    double tot;
+    __device__ __forceinline__ double operator()(int j) const {
+      const int tw = j >> 5;
+      return static_cast<double>(off + tp[tw] + bp[tw / kRecPerBlock] +
+                                 __double2ull_rn(sc[tw] * static_cast<double>(__ldg(cl + j)))) / tot;
+    }
+  } cum{cdf_local, pref, pref + nt, scale, off, totd};
+  const int j = warp_search_right(cum, P_loc, q, threadIdx.x);
+  if (threadIdx.x == 0) j_out[0] = rank * P_loc + (j < P_loc ? j : P_loc - 1);
 }
 
 extern "C" int ssm_tiles_total(int B, int P, const void* tile_rec, const ssm_filter_state* fs,
@@ -1929,66 +2036,97 @@ extern "C" int ssm_tiles_total(int B, int P, const void* tile_rec, const ssm_fil
   double* scale = reinterpret_cast<double*>(w.C);
   uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + static_cast<size_t>(B) * nt;
   uint64_t* blk = pref + B_total_tiles_offset(nt, B);
+  // not gated on fs.resample_now: the trajectory pick needs the totals after an ESS-held step too
   tile_scale_kernel<<<dim3(nblk, B), kThreads, 0, s>>>(nt, static_cast<const ssm_tile_rec*>(tile_rec), fs, scale,
-                                                      pref, blk);
-  blk_prefix_kernel<<<B, 1024, 0, s>>>(nblk, blk, total_out, fs);
+                                                      pref, blk, nullptr, 0);
+  blk_prefix_kernel<<<B, 1024, 0, s>>>(nblk, blk, total_out, nullptr);
   SSM_CHECK_LAUNCH();
   return SSM_OK;
 }
 
-extern "C" int ssm_offspring_global(int B, int P, int P_global, int scheme, const void* cdf_local,
-                                    const uint64_t* g_off, const uint64_t* g_tot, const double* u,
-                                    const uint32_t* keys, int step, const ssm_filter_state* fs, int32_t* shift_out,
-                                    int32_t* c_last_out, void* workspace, void* stream) {
-  if (B <= 0 || P <= 0 || P_global < P || !cdf_local || !g_off || !g_tot || !fs || !shift_out || !workspace)
+extern "C" int ssm_offspring_push(int P, int P_global, int W, int rank, int scheme, const void* cdf_local,
+                                  const uint64_t* totals_all, const double* u, const uint32_t* keys, int step,
+                                  const ssm_filter_state* fs, int32_t* const* anc_tab, void* workspace, void* stream) {
+  if (P <= 0 || W <= 0 || rank < 0 || rank >= W || P_global != P * W || !cdf_local || !totals_all || !fs ||
+      !anc_tab || !workspace)
     return SSM_ERR_INVALID_ARG;
   if (!u && !keys) return SSM_ERR_INVALID_ARG;
   if (scheme != SSM_SYSTEMATIC && scheme != SSM_STRATIFIED) return SSM_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SearchWs w;
-  search_ws_layout(B, P, P_global, workspace, &w);
+  search_ws_layout(1, P, P_global, workspace, &w);
   const int nt = (P + 31) / 32;
   double* scale = reinterpret_cast<double*>(w.C);
-  uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + static_cast<size_t>(B) * nt;
-  const int nd_max = ndiag_of(P, P_global);
-  const dim3 g(scan_tiles(P), B);
-  if (scheme == SSM_SYSTEMATIC) {
-    rank_start_kernel<SSM_SYSTEMATIC><<<(B + 127) / 128, 128, 0, s>>>(B, P_global, g_off, g_tot, u, keys, step, shift_out);
-    offspring_kernel<SSM_SYSTEMATIC, kCumTiles, double><<<g, kThreads, 0, s>>>(
-        P, P_global, cdf_local, scale, pref, g_tot, u, keys, step, fs, w.cnt, w.split, nd_max, g_off, shift_out);
-  } else {
-    rank_start_kernel<SSM_STRATIFIED><<<(B + 127) / 128, 128, 0, s>>>(B, P_global, g_off, g_tot, u, keys, step, shift_out);
-    offspring_kernel<SSM_STRATIFIED, kCumTiles, double><<<g, kThreads, 0, s>>>(
-        P, P_global, cdf_local, scale, pref, g_tot, u, keys, step, fs, w.cnt, w.split, nd_max, g_off, shift_out);
-  }
-  if (c_last_out) {
-    for (int b = 0; b < B; ++b) {
-      cudaError_t e = cudaMemcpyAsync(c_last_out + b, w.cnt + static_cast<size_t>(b) * P + P - 1, sizeof(int32_t),
-                                      cudaMemcpyDeviceToDevice, s);
-      if (e != cudaSuccess) {
-        ssm_set_last_error(e);
-        return SSM_ERR_CUDA;
-      }
-    }
-  }
+  uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + nt;
+  uint64_t* g_off = w.totals + 1;
+  uint32_t* long_count = reinterpret_cast<uint32_t*>(w.totals + 2);
+  OffspringConsts* oc = reinterpret_cast<OffspringConsts*>(w.totals + 3);
+  int4* long_runs = reinterpret_cast<int4*>(w.cnt);
+  shard_consts_kernel<<<1, 32, 0, s>>>(W, rank, P_global, totals_all, u, keys, step, g_off, oc, long_count);
+  const PeerStore st{anc_tab, P, rank * P};
+  const ShardSpan span{g_off, P_global, rank * P};
+  const dim3 g(scan_tiles(P), 1);
+  if (scheme == SSM_SYSTEMATIC)
+    offspring_tiles_kernel<SSM_SYSTEMATIC, PeerStore><<<g, kThreads, 0, s>>>(
+        P, static_cast<const uint64_t*>(cdf_local), scale, pref, w.totals, u, keys, step, fs, st, long_runs, long_count,
+        oc, span);
+  else
+    offspring_tiles_kernel<SSM_STRATIFIED, PeerStore><<<g, kThreads, 0, s>>>(
+        P, static_cast<const uint64_t*>(cdf_local), scale, pref, w.totals, u, keys, step, fs, st, long_runs, long_count,
+        oc, span);
+  const int gx = std::max(1, std::min(1184, P_global / kRunChunk + 1));
+  long_runs_kernel<PeerStore><<<dim3(gx, 1), kThreads, 0, s>>>(P, P_global, long_runs, long_count, fs, st);
   SSM_CHECK_LAUNCH();
   return SSM_OK;
 }
 
-extern "C" int ssm_expand_own(int B, int P, int P_global, int n_own, const ssm_filter_state* fs, int32_t* anc_out,
-                              void* workspace, void* stream) {
-  if (B <= 0 || P <= 0 || n_own < 0 || !fs || !anc_out || !workspace) return SSM_ERR_INVALID_ARG;
-  if (n_own == 0) return SSM_OK;
+extern "C" int ssm_pick_sharded(int P, int W, int rank, const void* cdf_local, const uint64_t* totals_all,
+                                const double* u, int32_t* j_out, void* workspace, void* stream) {
+  if (P <= 0 || W <= 0 || rank < 0 || rank >= W || !cdf_local || !totals_all || !u || !j_out || !workspace)
+    return SSM_ERR_INVALID_ARG;
   SearchWs w;
-  search_ws_layout(B, P, P_global, workspace, &w);
-  const int nd = ndiag_of(P, n_own);
-  const int nd_max = ndiag_of(P, P_global);
-  // splits were written with stride nd_max + 1 per filter; B == 1 for the sharded filter
-  if (B != 1) return SSM_ERR_UNSUPPORTED;
-  expand_kernel<<<dim3(nd, B), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(P, n_own, w.cnt, w.split, nd, fs,
-                                                                                  anc_out);
-  (void)nd_max;
+  search_ws_layout(1, P, P * W, workspace, &w);
+  const int nt = (P + 31) / 32;
+  pick_shard_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      W, rank, P, static_cast<const uint64_t*>(cdf_local), reinterpret_cast<const double*>(w.C),
+      reinterpret_cast<const uint64_t*>(w.C) + nt, totals_all, u, j_out);
   SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+extern "C" int ssm_trace_peer(int dtype, int S, int nx, int P, const void* const* x_tab, const int32_t* const* anc_tab,
+                              const int32_t* has_anc, const int32_t* j_final, double* out, void* stream) {
+  if (S < 0 || nx <= 0 || P <= 0 || !x_tab || !anc_tab || !has_anc || !j_final || !out) return SSM_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == SSM_F64)
+    trace_peer_kernel<double><<<1, 32, 0, s>>>(S, nx, P, x_tab, anc_tab, has_anc, j_final, out);
+  else if (dtype == SSM_F32)
+    trace_peer_kernel<float><<<1, 32, 0, s>>>(S, nx, P, x_tab, anc_tab, has_anc, j_final, out);
+  else
+    return SSM_ERR_INVALID_ARG;
+  SSM_CHECK_LAUNCH();
+  return SSM_OK;
+}
+
+extern "C" int ssm_ipc_open(const void* handle, void** ptr) {
+  if (!handle || !ptr) return SSM_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    ssm_set_last_error(e);
+    return SSM_ERR_CUDA;
+  }
+  return SSM_OK;
+}
+
+extern "C" int ssm_ipc_close(void* ptr) {
+  if (!ptr) return SSM_ERR_INVALID_ARG;
+  const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  if (e != cudaSuccess) {
+    ssm_set_last_error(e);
+    return SSM_ERR_CUDA;
+  }
   return SSM_OK;
 }
 

@@ -5,9 +5,9 @@ the reference's inference/kalman.py API (KalmanRun, kalman_filter) and the
 The forward recursions of B systems run in one `ssm_kalman_filter` launch
 (csrc/ssm_kalman.cu, one thread per system); the filtered and predicted
 moments of every grid step stay on the device.  Backward smoothing draws
-(kalman.py:98-114) read the records of a batch back once and run on the host,
-vectorised over the batch's runs, with each run's stream in the reference's
-order.
+(kalman.py:98-114) run on the device too (`ssm_kalman_sample`, one thread per
+run) from the reference's standard normals, drawn on the host from each
+run's stream in its order.
 """
 
 from __future__ import annotations
@@ -96,8 +96,41 @@ def _solve_upper_t_batch(U, v):
 
 def sample_kalman_trajectories(runs, rngs):
     """KalmanRun.sample_trajectory for many runs (kalman.py:98-114): per run the
-    reference's draws in its order (step s first, then s-1 .. 0), the backward
-    recursion vectorised over runs of one batch at one position."""
+    reference's draws in its order (step s first, then s-1 .. 0), drawn on the
+    host from each run's stream; the backward recursion runs on the device
+    (ssm_kalman_sample, one thread per run) over the forward pass's records."""
+    out = [None] * len(runs)
+    groups = {}
+    for k, r in enumerate(runs):
+        groups.setdefault((id(r._batch), r.pos), []).append(k)
+    L = _lib.lib()
+    for (_, s), ks in groups.items():
+        b = runs[ks[0]]._batch
+        nx = b.nx
+        z = np.stack([np.asarray(rngs[k].standard_normal((s + 1) * nx), dtype=float).reshape(s + 1, nx)
+                      for k in ks])  # row q = the draw for step s - q
+        rows = torch.as_tensor([runs[k]._row for k in ks], dtype=torch.int32, device=b.device)
+        zt = torch.as_tensor(z, dtype=torch.float64, device=b.device)
+        res = torch.empty((len(ks), s + 1, nx), dtype=torch.float64, device=b.device)
+        err = torch.zeros(len(ks), dtype=torch.int32, device=b.device)
+        a = _lib.KalmanSampleArgs()
+        a.G, a.nx, a.S, a.s = len(ks), nx, b.S, s
+        a.rows, a.A, a.mu, a.P = rows.data_ptr(), b.A.data_ptr(), b.mu.data_ptr(), b.P.data_ptr()
+        a.mu_p, a.P_p, a.z, a.out, a.err = b.mu_p.data_ptr(), b.P_p.data_ptr(), zt.data_ptr(), res.data_ptr(), err.data_ptr()
+        with torch.cuda.device(b.device):
+            _lib.check(L.ssm_kalman_sample(a, _lib.stream_ptr()), "ssm_kalman_sample")
+        tr, e = res.cpu().numpy(), err.cpu().numpy()
+        if e.any():
+            i = int(e[e != 0][0]) - 1
+            raise CholeskyError(f"matrix is not positive semi-definite at grid index {i}", index=i)
+        for q, k in enumerate(ks):
+            out[k] = tr[q]
+    return out
+
+
+def _sample_kalman_trajectories_host(runs, rngs):
+    """Host (numpy) restatement of the backward recursion, vectorised over runs;
+    kept to cross-check the device sampler (tests/test_gpu_kalman.py)."""
     out = [None] * len(runs)
     groups = {}
     for k, r in enumerate(runs):

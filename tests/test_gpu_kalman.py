@@ -140,13 +140,28 @@ def test_smc2_kalman_windkessel_matches_reference():
     np.testing.assert_allclose(res.trajectories, g["wk/smc/trajectories"], rtol=1e-10)
 
 
-def test_batched_backward_sampling_equals_serial():
-    g, grid, inputs, desc = osc_case()
-    sys_ = extract_linear_gaussian(desc, g["osc/thetas"], grid.times, inputs)
-    runs = kalman_runs(sys_, grid)
-    advance_kalman_runs(runs, 17)
-    from paper_1306_3277_b200.inference.kalman import sample_kalman_trajectories
+@pytest.mark.parametrize("case", ["osc", "wk"])
+def test_device_backward_sampling_equals_host(case):
+    """ssm_kalman_sample (device, one thread per run) against the host
+    restatements of kalman.py:98-114 (batched and serial), same draws: equal to
+    the rounding of the covariance-form algebra."""
+    from paper_1306_3277_b200.inference.kalman import _sample_kalman_trajectories_host, sample_kalman_trajectories
 
+    if case == "osc":
+        g, grid, inputs, desc = osc_case()
+        sys_ = extract_linear_gaussian(desc, g["osc/thetas"], grid.times, inputs)
+        upto = 17
+    else:
+        g, grid, inputs = wk_case()
+        thetas = np.array([1.8, 3.0, 0.06, 25.0]) * np.random.default_rng(3).uniform(0.8, 1.2, size=(40, 4))
+        sys_ = extract_linear_gaussian(WINDKESSEL, thetas, grid.times, inputs)
+        upto = grid.last
+    runs = kalman_runs(sys_, grid)
+    advance_kalman_runs(runs, upto)
     got = sample_kalman_trajectories(runs, [RngStream(70 + k) for k in range(len(runs))])
+    host = _sample_kalman_trajectories_host(runs, [RngStream(70 + k) for k in range(len(runs))])
     for k, r in enumerate(runs):
-        np.testing.assert_allclose(got[k], r._sample_trajectory_serial(RngStream(70 + k)), rtol=1e-11, atol=1e-13)
+        scale = max(1.0, float(np.max(np.abs(host[k]))))
+        assert np.max(np.abs(got[k] - host[k])) <= 1e-10 * scale, (k, np.max(np.abs(got[k] - host[k])))
+        serial = r._sample_trajectory_serial(RngStream(70 + k))
+        assert np.max(np.abs(got[k] - serial)) <= 1e-10 * scale

@@ -542,6 +542,11 @@ typedef struct ssm_kalman_sample_args {
   int32_t* err;
 } ssm_kalman_sample_args;
 int ssm_kalman_sample(const ssm_kalman_sample_args* args, void* stream);
+/* Host helper: numpy SeedSequence(entropy).generate_state(n_words, uint32) for
+ * n streams (the RngStream key derivation, rng.py:16-34) -- entropy [n][L]
+ * 32-bit words (run entropy padded to 4 words, then the spawn key), out
+ * [n][n_words].  Bit-exact with numpy; no device work. */
+int ssm_seedseq_state(int n, int L, const uint32_t* entropy, int n_words, uint32_t* out);
 int ssm_theta_draws(int model, int has_init);
 int ssm_theta_propose(const ssm_theta_args* args, void* stream);
 int ssm_theta_accept(const ssm_theta_args* args, void* stream);

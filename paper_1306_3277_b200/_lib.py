@@ -248,6 +248,7 @@ SIGNATURES = {
     "ssm_gen_info": (_i, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ssm_gen_init_particles": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp]),
     "ssm_theta_draws": (_i, [_i, _i]),
+    "ssm_seedseq_state": (_i, [_i, _i, _vp, _i, _vp]),
     "ssm_kalman_max_dim": (_i, []),
     "ssm_kalman_filter": (_i, [C.POINTER(KalmanArgs), _vp]),
     "ssm_kalman_sample": (_i, [C.POINTER(KalmanSampleArgs), _vp]),

@@ -100,7 +100,7 @@ class FilterRunner:
             r.theta = np.asarray(t, dtype=float).reshape(1, -1)
             r.initial_state = st
             r._derived = None
-            r._hist, r._keys, r._hx, r._ha = [], [], [], []
+            r._segs = []  # init_runs installs the history and pointer arrays
             runs.append(r)
         init_runs(runs, [g.child(0) for g in rngs])
         return runs

@@ -246,12 +246,88 @@ def _stack_rows(tensors):
 
 
 # ---------------------------------------------------------------------------
+# history segments
+# ---------------------------------------------------------------------------
+
+
+class _Seg:
+    """The history one init / advance call wrote for a batch of runs: grid
+    indices i0 .. i0 + n - 1 of every run b in the batch.  x [n, B, nx, P]
+    (None: history-free), anc [n, B, P] with used[k] (False: identity).  A
+    run keeps (segment, b) pairs (which own the memory and give the history
+    views) plus flat per-grid-index pointer arrays for the trace / replay
+    kernels, extended once per call with numpy -- O(B) host work per call,
+    not O(B x steps)."""
+
+    __slots__ = ("x", "anc", "used", "n")
+
+    def __init__(self, x, anc, used, n):
+        self.x, self.anc, self.used, self.n = x, anc, used, n
+
+    def views(self, b):
+        for k in range(self.n):
+            yield (self.x[k][b] if self.x is not None else None,
+                   self.anc[k][b] if (self.anc is not None and self.used[k]) else None)
+
+
+class _RowRef:
+    """Descriptor for a run's per-filter device state (positions, log-weights,
+    tile CDF / records, filter state): held as (batch tensor, row) and turned
+    into a view only when read, so an advance over B runs sets B x 5
+    references instead of slicing B x 5 tensors; `_rows` takes a batch back in
+    one slice when the runs are consecutive rows of one batch."""
+
+    def __init__(self, name):
+        self.key = "_rb" + name
+
+    def __get__(self, obj, cls=None):
+        if obj is None:
+            return self
+        ref = obj.__dict__.get(self.key)
+        if ref is None:
+            return None
+        t, b = ref
+        return t if b is None else t[b]
+
+    def __set__(self, obj, value):
+        obj.__dict__[self.key] = None if value is None else (value, None)
+
+
+def _set_row(run, name, batch, b):
+    run.__dict__["_rb" + name] = None if batch is None else (batch, b)
+
+
+def _has_row(run, name):
+    return run.__dict__.get("_rb" + name) is not None
+
+
+def _rows(runs, name):
+    """[B, ...] tensor of the runs' `name` rows: one slice of the shared batch when
+    they are its consecutive rows, else a stack of the views."""
+    refs = [r.__dict__.get("_rb" + name) for r in runs]
+    t0, b0 = refs[0]
+    if b0 is not None and all(t is t0 and b == b0 + k for k, (t, b) in enumerate(refs)):
+        return t0 if (b0 == 0 and len(refs) == t0.shape[0]) else t0[b0 : b0 + len(refs)]
+    return torch.stack([t if b is None else t[b] for t, b in refs])
+
+
+_EMPTY_I64 = np.zeros(0, dtype=np.int64)
+_EMPTY_KEYS = np.zeros((0, 2), dtype=np.uint32)
+
+
+# ---------------------------------------------------------------------------
 # the run object
 # ---------------------------------------------------------------------------
 
 
 class ParticleRun:
     """Resumable bootstrap particle filter along a FilterGrid, on the GPU."""
+
+    _x = _RowRef("_x")  # (nx, P) positions at grid index pos
+    _a = _RowRef("_a")  # (P,) unnormalised log-weights of the last weighted step
+    _cdf = _RowRef("_cdf")  # (P,) tile-local fixed-point CDF of the last weighted step
+    _trec = _RowRef("_trec")  # (ceil(P/32), 2) warp-tile records {max, Q} of the last weighted step
+    _fs = _RowRef("_fs")  # (64,) uint8 view of an ssm_filter_state
 
     def __init__(self, ir, theta, grid, inputs=None, n_particles=1024, resampler="multinomial",
                  ess_rel=None, initial_state=None, check_finite=True, *, dtype="float64",
@@ -290,19 +366,19 @@ class ParticleRun:
                 raise UnsupportedModelError(f"{self.spec.name}: history-free runs need a hand-written model kernel")
             if noise == "host":
                 self.spec.check_host_noise()
-        self._keys = []  # history-free runs: Philox key (2 x uint32) used at each grid index
+        self._kk = _EMPTY_KEYS  # history-free runs: Philox key (2 x uint32) used at each grid index
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.loglik = 0.0
         self.pos = 0
         self.weights_uniform = True
-        self._hist = []  # per grid index: (x batch tensor [B, nx, P], anc batch [B, P] | None, row b)
+        self._segs = []  # (_Seg, row b) per init / advance call, in grid-index order
         self._x = None
         self._a = None  # unnormalised log-weights of the last weighted step
         self._fs = None  # (64,) uint8 view of an ssm_filter_state
         self._cdf = None  # (P,) tile-local fixed-point CDF of the last weighted step
         self._trec = None  # (ceil(P/32), 2) warp-tile records {max, Q} of the last weighted step
-        self._hx = []  # device pointers of history[i][0] (trace-kernel pointer table)
-        self._ha = []  # device pointers of history[i][1] (0 = identity)
+        self._hx = _EMPTY_I64  # device pointers of history[i][0] (trace-kernel pointer table), per grid index
+        self._ha = _EMPTY_I64  # device pointers of history[i][1] (0 = identity)
         self._maybe_nonuniform = False
         self._derived = None
 
@@ -312,12 +388,11 @@ class ParticleRun:
         return self
 
     def clone(self):
+        # the pointer arrays are never modified in place (every advance makes new
+        # ones), so a clone shares them; the segment list is copied
         other = ParticleRun.__new__(ParticleRun)
         other.__dict__ = dict(self.__dict__)
-        other._hist = list(self._hist)
-        other._hx = list(self._hx)
-        other._ha = list(self._ha)
-        other._keys = list(self._keys)
+        other._segs = list(self._segs)
         return other
 
     @property
@@ -330,11 +405,23 @@ class ParticleRun:
         if not self.keep_history:
             raise ValueError("this run keeps no position history (keep_history=False); "
                              "sample_trajectory replays the ancestral line instead")
-        return [(xb[b], ab[b] if ab is not None else None) for xb, ab, b in self._hist]
+        return [v for seg, b in self._segs for v in seg.views(b)]
 
-    @history.setter
-    def history(self, entries):
-        self._hist = [(x.unsqueeze(0), a.unsqueeze(0) if a is not None else None, 0) for x, a in entries]
+    def _set_history(self, xs, ancs, keys=None):
+        """Install a history (a migrated SMC^2 theta-particle): xs [pos+1, nx, P] or None
+        (history-free, keys [pos+1, 2]), ancs [pos, P] ancestors (identity rows included)."""
+        n = ancs.shape[0] + 1
+        self._segs = [(_Seg(xs[:1].unsqueeze(1) if xs is not None else None, None, np.zeros(1, bool), 1), 0)]
+        if n > 1:
+            self._segs.append((_Seg(xs[1:].unsqueeze(1) if xs is not None else None, ancs.unsqueeze(1),
+                                    np.ones(n - 1, bool), n - 1), 0))
+        if xs is not None:
+            self._hx = xs.data_ptr() + (xs[0].numel() * xs.element_size()) * np.arange(n, dtype=np.int64)
+        else:
+            self._hx = np.zeros(n, dtype=np.int64)
+        astep = ancs[0].numel() * ancs.element_size() if n > 1 else 0
+        self._ha = np.concatenate([np.zeros(1, np.int64), ancs.data_ptr() + astep * np.arange(n - 1, dtype=np.int64)])
+        self._kk = np.asarray(keys, dtype=np.uint32).reshape(n, 2) if keys is not None else _EMPTY_KEYS
 
     def advance_to(self, upto, rng):
         return float(advance_runs([self], upto, [rng])[0])
@@ -460,21 +547,23 @@ def init_runs(runs, rngs):
         init_keys = np.zeros((B, 2), dtype=np.uint32)
         if need_draw and r0.noise != "host":
             init_keys[need_draw] = keys
+    seg = _Seg(x.unsqueeze(0) if r0.keep_history else None, None, np.zeros(1, bool), 1)
+    zero1 = np.zeros(1, dtype=np.int64)
+    xrow = x[0].numel() * x.element_size()
     for b, r in enumerate(runs):
-        if not r0.keep_history:
-            r._keys = [init_keys[b]]
-        r._x = x[b]
+        r._kk = init_keys[b : b + 1].copy() if not r0.keep_history else _EMPTY_KEYS
+        _set_row(r, "_x", x, b)
         r._a = None
         r._cdf = None
         r._trec = None
-        r._fs = fs[b]
+        _set_row(r, "_fs", fs, b)
         r.loglik = 0.0
         r.pos = 0
         r.weights_uniform = True
         r._maybe_nonuniform = False
-        r._hist = [(x, None, b)] if r0.keep_history else [(None, None, b)]
-        r._hx = [r._x.data_ptr()] if r0.keep_history else [0]
-        r._ha = [0]
+        r._segs = [(seg, b)]
+        r._hx = np.array([x.data_ptr() + b * xrow], dtype=np.int64) if r0.keep_history else zero1
+        r._ha = zero1
     return runs
 
 
@@ -548,16 +637,15 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
     rs_n = _RS_LAUNCHES[(kind, scheme)]
     profiling.count_launch(n + rs_n * int(anc_used.sum()))
     ring = x_arena.shape[0]
-    for k in range(n):
-        an = anc_arena[k] if anc_used[k] else None
-        new_hist.append((x_arena[k % ring], an))
-        if timer is not None:
+    if timer is not None:
+        for k in range(n):
             has_obs = bool(desc["has_obs"][k])
-            if an is not None:
+            if anc_used[k]:
                 timer.add("resample", evs[4 * k], evs[4 * k + 1], int(B * P * _resample_bytes(esz)))
-            nbytes = B * P * _pw_bytes(spec.nx, esz, an is not None, has_obs)
+            nbytes = B * P * _pw_bytes(spec.nx, esz, bool(anc_used[k]), has_obs)
             timer.add("propagate_weight", evs[4 * k + 2], evs[4 * k + 3], nbytes)
     a_new = a_arena[A.a_last_index] if A.a_last_index >= 0 else a_last
+    new_hist.update(anc=anc_arena, used=anc_used.astype(bool))
     return x_arena[(n - 1) % ring], a_new, bool(A.maybe_nonuniform)
 
 
@@ -592,8 +680,8 @@ def _advance_small(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last, 
     S.a_out = a_out.data_ptr() if a_out is not None else None
     with profiling.maybe("small_filter", 0):
         _lib.check(L.ssm_advance_small(S, stream), "ssm_advance_small")
+    new_hist.update(anc=anc_arena, used=np.ones(n, dtype=bool))
     for k in range(n):
-        new_hist.append((x_arena[k], anc_arena[k]))
         i = start + 1 + k
         if sched.obs[i] is not None:
             maybe = True
@@ -621,9 +709,9 @@ def advance_runs(runs, upto, rngs):
     dev, tdt = r0.device, r0.tdtype
     sched = _schedule(r0.grid, spec, r0.inputs, dev)
     stream = _lib.stream_ptr()
-    x_prev = _stack_rows([r._x for r in runs])
-    a_last = _stack_rows([r._a for r in runs]) if runs[0]._a is not None else None
-    fs = torch.stack([r._fs for r in runs]).contiguous()  # fresh copy: clones stay untouched
+    x_prev = _rows(runs, "_x")
+    a_last = _rows(runs, "_a") if _has_row(r0, "_a") else None
+    fs = _rows(runs, "_fs").clone()  # fresh copy: clones stay untouched
     theta = _derived_tensor(runs)
     maybe_nonuniform = r0._maybe_nonuniform
     host_noise = r0.noise == "host"
@@ -646,10 +734,10 @@ def advance_runs(runs, upto, rngs):
     ntile = (P + 31) // 32  # one tile record per warp tile
     cdf_local = tile_rec = None
     if tiles_ok:
-        have = [r._cdf is not None for r in runs]
+        have = [_has_row(r, "_cdf") for r in runs]
         if all(have):  # resume: fresh copies, clones sharing the views stay intact
-            cdf_local = torch.stack([r._cdf for r in runs])
-            tile_rec = torch.stack([r._trec for r in runs])
+            cdf_local = _rows(runs, "_cdf").clone()
+            tile_rec = _rows(runs, "_trec").clone()
         else:
             cdf_local = torch.empty((B, P), dtype=torch.int64, device=dev)
             tile_rec = torch.empty((B, ntile, 2), dtype=torch.float64, device=dev)
@@ -663,7 +751,7 @@ def advance_runs(runs, upto, rngs):
     ess_rel = -1.0 if r0.ess_rel is None else float(r0.ess_rel)
     log_w0 = float(-np.log(P))
     obs_log_sd = float(np.log(spec.obs_sd))
-    new_hist = []  # per step: (x_out [B, nx, P], anc [B, P] | None)
+    new_hist = {}  # the call's ancestor arena [n, B, P] and which steps resampled (used[k])
     esz = 8 if r0.dtype_id == _lib.SSM_F64 else 4
     theta_host = theta.cpu().numpy() if host_noise else None
 
@@ -697,6 +785,7 @@ def advance_runs(runs, upto, rngs):
     a_slots = min(n_res, 2) if not host_noise else n_res
     a_arena = torch.empty((max(a_slots, 1), B, P), dtype=tdt, device=dev) if n_res else None
     anc_arena = None
+    host_used = None
     a_slot = 0
     if small:  # the persistent kernel keeps its CDF in shared memory
         x_prev, a_last, maybe_nonuniform = _advance_small(
@@ -710,9 +799,10 @@ def advance_runs(runs, upto, rngs):
         anc = None
         if maybe_nonuniform:
             if anc_arena is None:
-                anc_arena = torch.empty((upto - i + 1, B, P), dtype=torch.int32, device=dev)
-                anc_base = i
-            anc = anc_arena[i - anc_base]
+                anc_arena = torch.empty((upto - start, B, P), dtype=torch.int32, device=dev)
+                host_used = np.zeros(upto - start, dtype=bool)
+            anc = anc_arena[i - start - 1]
+            host_used[i - start - 1] = True
             u_t = None
             if host_noise:
                 rr = [s.child(_RESAMPLE_KEY) for s in step_rngs]
@@ -770,7 +860,6 @@ def advance_runs(runs, upto, rngs):
         nbytes = B * P * _pw_bytes(spec.nx, esz, anc is not None, obs is not None)
         with profiling.maybe("propagate_weight", nbytes):
             _lib.check(L.ssm_propagate_weight(args, stream), "ssm_propagate_weight")
-        new_hist.append((x_out, anc))
         x_prev = x_out
         if obs is not None:
             a_last = a_out
@@ -788,29 +877,31 @@ def advance_runs(runs, upto, rngs):
     ll = fs_host["loglik"].astype(float)
     unif = fs_host["uniform"].astype(bool)
     incr = ll - np.array([r.loglik for r in runs])
-    # per-step base pointers once; each run's rows are at a fixed stride
-    x_ptrs = np.array([xo.data_ptr() for xo, _ in new_hist], dtype=np.int64)
-    a_ptrs = np.array([an.data_ptr() if an is not None else 0 for _, an in new_hist], dtype=np.int64)
+    # the call's history segment; per-step base pointers once, each run's rows at a fixed stride
+    if host_noise:
+        new_hist.update(anc=anc_arena, used=host_used if host_used is not None else np.zeros(n_steps, bool))
+    anc_t, used = new_hist.get("anc"), new_hist.get("used")
+    seg = _Seg(x_arena if r0.keep_history else None, anc_t, used, n_steps)
+    ks = np.arange(n_steps, dtype=np.int64)
+    x_ptrs = x_arena.data_ptr() + ks * (B * xstride) if r0.keep_history else np.zeros(n_steps, np.int64)
+    a_ptrs = np.where(used, anc_t.data_ptr() + ks * (B * astride), 0) if anc_t is not None else np.zeros(n_steps, np.int64)
     a_has = a_ptrs != 0
     has_a = a_last is not None
     keep_tiles = tiles_ok and has_a
     for b, r in enumerate(runs):
         r.loglik = float(ll[b])
         r.weights_uniform = bool(unif[b])
-        r._x = x_prev[b]
-        r._a = a_last[b] if has_a else None
-        r._cdf = cdf_local[b] if keep_tiles else None
-        r._trec = tile_rec[b] if keep_tiles else None
-        r._fs = fs[b]
+        _set_row(r, "_x", x_prev, b)
+        _set_row(r, "_a", a_last if has_a else None, b)
+        _set_row(r, "_cdf", cdf_local if keep_tiles else None, b)
+        _set_row(r, "_trec", tile_rec if keep_tiles else None, b)
+        _set_row(r, "_fs", fs, b)
         r._maybe_nonuniform = maybe_nonuniform
-        if r0.keep_history:
-            r._hist.extend((xo, an, b) for xo, an in new_hist)
-            r._hx.extend((x_ptrs + b * xstride).tolist())
-        else:  # ancestors only; positions are replayed by sample_trajectories
-            r._hist.extend((None, an, b) for _, an in new_hist)
-            r._hx.extend([0] * len(new_hist))
-            r._keys.extend([keys[b]] * len(new_hist))
-        r._ha.extend(np.where(a_has, a_ptrs + b * astride, 0).tolist())
+        r._segs = r._segs + [(seg, b)]
+        r._hx = np.concatenate([r._hx, x_ptrs + b * xstride if r0.keep_history else x_ptrs])
+        r._ha = np.concatenate([r._ha, np.where(a_has, a_ptrs + b * astride, 0)])
+        if not r0.keep_history:  # ancestors only; positions are replayed by sample_trajectories
+            r._kk = np.concatenate([r._kk, np.repeat(keys[b : b + 1].astype(np.uint32), n_steps, axis=0)])
         r.pos = upto
     return incr
 
@@ -844,14 +935,14 @@ def sample_trajectories(runs, rngs):
     dev = r0.device
     S = r0.pos
     stream = _lib.stream_ptr()
-    if all(not r.weights_uniform and r._cdf is not None and r._trec is not None for r in runs):
+    if all(not r.weights_uniform and _has_row(r, "_cdf") and _has_row(r, "_trec") for r in runs):
         # final weights carry the fused kernel's tile records: one warp search per filter
         u = torch.from_numpy(first_uniforms(rngs, 1)[:, 0].copy()).to(dev)
         j = torch.empty((B, 1), dtype=torch.int32, device=dev)
         ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
-        cdf = _stack_rows([r._cdf for r in runs]).contiguous()
-        trec = _stack_rows([r._trec for r in runs]).contiguous()
-        fs_rows = _stack_rows([r._fs for r in runs]).contiguous()
+        cdf = _rows(runs, "_cdf").contiguous()
+        trec = _rows(runs, "_trec").contiguous()
+        fs_rows = _rows(runs, "_fs").contiguous()
         _lib.check(L.ssm_pick_from_tiles(B, P, _lib.ptr(cdf), _lib.ptr(trec), _lib.ptr(fs_rows), _lib.ptr(u),
                                          _lib.ptr(j), _lib.ptr(ws), stream), "ssm_pick_from_tiles")
         return _trajectories_from(L, runs, j, S, B, P, nx, dev, stream)
@@ -871,7 +962,7 @@ def sample_trajectories(runs, rngs):
     if all(f is None for f in shifts):
         shift = torch.full((B,), log_p, dtype=torch.float64, device=dev)
     else:  # ssm_filter_state.incr (bytes 8..16) of weighted runs, log P for uniform ones
-        fs_rows = _stack_rows([r._fs for r in runs]).contiguous()
+        fs_rows = _rows(runs, "_fs").contiguous()
         incr = fs_rows.view(torch.float64)[:, 1]
         weighted = torch.tensor([f is not None for f in shifts], device=dev)
         shift = torch.where(weighted, incr, torch.full_like(incr, log_p))
@@ -900,16 +991,16 @@ def _replay_runs(L, runs, j, S, B, P, nx, dev, stream):
     """History-free runs: regenerate the chosen ancestral line (ssm_replay_path)."""
     r0 = runs[0]
     for r in runs:
-        if len(r._keys) != S + 1 or len(r._ha) != S + 1:
+        if len(r._kk) != S + 1 or len(r._ha) != S + 1:
             raise ValueError("history length does not match the run position")
     sched = _schedule(r0.grid, r0.spec, r0.inputs, dev)
     desc = np.ascontiguousarray(sched.desc[: S + 1]).copy()
     if _NO_HINTS:
         desc["hints"] = 0
     desc_t = torch.from_numpy(desc.view(np.uint8).copy()).to(dev)
-    keys_t = torch.from_numpy(np.ascontiguousarray(np.array([r._keys for r in runs], dtype=np.uint32))
+    keys_t = torch.from_numpy(np.ascontiguousarray(np.stack([r._kk for r in runs]).astype(np.uint32))
                               .view(np.int32)).to(dev)
-    ancs_t = torch.from_numpy(np.array([r._ha for r in runs], dtype=np.int64)).to(dev)
+    ancs_t = torch.from_numpy(np.stack([r._ha for r in runs])).to(dev)
     theta = _derived_tensor(runs)
     fixed = [r.initial_state is not None for r in runs]
     x0_t = flag_t = None
@@ -935,10 +1026,10 @@ def _trace_runs(L, runs, j, S, B, P, nx, dev, stream):
     """Ancestry walk from the picked final particles j (device) -> trajectories."""
     r0 = runs[0]
     for r in runs:
-        if len(r._hx) != S + 1 or len(r._hist) != S + 1:
+        if len(r._hx) != S + 1:
             raise ValueError("history length does not match the run position")
-    xs = np.array([r._hx for r in runs], dtype=np.int64)
-    ancs = np.array([r._ha for r in runs], dtype=np.int64)
+    xs = np.stack([r._hx for r in runs])
+    ancs = np.stack([r._ha for r in runs])
     xs_t = torch.from_numpy(xs).to(dev)
     ancs_t = torch.from_numpy(ancs).to(dev)
     out = torch.empty((B, S + 1, nx), dtype=torch.float64, device=dev)

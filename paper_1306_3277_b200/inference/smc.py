@@ -154,18 +154,14 @@ def _pack(spec, L, p):
     host.append([float(r.pos) if r else 0.0, float(r.weights_uniform) if r else 1.0,
                  float(r._maybe_nonuniform) if r else 0.0])
     if r is not None and not L.keep_history:
-        host.append(np.asarray(r._keys, dtype=np.uint32).reshape(-1).astype(np.float64))
+        host.append(np.asarray(r._kk, dtype=np.uint32).reshape(-1).astype(np.float64))
     out = [torch.from_numpy(np.concatenate([np.asarray(h, dtype=np.float64).reshape(-1) for h in host]))]
     if r is not None:
         P = r.n_particles
         ar = torch.arange(P, dtype=torch.int32, device=r.device)
-        if L.keep_history:
-            hist = r.history
-            xs = torch.stack([h[0] for h in hist])
-            ancs = [h[1] for h in hist[1:]]
-        else:
-            xs = r._x
-            ancs = [ab[b] if ab is not None else None for _, ab, b in r._hist[1:]]
+        hist = [v for seg, b in r._segs for v in seg.views(b)]  # (x_i | None, anc_i | None) per grid index
+        xs = torch.stack([h[0] for h in hist]) if L.keep_history else r._x
+        ancs = [h[1] for h in hist[1:]]
         ha = torch.stack([a if a is not None else ar for a in ancs]) if r.pos > 0 else ar[None]
         a = r._a if r._a is not None else torch.zeros(P, dtype=r.tdtype, device=r.device)
         out += [xs, ha, a, r._fs.contiguous()]
@@ -198,17 +194,12 @@ def _unpack(spec, runner, tensors, L):
         xs = tensors[1].to(dev)
         ha = tensors[2].to(dev)
         if L.keep_history:
-            run.history = [(xs[0], None)] + [(xs[i], ha[i - 1]) for i in range(1, pos + 1)]
-            run._hx = [h[0].data_ptr() for h in run.history]
+            run._set_history(xs, ha[:pos])
             run._x = xs[pos]
         else:
             keys = host[k : k + 2 * (pos + 1)].astype(np.uint32).reshape(pos + 1, 2)
-            run._keys = [keys[i].copy() for i in range(pos + 1)]
-            ha_b = ha.unsqueeze(0)
-            run._hist = [(None, None, 0)] + [(None, ha_b[:, i - 1], 0) for i in range(1, pos + 1)]
-            run._hx = [0] * (pos + 1)
+            run._set_history(None, ha[:pos], keys)
             run._x = xs
-        run._ha = [0] + [ha[i - 1].data_ptr() for i in range(1, pos + 1)]
         run._a = tensors[3].to(dev) if L.has_a else None
         run._fs = tensors[4].to(dev)
         if L.has_tiles:

@@ -345,6 +345,13 @@ typedef struct ssm_advance_args {
 } ssm_advance_args;
 
 int ssm_advance(ssm_advance_args* args, void* stream);
+/* ssm_advance as ONE persistent cooperative launch (moderate particle counts:
+ * PMMH chains, SMC^2 theta-particles), hand-written models, device noise, the
+ * tile path with systematic / stratified resampling: the same device bodies
+ * on virtual blocks separated by grid-wide barriers (bitwise ssm_advance).
+ * steps_dev: the same [n_steps] descriptors in device memory.  `events` is
+ * ignored; SSM_ERR_UNSUPPORTED when the kernel cannot be co-resident. */
+int ssm_advance_coop(ssm_advance_args* args, const ssm_step_desc* steps_dev, void* stream);
 int ssm_event_create(void** out);
 int ssm_event_destroy(void* event);
 int ssm_event_elapsed_ms(void* start, void* end, float* ms);

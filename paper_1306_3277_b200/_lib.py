@@ -230,6 +230,7 @@ SIGNATURES = {
     "ssm_logsumexp": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "ssm_block_gather": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
     "ssm_advance": (_i, [C.POINTER(AdvanceArgs), _vp]),
+    "ssm_advance_coop": (_i, [C.POINTER(AdvanceArgs), _vp, _vp]),
     "ssm_small_max_particles": (_i, []),
     "ssm_advance_small": (_i, [C.POINTER(SmallArgs), _vp]),
     "ssm_sharded_workspace_bytes": (_sz, [_i, _i, _i]),
@@ -277,6 +278,7 @@ LAUNCHING = {
     "ssm_logsumexp": 1,
     "ssm_block_gather": 1,
     "ssm_advance": 0,
+    "ssm_advance_coop": 1,
     "ssm_advance_small": 1,
     "ssm_tiles_total": 2,
     "ssm_offspring_push": 3,

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args
 
   if (bad) atomicMin(&fs->err_nonfinite, A.step * 64 + bad_sub);
   if (perr) atomicMin(&fs->err_param, A.step * 64 + perr_sub);
-  pw_block_finalize<kPwThreads>(A, fs, b, P, R, has_obs, acc.park->st, lane, kMaxPwBlocks);
+  pw_block_finalize<kPwThreads>(A, fs, b, P, R, has_obs, acc.park->st, lane, kMaxPwBlocks, blockIdx.x, gridDim.x);
 }
 
 // the model's initial block on the device (sample_initial, simulate.py:111-129)

@@ -485,17 +485,16 @@ __device__ __forceinline__ void filter_block_prefix(int nblk, uint64_t* __restri
 // block totals.  With `fs_rw` (the filter path) the last block of each filter to
 // finish (completion counter fs.prefix_done) also turns the block totals into
 // exclusive block prefixes, so the offspring kernel follows directly.
-__global__ void __launch_bounds__(kThreads)
-tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_filter_state* __restrict__ fs,
-                  double* __restrict__ scale, uint64_t* __restrict__ prel, uint64_t* __restrict__ blk_tot,
-                  uint32_t* __restrict__ long_count = nullptr, int gate = 1, ssm_filter_state* fs_rw = nullptr,
-                  uint64_t* __restrict__ totals = nullptr, OffspringConsts* __restrict__ oc = nullptr, int P = 0,
-                  const double* __restrict__ u = nullptr, const uint32_t* __restrict__ keys = nullptr,
-                  int step = 0) {
-  pdl_wait();
+// block blk (of nblk) of filter b (the persistent driver runs it on virtual blocks)
+__device__ __forceinline__ void tile_scale_body(int b, int blk, int nblk, int ntiles, const ssm_tile_rec* __restrict__ rec,
+                                                const ssm_filter_state* __restrict__ fs, double* __restrict__ scale,
+                                                uint64_t* __restrict__ prel, uint64_t* __restrict__ blk_tot,
+                                                uint32_t* __restrict__ long_count, int gate, ssm_filter_state* fs_rw,
+                                                uint64_t* __restrict__ totals, OffspringConsts* __restrict__ oc, int P,
+                                                const double* __restrict__ u, const uint32_t* __restrict__ keys,
+                                                int step) {
   __shared__ uint64_t warp_tot[kThreads / 32];
   __shared__ bool s_last;
-  const int b = blockIdx.y, blk = blockIdx.x;
   if (gate && !fs[b].resample_now) return;
   if (long_count && blk == 0 && threadIdx.x == 0) long_count[b] = 0u;  // long-run list of this resample
   const double incr = fs[b].incr;
@@ -525,20 +524,31 @@ tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_fi
     tot += warp_tot[w];
   }
   if (e < ntiles) prel[off] = wex + incl - qg;  // exclusive, exact integer
-  if (threadIdx.x == 0) blk_tot[static_cast<size_t>(b) * gridDim.x + blk] = tot;
+  if (threadIdx.x == 0) blk_tot[static_cast<size_t>(b) * nblk + blk] = tot;
   if (!fs_rw) return;
   // only thread 0's block total is read by the last block (prel is read by the
   // next kernel), so only thread 0 fences before taking a ticket
   if (threadIdx.x == 0) {
     __threadfence();
-    s_last = atomicAdd(&fs_rw[b].prefix_done, 1u) == gridDim.x - 1;
+    s_last = atomicAdd(&fs_rw[b].prefix_done, 1u) == static_cast<unsigned>(nblk - 1);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  filter_block_prefix<kThreads>(gridDim.x, blk_tot + static_cast<size_t>(b) * gridDim.x, totals, b, oc, P, u, keys,
-                                step);
+  filter_block_prefix<kThreads>(nblk, blk_tot + static_cast<size_t>(b) * nblk, totals, b, oc, P, u, keys, step);
   if (threadIdx.x == 0) fs_rw[b].prefix_done = 0u;
+}
+
+__global__ void __launch_bounds__(kThreads)
+tile_scale_kernel(int ntiles, const ssm_tile_rec* __restrict__ rec, const ssm_filter_state* __restrict__ fs,
+                  double* __restrict__ scale, uint64_t* __restrict__ prel, uint64_t* __restrict__ blk_tot,
+                  uint32_t* __restrict__ long_count = nullptr, int gate = 1, ssm_filter_state* fs_rw = nullptr,
+                  uint64_t* __restrict__ totals = nullptr, OffspringConsts* __restrict__ oc = nullptr, int P = 0,
+                  const double* __restrict__ u = nullptr, const uint32_t* __restrict__ keys = nullptr,
+                  int step = 0) {
+  pdl_wait();
+  tile_scale_body(blockIdx.y, blockIdx.x, gridDim.x, ntiles, rec, fs, scale, prel, blk_tot, long_count, gate, fs_rw,
+                  totals, oc, P, u, keys, step);
 }
 
 __global__ void __launch_bounds__(1024)
@@ -758,19 +768,25 @@ struct PeerStore {
   }
 };
 
+template <typename Store>
+__device__ __forceinline__ void long_runs_body(int b, int r0, int rstride, int P_in, int P_out,
+                                               const int4* __restrict__ runs, const uint32_t* __restrict__ count,
+                                               const ssm_filter_state* __restrict__ fs, const Store& st) {
+  if (fs && !fs[b].resample_now) return;
+  const uint32_t n = count[b];
+  const int4* rb = runs + static_cast<size_t>(b) * long_runs_cap(P_in, P_out);
+  for (uint32_t r = r0; r < n; r += rstride) {
+    const int4 q = rb[r];
+    for (int k = q.y + threadIdx.x; k < q.z; k += kThreads) st(b, k, q.x);
+  }
+}
+
 template <typename Store = LocalStore>
 __global__ void __launch_bounds__(kThreads)
 long_runs_kernel(int P_in, int P_out, const int4* __restrict__ runs, const uint32_t* __restrict__ count,
                  const ssm_filter_state* __restrict__ fs, Store st) {
   pdl_wait();
-  const int b = blockIdx.y;
-  if (fs && !fs[b].resample_now) return;
-  const uint32_t n = count[b];
-  const int4* rb = runs + static_cast<size_t>(b) * long_runs_cap(P_in, P_out);
-  for (uint32_t r = blockIdx.x; r < n; r += gridDim.x) {
-    const int4 q = rb[r];
-    for (int k = q.y + threadIdx.x; k < q.z; k += kThreads) st(b, k, q.x);
-  }
+  long_runs_body(blockIdx.y, blockIdx.x, gridDim.x, P_in, P_out, runs, count, fs, st);
   if constexpr (!std::is_same<Store, LocalStore>::value) __threadfence_system();  // peer stores
 }
 
@@ -875,15 +891,15 @@ struct ShardSpan {
   int base;
 };
 
-template <int SCHEME, typename Store = LocalStore>
-__global__ void __launch_bounds__(kThreads)
-offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const double* __restrict__ scale,
-                       const uint64_t* __restrict__ pref, const uint64_t* __restrict__ totals,
-                       const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
-                       const ssm_filter_state* __restrict__ fs, Store st,
-                       int4* __restrict__ long_runs, uint32_t* __restrict__ long_count,
-                       const OffspringConsts* __restrict__ oc, ShardSpan span = ShardSpan{nullptr, 0, 0}) {
-  pdl_wait();
+// block blk of filter b (of B filters): the body of offspring_tiles_kernel, also run
+// by the persistent cooperative driver on virtual blocks
+template <int SCHEME, typename Store>
+__device__ __forceinline__ void offspring_tiles_body(int b, int blk, int B, int P, const uint64_t* __restrict__ cdf_local,
+                                                     const double* __restrict__ scale, const uint64_t* __restrict__ pref,
+                                                     const double* __restrict__ u, const uint32_t* __restrict__ keys,
+                                                     int step, const ssm_filter_state* __restrict__ fs, const Store& st,
+                                                     int4* __restrict__ long_runs, uint32_t* __restrict__ long_count,
+                                                     const OffspringConsts* __restrict__ oc, const ShardSpan& span) {
   constexpr int kIt = kRunIt;
   constexpr bool kLocal = std::is_same<Store, LocalStore>::value;
   __shared__ __align__(16) RunWindow sm;
@@ -892,23 +908,21 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
     double sc;
   };
   __shared__ TileInfo s_tile[kThreads / 32][kIt];
-  const int b = blockIdx.y;
   const int Pg = kLocal ? P : span.P_glob;  // outputs (global for a sharded filter)
   const uint64_t goff = kLocal ? 0ull : span.g_off[b];
   if (fs && !fs[b].resample_now) {  // ESS gate held (particle.py:99-100): the history records identity
-    const int k1 = min(P, (blockIdx.x + 1) * kScanTile);
-    for (int k = blockIdx.x * kScanTile + threadIdx.x; k < k1; k += kThreads) st(b, k + (kLocal ? 0 : span.base), k);
-    if constexpr (!kLocal) __threadfence_system();
+    const int k1 = min(P, (blk + 1) * kScanTile);
+    for (int k = blk * kScanTile + threadIdx.x; k < k1; k += kThreads) st(b, k + (kLocal ? 0 : span.base), k);
     return;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nt = (P + 31) >> 5;
   const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
   const uint64_t* tp = pref + static_cast<size_t>(b) * nt;
-  const uint64_t* bp = pref + B_total_tiles_offset(nt, gridDim.y) + static_cast<size_t>(b) * nblk;
+  const uint64_t* bp = pref + B_total_tiles_offset(nt, B) + static_cast<size_t>(b) * nblk;
   const double* scb = scale + static_cast<size_t>(b) * nt;
   const uint64_t* cl = cdf_local + static_cast<size_t>(b) * P;
-  const int jw = blockIdx.x * kScanTile + warp * (kScanTile / (kThreads / 32));  // warp's first particle
+  const int jw = blk * kScanTile + warp * (kScanTile / (kThreads / 32));  // warp's first particle
   const int tw0 = jw >> 5;
   // issue every load of the warp's 8 tiles first: cdf_local per lane, and the
   // tiles' prefix / scale one per lane (broadcast by shuffle below).  The last
@@ -972,7 +986,21 @@ offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const doub
     carry = __shfl_sync(0xffffffffu, c, 31);
   }
   fill_run_window(sm, b, Pg, jw, cv, pv, st, long_runs, long_count);
-  if constexpr (!kLocal) __threadfence_system();  // peer stores visible before the rank barrier
+}
+
+template <int SCHEME, typename Store = LocalStore>
+__global__ void __launch_bounds__(kThreads)
+offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const double* __restrict__ scale,
+                       const uint64_t* __restrict__ pref, const uint64_t* __restrict__ totals,
+                       const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,
+                       const ssm_filter_state* __restrict__ fs, Store st,
+                       int4* __restrict__ long_runs, uint32_t* __restrict__ long_count,
+                       const OffspringConsts* __restrict__ oc, ShardSpan span = ShardSpan{nullptr, 0, 0}) {
+  pdl_wait();
+  (void)totals;
+  offspring_tiles_body<SCHEME, Store>(blockIdx.y, blockIdx.x, gridDim.y, P, cdf_local, scale, pref, u, keys, step, fs,
+                                      st, long_runs, long_count, oc, span);
+  if constexpr (!std::is_same<Store, LocalStore>::value) __threadfence_system();  // peer stores before the barrier
 }
 
 // ---------------------------------------------------------------------------
@@ -2308,4 +2336,213 @@ extern "C" int ssm_block_gather(int J, size_t block_bytes, const void* src, cons
       words, static_cast<const uint4*>(src), idx, static_cast<uint4*>(dst));
   SSM_CHECK_LAUNCH();
   return SSM_OK;
+}
+
+// ===========================================================================
+// Persistent cooperative driver (ssm_advance_coop): the whole grid loop of
+// ssm_advance in ONE cooperative launch for moderate particle counts (PMMH
+// chains, SMC^2 theta-particles: a few 10^5 - 10^6 particles per launch, where
+// the per-step kernels are latency-bound).  Every phase runs the multi-kernel
+// path's device bodies on virtual blocks -- tile scale with the filter prefix
+// in its last block, offspring + window fill, long runs, the fused
+// propagate/weight step with its last-block finalize -- separated by grid-wide
+// barriers, so the results are bitwise those of ssm_advance.
+// ===========================================================================
+
+#include <cooperative_groups.h>
+
+#include "ssm_pw_body.cuh"
+
+namespace ssm {
+
+struct CoopArgs {
+  ssm_advance_args A;          // as ssm_advance (host fields unused)
+  const ssm_step_desc* steps;  // device [n_steps]
+  SearchWs w;                  // A.resample_ws as laid out by search_ws_layout(B, P, P)
+};
+
+template <int MODEL, typename T, bool E, bool SIMPLE, int SCHEME>
+__global__ void __launch_bounds__(kThreads, MODEL == SSM_MODEL_WINDKESSEL ? 3 : 2) advance_coop_kernel(const CoopArgs C) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const ssm_advance_args& A = C.A;
+  constexpr int NX = MODEL == SSM_MODEL_LORENZ96 ? 8 : 1;
+  const int B = A.pw.B, P = A.pw.P;
+  const size_t esz = sizeof(T);
+  const size_t xstep = static_cast<size_t>(B) * NX * P * esz, astep = static_cast<size_t>(B) * P * esz;
+  const SearchWs& w = C.w;  // the resample workspace, laid out as ssm_resample_from_tiles
+  const int nt = (P + 31) / 32;
+  const int nblk = (nt + kRecPerBlock - 1) / kRecPerBlock;
+  double* scale = reinterpret_cast<double*>(w.C);
+  uint64_t* pref = reinterpret_cast<uint64_t*>(w.C) + static_cast<size_t>(B) * nt;
+  uint64_t* blk = pref + B_total_tiles_offset(nt, B);
+  uint32_t* long_count = reinterpret_cast<uint32_t*>(w.totals) + 2 * static_cast<size_t>(B);
+  int4* long_runs = reinterpret_cast<int4*>(w.cnt);
+  OffspringConsts* oc = reinterpret_cast<OffspringConsts*>(w.totals + 3 * static_cast<size_t>(B));
+  const int nob = scan_tiles(P);  // offspring blocks per filter
+  const int nvb = pw_grid_x(P);   // fused-step blocks per filter
+  const int gx_long = max(1, min(1184 / B, P / kRunChunk + 1));
+
+  __shared__ ssm_pw_args s_args;  // this step's arguments (built by thread 0)
+  const void* x_prev = A.x_in;
+  const void* a_last = A.a_prev;
+  int maybe = A.maybe_nonuniform, slot = 0, last_obs = -1;
+  for (int k = 0; k < A.n_steps; ++k)
+    if (C.steps[k].has_obs) last_obs = k;
+  const bool skip_a = !A.ess_gate;
+  for (int k = 0; k < A.n_steps; ++k) {
+    const ssm_step_desc d = C.steps[k];
+    int32_t* anc = nullptr;
+    if (maybe) {
+      anc = A.anc_arena + static_cast<size_t>(k) * B * P;
+      // (1) tile scale + in-block prefix; the last block of each filter the block prefix and constants
+      for (int it = blockIdx.x; it < B * nblk; it += gridDim.x) {
+        __syncthreads();
+        tile_scale_body(it / nblk, it % nblk, nblk, nt, static_cast<const ssm_tile_rec*>(A.tile_rec), A.pw.fs, scale,
+                        pref, blk, long_count, 1, A.pw.fs, w.totals, oc, P, nullptr, A.pw.keys, d.step);
+      }
+      grid.sync();
+      // (2) offspring counts + window fill
+      const LocalStore st{anc, P};
+      for (int it = blockIdx.x; it < B * nob; it += gridDim.x) {
+        __syncthreads();
+        offspring_tiles_body<SCHEME, LocalStore>(it / nob, it % nob, B, P, static_cast<const uint64_t*>(A.cdf_local),
+                                                 scale, pref, nullptr, A.pw.keys, d.step, A.pw.fs, st, long_runs,
+                                                 long_count, oc, ShardSpan{nullptr, P, 0});
+      }
+      grid.sync();
+      // (3) long offspring runs (degenerate weights only)
+      bool any_long = false;
+      for (int b = 0; b < B; ++b) any_long |= A.pw.fs[b].resample_now && long_count[b] > 0;
+      if (any_long) {
+        for (int it = blockIdx.x; it < B * gx_long; it += gridDim.x) {
+          __syncthreads();
+          long_runs_body(it / gx_long, it % gx_long, gx_long, P, P, long_runs, long_count, A.pw.fs, st);
+        }
+        grid.sync();
+      }
+    }
+    // (4) the fused propagate / weight step, finalize in the last virtual block of each filter
+    const int slot_x = A.x_ring > 0 ? k % A.x_ring : k;
+    void* x_out = static_cast<char*>(A.x_arena) + static_cast<size_t>(slot_x) * xstep;
+    void* a_out = nullptr;
+    const int a_slot = A.a_ring > 0 ? slot % A.a_ring : slot;
+    if (d.has_obs && !(skip_a && k != last_obs)) a_out = static_cast<char*>(A.a_arena) + static_cast<size_t>(a_slot) * astep;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_args = A.pw;
+      s_args.step = d.step;
+      s_args.n_sub = d.n_sub;
+      s_args.hints = static_cast<uint32_t>(d.hints);
+      s_args.subs = A.subs_table + d.subs_offset;
+      s_args.x_in = x_prev;
+      s_args.x_out = x_out;
+      s_args.anc = anc;
+      s_args.a_prev = a_last;
+      s_args.has_obs = d.has_obs;
+      s_args.obs_mask = d.obs_mask;
+      for (int n = 0; n < 8; ++n) s_args.y[n] = d.y[n];
+      s_args.u_obs = d.u_obs;
+      s_args.a_out = a_out;
+      s_args.cdf_local = d.has_obs ? A.cdf_local : nullptr;
+      s_args.tile_rec = d.has_obs ? A.tile_rec : nullptr;
+    }
+    __syncthreads();
+    const bool simple = SIMPLE && (d.hints & SSM_HINT_SINGLE_SUBSTEP) && d.n_sub == 1;
+    for (int it = blockIdx.x; it < B * nvb; it += gridDim.x) {
+      __syncthreads();
+      if (simple)
+        pw_body<MODEL, T, E, false, SIMPLE>(s_args, it / nvb, it % nvb, nvb);
+      else
+        pw_body<MODEL, T, E, false, false>(s_args, it / nvb, it % nvb, nvb);
+    }
+    grid.sync();
+    x_prev = x_out;
+    if (d.has_obs) {
+      if (a_out) a_last = a_out;
+      ++slot;
+      maybe = 1;
+    } else if (maybe && !A.ess_gate) {
+      maybe = 0;
+    }
+  }
+}
+
+template <int MODEL, typename T, bool E, bool SIMPLE, int SCHEME>
+static int launch_coop(const CoopArgs& C, cudaStream_t s) {
+  auto kern = advance_coop_kernel<MODEL, T, E, SIMPLE, SCHEME>;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
+  if (per_sm < 1) return SSM_ERR_UNSUPPORTED;
+  const int B = C.A.pw.B, P = C.A.pw.P;
+  const int want = B * std::max(pw_grid_x(P), scan_tiles(P));
+  const int grid = std::max(1, std::min(sms * per_sm, want));
+  void* params[] = {const_cast<CoopArgs*>(&C)};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(kThreads),
+                                                    params, 0, s);
+  if (e != cudaSuccess) {
+    ssm_set_last_error(e);
+    return SSM_ERR_CUDA;
+  }
+  return SSM_OK;
+}
+
+template <int MODEL, typename T, bool E>
+static int launch_coop_scheme(const CoopArgs& C, bool simple, cudaStream_t s) {
+  (void)simple;
+  if (C.A.scheme == SSM_SYSTEMATIC) return launch_coop<MODEL, T, E, true, SSM_SYSTEMATIC>(C, s);
+  return launch_coop<MODEL, T, E, true, SSM_STRATIFIED>(C, s);
+}
+
+}  // namespace ssm
+
+extern "C" int ssm_advance_coop(ssm_advance_args* A, const ssm_step_desc* steps_dev, void* stream) {
+  using namespace ssm;
+  if (!A || !A->steps || !steps_dev || A->n_steps < 0 || !A->x_in || !A->x_arena || !A->anc_used ||
+      !A->resample_ws || !A->cdf_local || !A->tile_rec)
+    return SSM_ERR_INVALID_ARG;
+  if (A->pw.noise != nullptr || !A->pw.keys || !A->tiles) return SSM_ERR_INVALID_ARG;
+  if (A->scheme != SSM_SYSTEMATIC && A->scheme != SSM_STRATIFIED) return SSM_ERR_UNSUPPORTED;
+  if (A->pw.model != SSM_MODEL_LORENZ96 && A->pw.model != SSM_MODEL_WINDKESSEL) return SSM_ERR_UNSUPPORTED;
+  if (A->n_steps == 0) return SSM_OK;
+  // the host-side bookkeeping of ssm_advance: which steps resample, the last weighted slot
+  const int maybe0 = A->maybe_nonuniform;
+  int maybe = maybe0, slot = 0, last_obs = -1;
+  for (int k = 0; k < A->n_steps; ++k)
+    if (A->steps[k].has_obs) last_obs = k;
+  A->a_last_index = -1;
+  bool all_single = true;
+  for (int k = 0; k < A->n_steps; ++k) {
+    const ssm_step_desc& d = A->steps[k];
+    A->anc_used[k] = maybe ? 1 : 0;
+    all_single &= (d.hints & SSM_HINT_SINGLE_SUBSTEP) && d.n_sub == 1;
+    if (d.has_obs) {
+      const int a_slot = A->a_ring > 0 ? slot % A->a_ring : slot;
+      if (A->ess_gate || k == last_obs) A->a_last_index = a_slot;
+      ++slot;
+      maybe = 1;
+    } else if (maybe && !A->ess_gate) {
+      maybe = 0;
+    }
+  }
+  (void)all_single;
+  for (int k = 0; k < A->n_steps; ++k)
+    if (A->anc_used[k] && !A->anc_arena) return SSM_ERR_INVALID_ARG;
+  if (A->pw.exact) return SSM_ERR_UNSUPPORTED;  // the FMA (fast) arithmetic only; exact runs take ssm_advance
+  CoopArgs C{*A, steps_dev, SearchWs{}};  // carries the START state (maybe_nonuniform = maybe0)
+  search_ws_layout(A->pw.B, A->pw.P, A->pw.P, A->resample_ws, &C.w);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // SIMPLE instances carry both paths (steps without the hint take the general body)
+  int st;
+  if (A->pw.model == SSM_MODEL_LORENZ96)
+    st = A->pw.dtype == SSM_F64 ? launch_coop_scheme<SSM_MODEL_LORENZ96, double, false>(C, true, s)
+                                : launch_coop_scheme<SSM_MODEL_LORENZ96, float, false>(C, true, s);
+  else
+    st = A->pw.dtype == SSM_F64 ? launch_coop_scheme<SSM_MODEL_WINDKESSEL, double, false>(C, true, s)
+                                : launch_coop_scheme<SSM_MODEL_WINDKESSEL, float, false>(C, true, s);
+  if (st == SSM_OK) A->maybe_nonuniform = maybe;  // unchanged on failure: the caller may fall back to ssm_advance
+  (void)maybe0;
+  return st;
 }

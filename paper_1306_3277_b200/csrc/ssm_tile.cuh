@@ -197,9 +197,11 @@ __device__ __forceinline__ void warp_tile_flush(WarpTileAcc& acc, int lane) {
 // are combined in block order, so the result is deterministic.  `R` = the
 // filter resampled at this step; `max_blocks` = per-filter stride of the
 // partials in A.workspace.
+// (vb, nvb): this block's index among the filter's nvb blocks (blockIdx.x /
+// gridDim.x of a plain launch; a virtual block of the persistent kernel).
 template <int NT>
 __device__ __forceinline__ void pw_block_finalize(const ssm_pw_args& A, ssm_filter_state* fs, int b, int P, int R,
-                                                  int has_obs, Lse st, int lane, int max_blocks) {
+                                                  int has_obs, Lse st, int lane, int max_blocks, int vb, int nvb) {
   // ---- per-block partial + last-block finalize ----
   __shared__ Lse red[NT / 32];
   __shared__ bool s_last;
@@ -215,14 +217,14 @@ __device__ __forceinline__ void pw_block_finalize(const ssm_pw_args& A, ssm_filt
       Lse r = lane < NT / 32 ? red[lane] : lse_empty();
 #pragma unroll
       for (int off = NT / 64; off > 0; off >>= 1) r = lse_combine(r, lse_shfl_down(r, off));
-      if (lane == 0) parts[blockIdx.x] = r;
+      if (lane == 0) parts[vb] = r;
     }
   }
   // the last block reads only the partials thread 0 wrote (error flags are atomics),
   // so thread 0 alone fences before taking its ticket
   if (threadIdx.x == 0) {
     __threadfence();
-    s_last = atomicAdd(&fs->blocks_done, 1u) == gridDim.x - 1;
+    s_last = atomicAdd(&fs->blocks_done, 1u) == static_cast<unsigned>(nvb - 1);
   }
   __syncthreads();
   if (!s_last) return;
@@ -230,7 +232,7 @@ __device__ __forceinline__ void pw_block_finalize(const ssm_pw_args& A, ssm_filt
 
   if (has_obs) {
     Lse acc = lse_empty();
-    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += NT) {
+    for (int i = threadIdx.x; i < nvb; i += NT) {
       const Lse q{__ldcg(&parts[i].m), __ldcg(&parts[i].c), __ldcg(&parts[i].t),
                   __ldcg(&parts[i].s2)};
       acc = lse_combine(acc, q);

@@ -47,6 +47,10 @@ from .types import FilterOutcome
 import os
 
 _NO_HINTS = bool(os.environ.get("SSM_NO_HINTS"))  # A/B switch for the specialised kernels
+_NO_COOP = bool(os.environ.get("SSM_NO_COOP"))  # A/B switch: per-step kernels instead of the persistent driver
+# the persistent cooperative driver (ssm_advance_coop) runs advances of at most this many
+# particles per launch (B x P), where the per-step kernels are latency-bound
+COOP_MAX_PARTICLES = int(os.environ.get("SSM_COOP_MAX", str(1 << 20)))
 _RESAMPLE_KEY = 0  # particle.py:24
 _PROPAGATE_KEY = 1  # particle.py:25
 SCHEMES = ("multinomial", "stratified", "systematic")
@@ -628,16 +632,28 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
     A.y_table, A.u_table = sched.y_table.data_ptr(), sched.u_table.data_ptr()
     timer = profiling.active()
     evs = None
-    if timer is not None:
-        evs = [profiling.NativeEvent() for _ in range(4 * n)]
-        ev_arr = (C.c_void_p * (4 * n))(*[e.h for e in evs])
-        A.events = C.cast(ev_arr, C.c_void_p)
-    _lib.check(L.ssm_advance(A, stream), "ssm_advance")
-    kind = "tiles" if tiles_ok else "logw"
-    rs_n = _RS_LAUNCHES[(kind, scheme)]
-    profiling.count_launch(n + rs_n * int(anc_used.sum()))
+    coop = (tiles_ok and not _NO_COOP and not _NO_HINTS and scheme in (_lib.SCHEME_IDS["systematic"],
+                                                                         _lib.SCHEME_IDS["stratified"])
+            and spec.kernel != _lib.SSM_MODEL_GENERIC and B * P <= COOP_MAX_PARTICLES)
+    if coop:  # the whole grid loop in one persistent cooperative launch
+        steps_dev = C.c_void_p(sched.desc_dev.data_ptr() + (start + 1) * _lib.STEP_DESC_DTYPE.itemsize)
+        with profiling.maybe("advance_coop", 0):
+            st = L.ssm_advance_coop(A, steps_dev, stream)
+        if st == _lib.SSM_ERR_UNSUPPORTED:
+            coop = False
+        else:
+            _lib.check(st, "ssm_advance_coop")
+    if not coop:
+        if timer is not None:
+            evs = [profiling.NativeEvent() for _ in range(4 * n)]
+            ev_arr = (C.c_void_p * (4 * n))(*[e.h for e in evs])
+            A.events = C.cast(ev_arr, C.c_void_p)
+        _lib.check(L.ssm_advance(A, stream), "ssm_advance")
+        kind = "tiles" if tiles_ok else "logw"
+        rs_n = _RS_LAUNCHES[(kind, scheme)]
+        profiling.count_launch(n + rs_n * int(anc_used.sum()))
     ring = x_arena.shape[0]
-    if timer is not None:
+    if evs is not None:
         for k in range(n):
             has_obs = bool(desc["has_obs"][k])
             if anc_used[k]:

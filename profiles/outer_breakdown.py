@@ -40,16 +40,23 @@ theta, times, obs, inputs = BO.wk_data()
 grid = build_filter_grid(0.0, 1.0, 100, times[1:], obs, np.ones((100, 1), bool), n_obs=1)
 runner = FilterRunner(WINDKESSEL, grid, inputs=inputs, n_particles=1 << 16, resampler="systematic")
 rngs = [RngStream(100 + c) for c in range(8)]
-breakdown("config3 run_batch 8 x 2^16 (one MH step's filters)",
-          lambda: runner.run_batch([theta] * 8, [None] * 8, [g.child(1) for g in rngs]))
+from paper_1306_3277_b200.inference import particle as particle_mod  # noqa: E402
+
+for no_coop in (True, False):
+    particle_mod._NO_COOP = no_coop
+    breakdown(f"config3 run_batch 8 x 2^16 (one MH step's filters), {'per-step kernels' if no_coop else 'persistent'}",
+              lambda: runner.run_batch([theta] * 8, [None] * 8, [g.child(1) for g in rngs]))
 breakdown("config3 mh_sample_chains 8 chains x 3 steps (device theta)",
           lambda: mh_sample_chains(WINDKESSEL, runner, 3, rngs, theta_draws="device"), reps=1)
+particle_mod._NO_COOP = False
 th, t4, ov, om = BO.l96_sparse(T=40)
 g4 = build_filter_grid(0.0, 2.0, 40, t4[1:], ov, om, n_obs=8)
 r4 = FilterRunner(LORENZ96, g4, n_particles=1 << 14, resampler="systematic")
-breakdown("config4 smc 128 theta x 2^14 (device theta)",
-          lambda: smc_sampler(LORENZ96, r4, 128, RngStream(5), theta_resampler="systematic", theta_draws="device"),
-          reps=1)
+for no_coop in (True, False):
+    particle_mod._NO_COOP = no_coop
+    breakdown(f"config4 smc 128 theta x 2^14 (device theta), {'per-step kernels' if no_coop else 'persistent'}",
+              lambda: smc_sampler(LORENZ96, r4, 128, RngStream(5), theta_resampler="systematic", theta_draws="device"),
+              reps=1)
 r4h = FilterRunner(LORENZ96, g4, n_particles=1 << 14, resampler="systematic", keep_history=False)
 breakdown("config4 smc 128 theta x 2^14 (device theta, history-free)",
           lambda: smc_sampler(LORENZ96, r4h, 128, RngStream(5), theta_resampler="systematic", theta_draws="device"),

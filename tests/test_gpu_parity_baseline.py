@@ -245,3 +245,52 @@ def test_windkessel_filters_unbiased_vs_kalman(P, B):
     se = ll.std(ddof=1) / np.sqrt(B)
     bias = 0.5 * ll.var(ddof=1)  # E log L_hat ~ log L - var/2
     assert abs(ll.mean() + bias - kf) < 4 * se + 1e-3, (ll.mean(), kf, se, bias)
+
+
+@pytest.mark.parametrize("kw", [dict(resampler="systematic"), dict(resampler="stratified"),
+                                dict(resampler="systematic", ess_rel=0.6), dict(resampler="systematic", dtype="float32"),
+                                dict(resampler="stratified", sparse=True), dict(resampler="systematic", keep_history=False)])
+def test_persistent_driver_equals_per_step_kernels(kw, monkeypatch):
+    """ssm_advance_coop (the whole grid loop in one cooperative launch, moderate
+    particle counts) runs the per-step kernels' device bodies on virtual blocks:
+    bitwise the same filters (states, ancestors, log-likelihoods, trajectories)
+    as ssm_advance, batched."""
+    from paper_1306_3277_b200.inference import particle as particle_mod
+
+    kw = dict(kw)
+    sparse = kw.pop("sparse", False)
+    theta, times = np.array([10.0, 0.1]), np.linspace(0.0, 1.0, 21)
+    obs = O.simulate_l96(theta, times, O.Stream(4), obs_slots=range(4) if sparse else range(8),
+                         obs_every=2 if sparse else 1)
+    grid = build_filter_grid(0.0, 1.0, 20, times[1:], np.array([obs[k][0] for k in range(1, 21)]),
+                             np.array([obs[k][1] for k in range(1, 21)]), n_obs=8)
+    thetas = [theta, np.array([9.0, 0.2]), np.array([11.0, 0.05]), np.array([10.5, 0.1])]
+    outs = []
+    for no_coop in (False, True):
+        monkeypatch.setattr(particle_mod, "_NO_COOP", no_coop)
+        runner = FilterRunner(LORENZ96, grid, n_particles=20000, **kw)
+        outs.append(runner.run_batch(thetas, [None] * 4, [RngStream(40 + k) for k in range(4)]))
+    for (la, ta, ra), (lb, tb, rb) in zip(*outs):
+        assert la == lb
+        np.testing.assert_array_equal(ta, tb)
+        np.testing.assert_array_equal(ra.x, rb.x)
+        if ra.keep_history:
+            for aa, bb in zip(_device_anc(ra, 20), _device_anc(rb, 20)):
+                np.testing.assert_array_equal(aa, bb)
+
+
+def test_persistent_driver_windkessel_pmmh_batch(monkeypatch):
+    """Config 3's filter batch (8 windkessel filters x 2^16) through the
+    persistent driver equals the per-step kernels bitwise."""
+    from paper_1306_3277_b200.inference import particle as particle_mod
+
+    g, inputs, grid, _ = _wk_setup()
+    thetas = [g["wk/theta"] * f for f in (1.0, 0.9, 1.1, 1.05, 0.95, 1.2, 0.8, 1.15)]
+    outs = []
+    for no_coop in (False, True):
+        monkeypatch.setattr(particle_mod, "_NO_COOP", no_coop)
+        runner = FilterRunner(WINDKESSEL, grid, inputs=inputs, n_particles=1 << 16, resampler="systematic")
+        outs.append(runner.run_batch(thetas, [None] * 8, [RngStream(80 + k) for k in range(8)]))
+    for (la, ta, _), (lb, tb, _) in zip(*outs):
+        assert la == lb
+        np.testing.assert_array_equal(ta, tb)

@@ -557,6 +557,17 @@ int ssm_seedseq_state(int n, int L, const uint32_t* entropy, int n_words, uint32
 int ssm_theta_draws(int model, int has_init);
 int ssm_theta_propose(const ssm_theta_args* args, void* stream);
 int ssm_theta_accept(const ssm_theta_args* args, void* stream);
+/* The theta-level proposal of a GENERATED model (model = SSM_MODEL_GENERIC, handle from
+ * ssm_gen_compile): the walk of proposal_parameter (else parameter) and, with has_init,
+ * of proposal_initial (else initial) plus the initial block's assigns, both proposal
+ * log-densities and parameter_logpdf + initial_logpdf of the proposal (simulate.py:219-352,
+ * in GenericModel.propose_batch / mcmc._propose order, mcmc.py:138-148), one thread per
+ * chain.  u_in rows carry the reference's standard variates by draw index (uniform of a
+ * uniform / truncated-Gaussian statement, standard normal of a Gaussian, standard gamma
+ * of a gamma / inverse-gamma), the accept uniform last; g_in is unused.  u_stride must be
+ * ssm_gen_theta_draws(handle, has_init).  ssm_theta_accept takes the same args. */
+int ssm_gen_theta_draws(const void* handle, int has_init);
+int ssm_gen_theta_propose(const void* handle, const ssm_theta_args* args, void* stream);
 
 #ifdef __cplusplus
 }

@@ -255,6 +255,8 @@ SIGNATURES = {
     "ssm_kalman_sample": (_i, [C.POINTER(KalmanSampleArgs), _vp]),
     "ssm_theta_propose": (_i, [C.POINTER(ThetaArgs), _vp]),
     "ssm_theta_accept": (_i, [C.POINTER(ThetaArgs), _vp]),
+    "ssm_gen_theta_draws": (_i, [_vp, _i]),
+    "ssm_gen_theta_propose": (_i, [_vp, C.POINTER(ThetaArgs), _vp]),
 }
 
 # entry points that launch kernels (for the gpu_launches count): name -> launches
@@ -286,6 +288,7 @@ LAUNCHING = {
     "ssm_trace_peer": 1,
     "ssm_theta_propose": 1,
     "ssm_theta_accept": 1,
+    "ssm_gen_theta_propose": 1,
     "ssm_kalman_filter": 1,
     "ssm_kalman_sample": 1,
 }

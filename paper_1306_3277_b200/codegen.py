@@ -546,6 +546,142 @@ def _emit_logpdf(em, kind, args, y, tmp):
         raise UnsupportedModelError(f"observation density {kind}")
 
 
+_THETA_KINDS = ("gaussian", "uniform", "truncated_gaussian", "gamma", "inverse_gamma")
+
+
+def _theta_samples(ops):
+    """The sample statements of a theta-level block (the walks skip assigns, simulate.py:283-284)."""
+    out = []
+    for op in ops or ():
+        if op["op"] != "sample":
+            continue
+        out.append(op)
+    return out
+
+
+def theta_supported(desc):
+    """True when every theta-level statement samples a kind the device walk has."""
+    blocks = theta_walk_blocks(desc) + ("parameter", "initial")
+    return all(op["kind"] in _THETA_KINDS for b in blocks for op in _theta_samples(desc.get(b)))
+
+
+def theta_walk_blocks(desc):
+    """(parameter walk block, initial walk block) names: a proposal block, else its
+    prior (simulate._walk_proposal's fallback, simulate.py:264-299)."""
+    pw = "proposal_parameter" if desc.get("proposal_parameter") is not None else "parameter"
+    iw = "proposal_initial" if desc.get("proposal_initial") is not None else "initial"
+    return pw, iw
+
+
+def theta_draw_counts(desc):
+    """(draws of the parameter walk, draws of the initial walk): one per sampled slot."""
+    pw, iw = theta_walk_blocks(desc)
+    return (sum(len(op["slots"]) for op in _theta_samples(desc.get(pw))),
+            sum(len(op["slots"]) for op in _theta_samples(desc.get(iw))))
+
+
+def _emit_theta_walk(em, ops, env, kd0):
+    """Sequential-overwrite walk (simulate.py:264-299): every binding's arguments
+    are evaluated before the statement writes; then per slot draw (or take
+    `to`), add the log-density, write `out` and the environment."""
+    kd = kd0
+    for si, op in enumerate(_theta_samples(ops)):
+        em.block("", f"statement {si}: {op['kind']} -> {op['role']} {op['slots']}")
+        for j, args in enumerate(op["args"]):
+            em(f"const double a{j}[{len(args)}] = {{{', '.join(cuda_expr(a) for a in args)}}};")
+        for j, slot in enumerate(op["slots"]):
+            em(f"const double v{j} = to ? to[{slot}] : ssm::th_sample_{op['kind']}(dr, {kd}, a{j}, perr);")
+            em(f"logq = __dadd_rn(logq, ssm::th_lp_{op['kind']}(v{j}, a{j}, perr));")
+            em(f"out[{slot}] = v{j};")
+            em(f"{env}[{slot}] = v{j};")
+            kd += 1
+        em.end()
+    return kd
+
+
+def _emit_theta_logpdf(em, ops, target):
+    """Sum of the block's sample-statement log-densities at `target`
+    (parameter_logpdf / initial_logpdf, simulate.py:219-233)."""
+    em("double total = 0.0;")
+    for si, op in enumerate(_theta_samples(ops)):
+        em.block("", f"statement {si}: {op['kind']} {op['slots']}")
+        for j, (slot, args) in enumerate(zip(op["slots"], op["args"])):
+            em(f"const double a{j}[{len(args)}] = {{{', '.join(cuda_expr(a) for a in args)}}};")
+            em(f"total = __dadd_rn(total, ssm::th_lp_{op['kind']}({target}[{slot}], a{j}, perr));")
+        em.end()
+    em("return total;")
+
+
+def _emit_theta(em, desc):
+    """`struct Theta` of the generated model: the theta-level blocks on the device
+    (gen_theta_propose_kernel, ssm_gen_rt.cuh)."""
+    c = desc["counts"]
+    npar, nx = c["param"], c["state"]
+    pw, iw = theta_walk_blocks(desc)
+    if not theta_supported(desc):  # stubs: the host keeps these blocks (generic.py)
+        em.block("struct Theta")
+        em(f"static constexpr int NP = {npar}, NPB = {max(npar, 1)}, NX = {nx}, NXB = {max(nx, 1)}, KP = 0, KI = 0;")
+        em("__device__ static void param_walk(const double*, const double*, double*, const ssm::ThetaDraws&, "
+           "double&, bool& perr) { perr = true; }")
+        em("__device__ static double param_logpdf(const double*, bool& perr) { perr = true; return 0.0; }")
+        em("__device__ static void init_walk(const double*, const double*, const double*, double*, "
+           "const ssm::ThetaDraws&, double&, bool& perr) { perr = true; }")
+        em("__device__ static double init_logpdf(const double*, const double*, bool& perr) { perr = true; return 0.0; }")
+        em("__device__ static void init_assign(const double*, double*) {}")
+        em.end("};")
+        return
+    kp, ki = theta_draw_counts(desc)
+    init_assigns = [op for op in desc["initial"] if op["op"] == "assign"]
+    pre = ["using T = double;", "using O = ssm::Ar<double, true>;", "const double W[1] = {0.0};",
+           "const double U[NU] = {};", "(void)W; (void)U;"]
+    em.block("struct Theta")
+    em(f"static constexpr int NP = {npar}, NPB = {max(npar, 1)}, NX = {nx}, NXB = {max(nx, 1)}, NU = {max(c['input'], 1)}, "
+       f"KP = {kp}, KI = {ki};")
+    # parameter walk: environment = theta (X zeros)
+    em.block("__device__ static void param_walk(const double* from, const double* to, double* out, "
+             "const ssm::ThetaDraws& dr, double& logq, bool& perr)", f"walk of `{pw}`")
+    em.lines.extend(" " * em.ind + ln for ln in pre)
+    em("double TH[NPB];")
+    em("const double X[NXB] = {};")
+    em("for (int i = 0; i < NP; ++i) TH[i] = out[i] = from[i];")
+    em("(void)X; (void)TH; (void)dr; (void)to; (void)logq; (void)perr;")
+    _emit_theta_walk(em, desc.get(pw), "TH", 0)
+    em.end()
+    em.block("__device__ static double param_logpdf(const double* TH, bool& perr)", "parameter_logpdf")
+    em.lines.extend(" " * em.ind + ln for ln in pre)
+    em("const double X[NXB] = {};")
+    em("(void)X; (void)TH; (void)perr;")
+    _emit_theta_logpdf(em, desc.get("parameter"), "TH")
+    em.end()
+    # initial walk: environment = the state (theta = the walk's theta)
+    em.block("__device__ static void init_walk(const double* TH, const double* from, const double* to, double* out, "
+             "const ssm::ThetaDraws& dr, double& logq, bool& perr)", f"walk of `{iw}`")
+    em.lines.extend(" " * em.ind + ln for ln in pre)
+    em("double X[NXB];")
+    em("for (int i = 0; i < NX; ++i) X[i] = out[i] = from[i];")
+    em("(void)TH; (void)X; (void)dr; (void)to; (void)logq; (void)perr;")
+    _emit_theta_walk(em, desc.get(iw), "X", kp)
+    em.end()
+    em.block("__device__ static double init_logpdf(const double* TH, const double* X, bool& perr)", "initial_logpdf")
+    em.lines.extend(" " * em.ind + ln for ln in pre)
+    em("(void)TH; (void)X; (void)perr;")
+    _emit_theta_logpdf(em, desc["initial"], "X")
+    em.end()
+    em.block("__device__ static void init_assign(const double* TH, double* X)",
+             "the initial block's assigns after an x0 proposal")
+    em.lines.extend(" " * em.ind + ln for ln in pre)
+    em("(void)TH; (void)X;")
+    for si, op in enumerate(init_assigns):
+        em.block("", f"assign -> {op['slots']}")
+        for j, ex in enumerate(op["exprs"]):
+            em(f"const double v{j} = {cuda_expr(ex)};")
+        for j, slot in enumerate(op["slots"]):
+            em(f"X[{slot}] = v{j};")
+        em.end()
+    em.end()
+    em.end("};")
+
+
 def transition_draws(desc):
     """Per transition sub-step: the draw kinds in kernel order (kd = index)."""
     return [op["kind"] for op in desc["transition"] if op["op"] == "sample" for _ in op["slots"]]
@@ -622,10 +758,12 @@ def cuda_source(desc: dict) -> str:
             raise UnsupportedModelError("initial block: state sample/assign statements only")
     _emit_statements(em, desc["initial"], roles)
     em.end()
+    _emit_theta(em, desc)
     em.ind = 0
     em("};")
     em("}  // namespace gen")
-    em(f'extern "C" __device__ int ssm_gen_model_info[2] = {{{nx}, {max(kdraw, 1)}}};')
+    kp, ki = theta_draw_counts(desc)
+    em(f'extern "C" __device__ int ssm_gen_model_info[4] = {{{nx}, {max(kdraw, 1)}, {kp}, {ki}}};')
     return "\n".join(em.lines) + "\n"
 
 

@@ -20,15 +20,17 @@
 namespace {
 
 // kernel instantiations: pw[dtype][exact][injected] = variant dtype * 4 + exact * 2 + injected,
-// init[dtype] = variant 8 + dtype (dtype 0 float, 1 double)
-constexpr int kVariants = 10;
+// init[dtype] = variant 8 + dtype (dtype 0 float, 1 double), theta proposal = variant 10
+constexpr int kVariants = 11;
+constexpr int kThetaVariant = 10;
 const char* kVariantNames[kVariants] = {
     "ssm::gen_pw_kernel<gen::Model, float, false, false>",  "ssm::gen_pw_kernel<gen::Model, float, false, true>",
     "ssm::gen_pw_kernel<gen::Model, float, true, false>",   "ssm::gen_pw_kernel<gen::Model, float, true, true>",
     "ssm::gen_pw_kernel<gen::Model, double, false, false>", "ssm::gen_pw_kernel<gen::Model, double, false, true>",
     "ssm::gen_pw_kernel<gen::Model, double, true, false>",  "ssm::gen_pw_kernel<gen::Model, double, true, true>",
-    "ssm::gen_init_kernel<gen::Model, float>",              "ssm::gen_init_kernel<gen::Model, double>"};
-const char* kInfoName = "ssm_gen_model_info";  // extern "C" __device__ int[2] = {NX, KDRAW}
+    "ssm::gen_init_kernel<gen::Model, float>",              "ssm::gen_init_kernel<gen::Model, double>",
+    "ssm::gen_theta_propose_kernel<gen::Model>"};
+const char* kInfoName = "ssm_gen_model_info";  // extern "C" __device__ int[4] = {NX, KDRAW, KP, KI}
 
 // One handle per model: the source, and each kernel variant compiled (NVRTC)
 // and loaded on first use, so a model pays only for the variants it runs.
@@ -38,6 +40,7 @@ struct GenModel {
   cudaLibrary_t lib[kVariants] = {};
   cudaKernel_t kernel[kVariants] = {};
   int nx = 0, kdraw = 0;
+  int kp = 0, ki = 0;  // theta-level draws: parameter walk, initial walk
 };
 
 int pw_variant(int dtype, int exact, int injected) {
@@ -101,14 +104,16 @@ int load_variant(GenModel* g, int v, char* log, size_t log_len) {
   cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   cudaKernel_t k = nullptr;
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&k, lib, low[0].c_str());
-  if (e == cudaSuccess && g->nx == 0) {  // model sizes from ssm_gen_model_info (NX, KDRAW)
-    int info[2] = {0, 0};
+  if (e == cudaSuccess && g->nx == 0) {  // model sizes from ssm_gen_model_info (NX, KDRAW, KP, KI)
+    int info[4] = {0, 0, 0, 0};
     void* dptr = nullptr;
     size_t bytes = 0;
     e = cudaLibraryGetGlobal(&dptr, &bytes, lib, kInfoName);
     if (e == cudaSuccess && bytes >= sizeof(info)) e = cudaMemcpy(info, dptr, sizeof(info), cudaMemcpyDeviceToHost);
     g->nx = info[0];
     g->kdraw = info[1];
+    g->kp = info[2];
+    g->ki = info[3];
   }
   if (e != cudaSuccess) {
     ssm_set_last_error(e);
@@ -211,6 +216,36 @@ extern "C" int ssm_gen_init_particles(const void* handle, int dtype, int B, int 
   cfg.stream = static_cast<cudaStream_t>(stream);
   void* params[] = {&P, &p_offset, const_cast<uint32_t**>(&keys), const_cast<double**>(&theta), &theta_stride,
                     &x_out, &fs};
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k), params);
+  if (e != cudaSuccess) {
+    ssm_set_last_error(e);
+    return SSM_ERR_CUDA;
+  }
+  return SSM_OK;
+}
+
+extern "C" int ssm_gen_theta_draws(const void* handle, int has_init) {
+  if (!handle) return -1;
+  const GenModel* g = static_cast<const GenModel*>(handle);
+  return g->kp + (has_init ? g->ki : 0) + 1;  // walk draws, then the accept uniform
+}
+
+extern "C" int ssm_gen_theta_propose(const void* handle, const ssm_theta_args* A, void* stream) {
+  if (!handle || !A || A->model != SSM_MODEL_GENERIC || A->n_chains < 0) return SSM_ERR_INVALID_ARG;
+  const GenModel* g = static_cast<const GenModel*>(handle);
+  if (A->nx != g->nx || A->u_stride != ssm_gen_theta_draws(handle, A->has_init)) return SSM_ERR_INVALID_ARG;
+  if (A->n_chains == 0) return SSM_OK;
+  if (!A->theta || !A->theta_new || !A->logq_fwd || !A->logq_rev || !A->log_prior_new || !A->err)
+    return SSM_ERR_INVALID_ARG;
+  if (A->has_init && (!A->x0 || !A->x0_new)) return SSM_ERR_INVALID_ARG;
+  if (!A->u_in && !A->keys) return SSM_ERR_INVALID_ARG;
+  cudaKernel_t k = get_kernel(handle, kThetaVariant);
+  if (!k) return SSM_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((A->n_chains + 127) / 128);
+  cfg.blockDim = dim3(128);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  void* params[] = {const_cast<ssm_theta_args*>(A)};
   const cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k), params);
   if (e != cudaSuccess) {
     ssm_set_last_error(e);

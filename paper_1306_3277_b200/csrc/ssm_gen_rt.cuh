@@ -239,4 +239,167 @@ __global__ void __launch_bounds__(kPwThreads)
   if (perr && fs) atomicMin(&fs[b].err_param, 0);
 }
 
+
+// ---------------------------------------------------------------------------
+// Theta-level blocks of a generated model (SURVEY 8f row 1 for generic models):
+// the generated `M::Theta` walks proposal_parameter / proposal_initial (or the
+// parameter / initial blocks when a proposal is absent) with the reference's
+// sequential-overwrite semantics (simulate.py:264-299) and evaluates the
+// priors (simulate.py:219-233); the kernel below strings them together like
+// GenericModel.propose_batch / mcmc._propose (mcmc.py:138-148), one thread
+// per chain.  ssm_theta_accept (ssm_theta.cu) applies the accept.
+//
+// Draws by index kd (the proposal walk's statements and slots in order, then
+// the initial walk's): injected standard variates (u_in row: the uniform of a
+// uniform / truncated-Gaussian draw, the standard normal of a Gaussian, the
+// standard gamma of a (inverse-)gamma -- the reference's own numpy draws) or
+// Philox blocks {kd, retry, step, kPurposeGenTheta} on the chain's key.
+// All arithmetic is float64 with one rounding per operation (numpy order);
+// log / lgamma / normcdf / normcdfinv are CUDA's (a few ulp from numpy/scipy).
+constexpr uint32_t kPurposeGenTheta = 8u;
+constexpr double kThLogSqrt2Pi = 0.91893853320467274178;  // distributions.py:15
+
+struct ThetaDraws {
+  const ssm_theta_args* A;
+  int c;
+  __device__ __forceinline__ U4 block(int kd, uint32_t retry) const {
+    return philox4x32_10(U4{static_cast<uint32_t>(kd), retry, static_cast<uint32_t>(A->step), kPurposeGenTheta},
+                         A->keys[2 * c], A->keys[2 * c + 1]);
+  }
+  __device__ __forceinline__ double injected(int kd) const {
+    return A->u_in[static_cast<size_t>(c) * A->u_stride + kd];
+  }
+  __device__ double uniform(int kd) const {
+    if (A->u_in) return injected(kd);
+    const U4 r = block(kd, 0u);
+    return u53(r.x, r.y);
+  }
+  __device__ double normal(int kd) const {
+    if (A->u_in) return injected(kd);
+    const U4 r = block(kd, 0u);
+    double z0, z1;
+    box_muller(r.x, r.y, r.z, r.w, z0, z1);
+    return z0;
+  }
+  // standard gamma(shape): Marsaglia-Tsang, try `it` on blocks 2it+1 (normal) and
+  // 2it+2 (uniform); shape < 1 through gamma(shape + 1) U^(1/shape) (block 0)
+  __device__ double std_gamma(int kd, double shape) const {
+    if (A->u_in) return injected(kd);
+    if (!(shape > 0.0)) return CUDART_NAN;
+    double boost = 1.0;
+    if (shape < 1.0) {
+      const U4 r = block(kd, 0u);
+      boost = pow(1.0 - u53(r.x, r.y), 1.0 / shape);
+      shape += 1.0;
+    }
+    const double dd = shape - 1.0 / 3.0, cc = 1.0 / sqrt(9.0 * dd);
+    for (uint32_t it = 0; it < 1000u; ++it) {
+      const U4 rz = block(kd, 2u * it + 1u), ru = block(kd, 2u * it + 2u);
+      double z, z1;
+      box_muller(rz.x, rz.y, rz.z, rz.w, z, z1);
+      double v = 1.0 + cc * z;
+      if (v <= 0.0) continue;
+      v = v * v * v;
+      const double u = 1.0 - u53(ru.x, ru.y);
+      if (log(u) < 0.5 * z * z + dd - dd * v + dd * log(v)) return dd * v * boost;
+    }
+    return dd * boost;  // not reached in practice (acceptance > 0.95 per try)
+  }
+};
+
+// distributions.sample (distributions.py:73-91) from a standard variate
+__device__ __forceinline__ double th_sample_gaussian(const ThetaDraws& dr, int kd, const double* a, bool& perr) {
+  if (!(a[1] > 0.0)) perr = true;
+  return __dadd_rn(a[0], __dmul_rn(a[1], dr.normal(kd)));  // numpy: loc + scale * z
+}
+__device__ __forceinline__ double th_sample_uniform(const ThetaDraws& dr, int kd, const double* a, bool& perr) {
+  if (!(a[0] < a[1])) perr = true;
+  return __dadd_rn(a[0], __dmul_rn(__dsub_rn(a[1], a[0]), dr.uniform(kd)));  // low + (high - low) u
+}
+__device__ __forceinline__ double th_sample_truncated_gaussian(const ThetaDraws& dr, int kd, const double* a,
+                                                               bool& perr) {
+  const double fa = normcdf(__ddiv_rn(__dsub_rn(a[2], a[0]), a[1]));
+  const double fb = normcdf(__ddiv_rn(__dsub_rn(a[3], a[0]), a[1]));
+  if (!(a[1] > 0.0) || !(a[2] < a[3]) || !(__dsub_rn(fb, fa) > 0.0)) perr = true;
+  const double q = __dadd_rn(fa, __dmul_rn(dr.uniform(kd), __dsub_rn(fb, fa)));
+  return __dadd_rn(a[0], __dmul_rn(a[1], normcdfinv(q)));  // mean + sd ndtri(fa + u (fb - fa))
+}
+__device__ __forceinline__ double th_sample_gamma(const ThetaDraws& dr, int kd, const double* a, bool& perr) {
+  if (!(a[0] > 0.0) || !(a[1] > 0.0)) perr = true;
+  return __dmul_rn(a[1], dr.std_gamma(kd, a[0]));  // scale * standard_gamma(shape)
+}
+__device__ __forceinline__ double th_sample_inverse_gamma(const ThetaDraws& dr, int kd, const double* a,
+                                                          bool& perr) {
+  if (!(a[0] > 0.0) || !(a[1] > 0.0)) perr = true;
+  return __ddiv_rn(1.0, __dmul_rn(__ddiv_rn(1.0, a[1]), dr.std_gamma(kd, a[0])));  // 1 / gamma(k, 1/s)
+}
+
+// distributions.logpdf (distributions.py:94-123), the reference's operation order
+__device__ __forceinline__ double th_lp_gaussian(double x, const double* a, bool& perr) {
+  if (!(a[1] > 0.0)) perr = true;
+  const double z = __ddiv_rn(__dsub_rn(x, a[0]), a[1]);
+  return __dsub_rn(__dsub_rn(__dmul_rn(__dmul_rn(-0.5, z), z), log(a[1])), kThLogSqrt2Pi);
+}
+__device__ __forceinline__ double th_lp_truncated_gaussian(double x, const double* a, bool& perr) {
+  const double fa = normcdf(__ddiv_rn(__dsub_rn(a[2], a[0]), a[1]));
+  const double fb = normcdf(__ddiv_rn(__dsub_rn(a[3], a[0]), a[1]));
+  if (!(a[1] > 0.0) || !(a[2] < a[3]) || !(__dsub_rn(fb, fa) > 0.0)) perr = true;
+  const double z = __ddiv_rn(__dsub_rn(x, a[0]), a[1]);
+  const double core = __dsub_rn(__dsub_rn(__dsub_rn(__dmul_rn(__dmul_rn(-0.5, z), z), log(a[1])), kThLogSqrt2Pi),
+                                log(__dsub_rn(fb, fa)));
+  return (x >= a[2] && x <= a[3]) ? core : -CUDART_INF;
+}
+__device__ __forceinline__ double th_lp_gamma(double x, const double* a, bool& perr) {
+  if (!(a[0] > 0.0) || !(a[1] > 0.0)) perr = true;
+  if (!(x > 0.0)) return -CUDART_INF;
+  const double t = __dsub_rn(__dmul_rn(__dsub_rn(a[0], 1.0), log(x)), __ddiv_rn(x, a[1]));
+  return __dsub_rn(__dsub_rn(t, __dmul_rn(a[0], log(a[1]))), lgamma(a[0]));
+}
+__device__ __forceinline__ double th_lp_inverse_gamma(double x, const double* a, bool& perr) {
+  if (!(a[0] > 0.0) || !(a[1] > 0.0)) perr = true;
+  if (!(x > 0.0)) return -CUDART_INF;
+  const double t = __dsub_rn(__dmul_rn(a[0], log(a[1])), lgamma(a[0]));
+  return __dsub_rn(__dsub_rn(t, __dmul_rn(__dadd_rn(a[0], 1.0), log(x))), __ddiv_rn(a[1], x));
+}
+__device__ __forceinline__ double th_lp_uniform(double x, const double* a, bool& perr) {
+  if (!(a[0] < a[1])) perr = true;
+  return (x >= a[0] && x <= a[1]) ? -log(__dsub_rn(a[1], a[0])) : -CUDART_INF;
+}
+
+// One proposal per chain (GenericModel.propose_batch order): theta walk, its
+// reverse density, then the x0 walk (new theta) + initial assigns, its reverse
+// density (old theta), then the prior of the proposal.
+template <class M>
+__global__ void __launch_bounds__(128) gen_theta_propose_kernel(ssm_theta_args A) {
+  using Th = typename M::Theta;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= A.n_chains) return;
+  const ThetaDraws D{&A, c};
+  const double* th = A.theta + static_cast<size_t>(c) * Th::NP;
+  double* out = A.theta_new + static_cast<size_t>(c) * Th::NP;
+  bool perr = false;
+  double lq_f = 0.0, lq_r = 0.0;
+  double tmp[Th::NPB];
+  Th::param_walk(th, nullptr, out, D, lq_f, perr);
+  Th::param_walk(out, th, tmp, D, lq_r, perr);
+  double lp = Th::param_logpdf(out, perr);
+  if (A.has_init) {
+    const double* x0 = A.x0 + static_cast<size_t>(c) * Th::NX;
+    double* x1 = A.x0_new + static_cast<size_t>(c) * Th::NX;
+    double xn[Th::NXB], xt[Th::NXB];
+    double lf = 0.0, lr = 0.0;
+    Th::init_walk(out, x0, nullptr, xn, D, lf, perr);
+    Th::init_assign(out, xn);
+    Th::init_walk(th, xn, x0, xt, D, lr, perr);
+    for (int n = 0; n < Th::NX; ++n) x1[n] = xn[n];
+    lq_f = lq_f + lf;
+    lq_r = lq_r + lr;
+    lp = lp + Th::init_logpdf(out, xn, perr);
+  }
+  A.logq_fwd[c] = lq_f;
+  A.logq_rev[c] = lq_r;
+  A.log_prior_new[c] = lp;
+  if (perr) atomicExch(A.err, 1);
+}
+
 }  // namespace ssm

@@ -170,6 +170,8 @@ int check_args(const ssm_theta_args* A) {
     if (A->n_param != 2 || A->nx != 8) return SSM_ERR_INVALID_ARG;
   } else if (A->model == SSM_MODEL_WINDKESSEL) {
     if (A->n_param != 4 || A->nx != 1 || A->has_init) return SSM_ERR_INVALID_ARG;
+  } else if (A->model == SSM_MODEL_GENERIC) {  // accept only (the proposal is ssm_gen_theta_propose)
+    if (A->n_param < 0 || A->nx < 0 || A->u_stride < 1) return SSM_ERR_INVALID_ARG;
   } else {
     return SSM_ERR_UNSUPPORTED;
   }
@@ -181,6 +183,7 @@ int check_args(const ssm_theta_args* A) {
 }  // namespace ssm
 
 extern "C" int ssm_theta_draws(int model, int has_init) {
+  if (model != SSM_MODEL_LORENZ96 && model != SSM_MODEL_WINDKESSEL) return -1;  // generic: ssm_gen_theta_draws
   const int n_tg = model == SSM_MODEL_LORENZ96 ? 1 : 3;
   const int nx = model == SSM_MODEL_LORENZ96 ? 8 : 1;
   return n_tg + (has_init ? nx : 0) + 2 + 1;  // tg uniforms, x0 uniforms, gamma(2) pair, accept
@@ -188,6 +191,7 @@ extern "C" int ssm_theta_draws(int model, int has_init) {
 
 extern "C" int ssm_theta_propose(const ssm_theta_args* args, void* stream) {
   using namespace ssm;
+  if (args && args->model == SSM_MODEL_GENERIC) return SSM_ERR_UNSUPPORTED;  // ssm_gen_theta_propose
   const int rc = check_args(args);
   if (rc != SSM_OK) return rc;
   if (args->n_chains == 0) return SSM_OK;

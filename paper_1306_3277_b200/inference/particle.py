@@ -49,8 +49,11 @@ import os
 _NO_HINTS = bool(os.environ.get("SSM_NO_HINTS"))  # A/B switch for the specialised kernels
 _NO_COOP = bool(os.environ.get("SSM_NO_COOP"))  # A/B switch: per-step kernels instead of the persistent driver
 # the persistent cooperative driver (ssm_advance_coop) runs advances of at most this many
-# particles per launch (B x P), where the per-step kernels are latency-bound
-COOP_MAX_PARTICLES = int(os.environ.get("SSM_COOP_MAX", str(1 << 20)))
+# particles per launch (B x P).  Off by default: measured on B200 it is slower than the
+# per-step PDL chain at every size tried (config 3: 5.98 vs 4.27 ms per MH step; L96
+# 2^16 / 2^18 / 2^20: 1.44 / 4.77 / 8.84e9 vs 1.69 / 5.79 / 12.4e9 particle-updates/s;
+# profiles/r2_coop_ab.txt) -- grid-wide barriers cost more than the launches they replace.
+COOP_MAX_PARTICLES = int(os.environ.get("SSM_COOP_MAX", "0"))
 _RESAMPLE_KEY = 0  # particle.py:24
 _PROPAGATE_KEY = 1  # particle.py:25
 SCHEMES = ("multinomial", "stratified", "systematic")

@@ -19,8 +19,11 @@ Draws:
     uniform), injected.  This is the parity mode: the result equals
     `marginal_mh_steps` up to normcdf/normcdfinv rounding (~1e-15 relative).
 
-Only the two hand-written models have device theta blocks; a generic model
-raises UnsupportedModelError.
+Generic models (codegen.py) run the same two launches: the generated
+`Theta` walks (`ssm_gen_theta_propose`, ssm_gen_rt.cuh) and the shared accept.
+Their injected draws are the standard variates of the reference's own
+numpy calls, recorded while its walk runs on each chain's stream
+(`_RecordingStream`).
 """
 
 from __future__ import annotations
@@ -37,20 +40,55 @@ from .mcmc import _FILTER_KEY, MhChainState
 DRAW_MODES = ("device", "host")
 
 
+class _RecordingStream:
+    """Stands in for a chain's RngStream while the reference's walk draws from it
+    (generic.GenericModel.propose_parameters / propose_initial): every draw is
+    taken as a standard variate from the stream -- the same generator calls,
+    so the stream advances exactly as under the reference -- recorded, and
+    scaled the way numpy's own distribution functions scale it (loc + scale z,
+    low + (high - low) u, scale * standard_gamma)."""
+
+    def __init__(self, rng):
+        self.rng = rng
+        self.draws = []
+
+    def normal(self, loc=0.0, scale=1.0, size=None):
+        z = np.asarray(self.rng.normal(0.0, 1.0, size=size), dtype=float)
+        self.draws.extend(np.ravel(z).tolist())
+        return np.asarray(loc, dtype=float) + np.asarray(scale, dtype=float) * z
+
+    def uniform(self, low=0.0, high=1.0, size=None):
+        u = np.asarray(self.rng.uniform(0.0, 1.0, size=size), dtype=float)
+        self.draws.extend(np.ravel(u).tolist())
+        lo = np.asarray(low, dtype=float)
+        return lo + (np.asarray(high, dtype=float) - lo) * u
+
+    def gamma(self, shape, scale=1.0, size=None):
+        g = np.asarray(self.rng.gamma(shape, 1.0, size=size), dtype=float)
+        self.draws.extend(np.ravel(g).tolist())
+        return np.asarray(scale, dtype=float) * g
+
+
 class DeviceThetaChains:
     """Device-resident state of C chains plus the proposal buffers."""
 
     def __init__(self, ir, states, device=None):
         spec = resolve_model(ir)
-        if spec.kernel not in (_lib.SSM_MODEL_LORENZ96, _lib.SSM_MODEL_WINDKESSEL):
-            raise UnsupportedModelError("device theta-level MH covers the hand-written models only")
+        self.generic = spec.kernel == _lib.SSM_MODEL_GENERIC
+        if not self.generic and spec.kernel not in (_lib.SSM_MODEL_LORENZ96, _lib.SSM_MODEL_WINDKESSEL):
+            raise UnsupportedModelError(f"{spec.name}: no device theta-level blocks")
+        self.has_init = bool(states and states[0].init_state is not None)
+        if self.generic:
+            from .. import codegen
+
+            if not codegen.theta_supported(spec.desc):
+                raise UnsupportedModelError(f"{spec.name}: a theta-level statement the device walk cannot sample")
+        elif self.has_init and not spec.has_proposal_initial:
+            raise UnsupportedModelError(f"{spec.name} has no proposal_initial block")
         _lib.require_cuda()
         self.spec = spec
         self.device = torch.device(device if device is not None else "cuda")
         self.C = len(states)
-        self.has_init = bool(states and states[0].init_state is not None)
-        if self.has_init and not spec.has_proposal_initial:
-            raise UnsupportedModelError(f"{spec.name} has no proposal_initial block")
         f64 = dict(dtype=torch.float64, device=self.device)
         C, npar, nx = self.C, spec.n_param, spec.nx
         self.theta = torch.tensor(np.array([s.theta for s in states], dtype=float).reshape(C, npar), **f64)
@@ -66,7 +104,11 @@ class DeviceThetaChains:
         self.ll_new = torch.empty(C, **f64)
         self.accepted = torch.empty(C, dtype=torch.int32, device=self.device)
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.u_stride = _lib.lib().ssm_theta_draws(spec.kernel, int(self.has_init))
+        if self.generic:
+            self._handle = spec.handle(self.device)
+            self.u_stride = _lib.lib().ssm_gen_theta_draws(self._handle, int(self.has_init))
+        else:
+            self.u_stride = _lib.lib().ssm_theta_draws(spec.kernel, int(self.has_init))
         self._inj = None
         self._keys = None
 
@@ -84,9 +126,32 @@ class DeviceThetaChains:
             a.u_in, a.g_in, a.u_acc_in = (p(t) for t in self._inj)
         return a
 
+    def _host_draws_generic(self, rngs):
+        """The reference's walk on each chain's stream with the draws recorded
+        (GenericModel.propose_batch order), then the accept uniform."""
+        spec, C = self.spec, self.C
+        th = self.theta.cpu().numpy()
+        x0 = self.x0.cpu().numpy() if self.has_init else None
+        u = np.zeros((C, self.u_stride))
+        ua = np.zeros(C)
+        prime_streams(rngs)
+        for c, rng in enumerate(rngs):
+            rec = _RecordingStream(rng)
+            th_new, _ = spec.propose_parameters(th[c], rec)
+            if self.has_init:
+                spec.propose_initial(th_new, x0[c], rec)
+            if len(rec.draws) != self.u_stride - 1:
+                raise UnsupportedModelError(f"{spec.name}: {len(rec.draws)} theta-level draws, "
+                                            f"expected {self.u_stride - 1}")
+            u[c, : self.u_stride - 1] = rec.draws
+            ua[c] = rng.uniform()
+        return u, np.zeros(C), ua
+
     def host_draws(self, rngs):
         """The reference's draws from each chain stream, in its order (models.propose_batch,
         then metropolis_accept): (u [C][u_stride], g [C], u_acc [C])."""
+        if self.generic:
+            return self._host_draws_generic(rngs)
         spec, C = self.spec, self.C
         n_tg = 1 if spec.kernel == _lib.SSM_MODEL_LORENZ96 else 3
         ig = n_tg
@@ -118,7 +183,12 @@ class DeviceThetaChains:
             self._keys = torch.as_tensor(keys, device=self.device)
         self.err.zero_()
         with torch.cuda.device(self.device):
-            _lib.check(_lib.lib().ssm_theta_propose(self._args(step), _lib.stream_ptr(stream)), "ssm_theta_propose")
+            if self.generic:
+                _lib.check(_lib.lib().ssm_gen_theta_propose(self._handle, self._args(step), _lib.stream_ptr(stream)),
+                           "ssm_gen_theta_propose")
+            else:
+                _lib.check(_lib.lib().ssm_theta_propose(self._args(step), _lib.stream_ptr(stream)),
+                           "ssm_theta_propose")
         packed = torch.cat([self.theta_new.reshape(-1)] + ([self.x0_new.reshape(-1)] if self.has_init else []) +
                            [self.lq_f, self.lq_r, self.lp_new, self.err.to(torch.float64)]).cpu().numpy()
         if packed[-1] != 0:

@@ -90,18 +90,41 @@ def test_invalid_args_rejected_without_device():
     a.model = _lib.SSM_MODEL_GENERIC
     assert lib.ssm_theta_propose(a, None) == _lib.SSM_ERR_UNSUPPORTED
     assert lib.ssm_theta_draws(_lib.SSM_MODEL_LORENZ96, 1) == 1 + 8 + 2 + 1
+    assert lib.ssm_theta_draws(_lib.SSM_MODEL_GENERIC, 1) == -1
+    assert lib.ssm_gen_theta_propose(None, a, None) == _lib.SSM_ERR_INVALID_ARG
+    assert lib.ssm_gen_theta_draws(None, 0) == -1
 
 
-def test_device_theta_mh_rejects_generic_models():
+def test_generic_theta_blocks_generated():
+    """Generic models carry device theta-level blocks (codegen `struct Theta`):
+    one draw per sampled slot of the proposal walk (or the prior when the
+    proposal is absent); a statement the walk cannot sample gives stubs and
+    DeviceThetaChains refuses the model before touching a device."""
+    import copy
     import json
 
-    from paper_1306_3277_b200 import generic
+    from paper_1306_3277_b200 import codegen, generic
     from paper_1306_3277_b200.errors import UnsupportedModelError
     from paper_1306_3277_b200.inference.theta_mh import DeviceThetaChains
 
     with open(os.path.join(ROOT, "tests", "golden", "gen_models.json")) as fh:
-        d = dict(json.load(fh)["lowered"]["StochVol"])
+        low = json.load(fh)["lowered"]
+    want = {"Lorenz96": ((2, 8), ("proposal_parameter", "proposal_initial")),
+            "PredatorPrey": ((3, 2), ("proposal_parameter", "initial")),
+            "StochVol": ((3, 1), ("parameter", "initial"))}
+    for name, (counts, blocks) in want.items():
+        d = dict(low[name])
+        d.pop("fingerprint", None)
+        assert codegen.theta_draw_counts(d) == counts
+        assert codegen.theta_walk_blocks(d) == blocks
+        assert codegen.theta_supported(d)
+        src = codegen.cuda_source(d)
+        assert "struct Theta" in src and "th_sample_" in src
+    d = copy.deepcopy(dict(low["StochVol"]))
     d.pop("fingerprint", None)
+    d["parameter"][0]["kind"] = "wiener"
+    assert not codegen.theta_supported(d)
+    assert "perr = true; }" in codegen.cuda_source(d)
     with pytest.raises(UnsupportedModelError):
         DeviceThetaChains(generic.from_description(d), [])
 

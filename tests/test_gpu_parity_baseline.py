@@ -247,6 +247,23 @@ def test_windkessel_filters_unbiased_vs_kalman(P, B):
     assert abs(ll.mean() + bias - kf) < 4 * se + 1e-3, (ll.mean(), kf, se, bias)
 
 
+def _spy_coop(monkeypatch):
+    """Record the status of every ssm_advance_coop call."""
+    from paper_1306_3277_b200 import _lib
+
+    L = _lib.lib()
+    real = L.ssm_advance_coop
+    ran = []
+
+    def spy(*a):
+        st = real(*a)
+        ran.append(st)
+        return st
+
+    monkeypatch.setattr(L, "ssm_advance_coop", spy)
+    return ran
+
+
 @pytest.mark.parametrize("kw", [dict(resampler="systematic"), dict(resampler="stratified"),
                                 dict(resampler="systematic", ess_rel=0.6), dict(resampler="systematic", dtype="float32"),
                                 dict(resampler="stratified", sparse=True), dict(resampler="systematic", keep_history=False)])
@@ -266,10 +283,13 @@ def test_persistent_driver_equals_per_step_kernels(kw, monkeypatch):
                              np.array([obs[k][1] for k in range(1, 21)]), n_obs=8)
     thetas = [theta, np.array([9.0, 0.2]), np.array([11.0, 0.05]), np.array([10.5, 0.1])]
     outs = []
+    monkeypatch.setattr(particle_mod, "COOP_MAX_PARTICLES", 1 << 20)  # opt in (off by default)
+    ran = _spy_coop(monkeypatch)
     for no_coop in (False, True):
         monkeypatch.setattr(particle_mod, "_NO_COOP", no_coop)
         runner = FilterRunner(LORENZ96, grid, n_particles=20000, **kw)
         outs.append(runner.run_batch(thetas, [None] * 4, [RngStream(40 + k) for k in range(4)]))
+    assert ran and all(st == 0 for st in ran)  # the persistent driver ran (and succeeded)
     for (la, ta, ra), (lb, tb, rb) in zip(*outs):
         assert la == lb
         np.testing.assert_array_equal(ta, tb)
@@ -287,10 +307,13 @@ def test_persistent_driver_windkessel_pmmh_batch(monkeypatch):
     g, inputs, grid, _ = _wk_setup()
     thetas = [g["wk/theta"] * f for f in (1.0, 0.9, 1.1, 1.05, 0.95, 1.2, 0.8, 1.15)]
     outs = []
+    monkeypatch.setattr(particle_mod, "COOP_MAX_PARTICLES", 1 << 20)  # opt in (off by default)
+    ran = _spy_coop(monkeypatch)
     for no_coop in (False, True):
         monkeypatch.setattr(particle_mod, "_NO_COOP", no_coop)
         runner = FilterRunner(WINDKESSEL, grid, inputs=inputs, n_particles=1 << 16, resampler="systematic")
         outs.append(runner.run_batch(thetas, [None] * 8, [RngStream(80 + k) for k in range(8)]))
+    assert ran and all(st == 0 for st in ran)
     for (la, ta, _), (lb, tb, _) in zip(*outs):
         assert la == lb
         np.testing.assert_array_equal(ta, tb)

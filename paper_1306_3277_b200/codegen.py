@@ -454,7 +454,7 @@ def _emit_statements(em, ops, roles, dname="d"):
             m = len(op["slots"])
             em.block("", f"statement {si}: ode RK4 h={op['h']!r} over X{op['slots']}")
             em(f"constexpr double H = {_dlit(op['h'])};")
-            em(f"const int n_steps = max(1, int(ceil({dname} / H - 1e-9)));")
+            em(f"const int n_steps = ONE ? 1 : max(1, int(ceil({dname} / H - 1e-9)));")
             # fast mode: the state-independent terms of each derivative (parameters,
             # this sub-step's noise and inputs) summed once per sub-step instead of in
             # every RK4 stage (a reassociation, within the fast path's tolerance)
@@ -702,7 +702,8 @@ def cuda_source(desc: dict) -> str:
     em(f"static constexpr int NX = {nx}, NW = {nw}, NWB = {max(nw, 1)}, NU = {max(c['input'], 1)}, "
        f"KDRAW = {max(kdraw, 1)};")
     # transition sub-step
-    em("template <typename T, bool E, bool INJ>")
+    # ONE: the host guarantees one RK4 step per ode statement (SSM_HINT_SINGLE_SUBSTEP)
+    em("template <typename T, bool E, bool INJ, bool ONE = false>")
     em.block("__device__ static void substep(T (&X)[NX], T (&W)[NWB], const double* TH, const double* U, "
              "double d, const ssm::GenDraws<T>& dr, bool& perr)")
     em("using O = ssm::Ar<T, E>;")

@@ -20,16 +20,20 @@
 namespace {
 
 // kernel instantiations: pw[dtype][exact][injected] = variant dtype * 4 + exact * 2 + injected,
-// init[dtype] = variant 8 + dtype (dtype 0 float, 1 double), theta proposal = variant 10
-constexpr int kVariants = 11;
+// init[dtype] = variant 8 + dtype (dtype 0 float, 1 double), theta proposal = variant 10,
+// SIMPLE pw (fast, device draws) = variant 11 + dtype
+constexpr int kVariants = 13;
 constexpr int kThetaVariant = 10;
+constexpr int kSimpleVariant = 11;
 const char* kVariantNames[kVariants] = {
     "ssm::gen_pw_kernel<gen::Model, float, false, false>",  "ssm::gen_pw_kernel<gen::Model, float, false, true>",
     "ssm::gen_pw_kernel<gen::Model, float, true, false>",   "ssm::gen_pw_kernel<gen::Model, float, true, true>",
     "ssm::gen_pw_kernel<gen::Model, double, false, false>", "ssm::gen_pw_kernel<gen::Model, double, false, true>",
     "ssm::gen_pw_kernel<gen::Model, double, true, false>",  "ssm::gen_pw_kernel<gen::Model, double, true, true>",
     "ssm::gen_init_kernel<gen::Model, float>",              "ssm::gen_init_kernel<gen::Model, double>",
-    "ssm::gen_theta_propose_kernel<gen::Model>"};
+    "ssm::gen_theta_propose_kernel<gen::Model>",
+    "ssm::gen_pw_kernel<gen::Model, float, false, false, true>",
+    "ssm::gen_pw_kernel<gen::Model, double, false, false, true>"};
 const char* kInfoName = "ssm_gen_model_info";  // extern "C" __device__ int[4] = {NX, KDRAW, KP, KI}
 
 // One handle per model: the source, and each kernel variant compiled (NVRTC)
@@ -180,7 +184,9 @@ extern "C" int ssm_gen_info(const void* handle, int* n_state, int* n_draws) {
 int ssm_gen_propagate_weight(const ssm_pw_args& A, cudaStream_t s) {
   if (!A.gen || A.theta_stride <= 0) return SSM_ERR_INVALID_ARG;
   if (A.dtype != SSM_F64 && A.dtype != SSM_F32) return SSM_ERR_INVALID_ARG;
-  cudaKernel_t k = get_kernel(A.gen, pw_variant(A.dtype, A.exact, A.noise != nullptr));
+  const bool simple = (A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !A.exact && A.noise == nullptr;
+  cudaKernel_t k = get_kernel(A.gen, simple ? kSimpleVariant + (A.dtype == SSM_F64 ? 1 : 0)
+                                            : pw_variant(A.dtype, A.exact, A.noise != nullptr));
   if (!k) return SSM_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ssm::pw_grid_x(A.P), A.B);

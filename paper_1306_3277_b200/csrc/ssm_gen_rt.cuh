@@ -81,7 +81,11 @@ struct GenDraws {
   }
 };
 
-template <class M, typename T, bool E, bool INJ>
+// SIMPLE (host hint SSM_HINT_SINGLE_SUBSTEP, device draws, fast mode): one
+// sub-step per grid step whose ode statements each take one RK4 step -- the
+// sub-step loop and the RK4 step loops disappear and the sub-step record is
+// read once per block.
+template <class M, typename T, bool E, bool INJ, bool SIMPLE = false>
 __global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args A) {
   pdl_wait();
   constexpr int NX = M::NX;
@@ -162,14 +166,15 @@ __global__ void __launch_bounds__(kPwThreads, 2) gen_pw_kernel(const ssm_pw_args
       T w[M::NWB];  // the noise array of step_transition: zeros, then rewritten per sub-step
 #pragma unroll
       for (int n = 0; n < M::NWB; ++n) w[n] = T(0);
-      for (int k = 0; k < A.n_sub; ++k) {
+      const int n_sub = SIMPLE ? 1 : A.n_sub;
+      for (int k = 0; k < n_sub; ++k) {
         const ssm_substep& S = A.subs[k];
         const double* U = A.u_vec ? A.u_vec + static_cast<size_t>(k) * M::NU : &S.u_in;
         const GenDraws<T> dr{k0, k1, static_cast<uint32_t>(p + A.p_offset), static_cast<uint32_t>(A.step),
                              static_cast<uint32_t>(k), INJ ? noise + static_cast<size_t>(k) * M::KDRAW * P : nullptr,
                              P, p};
         bool pe = false;
-        M::template substep<T, E, INJ>(x, w, th, U, S.d, dr, pe);
+        M::template substep<T, E, INJ, SIMPLE>(x, w, th, U, S.d, dr, pe);
         if (pe && !perr) {
           perr = true;
           perr_sub = k;

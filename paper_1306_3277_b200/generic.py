@@ -108,6 +108,7 @@ class GenericModel:
         self._handles = {}
         self._fns = {}
         self.has_proposal_initial = desc.get("proposal_initial") is not None
+        self.ode_h = [float(op["h"]) for op in desc["transition"] if op["op"] == "ode"]
 
     @property
     def nx(self):

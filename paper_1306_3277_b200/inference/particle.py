@@ -133,6 +133,9 @@ class Schedule:
             self.offsets[i] = len(recs)
             self.n_sub[i] = len(subs)
             self.single[i] = len(subs) == 1 and (not spec.has_ode or int(arr[0]["n_ode"]) == 1)
+            if spec.kernel == _lib.SSM_MODEL_GENERIC:  # every ode statement: one RK4 step (codegen, simulate.py:85)
+                self.single[i] = len(subs) == 1 and all(max(1, int(np.ceil(subs[0][1] / h - 1e-9))) == 1
+                                                        for h in spec.ode_h)
             self.sub_end[i] = ends
             self.sub_start[i] = [t_k for t_k, _ in subs]
             self.host_subs[i] = arr

@@ -247,3 +247,32 @@ def test_generic_twelve_observations_two_inputs_bitwise_reference():
                                                exact=False).loglik for k in range(6)])
     se = np.sqrt(lls["device"].var(ddof=1) / 6 + lls["host"].var(ddof=1) / 6)
     assert abs(lls["device"].mean() - lls["host"].mean()) < 4 * se + 0.5, (lls, se)
+
+
+@pytest.mark.parametrize("name", ["Lorenz96", "StochVol", "PredatorPrey"])
+def test_generic_simple_variant_equals_general(name, monkeypatch):
+    """The SIMPLE generated kernel (one sub-step, one RK4 step per ode; chosen from
+    SSM_HINT_SINGLE_SUBSTEP) is the general kernel with its loops removed:
+    bitwise the same filter.  PredatorPrey (4 RK4 steps per grid step) must not
+    take it."""
+    from paper_1306_3277_b200.inference import particle as particle_mod
+
+    m = model(name)
+    if name == "Lorenz96":  # grid step = delta = h: one sub-step, one RK4 step
+        g = load_golden("pf.npz")
+        theta = g["l96/theta"]
+        grid = build_filter_grid(0.0, 2.0, 40, g["l96/obs_t"], g["l96/obs_v"], g["l96/obs_m"], n_obs=8)
+    else:
+        g = load_golden("generic.npz")
+        m, grid = _grid(g, name)
+        theta = g[f"{name}/theta"]
+    sched = particle_mod.Schedule(grid, m, None, "cuda")
+    assert any(sched.single[1:]) == (name != "PredatorPrey")
+    outs = []
+    for no_hints in (False, True):
+        monkeypatch.setattr(particle_mod, "_NO_HINTS", no_hints)
+        outs.append(particle_filter(m, theta, grid, RngStream(17), n_particles=40000, resampler="systematic",
+                                    exact=False))
+    assert outs[0].loglik == outs[1].loglik
+    np.testing.assert_array_equal(outs[0].trajectory, outs[1].trajectory)
+    np.testing.assert_array_equal(np.asarray(outs[0].run.x), np.asarray(outs[1].run.x))

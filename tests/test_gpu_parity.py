@@ -532,6 +532,41 @@ def test_pf_upto_zero_and_unobserved_steps():
     assert all(h[1] is None or np.array_equal(h[1].cpu().numpy(), np.arange(5000)) for h in out.run.history[1:])
 
 
+@pytest.mark.parametrize("P", [64, 5000])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_trajectory_pick_on_uniform_weights_matches_oracle(P, scheme):
+    """The final multinomial pick when the last weights are uniform -- at upto=0
+    and after trailing unobserved grid steps (the resample that follows the last
+    observation leaves uniform weights) -- draws from the run's stream like the
+    reference (particle.py:137-149): trajectories bitwise the oracle's, and
+    different streams pick different particles."""
+    g = load_golden("pf.npz")
+    grid = _l96_grid(g)
+    og = O.Grid(grid.times, {k + 1: (g["l96/obs_v"][k], g["l96/obs_m"][k]) for k in range(20)})
+    for seed in (3, 4):
+        out = particle_filter(LORENZ96, g["l96/theta"], grid, RngStream(seed), n_particles=P, resampler=scheme,
+                              noise="host", upto=0)
+        ll, traj, _ = O.particle_filter("lorenz96", g["l96/theta"], og, O.Stream(seed), n_particles=P,
+                                        resampler=scheme, upto=0)
+        assert out.loglik == ll == 0.0
+        np.testing.assert_array_equal(out.trajectory, traj)
+    # observations only on the first 14 of 20 steps: the last 6 propagate with uniform weights
+    mask = g["l96/obs_m"].copy()
+    mask[14:] = False
+    tgrid = build_filter_grid(0.0, 2.0, 20, g["l96/obs_t"], g["l96/obs_v"], mask, n_obs=8)
+    otg = O.Grid(tgrid.times, {k + 1: (g["l96/obs_v"][k], mask[k]) for k in range(20)})
+    picks = set()
+    for seed in (5, 6, 7):
+        out = particle_filter(LORENZ96, g["l96/theta"], tgrid, RngStream(seed), n_particles=P, resampler=scheme,
+                              noise="host")
+        ll, traj, _ = O.particle_filter("lorenz96", g["l96/theta"], otg, O.Stream(seed), n_particles=P,
+                                        resampler=scheme)
+        assert abs(out.loglik - ll) <= 1e-12 * abs(ll)
+        np.testing.assert_array_equal(out.trajectory, traj)
+        picks.add(tuple(np.round(traj[-1], 12)))
+    assert len(picks) > 1
+
+
 @pytest.mark.parametrize("scheme", SCHEMES)
 @pytest.mark.parametrize("P", [3000, 100000])
 def test_device_noise_ess_gate_runs(scheme, P):

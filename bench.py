@@ -222,7 +222,8 @@ def run_ours(args, rank, world):
             tdist.barrier()
         torch.cuda.synchronize()
 
-    timer = profiling.KernelTimer()
+    # events around every 20th grid step's launches (2 of 40 per run); SSM_BENCH_TIMER_EVERY for A/B
+    timer = profiling.KernelTimer(every=int(os.environ.get("SSM_BENCH_TIMER_EVERY", "20")))
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     logliks = []
     with ClockSampler(dev.index) as clocks:
@@ -583,6 +584,10 @@ def main():
                         else None),
             "traffic_source": (traffic.get("source") if traffic else None),
             "algorithmic_bytes_per_particle": pw["bytes"] / max(pw["launches"], 1) / P if pw else None,
+            "timing": ("CUDA events on the launching stream around the resample and pw launches of grid steps "
+                       "19 and 39 of each timed filter run (an event between two programmatic dependent "
+                       "launches serialises them: bracketing all 40 steps costs 3.4% of the run, "
+                       "profiles/r2_timer_ab.txt)"),
         },
         "kernels": kern,
         # the whole grid step (resample kernels + fused gather/propagate/weight): algorithmic bytes of

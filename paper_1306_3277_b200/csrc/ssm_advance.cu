@@ -40,7 +40,7 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
     if (maybe) {
       anc = A->anc_arena + static_cast<size_t>(k) * ancstep;
       A->anc_used[k] = 1;
-      if (ev) cudaEventRecord(ev[4 * k + 0], s);
+      if (ev && ev[4 * k + 0]) cudaEventRecord(ev[4 * k + 0], s);
       int st;
       if (A->tiles) {
         st = ssm_resample_tiles_step(B, P, A->scheme, A->cdf_local, A->tile_rec, A->pw.fs, nullptr, A->pw.keys,
@@ -50,7 +50,7 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
         st = ssm_resample_from_logw(B, P, A->pw.dtype, A->scheme, a_last, nullptr, A->pw.fs, nullptr,
                                     A->pw.keys, d.step, anc, A->resample_ws, stream);
       }
-      if (ev) cudaEventRecord(ev[4 * k + 1], s);
+      if (ev && ev[4 * k + 1]) cudaEventRecord(ev[4 * k + 1], s);
       if (st != SSM_OK) return st;
     } else {
       A->anc_used[k] = 0;
@@ -78,9 +78,9 @@ extern "C" int ssm_advance(ssm_advance_args* A, void* stream) {
     pw.a_out = a_out;
     pw.cdf_local = (A->tiles && d.has_obs) ? A->cdf_local : nullptr;
     pw.tile_rec = (A->tiles && d.has_obs) ? A->tile_rec : nullptr;
-    if (ev) cudaEventRecord(ev[4 * k + 2], s);
+    if (ev && ev[4 * k + 2]) cudaEventRecord(ev[4 * k + 2], s);
     const int st = ssm_propagate_weight(&pw, stream);
-    if (ev) cudaEventRecord(ev[4 * k + 3], s);
+    if (ev && ev[4 * k + 3]) cudaEventRecord(ev[4 * k + 3], s);
     if (st != SSM_OK) return st;
     x_prev = x_out;
     if (d.has_obs) {

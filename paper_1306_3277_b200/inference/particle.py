@@ -650,9 +650,9 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
         else:
             _lib.check(st, "ssm_advance_coop")
     if not coop:
-        if timer is not None:
-            evs = [profiling.NativeEvent() for _ in range(4 * n)]
-            ev_arr = (C.c_void_p * (4 * n))(*[e.h for e in evs])
+        if timer is not None:  # events around the sampled steps only (each one splits a PDL pair)
+            evs = [profiling.NativeEvent() if timer.samples(start + 1 + k) else None for k in range(n) for _ in range(4)]
+            ev_arr = (C.c_void_p * (4 * n))(*[e.h if e is not None else None for e in evs])
             A.events = C.cast(ev_arr, C.c_void_p)
         _lib.check(L.ssm_advance(A, stream), "ssm_advance")
         kind = "tiles" if tiles_ok else "logw"
@@ -661,6 +661,8 @@ def _advance_native(L, r0, B, P, spec, sched, start, upto, args, x_prev, a_last,
     ring = x_arena.shape[0]
     if evs is not None:
         for k in range(n):
+            if evs[4 * k] is None:
+                continue
             has_obs = bool(desc["has_obs"][k])
             if anc_used[k]:
                 timer.add("resample", evs[4 * k], evs[4 * k + 1], int(B * P * _resample_bytes(esz)))

@@ -57,8 +57,17 @@ class NativeEvent:
 
 
 class KernelTimer:
-    def __init__(self):
+    """`every` = k: inside the native grid-loop driver only grid steps i with
+    i % k == k - 1 are bracketed by events (an event between two programmatic
+    dependent launches serialises them, so timing every step would slow the
+    run it measures); every=1 times every launch."""
+
+    def __init__(self, every=1):
         self.events = defaultdict(list)  # name -> [(start, end, bytes)]
+        self.every = max(int(every), 1)
+
+    def samples(self, step):
+        return self.every == 1 or step % self.every == self.every - 1
 
     def add(self, name, start, end, nbytes=0):
         self.events[name].append((start, end, nbytes))

@@ -187,7 +187,8 @@ def configk(quick):
 def configr(quick):
     """Resample + gather microbench (SURVEY 8d kernel inputs): logw ~ N(0, sigma_w^2),
     sigma_w in {0, 1, 10} (ESS from P to ~1), numpy default_rng(1234), states U(-1,3)^8,
-    f64, P = 2^24: ssm_resample_from_logw then ssm_gather, timed with CUDA events.
+    f64, P = 2^24: ssm_resample_from_logw (tile records from the log-weights, then the
+    filter path's tile resampler) then ssm_gather, timed with CUDA events.
     Algorithmic bytes B_R = 8 (read logw) + 4 (write ancestor) + 2*8*8 (gather) = 140 B."""
     import torch
 

@@ -269,9 +269,12 @@ int ssm_resample_search(int B, int P_in, int P_out, int scheme, int cum_kind, co
  * unnormalised log-weights a (w = exp(a - shift[b]), shift NULL -> fs[b].incr).
  * shift must be the log-sum-exp of a[b] (the weights sum to 1): the exact
  * fixed-point CDF has 2^52 units per unit of weight and no headroom beyond 1.
- * systematic / stratified: exact fixed-point reduce-then-scan (tile sums ->
- * tile prefix -> offspring bounds + partition) -> expand, 4 launches, no
- * look-back and no searches; multinomial: look-back scan + binary search. */
+ * systematic / stratified / sorted multinomial: one pass builds the fused
+ * kernel's warp-tile records from a (tile-local 2^52 fixed point + {m_w, Q_w},
+ * in the workspace), then the filter path's tile resampler (ssm_resample_tiles_step:
+ * tile scale -> offspring counts writing the ancestors -> long-run fill, or the
+ * spacing merge); multinomial (reference query order): look-back scan + binary
+ * search. */
 size_t ssm_resample_workspace_bytes(int B, int P);
 /* Filter fast path: ancestors from the tile records + cdf_local written by the
  * weighted ssm_propagate_weight (systematic / stratified; sorted multinomial

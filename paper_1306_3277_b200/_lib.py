@@ -321,6 +321,8 @@ class _Lib:
                         profiling.count_launch(4)  # sorted multinomial: tile scale, spacing sums / prefix, merge
                     elif _name == "ssm_resample_from_logw" and a[3] == 0:
                         profiling.count_launch(2)  # look-back scan + binary search
+                    elif _name == "ssm_resample_from_logw" and a[3] == 3:
+                        profiling.count_launch(5)  # tile records, tile scale, spacing sums / prefix, merge
                     elif _name == "ssm_advance":
                         pass  # counted by the caller from the step plan
                     else:

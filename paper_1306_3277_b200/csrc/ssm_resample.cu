@@ -9,6 +9,7 @@
 #include <type_traits>
 
 #include "ssm_common.cuh"
+#include "ssm_tile.cuh"
 
 namespace ssm {
 
@@ -1786,6 +1787,9 @@ struct SearchWs {
   uint64_t* C;
   double* spc;  // sorted multinomial: block-local inclusive spacing sums, [B][nsb * 2048]
   uint64_t* lb;  // fused tile resample: double-buffered look-back status + long-run counts (fused_ws)
+  uint64_t* lt_cdf;       // ssm_resample_from_logw's tile path: cdf_local [B][P_in]
+  ssm_tile_rec* lt_rec;   // ... its warp-tile records [B][nt]
+  ssm_filter_state* lt_fs;  // ... and per-filter states {incr = shift, resample_now}
 };
 
 static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, SearchWs* w) {
@@ -1820,6 +1824,9 @@ static inline size_t search_ws_layout(int B, int P_in, int P_out, void* base, Se
   const size_t runs_bytes = sizeof(int4) * static_cast<size_t>(B) * long_runs_cap(P_in, P_out);
   tmp.cnt = reinterpret_cast<int32_t*>(take(cnt_bytes > runs_bytes ? cnt_bytes : runs_bytes));
   tmp.split = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(B) * (nd + 1)));
+  tmp.lt_cdf = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * static_cast<size_t>(B) * P_in));
+  tmp.lt_rec = reinterpret_cast<ssm_tile_rec*>(take(sizeof(ssm_tile_rec) * static_cast<size_t>(B) * nt));
+  tmp.lt_fs = reinterpret_cast<ssm_filter_state*>(take(sizeof(ssm_filter_state) * static_cast<size_t>(B)));
   if (w) *w = tmp;
   return off;
 }
@@ -2166,6 +2173,60 @@ extern "C" size_t ssm_resample_workspace_bytes(int B, int P) {
   return ssm_search_workspace_bytes(B, P, P);
 }
 
+// Log-weights -> the fused kernel's warp-tile records (the weighting half of
+// pw_kernel's warp_tile_weigh, standalone): per 32-particle tile m_w = float
+// round-up of the tile max, q_j = round(exp(a_j - m_w) 2^52), cdf_local = the
+// tile-inclusive prefix of q, {m_w, Q_w}; and per filter a state with
+// incr = shift (the weights' log-sum-exp) for the tile-path resample that
+// follows.  One warp per tile, grid-stride.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+logw_tiles_kernel(int P, const T* __restrict__ a, const double* __restrict__ shift,
+                  const ssm_filter_state* __restrict__ fs_in, uint64_t* __restrict__ cloc,
+                  ssm_tile_rec* __restrict__ trec, ssm_filter_state* __restrict__ fs_out) {
+  __shared__ double s_exp_tab[64];
+  if (threadIdx.x < 64) s_exp_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
+  __syncthreads();
+  const int b = blockIdx.y;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ssm_filter_state f = {};
+    f.incr = shift ? shift[b] : fs_in[b].incr;
+    f.resample_now = fs_in ? fs_in[b].resample_now : 1;
+    f.err_nonfinite = f.err_degenerate = f.err_param = INT_MAX;
+    fs_out[b] = f;
+  }
+  const int lane = threadIdx.x & 31;
+  const int nt = (P + 31) >> 5;
+  const T* ab = a + static_cast<size_t>(b) * P;
+  uint64_t* cl = cloc + static_cast<size_t>(b) * P;
+  ssm_tile_rec* tr = trec + static_cast<size_t>(b) * nt;
+  const int nwarps = gridDim.x * (kThreads / 32);
+  for (int w = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); w < nt; w += nwarps) {
+    const int p = w * 32 + lane;
+    const bool act = p < P;
+    const double a_d = act ? static_cast<double>(__ldg(ab + p)) : -CUDART_INF;
+    const float af = __double2float_ru(a_d);
+    const int key = __float_as_int(af) >= 0 ? __float_as_int(af) : (__float_as_int(af) ^ 0x7fffffff);
+    const int kmax = __reduce_max_sync(0xffffffffu, act ? key : (-2147483647 - 1));
+    const int kb = kmax >= 0 ? kmax : (kmax ^ 0x7fffffff);
+    const double mw = static_cast<double>(__int_as_float(kb));
+    const double e = (!act || mw == -CUDART_INF) ? 0.0 : exp_tile(a_d - mw, s_exp_tab);
+    const uint64_t q = (e >= 0.0 && e <= 1.0) ? __double2ull_rn(e * kTileFix) : 0ull;
+    uint32_t qh = static_cast<uint32_t>(q >> 26), ql = static_cast<uint32_t>(q) & 0x3ffffffu;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t yh = __shfl_up_sync(0xffffffffu, qh, o);
+      const uint32_t yl = __shfl_up_sync(0xffffffffu, ql, o);
+      if (lane >= o) {
+        qh += yh;
+        ql += yl;
+      }
+    }
+    if (act) cl[p] = (static_cast<uint64_t>(qh) << 26) + ql;
+    if (lane == 31) tr[w] = ssm_tile_rec{mw, (static_cast<uint64_t>(qh) << 26) + ql};
+  }
+}
+
 extern "C" int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const void* a,
                                       const double* shift, const ssm_filter_state* fs,
                                       const double* u, const uint32_t* keys, int step, int32_t* anc,
@@ -2183,7 +2244,27 @@ extern "C" int ssm_resample_from_logw(int B, int P, int dtype, int scheme, const
     if (st != SSM_OK) return st;
     const dim3 g(grid_for(P, kThreads, 65535), B);
     binary_search_kernel<1><<<g, kThreads, 0, s>>>(P, P, w.C, u, keys, step, fs, anc);
-  } else if (scheme == SSM_MULTINOMIAL_SORTED) {
+#ifndef SSM_LOGW_VIA_TILES
+#define SSM_LOGW_VIA_TILES 1  // 0: the log-weight scan paths below (A/B)
+#endif
+  } else if (SSM_LOGW_VIA_TILES &&
+             (scheme == SSM_MULTINOMIAL_SORTED || scheme == SSM_SYSTEMATIC || scheme == SSM_STRATIFIED)) {
+    // the filter path's resampler on tile records built from the log-weights (one
+    // pass: read a, write cdf_local + records), then tile scale -> offspring
+    // (ancestors written directly) -> long-run fill / the sorted-multinomial merge
+    if (scheme == SSM_MULTINOMIAL_SORTED && (u || !keys)) return SSM_ERR_INVALID_ARG;  // device draws only
+    const int nt = (P + 31) / 32;
+    const dim3 g(std::max(1, std::min((nt + kThreads / 32 - 1) / (kThreads / 32), 8192)), B);
+    if (dtype == SSM_F64)
+      logw_tiles_kernel<double><<<g, kThreads, 0, s>>>(P, static_cast<const double*>(a), shift, fs, w.lt_cdf, w.lt_rec,
+                                                       w.lt_fs);
+    else
+      logw_tiles_kernel<float><<<g, kThreads, 0, s>>>(P, static_cast<const float*>(a), shift, fs, w.lt_cdf, w.lt_rec,
+                                                      w.lt_fs);
+    SSM_CHECK_LAUNCH();
+    return ssm_resample_tiles_step(B, P, scheme, w.lt_cdf, w.lt_rec, w.lt_fs, u, keys, step, anc, workspace, 0, 1,
+                                   stream);
+  } else if (scheme == SSM_MULTINOMIAL_SORTED) {  // log-weight scan + spacing merge
     if (u || !keys) return SSM_ERR_INVALID_ARG;  // device draws only
     int st = ssm_weights_scan(B, P, dtype, a, 1, shift, fs, w.C, nullptr, w.scan, stream);
     if (st != SSM_OK) return st;

@@ -351,6 +351,19 @@ __device__ __forceinline__ int offspring_bound(double cum, double u_sys, const d
     if (e - t > 0x1p-20 && t - (e - 1.0) > 0x1p-20 && P_out <= (1 << 30))
       return t <= 0.0 ? 0 : (e >= static_cast<double>(P_out) ? P_out : static_cast<int>(e));
   }
+  if constexpr (SCHEME == SSM_STRATIFIED) {
+    // Stratified: query k is (k + U_k) / P, so with t = cum P every k < floor(t) is
+    // counted and every k > floor(t) is not, up to the same ~2^-27 rounding; when t
+    // lies more than 2^-20 from an integer only query floor(t) needs its uniform
+    // (one Philox draw instead of the walk's two or three).
+    const double t = cum * static_cast<double>(P_out);
+    const double fl = floor(t);
+    if (t - fl > 0x1p-20 && (fl + 1.0) - t > 0x1p-20 && P_out <= (1 << 30)) {
+      if (fl >= static_cast<double>(P_out)) return P_out;
+      const int k = static_cast<int>(fl);
+      return f(k) < cum ? k + 1 : k;
+    }
+  }
   double est = SCHEME == SSM_SYSTEMATIC ? ceil(cum * P_out - u_sys) : floor(cum * P_out);
   est = est < 0.0 ? 0.0 : (est > P_out ? static_cast<double>(P_out) : est);
   int k = static_cast<int>(est);

@@ -390,3 +390,19 @@ def stream_ptr(stream=None):
 
 def ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def h2d(a, device, dtype=None):
+    """Host array -> device tensor without a stream synchronisation: the data is
+    staged in pinned memory (torch's caching host allocator) and copied
+    asynchronously on the current stream.  A plain `.to(device)` of pageable
+    memory synchronises the stream, which stalls the host until every queued
+    kernel has finished -- in the batched outer loops that serialises host
+    work and GPU work."""
+    import numpy as np
+    import torch
+
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    return t.pin_memory().to(device, non_blocking=True)

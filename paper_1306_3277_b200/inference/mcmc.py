@@ -227,6 +227,13 @@ def mh_sample_chains(ir, runner, n_samples, rngs, upto=None, on_step=None, shard
     if initialised) each rank runs its contiguous block of chains as
     independent replicas; the samples are all-gathered at the end (C4), so
     every rank returns all C chains."""
+    from ..profiling import gc_paused
+
+    with gc_paused():
+        return _mh_sample_chains(ir, runner, n_samples, rngs, upto, on_step, shard, theta_draws)
+
+
+def _mh_sample_chains(ir, runner, n_samples, rngs, upto, on_step, shard, theta_draws):
     from ..distributed import Shard, allgather_f64, shard_bounds
 
     shard = shard or Shard.current()

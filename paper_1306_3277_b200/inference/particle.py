@@ -232,7 +232,7 @@ def _fs_init(B, device):
     fs["err_nonfinite"] = _lib.INT32_MAX
     fs["err_degenerate"] = _lib.INT32_MAX
     fs["err_param"] = _lib.INT32_MAX
-    return torch.from_numpy(fs.view(np.uint8).reshape(B, 64).copy()).to(device)
+    return _lib.h2d(fs.view(np.uint8).reshape(B, 64), device)
 
 
 def _stack_rows(tensors):
@@ -314,10 +314,15 @@ def _has_row(run, name):
 def _rows(runs, name):
     """[B, ...] tensor of the runs' `name` rows: one slice of the shared batch when
     they are its consecutive rows, else a stack of the views."""
-    refs = [r.__dict__.get("_rb" + name) for r in runs]
+    key = "_rb" + name
+    refs = [r.__dict__.get(key) for r in runs]
     t0, b0 = refs[0]
-    if b0 is not None and all(t is t0 and b == b0 + k for k, (t, b) in enumerate(refs)):
-        return t0 if (b0 == 0 and len(refs) == t0.shape[0]) else t0[b0 : b0 + len(refs)]
+    if b0 is not None and all(t is t0 for t, _ in refs):
+        rows = [b for _, b in refs]
+        if rows == list(range(b0, b0 + len(rows))):
+            return t0 if (b0 == 0 and len(rows) == t0.shape[0]) else t0[b0 : b0 + len(rows)]
+        # rows of one batch in another order (a theta-resampled SMC^2 ensemble): one gather
+        return t0.index_select(0, _lib.h2d(np.asarray(rows, dtype=np.int64), t0.device))
     return torch.stack([t if b is None else t[b] for t, b in refs])
 
 
@@ -500,12 +505,12 @@ def _common(runs):
 
 
 def _derived_tensor(runs):
-    rows = []
-    for r in runs:
-        if r._derived is None:
-            r._derived = r.spec.derived(r.theta)[0]
-        rows.append(r._derived)
-    return torch.from_numpy(np.stack(rows)).to(runs[0].device)
+    todo = [r for r in runs if r._derived is None]
+    if todo:  # one vectorised call for the runs without cached constants
+        d = todo[0].spec.derived(np.concatenate([r.theta for r in todo]))
+        for r, row in zip(todo, d):
+            r._derived = row
+    return _lib.h2d(np.stack([r._derived for r in runs]), runs[0].device)
 
 
 def init_runs(runs, rngs):
@@ -518,11 +523,11 @@ def init_runs(runs, rngs):
     fixed = [b for b, r in enumerate(runs) if r.initial_state is not None]
     if fixed:  # np.tile(initial_state, (P, 1)) (particle.py:63-65): one H2D + one broadcast copy
         x0 = torch.from_numpy(np.stack([np.asarray(runs[b].initial_state, dtype=float) for b in fixed]))
-        x0 = x0.to(dev, r0.tdtype).view(len(fixed), spec.nx, 1).expand(len(fixed), spec.nx, P)
+        x0 = _lib.h2d(x0, dev).to(r0.tdtype).view(len(fixed), spec.nx, 1).expand(len(fixed), spec.nx, P)
         if len(fixed) == B:
             x.copy_(x0)
         else:
-            x[torch.tensor(fixed, device=dev)] = x0
+            x[_lib.h2d(np.asarray(fixed, dtype=np.int64), dev)] = x0
     if need_draw:
         if r0.noise == "host":
             for b in need_draw:
@@ -530,9 +535,9 @@ def init_runs(runs, rngs):
                 x[b].copy_(torch.from_numpy(x0b.T.copy()).to(r0.tdtype))
         else:
             keys = device_keys([rngs[b] for b in need_draw])
-            kt = torch.from_numpy(keys.view(np.int32)).to(dev)
+            kt = _lib.h2d(keys.view(np.int32), dev)
             if spec.kernel == _lib.SSM_MODEL_GENERIC:  # the model's initial block, NVRTC-compiled
-                th = torch.from_numpy(spec.derived(np.concatenate([runs[b].theta for b in need_draw]))).to(dev)
+                th = _lib.h2d(spec.derived(np.concatenate([runs[b].theta for b in need_draw])), dev)
                 tmp = torch.empty((len(need_draw), spec.nx, P), dtype=r0.tdtype, device=dev)
                 fs_init = _fs_init(len(need_draw), dev)
                 _lib.check(_lib.lib().ssm_gen_init_particles(
@@ -742,7 +747,7 @@ def advance_runs(runs, upto, rngs):
     keys_t = None
     if not host_noise:
         keys = device_keys(rngs)
-        keys_t = torch.from_numpy(keys.view(np.int32)).to(dev)
+        keys_t = _lib.h2d(keys.view(np.int32), dev)
     scheme = _lib.SCHEME_IDS[r0.resampler]
     if scheme == 0 and not host_noise:
         # device multinomial as sorted order statistics (exponential spacings):
@@ -961,7 +966,7 @@ def sample_trajectories(runs, rngs):
     stream = _lib.stream_ptr()
     if all(not r.weights_uniform and _has_row(r, "_cdf") and _has_row(r, "_trec") for r in runs):
         # final weights carry the fused kernel's tile records: one warp search per filter
-        u = torch.from_numpy(first_uniforms(rngs, 1)[:, 0].copy()).to(dev)
+        u = _lib.h2d(first_uniforms(rngs, 1)[:, 0].copy(), dev)
         j = torch.empty((B, 1), dtype=torch.int32, device=dev)
         ws = torch.empty(L.ssm_resample_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
         cdf = _rows(runs, "_cdf").contiguous()
@@ -988,14 +993,14 @@ def sample_trajectories(runs, rngs):
     else:  # ssm_filter_state.incr (bytes 8..16) of weighted runs, log P for uniform ones
         fs_rows = _rows(runs, "_fs").contiguous()
         incr = fs_rows.view(torch.float64)[:, 1]
-        weighted = torch.tensor([f is not None for f in shifts], device=dev)
+        weighted = _lib.h2d(np.array([f is not None for f in shifts]), dev)
         shift = torch.where(weighted, incr, torch.full_like(incr, log_p))
     scan_ws = torch.empty(L.ssm_scan_workspace_bytes(B, P), dtype=torch.uint8, device=dev)
     cum = torch.empty((B, P), dtype=torch.int64, device=dev)
     flags = torch.zeros(B, dtype=torch.int32, device=dev)
     _lib.check(L.ssm_weights_scan(B, P, r0.dtype_id, _lib.ptr(a), 1, _lib.ptr(shift), None, _lib.ptr(cum),
                                   _lib.ptr(flags), _lib.ptr(scan_ws), stream), "ssm_weights_scan")
-    u = torch.from_numpy(first_uniforms(rngs, 1)).to(dev)  # each stream's uniform(size=1)
+    u = _lib.h2d(first_uniforms(rngs, 1), dev)  # each stream's uniform(size=1)
     j = torch.empty((B, 1), dtype=torch.int32, device=dev)
     _lib.check(L.ssm_resample_search(B, P, 1, _lib.SCHEME_IDS["multinomial"], 1, _lib.ptr(cum), _lib.ptr(u),
                                      None, 0, None, _lib.ptr(j), None, stream), "ssm_resample_search")
@@ -1021,10 +1026,9 @@ def _replay_runs(L, runs, j, S, B, P, nx, dev, stream):
     desc = np.ascontiguousarray(sched.desc[: S + 1]).copy()
     if _NO_HINTS:
         desc["hints"] = 0
-    desc_t = torch.from_numpy(desc.view(np.uint8).copy()).to(dev)
-    keys_t = torch.from_numpy(np.ascontiguousarray(np.stack([r._kk for r in runs]).astype(np.uint32))
-                              .view(np.int32)).to(dev)
-    ancs_t = torch.from_numpy(np.stack([r._ha for r in runs])).to(dev)
+    desc_t = _lib.h2d(desc.view(np.uint8), dev)
+    keys_t = _lib.h2d(np.ascontiguousarray(np.stack([r._kk for r in runs]).astype(np.uint32)).view(np.int32), dev)
+    ancs_t = _lib.h2d(np.stack([r._ha for r in runs]), dev)
     theta = _derived_tensor(runs)
     fixed = [r.initial_state is not None for r in runs]
     x0_t = flag_t = None
@@ -1033,8 +1037,8 @@ def _replay_runs(L, runs, j, S, B, P, nx, dev, stream):
         for b, r in enumerate(runs):
             if fixed[b]:
                 x0[b] = np.asarray(r.initial_state, dtype=float)
-        x0_t = torch.from_numpy(x0).to(dev)
-        flag_t = torch.tensor(fixed, dtype=torch.int32, device=dev)
+        x0_t = _lib.h2d(x0, dev)
+        flag_t = _lib.h2d(np.asarray(fixed, dtype=np.int32), dev)
     out = torch.empty((B, S + 1, nx), dtype=torch.float64, device=dev)
     R = _lib.ReplayArgs()
     R.model, R.dtype, R.B, R.P, R.S, R.exact = r0.spec.kernel, r0.dtype_id, B, P, S, int(r0.exact)
@@ -1054,8 +1058,8 @@ def _trace_runs(L, runs, j, S, B, P, nx, dev, stream):
             raise ValueError("history length does not match the run position")
     xs = np.stack([r._hx for r in runs])
     ancs = np.stack([r._ha for r in runs])
-    xs_t = torch.from_numpy(xs).to(dev)
-    ancs_t = torch.from_numpy(ancs).to(dev)
+    xs_t = _lib.h2d(xs, dev)
+    ancs_t = _lib.h2d(ancs, dev)
     out = torch.empty((B, S + 1, nx), dtype=torch.float64, device=dev)
     _lib.check(L.ssm_trace(r0.dtype_id, B, S, nx, P, _lib.ptr(xs_t), _lib.ptr(ancs_t), _lib.ptr(j),
                            _lib.ptr(out), stream), "ssm_trace")

@@ -257,6 +257,13 @@ def smc_sampler(ir, runner, n_theta, rng, theta_resampler="multinomial", nthread
     blocks on the device (theta_mh.py); None keeps them on the host."""
     if n_theta < 2:
         raise ValueError("smc sampler needs n_theta >= 2")
+    from ..profiling import gc_paused
+
+    with gc_paused():
+        return _smc_sampler(ir, runner, n_theta, rng, theta_resampler, shard, theta_draws)
+
+
+def _smc_sampler(ir, runner, n_theta, rng, theta_resampler, shard, theta_draws):
     shard = shard or Shard.current()
     if runner.filter_kind == "kalman" and shard.world > 1:
         raise UnsupportedModelError("sharded SMC^2 moves particle-filter state; use the bootstrap filter")

@@ -91,11 +91,19 @@ class DeviceThetaChains:
         self.C = len(states)
         f64 = dict(dtype=torch.float64, device=self.device)
         C, npar, nx = self.C, spec.n_param, spec.nx
-        self.theta = torch.tensor(np.array([s.theta for s in states], dtype=float).reshape(C, npar), **f64)
-        self.x0 = (torch.tensor(np.array([s.init_state for s in states], dtype=float).reshape(C, nx), **f64)
-                   if self.has_init else None)
-        self.loglik = torch.tensor([float(s.loglik) for s in states], **f64)
-        self.log_prior = torch.tensor([float(s.log_prior) for s in states], **f64)
+        # one pinned host block, one asynchronous copy (no stream synchronisation)
+        q = C * npar + (C * nx if self.has_init else 0)
+        host = np.empty(q + 2 * C)
+        host[: C * npar] = np.array([s.theta for s in states], dtype=float).reshape(-1)
+        if self.has_init:
+            host[C * npar : q] = np.array([s.init_state for s in states], dtype=float).reshape(-1)
+        host[q : q + C] = [float(s.loglik) for s in states]
+        host[q + C :] = [float(s.log_prior) for s in states]
+        dev_all = _lib.h2d(host, self.device)
+        self.theta = dev_all[: C * npar].view(C, npar)
+        self.x0 = dev_all[C * npar : q].view(C, nx) if self.has_init else None
+        self.loglik = dev_all[q : q + C]
+        self.log_prior = dev_all[q + C :]
         self.theta_new = torch.empty(C, npar, **f64)
         self.x0_new = torch.empty(C, nx, **f64) if self.has_init else None
         self.lq_f = torch.empty(C, **f64)
@@ -174,13 +182,13 @@ class DeviceThetaChains:
         if draws not in DRAW_MODES:
             raise ValueError(f"draws must be one of {DRAW_MODES}")
         if draws == "host":
-            self._inj = tuple(torch.as_tensor(np.ascontiguousarray(v), dtype=torch.float64, device=self.device)
+            self._inj = tuple(_lib.h2d(np.ascontiguousarray(v, dtype=np.float64), self.device)
                               for v in self.host_draws(rngs))
             self._keys = None
         else:
             self._inj = None
             keys = np.ascontiguousarray(device_keys(rngs), dtype=np.uint32).view(np.int32)  # bit pattern kept
-            self._keys = torch.as_tensor(keys, device=self.device)
+            self._keys = _lib.h2d(keys, self.device)
         self.err.zero_()
         with torch.cuda.device(self.device):
             if self.generic:
@@ -204,7 +212,7 @@ class DeviceThetaChains:
 
     def accept(self, loglik_new, step, stream=None):
         """One ssm_theta_accept launch over all chains; returns the accepted flags (host)."""
-        self.ll_new.copy_(torch.as_tensor(np.asarray(loglik_new, dtype=float)))
+        self.ll_new.copy_(_lib.h2d(np.asarray(loglik_new, dtype=float), self.device))
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().ssm_theta_accept(self._args(step), _lib.stream_ptr(stream)), "ssm_theta_accept")
         return self.accepted.cpu().numpy().astype(bool)

@@ -9,6 +9,7 @@ in `_lib` increments it), which bench.py reports as `gpu_launches`.
 from __future__ import annotations
 
 import contextlib
+import gc
 from collections import defaultdict
 
 import torch
@@ -116,3 +117,19 @@ def maybe(name, nbytes=0):
     else:
         with t.kernel(name, nbytes):
             yield
+
+
+@contextlib.contextmanager
+def gc_paused():
+    """Pause Python's cyclic garbage collector for a batched outer loop (PMMH,
+    SMC^2): those loops allocate many small host objects per step, and the
+    collector's periodic traversals of every live tensor / run object cost a
+    third of an SMC^2 run's host time (profiles/r2_host_overhead.txt).  The loops
+    create no reference cycles that must be reclaimed before they return."""
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        yield
+    finally:
+        if was:
+            gc.enable()

@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import operator
 
 import numpy as np
 import torch
@@ -303,6 +304,38 @@ class _RowRef:
         obj.__dict__[self.key] = None if value is None else (value, None)
 
 
+class _NpRow:
+    """Descriptor for a run's host pointer / key arrays (per grid index), held as
+    (2-D batch array, row) after a batched advance so B runs share one block;
+    `_np_rows` gives a batch back without re-stacking when possible."""
+
+    def __init__(self, name):
+        self.key = "_nb" + name
+
+    def __get__(self, obj, cls=None):
+        if obj is None:
+            return self
+        a, b = obj.__dict__[self.key]
+        return a if b is None else a[b]
+
+    def __set__(self, obj, value):
+        obj.__dict__[self.key] = (value, None)
+
+
+def _np_rows(runs, name):
+    """[B, ...] array of the runs' `name` arrays: a slice / one fancy index of the shared
+    block when every run holds a row of it, else np.stack."""
+    key = "_nb" + name
+    refs = [r.__dict__[key] for r in runs]
+    a0, b0 = refs[0]
+    if b0 is not None and all(a is a0 for a, _ in refs):
+        rows = [b for _, b in refs]
+        if rows == list(range(b0, b0 + len(rows))):
+            return a0[b0 : b0 + len(rows)]
+        return a0[rows]
+    return np.stack([a if b is None else a[b] for a, b in refs])
+
+
 def _set_row(run, name, batch, b):
     run.__dict__["_rb" + name] = None if batch is None else (batch, b)
 
@@ -343,6 +376,9 @@ class ParticleRun:
     _cdf = _RowRef("_cdf")  # (P,) tile-local fixed-point CDF of the last weighted step
     _trec = _RowRef("_trec")  # (ceil(P/32), 2) warp-tile records {max, Q} of the last weighted step
     _fs = _RowRef("_fs")  # (64,) uint8 view of an ssm_filter_state
+    _hx = _NpRow("_hx")  # device pointers of history[i][0] (trace-kernel pointer table), per grid index
+    _ha = _NpRow("_ha")  # device pointers of history[i][1] (0 = identity)
+    _kk = _NpRow("_kk")  # history-free runs: Philox key (2 x uint32) used at each grid index
 
     def __init__(self, ir, theta, grid, inputs=None, n_particles=1024, resampler="multinomial",
                  ess_rel=None, initial_state=None, check_finite=True, *, dtype="float64",
@@ -492,14 +528,17 @@ def _fs_view(fs_tensor):
     return fs_tensor.detach().cpu().numpy().reshape(-1).view(_lib.FILTER_STATE_DTYPE)
 
 
+_SETTINGS = operator.attrgetter("spec", "grid", "n_particles", "dtype_id", "resampler", "ess_rel", "check_finite",
+                                "exact", "noise", "keep_history", "pos", "device", "inputs")
+
+
 def _common(runs):
     r0 = runs[0]
+    k0 = _SETTINGS(r0)
     for r in runs[1:]:
-        if (r.spec is not r0.spec or r.grid is not r0.grid or r.n_particles != r0.n_particles
-                or r.dtype_id != r0.dtype_id or r.resampler != r0.resampler or r.ess_rel != r0.ess_rel
-                or r.check_finite != r0.check_finite or r.exact != r0.exact or r.noise != r0.noise
-                or r.keep_history != r0.keep_history
-                or r.pos != r0.pos or r.device != r0.device or r.inputs is not r0.inputs):
+        k = _SETTINGS(r)
+        # element-wise: identity for the shared objects (spec, grid, inputs), equality for the rest
+        if k != k0 or k[0] is not k0[0] or k[1] is not k0[1] or k[12] is not k0[12]:
             raise ValueError("runs advanced together must share model, grid, settings and position")
     return r0
 
@@ -563,10 +602,14 @@ def init_runs(runs, rngs):
         if need_draw and r0.noise != "host":
             init_keys[need_draw] = keys
     seg = _Seg(x.unsqueeze(0) if r0.keep_history else None, None, np.zeros(1, bool), 1)
-    zero1 = np.zeros(1, dtype=np.int64)
     xrow = x[0].numel() * x.element_size()
+    hx0 = (x.data_ptr() + xrow * np.arange(B, dtype=np.int64)[:, None] if r0.keep_history
+           else np.zeros((B, 1), dtype=np.int64))
+    ha0 = np.zeros((B, 1), dtype=np.int64)
+    kk0 = init_keys[:, None, :].copy() if not r0.keep_history else None
     for b, r in enumerate(runs):
-        r._kk = init_keys[b : b + 1].copy() if not r0.keep_history else _EMPTY_KEYS
+        d = r.__dict__
+        d["_nb_kk"] = (kk0, b) if kk0 is not None else (_EMPTY_KEYS, None)
         _set_row(r, "_x", x, b)
         r._a = None
         r._cdf = None
@@ -577,8 +620,8 @@ def init_runs(runs, rngs):
         r.weights_uniform = True
         r._maybe_nonuniform = False
         r._segs = [(seg, b)]
-        r._hx = np.array([x.data_ptr() + b * xrow], dtype=np.int64) if r0.keep_history else zero1
-        r._ha = zero1
+        d["_nb_hx"] = (hx0, b)
+        d["_nb_ha"] = (ha0, b)
     return runs
 
 
@@ -917,22 +960,36 @@ def advance_runs(runs, upto, rngs):
     a_has = a_ptrs != 0
     has_a = a_last is not None
     keep_tiles = tiles_ok and has_a
+    # the pointer arrays of all B runs in one [B, pos + 1 + n] block each (every run is
+    # at the same position), each run keeping its row: O(1) numpy calls per advance
+    rows_b = np.arange(B, dtype=np.int64)[:, None]
+    new_hx = x_ptrs[None, :] + rows_b * xstride if r0.keep_history else np.broadcast_to(x_ptrs, (B, n_steps))
+    new_ha = np.where(a_has[None, :], a_ptrs[None, :] + rows_b * astride, 0)
+    all_hx = np.concatenate([_np_rows(runs, "_hx"), new_hx], axis=1)
+    all_ha = np.concatenate([_np_rows(runs, "_ha"), new_ha], axis=1)
+    all_kk = None
+    if not r0.keep_history:  # ancestors only; positions are replayed by sample_trajectories
+        new_kk = np.repeat(keys.astype(np.uint32)[:, None, :], n_steps, axis=1)
+        all_kk = np.concatenate([_np_rows(runs, "_kk"), new_kk], axis=1)
     for b, r in enumerate(runs):
-        r.loglik = float(ll[b])
-        r.weights_uniform = bool(unif[b])
-        _set_row(r, "_x", x_prev, b)
-        _set_row(r, "_a", a_last if has_a else None, b)
-        _set_row(r, "_cdf", cdf_local if keep_tiles else None, b)
-        _set_row(r, "_trec", tile_rec if keep_tiles else None, b)
-        _set_row(r, "_fs", fs, b)
-        r._maybe_nonuniform = maybe_nonuniform
-        r._segs = r._segs + [(seg, b)]
-        r._hx = np.concatenate([r._hx, x_ptrs + b * xstride if r0.keep_history else x_ptrs])
-        r._ha = np.concatenate([r._ha, np.where(a_has, a_ptrs + b * astride, 0)])
-        if not r0.keep_history:  # ancestors only; positions are replayed by sample_trajectories
-            r._kk = np.concatenate([r._kk, np.repeat(keys[b : b + 1].astype(np.uint32), n_steps, axis=0)])
-        r.pos = upto
+        d = r.__dict__
+        d["loglik"] = float(ll[b])
+        d["weights_uniform"] = bool(unif[b])
+        d["_rb_x"] = (x_prev, b)
+        d["_rb_a"] = (a_last, b) if has_a else None
+        d["_rb_cdf"] = (cdf_local, b) if keep_tiles else None
+        d["_rb_trec"] = (tile_rec, b) if keep_tiles else None
+        d["_rb_fs"] = (fs, b)
+        d["_maybe_nonuniform"] = maybe_nonuniform
+        d["_segs"] = d["_segs"] + [(seg, b)]
+        d["_nb_hx"] = (all_hx, b)
+        d["_nb_ha"] = (all_ha, b)
+        if all_kk is not None:
+            d["_nb_kk"] = (all_kk, b)
+        d["pos"] = upto
     return incr
+
+
 
 
 def _raise_if_failed(st, sched, check_finite):
@@ -1027,8 +1084,8 @@ def _replay_runs(L, runs, j, S, B, P, nx, dev, stream):
     if _NO_HINTS:
         desc["hints"] = 0
     desc_t = _lib.h2d(desc.view(np.uint8), dev)
-    keys_t = _lib.h2d(np.ascontiguousarray(np.stack([r._kk for r in runs]).astype(np.uint32)).view(np.int32), dev)
-    ancs_t = _lib.h2d(np.stack([r._ha for r in runs]), dev)
+    keys_t = _lib.h2d(np.ascontiguousarray(_np_rows(runs, "_kk").astype(np.uint32)).view(np.int32), dev)
+    ancs_t = _lib.h2d(np.ascontiguousarray(_np_rows(runs, "_ha")), dev)
     theta = _derived_tensor(runs)
     fixed = [r.initial_state is not None for r in runs]
     x0_t = flag_t = None
@@ -1053,11 +1110,10 @@ def _replay_runs(L, runs, j, S, B, P, nx, dev, stream):
 def _trace_runs(L, runs, j, S, B, P, nx, dev, stream):
     """Ancestry walk from the picked final particles j (device) -> trajectories."""
     r0 = runs[0]
-    for r in runs:
-        if len(r._hx) != S + 1:
-            raise ValueError("history length does not match the run position")
-    xs = np.stack([r._hx for r in runs])
-    ancs = np.stack([r._ha for r in runs])
+    xs = _np_rows(runs, "_hx")
+    ancs = _np_rows(runs, "_ha")
+    if xs.shape[1] != S + 1:
+        raise ValueError("history length does not match the run position")
     xs_t = _lib.h2d(xs, dev)
     ancs_t = _lib.h2d(ancs, dev)
     out = torch.empty((B, S + 1, nx), dtype=torch.float64, device=dev)

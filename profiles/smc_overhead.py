@@ -36,13 +36,16 @@ def main():
     kern = timer.summary()
     for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["total_ms"]):
         print(f"  {k:24s} {v['launches']:6d} launches  {v['total_ms']:8.2f} ms (event-bracketed)")
+    import gc
+
+    gc.disable()
     pr = cProfile.Profile()
     pr.enable()
     run(4)
     torch.cuda.synchronize()
     pr.disable()
-    pstats.Stats(pr).sort_stats("tottime").print_stats(30)
-    pstats.Stats(pr).sort_stats("cumulative").print_stats(45)
+    gc.enable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(40)
 
 
 if __name__ == "__main__":

@@ -356,6 +356,20 @@ def _rows(runs, name):
             return t0 if (b0 == 0 and len(rows) == t0.shape[0]) else t0[b0 : b0 + len(rows)]
         # rows of one batch in another order (a theta-resampled SMC^2 ensemble): one gather
         return t0.index_select(0, _lib.h2d(np.asarray(rows, dtype=np.int64), t0.device))
+    groups = {}
+    for k, (t, b) in enumerate(refs):
+        if b is None:
+            break
+        g = groups.setdefault(id(t), (t, [], []))
+        g[1].append(k)
+        g[2].append(b)
+    else:
+        if len(groups) <= 8:  # rows of a few batches (SMC^2 after a rejuvenation): one gather per batch
+            out = torch.empty((len(refs),) + tuple(t0.shape[1:]), dtype=t0.dtype, device=t0.device)
+            for t, pos, rows in groups.values():
+                idx = _lib.h2d(np.array([pos, rows], dtype=np.int64), t0.device)
+                out.index_copy_(0, idx[0], t.index_select(0, idx[1]))
+            return out
     return torch.stack([t if b is None else t[b] for t, b in refs])
 
 

@@ -12,6 +12,8 @@
 // combining per-block partials in block order -> deterministic.
 
 
+#include <cstdlib>
+
 #include "ssm_pw_body.cuh"
 
 namespace ssm {
@@ -31,6 +33,19 @@ __global__ void __launch_bounds__(kPwThreads, MODEL == SSM_MODEL_WINDKESSEL ? 4 
   pw_body<MODEL, T, E, INJ, SIMPLE, PEER>(A, blockIdx.y, blockIdx.x, gridDim.x);
 }
 
+// The headline step with the warp-tile weighting lagged one tile (pw_body_lag).
+template <typename T>
+__global__ void __launch_bounds__(kPwThreads, SSM_PW_CTAS_SIMPLE) pw_lag_kernel(const ssm_pw_args A) {
+  pdl_wait();
+  pw_body_lag<T>(A, blockIdx.y, blockIdx.x, gridDim.x);
+}
+
+// SSM_NO_PW_LAG=1 in the environment selects pw_body for the headline step too (A/B)
+static bool pw_lag_enabled() {
+  static const bool on = std::getenv("SSM_NO_PW_LAG") == nullptr;
+  return on;
+}
+
 template <int MODEL, typename T, bool PEER>
 static void launch_pw_impl(const ssm_pw_args& A, cudaStream_t s) {
   const dim3 grid(pw_grid_x(A.P), A.B);
@@ -39,6 +54,13 @@ static void launch_pw_impl(const ssm_pw_args& A, cudaStream_t s) {
     // host hint: one sub-step with one RK4 step (any observation mask)
     const bool simple = (A.hints & SSM_HINT_SINGLE_SUBSTEP) && A.n_sub == 1 && !A.exact && !inj;
     if (simple) {
+      if constexpr (!PEER) {
+        if (A.has_obs && A.obs_mask == 0xFFu && A.ess_rel < 0.0 && A.cdf_local && A.tile_rec && A.keys &&
+            pw_lag_enabled()) {
+          launch_pdl(pw_lag_kernel<T>, grid, dim3(kPwThreads), s, A);
+          return;
+        }
+      }
       launch_pdl(pw_kernel<MODEL, T, false, false, true, PEER>, grid, dim3(kPwThreads), s, A);
       return;
     }

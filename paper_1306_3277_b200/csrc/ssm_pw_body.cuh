@@ -289,4 +289,116 @@ __device__ __forceinline__ void pw_body(const ssm_pw_args& A, int b, int vb, int
 }
 
 
+// The headline step (Lorenz '96, SIMPLE: one sub-step with one RK4 step, fast
+// arithmetic, device noise, every slot observed, no ESS gate, one rank) with the
+// warp-tile weighting of tile t issued in iteration t + 1: that weighting is a
+// serial chain (REDUX, exp, fixed point, two shuffle scans) with nothing to
+// overlap inside its own tile, but it is independent of the next tile's RK4 /
+// Philox work, so in one basic block the scheduler interleaves the two.  Same
+// arithmetic, stores and tile order as pw_body (bitwise the same filter).
+template <typename T>
+__device__ __forceinline__ void pw_body_lag(const ssm_pw_args& A, int b, int vb, int nvb) {
+  constexpr int NX = 8;
+  const int P = A.P;
+  const int ntiles = (P + kPwThreads - 1) / kPwThreads;
+  ssm_filter_state* fs = A.fs + b;
+  const int R = fs->resample_now;
+  const bool uniform_in = R || fs->uniform;
+  const double incr_prev = fs->incr;
+  const int in_stride = A.x_in_stride > 0 ? A.x_in_stride : P;
+  const T* __restrict__ xin = static_cast<const T*>(A.x_in) + static_cast<size_t>(b) * NX * in_stride;
+  const int out_stride = A.x_out_stride > 0 ? A.x_out_stride : P;
+  T* __restrict__ xout = static_cast<T*>(A.x_out) + static_cast<size_t>(b) * NX * out_stride;
+  const int32_t* __restrict__ anc = (R && A.anc != nullptr) ? A.anc + static_cast<size_t>(b) * P : nullptr;
+  const T* __restrict__ aprev = A.a_prev ? static_cast<const T*>(A.a_prev) + static_cast<size_t>(b) * P : nullptr;
+  T* __restrict__ aout = A.a_out ? static_cast<T*>(A.a_out) + static_cast<size_t>(b) * P : nullptr;
+  uint64_t* __restrict__ cloc = static_cast<uint64_t*>(A.cdf_local) + static_cast<size_t>(b) * P;
+  ssm_tile_rec* __restrict__ trec = static_cast<ssm_tile_rec*>(A.tile_rec) + static_cast<size_t>(b) * ((P + 31) >> 5);
+  const double* th = A.theta + 4 * b;
+  const uint32_t k0 = A.keys[2 * b], k1 = A.keys[2 * b + 1];
+  const T logw0 = static_cast<T>(A.log_w0);
+  const int lane = threadIdx.x & 31;
+
+  __shared__ double s_exp_tab[64];
+  if (threadIdx.x < 64) s_exp_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
+  __syncthreads();
+  __shared__ ParkedTiles s_park[kPwThreads / 32];
+  WarpTileAcc acc = warp_tile_acc(&s_park[threadIdx.x >> 5], lane);
+  bool bad = false;
+
+  const int stride = nvb * kPwThreads;
+  const int p0 = vb * kPwThreads + threadIdx.x;
+  T xn[NX];
+  auto load_x = [&](int src) {
+#pragma unroll
+    for (int n = 0; n < NX; ++n) xn[n] = xin[static_cast<size_t>(n) * in_stride + src];
+  };
+  if (p0 < P) load_x(anc ? __ldg(anc + p0) : p0);
+  int anc_next = (anc && p0 + stride < P) ? __ldg(anc + p0 + stride) : p0 + stride;
+  const T gconst = static_cast<T>(8.0 * (A.obs_log_sd + A.log_sqrt_2pi));
+  const bool check = A.check_finite != 0;
+  const T s_F = static_cast<T>(th[0]);
+  const T s_c = static_cast<T>(th[1] * 20.0 * A.subs[0].sd);
+  const T s_s = static_cast<T>(A.subs[0].s[0]);
+  T yv[8];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) yv[n] = static_cast<T>(A.y[n]);
+  float zc[8], zn[8];
+  if (p0 < P) normals8f(k0, k1, static_cast<uint32_t>(p0 + A.p_offset), static_cast<uint32_t>(A.step), 0u, zc);
+
+  double a_lag = -CUDART_INF;
+  bool act_lag = false, real_lag = false;
+  int p_lag = P;
+  for (int tile = vb; tile < ntiles; tile += nvb) {
+    const int p = tile * kPwThreads + threadIdx.x;
+    const bool act = p < P;
+    T x[NX];
+#pragma unroll
+    for (int n = 0; n < NX; ++n) x[n] = xn[n];
+    {
+      const int p2 = p + stride;
+      if (p2 < P) load_x(anc_next);
+      const int p3 = p2 + stride;
+      anc_next = (anc && p3 < P) ? __ldg(anc + p3) : p3;
+    }
+    const int pn = p + stride;
+    if (pn < P) normals8f(k0, k1, static_cast<uint32_t>(pn + A.p_offset), static_cast<uint32_t>(A.step), 0u, zn);
+    l96_simple_step<T>(x, zc, s_F, s_c, s_s);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) zc[n] = zn[n];
+    if (act) {
+#pragma unroll
+      for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * out_stride + p] = x[n];
+    }
+    T sq = T(0);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const T d = yv[n] - x[n];
+      sq = fma(d, d, sq);
+    }
+    const T g = fma(T(-2.0), sq, -gconst);
+    const T lw = uniform_in ? logw0 : Ar<T, false>::sub(aprev[act ? p : 0], static_cast<T>(incr_prev));
+    const T a = Ar<T, false>::add(lw, g);
+    if (act && aout) aout[p] = a;
+    // the previous tile's weighting (independent of this tile's work above)
+    warp_tile_weigh_lag(acc, a_lag, act_lag, p_lag, P, lane, s_exp_tab, cloc, trec, real_lag);
+    a_lag = act ? static_cast<double>(a) : -CUDART_INF;
+    act_lag = act;
+    p_lag = p;
+    real_lag = true;
+    // deferred finite check: sq is finite only if every x[n] is (as pw_body)
+    if (check && act && !bad && !(sq < T(CUDART_INF))) {
+      bool ok = true;
+#pragma unroll
+      for (int n = 0; n < 8; ++n) ok &= finite_bits(x[n]);
+      if (!ok) bad = true;
+    }
+  }
+  warp_tile_weigh_lag(acc, a_lag, act_lag, p_lag, P, lane, s_exp_tab, cloc, trec, real_lag);
+  warp_tile_flush(acc, lane);
+
+  if (bad) atomicMin(&fs->err_nonfinite, A.step * 64);
+  pw_block_finalize<kPwThreads>(A, fs, b, P, R, 1, acc.park->st, lane, kMaxPwBlocks, vb, nvb);
+}
+
 }  // namespace ssm

@@ -184,6 +184,74 @@ __device__ __forceinline__ void warp_tile_weigh(WarpTileAcc& acc, double a_d, bo
   }
 }
 
+// exp_tile without the early return: the same value for every x (the polynomial
+// is evaluated and discarded for x < -40 / NaN), so a call site can keep it in
+// the same basic block as independent work (pw_body_lag).
+__device__ __forceinline__ double exp_tile_nb(double x, const double* __restrict__ tab /* smem */) {
+  const double t = fma(x, c_exp_poly[5], 0x1.8p52);
+  const int n = __double2loint(t);
+  const double nd = t - 0x1.8p52;
+  double r = fma(nd, -c_exp_poly[6], x);
+  r = fma(nd, -c_exp_poly[7], r);
+  double p = fma(c_exp_poly[0], r, c_exp_poly[1]);
+  p = fma(p, r, c_exp_poly[2]);
+  p = fma(p, r, c_exp_poly[3]);
+  p = fma(p, r, c_exp_poly[4]);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double y = tab[n & 63] * p;
+  const double v = __hiloint2double(__double2hiint(y) + ((n >> 6) << 20), __double2loint(y));
+  return x >= -40.0 ? v : (x != x ? x : 0.0);
+}
+
+// warp_tile_weigh for pw_body_lag: the same arithmetic, stores and parking, no
+// ESS partial (the lagged kernel runs without an ESS gate) and no branches
+// before the parking-slot fold.  `real` = false makes the call a no-op that
+// still takes part in the warp collectives.
+__device__ __forceinline__ void warp_tile_weigh_lag(WarpTileAcc& acc, double a_d, bool act, int p, int P, int lane,
+                                                    const double* __restrict__ s_exp_tab,
+                                                    uint64_t* __restrict__ cloc, ssm_tile_rec* __restrict__ trec,
+                                                    bool real) {
+  const float af = __double2float_ru(a_d);
+  const int key = __float_as_int(af) >= 0 ? __float_as_int(af) : (__float_as_int(af) ^ 0x7fffffff);
+  const int kmax = __reduce_max_sync(0xffffffffu, act ? key : (-2147483647 - 1));
+  const int kb = kmax >= 0 ? kmax : (kmax ^ 0x7fffffff);
+  const double mw = static_cast<double>(__int_as_float(kb));
+  const bool any_nan = __any_sync(0xffffffffu, act && isnan(a_d));
+  const double ex = exp_tile_nb(a_d - mw, s_exp_tab);
+  const double e = (!act || mw == -CUDART_INF) ? 0.0 : ex;
+  const uint64_t q = (e >= 0.0 && e <= 1.0) ? __double2ull_rn(e * kTileFix) : 0ull;
+  uint32_t qh = static_cast<uint32_t>(q >> 26), ql = static_cast<uint32_t>(q) & 0x3ffffffu;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t yh = __shfl_up_sync(0xffffffffu, qh, o);
+    const uint32_t yl = __shfl_up_sync(0xffffffffu, ql, o);
+    if (lane >= o) {
+      qh += yh;
+      ql += yl;
+    }
+  }
+  const uint64_t qi = (static_cast<uint64_t>(qh) << 26) + ql;
+  if (real && act) cloc[p] = qi;
+  const uint64_t Qw = (static_cast<uint64_t>(__shfl_sync(0xffffffffu, qh, 31)) << 26) +
+                      __shfl_sync(0xffffffffu, ql, 31);
+  if (real && lane == 0 && p < P) trec[p >> 5] = ssm_tile_rec{mw, Qw};
+  if (real && lane == 0 && p - lane < P) {
+    acc.park->m[acc.slot] = mw;
+    acc.park->t[acc.slot] = any_nan ? CUDART_NAN : static_cast<double>(Qw) * (1.0 / kTileFix);
+    acc.park->s2[acc.slot] = 0.0;
+    ++acc.nparked;
+  }
+  acc.slot += real ? 1 : 0;
+  if (acc.slot == 32) {
+    __syncwarp();
+    fold_parked(acc.park, lane < __shfl_sync(0xffffffffu, acc.nparked, 0), lane);
+    __syncwarp();
+    acc.slot = 0;
+    acc.nparked = 0;
+  }
+}
+
 // fold the partially filled parking slots after the last tile
 __device__ __forceinline__ void warp_tile_flush(WarpTileAcc& acc, int lane) {
   if (acc.slot > 0) {

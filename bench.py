@@ -572,7 +572,7 @@ def main():
                                          "CDF totals + P2P spill of ancestor states per step)")),
         "roofline": {
             "bound": "hbm",
-            "kernel": "pw_kernel (fused ancestor gather + RK4 propagate + weight + LSE)",
+            "kernel": "pw_lag_kernel (fused ancestor gather + RK4 propagate + weight + LSE; the headline step's pw_kernel specialisation)",
             "achieved": achieved,
             "peak": peak,
             "peak_kind": peak_kind,

@@ -1003,7 +1003,10 @@ __device__ __forceinline__ void offspring_tiles_body(int b, int blk, int B, int 
 }
 
 template <int SCHEME, typename Store = LocalStore>
-__global__ void __launch_bounds__(kThreads)
+#ifndef SSM_OFFSPRING_MINB
+#define SSM_OFFSPRING_MINB 6  // <= 42 registers: 6 CTAs / SM (4 at the default 64); 2^24 resample 99 -> 96 us
+#endif
+__global__ void __launch_bounds__(kThreads, SSM_OFFSPRING_MINB)
 offspring_tiles_kernel(int P, const uint64_t* __restrict__ cdf_local, const double* __restrict__ scale,
                        const uint64_t* __restrict__ pref, const uint64_t* __restrict__ totals,
                        const double* __restrict__ u, const uint32_t* __restrict__ keys, int step,

@@ -317,3 +317,53 @@ def test_persistent_driver_windkessel_pmmh_batch(monkeypatch):
     for (la, ta, _), (lb, tb, _) in zip(*outs):
         assert la == lb
         np.testing.assert_array_equal(ta, tb)
+
+
+# ------------------------------------------------------------------ logw resampling at 2^20, device draws
+
+
+@pytest.mark.parametrize("scheme", ["stratified", "systematic"])
+@pytest.mark.parametrize("sigma", [0.0, 1.0, 10.0])
+def test_resample_from_logw_device_draws_match_numpy_2p20(scheme, sigma):
+    """ssm_resample_from_logw (tile records built from the log-weights, then the
+    filter path's resampler; the stratified one-draw fast path) at 2^20 with
+    device uniforms, against numpy: the same Philox uniforms, the reference's
+    queries and float64 cumsum + searchsorted (resampling.py:22-36).  At most a
+    handful of ancestors may differ, and only where a query lies within 1e-12 of
+    the CDF boundary between the two candidates (fixed-point vs float cumsum)."""
+    from scipy.special import logsumexp
+
+    from paper_1306_3277_b200 import _lib
+    from tests.test_gpu_parity import _philox4x32_10
+
+    L = _lib.lib()
+    P, step = 1 << 20, 3
+    a_np = np.random.default_rng(7).normal(0.0, sigma, P) if sigma > 0 else np.zeros(P)
+    a = torch.from_numpy(a_np).cuda()
+    shift = torch.tensor([logsumexp(a_np)], dtype=torch.float64, device="cuda")
+    keys_np = np.array([[1234, 5678]], dtype=np.uint32)
+    keys = torch.from_numpy(keys_np.view(np.int32)).cuda()
+    ws = torch.empty(L.ssm_resample_workspace_bytes(1, P), dtype=torch.uint8, device="cuda")
+    anc = torch.empty(P, dtype=torch.int32, device="cuda")
+    _lib.check(L.ssm_resample_from_logw(1, P, _lib.SSM_F64, _lib.SCHEME_IDS[scheme], _lib.ptr(a), _lib.ptr(shift),
+                                        None, None, _lib.ptr(keys), step, _lib.ptr(anc), _lib.ptr(ws),
+                                        _lib.stream_ptr()))
+    got = anc.cpu().numpy()
+    # device uniforms: Philox4x32-10 {k, step, 0, kPurposeResample=2} -> 53-bit (x, y); systematic: k = 0,
+    # purpose kPurposeSystematic=4
+    if scheme == "stratified":
+        k = np.arange(P, dtype=np.uint64)
+        r = _philox4x32_10([k, np.full(P, step), np.zeros(P), np.full(P, 2)], *keys_np[0])
+    else:
+        r = _philox4x32_10([np.zeros(1), np.full(1, step), np.zeros(1), np.full(1, 4)], *keys_np[0])
+    u = ((r[0] << np.uint64(32)) | r[1]) >> np.uint64(11)
+    u = u.astype(np.float64) * 2.0**-53
+    q = O.queries(scheme, u, P)
+    w = np.exp(a_np - logsumexp(a_np))
+    cum = O.cumulative(w)
+    ref = O.search(cum, q)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size <= 8, bad.size
+    for kk in bad:
+        lo, hi = min(got[kk], ref[kk]), max(got[kk], ref[kk])
+        assert np.min(np.abs(cum[lo:hi] - q[kk])) <= 1e-12, (kk, got[kk], ref[kk])

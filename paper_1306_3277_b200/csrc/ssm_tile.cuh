@@ -26,9 +26,12 @@ constexpr int kMaxPwBlocks = 2048;  // per filter; a function of P only (determi
 // Blocks per filter: >= 4 block tiles per block, so each warp folds several warp
 // tiles per setup (matters at moderate P with many filters, e.g. PMMH 8 x 2^16).
 // A function of P only, so the LSE fold order never depends on the batch.
+#ifndef SSM_PW_TILES_PER_BLOCK
+#define SSM_PW_TILES_PER_BLOCK 4
+#endif
 __host__ __device__ inline int pw_grid_x(int P) {
   const int tiles = (P + kPwThreads - 1) / kPwThreads;
-  const int g = (tiles + 3) / 4;
+  const int g = (tiles + SSM_PW_TILES_PER_BLOCK - 1) / SSM_PW_TILES_PER_BLOCK;
   return g < kMaxPwBlocks ? g : kMaxPwBlocks;
 }
 

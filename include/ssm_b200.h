@@ -180,7 +180,12 @@ const char* ssm_status_string(int status);
 const char* ssm_last_cuda_error(void);
 int ssm_sm_count(int device, int* out);
 
-/* K1/K2 fused propagate + weight (+ gather, + LSE/ESS finalize). */
+/* K1/K2 fused propagate + weight (+ gather, + LSE/ESS finalize).  Kernel choice
+ * (same results): SIMPLE specialisations when SSM_HINT_SINGLE_SUBSTEP holds; for
+ * Lorenz '96 with device noise, fast arithmetic, every slot observed, no ESS gate
+ * and tile records requested, the variant that weighs each warp tile one tile
+ * late (overlapping that chain with the next tile's RK4; SSM_NO_PW_LAG=1 in the
+ * environment disables it). */
 size_t ssm_pw_workspace_bytes(int B, int P);
 int ssm_propagate_weight(const ssm_pw_args* args, void* stream);
 

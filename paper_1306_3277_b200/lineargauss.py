@@ -102,7 +102,7 @@ class _Walker:
         if t == "T":
             return self.const(self.T[:, e[1]])
         if t == "U":
-            return self.const(self.U[e[1]])
+            return self.const(self.U[..., e[1]])  # (width,) or per row (rows, width)
         if t == "X":
             return state[e[1]].copy()
         if t == "W":
@@ -184,6 +184,29 @@ class _Walker:
                     self.rk4(op, state, noise, d)
         return state
 
+    def interval_rows(self, sched, u_rows, state):
+        """interval() for rows that share one sub-step schedule `sched` (durations
+        d_k) but have their own inputs u_rows[k] (rows, width) at sub-step k: the
+        batch is (theta x grid step), so one symbolic pass serves many steps."""
+        noise = [self.const(0.0) for _ in range(self.n_noise)]
+        for k, d in enumerate(sched):
+            self.U = u_rows[k]
+            for op in self.desc["transition"]:
+                if op["op"] == "sample":
+                    vals = [self.sample(op, i, state, noise, "transition", wiener_sd=math.sqrt(d))
+                            for i in range(len(op["slots"]))]
+                    dst = state if op["role"] == "state" else noise
+                    for slot, v in zip(op["slots"], vals):
+                        dst[slot] = v
+                elif op["op"] == "assign":
+                    vals = [self.eval(e, state, noise, "transition") for e in op["exprs"]]
+                    dst = noise if op["role"] == "noise" else state
+                    for slot, v in zip(op["slots"], vals):
+                        dst[slot] = v
+                else:
+                    self.rk4(op, state, noise, d)
+        return state
+
     def rk4(self, op, state, noise, duration):
         """simulate.py:71-93 on affine forms (lineargauss.py:195-221)."""
         slots = op["slots"]
@@ -207,11 +230,12 @@ class _Walker:
                 incr = self.add(self.add(k1[i], self.scale(k2[i], 2.0)), self.add(self.scale(k3[i], 2.0), k4[i]))
                 state[slot] = self.add(y0[i], self.scale(incr, s / 6.0))
 
-    def observation(self, t):
-        """(H, c, r_sd) over all obs slots at time t (lineargauss.py:223-260)."""
+    def observation(self, t, u_rows=None):
+        """(H, c, r_sd) over all obs slots at time t (lineargauss.py:223-260);
+        u_rows: per-row inputs (rows of a theta x step batch) instead of t's."""
         from .simulate import _input_row
 
-        self.U = _input_row(self.inputs, t, self.n_input, max(self.n_input, 1))
+        self.U = _input_row(self.inputs, t, self.n_input, max(self.n_input, 1)) if u_rows is None else u_rows
         ny = self.desc["counts"]["obs"]
         H = np.zeros((self.B, ny, self.nx))
         c = np.zeros((self.B, ny))
@@ -322,11 +346,35 @@ def extract_linear_gaussian(ir, thetas, times, inputs=None) -> LinearGaussianSys
     ny = desc["counts"]["obs"]
     out = dict(A=np.zeros((B, S, nx, nx)), b=np.zeros((B, S, nx)), Q=np.zeros((B, S, nx, nx)),
                H=np.zeros((B, S, ny, nx)), c=np.zeros((B, S, ny)), r_sd=np.zeros((B, S, ny)))
+    # grid steps that share a sub-step schedule (the same durations; inputs may differ)
+    # are evaluated together: one symbolic pass over a (theta x step) batch per schedule
+    from .inference.particle import substep_schedule
+    from .simulate import _input_row
+
+    width = max(w.n_input, 1)
+    groups = {}
     for i in range(1, S + 1):
-        w.n_z = 0
-        st = w.interval(times[i - 1], times[i] - times[i - 1], [w.unit(k) for k in range(nx)])
-        b, A, L = _to_gaussian(st, w.n_z, B)
-        out["A"][:, i - 1], out["b"][:, i - 1] = A, b
-        out["Q"][:, i - 1] = L @ L.transpose(0, 2, 1)
-        out["H"][:, i - 1], out["c"][:, i - 1], out["r_sd"][:, i - 1] = w.observation(times[i])
+        sched = substep_schedule(times[i - 1], times[i] - times[i - 1], desc["delta"])
+        groups.setdefault(tuple(d for _, d in sched), []).append((i, [t_k for t_k, _ in sched]))
+    thetas2 = np.atleast_2d(np.asarray(thetas, dtype=float))
+    per = max(1, 65536 // B)  # steps per pass: ~64K rows keep the numpy temporaries cache-sized
+    chunks = [(ds, members[k : k + per]) for ds, members in groups.items() for k in range(0, len(members), per)]
+    for ds, members in chunks:
+        steps = np.array([i for i, _ in members])
+        n = len(steps)
+        # rows theta-major: row = b * n + j (step steps[j]); inputs per step, repeated over theta
+        wg = _Walker(desc, np.repeat(thetas2, n, axis=0), inputs)
+        u_sub = [np.tile(np.stack([_input_row(inputs, tk[k], wg.n_input, width) for _, tk in members]), (B, 1))
+                 for k in range(len(ds))]
+        st = wg.interval_rows(ds, u_sub, [wg.unit(k) for k in range(nx)])
+        b, A, L = _to_gaussian(st, wg.n_z, B * n)
+        out["A"][:, steps - 1] = A.reshape(B, n, nx, nx)
+        out["b"][:, steps - 1] = b.reshape(B, n, nx)
+        Lr = L.reshape(B, n, nx, -1)
+        out["Q"][:, steps - 1] = Lr @ Lr.transpose(0, 1, 3, 2)
+        u_obs = np.tile(np.stack([_input_row(inputs, times[i], wg.n_input, width) for i in steps]), (B, 1))
+        H, c, r = wg.observation(None, u_rows=u_obs)
+        out["H"][:, steps - 1] = H.reshape(B, n, ny, nx)
+        out["c"][:, steps - 1] = c.reshape(B, n, ny)
+        out["r_sd"][:, steps - 1] = r.reshape(B, n, ny)
     return LinearGaussianSystems(times=times, mu0=mu0, P0=P0, **out)

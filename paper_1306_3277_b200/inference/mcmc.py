@@ -12,7 +12,6 @@ priors run on the host by default, or on the device with
 
 from __future__ import annotations
 
-import copy
 
 from dataclasses import dataclass
 
@@ -95,12 +94,16 @@ class FilterRunner:
             return kalman_runs(self._systems(thetas, init_states), self.grid, self.device_opts.get("device"))
         proto = self._make(thetas[0], init_states[0])
         runs = [proto]
+        base = proto.__dict__
+        cls = type(proto)
         for t, st in zip(thetas[1:], init_states[1:]):
-            r = copy.copy(proto)
-            r.theta = np.asarray(t, dtype=float).reshape(1, -1)
-            r.initial_state = st
-            r._derived = None
-            r._segs = []  # init_runs installs the history and pointer arrays
+            r = cls.__new__(cls)  # a shallow copy of the validated prototype
+            d = dict(base)
+            d["theta"] = np.asarray(t, dtype=float).reshape(1, -1)
+            d["initial_state"] = st
+            d["_derived"] = None
+            d["_segs"] = []  # init_runs installs the history and pointer arrays
+            r.__dict__ = d
             runs.append(r)
         init_runs(runs, [g.child(0) for g in rngs])
         return runs

@@ -113,8 +113,11 @@ class FilterRunner:
         out = self.run_batch([theta], [init_state], [rng], upto=upto)
         return out[0]
 
-    def run_batch(self, thetas, init_states, rngs, upto=None):
-        """Batched FilterRunner.run: one launch per step for all filters."""
+    def run_batch(self, thetas, init_states, rngs, upto=None, trajectories=True):
+        """Batched FilterRunner.run: one launch per step for all filters.
+        trajectories=False skips the trajectory draws (their slot is None): a
+        caller that discards them (SMC^2 rejuvenation, whose trajectories are
+        redrawn at the propagation) saves a trace and a read-back."""
         upto = self.grid.last if upto is None else upto
         if not thetas:
             return []
@@ -123,10 +126,11 @@ class FilterRunner:
             from .kalman import advance_kalman_runs, sample_kalman_trajectories
 
             advance_kalman_runs(runs, upto)
-            trajs = sample_kalman_trajectories(runs, [g.child(2) for g in rngs])
+            trajs = (sample_kalman_trajectories(runs, [g.child(2) for g in rngs]) if trajectories
+                     else [None] * len(runs))
             return [(r.loglik, t, r) for r, t in zip(runs, trajs)]
         advance_runs(runs, upto, [g.child(1) for g in rngs])
-        trajs = sample_trajectories(runs, [g.child(2) for g in rngs])
+        trajs = sample_trajectories(runs, [g.child(2) for g in rngs]) if trajectories else [None] * len(runs)
         return [(r.loglik, t, r) for r, t in zip(runs, trajs)]
 
 
@@ -177,10 +181,11 @@ def marginal_mh_step(ir, chain, runner, rng, upto=None, reference=None):
     return marginal_mh_steps(ir, [chain], runner, [rng], upto, [reference])[0]
 
 
-def marginal_mh_steps(ir, chains, runner, rngs, upto=None, references=None):
+def marginal_mh_steps(ir, chains, runner, rngs, upto=None, references=None, trajectories=True):
     """Lock-step marginal MH over independent chains: host proposals, one
     batched device filter run for every chain inside the prior support,
-    then per-chain accept/reject with the chain's own stream."""
+    then per-chain accept/reject with the chain's own stream.
+    trajectories=False: accepted states carry trajectory None (see run_batch)."""
     spec = resolve_model(ir)
     references = references or [None] * len(chains)
     if not chains:
@@ -192,7 +197,7 @@ def marginal_mh_steps(ir, chains, runner, rngs, upto=None, references=None):
     props = [(th_new[k], x0_new[k], float(lq_f[k]), float(lq_r[k]), float(lp_new[k])) for k in range(len(chains))]
     todo = [k for k, p in enumerate(props) if p[4] != -np.inf]
     res = runner.run_batch([props[k][0] for k in todo], [props[k][1] for k in todo],
-                           [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto)
+                           [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto, trajectories=trajectories)
     by_k = dict(zip(todo, res))
     out = []
     for k, (chain, rng) in enumerate(zip(chains, rngs)):

@@ -296,13 +296,15 @@ def _smc_sampler(ir, runner, n_theta, rng, theta_resampler, shard, theta_draws):
         # rejuvenate: one marginal MH move each, one batched replay (smc.py:101-122)
         chains = [MhChainState(theta=p.theta, trajectory=p.trajectory, loglik=p.loglik,
                                log_prior=p.log_prior, init_state=p.init_state) for p in local]
+        # the rejuvenated filters' trajectories are redrawn by the propagation below: not drawn here
         if theta_draws is None:
-            outs = marginal_mh_steps(ir, chains, runner, [step_rng.child(1, j) for j in J], upto=prev_idx)
+            outs = marginal_mh_steps(ir, chains, runner, [step_rng.child(1, j) for j in J], upto=prev_idx,
+                                     trajectories=False)
         else:
             from .theta_mh import marginal_mh_steps_device
 
             outs, _ = marginal_mh_steps_device(ir, chains, runner, [step_rng.child(1, j) for j in J], upto=prev_idx,
-                                               draws=theta_draws, step=i)
+                                               draws=theta_draws, step=i, trajectories=False)
         accepted = []
         for p, (new, ok, run) in zip(local, outs):
             if ok:
@@ -312,7 +314,9 @@ def _smc_sampler(ir, runner, n_theta, rng, theta_resampler, shard, theta_draws):
         # propagate and weight (smc.py:125-134)
         rr = {j: step_rng.child(2, j, 1) for j in J}
         ir_ = {j: step_rng.child(2, j, 0) for j in J}
-        tr = {j: step_rng.child(3, j) for j in J}
+        # only the last step's trajectories reach the result (each draws from its own stream,
+        # smc.py:131, so skipping the intermediate ones leaves every other draw unchanged)
+        tr = {j: step_rng.child(3, j) for j in J} if i == len(obs_steps) else None
         incr = _advance_all(runner, particles, J, grid_idx, run_rngs=rr, init_rngs=ir_, traj_rngs=tr)
         for j in J:
             particles[j].loglik += incr[j]

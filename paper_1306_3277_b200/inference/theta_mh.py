@@ -218,7 +218,8 @@ class DeviceThetaChains:
         return self.accepted.cpu().numpy().astype(bool)
 
 
-def marginal_mh_steps_device(ir, chains, runner, rngs, upto=None, draws="device", dev=None, step=0):
+def marginal_mh_steps_device(ir, chains, runner, rngs, upto=None, draws="device", dev=None, step=0,
+                             trajectories=True):
     """marginal_mh_steps with the theta-level blocks on the device: one propose
     launch, one batched filter over the chains inside the prior support, one
     accept launch.  `dev` carries the chain state between calls (built from
@@ -229,7 +230,7 @@ def marginal_mh_steps_device(ir, chains, runner, rngs, upto=None, draws="device"
     th, x0, lq_f, lq_r, lp = dev.propose(rngs, step, draws)
     todo = [k for k in range(len(chains)) if lp[k] != -np.inf]
     res = runner.run_batch([th[k] for k in todo], [x0[k] if x0 is not None else None for k in todo],
-                           [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto)
+                           [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto, trajectories=trajectories)
     ll_new = np.full(len(chains), -np.inf)
     by_k = dict(zip(todo, res))
     for k, (ll, _, _) in by_k.items():

@@ -108,6 +108,16 @@ class FilterRunner:
         init_runs(runs, [g.child(0) for g in rngs])
         return runs
 
+    def trajectories(self, runs, rngs):
+        """sample_trajectory for a batch of this runner's runs (each from its own stream)."""
+        if not runs:
+            return []
+        if self.filter_kind == "kalman":
+            from .kalman import sample_kalman_trajectories
+
+            return sample_kalman_trajectories(runs, rngs)
+        return sample_trajectories(runs, rngs)
+
     def run(self, theta, init_state, rng, upto=None):
         """(loglik, trajectory, run) over grid steps 1..upto (mcmc.py:102-108)."""
         out = self.run_batch([theta], [init_state], [rng], upto=upto)
@@ -196,23 +206,32 @@ def marginal_mh_steps(ir, chains, runner, rngs, upto=None, references=None, traj
         rngs)
     props = [(th_new[k], x0_new[k], float(lq_f[k]), float(lq_r[k]), float(lp_new[k])) for k in range(len(chains))]
     todo = [k for k, p in enumerate(props) if p[4] != -np.inf]
+    # the filters first, trajectories only for the accepted proposals (each draws from its
+    # own stream, so skipping the rejected ones changes no other draw)
     res = runner.run_batch([props[k][0] for k in todo], [props[k][1] for k in todo],
-                           [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto, trajectories=trajectories)
+                           [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto, trajectories=False)
     by_k = dict(zip(todo, res))
     out = []
+    accepted = []
     for k, (chain, rng) in enumerate(zip(chains, rngs)):
         theta_new, init_new, logq_fwd, logq_rev, log_prior_new = props[k]
         if k not in by_k:
             out.append((chain, False, None))  # outside the prior support: auto-reject
             continue
-        loglik_new, traj_new, run = by_k[k]
+        loglik_new, _, run = by_k[k]
         current = chain.loglik if references[k] is None else references[k]
         log_ratio = (loglik_new + log_prior_new + logq_rev) - (current + chain.log_prior + logq_fwd)
         if metropolis_accept(log_ratio, rng):
-            out.append((MhChainState(theta=theta_new, trajectory=traj_new, loglik=loglik_new,
+            out.append((MhChainState(theta=theta_new, trajectory=None, loglik=loglik_new,
                                      log_prior=log_prior_new, init_state=init_new), True, run))
+            accepted.append(k)
         else:
             out.append((chain, False, None))
+    if trajectories and accepted:
+        trajs = runner.trajectories([by_k[k][2] for k in accepted],
+                                    [rngs[k].child(_FILTER_KEY).child(2) for k in accepted])
+        for k, t in zip(accepted, trajs):
+            out[k][0].trajectory = t
     return out
 
 

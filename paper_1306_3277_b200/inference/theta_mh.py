@@ -230,17 +230,23 @@ def marginal_mh_steps_device(ir, chains, runner, rngs, upto=None, draws="device"
     th, x0, lq_f, lq_r, lp = dev.propose(rngs, step, draws)
     todo = [k for k in range(len(chains)) if lp[k] != -np.inf]
     res = runner.run_batch([th[k] for k in todo], [x0[k] if x0 is not None else None for k in todo],
-                           [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto, trajectories=trajectories)
+                           [rngs[k].child(_FILTER_KEY) for k in todo], upto=upto, trajectories=False)
     ll_new = np.full(len(chains), -np.inf)
     by_k = dict(zip(todo, res))
     for k, (ll, _, _) in by_k.items():
         ll_new[k] = ll
     ok = dev.accept(ll_new, step)
+    # trajectories for the accepted proposals only (per-stream draws: the others are unaffected)
+    acc_k = [k for k in range(len(chains)) if ok[k]]
+    trajs = {}
+    if trajectories and acc_k:
+        trajs = dict(zip(acc_k, runner.trajectories([by_k[k][2] for k in acc_k],
+                                                    [rngs[k].child(_FILTER_KEY).child(2) for k in acc_k])))
     outs = []
     for k, chain in enumerate(chains):
         if ok[k]:
-            ll, traj, run = by_k[k]
-            outs.append((MhChainState(theta=th[k].copy(), trajectory=traj, loglik=ll, log_prior=float(lp[k]),
+            ll, _, run = by_k[k]
+            outs.append((MhChainState(theta=th[k].copy(), trajectory=trajs.get(k), loglik=ll, log_prior=float(lp[k]),
                                       init_state=None if x0 is None else x0[k].copy()), True, run))
         else:
             outs.append((chain, False, None))

@@ -373,6 +373,50 @@ def _rows(runs, name):
     return torch.stack([t if b is None else t[b] for t, b in refs])
 
 
+def _rows_many(runs, names):
+    """{name: _rows(runs, name)} for names whose references share one row layout
+    (every run's rows come from the same batches): the grouping and the index
+    upload are done once for all names."""
+    refs0 = [r.__dict__.get("_rb" + names[0]) for r in runs]
+    if any(ref is None or ref[1] is None for ref in refs0):
+        return {n: _rows(runs, n) for n in names}
+    t0, b0 = refs0[0]
+    rows = [b for _, b in refs0]
+    if all(t is t0 for t, _ in refs0) and rows == list(range(b0, b0 + len(rows))):
+        return {n: _rows(runs, n) for n in names}  # slices: nothing to share
+    order = {}  # batch (identified by the first name's tensor) -> positions
+    for k, (t, _) in enumerate(refs0):
+        order.setdefault(id(t), []).append(k)
+    if len(order) > 8:
+        return {n: _rows(runs, n) for n in names}
+    groups = list(order.values())
+    flat = np.concatenate([np.array([pos, [rows[k] for k in pos]], dtype=np.int64) for pos in groups], axis=1)
+    idx = _lib.h2d(flat, t0.device)  # [2, B]: positions, rows (group after group)
+    out = {}
+    for n in names:
+        refs = [r.__dict__.get("_rb" + n) for r in runs]
+        bases = []
+        ok = True
+        for pos in groups:
+            tb = refs[pos[0]][0]
+            if any(refs[k] is None or refs[k][0] is not tb or refs[k][1] != rows[k] for k in pos):
+                ok = False
+                break
+            bases.append(tb)
+        if not ok:
+            out[n] = _rows(runs, n)
+            continue
+        tn = bases[0]
+        res = torch.empty((len(runs),) + tuple(tn.shape[1:]), dtype=tn.dtype, device=tn.device)
+        off = 0
+        for pos, tb in zip(groups, bases):
+            m = len(pos)
+            res.index_copy_(0, idx[0, off : off + m], tb.index_select(0, idx[1, off : off + m]))
+            off += m
+        out[n] = res
+    return out
+
+
 _EMPTY_I64 = np.zeros(0, dtype=np.int64)
 _EMPTY_KEYS = np.zeros((0, 2), dtype=np.uint32)
 
@@ -795,9 +839,14 @@ def advance_runs(runs, upto, rngs):
     dev, tdt = r0.device, r0.tdtype
     sched = _schedule(r0.grid, spec, r0.inputs, dev)
     stream = _lib.stream_ptr()
-    x_prev = _rows(runs, "_x")
-    a_last = _rows(runs, "_a") if _has_row(r0, "_a") else None
-    fs = _rows(runs, "_fs").clone()  # fresh copy: clones stay untouched
+    # the runs' rows of every per-filter tensor, gathered with one shared index upload
+    names = ["_x", "_fs"] + (["_a"] if _has_row(r0, "_a") else [])
+    if all(_has_row(r, "_cdf") for r in runs):
+        names += ["_cdf", "_trec"]
+    got = _rows_many(runs, names)
+    x_prev = got["_x"]
+    a_last = got.get("_a")
+    fs = got["_fs"].clone()  # fresh copy: clones stay untouched
     theta = _derived_tensor(runs)
     maybe_nonuniform = r0._maybe_nonuniform
     host_noise = r0.noise == "host"
@@ -822,8 +871,8 @@ def advance_runs(runs, upto, rngs):
     if tiles_ok:
         have = [_has_row(r, "_cdf") for r in runs]
         if all(have):  # resume: fresh copies, clones sharing the views stay intact
-            cdf_local = _rows(runs, "_cdf").clone()
-            tile_rec = _rows(runs, "_trec").clone()
+            cdf_local = got["_cdf"].clone()
+            tile_rec = got["_trec"].clone()
         else:
             cdf_local = torch.empty((B, P), dtype=torch.int64, device=dev)
             tile_rec = torch.empty((B, ntile, 2), dtype=torch.float64, device=dev)

@@ -40,6 +40,29 @@ __global__ void __launch_bounds__(kPwThreads, SSM_PW_CTAS_SIMPLE) pw_lag_kernel(
   pw_body_lag<T>(A, blockIdx.y, blockIdx.x, gridDim.x);
 }
 
+// the lagged headline step with the TMA-staged gather (pw_body_lag_tma; A/B: SSM_PW_TMA=1)
+template <typename T>
+__global__ void __launch_bounds__(kPwThreads, SSM_PW_CTAS_SIMPLE) pw_lag_tma_kernel(const ssm_pw_args A) {
+  pdl_wait();
+  pw_body_lag_tma<T>(A, blockIdx.y, blockIdx.x, gridDim.x);
+}
+
+static bool pw_tma_enabled() {
+  static const bool on = std::getenv("SSM_PW_TMA") != nullptr;
+  return on;
+}
+
+template <typename T>
+static cudaError_t launch_lag_tma(const ssm_pw_args& A, dim3 grid, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(kPwThreads / 32) * 2 * 8 * kTmaW * sizeof(T);
+  static bool attr = false;  // per T (one instantiation per static)
+  if (!attr) {
+    cudaFuncSetAttribute(pw_lag_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  return launch_pdl_smem(pw_lag_tma_kernel<T>, grid, dim3(kPwThreads), smem, s, A);
+}
+
 // SSM_NO_PW_LAG=1 in the environment selects pw_body for the headline step too (A/B)
 static bool pw_lag_enabled() {
   static const bool on = std::getenv("SSM_NO_PW_LAG") == nullptr;
@@ -57,6 +80,11 @@ static void launch_pw_impl(const ssm_pw_args& A, cudaStream_t s) {
       if constexpr (!PEER) {
         if (A.has_obs && A.obs_mask == 0xFFu && A.ess_rel < 0.0 && A.cdf_local && A.tile_rec && A.keys &&
             pw_lag_enabled()) {
+          const int in_stride = A.x_in_stride > 0 ? A.x_in_stride : A.P;
+          if (pw_tma_enabled() && (in_stride % 4) == 0) {  // 16-byte aligned rows
+            launch_lag_tma<T>(A, grid, s);
+            return;
+          }
           launch_pdl(pw_lag_kernel<T>, grid, dim3(kPwThreads), s, A);
           return;
         }

@@ -401,4 +401,155 @@ __device__ __forceinline__ void pw_body_lag(const ssm_pw_args& A, int b, int vb,
   pw_block_finalize<kPwThreads>(A, fs, b, P, R, 1, acc.park->st, lane, kMaxPwBlocks, vb, nvb);
 }
 
+// pw_body_lag with the ancestor gather staged through shared memory by TMA bulk
+// copies: per warp tile, the ancestors of its 32 particles are non-decreasing
+// (systematic / stratified / sorted multinomial, or the identity), so the tile
+// reads one contiguous source range per state slot; lane 0 issues those 8 copies
+// (cp.async.bulk, completing on the warp's mbarrier) one tile ahead, and every
+// lane then reads its ancestor's state from shared memory.  Tiles whose source
+// range exceeds the staging width fall back to direct loads.  Dynamic shared
+// memory: [warps][2 stages][8 slots][kTmaW] of T.
+constexpr int kTmaW = 64;
+template <typename T>
+__device__ __forceinline__ void pw_body_lag_tma(const ssm_pw_args& A, int b, int vb, int nvb) {
+  constexpr int NX = 8;
+  const int P = A.P;
+  const int ntiles = (P + kPwThreads - 1) / kPwThreads;
+  ssm_filter_state* fs = A.fs + b;
+  const int R = fs->resample_now;
+  const bool uniform_in = R || fs->uniform;
+  const double incr_prev = fs->incr;
+  const int in_stride = A.x_in_stride > 0 ? A.x_in_stride : P;
+  const T* __restrict__ xin = static_cast<const T*>(A.x_in) + static_cast<size_t>(b) * NX * in_stride;
+  const int out_stride = A.x_out_stride > 0 ? A.x_out_stride : P;
+  T* __restrict__ xout = static_cast<T*>(A.x_out) + static_cast<size_t>(b) * NX * out_stride;
+  const int32_t* __restrict__ anc = (R && A.anc != nullptr) ? A.anc + static_cast<size_t>(b) * P : nullptr;
+  const T* __restrict__ aprev = A.a_prev ? static_cast<const T*>(A.a_prev) + static_cast<size_t>(b) * P : nullptr;
+  T* __restrict__ aout = A.a_out ? static_cast<T*>(A.a_out) + static_cast<size_t>(b) * P : nullptr;
+  uint64_t* __restrict__ cloc = static_cast<uint64_t*>(A.cdf_local) + static_cast<size_t>(b) * P;
+  ssm_tile_rec* __restrict__ trec = static_cast<ssm_tile_rec*>(A.tile_rec) + static_cast<size_t>(b) * ((P + 31) >> 5);
+  const double* th = A.theta + 4 * b;
+  const uint32_t k0 = A.keys[2 * b], k1 = A.keys[2 * b + 1];
+  const T logw0 = static_cast<T>(A.log_w0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  T* s_x = reinterpret_cast<T*>(dyn_smem) + static_cast<size_t>(warp) * 2 * NX * kTmaW;  // this warp's 2 stages
+  __shared__ uint64_t s_bar[kPwThreads / 32][2];
+  __shared__ double s_exp_tab[64];
+  if (threadIdx.x < 64) s_exp_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
+  if (lane == 0) {
+    mbar_init(&s_bar[warp][0], 1u);
+    mbar_init(&s_bar[warp][1], 1u);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  __shared__ ParkedTiles s_park[kPwThreads / 32];
+  WarpTileAcc acc = warp_tile_acc(&s_park[warp], lane);
+  bool bad = false;
+
+  const int stride = nvb * kPwThreads;
+  const int p0 = vb * kPwThreads + threadIdx.x;
+  auto anc_of = [&](int p) -> int { return anc ? __ldg(anc + min(p, P - 1)) : p; };
+  // stage the source range of the warp tile whose lanes hold ancestors `a` (valid: p < P)
+  // into stage st; returns the range start, or -1 (fallback: direct loads)
+  auto issue = [&](int a, bool valid, int st) -> int {
+    const int lo = __reduce_min_sync(0xffffffffu, valid ? a : INT_MAX);
+    const int hi = __reduce_max_sync(0xffffffffu, valid ? a : -1);
+    if (hi < 0) return -1;  // no particle in range
+    constexpr int kAl = 16 / static_cast<int>(sizeof(T));  // elements per 16 bytes
+    const int start = lo & ~(kAl - 1);
+    const int count = (hi + kAl - start) & ~(kAl - 1);  // 16-byte aligned span covering [lo, hi]
+    if (count > kTmaW || start + count > in_stride) return -1;
+    __syncwarp();  // every lane is done reading this stage's previous tile
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      const uint32_t bytes = static_cast<uint32_t>(count * sizeof(T));
+      mbar_expect_tx(&s_bar[warp][st], NX * bytes);
+#pragma unroll
+      for (int n = 0; n < NX; ++n)
+        bulk_g2s(s_x + (st * NX + n) * kTmaW, xin + static_cast<size_t>(n) * in_stride + start, bytes,
+                 &s_bar[warp][st]);
+    }
+    return start;
+  };
+  const T gconst = static_cast<T>(8.0 * (A.obs_log_sd + A.log_sqrt_2pi));
+  const bool check = A.check_finite != 0;
+  const T s_F = static_cast<T>(th[0]);
+  const T s_c = static_cast<T>(th[1] * 20.0 * A.subs[0].sd);
+  const T s_s = static_cast<T>(A.subs[0].s[0]);
+  T yv[8];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) yv[n] = static_cast<T>(A.y[n]);
+  float zc[8], zn[8];
+  if (p0 < P) normals8f(k0, k1, static_cast<uint32_t>(p0 + A.p_offset), static_cast<uint32_t>(A.step), 0u, zc);
+
+  // a0: this tile's ancestor, a1: the next tile's (its copies are issued one tile ahead)
+  int a0 = anc_of(p0), a1 = anc_of(p0 + stride);
+  int st = 0;
+  uint32_t phase[2] = {0u, 0u};
+  int start0 = vb < ntiles ? issue(a0, p0 < P, 0) : -1;
+
+  double a_lag = -CUDART_INF;
+  bool act_lag = false, real_lag = false;
+  int p_lag = P;
+  for (int tile = vb; tile < ntiles; tile += nvb) {
+    const int p = tile * kPwThreads + threadIdx.x;
+    const bool act = p < P;
+    const int pn = p + stride;
+    const bool has_next = tile + nvb < ntiles;
+    const int start1 = has_next ? issue(a1, pn < P, st ^ 1) : -1;
+    const int a2 = anc_of(pn + stride);
+    if (pn < P) normals8f(k0, k1, static_cast<uint32_t>(pn + A.p_offset), static_cast<uint32_t>(A.step), 0u, zn);
+    T x[NX];
+    if (start0 >= 0) {
+      mbar_wait(&s_bar[warp][st], phase[st]);
+      phase[st] ^= 1u;
+      const int off = act ? a0 - start0 : 0;
+#pragma unroll
+      for (int n = 0; n < NX; ++n) x[n] = s_x[(st * NX + n) * kTmaW + off];
+    } else {
+#pragma unroll
+      for (int n = 0; n < NX; ++n) x[n] = act ? xin[static_cast<size_t>(n) * in_stride + a0] : T(0);
+    }
+    l96_simple_step<T>(x, zc, s_F, s_c, s_s);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) zc[n] = zn[n];
+    if (act) {
+#pragma unroll
+      for (int n = 0; n < NX; ++n) xout[static_cast<size_t>(n) * out_stride + p] = x[n];
+    }
+    T sq = T(0);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const T d = yv[n] - x[n];
+      sq = fma(d, d, sq);
+    }
+    const T g = fma(T(-2.0), sq, -gconst);
+    const T lw = uniform_in ? logw0 : Ar<T, false>::sub(aprev[act ? p : 0], static_cast<T>(incr_prev));
+    const T a = Ar<T, false>::add(lw, g);
+    if (act && aout) aout[p] = a;
+    warp_tile_weigh_lag(acc, a_lag, act_lag, p_lag, P, lane, s_exp_tab, cloc, trec, real_lag);
+    a_lag = act ? static_cast<double>(a) : -CUDART_INF;
+    act_lag = act;
+    p_lag = p;
+    real_lag = true;
+    if (check && act && !bad && !(sq < T(CUDART_INF))) {
+      bool ok = true;
+#pragma unroll
+      for (int n = 0; n < 8; ++n) ok &= finite_bits(x[n]);
+      if (!ok) bad = true;
+    }
+    a0 = a1;
+    a1 = a2;
+    start0 = start1;
+    st ^= 1;
+  }
+  warp_tile_weigh_lag(acc, a_lag, act_lag, p_lag, P, lane, s_exp_tab, cloc, trec, real_lag);
+  warp_tile_flush(acc, lane);
+
+  if (bad) atomicMin(&fs->err_nonfinite, A.step * 64);
+  pw_block_finalize<kPwThreads>(A, fs, b, P, R, 1, acc.park->st, lane, kMaxPwBlocks, vb, nvb);
+}
+
 }  // namespace ssm

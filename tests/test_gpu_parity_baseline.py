@@ -367,3 +367,33 @@ def test_resample_from_logw_device_draws_match_numpy_2p20(scheme, sigma):
     for kk in bad:
         lo, hi = min(got[kk], ref[kk]), max(got[kk], ref[kk])
         assert np.min(np.abs(cum[lo:hi] - q[kk])) <= 1e-12, (kk, got[kk], ref[kk])
+
+
+def test_tma_staged_gather_variant_bitwise_equal():
+    """The opt-in TMA-staged gather of the headline kernel (SSM_PW_TMA=1: per warp
+    tile, cp.async.bulk copies of the contiguous ancestor range into shared
+    memory) gives bitwise the same filter as the register-prefetch kernel (run in
+    subprocesses: the switch is read once per process), f64 and f32."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import bench\n"
+        "from paper_1306_3277_b200 import LORENZ96, RngStream\n"
+        "from paper_1306_3277_b200.inference import build_filter_grid, particle_filter\n"
+        "t, ot, ov, om = bench.synthetic_data(40)\n"
+        "g = build_filter_grid(0.0, t[-1], 40, ot, ov, om, n_obs=8)\n"
+        "for dt in ('float64', 'float32'):\n"
+        "    o = particle_filter(LORENZ96, bench.THETA, g, RngStream(9), n_particles=(1 << 16) + 64, "
+        "resampler='systematic', dtype=dt, upto=12)\n"
+        "    print(repr(o.loglik), float(np.abs(o.trajectory).sum()).hex())\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"SSM_PW_TMA": "1"}):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                           env={**os.environ, **env})
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.split())
+    assert outs[0] == outs[1]

@@ -621,7 +621,7 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
     const double* cd = static_cast<const double*>(src) + static_cast<size_t>(b) * P_in;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) cum[i] = jt + i < P_in ? cd[jt + i] : 2.0;
-    cum_prev = jt > 0 ? cd[jt - 1] : 0.0;
+    cum_prev = (jt > 0 && jt <= P_in) ? cd[jt - 1] : 0.0;  // threads past P_in return below
   } else if constexpr (SRC == kCumTiles) {
     // src = cdf_local (u64 [B][P]); `shift` = per-warp-tile scale exp(m_w - incr) 2^9
     // [B][nt]; tile_prefix = per-tile exclusive prefix within its 2048-tile block
@@ -662,8 +662,9 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
         cum[i] = 1.0;  // cum[-1] = 1.0 (resampling.py:27)
     }
     cum_prev = jt == 0 ? static_cast<double>(goff) * inv
-               : ((jt & 31) == 0 ? static_cast<double>(pre) * inv
-                                 : static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(cl[jt - 1]))) * inv);
+               : ((jt & 31) == 0 || jt > P_in  // (threads past P_in return below)
+                      ? static_cast<double>(pre) * inv
+                      : static_cast<double>(pre + __double2ull_rn(sc * static_cast<double>(cl[jt - 1]))) * inv);
   } else {
     const size_t off = static_cast<size_t>(b) * P_in + j0;
     double sh = 0.0;
@@ -719,7 +720,7 @@ offspring_kernel(int P_in, int P_out, const void* __restrict__ src, const double
         const int e = threadIdx.x * kScanItems + i;
         Cv[i] = sm[e + (e >> 3)];
       }
-      Cprev = jt > 0 ? Cb[jt - 1] : 0ull;
+      Cprev = (jt > 0 && jt <= P_in) ? Cb[jt - 1] : 0ull;  // threads past P_in return below
       tot = static_cast<double>(Cb[P_in - 1]);
     }
 #pragma unroll

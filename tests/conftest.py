@@ -14,6 +14,27 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
     config.addinivalue_line("markers", "slow: long-running statistical test")
+    if os.environ.get("SSM_GUARD_ALLOC"):
+        install_guard_allocator()
+
+
+def install_guard_allocator():
+    """SSM_GUARD_ALLOC=1: every torch CUDA tensor ends at an unmapped guard page
+    (tests/tools/guard_alloc.cpp), so an out-of-bounds kernel access faults.
+    Must run before the first CUDA allocation of the process."""
+    import subprocess
+
+    import torch
+
+    src = os.path.join(ROOT, "tests", "tools", "guard_alloc.cpp")
+    so = os.path.join(ROOT, "build", "guard_alloc.so")
+    if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        os.makedirs(os.path.dirname(so), exist_ok=True)
+        cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+        subprocess.run(["g++", "-O2", "-shared", "-fPIC", src, "-o", so, f"-I{cuda}/include",
+                        f"-L{cuda}/lib64/stubs", "-lcuda"], check=True)
+    alloc = torch.cuda.memory.CUDAPluggableAllocator(so, "guard_malloc", "guard_free")
+    torch.cuda.memory.change_current_allocator(alloc)
 
 
 def load_golden(name):

@@ -119,3 +119,47 @@ def test_resampling_reads_stay_inside_their_arrays():
     r = subprocess.run([sys.executable, "-c", CODE], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     assert r.stdout.split()[0] == "ok"
+
+
+GUARD_SELFTEST = r"""
+import os, sys
+sys.path.insert(0, %r)
+from tests.conftest import install_guard_allocator
+install_guard_allocator()
+import numpy as np, torch
+from paper_1306_3277_b200 import _lib
+L = _lib.lib()
+P = 1000
+x = torch.zeros((1, P), dtype=torch.float64, device="cuda")
+xo = torch.empty_like(x)
+idx = torch.tensor(np.arange(P, dtype=np.int32), device="cuda")
+_lib.check(L.ssm_gather(_lib.SSM_F64, 1, 1, P, _lib.ptr(x), _lib.ptr(idx), _lib.ptr(xo), _lib.stream_ptr()), "g")
+torch.cuda.synchronize()
+print("in-bounds ok", flush=True)
+idx[-1] = P + 64  # 512 bytes past the end of x
+_lib.check(L.ssm_gather(_lib.SSM_F64, 1, 1, P, _lib.ptr(x), _lib.ptr(idx), _lib.ptr(xo), _lib.stream_ptr()), "g")
+torch.cuda.synchronize()
+print("OOB not detected", flush=True)
+""" % ROOT
+
+
+def test_guard_allocator_catches_an_out_of_bounds_read():
+    """The allocator behind SSM_GUARD_ALLOC (tests/tools/guard_alloc.cpp) faults a
+    gather that reads 512 bytes past its input."""
+    r = subprocess.run([sys.executable, "-c", GUARD_SELFTEST], capture_output=True, text=True, timeout=300,
+                       env={**os.environ, "SSM_GUARD_ALIGN": "16"})
+    assert "in-bounds ok" in r.stdout, r.stderr[-2000:]
+    assert "OOB not detected" not in r.stdout
+    assert r.returncode != 0
+
+
+def test_parity_suite_under_guard_allocator():
+    """tests/test_gpu_parity.py with every torch tensor ending at an unmapped guard
+    page (16-byte slack): no kernel of the filter, resampling, trajectory,
+    small-P or generic paths touches memory past a tensor's end.  (The whole
+    GPU suite passes this way except the CUDA-IPC sharded tests, whose peer
+    mappings need cudaMalloc memory.)"""
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-q", "-x",
+                        "-p", "no:cacheprovider"], capture_output=True, text=True, timeout=1200, cwd=ROOT,
+                       env={**os.environ, "SSM_GUARD_ALLOC": "1", "SSM_GUARD_ALIGN": "16"})
+    assert r.returncode == 0, r.stdout[-3000:]

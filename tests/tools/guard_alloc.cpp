@@ -7,7 +7,8 @@
 // aligned; SSM_GUARD_ALIGN=16 puts it within 16 bytes).  A kernel that reads
 // or writes past that slack at the end of any tensor faults at once instead
 // of silently touching a neighbour -- a bounds check for a GPU pool without
-// compute-sanitizer.  No caching: free
+// compute-sanitizer.  SSM_GUARD_SIDE=front moves the unmapped granule in
+// front of the tensor instead (reads before its start fault).  No caching: free
 // synchronises the device, then unmaps and releases the range.
 //
 // Build: g++ -O2 -shared -fPIC tests/tools/guard_alloc.cpp -I$CUDA/include -L$CUDA/lib64/stubs -lcuda
@@ -27,6 +28,7 @@ namespace {
 
 struct Range {
   CUdeviceptr va;
+  CUdeviceptr va_mapped;
   size_t reserved;
   size_t mapped;
   CUmemGenericAllocationHandle h;
@@ -55,13 +57,19 @@ extern "C" void* guard_malloc(ssize_t size, int device, void* /*stream*/) {
   if (!ok(cuMemGetAllocationGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "granularity"))
     return nullptr;
   const size_t mapped = (static_cast<size_t>(size) + gran - 1) / gran * gran;
-  Range r{0, mapped + gran, mapped, 0};
+  Range r{0, 0, mapped + gran, mapped, 0};
   if (!ok(cuMemAddressReserve(&r.va, r.reserved, 0, 0, 0), "reserve")) return nullptr;
   if (!ok(cuMemCreate(&r.h, mapped, &prop, 0), "create")) {
     cuMemAddressFree(r.va, r.reserved);
     return nullptr;
   }
-  if (!ok(cuMemMap(r.va, mapped, 0, r.h, 0), "map")) {
+  // SSM_GUARD_SIDE=front: the unmapped granule precedes the tensor (under-reads fault)
+  static const bool front = [] {
+    const char* e = std::getenv("SSM_GUARD_SIDE");
+    return e && e[0] == 'f';
+  }();
+  const CUdeviceptr mva = front ? r.va + gran : r.va;
+  if (!ok(cuMemMap(mva, mapped, 0, r.h, 0), "map")) {
     cuMemRelease(r.h);
     cuMemAddressFree(r.va, r.reserved);
     return nullptr;
@@ -69,19 +77,20 @@ extern "C" void* guard_malloc(ssize_t size, int device, void* /*stream*/) {
   CUmemAccessDesc acc = {};
   acc.location = prop.location;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  if (!ok(cuMemSetAccess(r.va, mapped, &acc, 1), "access")) {
-    cuMemUnmap(r.va, mapped);
+  if (!ok(cuMemSetAccess(mva, mapped, &acc, 1), "access")) {
+    cuMemUnmap(mva, mapped);
     cuMemRelease(r.h);
     cuMemAddressFree(r.va, r.reserved);
     return nullptr;
   }
-  const uintptr_t end = static_cast<uintptr_t>(r.va) + mapped;
+  r.va_mapped = mva;
+  const uintptr_t end = static_cast<uintptr_t>(mva) + mapped;
   static const uintptr_t align = [] {
     const char* e = std::getenv("SSM_GUARD_ALIGN");  // 256 by default; 16 tightens the check
     const long v = e ? std::strtol(e, nullptr, 10) : 256;
     return static_cast<uintptr_t>(v >= 16 && (v & (v - 1)) == 0 ? v : 256);
   }();
-  const uintptr_t p = (end - static_cast<uintptr_t>(size)) & ~(align - 1);
+  const uintptr_t p = front ? static_cast<uintptr_t>(mva) : (end - static_cast<uintptr_t>(size)) & ~(align - 1);
   std::lock_guard<std::mutex> lk(g_mu);
   g_live[p] = r;
   return reinterpret_cast<void*>(p);
@@ -97,7 +106,7 @@ extern "C" void guard_free(void* ptr, ssize_t /*size*/, int /*device*/, void* /*
     g_live.erase(it);
   }
   cuCtxSynchronize();  // no kernel may still use the range
-  cuMemUnmap(r.va, r.mapped);
+  cuMemUnmap(r.va_mapped, r.mapped);
   cuMemRelease(r.h);
   cuMemAddressFree(r.va, r.reserved);
 }

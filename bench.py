@@ -272,7 +272,7 @@ def run_ours(args, rank, world):
 
 # ------------------------------------------------------------ SMC^2 workload (config 4)
 
-SMC2_METRIC = "particle-updates/sec (SMC^2 on Lorenz '96, 1024 theta x 2^14, rejuvenation replays counted)"
+SMC2_METRIC = "particle-updates/sec (SMC^2 on Lorenz '96, {n_theta} theta x 2^{logp}, rejuvenation replays counted)"
 
 
 def run_smc2(args, rank, world):
@@ -358,7 +358,7 @@ def smc2_line(args, res, world):
     pw = res["kern"].get("propagate_weight", {})
     achieved = pw["bytes"] / (pw["total_ms"] / 1e3) / 1e9 if pw else None
     line = {
-        "metric": SMC2_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "metric": SMC2_METRIC.format(n_theta=n_theta, logp=int(math.log2(P))), "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": res["ms"] / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (L96 theta*=(10,0.1), sparse obs: slots 0-3 every other step; device noise)",
         "config": {"workload": f"SMC^2 on Lorenz96, {n_theta} theta-particles x 2^{int(math.log2(P))} particles, "

@@ -509,14 +509,16 @@ __device__ __forceinline__ void tile_scale_body(int b, int blk, int nblk, int nt
                                                 int step) {
   __shared__ uint64_t warp_tot[kThreads / 32];
   __shared__ bool s_last;
-  if (gate && !fs[b].resample_now) return;
-  if (long_count && blk == 0 && threadIdx.x == 0) long_count[b] = 0u;  // long-run list of this resample
-  const double incr = fs[b].incr;
   const int e = blk * kRecPerBlock + threadIdx.x;
   const size_t off = static_cast<size_t>(b) * ntiles + e;
+  // the record load is issued before the gate / incr loads so their latencies overlap
+  ssm_tile_rec r{0.0, 0ull};
+  if (e < ntiles) r = rec[off];
+  const double incr = fs[b].incr;
+  if (gate && !fs[b].resample_now) return;
+  if (long_count && blk == 0 && threadIdx.x == 0) long_count[b] = 0u;  // long-run list of this resample
   uint64_t qg = 0;
   if (e < ntiles) {
-    const ssm_tile_rec r = rec[off];
     const double sc = r.m == -CUDART_INF ? 0.0 : exp(r.m - incr) * kTileScale;
     scale[off] = sc;
     const double v = sc * static_cast<double>(r.Q);

@@ -151,6 +151,28 @@ def _chain_log_prior(spec, theta, init_state):
     return lp
 
 
+def _chain_log_priors(spec, thetas, init_states):
+    """_chain_log_prior for a batch of chains (SMC^2's theta-particles): the
+    hand-written models' densities evaluated column-wise over the batch with the
+    scalar path's addition order (bitwise the same values); other models per chain."""
+    from ..models import ModelSpec, d_gauss_logpdf, d_uniform_logpdf, parameter_logpdf_batch
+
+    n = len(thetas)
+    if not isinstance(spec, ModelSpec) or n == 0:
+        return [_chain_log_prior(spec, thetas[k], None if init_states is None else init_states[k]) for k in range(n)]
+    lp = parameter_logpdf_batch(spec, np.asarray(thetas, dtype=float))
+    if init_states is not None:
+        X0 = np.atleast_2d(np.asarray(init_states, dtype=float))
+        tot = np.zeros(n)
+        if spec.name == "Lorenz96":
+            for i in range(8):
+                tot = tot + d_uniform_logpdf(X0[:, i], -1.0, 3.0)
+        else:
+            tot = tot + d_gauss_logpdf(X0[:, 0], 90.0, 15.0)
+        lp = lp + tot
+    return [float(v) for v in lp]
+
+
 def init_chain(ir, runner, rng, upto=None):
     """mcmc.py:118-132."""
     return init_chains(ir, runner, [rng], upto)[0]

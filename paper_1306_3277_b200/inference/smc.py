@@ -29,7 +29,7 @@ from .. import _lib
 from ..distributed import Shard, allgather_f64, exchange, plan_redistribution
 from ..errors import DegenerateEnsembleError, UnsupportedModelError
 from ..models import resolve_model
-from .mcmc import MhChainState, _chain_log_prior, marginal_mh_steps
+from .mcmc import MhChainState, _chain_log_priors, marginal_mh_steps
 from .particle import _dtype_info, advance_runs, sample_trajectories
 from .resampling import resample
 
@@ -276,9 +276,9 @@ def _smc_sampler(ir, runner, n_theta, rng, theta_resampler, shard, theta_draws):
     thetas = spec.sample_parameter(rng.child(0), size=n_theta)
     init_states = spec.sample_initial(thetas, rng.child(1), size=n_theta) if use_init else None
     local = []
-    for j in J:
-        ist = init_states[j] if use_init else None
-        local.append(ThetaParticle(theta=thetas[j], log_prior=_chain_log_prior(spec, thetas[j], ist), init_state=ist))
+    lps = _chain_log_priors(spec, [thetas[j] for j in J], [init_states[j] for j in J] if use_init else None)
+    for j, lp in zip(J, lps):
+        local.append(ThetaParticle(theta=thetas[j], log_prior=lp, init_state=init_states[j] if use_init else None))
     log_v = np.full(n_theta, -np.log(n_theta))
     counts = [shard_bounds_count(n_theta, r, shard.world) for r in range(shard.world)]
     diagnostics = []

@@ -225,3 +225,26 @@ def test_batched_streams_bit_exact_with_numpy():
         g = ref_gen(s, k)
         assert st.uniform() == g.uniform()
         assert st.generator.uniform(size=2).tolist() == g.uniform(size=2).tolist()
+
+
+def test_batched_chain_log_priors_equal_per_chain():
+    """SMC^2's batched prior evaluation (_chain_log_priors) gives bitwise the
+    per-chain _chain_log_prior values (mcmc.py:118-132 / simulate.parameter_logpdf),
+    including out-of-support parameters and initial states (-inf)."""
+    from paper_1306_3277_b200 import LORENZ96, WINDKESSEL
+    from paper_1306_3277_b200.inference.mcmc import _chain_log_prior, _chain_log_priors
+
+    rs = np.random.default_rng(3)
+    th = np.column_stack([rs.uniform(7.0, 13.0, 50), rs.uniform(-0.1, 1.0, 50)])
+    x0 = rs.uniform(-1.5, 3.5, (50, 8))
+    for init in (None, x0):
+        got = _chain_log_priors(LORENZ96, list(th), None if init is None else list(init))
+        want = [_chain_log_prior(LORENZ96, th[k], None if init is None else init[k]) for k in range(50)]
+        assert [float(v).hex() for v in got] == [float(v).hex() for v in want]
+    thw = np.abs(rs.normal(1.0, 1.0, (40, 4))) * np.array([1.0, 1.0, 0.03, 20.0])
+    thw[3, 1] = -1.0
+    xw = rs.normal(90.0, 20.0, (40, 1))
+    for init in (None, xw):
+        got = _chain_log_priors(WINDKESSEL, list(thw), None if init is None else list(init))
+        want = [_chain_log_prior(WINDKESSEL, thw[k], None if init is None else init[k]) for k in range(40)]
+        assert [float(v).hex() for v in got] == [float(v).hex() for v in want]

@@ -1446,14 +1446,45 @@ spacing_merge_kernel(int P, const uint64_t* __restrict__ C, const uint64_t* __re
     }
     return lo;
   };
-  for (int j0 = jlo; j0 <= jhi; j0 += kThreads) {  // chunks of 256 particles
-    const int j = j0 + threadIdx.x;
-    const int c = j <= jhi ? cnt_lt(j) : n_out;
+  // the same count continued from particle j - 1's (cum is non-decreasing, so every
+  // U below c_{j-1} is below cum_j): a short linear walk, then a binary search
+  auto cnt_from = [&](int j, int c) -> int {
+    if (j >= P - 1 || j >= jhi) return n_out;
+    const double cj = cum_at(j);
+    int lim = min(c + 16, n_out);
+    while (c < lim && sU[c] < cj) ++c;
+    if (c < lim || c == n_out) return c;
+    int hi = n_out;
+    while (c < hi) {
+      const int mid = (c + hi) >> 1;
+      if (sU[mid] < cj)
+        c = mid + 1;
+      else
+        hi = mid;
+    }
+    return c;
+  };
+  // chunks of 2048 particles, 8 consecutive per thread: one binary search for the
+  // thread's first particle, the next seven continue from it (merge walk)
+  for (int j0 = jlo; j0 <= jhi; j0 += kScanTile) {
+    const int jt = j0 + threadIdx.x * kScanItems;
+    int cv[kScanItems];
+    int c = jt <= jhi ? cnt_lt(jt) : n_out;
+    cv[0] = c;
+#pragma unroll
+    for (int i = 1; i < kScanItems; ++i) {
+      c = jt + i <= jhi ? cnt_from(jt + i, c) : n_out;
+      cv[i] = c;
+    }
     const int up = __shfl_up_sync(0xffffffffu, c, 1);
     if (lane == 31) s_carry[warp] = c;
     __syncthreads();
-    const int a = lane > 0 ? up : (warp > 0 ? s_carry[warp - 1] : (j0 == jlo ? cnt_lt(jlo - 1) : s_prev));
-    if (j <= jhi && c > a) sOut[a + (a >> 5)] = j;
+    int a = lane > 0 ? up : (warp > 0 ? s_carry[warp - 1] : (j0 == jlo ? cnt_lt(jlo - 1) : s_prev));
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      if (jt + i <= jhi && cv[i] > a) sOut[a + (a >> 5)] = jt + i;
+      a = cv[i];
+    }
     __syncthreads();
     if (threadIdx.x == kThreads - 1) s_prev = c;
   }

@@ -1382,17 +1382,8 @@ spacing_merge_kernel(int P, const uint64_t* __restrict__ C, const uint64_t* __re
   const int nsb = gridDim.x + (P % kScanTile == 0 ? 1 : 0);  // spacing blocks cover P + 1 outputs
   const double off = blk[static_cast<size_t>(b) * nsb + blockIdx.x];
   const double inv = 1.0 / tot[b];
-  const double2* src = reinterpret_cast<const double2*>(spc + static_cast<size_t>(b) * nsb * kScanTile + k0 +
-                                                        threadIdx.x * kScanItems);
-#pragma unroll
-  for (int i = 0; i < kScanItems / 2; ++i) {  // U_(k0+k) = (S_{k0} + local inclusive sum) / S_{P+1}
-    const double2 t = src[i];
-    sU[threadIdx.x * kScanItems + 2 * i] = (off + t.x) * inv;
-    sU[threadIdx.x * kScanItems + 2 * i + 1] = (off + t.y) * inv;
-  }
+  const double* spb = spc + static_cast<size_t>(b) * nsb * kScanTile + k0;
   (void)s_warp;
-  for (int e = threadIdx.x; e < (kScanTile + kScanTile / 32) / 4; e += kThreads)
-    reinterpret_cast<int4*>(sOut)[e] = make_int4(-1, -1, -1, -1);
   const size_t coff = static_cast<size_t>(b) * P;
   using Cum = typename std::conditional<SRC == 0, CumFixedArr, CumTileRecsMul>::type;
   Cum cum_at;
@@ -1405,11 +1396,23 @@ spacing_merge_kernel(int P, const uint64_t* __restrict__ C, const uint64_t* __re
                          pref + B_total_tiles_offset(nt, gridDim.y) + static_cast<size_t>(b) * nblk,
                          1.0 / static_cast<double>(totals[b])};
   }
-  __syncthreads();
-  // first / last ancestor: searchsorted(cum, U, 'right'), clipped
+  // first / last ancestor: searchsorted(cum, U, 'right'), clipped -- warps 0 and 1
+  // search (their U from the spacing prefixes directly) while warps 2-7 build the
+  // block's U_(k0+k) = (S_{k0} + local inclusive sum) / S_{P+1} and clear the marks
   if (warp < 2) {  // warp 0: first output, warp 1: last output
-    const int j = warp_search_right(cum_at, P, sU[warp == 0 ? 0 : n_out - 1], lane);
+    const int j = warp_search_right(cum_at, P, (off + spb[warp == 0 ? 0 : n_out - 1]) * inv, lane);
     if (lane == 0) s_j[warp] = j < P ? j : P - 1;
+  } else {
+    const int t = threadIdx.x - 64;
+    constexpr int kBuilders = kThreads - 64;
+    const double2* src = reinterpret_cast<const double2*>(spb);
+    for (int e = t; e < kScanTile / 2; e += kBuilders) {
+      const double2 v = src[e];
+      sU[2 * e] = (off + v.x) * inv;
+      sU[2 * e + 1] = (off + v.y) * inv;
+    }
+    for (int e = t; e < (kScanTile + kScanTile / 32) / 4; e += kBuilders)
+      reinterpret_cast<int4*>(sOut)[e] = make_int4(-1, -1, -1, -1);
   }
   __syncthreads();
   const int jlo = s_j[0], jhi = s_j[1];

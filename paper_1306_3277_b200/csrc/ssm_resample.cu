@@ -1355,6 +1355,41 @@ __device__ __forceinline__ int warp_search_right(const Cum& cum_at, int P, doubl
   return lo + __popc(m);
 }
 
+// warp_search_right starting from a window of 32 x 1024 entries around `guess`
+// (output k's ancestor is near k unless the weights are very uneven): one round
+// places q inside the window -- or outside it, and the full search runs --, then
+// two rounds finish instead of five.  Same answer as warp_search_right.
+template <typename Cum>
+__device__ __forceinline__ int warp_search_right_near(const Cum& cum_at, int P, double q, int lane, int guess) {
+  constexpr int kW = 32 * 1024;
+  if (P > 4 * kW) {
+    const int wlo = max(0, min(guess - kW / 2, P - kW));
+    const int step = kW / 32;
+    const int p = wlo + (lane + 1) * step - 1;
+    const bool below_ok = wlo == 0 || cum_at(wlo - 1) <= q;  // every lane: the same probe (cached)
+    const unsigned m = __ballot_sync(0xffffffffu, cum_at(p) <= q);
+    const int cnt = __popc(m);
+    if (below_ok && cnt < 32) {  // answer in [wlo, wlo + kW)
+      int lo = cnt > 0 ? wlo + cnt * step : wlo;
+      int hi = wlo + (cnt + 1) * step - 1;
+      while (hi - lo > 32) {
+        const int st = (hi - lo + 31) / 32;
+        const int pp = min(lo + (lane + 1) * st - 1, hi - 1);
+        const unsigned mm = __ballot_sync(0xffffffffu, cum_at(pp) <= q);
+        const int c2 = __popc(mm);
+        const int p_last = __shfl_sync(0xffffffffu, pp, c2 > 0 ? c2 - 1 : 0);
+        const int p_next = __shfl_sync(0xffffffffu, pp, c2 < 32 ? c2 : 31);
+        if (c2 > 0) lo = p_last + 1;
+        if (c2 < 32) hi = p_next;
+      }
+      const int pf = lo + lane;
+      const unsigned mf = __ballot_sync(0xffffffffu, pf < hi && cum_at(pf) <= q);
+      return lo + __popc(mf);
+    }
+  }
+  return warp_search_right(cum_at, P, q, lane);
+}
+
 // SRC 0: cum = inclusive u64 array `C` ([B][P]); SRC 1: tile records (cdf_local,
 // scale [B][nt], tile prefixes [B][nt] then block prefixes [B][nblk], totals)
 template <int SRC>
@@ -1400,7 +1435,8 @@ spacing_merge_kernel(int P, const uint64_t* __restrict__ C, const uint64_t* __re
   // search (their U from the spacing prefixes directly) while warps 2-7 build the
   // block's U_(k0+k) = (S_{k0} + local inclusive sum) / S_{P+1} and clear the marks
   if (warp < 2) {  // warp 0: first output, warp 1: last output
-    const int j = warp_search_right(cum_at, P, (off + spb[warp == 0 ? 0 : n_out - 1]) * inv, lane);
+    const int kq = warp == 0 ? 0 : n_out - 1;
+    const int j = warp_search_right_near(cum_at, P, (off + spb[kq]) * inv, lane, k0 + kq);
     if (lane == 0) s_j[warp] = j < P ? j : P - 1;
   } else {
     const int t = threadIdx.x - 64;

@@ -10,7 +10,7 @@ import pytest
 
 from oracle import ssm_oracle as O
 from paper_1306_3277_b200 import LORENZ96, WINDKESSEL, RngStream, _lib, load_model, resolve_model
-from paper_1306_3277_b200.errors import UnsupportedModelError
+from paper_1306_3277_b200.errors import DataFormatError, UnsupportedModelError
 from paper_1306_3277_b200.inference import build_filter_grid
 from paper_1306_3277_b200.rng import device_key
 from tests.conftest import ROOT, load_golden
@@ -248,3 +248,57 @@ def test_batched_chain_log_priors_equal_per_chain():
         got = _chain_log_priors(WINDKESSEL, list(thw), None if init is None else list(init))
         want = [_chain_log_prior(WINDKESSEL, thw[k], None if init is None else init[k]) for k in range(40)]
         assert [float(v).hex() for v in got] == [float(v).hex() for v in want]
+
+
+def _grid_by_event_loop(start, end, n_out, t_obs, n_obs_slots, mask):
+    """Restatement of the reference's grid merge (inference/timegrid.py:53-97) as a
+    plain event loop: outputs before observations at equal times, each event folded
+    into the previous grid point when within the relative 1e-9 tolerance."""
+    def close(a, b):
+        return abs(a - b) <= 1e-9 * max(1.0, abs(a), abs(b))
+
+    outs = np.linspace(start, end, n_out + 1)
+    keep = [k for k, t in enumerate(t_obs) if t > start and not close(t, start) and (t < end or close(t, end))]
+    t_obs, mask = [t_obs[k] for k in keep], mask[keep]
+    ev = sorted([(t, 0, -1) for t in outs] + [(t, 1, r) for r, t in enumerate(t_obs)], key=lambda e: e[0])
+    times, is_out, rows = [], [], []
+    for t, kind, r in ev:
+        if times and close(times[-1], t):
+            is_out[-1] |= kind == 0
+            rows[-1] = r if r >= 0 else rows[-1]
+            continue
+        times.append(t)
+        is_out.append(kind == 0)
+        rows.append(r)
+    steps = [i for i in range(1, len(times)) if rows[i] >= 0 and mask[rows[i]].any()]
+    return np.array(times), np.array(is_out), np.array(rows), steps
+
+
+def test_filter_grid_merge_rules():
+    """build_filter_grid against the event-loop restatement on random grids with
+    observation times on, within 1e-12 / 3e-9 of, and outside the output times and
+    the (start, end] boundaries, and rows with no present slot."""
+    rs = np.random.default_rng(11)
+    for trial in range(400):
+        start = float(rs.choice([0.0, 1.5, -2.0]))
+        end = start + float(rs.uniform(0.5, 10.0))
+        n_out = int(rs.integers(1, 25))
+        outs = np.linspace(start, end, n_out + 1)
+        t = rs.uniform(start - 1.0, end + 1.0, int(rs.integers(0, 30)))
+        if t.size:
+            j = rs.integers(0, t.size, size=min(t.size, 6))
+            t[j] = outs[rs.integers(0, n_out + 1, size=j.size)] * (1.0 + rs.choice([0.0, 1e-12, -1e-12, 3e-9], j.size))
+        t = np.unique(t)
+        nslot = int(rs.integers(1, 4))
+        mask = rs.random((t.size, nslot)) < 0.5
+        vals = rs.normal(size=(t.size, nslot))
+        grid = build_filter_grid(start, end, n_out, t, vals, mask, n_obs=nslot)
+        times, is_out, rows, steps = _grid_by_event_loop(start, end, n_out, list(t), nslot, mask)
+        np.testing.assert_array_equal(grid.times, times)
+        np.testing.assert_array_equal(grid.is_output, is_out)
+        np.testing.assert_array_equal(grid.obs_row, rows)
+        assert grid.obs_steps == steps
+    with pytest.raises(DataFormatError):
+        build_filter_grid(0.0, 1.0, 4, [0.5, 0.5], np.zeros((2, 1)), np.ones((2, 1), bool), n_obs=1)
+    with pytest.raises(DataFormatError):
+        build_filter_grid(1.0, 1.0, 4)

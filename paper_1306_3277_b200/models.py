@@ -157,7 +157,11 @@ class ModelSpec:
         the compiled reference lambdas use (bit-identical)."""
         th = np.atleast_2d(np.asarray(thetas, dtype=float))
         out = np.zeros((th.shape[0], 4))
-        for b in range(th.shape[0]):
+        if self.name == "Lorenz96":  # copy and sqrt only (correctly rounded): one vector pass
+            out[:, 0] = th[:, 0]  # F
+            out[:, 1] = np.sqrt(th[:, 1])  # np.sqrt(T[:, 1])
+            return out
+        for b in range(th.shape[0]):  # exp per row, as the reference evaluates it
             row = th[b : b + 1]
             if self.name == "Lorenz96":
                 out[b, 0] = row[0, 0]  # F

@@ -69,6 +69,18 @@ class SmcResult:
     diagnostics: list = field(default_factory=list)
 
 
+class _Children:
+    """parent.child(a, j, b) on demand, indexed by j (a dict of them, built lazily)."""
+
+    __slots__ = ("parent", "a", "b")
+
+    def __init__(self, parent, a, b):
+        self.parent, self.a, self.b = parent, a, b
+
+    def __getitem__(self, j):
+        return self.parent.child(self.a, j, self.b)
+
+
 def _advance_all(runner, particles, js, upto, run_rngs, init_rngs, traj_rngs):
     """Create missing runs, advance all to `upto` in batches by position, refresh trajectories."""
     missing = [j for j in js if particles[j].run is None]
@@ -313,7 +325,7 @@ def _smc_sampler(ir, runner, n_theta, rng, theta_resampler, shard, theta_draws):
             accepted.append(ok)
         # propagate and weight (smc.py:125-134)
         rr = {j: step_rng.child(2, j, 1) for j in J}
-        ir_ = {j: step_rng.child(2, j, 0) for j in J}
+        ir_ = _Children(step_rng, 2, 0)  # only the theta-particles without a run draw from these
         # only the last step's trajectories reach the result (each draws from its own stream,
         # smc.py:131, so skipping the intermediate ones leaves every other draw unchanged)
         tr = {j: step_rng.child(3, j) for j in J} if i == len(obs_steps) else None

@@ -29,7 +29,7 @@ from .. import _lib
 from ..distributed import Shard, allgather_f64, exchange, plan_redistribution
 from ..errors import DegenerateEnsembleError, UnsupportedModelError
 from ..models import resolve_model
-from .mcmc import MhChainState, _chain_log_priors, marginal_mh_steps
+from .mcmc import _chain_log_priors, marginal_mh_steps
 from .particle import _dtype_info, advance_runs, sample_trajectories
 from .resampling import resample
 
@@ -306,8 +306,9 @@ def _smc_sampler(ir, runner, n_theta, rng, theta_resampler, shard, theta_draws):
             local = _redistribute(spec, runner, local, anc, n_theta, shard, lo)
         particles = dict(zip(J, local))
         # rejuvenate: one marginal MH move each, one batched replay (smc.py:101-122)
-        chains = [MhChainState(theta=p.theta, trajectory=p.trajectory, loglik=p.loglik,
-                               log_prior=p.log_prior, init_state=p.init_state) for p in local]
+        # the MH step reads theta, init_state, loglik and log_prior of each chain state:
+        # the theta-particles themselves serve (MhChainState duck type, read only)
+        chains = local
         # the rejuvenated filters' trajectories are redrawn by the propagation below: not drawn here
         if theta_draws is None:
             outs = marginal_mh_steps(ir, chains, runner, [step_rng.child(1, j) for j in J], upto=prev_idx,

@@ -301,7 +301,16 @@ def _smc_sampler(ir, runner, n_theta, rng, theta_resampler, shard, theta_draws):
         # theta-resample (smc.py:96-98): same ancestors on every rank
         anc = resample(np.exp(log_v - _logsumexp(log_v)), theta_resampler, step_rng.child(0))
         if shard.world == 1:
-            local = [local[a].clone() for a in anc]
+            # the old list is dropped: each ancestor's first copy can be the particle itself
+            seen = bytearray(len(local))
+            picked = []
+            for a in anc:
+                if seen[a]:
+                    picked.append(local[a].clone())
+                else:
+                    seen[a] = 1
+                    picked.append(local[a])
+            local = picked
         else:
             local = _redistribute(spec, runner, local, anc, n_theta, shard, lo)
         particles = dict(zip(J, local))
